@@ -1,0 +1,171 @@
+"""float64 CPU oracle for VISTA stage-1 summarization -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline / ``--impl
+reference`` leg may import this package.  The product package ``paper_2510_22049_b200`` never
+imports it and shares no code with it.
+
+The arithmetic lives in ``vista_oracle.c`` (plain C, float64, OpenMP over (user, head, row));
+this file only marshals numpy arrays.  Every function cites the passage it implements in the C
+source.  Parity pins: tests/test_oracle_pins.py.  Readings where the paper is silent are listed
+in DESIGN.md ("Readings"); the softmax scale (R4), the 1/N-before-phi2 order (R10) and the
+empty-history convention (R6) have no paper value to match -> "parity unpinned" for those
+choices specifically (their arithmetic is pinned by the closed forms below).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "vista_oracle.c")
+_LIB = os.path.join(_HERE, "libvista_oracle.so")
+
+ACT = {"identity": 0, "silu": 1, "shifted_elu": 2}
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc -O2 -fopenmp, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        i64, f64, i32 = ctypes.c_int64, ctypes.c_double, ctypes.c_int
+        P = ctypes.c_void_p
+        lib.vo_softmax.argtypes = [i64, i64, i64, i64, P, i64, P, P, P, f64, P, i64, P, P, i32]
+        lib.vo_qla_state.argtypes = [i64, i64, i64, P, P, P, i32, P, i32]
+        lib.vo_qla_finalize.argtypes = [i64, i64, i64, i64, P, i64, P, P, i32, i32, i32, P, i32]
+        lib.vo_merge_lse.argtypes = [i64, i64, i64, P, P, P, P]
+        lib.vo_merge_sum.argtypes = [i64, i64, P, P]
+        lib.vo_act.argtypes = [i32, f64]
+        lib.vo_act.restype = f64
+        lib.vo_num_threads.restype = i32
+        _lib = lib
+    return _lib
+
+
+def num_threads() -> int:
+    return int(_load().vo_num_threads())
+
+
+def _f32(x):
+    x = np.ascontiguousarray(x)
+    if x.dtype != np.float32:
+        # the inputs are grid values exact in float32 (synth/); float64 inputs are accepted
+        # only when they are exactly representable in float32
+        y = x.astype(np.float32)
+        if not np.array_equal(y.astype(x.dtype), x):
+            raise ValueError("oracle inputs must be exactly representable in float32")
+        x = y
+    return x
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def act(kind: str, x: float) -> float:
+    """phi(x) in float64."""
+    return float(_load().vo_act(ACT[kind], float(x)))
+
+
+def softmax_summarize(q, k, v, offsets, scale=None, rows=None, q_per_user=False, threads=0):
+    """Seed-row softmax attention over each user's history.
+
+    q: [S,H,d] (shared seeds) or [B,S,H,d] with q_per_user=True; k, v: [sumL,H,d];
+    offsets: [B+1] int64.  rows: optional subset of query rows.
+    Returns out [B, R, H, d] float64 and lse [B, H, R] float64 (natural log).
+    """
+    q, k, v = _f32(q), _f32(k), _f32(v)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    B = len(offsets) - 1
+    S, H, d = q.shape[-3:]
+    if k.shape[1:] != (H, d) or v.shape != k.shape or offsets[-1] != k.shape[0]:
+        raise ValueError("shape mismatch")
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    rows = np.arange(S, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    R = len(rows)
+    out = np.empty((B, R, H, d), np.float64)
+    lse = np.empty((B, H, R), np.float64)
+    stride = S * H * d if q_per_user else 0
+    if k.shape[0] == 0:
+        k = np.zeros((1, H, d), np.float32)
+        v = k
+    rc = _load().vo_softmax(B, S, H, d, _ptr(q), stride, _ptr(k), _ptr(v), _ptr(offsets),
+                            float(scale), _ptr(rows), R, _ptr(out), _ptr(lse), int(threads))
+    if rc != 0:
+        raise ValueError("vo_softmax failed")
+    return out, lse
+
+
+def qla_state(k, v, offsets, phi1="silu", threads=0):
+    """Z[u,h] = sum_j phi1(k_j)^T v_j.  Returns [B,H,d,d] float64."""
+    k, v = _f32(k), _f32(v)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    B = len(offsets) - 1
+    _, H, d = k.shape
+    z = np.empty((B, H, d, d), np.float64)
+    if k.shape[0] == 0:
+        k = np.zeros((1, H, d), np.float32)
+        v = k
+    _load().vo_qla_state(B, H, d, _ptr(k), _ptr(v), _ptr(offsets), ACT[phi1], _ptr(z), int(threads))
+    return z
+
+
+def qla_finalize(q, z, n_items, phi1="silu", phi2="silu", normalize=True, q_per_user=False,
+                 threads=0):
+    """O = phi1(Q) phi2(Z / N_u).  Returns [B,S,H,d]."""
+    q = _f32(q)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    n_items = np.ascontiguousarray(n_items, dtype=np.int64)
+    B, H, d, _ = z.shape
+    S = q.shape[-3]
+    out = np.empty((B, S, H, d), np.float64)
+    stride = S * H * d if q_per_user else 0
+    _load().vo_qla_finalize(B, S, H, d, _ptr(q), stride, _ptr(z), _ptr(n_items), ACT[phi1],
+                            ACT[phi2], int(bool(normalize)), _ptr(out), int(threads))
+    return out
+
+
+def qla_summarize(q, k, v, offsets, phi1="silu", phi2="silu", normalize=True, q_per_user=False,
+                  threads=0):
+    """QLA source part at the seed rows: state then finalize.  Returns out [B,S,H,d]."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    z = qla_state(k, v, offsets, phi1, threads)
+    return qla_finalize(q, z, np.diff(offsets), phi1, phi2, normalize, q_per_user, threads)
+
+
+def merge_lse(part_o, part_lse):
+    """LSE merge of P partials. part_o [P, ..., d], part_lse [P, ...] -> (out, lse)."""
+    part_o = np.ascontiguousarray(part_o, dtype=np.float64)
+    part_lse = np.ascontiguousarray(part_lse, dtype=np.float64)
+    P = part_o.shape[0]
+    d = part_o.shape[-1]
+    n = int(np.prod(part_o.shape[1:-1]))
+    assert part_lse.shape == part_o.shape[:-1]
+    out = np.empty(part_o.shape[1:], np.float64)
+    lse = np.empty(part_lse.shape[1:], np.float64)
+    _load().vo_merge_lse(P, n, d, _ptr(part_o), _ptr(part_lse), _ptr(out), _ptr(lse))
+    return out, lse
+
+
+def merge_sum(parts):
+    parts = np.ascontiguousarray(parts, dtype=np.float64)
+    out = np.empty(parts.shape[1:], np.float64)
+    _load().vo_merge_sum(parts.shape[0], int(np.prod(parts.shape[1:])), _ptr(parts), _ptr(out))
+    return out

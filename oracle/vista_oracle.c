@@ -1,0 +1,243 @@
+/*
+ * vista_oracle.c -- float64 CPU oracle for VISTA stage-1 user-history summarization.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` leg may load this library.  The product path (paper_2510_22049_b200) never
+ * links, imports or executes it, and shares no source with it.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, the VISTA paper, arXiv 2510.22049):
+ *
+ *  Softmax summarization -- the seed rows of self-attention over the user history.
+ *    SoftmaxAttn(S =>full S) = RowSoftmax(Q K^T) V        (Sec. 3.2.1)
+ *    with the queries being the k virtual seeds, "initialized randomly as shared parameters
+ *    across users" (Sec. 3.2) and the keys/values the user's history items.
+ *    Per user u, head h, seed row i, over keys j in [off_u, off_{u+1}):
+ *      s_j = scale * sum_c q_{i,h,c} k_{j,h,c};  m = max_j s_j;  l = sum_j e^{s_j - m}
+ *      o_{i,h,:} = sum_j e^{s_j - m} v_{j,h,:} / l;   lse_{h,i} = m + ln l
+ *    Empty history: o = 0, lse = -inf (reading R6).  Two passes, sequential sums.
+ *
+ *  Quasi-linear attention (QLA), source part (Sec. 3.2.2; two-activation form
+ *  PAPER.md:831-836, App. B.2):
+ *      O[S] = phi1(Q[S]) phi2( phi1(K[S])^T V[S] )
+ *    evaluated at the seed-row queries:  Z = sum_j phi1(k_j)^T v_j  (d x d),
+ *    Zbar = Z / N_u when normalizing (the "1/N factor", App. B; N_u = L_u,
+ *    DESIGN.md reading R10), O = phi1(Q) phi2(Zbar).
+ *    phi: identity, SiLU ("we use SiLU"), shifted ELU (App. B.1.5:
+ *    phi(x) = x if x >= 1 else e^{x-1}).
+ *
+ *  Merges used only to test split invariants: LSE merge of softmax partials and plain sum of
+ *  QLA states.
+ *
+ * Inputs are float32 arrays whose values are exact (bf16 / f32 grid values from synth/); every
+ * element is converted exactly to double and all arithmetic is double.  No blocking, no
+ * reordering beyond the definitions above.  Compile: gcc -O2 -fopenmp (no -ffast-math).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define VO_ACT_IDENTITY 0
+#define VO_ACT_SILU 1
+#define VO_ACT_SHIFTED_ELU 2
+
+/* phi, PAPER.md:795-800 (shifted ELU, "x >= 1" takes the x branch) and PAPER.md:219 (SiLU). */
+double vo_act(int kind, double x) {
+    switch (kind) {
+        case VO_ACT_IDENTITY: return x;
+        case VO_ACT_SILU: return x / (1.0 + exp(-x));
+        case VO_ACT_SHIFTED_ELU: return x >= 1.0 ? x : exp(x - 1.0);
+        default: return NAN;
+    }
+}
+
+int vo_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+static void set_threads(int threads) {
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#else
+    (void)threads;
+#endif
+}
+
+/*
+ * Softmax summarization for the query rows rows[0..n_rows) of every (user, head).
+ *   q:   [S, H, d] when q_user_stride == 0 (shared seeds), else user u's block starts at
+ *        q + u * q_user_stride (elements) and is laid out [S, H, d].
+ *   k,v: [total_len, H, d];  offsets: [B+1] (offsets[0] = 0, non-decreasing).
+ *   out: [B, n_rows, H, d];  lse: [B, H, n_rows].
+ * Returns 0, or -1 on bad arguments / allocation failure.
+ */
+int vo_softmax(int64_t B, int64_t S, int64_t H, int64_t d, const float* q, int64_t q_user_stride,
+               const float* k, const float* v, const int64_t* offsets, double scale,
+               const int64_t* rows, int64_t n_rows, double* out, double* lse, int threads) {
+    if (B < 0 || S < 1 || H < 1 || d < 1 || n_rows < 0) return -1;
+    for (int64_t r = 0; r < n_rows; ++r)
+        if (rows[r] < 0 || rows[r] >= S) return -1;
+    set_threads(threads);
+    int err = 0;
+    const int64_t total = B * H * n_rows;
+#pragma omp parallel
+    {
+        double* s = NULL;
+        int64_t cap = 0;
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < total; ++t) {
+            const int64_t u = t / (H * n_rows);
+            const int64_t h = (t / n_rows) % H;
+            const int64_t r = t % n_rows;
+            const int64_t i = rows[r];
+            const int64_t j0 = offsets[u], L = offsets[u + 1] - offsets[u];
+            const float* qi = q + u * q_user_stride + (i * H + h) * d;
+            double* o = out + ((u * n_rows + r) * H + h) * d;
+            double* ls = lse + (u * H + h) * n_rows + r;
+            if (L <= 0) {
+                for (int64_t c = 0; c < d; ++c) o[c] = 0.0;
+                *ls = -INFINITY;
+                continue;
+            }
+            if (L > cap) {
+                free(s);
+                s = (double*)malloc((size_t)L * sizeof(double));
+                cap = s ? L : 0;
+                if (!s) {
+#pragma omp atomic write
+                    err = 1;
+                    continue;
+                }
+            }
+            /* pass 1: scores and their maximum */
+            double m = -INFINITY;
+            for (int64_t j = 0; j < L; ++j) {
+                const float* kj = k + ((j0 + j) * H + h) * d;
+                double acc = 0.0;
+                for (int64_t c = 0; c < d; ++c) acc += (double)qi[c] * (double)kj[c];
+                s[j] = scale * acc;
+                if (s[j] > m) m = s[j];
+            }
+            /* pass 2: weights, their sum, weighted values */
+            double l = 0.0;
+            for (int64_t c = 0; c < d; ++c) o[c] = 0.0;
+            for (int64_t j = 0; j < L; ++j) {
+                const double p = exp(s[j] - m);
+                const float* vj = v + ((j0 + j) * H + h) * d;
+                l += p;
+                for (int64_t c = 0; c < d; ++c) o[c] += p * (double)vj[c];
+            }
+            for (int64_t c = 0; c < d; ++c) o[c] /= l;
+            *ls = m + log(l);
+        }
+        free(s);
+    }
+    return err ? -1 : 0;
+}
+
+/*
+ * QLA state of every (user, head):  z[u,h,c1,c2] = sum_j phi1(k_{j,h,c1}) v_{j,h,c2}
+ * ("phi(K[S])^T V[S]"; App. B "sum_j K[S]_j^T V[S]_j ... computed first",
+ * PAPER.md:680).  z: [B, H, d, d].
+ */
+int vo_qla_state(int64_t B, int64_t H, int64_t d, const float* k, const float* v,
+                 const int64_t* offsets, int phi1, double* z, int threads) {
+    if (B < 0 || H < 1 || d < 1) return -1;
+    set_threads(threads);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t t = 0; t < B * H; ++t) {
+        const int64_t u = t / H, h = t % H;
+        double* zu = z + t * d * d;
+        for (int64_t e = 0; e < d * d; ++e) zu[e] = 0.0;
+        for (int64_t j = offsets[u]; j < offsets[u + 1]; ++j) {
+            const float* kj = k + (j * H + h) * d;
+            const float* vj = v + (j * H + h) * d;
+            for (int64_t c1 = 0; c1 < d; ++c1) {
+                const double a = vo_act(phi1, (double)kj[c1]);
+                for (int64_t c2 = 0; c2 < d; ++c2) zu[c1 * d + c2] += a * (double)vj[c2];
+            }
+        }
+    }
+    return 0;
+}
+
+/*
+ * QLA output from a state:  Zbar = Z / N_u (if normalize and N_u > 0; Z itself is 0 when
+ * N_u = 0), O[u,i,h,:] = phi1(q_i) phi2(Zbar)   (B.2 PAPER.md:834;
+ * 1/N PAPER.md:646-649).  z: [B, H, d, d]; n_items: [B]; out: [B, S, H, d].
+ */
+int vo_qla_finalize(int64_t B, int64_t S, int64_t H, int64_t d, const float* q,
+                    int64_t q_user_stride, const double* z, const int64_t* n_items, int phi1,
+                    int phi2, int normalize, double* out, int threads) {
+    if (B < 0 || S < 1 || H < 1 || d < 1) return -1;
+    set_threads(threads);
+#pragma omp parallel
+    {
+        double* w = (double*)malloc((size_t)(d * d) * sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < B * H; ++t) {
+            const int64_t u = t / H, h = t % H;
+            const double* zu = z + t * d * d;
+            const double inv = (normalize && n_items[u] > 0) ? 1.0 / (double)n_items[u] : 1.0;
+            for (int64_t e = 0; e < d * d; ++e) w[e] = vo_act(phi2, zu[e] * inv);
+            for (int64_t i = 0; i < S; ++i) {
+                const float* qi = q + u * q_user_stride + (i * H + h) * d;
+                double* o = out + ((u * S + i) * H + h) * d;
+                for (int64_t c2 = 0; c2 < d; ++c2) o[c2] = 0.0;
+                for (int64_t c1 = 0; c1 < d; ++c1) {
+                    const double a = vo_act(phi1, (double)qi[c1]);
+                    for (int64_t c2 = 0; c2 < d; ++c2) o[c2] += a * w[c1 * d + c2];
+                }
+            }
+        }
+        free(w);
+    }
+    return 0;
+}
+
+/*
+ * LSE merge of P softmax partials over disjoint key sets, for n rows of width d
+ * (flash-decoding style combination; the exact identity
+ *   softmax over A u B = e^{lse_A - lse} O_A + e^{lse_B - lse} O_B,  lse = ln(e^{lse_A}+e^{lse_B})).
+ *   part_o: [P, n, d]; part_lse: [P, n]; out: [n, d]; lse: [n].  Parts with lse = -inf weigh 0.
+ */
+int vo_merge_lse(int64_t P, int64_t n, int64_t d, const double* part_o, const double* part_lse,
+                 double* out, double* lse) {
+    for (int64_t r = 0; r < n; ++r) {
+        double m = -INFINITY;
+        for (int64_t p = 0; p < P; ++p)
+            if (part_lse[p * n + r] > m) m = part_lse[p * n + r];
+        double* o = out + r * d;
+        for (int64_t c = 0; c < d; ++c) o[c] = 0.0;
+        if (m == -INFINITY) {
+            lse[r] = -INFINITY;
+            continue;
+        }
+        double l = 0.0;
+        for (int64_t p = 0; p < P; ++p) l += exp(part_lse[p * n + r] - m);
+        const double L = m + log(l);
+        for (int64_t p = 0; p < P; ++p) {
+            const double w = exp(part_lse[p * n + r] - L);
+            for (int64_t c = 0; c < d; ++c) o[c] += w * part_o[(p * n + r) * d + c];
+        }
+        lse[r] = L;
+    }
+    return 0;
+}
+
+/* Plain sum of P QLA states (split == sum of states, the associativity of sum_j). */
+int vo_merge_sum(int64_t P, int64_t n, const double* parts, double* out) {
+    for (int64_t e = 0; e < n; ++e) {
+        double acc = 0.0;
+        for (int64_t p = 0; p < P; ++p) acc += parts[p * n + e];
+        out[e] = acc;
+    }
+    return 0;
+}

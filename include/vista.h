@@ -1,0 +1,164 @@
+/*
+ * vista.h -- C ABI of libvista: B200 (sm_100a) kernels for VISTA stage-1 user-history
+ * summarization (arXiv 2510.22049, "VISTA").  Citations are PAPER.md:<line> of the paper source.
+ *
+ * WHAT IS COMPUTED.  S learned "virtual seed" query tokens, shared across users (PAPER.md:148,
+ * Sec. 3.2 "initialized randomly as shared parameters across users"), attend over each user's
+ * interaction history (UIH) of L_u item embeddings; the seed rows' outputs are the user's summary
+ * tokens.  Two accumulator forms:
+ *
+ *   VISTA_SOFTMAX  RowSoftmax(Q K^T) V  (Sec. 3.2.1), queries = the S seed rows:
+ *                  out[u,i,h,:] = sum_j softmax_j(scale * q_{i,h} . k_{j,h}) v_{j,h,:}
+ *                  lse[u,h,i]   = ln sum_j exp(scale * q_{i,h} . k_{j,h})        (natural log)
+ *   VISTA_QLA      quasi-linear attention, source part (Sec. 3.2.2; two
+ *                  activations PAPER.md:831-836, App. B.2):
+ *                  Z = sum_j phi1(k_j)^T v_j (d x d);  Zbar = Z / N_u if qla_normalize
+ *                  (the "1/N factor"; N_u = L_u);  out = phi1(Q) phi2(Zbar)
+ *
+ * No mask and no positional term (full attention).  Users are independent.
+ * Empty history (L_u = 0): softmax out = 0 and lse = -inf (the identity of the LSE merge);
+ * QLA Zbar = 0 so out = phi1(Q) phi2(0).
+ *
+ * LAYOUTS (row-major, last dimension contiguous, element strides in parentheses):
+ *   q       [S, H, d]     shared seeds (q_user_stride = 0), or user u's block at q + u*q_user_stride
+ *   k, v    [total_len, H, d]   jagged history of all users, user u owns rows
+ *                               [offsets[u], offsets[u+1])
+ *   offsets [B + 1] int64, DEVICE memory; offsets[0] = 0, non-decreasing, offsets[B] = total_len
+ *   out     [B, S, H, d]  (out_dtype)
+ *   lse     [B, H, S]     float32, may be NULL
+ *   part_o  softmax: [B, H, S, d] float32 normalized partial output;
+ *           QLA:     [B, H, d, d] float32 unnormalized partial state Z_p
+ *   part_lse softmax: [B, H, S] float32 (-inf for an empty shard); QLA: unused (may be NULL)
+ *
+ * OWNERSHIP AND SYNCHRONIZATION.  All tensor pointers are DEVICE pointers owned by the caller,
+ * who also owns the workspace.  The library never allocates or frees device memory on these
+ * calls and never synchronizes: every call only enqueues kernels on `stream` (a cudaStream_t,
+ * NULL = legacy default stream).  Results are bitwise deterministic for fixed inputs, device and
+ * partition.  Calls are reentrant; concurrent calls on different streams need different
+ * workspaces.
+ *
+ * ERRORS.  Return codes only (no exceptions cross the ABI).  Every host-checkable error is
+ * reported BEFORE any launch, with no side effect: NULL pointers, B < 0, S < 1, H < 1, an
+ * unsupported (dtype, d, attn) combination, misalignment (16 B base for q/k/v/out; TMA needs
+ * 16 B strides), too small a workspace.  Offsets are a precondition (not read on the host);
+ * vista_check_offsets() validates them (synchronizing, debug only).  Launch failures return
+ * VISTA_ERR_CUDA.
+ *
+ * DISPATCH (by shape, not a backend switch):
+ *   bf16, d = 128, softmax, S % 128 == 0  -> TMA + tcgen05/TMEM kernel (sm_100a)
+ *   bf16, d = 128, QLA                    -> TMA + tcgen05/TMEM state kernel + finalize
+ *   f32 or bf16 with d in {32, 64, 128} otherwise -> SIMT fp32-accumulate kernels
+ */
+#ifndef VISTA_H_
+#define VISTA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VISTA_ABI_VERSION 1
+
+typedef enum {
+    VISTA_OK = 0,
+    VISTA_ERR_NULL = 1,        /* a required pointer is NULL                          */
+    VISTA_ERR_INVALID = 2,     /* bad size / enum / abi_version                       */
+    VISTA_ERR_UNSUPPORTED = 3, /* valid but unsupported (dtype, d, attn, S) combination */
+    VISTA_ERR_MISALIGNED = 4,  /* a pointer is not 16-byte aligned                    */
+    VISTA_ERR_WORKSPACE = 5,   /* workspace_bytes < vista_summarize_workspace_size     */
+    VISTA_ERR_CUDA = 6,        /* a CUDA runtime / driver call failed                 */
+    VISTA_ERR_OFFSETS = 7      /* vista_check_offsets: offsets violate the precondition */
+} vista_status_t;
+
+typedef enum { VISTA_F32 = 0, VISTA_BF16 = 1 } vista_dtype_t;
+typedef enum { VISTA_SOFTMAX = 0, VISTA_QLA = 1 } vista_attn_t;
+/* phi choices: identity; SiLU x*sigmoid(x); shifted ELU x if x >= 1 else e^{x-1}
+ * (App. B.1.5). */
+typedef enum { VISTA_ACT_IDENTITY = 0, VISTA_ACT_SILU = 1, VISTA_ACT_SHIFTED_ELU = 2 } vista_act_t;
+
+typedef struct {
+    int32_t abi_version;   /* must equal VISTA_ABI_VERSION                                  */
+    int32_t num_users;     /* B >= 0                                                        */
+    int32_t num_summary;   /* S >= 1  (summary tokens = seed queries)                       */
+    int32_t num_heads;     /* H >= 1                                                        */
+    int32_t head_dim;      /* d in {32, 64, 128}                                            */
+    int32_t in_dtype;      /* vista_dtype_t of q, k, v                                      */
+    int32_t out_dtype;     /* vista_dtype_t of out                                          */
+    int32_t attn;          /* vista_attn_t                                                  */
+    float softmax_scale;   /* softmax only; NaN => 1/sqrt(d) (reading R4)          */
+    int32_t qla_phi1;      /* vista_act_t, QLA only                                         */
+    int32_t qla_phi2;      /* vista_act_t, QLA only                                         */
+    int32_t qla_normalize; /* QLA only: 1 => Zbar = Z / L_u (reading R10), 0 => Zbar = Z     */
+    int64_t q_user_stride; /* elements between consecutive users' Q blocks; 0 => shared seeds */
+} vista_desc_t;
+
+/* Version of the ABI this library implements (VISTA_ABI_VERSION). */
+int vista_abi_version(void);
+
+/* Static, human-readable name of a status code (never NULL). */
+const char* vista_status_string(int status);
+
+/* Last CUDA error string recorded by a call that returned VISTA_ERR_CUDA on this thread. */
+const char* vista_last_cuda_error(void);
+
+/*
+ * Bytes of device workspace vista_summarize_fwd / vista_summarize_partial need for this
+ * descriptor and history size.  Depends on (B, S, H, d, attn, total_len) and the current
+ * device's SM count.  Writes *bytes; host only, no launch.
+ */
+vista_status_t vista_summarize_workspace_size(const vista_desc_t* desc, int64_t total_len,
+                                              size_t* bytes);
+
+/*
+ * Full summarization of B users: writes out [B,S,H,d] and (softmax, if lse != NULL) lse [B,H,S].
+ * total_len is the host copy of offsets[B].  Asynchronous on `stream`.
+ */
+vista_status_t vista_summarize_fwd(const vista_desc_t* desc, const void* q, const void* k,
+                                   const void* v, const int64_t* offsets, int64_t total_len,
+                                   void* out, float* lse, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
+/*
+ * Partial pass over one shard of every user's history (split-L across GPUs, flash-decoding
+ * style).  Same inputs as vista_summarize_fwd; here offsets describe THIS shard's rows of each
+ * user.  Writes part_o and (softmax) part_lse, laid out as described above.  Combine the shards
+ * of all parts with vista_summarize_merge.
+ */
+vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, const void* k,
+                                       const void* v, const int64_t* offsets, int64_t total_len,
+                                       float* part_o, float* part_lse, void* workspace,
+                                       size_t workspace_bytes, void* stream);
+
+/*
+ * Merge num_parts >= 1 partials stacked along a leading axis (e.g. an all_gather output):
+ *   softmax: part_o [P,B,H,S,d], part_lse [P,B,H,S] -> out [B,S,H,d], lse [B,H,S] (lse may be
+ *            NULL).  lse = logsumexp_p lse_p; out = sum_p exp(lse_p - lse) O_p, ascending p;
+ *            parts with lse_p = -inf weigh 0; all -inf -> out 0, lse -inf.
+ *   QLA:     part_o [P,B,H,d,d] -> Z = sum_p Z_p (ascending p), then finalize with q and
+ *            user_len [B] (int64, device; total L_u over all parts, used when qla_normalize).
+ * q and user_len are read for QLA only (may be NULL for softmax).
+ */
+vista_status_t vista_summarize_merge(const vista_desc_t* desc, int32_t num_parts,
+                                     const float* part_o, const float* part_lse, const void* q,
+                                     const int64_t* user_len, void* out, float* lse, void* stream);
+
+/*
+ * Debug: copies offsets to the host (synchronizes `stream`) and checks offsets[0] = 0,
+ * non-decreasing, offsets[B] = total_len.  VISTA_OK or VISTA_ERR_OFFSETS.
+ */
+vista_status_t vista_check_offsets(const int64_t* offsets, int32_t num_users, int64_t total_len,
+                                   void* stream);
+
+/*
+ * Name of the kernel path vista_summarize_fwd would take for this descriptor:
+ * "sm100_softmax", "sm100_qla", "simt_softmax", "simt_qla", or NULL if unsupported.
+ */
+const char* vista_dispatch_name(const vista_desc_t* desc);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VISTA_H_ */

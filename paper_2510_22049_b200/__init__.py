@@ -1,0 +1,262 @@
+"""VISTA stage-1 user-history summarization on B200 -- Python binding of libvista (include/vista.h).
+
+The binding only marshals arguments: every step of the hot path runs in the CUDA kernels of
+``libvista.so`` (built in-tree from ``csrc/`` by ``__graft_entry__.build()``).  There is no CPU or
+PyTorch fallback: ``load()`` raises if the library or a CUDA device is missing.  PyTorch is used
+for device memory and streams only.
+
+ABI entry points (same names as the C ABI):
+    vista_abi_version, vista_status_string, vista_summarize_workspace_size,
+    vista_summarize_fwd, vista_summarize_partial, vista_summarize_merge,
+    vista_check_offsets, vista_dispatch_name
+Convenience wrappers on torch tensors: ``make_desc``, ``summarize``, ``summarize_partial``,
+``summarize_merge``.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+__all__ = [
+    "VistaError", "Desc", "load", "lib_path", "make_desc",
+    "vista_abi_version", "vista_status_string", "vista_summarize_workspace_size",
+    "vista_summarize_fwd", "vista_summarize_partial", "vista_summarize_merge",
+    "vista_check_offsets", "vista_dispatch_name",
+    "summarize", "summarize_partial", "summarize_merge",
+    "SOFTMAX", "QLA", "F32", "BF16", "ACT",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libvista.so")
+
+ABI_VERSION = 1
+F32, BF16 = 0, 1
+SOFTMAX, QLA = 0, 1
+ACT = {"identity": 0, "silu": 1, "shifted_elu": 2}
+
+_lib = None
+
+
+class VistaError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = f"{where}: {_status_name(status)}"
+        if status == 6 and _lib is not None:
+            msg += f" ({_lib.vista_last_cuda_error().decode()})"
+        super().__init__(msg)
+        self.status = status
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("num_users", ctypes.c_int32),
+        ("num_summary", ctypes.c_int32),
+        ("num_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("in_dtype", ctypes.c_int32),
+        ("out_dtype", ctypes.c_int32),
+        ("attn", ctypes.c_int32),
+        ("softmax_scale", ctypes.c_float),
+        ("qla_phi1", ctypes.c_int32),
+        ("qla_phi2", ctypes.c_int32),
+        ("qla_normalize", ctypes.c_int32),
+        ("q_user_stride", ctypes.c_int64),
+    ]
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libvista.so (fails loudly: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(f"libvista.so not built ({_LIB_PATH}); run __graft_entry__.build()")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    DP = ctypes.POINTER(Desc)
+    lib.vista_abi_version.restype = ctypes.c_int
+    lib.vista_status_string.restype = ctypes.c_char_p
+    lib.vista_status_string.argtypes = [ctypes.c_int]
+    lib.vista_last_cuda_error.restype = ctypes.c_char_p
+    lib.vista_dispatch_name.restype = ctypes.c_char_p
+    lib.vista_dispatch_name.argtypes = [DP]
+    lib.vista_summarize_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
+    lib.vista_summarize_fwd.argtypes = [DP, P, P, P, P, i64, P, P, P, sz, P]
+    lib.vista_summarize_partial.argtypes = [DP, P, P, P, P, i64, P, P, P, sz, P]
+    lib.vista_summarize_merge.argtypes = [DP, i32, P, P, P, P, P, P, P]
+    lib.vista_check_offsets.argtypes = [P, i32, i64, P]
+    for f in ("vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
+              "vista_summarize_merge", "vista_check_offsets"):
+        getattr(lib, f).restype = ctypes.c_int
+    if lib.vista_abi_version() != ABI_VERSION:
+        raise RuntimeError("libvista ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def _status_name(s: int) -> str:
+    return load().vista_status_string(s).decode() if _lib else str(s)
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise VistaError(status, where)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+# ----------------------------------------------------------------------------- raw ABI
+def vista_abi_version() -> int:
+    return load().vista_abi_version()
+
+
+def vista_status_string(status: int) -> str:
+    return load().vista_status_string(status).decode()
+
+
+def vista_dispatch_name(desc: Desc) -> str | None:
+    r = load().vista_dispatch_name(ctypes.byref(desc))
+    return r.decode() if r else None
+
+
+def vista_summarize_workspace_size(desc: Desc, total_len: int) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load().vista_summarize_workspace_size(ctypes.byref(desc), int(total_len), ctypes.byref(n)),
+           "vista_summarize_workspace_size")
+    return n.value
+
+
+def vista_summarize_fwd(desc, q, k, v, offsets, total_len, out, lse, workspace, workspace_bytes, stream=None):
+    _check(load().vista_summarize_fwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                                      int(total_len), _ptr(out), _ptr(lse), _ptr(workspace),
+                                      int(workspace_bytes), _stream(stream)), "vista_summarize_fwd")
+
+
+def vista_summarize_partial(desc, q, k, v, offsets, total_len, part_o, part_lse, workspace,
+                            workspace_bytes, stream=None):
+    _check(load().vista_summarize_partial(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                                          int(total_len), _ptr(part_o), _ptr(part_lse), _ptr(workspace),
+                                          int(workspace_bytes), _stream(stream)), "vista_summarize_partial")
+
+
+def vista_summarize_merge(desc, num_parts, part_o, part_lse, q, user_len, out, lse, stream=None):
+    _check(load().vista_summarize_merge(ctypes.byref(desc), int(num_parts), _ptr(part_o), _ptr(part_lse),
+                                        _ptr(q), _ptr(user_len), _ptr(out), _ptr(lse), _stream(stream)),
+           "vista_summarize_merge")
+
+
+def vista_check_offsets(offsets, num_users, total_len, stream=None):
+    _check(load().vista_check_offsets(_ptr(offsets), int(num_users), int(total_len), _stream(stream)),
+           "vista_check_offsets")
+
+
+# ----------------------------------------------------------------------------- torch helpers
+def make_desc(B, S, H, d, *, in_dtype=BF16, out_dtype=None, attn=SOFTMAX, scale=None,
+              phi1="silu", phi2="silu", normalize=True, q_user_stride=0) -> Desc:
+    return Desc(ABI_VERSION, int(B), int(S), int(H), int(d), int(in_dtype),
+                int(in_dtype if out_dtype is None else out_dtype), int(attn),
+                float("nan") if scale is None else float(scale), ACT[phi1], ACT[phi2],
+                int(bool(normalize)), int(q_user_stride))
+
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _desc_for(q, k, offsets, attn, scale, phi1, phi2, normalize, out_dtype):
+    B = offsets.numel() - 1
+    S, H, d = q.shape[-3:]
+    stride = S * H * d if q.dim() == 4 else 0
+    return make_desc(B, S, H, d, in_dtype=_dtype_code(q), out_dtype=out_dtype, attn=attn, scale=scale,
+                     phi1=phi1, phi2=phi2, normalize=normalize, q_user_stride=stride)
+
+
+def _workspace(desc, total_len, device, workspace=None):
+    import torch
+    need = vista_summarize_workspace_size(desc, total_len)
+    if workspace is not None and workspace.numel() >= need:
+        return workspace, need
+    return torch.empty(max(need, 16), dtype=torch.uint8, device=device), need
+
+
+def summarize(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=None, phi1="silu", phi2="silu",
+              normalize=True, out_dtype=None, workspace=None, stream=None):
+    """Summary tokens of every user: out [B,S,H,d] (+ lse [B,H,S] for softmax).
+
+    q: [S,H,d] shared seeds or [B,S,H,d]; k, v: [total_len,H,d]; offsets: int64 [B+1] on device.
+    total_len (host int) avoids a device read; pass it on the hot path.
+    """
+    import torch
+    if total_len is None:
+        total_len = k.shape[0]
+    desc = _desc_for(q, k, offsets, attn, scale, phi1, phi2, normalize, out_dtype)
+    B, S, H, d = desc.num_users, desc.num_summary, desc.num_heads, desc.head_dim
+    odt = torch.bfloat16 if desc.out_dtype == BF16 else torch.float32
+    out = torch.empty((B, S, H, d), dtype=odt, device=q.device)
+    lse = torch.empty((B, H, S), dtype=torch.float32, device=q.device) if attn == SOFTMAX else None
+    ws, need = _workspace(desc, total_len, q.device, workspace)
+    vista_summarize_fwd(desc, q, k, v, offsets, total_len, out, lse, ws, ws.numel(), stream)
+    return out, lse
+
+
+def summarize_partial(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=None, phi1="silu",
+                      phi2="silu", normalize=True, workspace=None, stream=None):
+    """Partial over one history shard: softmax -> (part_o [B,H,S,d] f32, part_lse [B,H,S]);
+    QLA -> (Z [B,H,d,d] f32, None)."""
+    import torch
+    if total_len is None:
+        total_len = k.shape[0]
+    desc = _desc_for(q, k, offsets, attn, scale, phi1, phi2, normalize, None)
+    B, S, H, d = desc.num_users, desc.num_summary, desc.num_heads, desc.head_dim
+    if attn == SOFTMAX:
+        po = torch.empty((B, H, S, d), dtype=torch.float32, device=q.device)
+        pl = torch.empty((B, H, S), dtype=torch.float32, device=q.device)
+    else:
+        po = torch.empty((B, H, d, d), dtype=torch.float32, device=q.device)
+        pl = None
+    ws, need = _workspace(desc, total_len, q.device, workspace)
+    vista_summarize_partial(desc, q, k, v, offsets, total_len, po, pl, ws, ws.numel(), stream)
+    return po, pl
+
+
+def summarize_merge(part_o, part_lse, *, q, attn=SOFTMAX, user_len=None, scale=None, phi1="silu",
+                    phi2="silu", normalize=True, out_dtype=None, stream=None):
+    """Merge stacked partials [P, ...] (e.g. all_gather output) into (out [B,S,H,d], lse)."""
+    import torch
+    P = part_o.shape[0]
+    if attn == SOFTMAX:
+        B, H, S, d = part_o.shape[1:]
+    else:
+        B, H, d, _ = part_o.shape[1:]
+        S = q.shape[-3]
+    in_dtype = _dtype_code(q)
+    desc = make_desc(B, S, H, d, in_dtype=in_dtype, out_dtype=out_dtype, attn=attn, scale=scale, phi1=phi1,
+                     phi2=phi2, normalize=normalize, q_user_stride=(S * H * d if q.dim() == 4 else 0))
+    odt = torch.bfloat16 if desc.out_dtype == BF16 else torch.float32
+    out = torch.empty((B, S, H, d), dtype=odt, device=part_o.device)
+    lse = torch.empty((B, H, S), dtype=torch.float32, device=part_o.device) if attn == SOFTMAX else None
+    vista_summarize_merge(desc, P, part_o, part_lse, q, user_len, out, lse, stream)
+    return out, lse

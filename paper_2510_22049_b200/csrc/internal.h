@@ -1,0 +1,71 @@
+// internal.h -- host/device declarations shared by the libvista kernels and the C ABI layer.
+// Not part of the public ABI (include/vista.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/vista.h"
+
+namespace vista {
+
+constexpr int kTile = 128;  // history items per tile (= TMA box rows = MMA N of the score GEMM)
+
+enum OutMode : int { OUT_FINAL = 0, OUT_PARTIAL = 1 };
+
+// Where a finished (normalized) output row goes.
+struct OutSpec {
+    int mode;            // OUT_FINAL: out[B,S,H,d] (out_dtype) + lse[B,H,S]; OUT_PARTIAL: part_o[B,H,S,d] f32 + part_lse[B,H,S]
+    int out_bf16;        // OUT_FINAL only: 1 -> bf16, 0 -> f32
+    void* out;           // FINAL: out;  PARTIAL: part_o (float*)
+    float* lse;          // may be NULL in FINAL mode
+};
+
+// Everything a launch needs (filled by the ABI layer after validation).
+struct Problem {
+    int B, S, H, d;
+    int in_bf16;               // 1: q/k/v bf16, 0: f32
+    int attn;                  // vista_attn_t
+    float scale;               // softmax scale (> 0)
+    int phi1, phi2, normalize; // QLA
+    int64_t q_user_stride;     // elements; 0 = shared
+    int64_t total_len;
+    const void* q;
+    const void* k;
+    const void* v;
+    const int64_t* offsets;
+    OutSpec outs;
+    cudaStream_t stream;
+    int num_sms;
+};
+
+// Workspace carve-up (all offsets 256-B aligned).
+struct Workspace {
+    size_t uts_off, slot_unit_off, slot_o_off, slot_lse_off, zbuf_off, total;
+    int num_ctas;      // persistent grid size used by the tiled kernels
+    int rows_per_unit; // softmax: query rows per work unit (NQ * 128); QLA: d
+};
+
+enum Path : int { PATH_NONE = 0, PATH_SM100_SOFTMAX, PATH_SM100_QLA, PATH_SIMT_SOFTMAX, PATH_SIMT_QLA };
+
+Path choose_path(const Problem& p);
+Workspace plan_workspace(const Problem& p, bool partial);
+
+// ---- launchers (return cudaError_t of the launch) ----
+// user tile starts: uts[u] = sum_{u'<u} ceil(L_u' / 128); also fills the outputs of empty users
+// (softmax: zeros / -inf in outs; QLA: zeros in zbuf if non-NULL).
+cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf);
+cudaError_t launch_sm100_softmax(const Problem& p, const Workspace& w, char* ws);
+cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf);
+cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, char* ws);
+cudaError_t launch_merge_qla_slots(const Problem& p, const Workspace& w, char* ws, float* zbuf);
+cudaError_t launch_simt_softmax(const Problem& p);
+cudaError_t launch_simt_qla_state(const Problem& p, float* zbuf);
+// O = phi1(Q) phi2( (sum_{p<P} Z_p) / N_u ) ; Z parts at zparts + p * part_stride (floats),
+// N_u from offsets (user_len == NULL) or user_len[u].
+cudaError_t launch_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
+                                const int64_t* user_len);
+// Merge P stacked softmax partials [P,B,H,S,d] / [P,B,H,S] into outs.
+cudaError_t launch_merge_softmax_parts(const Problem& p, int P, const float* part_o, const float* part_lse);
+
+}  // namespace vista

@@ -1,0 +1,526 @@
+// kernels_misc.cu -- the small kernels around the tiled sm100 kernels, and the SIMT path.
+//
+//   user_tiles_kernel        offsets -> per-user tile prefix (work decomposition), empty-user fill
+//   merge_softmax_slots      split-L LSE merge of intra-GPU partial slots (flash-decoding combine)
+//   merge_qla_slots          split-L sum of QLA state partials (plain sum, ascending CTA order)
+//   merge_softmax_parts      LSE merge of P stacked partials (multi-GPU history-length shards)
+//   qla_finalize_kernel      O = phi1(Q) phi2((sum_p Z_p) / N_u)
+//   simt_softmax_kernel      fp32-accumulate SIMT seed-row softmax (f32 inputs, or d / S the tiled
+//                            kernel does not cover); online softmax over 32-key chunks
+//   simt_qla_state_kernel    Z = sum_j phi1(k_j)^T v_j with FFMA (f32 inputs or d != 128)
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "internal.h"
+
+namespace vista {
+
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float act(int kind, float x) {
+    // phi: identity; SiLU x*sigmoid(x); shifted ELU (x >= 1 -> x)
+    if (kind == VISTA_ACT_SILU) return x / (1.f + __expf(-x));
+    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? x : __expf(x - 1.f);
+    return x;
+}
+
+template <typename T>
+__device__ __forceinline__ float ld(const T* p);
+template <>
+__device__ __forceinline__ float ld<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ld<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Store one normalized output element (row i of user u, head h, channel c) per OutSpec.
+__device__ __forceinline__ void out_store(const OutSpec& o, int S, int H, int d, int u, int h, int i, int c, float val) {
+    if (o.mode == OUT_PARTIAL) {
+        reinterpret_cast<float*>(o.out)[(((size_t)u * H + h) * S + i) * d + c] = val;
+    } else {
+        const size_t idx = (((size_t)u * S + i) * H + h) * d + c;
+        if (o.out_bf16) reinterpret_cast<__nv_bfloat16*>(o.out)[idx] = __float2bfloat16_rn(val);
+        else reinterpret_cast<float*>(o.out)[idx] = val;
+    }
+}
+__device__ __forceinline__ void lse_store(const OutSpec& o, int S, int H, int u, int h, int i, float val) {
+    if (o.lse) o.lse[((size_t)u * H + h) * S + i] = val;
+}
+
+// ---------------------------------------------------------------------------------------------
+__global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, int64_t* __restrict__ uts, OutSpec outs,
+                                  int S, int H, int d, int softmax, float* __restrict__ zbuf) {
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        carry = 0;
+        uts[0] = 0;
+    }
+    __syncthreads();
+    for (int base = 0; base < B; base += blockDim.x) {
+        const int u = base + tid;
+        int64_t T = 0;
+        if (u < B) T = (offsets[u + 1] - offsets[u] + kTile - 1) / kTile;
+        int64_t x = T;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int64_t w = (lane < (int)(blockDim.x / 32)) ? wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;  // inclusive warp prefix
+        }
+        __syncthreads();
+        const int64_t incl = x + (warp > 0 ? wsum[warp - 1] : 0) + carry;
+        if (u < B) uts[u + 1] = incl;
+        __syncthreads();
+        if (tid == blockDim.x - 1) carry = incl;
+        __syncthreads();
+    }
+    // empty users: softmax out = 0, lse = -inf (identity of the LSE merge); QLA Z = 0
+    for (int u = 0; u < B; ++u) {
+        if (offsets[u + 1] != offsets[u]) continue;
+        if (softmax) {
+            const size_t n = (size_t)S * H * d;
+            if (outs.mode == OUT_PARTIAL) {
+                float* o = reinterpret_cast<float*>(outs.out) + (size_t)u * n;
+                for (size_t e = tid; e < n; e += blockDim.x) o[e] = 0.f;
+            } else if (outs.out_bf16) {
+                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(outs.out) + (size_t)u * n;
+                for (size_t e = tid; e < n; e += blockDim.x) o[e] = __float2bfloat16_rn(0.f);
+            } else {
+                float* o = reinterpret_cast<float*>(outs.out) + (size_t)u * n;
+                for (size_t e = tid; e < n; e += blockDim.x) o[e] = 0.f;
+            }
+            if (outs.lse)
+                for (int e = tid; e < H * S; e += blockDim.x) outs.lse[(size_t)u * H * S + e] = -INFINITY;
+        } else if (zbuf) {
+            const size_t n = (size_t)H * d * d;
+            for (size_t e = tid; e < n; e += blockDim.x) zbuf[(size_t)u * n + e] = 0.f;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Is slot s the first slot of its unit's run?  (units are non-decreasing over valid slots)
+__device__ __forceinline__ bool slot_is_head(const int* slot_unit, int s, int n) {
+    for (int p = s - 1; p >= 0; --p) {
+        const int m = slot_unit[p];
+        if (m >= 0) return m != n;
+    }
+    return true;
+}
+
+// One warp per output row; lanes over 128 channels (float4).  rows = query rows per unit.
+__global__ void merge_softmax_slots_kernel(const int* __restrict__ slot_unit, int num_slots, const float* __restrict__ slot_o,
+                                           const float* __restrict__ slot_lse, int rows, OutSpec outs, int S, int H,
+                                           int G) {
+    const int s = blockIdx.x;
+    const int n = slot_unit[s];
+    if (n < 0 || !slot_is_head(slot_unit, s, n)) return;
+    const int row = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    float M = -INFINITY;
+    for (int x = s; x < num_slots; ++x) {
+        const int m = slot_unit[x];
+        if (m < 0) continue;
+        if (m != n) break;
+        M = fmaxf(M, slot_lse[(size_t)x * rows + row]);
+    }
+    float l = 0.f;
+    for (int x = s; x < num_slots; ++x) {
+        const int m = slot_unit[x];
+        if (m < 0) continue;
+        if (m != n) break;
+        l += expf(slot_lse[(size_t)x * rows + row] - M);
+    }
+    const float lse = M + logf(l);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int x = s; x < num_slots; ++x) {
+        const int m = slot_unit[x];
+        if (m < 0) continue;
+        if (m != n) break;
+        const float w = expf(slot_lse[(size_t)x * rows + row] - lse);
+        const float4 o = reinterpret_cast<const float4*>(slot_o + ((size_t)x * rows + row) * 128)[lane];
+        acc.x += w * o.x;
+        acc.y += w * o.y;
+        acc.z += w * o.z;
+        acc.w += w * o.w;
+    }
+    const int HG = H * G;
+    const int u = n / HG, hg = n % HG, h = hg / G, g = hg % G;
+    const int i = g * rows + row;
+    out_store(outs, S, H, 128, u, h, i, lane * 4 + 0, acc.x);
+    out_store(outs, S, H, 128, u, h, i, lane * 4 + 1, acc.y);
+    out_store(outs, S, H, 128, u, h, i, lane * 4 + 2, acc.z);
+    out_store(outs, S, H, 128, u, h, i, lane * 4 + 3, acc.w);
+    if (lane == 0) lse_store(outs, S, H, u, h, i, lse);
+}
+
+// Sum the run of QLA state slots of each split unit into zbuf[unit] (d = 128 rows of 128).
+__global__ void merge_qla_slots_kernel(const int* __restrict__ slot_unit, int num_slots, const float* __restrict__ slot_o,
+                                       float* __restrict__ zbuf) {
+    const int s = blockIdx.x;
+    const int n = slot_unit[s];
+    if (n < 0 || !slot_is_head(slot_unit, s, n)) return;
+    const int row = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int x = s; x < num_slots; ++x) {
+        const int m = slot_unit[x];
+        if (m < 0) continue;
+        if (m != n) break;
+        const float4 o = reinterpret_cast<const float4*>(slot_o + ((size_t)x * 128 + row) * 128)[lane];
+        acc.x += o.x;
+        acc.y += o.y;
+        acc.z += o.z;
+        acc.w += o.w;
+    }
+    reinterpret_cast<float4*>(zbuf + ((size_t)n * 128 + row) * 128)[lane] = acc;
+}
+
+// P stacked partials part_o [P,B,H,S,d] / part_lse [P,B,H,S] -> outs (FINAL).  One warp per row.
+template <int D>
+__global__ void merge_softmax_parts_kernel(int P, int B, int H, int S, const float* __restrict__ part_o,
+                                           const float* __restrict__ part_lse, OutSpec outs) {
+    const int64_t r = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;  // row index over (u, h, i)
+    const int lane = threadIdx.x % 32;
+    const int64_t nrows = (int64_t)B * H * S;
+    if (r >= nrows) return;
+    float M = -INFINITY;
+    for (int p = 0; p < P; ++p) M = fmaxf(M, part_lse[p * nrows + r]);
+    constexpr int V = D / 32;
+    float acc[V];
+#pragma unroll
+    for (int t = 0; t < V; ++t) acc[t] = 0.f;
+    float lse = -INFINITY;
+    if (M != -INFINITY) {
+        float l = 0.f;
+        for (int p = 0; p < P; ++p) l += expf(part_lse[p * nrows + r] - M);
+        lse = M + logf(l);
+        for (int p = 0; p < P; ++p) {
+            const float w = expf(part_lse[p * nrows + r] - lse);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc[t] += w * part_o[(p * nrows + r) * D + lane + 32 * t];
+        }
+    }
+    const int u = (int)(r / ((int64_t)H * S)), h = (int)((r / S) % H), i = (int)(r % S);
+#pragma unroll
+    for (int t = 0; t < V; ++t) out_store(outs, S, H, D, u, h, i, lane + 32 * t, acc[t]);
+    if (lane == 0) lse_store(outs, S, H, u, h, i, lse);
+}
+
+// ---------------------------------------------------------------------------------------------
+// O[u, i, h, :] = phi1(q_i) W,  W = phi2((sum_p Z_p[u,h]) * inv_N).  Block: 64 rows x D cols,
+// 256 threads, thread tile RT rows x 4 cols.
+template <int D, typename TQ>
+__global__ void __launch_bounds__(256) qla_finalize_kernel(const TQ* __restrict__ q, int64_t q_user_stride,
+                                                           const float* __restrict__ zparts, int P, int64_t part_stride,
+                                                           const int64_t* __restrict__ offsets,
+                                                           const int64_t* __restrict__ user_len, int S, int H, int phi1,
+                                                           int phi2, int normalize, OutSpec outs) {
+    constexpr int CT = D / 4;          // column-threads
+    constexpr int RTH = 256 / CT;      // row-threads
+    constexpr int RT = 64 / RTH;       // rows per thread
+    extern __shared__ float sm[];
+    float* W = sm;                     // [D][D]
+    float* Qt = sm + D * D;            // [D][64] phi1(q) transposed
+    const int unit = blockIdx.y;       // u * H + h
+    const int u = unit / H, h = unit % H;
+    const int i0 = blockIdx.x * 64;
+    const int64_t N = user_len ? user_len[u] : (offsets[u + 1] - offsets[u]);
+    const float inv = (normalize && N > 0) ? 1.f / (float)N : 1.f;
+    for (int e = threadIdx.x; e < D * D; e += 256) {
+        float z = 0.f;
+        for (int p = 0; p < P; ++p) z += zparts[(size_t)p * part_stride + (size_t)unit * D * D + e];
+        W[e] = act(phi2, z * inv);
+    }
+    const TQ* qb = q + (size_t)u * q_user_stride;
+    for (int e = threadIdx.x; e < 64 * D; e += 256) {
+        const int r = e / D, c = e % D;
+        const int i = i0 + r;
+        Qt[c * 64 + r] = (i < S) ? act(phi1, ld<TQ>(qb + ((size_t)i * H + h) * D + c)) : 0.f;
+    }
+    __syncthreads();
+    const int ct = threadIdx.x % CT, rt = threadIdx.x / CT;
+    float acc[RT][4];
+#pragma unroll
+    for (int a = 0; a < RT; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+#pragma unroll 4
+    for (int c1 = 0; c1 < D; ++c1) {
+        const float4 w = *reinterpret_cast<const float4*>(W + c1 * D + ct * 4);
+        float qv[RT];
+#pragma unroll
+        for (int a = 0; a < RT; ++a) qv[a] = Qt[c1 * 64 + rt * RT + a];
+#pragma unroll
+        for (int a = 0; a < RT; ++a) {
+            acc[a][0] = fmaf(qv[a], w.x, acc[a][0]);
+            acc[a][1] = fmaf(qv[a], w.y, acc[a][1]);
+            acc[a][2] = fmaf(qv[a], w.z, acc[a][2]);
+            acc[a][3] = fmaf(qv[a], w.w, acc[a][3]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < RT; ++a) {
+        const int i = i0 + rt * RT + a;
+        if (i >= S) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) out_store(outs, S, H, D, u, h, i, ct * 4 + b, acc[a][b]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// SIMT softmax: block = 8 warps = 8 query rows of one (user, head); 32-key chunks in smem.
+template <int D, typename T>
+__global__ void __launch_bounds__(256) simt_softmax_kernel(const T* __restrict__ q, int64_t q_user_stride,
+                                                           const T* __restrict__ k, const T* __restrict__ v,
+                                                           const int64_t* __restrict__ offsets, int S, int H,
+                                                           float scale_log2, OutSpec outs) {
+    __shared__ float Ks[32][D + 1];
+    __shared__ float Vs[32][D];
+    __shared__ float Qs[8][D];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int unit = blockIdx.y, u = unit / H, h = unit % H;
+    const int i = blockIdx.x * 8 + warp;
+    const bool active = i < S;
+    const int64_t j0 = offsets[u], L = offsets[u + 1] - offsets[u];
+    for (int c = lane; c < D; c += 32)
+        Qs[warp][c] = active ? ld<T>(q + (size_t)u * q_user_stride + ((size_t)i * H + h) * D + c) * scale_log2 : 0.f;
+    constexpr int V = D / 32;
+    float o[V];
+#pragma unroll
+    for (int t = 0; t < V; ++t) o[t] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int64_t kb = 0; kb < L; kb += 32) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 32 * D; e += 256) {
+            const int jj = e / D, c = e % D;
+            const int64_t j = kb + jj;
+            float kv = 0.f, vv = 0.f;
+            if (j < L) {
+                const size_t idx = ((size_t)(j0 + j) * H + h) * D + c;
+                kv = ld<T>(k + idx);
+                vv = ld<T>(v + idx);
+            }
+            Ks[jj][c] = kv;
+            Vs[jj][c] = vv;
+        }
+        __syncthreads();
+        if (!active) continue;
+        float s = 0.f;
+#pragma unroll 8
+        for (int c = 0; c < D; ++c) s = fmaf(Qs[warp][c], Ks[lane][c], s);
+        if (kb + lane >= L) s = -INFINITY;
+        const float m_new = fmaxf(m, warp_max(s));
+        const float corr = exp2f(m - m_new);
+        const float p = exp2f(s - m_new);
+        l = l * corr + warp_sum(p);
+#pragma unroll
+        for (int t = 0; t < V; ++t) o[t] *= corr;
+#pragma unroll 4
+        for (int jj = 0; jj < 32; ++jj) {
+            const float pj = __shfl_sync(0xffffffffu, p, jj);
+#pragma unroll
+            for (int t = 0; t < V; ++t) o[t] = fmaf(pj, Vs[jj][lane + 32 * t], o[t]);
+        }
+        m = m_new;
+    }
+    if (!active) return;
+    const float inv = L > 0 ? 1.f / l : 0.f;
+#pragma unroll
+    for (int t = 0; t < V; ++t) out_store(outs, S, H, D, u, h, i, lane + 32 * t, o[t] * inv);
+    if (lane == 0) {
+        const float lse = L > 0 ? (m + log2f(l)) * kLn2 : -INFINITY;
+        if (outs.mode == OUT_PARTIAL) outs.lse[((size_t)u * H + h) * S + i] = lse;
+        else lse_store(outs, S, H, u, h, i, lse);
+    }
+}
+
+// SIMT QLA state: block per (user, head); thread owns column c2 = t % D and rows c1 = t / D + k * (256 / D).
+template <int D, typename T>
+__global__ void __launch_bounds__(256) simt_qla_state_kernel(const T* __restrict__ k, const T* __restrict__ v,
+                                                             const int64_t* __restrict__ offsets, int H, int phi1,
+                                                             float* __restrict__ zbuf) {
+    constexpr int RSTEP = 256 / D;
+    constexpr int NR = D / RSTEP;  // accumulators per thread = D*D/256
+    __shared__ float Ks[32][D];
+    __shared__ float Vs[32][D];
+    const int unit = blockIdx.x, u = unit / H, h = unit % H;
+    const int c2 = threadIdx.x % D, r0 = threadIdx.x / D;
+    const int64_t j0 = offsets[u], L = offsets[u + 1] - offsets[u];
+    float acc[NR];
+#pragma unroll
+    for (int a = 0; a < NR; ++a) acc[a] = 0.f;
+    for (int64_t kb = 0; kb < L; kb += 32) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 32 * D; e += 256) {
+            const int jj = e / D, c = e % D;
+            const int64_t j = kb + jj;
+            float kv = 0.f, vv = 0.f;
+            if (j < L) {
+                const size_t idx = ((size_t)(j0 + j) * H + h) * D + c;
+                kv = act(phi1, ld<T>(k + idx));  // phi1 applied, then rows past L stay 0
+                vv = ld<T>(v + idx);
+            }
+            Ks[jj][c] = kv;
+            Vs[jj][c] = vv;
+        }
+        __syncthreads();
+        const int jn = (L - kb) < 32 ? (int)(L - kb) : 32;
+        for (int jj = 0; jj < jn; ++jj) {
+            const float vv = Vs[jj][c2];
+#pragma unroll
+            for (int a = 0; a < NR; ++a) acc[a] = fmaf(Ks[jj][r0 + a * RSTEP], vv, acc[a]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NR; ++a) zbuf[((size_t)unit * D + r0 + a * RSTEP) * D + c2] = acc[a];
+}
+
+}  // namespace
+
+// ============================================================================== launchers
+cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf) {
+    user_tiles_kernel<<<1, 1024, 0, p.stream>>>(p.offsets, p.B, uts, p.outs, p.S, p.H, p.d,
+                                                 p.attn == VISTA_SOFTMAX, zbuf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, char* ws) {
+    const int num_slots = 2 * w.num_ctas;
+    dim3 grid(num_slots, (w.rows_per_unit + 7) / 8);
+    merge_softmax_slots_kernel<<<grid, 256, 0, p.stream>>>(
+        reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots, reinterpret_cast<const float*>(ws + w.slot_o_off),
+        reinterpret_cast<const float*>(ws + w.slot_lse_off), w.rows_per_unit, p.outs, p.S, p.H, p.S / w.rows_per_unit);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_qla_slots(const Problem& p, const Workspace& w, char* ws, float* zbuf) {
+    const int num_slots = 2 * w.num_ctas;
+    dim3 grid(num_slots, 128 / 8);
+    merge_qla_slots_kernel<<<grid, 256, 0, p.stream>>>(reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots,
+                                                       reinterpret_cast<const float*>(ws + w.slot_o_off), zbuf);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t merge_parts_d(const Problem& p, int P, const float* po, const float* pl) {
+    const int64_t nrows = (int64_t)p.B * p.H * p.S;
+    if (nrows == 0) return cudaSuccess;
+    merge_softmax_parts_kernel<D><<<(unsigned)((nrows + 7) / 8), 256, 0, p.stream>>>(P, p.B, p.H, p.S, po, pl, p.outs);
+    return cudaGetLastError();
+}
+cudaError_t launch_merge_softmax_parts(const Problem& p, int P, const float* po, const float* pl) {
+    switch (p.d) {
+        case 32: return merge_parts_d<32>(p, P, po, pl);
+        case 64: return merge_parts_d<64>(p, P, po, pl);
+        case 128: return merge_parts_d<128>(p, P, po, pl);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int D, typename TQ>
+static cudaError_t finalize_d(const Problem& p, const float* zparts, int P, int64_t part_stride, const int64_t* user_len) {
+    if (p.B == 0) return cudaSuccess;
+    const size_t smem = (size_t)(D * D + D * 64) * sizeof(float);
+    static const cudaError_t attr = cudaFuncSetAttribute(qla_finalize_kernel<D, TQ>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (attr != cudaSuccess) return attr;
+    dim3 grid((p.S + 63) / 64, p.B * p.H);
+    qla_finalize_kernel<D, TQ><<<grid, 256, smem, p.stream>>>(
+        reinterpret_cast<const TQ*>(p.q), p.q_user_stride, zparts, P, part_stride, p.offsets, user_len, p.S, p.H, p.phi1,
+        p.phi2, p.normalize, p.outs);
+    return cudaGetLastError();
+}
+cudaError_t launch_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
+                                const int64_t* user_len) {
+    if (p.in_bf16) {
+        switch (p.d) {
+            case 32: return finalize_d<32, __nv_bfloat16>(p, zparts, P, part_stride, user_len);
+            case 64: return finalize_d<64, __nv_bfloat16>(p, zparts, P, part_stride, user_len);
+            case 128: return finalize_d<128, __nv_bfloat16>(p, zparts, P, part_stride, user_len);
+        }
+    } else {
+        switch (p.d) {
+            case 32: return finalize_d<32, float>(p, zparts, P, part_stride, user_len);
+            case 64: return finalize_d<64, float>(p, zparts, P, part_stride, user_len);
+            case 128: return finalize_d<128, float>(p, zparts, P, part_stride, user_len);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int D, typename T>
+static cudaError_t simt_softmax_d(const Problem& p) {
+    if (p.B == 0) return cudaSuccess;
+    dim3 grid((p.S + 7) / 8, p.B * p.H);
+    simt_softmax_kernel<D, T><<<grid, 256, 0, p.stream>>>(reinterpret_cast<const T*>(p.q), p.q_user_stride,
+                                                           reinterpret_cast<const T*>(p.k), reinterpret_cast<const T*>(p.v),
+                                                           p.offsets, p.S, p.H, p.scale * kLog2e, p.outs);
+    return cudaGetLastError();
+}
+cudaError_t launch_simt_softmax(const Problem& p) {
+    if (p.in_bf16) {
+        switch (p.d) {
+            case 32: return simt_softmax_d<32, __nv_bfloat16>(p);
+            case 64: return simt_softmax_d<64, __nv_bfloat16>(p);
+            case 128: return simt_softmax_d<128, __nv_bfloat16>(p);
+        }
+    } else {
+        switch (p.d) {
+            case 32: return simt_softmax_d<32, float>(p);
+            case 64: return simt_softmax_d<64, float>(p);
+            case 128: return simt_softmax_d<128, float>(p);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int D, typename T>
+static cudaError_t simt_qla_d(const Problem& p, float* zbuf) {
+    if (p.B == 0) return cudaSuccess;
+    simt_qla_state_kernel<D, T><<<p.B * p.H, 256, 0, p.stream>>>(reinterpret_cast<const T*>(p.k),
+                                                                  reinterpret_cast<const T*>(p.v), p.offsets, p.H, p.phi1,
+                                                                  zbuf);
+    return cudaGetLastError();
+}
+cudaError_t launch_simt_qla_state(const Problem& p, float* zbuf) {
+    if (p.in_bf16) {
+        switch (p.d) {
+            case 32: return simt_qla_d<32, __nv_bfloat16>(p, zbuf);
+            case 64: return simt_qla_d<64, __nv_bfloat16>(p, zbuf);
+            case 128: return simt_qla_d<128, __nv_bfloat16>(p, zbuf);
+        }
+    } else {
+        switch (p.d) {
+            case 32: return simt_qla_d<32, float>(p, zbuf);
+            case 64: return simt_qla_d<64, float>(p, zbuf);
+            case 128: return simt_qla_d<128, float>(p, zbuf);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace vista

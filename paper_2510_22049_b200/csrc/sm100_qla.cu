@@ -1,0 +1,252 @@
+// sm100_qla.cu -- QLA state on B200: Z_uh = sum_j phi1(k_j)^T v_j  (d x d, fp32 in TMEM).
+//
+// "phi(K[S])^T V[S]" (Sec. 3.2.2); App. B: "sum_j K[S]_j^T V[S]_j can be computed
+// first".  The state GEMM has M = d (c1), N = d (c2), K = history items, so each
+// 128-item tile is one 128x128x128 tcgen05 MMA chain with BOTH operands MN-major straight out of
+// the TMA tiles (no transpose):  A[c1][j] = phi1(K)[j][c1],  B[j][c2] = V[j][c2].
+// HBM-bound (2 d^2 = 32768 flop per 512 B of K+V), so the design goal is to keep the TMA ring
+// full: 3 x 64 KB stages, one CTA per SM, stream-K flat tile ranges (work.cuh).
+//
+//   warp 0        TMA producer (K, V tiles of 128 items x 128 channels, bf16, 128-B swizzle)
+//   warp 1        MMA issuer (one thread), Z double-buffered in TMEM (2 x 128 columns)
+//   warps 4..11   phi1 transform of the K tile in shared memory (bf16 -> f32 -> phi1 -> bf16,
+//                 rows past the user's end zeroed AFTER activation: phi1(0) != 0 for shifted ELU),
+//                 then the epilogue: Z rows (TMEM lane = c1) -> zbuf[u,h] or a split slot.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "sm100_ptx.cuh"
+#include "work.cuh"
+
+namespace vista {
+
+bool make_kv_map(CUtensorMap* map, const void* base, int64_t total_len, int H);
+
+namespace {
+
+constexpr int kHalfBytes = 128 * 128;
+constexpr int kTileBytes = 2 * kHalfBytes;
+constexpr int kStages = 3;
+constexpr int kStageBytes = 2 * kTileBytes;
+constexpr int kBarOff = kStages * kStageBytes;
+constexpr int kSmem = kBarOff + 256 + 1024;
+constexpr int kXformWarps = 8;
+constexpr int kThreads = 128 + kXformWarps * 32;
+constexpr int kTmemCols = 256;
+
+struct Bars {
+    uint64_t kv_full[kStages], k_ready[kStages], kv_empty[kStages];
+    uint64_t z_full[2], z_empty[2];
+    uint32_t tmem_base;
+};
+
+struct Params {
+    const int64_t* offsets;
+    const int64_t* uts;
+    int* slot_unit;
+    float* slot_o;
+    float* zbuf;
+    int B, H, phi1;
+};
+
+__device__ __forceinline__ float phi(int kind, float x) {
+    if (kind == VISTA_ACT_SILU) {
+        float t;
+        asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+        return x * fmaf(0.5f, t, 0.5f);  // x * sigmoid(x)
+    }
+    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? x : ptx::ex2((x - 1.f) * 1.4426950408889634f);
+    return x;
+}
+
+__device__ __forceinline__ uint32_t phi_bf16x2(int kind, uint32_t w) {
+    const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xFFFF0000u);
+    return ptx::pack_bf16x2(phi(kind, lo), phi(kind, hi));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    sm100_qla_state_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+                           const Params P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int cta = blockIdx.x, num_ctas = gridDim.x;
+    const int HG = P.H;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&bars->kv_full[s], 1);
+            ptx::mbar_init(&bars->k_ready[s], kXformWarps * 32);
+            ptx::mbar_init(&bars->kv_empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bars->z_full[b], 1);
+            ptx::mbar_init(&bars->z_empty[b], kXformWarps * 32);
+        }
+        ptx::fence_mbar_init();
+        ItemIter itr;
+        itr.init(P.uts, P.B, HG, cta, num_ctas);
+        Item it;
+        int s0 = -1, s1 = -1;
+        while (itr.next(it))
+            if (!item_complete(it)) {
+                if (it.first) s0 = it.u * HG + it.hg; else s1 = it.u * HG + it.hg;
+            }
+        P.slot_unit[2 * cta] = s0;
+        P.slot_unit[2 * cta + 1] = s1;
+    }
+    if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+
+    ItemIter iter;
+    iter.init(P.uts, P.B, HG, cta, num_ctas);
+    Item it;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            ptx::tma_prefetch(&mapK);
+            ptx::tma_prefetch(&mapV);
+            const uint64_t pol = ptx::policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            while (iter.next(it)) {
+                const int h = it.hg;
+                const int64_t row0 = P.offsets[it.u];
+                for (int t = it.t0; t < it.t1; ++t) {
+                    ptx::mbar_wait(&bars->kv_empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&bars->kv_full[stage], kStageBytes);
+                    uint8_t* sk = smem + stage * kStageBytes;
+                    const int32_t row = (int32_t)(row0 + (int64_t)t * kTile);
+                    for (int half = 0; half < 2; ++half) {
+                        ptx::tma_load_3d(sk + half * kHalfBytes, &mapK, &bars->kv_full[stage], half * 64, h, row, pol);
+                        ptx::tma_load_3d(sk + kTileBytes + half * kHalfBytes, &mapV, &bars->kv_full[stage], half * 64,
+                                         h, row, pol);
+                    }
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idZ = ptx::idesc_bf16_f32(128, 128, 1, 1);  // A, B both MN-major
+            const uint32_t base = ptx::smem_u32(smem);
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t zuse[2] = {0, 0};
+            int k = 0;
+            while (iter.next(it)) {
+                const int zb = k & 1;
+                ptx::mbar_wait(&bars->z_empty[zb], (zuse[zb] & 1) ^ 1);
+                ++zuse[zb];
+                const uint32_t dz = tmem + zb * 128;
+                for (int t = it.t0; t < it.t1; ++t) {
+                    ptx::mbar_wait(&bars->k_ready[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t ka = base + stage * kStageBytes, va = ka + kTileBytes;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        ptx::mma_ss(dz, ptx::sdesc_sw128(ka + kk * 2048, kHalfBytes, 1024),
+                                    ptx::sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), idZ,
+                                    (t > it.t0 || kk > 0) ? 1u : 0u);
+                    ptx::mma_commit(&bars->kv_empty[stage]);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit(&bars->z_full[zb]);
+                ++k;
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        const int xt = threadIdx.x - 128;  // 0 .. 255
+        const int wq = warp % 4;
+        const int chalf = (warp - 4) / 4;  // epilogue: columns [64*chalf, 64*chalf + 64)
+        const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
+        const int phi1 = P.phi1;
+        int stage = 0;
+        uint32_t phase = 0;
+        uint32_t zphase[2] = {0, 0};
+        int k = 0;
+        while (iter.next(it)) {
+            const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->kv_full[stage], phase);
+                const int64_t valid = L - (int64_t)t * kTile;
+                uint4* sk = reinterpret_cast<uint4*>(smem + stage * kStageBytes);
+                if (phi1 != VISTA_ACT_IDENTITY || valid < kTile) {
+#pragma unroll 4
+                    for (int c = xt; c < kTileBytes / 16; c += kXformWarps * 32) {
+                        const int j = (c & 1023) >> 3;  // 128-B line = history row within the tile
+                        uint4 x = sk[c];
+                        if (j >= valid) {
+                            x = make_uint4(0, 0, 0, 0);
+                        } else if (phi1 != VISTA_ACT_IDENTITY) {
+                            x.x = phi_bf16x2(phi1, x.x);
+                            x.y = phi_bf16x2(phi1, x.y);
+                            x.z = phi_bf16x2(phi1, x.z);
+                            x.w = phi_bf16x2(phi1, x.w);
+                        }
+                        sk[c] = x;
+                    }
+                    ptx::fence_proxy_async_smem();
+                }
+                ptx::mbar_arrive(&bars->k_ready[stage]);
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
+            }
+            // epilogue
+            const int zb = k & 1;
+            ptx::mbar_wait(&bars->z_full[zb], zphase[zb]);
+            zphase[zb] ^= 1;
+            ptx::tc_fence_after();
+            const int c1 = wq * 32 + lane;
+            float* dst;
+            if (item_complete(it)) dst = P.zbuf + ((size_t)(it.u * HG + it.hg) * 128 + c1) * 128;
+            else dst = P.slot_o + ((size_t)item_slot(it, cta) * 128 + c1) * 128;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t r[32];
+                ptx::tmem_ld32_sync(tmem + lane_bits + zb * 128 + chalf * 64 + c * 32, r);
+                float4* d4 = reinterpret_cast<float4*>(dst + chalf * 64 + c * 32);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&bars->z_empty[zb]);
+            ++k;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc(tmem, kTmemCols);
+}
+
+}  // namespace
+
+cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf) {
+    CUtensorMap mk, mv;
+    if (!make_kv_map(&mk, p.k, p.total_len, p.H) || !make_kv_map(&mv, p.v, p.total_len, p.H))
+        return cudaErrorInvalidValue;
+    Params P;
+    P.offsets = p.offsets;
+    P.uts = reinterpret_cast<const int64_t*>(ws + w.uts_off);
+    P.slot_unit = reinterpret_cast<int*>(ws + w.slot_unit_off);
+    P.slot_o = reinterpret_cast<float*>(ws + w.slot_o_off);
+    P.zbuf = zbuf;
+    P.B = p.B;
+    P.H = p.H;
+    P.phi1 = p.phi1;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(sm100_qla_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (attr != cudaSuccess) return attr;
+    sm100_qla_state_kernel<<<w.num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P);
+    return cudaGetLastError();
+}
+
+}  // namespace vista

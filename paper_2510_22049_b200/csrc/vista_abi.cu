@@ -1,0 +1,268 @@
+// vista_abi.cu -- the C ABI of libvista (include/vista.h): validation, workspace planning,
+// dispatch by shape, launch sequencing.  All device work is enqueued on the caller's stream;
+// nothing here synchronizes (except the debug entry vista_check_offsets).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+using namespace vista;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+
+vista_status_t cuda_fail(cudaError_t e) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return VISTA_ERR_CUDA;
+}
+
+int device_sms() {
+    static std::mutex mu;
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!cache[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+vista_status_t validate_desc(const vista_desc_t* d) {
+    if (!d) return VISTA_ERR_NULL;
+    if (d->abi_version != VISTA_ABI_VERSION) return VISTA_ERR_INVALID;
+    if (d->num_users < 0 || d->num_summary < 1 || d->num_heads < 1) return VISTA_ERR_INVALID;
+    if (d->in_dtype != VISTA_F32 && d->in_dtype != VISTA_BF16) return VISTA_ERR_INVALID;
+    if (d->out_dtype != VISTA_F32 && d->out_dtype != VISTA_BF16) return VISTA_ERR_INVALID;
+    if (d->attn != VISTA_SOFTMAX && d->attn != VISTA_QLA) return VISTA_ERR_INVALID;
+    if (d->head_dim != 32 && d->head_dim != 64 && d->head_dim != 128) return VISTA_ERR_UNSUPPORTED;
+    if (d->attn == VISTA_SOFTMAX && !isnan(d->softmax_scale) && !(d->softmax_scale > 0.f && isfinite(d->softmax_scale)))
+        return VISTA_ERR_INVALID;
+    if (d->attn == VISTA_QLA) {
+        for (int phi : {d->qla_phi1, d->qla_phi2})
+            if (phi < VISTA_ACT_IDENTITY || phi > VISTA_ACT_SHIFTED_ELU) return VISTA_ERR_INVALID;
+        if (d->qla_normalize != 0 && d->qla_normalize != 1) return VISTA_ERR_INVALID;
+    }
+    if (d->q_user_stride < 0) return VISTA_ERR_INVALID;
+    if (d->q_user_stride > 0 && d->q_user_stride < (int64_t)d->num_summary * d->num_heads * d->head_dim)
+        return VISTA_ERR_INVALID;
+    return VISTA_OK;
+}
+
+Problem make_problem(const vista_desc_t* d, int64_t total_len) {
+    Problem p{};
+    p.B = d->num_users;
+    p.S = d->num_summary;
+    p.H = d->num_heads;
+    p.d = d->head_dim;
+    p.in_bf16 = d->in_dtype == VISTA_BF16;
+    p.attn = d->attn;
+    p.scale = isnan(d->softmax_scale) ? 1.0f / sqrtf((float)d->head_dim) : d->softmax_scale;
+    p.phi1 = d->qla_phi1;
+    p.phi2 = d->qla_phi2;
+    p.normalize = d->qla_normalize;
+    p.q_user_stride = d->q_user_stride;
+    p.total_len = total_len;
+    p.num_sms = device_sms();
+    return p;
+}
+
+}  // namespace
+
+namespace vista {
+
+Path choose_path(const Problem& p) {
+    const bool tma_ok = p.in_bf16 && p.d == 128 && p.total_len < (int64_t(1) << 31) && (p.q_user_stride % 8) == 0;
+    if (p.attn == VISTA_SOFTMAX) return (tma_ok && p.S % 128 == 0) ? PATH_SM100_SOFTMAX : PATH_SIMT_SOFTMAX;
+    return tma_ok ? PATH_SM100_QLA : PATH_SIMT_QLA;
+}
+
+int sm100_softmax_nq(int S);
+
+Workspace plan_workspace(const Problem& p, bool partial) {
+    (void)partial;
+    Workspace w{};
+    const Path path = choose_path(p);
+    size_t off = 0;
+    w.num_ctas = 0;
+    w.rows_per_unit = 0;
+    if (path == PATH_SM100_SOFTMAX || path == PATH_SM100_QLA) {
+        w.num_ctas = p.num_sms;
+        w.rows_per_unit = path == PATH_SM100_SOFTMAX ? sm100_softmax_nq(p.S) * 128 : 128;
+    }
+    w.uts_off = off;
+    off = align256(off + (size_t)(p.B + 1) * sizeof(int64_t));
+    w.slot_unit_off = off;
+    off = align256(off + (size_t)2 * w.num_ctas * sizeof(int));
+    w.slot_o_off = off;
+    off = align256(off + (size_t)2 * w.num_ctas * w.rows_per_unit * 128 * sizeof(float));
+    w.slot_lse_off = off;
+    off = align256(off + (size_t)2 * w.num_ctas * w.rows_per_unit * sizeof(float));
+    w.zbuf_off = off;
+    if (p.attn == VISTA_QLA) off = align256(off + (size_t)p.B * p.H * p.d * p.d * sizeof(float));
+    w.total = off;
+    return w;
+}
+
+}  // namespace vista
+
+extern "C" {
+
+int vista_abi_version(void) { return VISTA_ABI_VERSION; }
+
+const char* vista_status_string(int s) {
+    switch (s) {
+        case VISTA_OK: return "VISTA_OK";
+        case VISTA_ERR_NULL: return "VISTA_ERR_NULL";
+        case VISTA_ERR_INVALID: return "VISTA_ERR_INVALID";
+        case VISTA_ERR_UNSUPPORTED: return "VISTA_ERR_UNSUPPORTED";
+        case VISTA_ERR_MISALIGNED: return "VISTA_ERR_MISALIGNED";
+        case VISTA_ERR_WORKSPACE: return "VISTA_ERR_WORKSPACE";
+        case VISTA_ERR_CUDA: return "VISTA_ERR_CUDA";
+        case VISTA_ERR_OFFSETS: return "VISTA_ERR_OFFSETS";
+    }
+    return "VISTA_ERR_UNKNOWN";
+}
+
+const char* vista_last_cuda_error(void) { return g_cuda_err; }
+
+const char* vista_dispatch_name(const vista_desc_t* desc) {
+    if (validate_desc(desc) != VISTA_OK) return nullptr;
+    Problem p = make_problem(desc, 0);
+    switch (choose_path(p)) {
+        case PATH_SM100_SOFTMAX: return "sm100_softmax";
+        case PATH_SM100_QLA: return "sm100_qla";
+        case PATH_SIMT_SOFTMAX: return "simt_softmax";
+        case PATH_SIMT_QLA: return "simt_qla";
+        default: return nullptr;
+    }
+}
+
+vista_status_t vista_summarize_workspace_size(const vista_desc_t* desc, int64_t total_len, size_t* bytes) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (!bytes) return VISTA_ERR_NULL;
+    if (total_len < 0) return VISTA_ERR_INVALID;
+    Problem p = make_problem(desc, total_len);
+    *bytes = plan_workspace(p, false).total;
+    return VISTA_OK;
+}
+
+static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                          const int64_t* offsets, int64_t total_len, OutSpec outs, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (total_len < 0) return VISTA_ERR_INVALID;
+    if (!q || !offsets || !outs.out) return VISTA_ERR_NULL;
+    if (total_len > 0 && (!k || !v)) return VISTA_ERR_NULL;
+    if (outs.mode == OUT_PARTIAL && desc->attn == VISTA_SOFTMAX && !outs.lse) return VISTA_ERR_NULL;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(outs.out)) return VISTA_ERR_MISALIGNED;
+    if (outs.lse && (reinterpret_cast<uintptr_t>(outs.lse) & 3)) return VISTA_ERR_MISALIGNED;
+    Problem p = make_problem(desc, total_len);
+    p.q = q;
+    p.k = k;
+    p.v = v;
+    p.offsets = offsets;
+    p.outs = outs;
+    p.stream = reinterpret_cast<cudaStream_t>(stream);
+    if (p.B == 0) return VISTA_OK;
+    const bool partial = outs.mode == OUT_PARTIAL;
+    const Workspace w = plan_workspace(p, partial);
+    if (w.total > 0 && (!workspace || workspace_bytes < w.total)) return VISTA_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
+    char* ws = reinterpret_cast<char*>(workspace);
+    cudaError_t e = cudaSuccess;
+    switch (choose_path(p)) {
+        case PATH_SM100_SOFTMAX: {
+            if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), nullptr)) != cudaSuccess) break;
+            if ((e = launch_sm100_softmax(p, w, ws)) != cudaSuccess) break;
+            e = launch_merge_softmax_slots(p, w, ws);
+            break;
+        }
+        case PATH_SM100_QLA: {
+            float* zbuf = partial ? reinterpret_cast<float*>(outs.out) : reinterpret_cast<float*>(ws + w.zbuf_off);
+            if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), zbuf)) != cudaSuccess) break;
+            if ((e = launch_sm100_qla_state(p, w, ws, zbuf)) != cudaSuccess) break;
+            if ((e = launch_merge_qla_slots(p, w, ws, zbuf)) != cudaSuccess) break;
+            if (!partial) e = launch_qla_finalize(p, zbuf, 1, 0, nullptr);
+            break;
+        }
+        case PATH_SIMT_SOFTMAX: e = launch_simt_softmax(p); break;
+        case PATH_SIMT_QLA: {
+            float* zbuf = partial ? reinterpret_cast<float*>(outs.out) : reinterpret_cast<float*>(ws + w.zbuf_off);
+            if ((e = launch_simt_qla_state(p, zbuf)) != cudaSuccess) break;
+            if (!partial) e = launch_qla_finalize(p, zbuf, 1, 0, nullptr);
+            break;
+        }
+        default: return VISTA_ERR_UNSUPPORTED;
+    }
+    return e == cudaSuccess ? VISTA_OK : cuda_fail(e);
+}
+
+vista_status_t vista_summarize_fwd(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                   const int64_t* offsets, int64_t total_len, void* out, float* lse, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+    if (!desc) return VISTA_ERR_NULL;
+    OutSpec o{OUT_FINAL, desc->out_dtype == VISTA_BF16, out, desc->attn == VISTA_SOFTMAX ? lse : nullptr};
+    return run(desc, q, k, v, offsets, total_len, o, workspace, workspace_bytes, stream);
+}
+
+vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                       const int64_t* offsets, int64_t total_len, float* part_o, float* part_lse,
+                                       void* workspace, size_t workspace_bytes, void* stream) {
+    if (!desc) return VISTA_ERR_NULL;
+    OutSpec o{OUT_PARTIAL, 0, part_o, desc->attn == VISTA_SOFTMAX ? part_lse : nullptr};
+    return run(desc, q, k, v, offsets, total_len, o, workspace, workspace_bytes, stream);
+}
+
+vista_status_t vista_summarize_merge(const vista_desc_t* desc, int32_t num_parts, const float* part_o,
+                                     const float* part_lse, const void* q, const int64_t* user_len, void* out,
+                                     float* lse, void* stream) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (num_parts < 1) return VISTA_ERR_INVALID;
+    if (!part_o || !out) return VISTA_ERR_NULL;
+    if (desc->attn == VISTA_SOFTMAX && !part_lse) return VISTA_ERR_NULL;
+    if (desc->attn == VISTA_QLA && (!q || !user_len)) return VISTA_ERR_NULL;
+    if (!aligned16(part_o) || !aligned16(out) || (q && !aligned16(q))) return VISTA_ERR_MISALIGNED;
+    Problem p = make_problem(desc, 0);
+    p.q = q;
+    p.outs = OutSpec{OUT_FINAL, desc->out_dtype == VISTA_BF16, out, desc->attn == VISTA_SOFTMAX ? lse : nullptr};
+    p.stream = reinterpret_cast<cudaStream_t>(stream);
+    if (p.B == 0) return VISTA_OK;
+    cudaError_t e;
+    if (desc->attn == VISTA_SOFTMAX) {
+        e = launch_merge_softmax_parts(p, num_parts, part_o, part_lse);
+    } else {
+        e = launch_qla_finalize(p, part_o, num_parts, (int64_t)p.B * p.H * p.d * p.d, user_len);
+    }
+    return e == cudaSuccess ? VISTA_OK : cuda_fail(e);
+}
+
+vista_status_t vista_check_offsets(const int64_t* offsets, int32_t num_users, int64_t total_len, void* stream) {
+    if (!offsets) return VISTA_ERR_NULL;
+    if (num_users < 0) return VISTA_ERR_INVALID;
+    std::vector<int64_t> h((size_t)num_users + 1);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(h.data(), offsets, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (h[0] != 0 || h[num_users] != total_len) return VISTA_ERR_OFFSETS;
+    for (int32_t u = 0; u < num_users; ++u)
+        if (h[u + 1] < h[u]) return VISTA_ERR_OFFSETS;
+    return VISTA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,236 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on the same seeded
+inputs.  Gate (reading R14): per (user, head) block
+    max|gpu - oracle| / max|oracle| <= 2e-2 (bf16 inputs) or 1e-4 (f32 inputs)
+and |lse_gpu - lse_oracle| <= 1e-3 (bf16) / 1e-5 (f32), natural log.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16": (2e-2, 1e-3), "f32": (1e-4, 1e-5)}
+
+
+def to_dev(x, dtype):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(torch.bfloat16) if dtype == "bf16" else t.float()
+
+
+def block_err(g, o):
+    den = np.abs(o).max()
+    return np.abs(g - o).max() / den if den > 0 else np.abs(g).max()
+
+
+def check_softmax(out, lse, ref, ref_lse, lens, dtype, rows=None):
+    tol, ltol = TOL[dtype]
+    g = out.float().cpu().numpy().astype(np.float64)
+    gl = lse.cpu().numpy().astype(np.float64)
+    if rows is not None:
+        g = g[:, rows]
+        gl = gl[:, :, rows]
+    B, _, H, _ = ref.shape
+    worst = 0.0
+    for u in range(B):
+        for h in range(H):
+            if lens[u] == 0:
+                assert np.all(g[u, :, h] == 0) and np.all(gl[u, h] == -np.inf)
+                continue
+            e = block_err(g[u, :, h], ref[u, :, h])
+            worst = max(worst, e)
+            assert e <= tol, f"user {u} head {h}: rel err {e:.3g} > {tol}"
+            le = np.abs(gl[u, h] - ref_lse[u, h]).max()
+            assert le <= ltol, f"user {u} head {h}: lse err {le:.3g}"
+    return worst
+
+
+def run_case(vista, lens, S, H, d, dtype="bf16", tau=1, category=False, seed=0, attn=None, **kw):
+    q, k, v, off = synth.make_batch(lens, S, H, d, dtype=dtype, seed=seed, tau=tau, category=category)
+    qt, kt, vt = to_dev(q, dtype), to_dev(k, dtype), to_dev(v, dtype)
+    ot = torch.from_numpy(off).cuda()
+    res = vista.summarize(qt, kt, vt, ot, int(off[-1]), attn=vista.SOFTMAX if attn is None else attn,
+                          out_dtype=vista.F32, **kw)
+    torch.cuda.synchronize()
+    return (q, k, v, off), res
+
+
+EDGE_LENS = [0, 1, 127, 128, 129, 300, 1000, 0, 2049, 5]
+
+
+@pytest.mark.parametrize("S", [128, 256, 384, 512])
+def test_softmax_tcgen05_jagged_edges(cuda_lib, S):
+    vista = cuda_lib
+    assert vista.vista_dispatch_name(vista.make_desc(1, S, 2, 128)) == "sm100_softmax"
+    (q, k, v, off), (out, lse) = run_case(vista, EDGE_LENS, S, 2, 128, tau=2, seed=S)
+    ref, ref_lse = oracle.softmax_summarize(q, k, v, off)
+    check_softmax(out, lse, ref, ref_lse, EDGE_LENS, "bf16")
+
+
+@pytest.mark.parametrize("tau,category", [(4, False), (1, True), (4, True)])
+def test_softmax_tcgen05_peaky_and_category(cuda_lib, tau, category):
+    lens = [10_000, 3000, 129]
+    (q, k, v, off), (out, lse) = run_case(cuda_lib, lens, 256, 1, 128, tau=tau, category=category, seed=7)
+    ref, ref_lse = oracle.softmax_summarize(q, k, v, off)
+    check_softmax(out, lse, ref, ref_lse, lens, "bf16")
+
+
+def test_softmax_many_users_split_across_ctas(cuda_lib):
+    """More users than SMs with power-law lengths: exercises stream-K splits and the slot merge."""
+    rng = np.random.default_rng(3)
+    lens = np.minimum((1.0 / (1e-3 - rng.random(300) * (1e-3 - 1e-5))).astype(np.int64), 40_000)
+    lens[::37] = 0
+    S, H = 256, 1
+    (q, k, v, off), (out, lse) = run_case(cuda_lib, lens, S, H, 128, seed=11)
+    rows = np.array([0, 77, 128, 255])
+    ref, ref_lse = oracle.softmax_summarize(q, k, v, off, rows=rows)
+    check_softmax(out, lse, ref, ref_lse, lens, "bf16", rows=rows)
+
+
+def test_softmax_c1_fp32_simt(cuda_lib):
+    vista = cuda_lib
+    cfg = synth.CONFIGS["c1"]
+    lens = synth.user_lengths("c1")
+    assert vista.vista_dispatch_name(vista.make_desc(1, 16, 1, 32, in_dtype=vista.F32)) == "simt_softmax"
+    (q, k, v, off), (out, lse) = run_case(vista, lens, cfg["S"], cfg["H"], cfg["d"], dtype="f32", seed=0)
+    ref, ref_lse = oracle.softmax_summarize(q, k, v, off)
+    check_softmax(out, lse, ref, ref_lse, lens, "f32")
+
+
+@pytest.mark.parametrize("d,dtype,S", [(64, "bf16", 256), (128, "bf16", 100), (32, "f32", 33), (128, "f32", 64)])
+def test_softmax_simt_shapes(cuda_lib, d, dtype, S):
+    lens = [0, 1, 33, 500]
+    (q, k, v, off), (out, lse) = run_case(cuda_lib, lens, S, 2, d, dtype=dtype, tau=2, seed=d + S)
+    ref, ref_lse = oracle.softmax_summarize(q, k, v, off)
+    check_softmax(out, lse, ref, ref_lse, lens, dtype)
+
+
+def test_softmax_c2_full_size_sampled_rows(cuda_lib):
+    """BASELINE config 2 at full size (64 users x 10k items, S=256, H=4) in the bench's launch
+    configuration; sampled rows of sampled users checked one by one against the oracle."""
+    vista = cuda_lib
+    cfg = synth.CONFIGS["c2"]
+    lens = synth.user_lengths("c2")
+    S, H, d = cfg["S"], cfg["H"], cfg["d"]
+    q, K, V, off = synth.make_batch(lens, S, H, d, backend="torch", device="cuda")
+    ot = torch.from_numpy(off).cuda()
+    out, lse = vista.summarize(q, K, V, ot, int(off[-1]), out_dtype=vista.BF16)
+    torch.cuda.synchronize()
+    users = [0, 31, 63]
+    rows = np.array([0, 1, 127, 128, 200, 255])
+    qn = q.float().cpu().numpy()
+    for u in users:
+        a, b = int(off[u]), int(off[u + 1])
+        kn = K[a:b].float().cpu().numpy()
+        vn = V[a:b].float().cpu().numpy()
+        ref, ref_lse = oracle.softmax_summarize(qn, kn, vn, [0, b - a], rows=rows)
+        check_softmax(out[u:u + 1], lse[u:u + 1], ref, ref_lse, [b - a], "bf16", rows=rows)
+
+
+@pytest.mark.parametrize("phi1,phi2,normalize", [("silu", "silu", True), ("shifted_elu", "identity", False),
+                                                 ("identity", "identity", True), ("shifted_elu", "shifted_elu", True),
+                                                 ("silu", "identity", False)])
+def test_qla_tcgen05(cuda_lib, phi1, phi2, normalize):
+    vista = cuda_lib
+    assert vista.vista_dispatch_name(vista.make_desc(1, 256, 2, 128, attn=vista.QLA)) == "sm100_qla"
+    lens = EDGE_LENS
+    (q, k, v, off), (out, _) = run_case(vista, lens, 256, 2, 128, seed=5, attn=vista.QLA, phi1=phi1, phi2=phi2,
+                                        normalize=normalize)
+    ref = oracle.qla_summarize(q, k, v, off, phi1, phi2, normalize)
+    g = out.cpu().numpy()
+    for u in range(len(lens)):
+        for h in range(2):
+            e = block_err(g[u, :, h], ref[u, :, h])
+            assert e <= 2e-2, f"user {u} head {h} ({phi1},{phi2},{normalize}): {e:.3g}"
+
+
+@pytest.mark.parametrize("phi1,phi2", [("silu", "silu"), ("shifted_elu", "identity")])
+def test_qla_simt_fp32(cuda_lib, phi1, phi2):
+    vista = cuda_lib
+    lens = [1024, 0, 7]
+    (q, k, v, off), (out, _) = run_case(vista, lens, 16, 1, 32, dtype="f32", seed=2, attn=vista.QLA, phi1=phi1,
+                                        phi2=phi2)
+    ref = oracle.qla_summarize(q, k, v, off, phi1, phi2, True)
+    g = out.cpu().numpy()
+    for u in range(3):
+        assert block_err(g[u, :, 0], ref[u, :, 0]) <= 1e-4
+
+
+def test_qla_state_split_across_ctas(cuda_lib):
+    vista = cuda_lib
+    lens = [200_000, 128, 70_001]
+    (q, k, v, off), (out, _) = run_case(vista, lens, 256, 1, 128, seed=9, attn=vista.QLA)
+    ref = oracle.qla_summarize(q, k, v, off, "silu", "silu", True)
+    g = out.cpu().numpy()
+    for u in range(3):
+        assert block_err(g[u, :, 0], ref[u, :, 0]) <= 2e-2
+
+
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_partial_merge_equals_oracle(cuda_lib, attn):
+    """History-length shards (the multi-GPU split-L path, run here shard by shard on one GPU):
+    partial on each shard, stack, merge -> oracle of the unsplit history."""
+    vista = cuda_lib
+    a = vista.SOFTMAX if attn == "softmax" else vista.QLA
+    lens = np.array([3000, 0, 129, 1001])
+    S, H, d = 256, 2, 128
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=21, tau=2)
+    P = 3
+    parts_o, parts_l = [], []
+    qt = to_dev(q, "bf16")
+    for p in range(P):
+        # shard p = p-th contiguous third of every user's history
+        sl = [(int(off[u] + lens[u] * p // P), int(off[u] + lens[u] * (p + 1) // P)) for u in range(len(lens))]
+        ks = np.concatenate([k[x:y] for x, y in sl]) if sum(y - x for x, y in sl) else np.zeros((0, H, d), np.float32)
+        vs = np.concatenate([v[x:y] for x, y in sl]) if sum(y - x for x, y in sl) else np.zeros((0, H, d), np.float32)
+        soff = synth.offsets_from_lengths([y - x for x, y in sl])
+        po, pl = vista.summarize_partial(qt, to_dev(ks, "bf16"), to_dev(vs, "bf16"), torch.from_numpy(soff).cuda(),
+                                         int(soff[-1]), attn=a)
+        parts_o.append(po)
+        parts_l.append(pl)
+    po = torch.stack(parts_o)
+    pl = torch.stack(parts_l) if a == vista.SOFTMAX else None
+    ulen = torch.from_numpy(lens).cuda()
+    out, lse = vista.summarize_merge(po, pl, q=qt, attn=a, user_len=ulen, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    if a == vista.SOFTMAX:
+        ref, ref_lse = oracle.softmax_summarize(q, k, v, off)
+        check_softmax(out, lse, ref, ref_lse, lens, "bf16")
+    else:
+        ref = oracle.qla_summarize(q, k, v, off)
+        g = out.cpu().numpy()
+        for u in range(len(lens)):
+            for h in range(H):
+                assert block_err(g[u, :, h], ref[u, :, h]) <= 2e-2
+
+
+def test_determinism_and_invariants(cuda_lib):
+    vista = cuda_lib
+    lens = [5000, 777, 0, 12_000]
+    q, k, v, off = synth.make_batch(lens, 256, 2, 128, seed=31)
+    qt, kt, vt = to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16")
+    ot = torch.from_numpy(off).cuda()
+    o1, l1 = vista.summarize(qt, kt, vt, ot, int(off[-1]), out_dtype=vista.F32)
+    o2, l2 = vista.summarize(qt, kt, vt, ot, int(off[-1]), out_dtype=vista.F32)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)          # bitwise deterministic
+    # item permutation within each user (no positional term): same result within tolerance
+    perm = np.concatenate([off[u] + np.random.default_rng(u).permutation(lens[u]) for u in range(len(lens))])
+    o3, l3 = vista.summarize(qt, kt[perm], vt[perm], ot, int(off[-1]), out_dtype=vista.F32)
+    # constant V -> output equals that constant
+    vc = torch.zeros_like(vt) + vt[:1]
+    o4, _ = vista.summarize(qt, kt, vc, ot, int(off[-1]), out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    for u in (0, 1, 3):
+        assert block_err(o3[u].cpu().numpy(), o1[u].cpu().numpy()) <= 2e-2
+        assert (l3[u] - l1[u]).abs().max().item() <= 1e-3
+        np.testing.assert_allclose(o4[u].cpu().numpy(), np.broadcast_to(vc[0].float().cpu().numpy(), o4[u].shape),
+                                   rtol=2e-2, atol=2e-2)
+
+
+def test_gpu_generator_matches_numpy(cuda_lib):
+    q, k, v, off = synth.make_batch([100, 0, 300], 8, 2, 128, seed=4, category=True)
+    qt, kt, vt, _ = synth.make_batch([100, 0, 300], 8, 2, 128, seed=4, category=True, backend="torch", device="cuda")
+    assert np.array_equal(k, kt.float().cpu().numpy()) and np.array_equal(v, vt.float().cpu().numpy())
+    assert np.array_equal(q, qt.float().cpu().numpy())

@@ -157,6 +157,21 @@ vista_status_t vista_check_offsets(const int64_t* offsets, int32_t num_users, in
  */
 const char* vista_dispatch_name(const vista_desc_t* desc);
 
+/*
+ * Measurement hooks (used by bench.py; not needed for correctness).
+ *
+ * vista_time_next_main_kernel: arms a one-shot, per-thread hook: the next summarize call
+ * (fwd or partial) made by this thread records `start_event` immediately before launching its
+ * dominant kernel (the TMA/tcgen05 kernel, or the SIMT kernel) and `stop_event` immediately
+ * after, both on that call's stream.  Arguments are cudaEvent_t handles owned by the caller;
+ * passing NULL, NULL disarms.  Returns VISTA_OK.
+ *
+ * vista_launch_counter: total number of kernels this library has launched in this process
+ * (monotonic, all threads).
+ */
+vista_status_t vista_time_next_main_kernel(void* start_event, void* stop_event);
+uint64_t vista_launch_counter(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,12 +48,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 // Wait until the phase with the given parity has completed.  A protocol bug would otherwise
-// hang the GPU: after ~2^26 suspended polls (far beyond any legitimate wait) trap instead.
+// hang the GPU: after 4 s of waiting (far beyond any legitimate wait) trap instead.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t n = 0;
+    if (mbar_try_wait(bar, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
     while (!mbar_try_wait(bar, parity)) {
-        if (++n == (1u << 26)) __trap();
+        if (globaltimer_ns() - t0 > 4000000000ull) __trap();
     }
 }
 

@@ -163,8 +163,9 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     Item it;
 
     if (warp < 4) {
-        // register split (65536 = 128 x 96 + 256 x 208): the softmax rows hold 128 fp32 scores
-        if constexpr (NQ == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+        // register split: the launch grants 168 x 384 = 64512 registers; 128 x 88 + 256 x 208 = 64512
+        // (setmaxnreg.inc blocks forever if the pool cannot cover it).  Softmax rows hold 128 fp32 scores.
+        if constexpr (NQ == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     if (warp == 0) {
         // ============================ TMA producer ============================
         if (lane == 0) {

@@ -6,6 +6,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -16,6 +17,20 @@ using namespace vista;
 namespace {
 
 thread_local char g_cuda_err[256] = "";
+thread_local cudaEvent_t g_ev_start = nullptr, g_ev_stop = nullptr;
+std::atomic<unsigned long long> g_launches{0};
+
+// Launch the dominant kernel of a call, bracketed by the armed timing events if any.
+template <typename F>
+cudaError_t timed_main(cudaStream_t s, F&& launch) {
+    cudaEvent_t a = g_ev_start, b = g_ev_stop;
+    g_ev_start = g_ev_stop = nullptr;
+    cudaError_t e;
+    if (a && (e = cudaEventRecord(a, s)) != cudaSuccess) return e;
+    e = launch();
+    if (e == cudaSuccess && b) e = cudaEventRecord(b, s);
+    return e;
+}
 
 vista_status_t cuda_fail(cudaError_t e) {
     snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
@@ -184,31 +199,40 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
     if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
     char* ws = reinterpret_cast<char*>(workspace);
     cudaError_t e = cudaSuccess;
+    int nlaunch = 0;
     switch (choose_path(p)) {
         case PATH_SM100_SOFTMAX: {
             if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), nullptr)) != cudaSuccess) break;
-            if ((e = launch_sm100_softmax(p, w, ws)) != cudaSuccess) break;
+            if ((e = timed_main(p.stream, [&] { return launch_sm100_softmax(p, w, ws); })) != cudaSuccess) break;
             e = launch_merge_softmax_slots(p, w, ws);
+            nlaunch = 3;
             break;
         }
         case PATH_SM100_QLA: {
             float* zbuf = partial ? reinterpret_cast<float*>(outs.out) : reinterpret_cast<float*>(ws + w.zbuf_off);
             if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), zbuf)) != cudaSuccess) break;
-            if ((e = launch_sm100_qla_state(p, w, ws, zbuf)) != cudaSuccess) break;
+            if ((e = timed_main(p.stream, [&] { return launch_sm100_qla_state(p, w, ws, zbuf); })) != cudaSuccess) break;
             if ((e = launch_merge_qla_slots(p, w, ws, zbuf)) != cudaSuccess) break;
             if (!partial) e = launch_qla_finalize(p, zbuf, 1, 0, nullptr);
+            nlaunch = partial ? 3 : 4;
             break;
         }
-        case PATH_SIMT_SOFTMAX: e = launch_simt_softmax(p); break;
+        case PATH_SIMT_SOFTMAX:
+            e = timed_main(p.stream, [&] { return launch_simt_softmax(p); });
+            nlaunch = 1;
+            break;
         case PATH_SIMT_QLA: {
             float* zbuf = partial ? reinterpret_cast<float*>(outs.out) : reinterpret_cast<float*>(ws + w.zbuf_off);
-            if ((e = launch_simt_qla_state(p, zbuf)) != cudaSuccess) break;
+            if ((e = timed_main(p.stream, [&] { return launch_simt_qla_state(p, zbuf); })) != cudaSuccess) break;
             if (!partial) e = launch_qla_finalize(p, zbuf, 1, 0, nullptr);
+            nlaunch = partial ? 1 : 2;
             break;
         }
         default: return VISTA_ERR_UNSUPPORTED;
     }
-    return e == cudaSuccess ? VISTA_OK : cuda_fail(e);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches += (unsigned long long)nlaunch;
+    return VISTA_OK;
 }
 
 vista_status_t vista_summarize_fwd(const vista_desc_t* desc, const void* q, const void* k, const void* v,
@@ -248,8 +272,18 @@ vista_status_t vista_summarize_merge(const vista_desc_t* desc, int32_t num_parts
     } else {
         e = launch_qla_finalize(p, part_o, num_parts, (int64_t)p.B * p.H * p.d * p.d, user_len);
     }
-    return e == cudaSuccess ? VISTA_OK : cuda_fail(e);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches += 1;
+    return VISTA_OK;
 }
+
+vista_status_t vista_time_next_main_kernel(void* start_event, void* stop_event) {
+    g_ev_start = reinterpret_cast<cudaEvent_t>(start_event);
+    g_ev_stop = reinterpret_cast<cudaEvent_t>(stop_event);
+    return VISTA_OK;
+}
+
+uint64_t vista_launch_counter(void) { return g_launches.load(); }
 
 vista_status_t vista_check_offsets(const int64_t* offsets, int32_t num_users, int64_t total_len, void* stream) {
     if (!offsets) return VISTA_ERR_NULL;

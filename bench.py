@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""bench.py -- VISTA stage-1 user-history summarization throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--attn softmax|qla]
+                    [--impl own|reference]
+
+A step = one pass of the whole hot path (vista_summarize_fwd: tile scan, TMA/tcgen05 summarize
+kernel, split-L merge) over one batch of synthetic histories already resident in HBM.  Default
+workload = BASELINE.json configs[1] (c2: 64 users x 10,000 items, S=256, d=128, H=4, bf16).
+Multi-GPU (torchrun, one process per GPU): every rank summarizes its own batch of users (by-user
+sharding, weak scaling, no data-path collective); timing is max over ranks of CUDA-event time.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+``--impl reference`` times the float64 CPU oracle (the reference arm of this tier) on a bounded
+sample of the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "history items summarized/sec (S=256,d=128) + % bf16 tensor peak, 1/2/4/8 GPU"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--attn", default="softmax", choices=["softmax", "qla"])
+    ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+def workload(config, attn):
+    import synth
+    cfg = synth.CONFIGS[config]
+    lens = synth.user_lengths(config, seed=0)
+    S, H, d = cfg["S"], cfg["H"], cfg["d"]
+    desc = {
+        "c2": "c2: 64 users x 10,000 items, S=256, d=128, H=4, bf16",
+        "c3": "c3: 32 users x U[10k,100k] items, S=256, d=128, H=1, bf16",
+        "c4": "c4: 8 users x 1,000,000 items, S=256, d=128, H=1, bf16",
+        "c5": "c5: 1,024 users x power-law[1k,1M] items, S=512, d=128, H=1, bf16",
+    }[config]
+    return cfg, lens, S, H, d, desc + f", {attn}"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms; keep samples in [t0, t1]."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.lines = []
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self, t0, t1):
+        if self.p is None:
+            return None
+        time.sleep(0.12)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=2)
+        except Exception:
+            self.p.kill()
+        rows = [l for (ts, l) in self.lines if t0 - 0.06 <= ts <= t1 + 0.06]
+        if not rows:  # timed region shorter than one sample period: nearest sample after it
+            after = [l for (ts, l) in self.lines if ts >= t0]
+            rows = after[:1]
+        mhz, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                mhz.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not mhz:
+            return None
+        mhz.sort()
+        return {"sm_mhz": mhz[len(mhz) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(mhz)}
+
+
+# ----------------------------------------------------------------------------- own arm
+def run_own(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2510_22049_b200 as vista
+    import synth
+
+    vista.load()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
+    attn = vista.SOFTMAX if args.attn == "softmax" else vista.QLA
+    # by-user sharding: rank r summarizes its own batch (seed r); identical shape on every rank
+    q, K, V, off = synth.make_batch(lens, S, H, d, seed=rank, backend="torch", device=dev)
+    total = int(off[-1])
+    off_t = torch.from_numpy(off).to(dev)
+    B = len(lens)
+    desc = vista.make_desc(B, S, H, d, in_dtype=vista.BF16, out_dtype=vista.BF16, attn=attn)
+    path = vista.vista_dispatch_name(desc)
+    ws_bytes = vista.vista_summarize_workspace_size(desc, total)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    out = torch.empty((B, S, H, d), dtype=torch.bfloat16, device=dev)
+    lse = torch.empty((B, H, S), dtype=torch.float32, device=dev) if attn == vista.SOFTMAX else None
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    def step():
+        vista.vista_summarize_fwd(desc, q, K, V, off_t, total, out, lse, ws, ws_bytes, sh)
+
+    # warm-up
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    K_steps = args.steps
+    ev_k = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K_steps)]
+    for a, b in ev_k:  # materialize the event handles
+        a.record(stream)
+        b.record(stream)
+    t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gpu_index = os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[local_rank] \
+        if "CUDA_VISIBLE_DEVICES" in os.environ else str(local_rank)
+    sampler = ClockSampler(gpu_index)
+    time.sleep(0.3)  # let nvidia-smi start sampling
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = vista.vista_launch_counter()
+    w0 = time.time()
+    t_start.record(stream)
+    for i in range(K_steps):
+        vista.vista_time_next_main_kernel(ev_k[i][0], ev_k[i][1])
+        step()
+    t_stop.record(stream)
+    torch.cuda.synchronize()
+    w1 = time.time()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = vista.vista_launch_counter() - launches0
+    clocks = sampler.stop(w0, w1)
+    elapsed_ms = t_start.elapsed_time(t_stop)
+    kern_ms = sum(a.elapsed_time(b) for a, b in ev_k) / K_steps
+    if world > 1:
+        t = torch.tensor([elapsed_ms, kern_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed_ms, kern_ms = float(t[0]), float(t[1])
+    items_per_step = world * total
+    value = items_per_step * K_steps / (elapsed_ms / 1e3)
+
+    # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        hq, hK, hV = q.cpu().pin_memory(), K.cpu().pin_memory(), V.cpu().pin_memory()
+        hoff = off_t.cpu().pin_memory()
+        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        hlse = torch.empty(lse.shape, dtype=lse.dtype).pin_memory() if lse is not None else None
+        dq, dK, dV, doff = torch.empty_like(q), torch.empty_like(K), torch.empty_like(V), torch.empty_like(off_t)
+
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True)
+            dK.copy_(hK, non_blocking=True)
+            dV.copy_(hV, non_blocking=True)
+            doff.copy_(hoff, non_blocking=True)
+            vista.vista_summarize_fwd(desc, dq, dK, dV, doff, total, out, lse, ws, ws_bytes, sh)
+            hout.copy_(out, non_blocking=True)
+            if hlse is not None:
+                hlse.copy_(lse, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(t[0])
+        h2d = sum(x.numel() * x.element_size() for x in (hq, hK, hV, hoff))
+        d2h = hout.numel() * hout.element_size() + (hlse.numel() * hlse.element_size() if hlse is not None else 0)
+        e2e = {"value": items_per_step * args.e2e_steps / (e_ms / 1e3), "unit": "items/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "note": "pinned host buffers -> H2D copies -> vista_summarize_fwd -> D2H of out+lse, CUDA events"}
+
+    if rank != 0:
+        return None
+    pk, pk_kind = peaks()
+    flops = 4.0 * S * d * H * total if attn == vista.SOFTMAX else 2.0 * d * d * H * total
+    kv_bytes = 4.0 * d * H * total  # bf16 K + V, read once
+    io_bytes = kv_bytes + S * H * d * 2 + B * S * H * d * 2 + (B * H * S * 4 if lse is not None else 0)
+    tflops = flops / (kern_ms / 1e3) / 1e12
+    gbs = io_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"{args.config}_{args.attn}")
+    if attn == vista.SOFTMAX:
+        roof = {"bound": "tensor", "achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": round(tflops / pk["bf16_tflops"], 4), "traffic": traffic,
+                "peak_kind": f"{pk_kind} bf16 burst (kernel timed alone per launch)",
+                "kernel": "sm100_softmax_kernel", "kernel_ms": round(kern_ms, 5),
+                "algorithmic_flop_per_launch": flops,
+                "hbm": {"achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": round(gbs / pk["hbm_gbs"], 4), "algorithmic_bytes_per_launch": io_bytes}}
+    else:
+        roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic, "peak_kind": f"{pk_kind} HBM copy",
+                "kernel": "sm100_qla_state_kernel", "kernel_ms": round(kern_ms, 5),
+                "algorithmic_bytes_per_launch": io_bytes,
+                "tensor": {"achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                           "frac": round(tflops / pk["bf16_tflops"], 4)}}
+    res = {
+        "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": world, "steps": K_steps,
+        "warmup": args.warmup, "ms_per_step": elapsed_ms / K_steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded counter-based generator, bf16-exact grid values; synth/)",
+        "config": {"workload": wdesc, "users_per_gpu": B, "items_per_gpu": total, "S": S, "d": d, "H": H,
+                   "attn": args.attn, "parallelism": f"by_user x{world} (no data-path collective)",
+                   "path": path, "l2": f"inputs {kv_bytes / 1e9:.2f} GB/GPU > 126 MB L2, no flush",
+                   "pct_bf16_tensor_peak": round(100 * tflops / pk["bf16_tflops"], 2)},
+        "roofline": roof,
+        "clocks": clocks,
+        "e2e": e2e,
+        "gpu_launches": launches,
+    }
+    return res
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_sample(config, attn, seconds, rows=None):
+    """Time the float64 oracle on whole users (all rows, all heads) of the rank-0 batch until
+    ~`seconds` of CPU work; returns (items/s, cores, sample description, equivalent items, s)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    cfg, lens, S, H, d, _ = workload(config, attn)
+    off = synth.offsets_from_lengths(lens)
+    cores = len(os.sched_getaffinity(0))
+    q = synth.make_q(S, H, d, seed=0)
+    done_items, done_t, users = 0.0, 0.0, 0
+    rsel = None if rows is None else np.arange(rows, dtype=np.int64)
+    frac = 1.0 if rows is None else rows / S
+    for u in range(len(lens)):
+        a, b = int(off[u]), int(off[u + 1])
+        rr = np.arange(a, b, dtype=np.int64)
+        k, v = synth.make_kv(rr, np.full(b - a, u), H, d, seed=0)
+        t0 = time.perf_counter()
+        if attn == "softmax":
+            oracle.softmax_summarize(q, k, v, [0, b - a], rows=rsel, threads=cores)
+        else:
+            oracle.qla_summarize(q, k, v, [0, b - a], threads=cores)
+        done_t += time.perf_counter() - t0
+        done_items += (b - a) * frac
+        users += 1
+        if done_t >= seconds:
+            break
+    rdesc = "all S rows" if rows is None else f"{rows} of {S} rows (items counted x {rows}/{S})"
+    sample = f"{users} whole user(s) of {config} ({rdesc}, all {H} heads, full histories), float64 C oracle, OpenMP"
+    return done_items / done_t, cores, sample, done_items, done_t
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the float64 oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return None
+    import numpy as np
+
+    import oracle
+    import synth
+    cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    off = synth.offsets_from_lengths(lens)
+    q = synth.make_q(S, H, d, seed=0)
+    # per-step sample: user (i mod B), all heads, R query rows; R sized so the run takes ~90 s
+    total_steps = args.steps + args.warmup
+    u0 = 0
+    a, b = int(off[u0]), int(off[u0 + 1])
+    k, v = synth.make_kv(np.arange(a, b, dtype=np.int64), np.full(b - a, u0), H, d, seed=0)
+    t0 = time.perf_counter()
+    if args.attn == "softmax":
+        oracle.softmax_summarize(q, k, v, [0, b - a], rows=np.arange(1), threads=cores)
+    else:
+        oracle.qla_state(k[: max(1, (b - a) // 16)], v[: max(1, (b - a) // 16)], [0, max(1, (b - a) // 16)],
+                         threads=cores)
+    t_unit = max(time.perf_counter() - t0, 1e-4)
+    budget = 90.0 / max(total_steps, 1)
+    R = int(max(1, min(S, budget / t_unit)))
+    cache = {}
+
+    def kv_of(u):
+        if u not in cache:
+            a, b = int(off[u]), int(off[u + 1])
+            cache.clear()
+            cache[u] = synth.make_kv(np.arange(a, b, dtype=np.int64), np.full(b - a, u), H, d, seed=0)
+        return cache[u]
+
+    items, tt = 0.0, 0.0
+    for i in range(total_steps):
+        u = i % len(lens)
+        k, v = kv_of(u)
+        L = k.shape[0]
+        t0 = time.perf_counter()
+        if args.attn == "softmax":
+            oracle.softmax_summarize(q, k, v, [0, L], rows=np.arange(R), threads=cores)
+            eq = L * R / S
+        else:
+            n = max(1, min(L, int(L * R / S)))
+            oracle.qla_state(k[:n], v[:n], [0, n], threads=cores)
+            eq = n
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            items += eq
+            tt += dt
+    value = items / tt
+    sample = (f"per step: 1 user of {args.config} (cycling), all {H} heads, "
+              + (f"{R} of {S} query rows over the full history (items counted x {R}/{S})" if args.attn == "softmax"
+                 else f"QLA state over the first {R}/{S} of the history"))
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (same generator and seed as the own arm)",
+        "config": {"workload": wdesc, "S": S, "d": d, "H": H, "attn": args.attn},
+        "cpu_baseline": {"value": value, "unit": "items/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_own(args, rank, world, local_rank)
+    if res is not None and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds,
+                                               rows=None if args.attn == "qla" else 32)
+        res["cpu_baseline"] = {"value": v, "unit": "items/s", "cores": cores, "kind": "oracle",
+                               "sample": sample, "seconds": round(t, 2)}
+    elif res is not None:
+        res["cpu_baseline"] = None
+    if res is not None:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -22,7 +22,7 @@ __all__ = [
     "VistaError", "Desc", "load", "lib_path", "make_desc",
     "vista_abi_version", "vista_status_string", "vista_summarize_workspace_size",
     "vista_summarize_fwd", "vista_summarize_partial", "vista_summarize_merge",
-    "vista_check_offsets", "vista_dispatch_name",
+    "vista_check_offsets", "vista_dispatch_name", "vista_time_next_main_kernel", "vista_launch_counter",
     "summarize", "summarize_partial", "summarize_merge",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
@@ -90,6 +90,9 @@ def load():
     lib.vista_summarize_partial.argtypes = [DP, P, P, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge.argtypes = [DP, i32, P, P, P, P, P, P, P]
     lib.vista_check_offsets.argtypes = [P, i32, i64, P]
+    lib.vista_time_next_main_kernel.argtypes = [P, P]
+    lib.vista_time_next_main_kernel.restype = ctypes.c_int
+    lib.vista_launch_counter.restype = ctypes.c_uint64
     for f in ("vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
               "vista_summarize_merge", "vista_check_offsets"):
         getattr(lib, f).restype = ctypes.c_int
@@ -166,6 +169,16 @@ def vista_summarize_merge(desc, num_parts, part_o, part_lse, q, user_len, out, l
 def vista_check_offsets(offsets, num_users, total_len, stream=None):
     _check(load().vista_check_offsets(_ptr(offsets), int(num_users), int(total_len), _stream(stream)),
            "vista_check_offsets")
+
+
+def vista_time_next_main_kernel(start_event, stop_event):
+    """Arm the one-shot timing hook (torch.cuda.Event objects or raw cudaEvent_t handles)."""
+    h = [None if e is None else (e if isinstance(e, int) else e.cuda_event) for e in (start_event, stop_event)]
+    _check(load().vista_time_next_main_kernel(h[0], h[1]), "vista_time_next_main_kernel")
+
+
+def vista_launch_counter() -> int:
+    return int(load().vista_launch_counter())
 
 
 # ----------------------------------------------------------------------------- torch helpers

@@ -28,7 +28,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libvista.so")
+_LIB_PATH = os.environ.get("VISTA_LIB") or os.path.join(_HERE, "libvista.so")  # VISTA_LIB: A/B builds
 
 ABI_VERSION = 1
 F32, BF16 = 0, 1

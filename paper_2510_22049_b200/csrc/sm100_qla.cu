@@ -149,11 +149,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&bars->k_ready[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t ka = base + stage * kStageBytes, va = ka + kTileBytes;
+#ifndef VISTA_EXP_QLA_NOMMA
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk)
                         ptx::mma_ss(dz, ptx::sdesc_sw128(ka + kk * 2048, kHalfBytes, 1024),
                                     ptx::sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), idZ,
                                     (t > it.t0 || kk > 0) ? 1u : 0u);
+#endif
                     ptx::mma_commit(&bars->kv_empty[stage]);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
@@ -178,7 +180,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(&bars->kv_full[stage], phase);
                 const int64_t valid = L - (int64_t)t * kTile;
                 uint4* sk = reinterpret_cast<uint4*>(smem + stage * kStageBytes);
+#ifdef VISTA_EXP_QLA_NOXFORM
+                if (false) {
+#else
                 if (phi1 != VISTA_ACT_IDENTITY || valid < kTile) {
+#endif
 #pragma unroll 4
                     for (int c = xt; c < kTileBytes / 16; c += kXformWarps * 32) {
                         const int j = (c & 1023) >> 3;  // 128-B line = history row within the tile

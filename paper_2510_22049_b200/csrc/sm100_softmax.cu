@@ -33,25 +33,34 @@ namespace {
 constexpr int kHalfBytes = 128 * 128;       // 128 rows x 64 bf16 (one 128-B swizzle column block)
 constexpr int kTileBytes = 2 * kHalfBytes;  // 128 x 128 bf16
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
+#ifndef VISTA_SETMAXNREG
+#define VISTA_SETMAXNREG 0
+#endif
+constexpr bool kSetMaxNReg = VISTA_SETMAXNREG;  // shift registers from the control warps to the softmax warps
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
 template <int NQ>
 struct Cfg {
-    static constexpr int kStages = NQ == 2 ? 2 : 3;
+    // smem: Q tiles, a ring of K tiles and a separate (shallower) ring of V tiles.  K is released as
+    // soon as the score GEMMs of its tile have run, V only after the PV GEMMs, so splitting the
+    // rings keeps ~3 tiles of HBM reads in flight per SM instead of ~2.
+    static constexpr int kKStages = 3;
+    static constexpr int kVStages = NQ == 2 ? 2 : 3;  // 224 KB total either way
     static constexpr int kQOff = 0;
-    static constexpr int kKVOff = NQ * kTileBytes;
-    static constexpr int kStageBytes = 2 * kTileBytes;  // K + V
-    static constexpr int kBarOff = kKVOff + kStages * kStageBytes;
-    static constexpr int kSmem = kBarOff + 256 + 1024;  // + alignment slack
-    static constexpr int kThreads = 128 + NQ * 128;  // control warpgroup + NQ softmax warpgroups
+    static constexpr int kKOff = NQ * kTileBytes;
+    static constexpr int kVOff = kKOff + kKStages * kTileBytes;
+    static constexpr int kBarOff = kVOff + kVStages * kTileBytes;
+    static constexpr int kSmem = kBarOff + 512 + 1024;  // + alignment slack
+    static constexpr int kThreads = 128 + NQ * 128;     // control warpgroup + NQ softmax warpgroups
     static constexpr int kTmemCols = NQ == 2 ? 512 : 256;
 };
 
 struct Bars {
     uint64_t q_full, q_empty;
-    uint64_t kv_full[3], kv_empty[3];
-    uint64_t s_full[2], p_full[2], o_full[2];
+    uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
+    uint64_t s_full[2][2], p_full[2][2];  // [q tile][S buffer]
+    uint64_t pv_done[2], o_full[2];
     uint32_t tmem_base;
 };
 
@@ -110,6 +119,65 @@ __device__ __forceinline__ void store_row(const Params& P, const Item& it, int c
     if (write_lse && P.outs.lse) P.outs.lse[((size_t)it.u * P.H + h) * P.S + i] = lse;
 }
 
+// ---- MMA issue with compile-time geometry (see the MMA role) ----
+template <int NQ, int Q, int HALF, int ST>
+__device__ __forceinline__ void issue_S_t(uint32_t tmem, uint32_t sQa, uint32_t sKa) {
+    // S_Q(h) = Q_Q K^T over the 64 keys [64 HALF, 64 HALF + 64) of K stage ST -> S buffer HALF (N = 64)
+    constexpr uint32_t idS = ptx::idesc_bf16_f32(128, 64, 0, 0);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
+        ptx::mma_ss_w(tmem + Q * 128 + HALF * 64, ptx::sdesc_sw128(sQa + Q * kTileBytes + off, 16, 1024),
+                      ptx::sdesc_sw128(sKa + ST * kTileBytes + HALF * 64 * 128 + off, 16, 1024), idS, kk > 0);
+    }
+}
+template <int NQ, int Q, int HALF, int ST, bool ACC>
+__device__ __forceinline__ void issue_PV_t(uint32_t tmem, uint32_t sVa) {
+    // O_Q += P_Q(h) V over keys [64 HALF, 64 HALF + 64) of V stage ST; P read from S buffer HALF
+    constexpr uint32_t idP = ptx::idesc_bf16_f32(128, 128, 0, 1);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+        ptx::mma_ts_w(tmem + NQ * 128 + Q * 128, tmem + Q * 128 + HALF * 64 + kk * 8,
+                      ptx::sdesc_sw128(sVa + ST * kTileBytes + HALF * 64 * 128 + kk * 2048, kHalfBytes, 1024), idP,
+                      (ACC || kk > 0) ? 1u : 0u);
+}
+template <int NQ, int Q, int HALF>
+__device__ __forceinline__ void issue_S_q(int st, uint32_t tmem, uint32_t sQa, uint32_t sKa) {
+    switch (st) {
+        case 0: issue_S_t<NQ, Q, HALF, 0>(tmem, sQa, sKa); break;
+        case 1: issue_S_t<NQ, Q, HALF, 1>(tmem, sQa, sKa); break;
+        default: issue_S_t<NQ, Q, HALF, 2>(tmem, sQa, sKa); break;
+    }
+}
+template <int NQ>
+__device__ __forceinline__ void issue_S_d(int q, int half, int st, uint32_t tmem, uint32_t sQa, uint32_t sKa) {
+    if (q == 0) {
+        if (half == 0) issue_S_q<NQ, 0, 0>(st, tmem, sQa, sKa); else issue_S_q<NQ, 0, 1>(st, tmem, sQa, sKa);
+    } else if constexpr (NQ > 1) {
+        if (half == 0) issue_S_q<NQ, 1, 0>(st, tmem, sQa, sKa); else issue_S_q<NQ, 1, 1>(st, tmem, sQa, sKa);
+    }
+}
+template <int NQ, int Q, int HALF, bool ACC>
+__device__ __forceinline__ void issue_PV_q(int st, uint32_t tmem, uint32_t sVa) {
+    switch (st) {
+        case 0: issue_PV_t<NQ, Q, HALF, 0, ACC>(tmem, sVa); break;
+        case 1: issue_PV_t<NQ, Q, HALF, 1, ACC>(tmem, sVa); break;
+        default: issue_PV_t<NQ, Q, HALF, 2, ACC>(tmem, sVa); break;
+    }
+}
+template <int NQ>
+__device__ __forceinline__ void issue_PV_d(int q, int half, int st, bool acc, uint32_t tmem, uint32_t sVa) {
+    if (q == 0) {
+        if (half == 1) issue_PV_q<NQ, 0, 1, true>(st, tmem, sVa);
+        else if (acc) issue_PV_q<NQ, 0, 0, true>(st, tmem, sVa);
+        else issue_PV_q<NQ, 0, 0, false>(st, tmem, sVa);
+    } else if constexpr (NQ > 1) {
+        if (half == 1) issue_PV_q<NQ, 1, 1, true>(st, tmem, sVa);
+        else if (acc) issue_PV_q<NQ, 1, 0, true>(st, tmem, sVa);
+        else issue_PV_q<NQ, 1, 0, false>(st, tmem, sVa);
+    }
+}
+
 template <int NQ>
 __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     sm100_softmax_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
@@ -118,7 +186,8 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem + C::kQOff;
-    uint8_t* sKV = smem + C::kKVOff;
+    uint8_t* sK = smem + C::kKOff;
+    uint8_t* sV = smem + C::kVOff;
     Bars* bars = reinterpret_cast<Bars*>(smem + C::kBarOff);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -129,13 +198,20 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     if (threadIdx.x == 0) {
         ptx::mbar_init(&bars->q_full, 1);
         ptx::mbar_init(&bars->q_empty, 1);
-        for (int s = 0; s < C::kStages; ++s) {
-            ptx::mbar_init(&bars->kv_full[s], 1);
-            ptx::mbar_init(&bars->kv_empty[s], 1);
+        for (int s = 0; s < C::kKStages; ++s) {
+            ptx::mbar_init(&bars->k_full[s], 1);
+            ptx::mbar_init(&bars->k_empty[s], 1);
+        }
+        for (int s = 0; s < C::kVStages; ++s) {
+            ptx::mbar_init(&bars->v_full[s], 1);
+            ptx::mbar_init(&bars->v_empty[s], 1);
         }
         for (int q = 0; q < NQ; ++q) {
-            ptx::mbar_init(&bars->s_full[q], 1);
-            ptx::mbar_init(&bars->p_full[q], 128);
+            for (int b = 0; b < 2; ++b) {
+                ptx::mbar_init(&bars->s_full[q][b], 1);
+                ptx::mbar_init(&bars->p_full[q][b], 128);
+            }
+            ptx::mbar_init(&bars->pv_done[q], 1);
             ptx::mbar_init(&bars->o_full[q], 1);
         }
         ptx::fence_mbar_init();
@@ -156,7 +232,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = bars->tmem_base;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
 
     ItemIter iter;
     iter.init(P.uts, P.B, HG, cta, num_ctas);
@@ -164,14 +240,12 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
 
     if (warp < 4) {
         // register split: the launch grants 168 x 384 = 64512 registers; 128 x 88 + 256 x 208 = 64512
-        // (setmaxnreg.inc blocks forever if the pool cannot cover it).  Softmax rows hold 128 fp32 scores.
-        if constexpr (NQ == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
-    if (warp == 0) {
-        // ============================ TMA producer ============================
-        if (lane == 0) {
+        // (setmaxnreg.inc blocks forever if the pool cannot cover it).
+        if constexpr (NQ == 2 && kSetMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+        if (warp == 0) {
+            // ============================ TMA producer: Q, K ============================
             ptx::tma_prefetch(&mapQ);
             ptx::tma_prefetch(&mapK);
-            ptx::tma_prefetch(&mapV);
             const uint64_t pol_kv = ptx::policy_evict_first();
             const uint64_t pol_q = ptx::policy_evict_last();
             int stage = 0;
@@ -180,97 +254,122 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             while (iter.next(it)) {
                 const int h = it.hg / P.G, g = it.hg % P.G;
                 if (k > 0) ptx::mbar_wait(&bars->q_empty, (k - 1) & 1);
-                ptx::mbar_arrive_expect_tx(&bars->q_full, NQ * kTileBytes);
+                ptx::mbar_arrive_expect_tx_w(&bars->q_full, NQ * kTileBytes);
                 for (int q = 0; q < NQ; ++q)
                     for (int half = 0; half < 2; ++half)
-                        ptx::tma_load_4d(sQ + q * kTileBytes + half * kHalfBytes, &mapQ, &bars->q_full, half * 64, h,
+                        ptx::tma_load_4d_w(sQ + q * kTileBytes + half * kHalfBytes, &mapQ, &bars->q_full, half * 64, h,
                                          g * kRows + q * 128, P.q_per_user ? it.u : 0, pol_q);
                 const int64_t row0 = P.offsets[it.u];
                 for (int t = it.t0; t < it.t1; ++t) {
-                    ptx::mbar_wait(&bars->kv_empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&bars->kv_full[stage], C::kStageBytes);
-                    uint8_t* sk = sKV + stage * C::kStageBytes;
-                    uint8_t* sv = sk + kTileBytes;
-                    const int32_t row = (int32_t)(row0 + (int64_t)t * kTile);
-                    for (int half = 0; half < 2; ++half) {
-                        ptx::tma_load_3d(sk + half * kHalfBytes, &mapK, &bars->kv_full[stage], half * 64, h, row, pol_kv);
-                        ptx::tma_load_3d(sv + half * kHalfBytes, &mapV, &bars->kv_full[stage], half * 64, h, row, pol_kv);
+                    ptx::mbar_wait(&bars->k_empty[stage], phase ^ 1);
+#ifdef VISTA_EXP_NOLOAD  // experiment: keep re-using resident tiles (no HBM traffic after the first ones)
+                    if (t >= it.t0 + C::kKStages) {
+                        if (ptx::elect_one()) ptx::mbar_arrive(&bars->k_full[stage]);
+                        __syncwarp();
+                        if (++stage == C::kKStages) { stage = 0; phase ^= 1; }
+                        continue;
                     }
-                    if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+#endif
+                    ptx::mbar_arrive_expect_tx_w(&bars->k_full[stage], kTileBytes);
+                    const int32_t row = (int32_t)(row0 + (int64_t)t * kTile);
+                    for (int half = 0; half < 2; ++half)
+                        ptx::tma_load_3d_w(sK + stage * kTileBytes + half * kHalfBytes, &mapK, &bars->k_full[stage],
+                                         half * 64, h, row, pol_kv);
+                    if (++stage == C::kKStages) { stage = 0; phase ^= 1; }
                 }
                 ++k;
             }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        // ============================ MMA issuer ============================
-        if (lane == 0) {
-            constexpr uint32_t idS = ptx::idesc_bf16_f32(128, 128, 0, 0);  // Q, K both K-major
-            constexpr uint32_t idP = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM), V MN-major
-            const uint32_t sQa = ptx::smem_u32(sQ), sKVa = ptx::smem_u32(sKV);
+        } else if (warp == 2) {
+            // ============================ TMA producer: V ============================
+            ptx::tma_prefetch(&mapV);
+            const uint64_t pol_kv = ptx::policy_evict_first();
             int stage = 0;
-            uint32_t kv_phase = 0, q_phase = 0;
-            uint32_t p_phase[2] = {0, 0};
-            auto issue_S = [&](int q, int st) {
-                const uint32_t qa = sQa + q * kTileBytes;
-                const uint32_t ka = sKVa + st * C::kStageBytes;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-                    ptx::mma_ss(tmem + q * 128, ptx::sdesc_sw128(qa + off, 16, 1024),
-                                ptx::sdesc_sw128(ka + off, 16, 1024), idS, kk > 0);
-                }
-            };
-            auto issue_PV = [&](int q, int st, bool acc) {
-                const uint32_t va = sKVa + st * C::kStageBytes + kTileBytes;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    ptx::mma_ts(tmem + NQ * 128 + q * 128, tmem + q * 128 + kk * 8,
-                                ptx::sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), idP, (acc || kk > 0) ? 1u : 0u);
-                }
-            };
+            uint32_t phase = 0;
             while (iter.next(it)) {
-                const int n = it.t1 - it.t0;
+                const int h = it.hg / P.G;
+                const int64_t row0 = P.offsets[it.u];
+                for (int t = it.t0; t < it.t1; ++t) {
+                    ptx::mbar_wait(&bars->v_empty[stage], phase ^ 1);
+#ifdef VISTA_EXP_NOLOAD
+                    if (t >= it.t0 + C::kVStages) {
+                        if (ptx::elect_one()) ptx::mbar_arrive(&bars->v_full[stage]);
+                        __syncwarp();
+                        if (++stage == C::kVStages) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
+#endif
+                    ptx::mbar_arrive_expect_tx_w(&bars->v_full[stage], kTileBytes);
+                    const int32_t row = (int32_t)(row0 + (int64_t)t * kTile);
+                    for (int half = 0; half < 2; ++half)
+                        ptx::tma_load_3d_w(sV + stage * kTileBytes + half * kHalfBytes, &mapV, &bars->v_full[stage],
+                                         half * 64, h, row, pol_kv);
+                    if (++stage == C::kVStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        } else if (warp == 1) {
+            // ============================ MMA issuer ============================
+            // Work proceeds in half tiles h (64 keys): S_q(h) = Q_q K_h^T into S buffer h%2 of Q tile q,
+            // O_q += P_q(h) V_h.  Two S buffers per Q tile let S(h+1) be ready while the softmax works
+            // on S(h); issue order  PV_0(h) S_0(h+2) PV_1(h) S_1(h+2) ...
+            // The whole warp runs this loop and every MMA operand is a uniform base plus a compile-time
+            // offset (stage / half / q / k-step are template arguments), so ptxas keeps descriptors in
+            // uniform registers and the tcgen05.mma issue is a few instructions each.
+            const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+            const uint32_t sQa = base + C::kQOff, sKa = base + C::kKOff, sVa = base + C::kVOff;
+            int kst = 0, vst = 0;
+            uint32_t kph = 0, vph = 0, q_phase = 0;
+            uint32_t p_phase[2][2] = {{0, 0}, {0, 0}};
+            while (iter.next(it)) {
+                const int ntiles = it.t1 - it.t0;
                 ptx::mbar_wait(&bars->q_full, q_phase);
                 q_phase ^= 1;
-                ptx::mbar_wait(&bars->kv_full[stage], kv_phase);
+                ptx::mbar_wait(&bars->k_full[kst], kph);
                 ptx::tc_fence_after();
+#pragma unroll
                 for (int q = 0; q < NQ; ++q) {
-                    issue_S(q, stage);
-                    ptx::mma_commit(&bars->s_full[q]);
+                    issue_S_d<NQ>(q, 0, kst, tmem, sQa, sKa);
+                    ptx::mma_commit_w(&bars->s_full[q][0]);
+                    issue_S_d<NQ>(q, 1, kst, tmem, sQa, sKa);
+                    ptx::mma_commit_w(&bars->s_full[q][1]);
                 }
-                for (int i = 0; i < n; ++i) {
-                    const int cur = stage;
-                    int nst = stage + 1;
-                    uint32_t nph = kv_phase;
-                    if (nst == C::kStages) { nst = 0; nph ^= 1; }
-                    for (int q = 0; q < NQ; ++q) {
-                        ptx::mbar_wait(&bars->p_full[q], p_phase[q]);
-                        p_phase[q] ^= 1;
-                        ptx::tc_fence_after();
-                        issue_PV(q, cur, i > 0);
-                        if (q == NQ - 1) ptx::mma_commit(&bars->kv_empty[cur]);
-                        if (i == n - 1) {
-                            ptx::mma_commit(&bars->o_full[q]);
-                            if (q == NQ - 1) ptx::mma_commit(&bars->q_empty);
-                        } else {
-                            if (q == 0) {
-                                ptx::mbar_wait(&bars->kv_full[nst], nph);
-                                ptx::tc_fence_after();
+                for (int t = 0; t < ntiles; ++t) {
+                    const bool more = t + 1 < ntiles;
+                    ptx::mbar_wait(&bars->v_full[vst], vph);
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                        for (int q = 0; q < NQ; ++q) {
+                            ptx::mbar_wait(&bars->p_full[q][half], p_phase[q][half]);
+                            p_phase[q][half] ^= 1;
+                            ptx::tc_fence_after();
+                            issue_PV_d<NQ>(q, half, vst, half == 1 || t > 0, tmem, sVa);
+                            ptx::mma_commit_w(&bars->pv_done[q]);
+                            if (half == 1 && !more) ptx::mma_commit_w(&bars->o_full[q]);
+                            if (more) {
+                                if (q == 0 && half == 0) {
+                                    // every score GEMM of this K tile has been issued: release it, take the next
+                                    ptx::mma_commit_w(&bars->k_empty[kst]);
+                                    if (++kst == C::kKStages) { kst = 0; kph ^= 1; }
+                                    ptx::mbar_wait(&bars->k_full[kst], kph);
+                                    ptx::tc_fence_after();
+                                }
+                                issue_S_d<NQ>(q, half, kst, tmem, sQa, sKa);
+                                ptx::mma_commit_w(&bars->s_full[q][half]);
                             }
-                            issue_S(q, nst);
-                            ptx::mma_commit(&bars->s_full[q]);
                         }
                     }
-                    stage = nst;
-                    kv_phase = nph;
+                    ptx::mma_commit_w(&bars->v_empty[vst]);
+                    if (++vst == C::kVStages) { vst = 0; vph ^= 1; }
                 }
+                ptx::mma_commit_w(&bars->k_empty[kst]);  // last K tile of the item
+                if (++kst == C::kKStages) { kst = 0; kph ^= 1; }
+                ptx::mma_commit_w(&bars->q_empty);
             }
         }
         __syncwarp();
-    }
     } else {
-        if constexpr (NQ == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+        if constexpr (NQ == 2 && kSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
         // ============================ softmax warpgroups ============================
         const int wg = (warp - 4) / 4;  // warps 4..7 -> Q tile 0, 8..11 -> Q tile 1
         const int wq = warp % 4;
@@ -279,71 +378,103 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
         const uint32_t tS = tmem + lane_bits + wg * 128;
         const uint32_t tO = tmem + lane_bits + NQ * 128 + wg * 128;
         const float sl2 = P.scale_log2;
-        uint32_t s_phase = 0, o_phase = 0;
+        uint32_t s_phase[2] = {0, 0}, o_phase = 0;
+        uint32_t pv_base = 0;  // PV GEMMs of this Q tile issued before the current item
         while (iter.next(it)) {
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
+            const int nh = 2 * (it.t1 - it.t0);
             float m_used = -INFINITY, l = 0.f;
-            for (int t = it.t0; t < it.t1; ++t) {
-                ptx::mbar_wait(&bars->s_full[wg], s_phase);
-                s_phase ^= 1;
+            for (int h = 0; h < nh; ++h) {
+                const int b = h & 1;
+                ptx::mbar_wait(&bars->s_full[wg][b], s_phase[b]);
+                s_phase[b] ^= 1;
                 ptx::tc_fence_after();
-                uint32_t r[4][32];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + c * 32, r[c]);
+                uint32_t r[2][32];
+                ptx::tmem_ld32(tS + b * 64, r[0]);
+                ptx::tmem_ld32(tS + b * 64 + 32, r[1]);
                 ptx::tmem_wait_ld();
+                ptx::reg_fence(r[0]);
+                ptx::reg_fence(r[1]);
+#ifdef VISTA_EXP_NOSOFTMAX  // experiment: skip the softmax math (P = stale TMEM contents)
+                if (true) {
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars->p_full[wg][b]);
+                    l = 1.f;
+                    m_used = 0.f;
+                    continue;
+                }
+#endif
+                const int64_t valid = L - ((int64_t)(it.t0 + (h >> 1)) * kTile + b * 64);
+                if (valid < 64) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) ptx::reg_fence(r[c]);
-                const int64_t valid = L - (int64_t)t * kTile;
-                if (valid < kTile) {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
+                    for (int c = 0; c < 2; ++c)
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             if (c * 32 + j >= valid) r[c][j] = __float_as_uint(-INFINITY);
                 }
-                float mx = -INFINITY;
+                // row max: 4 independent FMNMX3 chains, then a small tree
+                float m4[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int a = 0; a < 4; ++a) {
+                    const int c = a >> 1, o = (a & 1) * 16;
+                    float m = ptx::max3(__uint_as_float(r[c][o]), __uint_as_float(r[c][o + 1]),
+                                        __uint_as_float(r[c][o + 2]));
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(r[c][j]));
-                const float mxs = mx * sl2;
+                    for (int j = 3; j < 15; j += 2)
+                        m = ptx::max3(m, __uint_as_float(r[c][o + j]), __uint_as_float(r[c][o + j + 1]));
+                    m4[a] = fmaxf(m, __uint_as_float(r[c][o + 15]));
+                }
+                const float mxs = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
                 const bool need = mxs > m_used + kRescaleThreshold;
-                const bool any = __any_sync(0xffffffffu, need);
-                const float m_old = m_used;
-                if (any) m_used = fmaxf(m_used, mxs);
-                const float neg = -m_used;
-                float lt = 0.f;
+                if (__any_sync(0xffffffffu, need)) {
+                    const float m_new = fmaxf(m_used, mxs);
+                    if (h > 0) {
+                        // O_q must hold PV(h-1) before it is rescaled.  S(h) was committed after PV(h-2), so
+                        // at most one PV completion is outstanding and the parity wait is unambiguous.
+                        ptx::mbar_wait(&bars->pv_done[wg], (pv_base + h - 1) & 1);
+                        ptx::tc_fence_after();
+                        const float f = ptx::ex2(m_used - m_new);
+                        l *= f;
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t pk[32];
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t o[32];
+                            ptx::tmem_ld32_sync(tO + c * 32, o);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = hf * 64 + 2 * j;
-                        const float p0 = ptx::ex2(fmaf(__uint_as_float(r[col >> 5][col & 31]), sl2, neg));
-                        const float p1 = ptx::ex2(fmaf(__uint_as_float(r[(col + 1) >> 5][(col + 1) & 31]), sl2, neg));
-                        lt += p0 + p1;
+                            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
+                            ptx::tmem_st32(tO + c * 32, o);
+                        }
+                    }
+                    m_used = m_new;
+                }
+                // p = 2^(s * scale * log2 e - m): packed FFMA2, MUFU ex2, bf16x2 pack into the first
+                // 32 columns of this S buffer (P aliases S; the next S into it is issued after PV reads P)
+                const uint64_t sl2x2 = ptx::f2_pack(sl2, sl2);
+                const uint64_t negx2 = ptx::f2_pack(-m_used, -m_used);
+                uint64_t acc[2] = {ptx::f2_pack(0.f, 0.f), ptx::f2_pack(0.f, 0.f)};
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint64_t x2 = ptx::f2_fma(
+                            ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
+                        float x0, x1;
+                        ptx::f2_unpack(x2, x0, x1);
+                        const float p0 = ptx::ex2(x0), p1 = ptx::ex2(x1);
+                        acc[j & 1] = ptx::f2_add(acc[j & 1], ptx::f2_pack(p0, p1));
                         pk[j] = ptx::pack_bf16x2(p0, p1);
                     }
-                    ptx::tmem_st32(tS + hf * 32, pk);
+                    ptx::tmem_st16(tS + b * 64 + c * 16, pk);
                 }
-                if (any && t > it.t0) {
-                    // O_q holds this item's sum so far (PV_q(t-1) completed: covered by s_full(t))
-                    const float f = ptx::ex2(m_old - m_used);
-                    l *= f;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t o[32];
-                        ptx::tmem_ld32_sync(tO + c * 32, o);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
-                        ptx::tmem_st32(tO + c * 32, o);
-                    }
-                }
-                l += lt;
+                float la, lb, lc, ld;
+                ptx::f2_unpack(acc[0], la, lb);
+                ptx::f2_unpack(acc[1], lc, ld);
+                l += (la + lb) + (lc + ld);
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&bars->p_full[wg]);
+                ptx::mbar_arrive(&bars->p_full[wg][b]);
             }
+            pv_base += (uint32_t)nh;
             // epilogue: O / l, lse
             ptx::mbar_wait(&bars->o_full[wg], o_phase);
             o_phase ^= 1;

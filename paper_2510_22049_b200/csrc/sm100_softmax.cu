@@ -28,14 +28,32 @@
 
 namespace vista {
 
+#ifdef VISTA_TRACE  // debug timeline of CTA 0, first item: clock64 per (event, tile, q tile)
+__device__ unsigned long long g_vista_trace[12][64][2];
+#define VTRACE(ev, t, q) \
+    do { if (blockIdx.x == 0 && (t) < 64) g_vista_trace[ev][t][q] = clock64(); } while (0)
+#else
+#define VTRACE(ev, t, q) do { } while (0)
+#endif
+
 namespace {
 
 constexpr int kHalfBytes = 128 * 128;       // 128 rows x 64 bf16 (one 128-B swizzle column block)
 constexpr int kTileBytes = 2 * kHalfBytes;  // 128 x 128 bf16
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
 #ifndef VISTA_SETMAXNREG
-#define VISTA_SETMAXNREG 0
+#define VISTA_SETMAXNREG 1
 #endif
+#ifndef VISTA_EMU_PER_EIGHT
+#define VISTA_EMU_PER_EIGHT 0
+#endif
+constexpr int kEmuPerEight = VISTA_EMU_PER_EIGHT;  // exp2 on the FMA pipe for this many of every 8 score pairs
+#ifndef VISTA_CTL_REGS
+#define VISTA_CTL_REGS 152
+#endif
+// the launch grants 168 x 384 = 64512 registers; 128 x ctl + 256 x softmax must not exceed it
+constexpr int kCtlRegs = VISTA_CTL_REGS;
+constexpr int kSoftmaxRegs = ((64512 - 128 * kCtlRegs) / 256) & ~7;
 constexpr bool kSetMaxNReg = VISTA_SETMAXNREG;  // shift registers from the control warps to the softmax warps
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -119,62 +137,92 @@ __device__ __forceinline__ void store_row(const Params& P, const Item& it, int c
     if (write_lse && P.outs.lse) P.outs.lse[((size_t)it.u * P.H + h) * P.S + i] = lse;
 }
 
+// p = 2^(s * scale * log2 e - m) for one 128-key row: packed FFMA2, exp2 on MUFU (ex2.approx) and,
+// for EMU of every 8 pairs, on the FMA pipe (exp2_emu2; only for tiles without masked keys);
+// bf16x2 pack; P overwrites the first 64 TMEM columns of S (16 columns per 32 keys).  Returns the
+// row sum of the (unrounded) p.
+template <int EMU>
+__device__ __forceinline__ float exp_tile(const uint32_t (&r)[4][32], float sl2, float neg, uint32_t tS) {
+    const uint64_t sl2x2 = ptx::f2_pack(sl2, sl2);
+    const uint64_t negx2 = ptx::f2_pack(neg, neg);
+    uint64_t acc[2] = {ptx::f2_pack(0.f, 0.f), ptx::f2_pack(0.f, 0.f)};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t x2 = ptx::f2_fma(
+                ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
+            uint64_t p2;
+            if (EMU > 0 && (j & 7) >= 8 - EMU) {
+                p2 = ptx::exp2_emu2(x2);
+            } else {
+                float x0, x1;
+                ptx::f2_unpack(x2, x0, x1);
+                p2 = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+            }
+            acc[j & 1] = ptx::f2_add(acc[j & 1], p2);
+            float p0, p1;
+            ptx::f2_unpack(p2, p0, p1);
+            pk[j] = ptx::pack_bf16x2(p0, p1);
+        }
+        ptx::tmem_st16(tS + c * 16, pk);
+    }
+    float la, lb, lc, ld;
+    ptx::f2_unpack(acc[0], la, lb);
+    ptx::f2_unpack(acc[1], lc, ld);
+    return (la + lb) + (lc + ld);
+}
+
 // ---- MMA issue with compile-time geometry (see the MMA role) ----
-template <int NQ, int Q, int HALF, int ST>
+template <int NQ, int Q, int ST>
 __device__ __forceinline__ void issue_S_t(uint32_t tmem, uint32_t sQa, uint32_t sKa) {
-    // S_Q(h) = Q_Q K^T over the 64 keys [64 HALF, 64 HALF + 64) of K stage ST -> S buffer HALF (N = 64)
-    constexpr uint32_t idS = ptx::idesc_bf16_f32(128, 64, 0, 0);
+    // S_Q = Q_Q K^T over the 128 keys of K stage ST -> TMEM columns [128 Q, 128 Q + 128)
+    constexpr uint32_t idS = ptx::idesc_bf16_f32(128, 128, 0, 0);  // Q, K both K-major
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-        ptx::mma_ss_w(tmem + Q * 128 + HALF * 64, ptx::sdesc_sw128(sQa + Q * kTileBytes + off, 16, 1024),
-                      ptx::sdesc_sw128(sKa + ST * kTileBytes + HALF * 64 * 128 + off, 16, 1024), idS, kk > 0);
+        ptx::mma_ss_w(tmem + Q * 128, ptx::sdesc_sw128(sQa + Q * kTileBytes + off, 16, 1024),
+                      ptx::sdesc_sw128(sKa + ST * kTileBytes + off, 16, 1024), idS, kk > 0);
     }
 }
-template <int NQ, int Q, int HALF, int ST, bool ACC>
+template <int NQ, int Q, int ST, bool ACC>
 __device__ __forceinline__ void issue_PV_t(uint32_t tmem, uint32_t sVa) {
-    // O_Q += P_Q(h) V over keys [64 HALF, 64 HALF + 64) of V stage ST; P read from S buffer HALF
-    constexpr uint32_t idP = ptx::idesc_bf16_f32(128, 128, 0, 1);
+    // O_Q += P_Q V over the 128 keys of V stage ST; P (bf16) read from TMEM columns [128 Q, 128 Q + 64)
+    constexpr uint32_t idP = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM) x V (MN-major)
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-        ptx::mma_ts_w(tmem + NQ * 128 + Q * 128, tmem + Q * 128 + HALF * 64 + kk * 8,
-                      ptx::sdesc_sw128(sVa + ST * kTileBytes + HALF * 64 * 128 + kk * 2048, kHalfBytes, 1024), idP,
+    for (int kk = 0; kk < 8; ++kk)
+        ptx::mma_ts_w(tmem + NQ * 128 + Q * 128, tmem + Q * 128 + kk * 8,
+                      ptx::sdesc_sw128(sVa + ST * kTileBytes + kk * 2048, kHalfBytes, 1024), idP,
                       (ACC || kk > 0) ? 1u : 0u);
 }
-template <int NQ, int Q, int HALF>
+template <int NQ, int Q>
 __device__ __forceinline__ void issue_S_q(int st, uint32_t tmem, uint32_t sQa, uint32_t sKa) {
     switch (st) {
-        case 0: issue_S_t<NQ, Q, HALF, 0>(tmem, sQa, sKa); break;
-        case 1: issue_S_t<NQ, Q, HALF, 1>(tmem, sQa, sKa); break;
-        default: issue_S_t<NQ, Q, HALF, 2>(tmem, sQa, sKa); break;
+        case 0: issue_S_t<NQ, Q, 0>(tmem, sQa, sKa); break;
+        case 1: issue_S_t<NQ, Q, 1>(tmem, sQa, sKa); break;
+        default: issue_S_t<NQ, Q, 2>(tmem, sQa, sKa); break;
     }
 }
 template <int NQ>
-__device__ __forceinline__ void issue_S_d(int q, int half, int st, uint32_t tmem, uint32_t sQa, uint32_t sKa) {
-    if (q == 0) {
-        if (half == 0) issue_S_q<NQ, 0, 0>(st, tmem, sQa, sKa); else issue_S_q<NQ, 0, 1>(st, tmem, sQa, sKa);
-    } else if constexpr (NQ > 1) {
-        if (half == 0) issue_S_q<NQ, 1, 0>(st, tmem, sQa, sKa); else issue_S_q<NQ, 1, 1>(st, tmem, sQa, sKa);
-    }
+__device__ __forceinline__ void issue_S_d(int q, int st, uint32_t tmem, uint32_t sQa, uint32_t sKa) {
+    if (q == 0) issue_S_q<NQ, 0>(st, tmem, sQa, sKa);
+    else if constexpr (NQ > 1) issue_S_q<NQ, 1>(st, tmem, sQa, sKa);
 }
-template <int NQ, int Q, int HALF, bool ACC>
+template <int NQ, int Q, bool ACC>
 __device__ __forceinline__ void issue_PV_q(int st, uint32_t tmem, uint32_t sVa) {
     switch (st) {
-        case 0: issue_PV_t<NQ, Q, HALF, 0, ACC>(tmem, sVa); break;
-        case 1: issue_PV_t<NQ, Q, HALF, 1, ACC>(tmem, sVa); break;
-        default: issue_PV_t<NQ, Q, HALF, 2, ACC>(tmem, sVa); break;
+        case 0: issue_PV_t<NQ, Q, 0, ACC>(tmem, sVa); break;
+        case 1: issue_PV_t<NQ, Q, 1, ACC>(tmem, sVa); break;
+        default: issue_PV_t<NQ, Q, 2, ACC>(tmem, sVa); break;
     }
 }
 template <int NQ>
-__device__ __forceinline__ void issue_PV_d(int q, int half, int st, bool acc, uint32_t tmem, uint32_t sVa) {
+__device__ __forceinline__ void issue_PV_d(int q, int st, bool acc, uint32_t tmem, uint32_t sVa) {
     if (q == 0) {
-        if (half == 1) issue_PV_q<NQ, 0, 1, true>(st, tmem, sVa);
-        else if (acc) issue_PV_q<NQ, 0, 0, true>(st, tmem, sVa);
-        else issue_PV_q<NQ, 0, 0, false>(st, tmem, sVa);
+        if (acc) issue_PV_q<NQ, 0, true>(st, tmem, sVa); else issue_PV_q<NQ, 0, false>(st, tmem, sVa);
     } else if constexpr (NQ > 1) {
-        if (half == 1) issue_PV_q<NQ, 1, 1, true>(st, tmem, sVa);
-        else if (acc) issue_PV_q<NQ, 1, 0, true>(st, tmem, sVa);
-        else issue_PV_q<NQ, 1, 0, false>(st, tmem, sVa);
+        if (acc) issue_PV_q<NQ, 1, true>(st, tmem, sVa); else issue_PV_q<NQ, 1, false>(st, tmem, sVa);
     }
 }
 
@@ -239,9 +287,9 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     Item it;
 
     if (warp < 4) {
-        // register split: the launch grants 168 x 384 = 64512 registers; 128 x 88 + 256 x 208 = 64512
-        // (setmaxnreg.inc blocks forever if the pool cannot cover it).
-        if constexpr (NQ == 2 && kSetMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+        // register split (kCtlRegs / kSoftmaxRegs): setmaxnreg.inc blocks forever if the pool cannot
+        // cover it, so the two budgets add up to exactly the launch grant.
+        if constexpr (NQ == 2 && kSetMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtlRegs));
         if (warp == 0) {
             // ============================ TMA producer: Q, K ============================
             ptx::tma_prefetch(&mapQ);
@@ -262,6 +310,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 const int64_t row0 = P.offsets[it.u];
                 for (int t = it.t0; t < it.t1; ++t) {
                     ptx::mbar_wait(&bars->k_empty[stage], phase ^ 1);
+                    if (k == 0 && lane == 0) VTRACE(8, t - it.t0, 0);
 #ifdef VISTA_EXP_NOLOAD  // experiment: keep re-using resident tiles (no HBM traffic after the first ones)
                     if (t >= it.t0 + C::kKStages) {
                         if (ptx::elect_one()) ptx::mbar_arrive(&bars->k_full[stage]);
@@ -285,11 +334,13 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             const uint64_t pol_kv = ptx::policy_evict_first();
             int stage = 0;
             uint32_t phase = 0;
+            bool first_item = true;
             while (iter.next(it)) {
                 const int h = it.hg / P.G;
                 const int64_t row0 = P.offsets[it.u];
                 for (int t = it.t0; t < it.t1; ++t) {
                     ptx::mbar_wait(&bars->v_empty[stage], phase ^ 1);
+                    if (first_item && lane == 0) VTRACE(9, t - it.t0, 0);
 #ifdef VISTA_EXP_NOLOAD
                     if (t >= it.t0 + C::kVStages) {
                         if (ptx::elect_one()) ptx::mbar_arrive(&bars->v_full[stage]);
@@ -305,71 +356,85 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                                          half * 64, h, row, pol_kv);
                     if (++stage == C::kVStages) { stage = 0; phase ^= 1; }
                 }
+                first_item = false;
             }
         } else if (warp == 1) {
             // ============================ MMA issuer ============================
-            // Work proceeds in half tiles h (64 keys): S_q(h) = Q_q K_h^T into S buffer h%2 of Q tile q,
-            // O_q += P_q(h) V_h.  Two S buffers per Q tile let S(h+1) be ready while the softmax works
-            // on S(h); issue order  PV_0(h) S_0(h+2) PV_1(h) S_1(h+2) ...
-            // The whole warp runs this loop and every MMA operand is a uniform base plus a compile-time
-            // offset (stage / half / q / k-step are template arguments), so ptxas keeps descriptors in
-            // uniform registers and the tcgen05.mma issue is a few instructions each.
+            // Per K/V tile t and Q tile q: S_q(t) = Q_q K_t^T (TMEM cols of q), softmax writes P_q(t)
+            // over it, O_q += P_q(t) V_t.  Issue order PV_0(t) S_0(t+1) PV_1(t) S_1(t+1): one Q tile's
+            // exponentials overlap the other's GEMMs, and the commit after S_q(t+1) also covers
+            // PV_q(t) (in-order completion), which is what lets a softmax thread rescale O_q.
+            // The whole warp runs this loop and every MMA operand is a uniform base plus a
+            // compile-time offset, so ptxas keeps descriptors in uniform registers.
             const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
             const uint32_t sQa = base + C::kQOff, sKa = base + C::kKOff, sVa = base + C::kVOff;
             int kst = 0, vst = 0;
             uint32_t kph = 0, vph = 0, q_phase = 0;
-            uint32_t p_phase[2][2] = {{0, 0}, {0, 0}};
+            uint32_t p_phase[2] = {0, 0};
+            bool first_item = true;
+#ifdef VISTA_TRACE
+            int item_no = 0;
+#endif
             while (iter.next(it)) {
                 const int ntiles = it.t1 - it.t0;
+#ifdef VISTA_TRACE
+                if (blockIdx.x == 0 && lane == 0 && item_no < 32) {
+                    g_vista_trace[10][item_no][0] = clock64();
+                    g_vista_trace[10][item_no][1] = ptx::globaltimer_ns();
+                    g_vista_trace[11][item_no][0] = (unsigned long long)ntiles;
+                }
+                ++item_no;
+#endif
                 ptx::mbar_wait(&bars->q_full, q_phase);
                 q_phase ^= 1;
                 ptx::mbar_wait(&bars->k_full[kst], kph);
                 ptx::tc_fence_after();
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
-                    issue_S_d<NQ>(q, 0, kst, tmem, sQa, sKa);
+                    issue_S_d<NQ>(q, kst, tmem, sQa, sKa);
                     ptx::mma_commit_w(&bars->s_full[q][0]);
-                    issue_S_d<NQ>(q, 1, kst, tmem, sQa, sKa);
-                    ptx::mma_commit_w(&bars->s_full[q][1]);
                 }
+                ptx::mma_commit_w(&bars->k_empty[kst]);  // K tile t0 fully consumed once these complete
+                if (++kst == C::kKStages) { kst = 0; kph ^= 1; }
                 for (int t = 0; t < ntiles; ++t) {
                     const bool more = t + 1 < ntiles;
                     ptx::mbar_wait(&bars->v_full[vst], vph);
                     ptx::tc_fence_after();
 #pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-#pragma unroll
-                        for (int q = 0; q < NQ; ++q) {
-                            ptx::mbar_wait(&bars->p_full[q][half], p_phase[q][half]);
-                            p_phase[q][half] ^= 1;
-                            ptx::tc_fence_after();
-                            issue_PV_d<NQ>(q, half, vst, half == 1 || t > 0, tmem, sVa);
-                            ptx::mma_commit_w(&bars->pv_done[q]);
-                            if (half == 1 && !more) ptx::mma_commit_w(&bars->o_full[q]);
-                            if (more) {
-                                if (q == 0 && half == 0) {
-                                    // every score GEMM of this K tile has been issued: release it, take the next
-                                    ptx::mma_commit_w(&bars->k_empty[kst]);
-                                    if (++kst == C::kKStages) { kst = 0; kph ^= 1; }
-                                    ptx::mbar_wait(&bars->k_full[kst], kph);
-                                    ptx::tc_fence_after();
-                                }
-                                issue_S_d<NQ>(q, half, kst, tmem, sQa, sKa);
-                                ptx::mma_commit_w(&bars->s_full[q][half]);
+                    for (int q = 0; q < NQ; ++q) {
+                        if (first_item && lane == 0) VTRACE(0, t, q);
+                        ptx::mbar_wait(&bars->p_full[q][0], p_phase[q]);
+                        if (first_item && lane == 0) VTRACE(1, t, q);
+                        p_phase[q] ^= 1;
+                        ptx::tc_fence_after();
+                        issue_PV_d<NQ>(q, vst, t > 0, tmem, sVa);
+                        if (!more) {
+                            ptx::mma_commit_w(&bars->o_full[q]);
+                        } else {
+                            if (q == 0) {
+                                ptx::mbar_wait(&bars->k_full[kst], kph);
+                                ptx::tc_fence_after();
+                            }
+                            issue_S_d<NQ>(q, kst, tmem, sQa, sKa);
+                            ptx::mma_commit_w(&bars->s_full[q][0]);
+                            if (first_item && lane == 0) VTRACE(2, t, q);
+                            if (q == NQ - 1) {
+                                ptx::mma_commit_w(&bars->k_empty[kst]);
+                                if (++kst == C::kKStages) { kst = 0; kph ^= 1; }
                             }
                         }
                     }
                     ptx::mma_commit_w(&bars->v_empty[vst]);
                     if (++vst == C::kVStages) { vst = 0; vph ^= 1; }
                 }
-                ptx::mma_commit_w(&bars->k_empty[kst]);  // last K tile of the item
-                if (++kst == C::kKStages) { kst = 0; kph ^= 1; }
                 ptx::mma_commit_w(&bars->q_empty);
+                first_item = false;
             }
+            (void)first_item;
         }
         __syncwarp();
     } else {
-        if constexpr (NQ == 2 && kSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+        if constexpr (NQ == 2 && kSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
         // ============================ softmax warpgroups ============================
         const int wg = (warp - 4) / 4;  // warps 4..7 -> Q tile 0, 8..11 -> Q tile 1
         const int wq = warp % 4;
@@ -378,103 +443,84 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
         const uint32_t tS = tmem + lane_bits + wg * 128;
         const uint32_t tO = tmem + lane_bits + NQ * 128 + wg * 128;
         const float sl2 = P.scale_log2;
-        uint32_t s_phase[2] = {0, 0}, o_phase = 0;
-        uint32_t pv_base = 0;  // PV GEMMs of this Q tile issued before the current item
+        uint32_t s_phase = 0, o_phase = 0;
+        bool first_item = true;
         while (iter.next(it)) {
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
-            const int nh = 2 * (it.t1 - it.t0);
             float m_used = -INFINITY, l = 0.f;
-            for (int h = 0; h < nh; ++h) {
-                const int b = h & 1;
-                ptx::mbar_wait(&bars->s_full[wg][b], s_phase[b]);
-                s_phase[b] ^= 1;
+            for (int t = it.t0; t < it.t1; ++t) {
+                const bool tr = first_item && row == 0;
+                if (tr) VTRACE(3, t - it.t0, wg);
+                ptx::mbar_wait(&bars->s_full[wg][0], s_phase);
+                if (tr) VTRACE(4, t - it.t0, wg);
+                s_phase ^= 1;
                 ptx::tc_fence_after();
-                uint32_t r[2][32];
-                ptx::tmem_ld32(tS + b * 64, r[0]);
-                ptx::tmem_ld32(tS + b * 64 + 32, r[1]);
+                uint32_t r[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + c * 32, r[c]);
                 ptx::tmem_wait_ld();
-                ptx::reg_fence(r[0]);
-                ptx::reg_fence(r[1]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ptx::reg_fence(r[c]);
+                if (tr) VTRACE(5, t - it.t0, wg);
 #ifdef VISTA_EXP_NOSOFTMAX  // experiment: skip the softmax math (P = stale TMEM contents)
                 if (true) {
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive(&bars->p_full[wg][b]);
+                    ptx::mbar_arrive(&bars->p_full[wg][0]);
                     l = 1.f;
                     m_used = 0.f;
                     continue;
                 }
 #endif
-                const int64_t valid = L - ((int64_t)(it.t0 + (h >> 1)) * kTile + b * 64);
-                if (valid < 64) {
+                const int64_t valid = L - (int64_t)t * kTile;
+                const bool full = valid >= kTile;
+                if (!full) {
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
+                    for (int c = 0; c < 4; ++c)
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             if (c * 32 + j >= valid) r[c][j] = __float_as_uint(-INFINITY);
                 }
-                // row max: 4 independent FMNMX3 chains, then a small tree
-                float m4[4];
+                // row max: 8 independent FMNMX3 chains, then a small tree
+                float m8[8];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
+                for (int a = 0; a < 8; ++a) {
                     const int c = a >> 1, o = (a & 1) * 16;
                     float m = ptx::max3(__uint_as_float(r[c][o]), __uint_as_float(r[c][o + 1]),
                                         __uint_as_float(r[c][o + 2]));
 #pragma unroll
                     for (int j = 3; j < 15; j += 2)
                         m = ptx::max3(m, __uint_as_float(r[c][o + j]), __uint_as_float(r[c][o + j + 1]));
-                    m4[a] = fmaxf(m, __uint_as_float(r[c][o + 15]));
+                    m8[a] = fmaxf(m, __uint_as_float(r[c][o + 15]));
                 }
-                const float mxs = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
+                const float mxs = ptx::max3(ptx::max3(m8[0], m8[1], m8[2]), ptx::max3(m8[3], m8[4], m8[5]),
+                                            fmaxf(m8[6], m8[7])) * sl2;
                 const bool need = mxs > m_used + kRescaleThreshold;
-                if (__any_sync(0xffffffffu, need)) {
-                    const float m_new = fmaxf(m_used, mxs);
-                    if (h > 0) {
-                        // O_q must hold PV(h-1) before it is rescaled.  S(h) was committed after PV(h-2), so
-                        // at most one PV completion is outstanding and the parity wait is unambiguous.
-                        ptx::mbar_wait(&bars->pv_done[wg], (pv_base + h - 1) & 1);
-                        ptx::tc_fence_after();
-                        const float f = ptx::ex2(m_used - m_new);
-                        l *= f;
+                const bool any = __any_sync(0xffffffffu, need);
+                const float m_old = m_used;
+                if (any) m_used = fmaxf(m_used, mxs);
+                // P = 2^(S scale log2e - m) over S_q (exp_tile); FMA-pipe exp2 only on unmasked tiles
+                const float lt = full ? exp_tile<kEmuPerEight>(r, sl2, -m_used, tS) : exp_tile<0>(r, sl2, -m_used, tS);
+                if (tr) VTRACE(6, t - it.t0, wg);
+                if (any && t > it.t0) {
+                    // O_q holds this item's sum so far: PV_q(t-1) completed (covered by s_full(t))
+                    const float f = ptx::ex2(m_old - m_used);
+                    l *= f;
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            uint32_t o[32];
-                            ptx::tmem_ld32_sync(tO + c * 32, o);
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t o[32];
+                        ptx::tmem_ld32_sync(tO + c * 32, o);
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
-                            ptx::tmem_st32(tO + c * 32, o);
-                        }
+                        for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
+                        ptx::tmem_st32(tO + c * 32, o);
                     }
-                    m_used = m_new;
                 }
-                // p = 2^(s * scale * log2 e - m): packed FFMA2, MUFU ex2, bf16x2 pack into the first
-                // 32 columns of this S buffer (P aliases S; the next S into it is issued after PV reads P)
-                const uint64_t sl2x2 = ptx::f2_pack(sl2, sl2);
-                const uint64_t negx2 = ptx::f2_pack(-m_used, -m_used);
-                uint64_t acc[2] = {ptx::f2_pack(0.f, 0.f), ptx::f2_pack(0.f, 0.f)};
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const uint64_t x2 = ptx::f2_fma(
-                            ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
-                        float x0, x1;
-                        ptx::f2_unpack(x2, x0, x1);
-                        const float p0 = ptx::ex2(x0), p1 = ptx::ex2(x1);
-                        acc[j & 1] = ptx::f2_add(acc[j & 1], ptx::f2_pack(p0, p1));
-                        pk[j] = ptx::pack_bf16x2(p0, p1);
-                    }
-                    ptx::tmem_st16(tS + b * 64 + c * 16, pk);
-                }
-                float la, lb, lc, ld;
-                ptx::f2_unpack(acc[0], la, lb);
-                ptx::f2_unpack(acc[1], lc, ld);
-                l += (la + lb) + (lc + ld);
+                l += lt;
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&bars->p_full[wg][b]);
+                ptx::mbar_arrive(&bars->p_full[wg][0]);
+                if (tr) VTRACE(7, t - it.t0, wg);
             }
-            pv_base += (uint32_t)nh;
+            first_item = false;
             // epilogue: O / l, lse
             ptx::mbar_wait(&bars->o_full[wg], o_phase);
             o_phase ^= 1;
@@ -494,6 +540,12 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+#ifdef VISTA_TRACE
+    if (threadIdx.x == 0) {
+        g_vista_trace[11][32 + (blockIdx.x & 31)][0] = clock64();
+        g_vista_trace[11][32 + (blockIdx.x & 31)][1] = ptx::globaltimer_ns();
+    }
+#endif
     if (warp == 1) ptx::tmem_dealloc(tmem, C::kTmemCols);
 }
 
@@ -572,6 +624,12 @@ static cudaError_t launch_nq(const Problem& p, const Workspace& w, char* ws) {
 }
 
 int sm100_softmax_nq(int S) { return (S % 256 == 0) ? 2 : 1; }
+
+#ifdef VISTA_TRACE
+extern "C" int vista_debug_trace(void* host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, g_vista_trace, bytes < sizeof(g_vista_trace) ? bytes : sizeof(g_vista_trace));
+}
+#endif
 
 cudaError_t launch_sm100_softmax(const Problem& p, const Workspace& w, char* ws) {
     return sm100_softmax_nq(p.S) == 2 ? launch_nq<2>(p, w, ws) : launch_nq<1>(p, w, ws);

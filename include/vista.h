@@ -131,6 +131,9 @@ vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, 
                                        float* part_o, float* part_lse, void* workspace,
                                        size_t workspace_bytes, void* stream);
 
+/* Bytes of device workspace vista_summarize_merge needs for this descriptor (0 for softmax). */
+vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes);
+
 /*
  * Merge num_parts >= 1 partials stacked along a leading axis (e.g. an all_gather output):
  *   softmax: part_o [P,B,H,S,d], part_lse [P,B,H,S] -> out [B,S,H,d], lse [B,H,S] (lse may be
@@ -138,11 +141,13 @@ vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, 
  *            parts with lse_p = -inf weigh 0; all -inf -> out 0, lse -inf.
  *   QLA:     part_o [P,B,H,d,d] -> Z = sum_p Z_p (ascending p), then finalize with q and
  *            user_len [B] (int64, device; total L_u over all parts, used when qla_normalize).
- * q and user_len are read for QLA only (may be NULL for softmax).
+ * q and user_len are read for QLA only (may be NULL for softmax).  workspace: at least
+ * vista_summarize_merge_workspace_size bytes (may be NULL when that is 0).
  */
 vista_status_t vista_summarize_merge(const vista_desc_t* desc, int32_t num_parts,
                                      const float* part_o, const float* part_lse, const void* q,
-                                     const int64_t* user_len, void* out, float* lse, void* stream);
+                                     const int64_t* user_len, void* out, float* lse,
+                                     void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Debug: copies offsets to the host (synchronizes `stream`) and checks offsets[0] = 0,

@@ -22,6 +22,7 @@ __all__ = [
     "VistaError", "Desc", "load", "lib_path", "make_desc",
     "vista_abi_version", "vista_status_string", "vista_summarize_workspace_size",
     "vista_summarize_fwd", "vista_summarize_partial", "vista_summarize_merge",
+    "vista_summarize_merge_workspace_size",
     "vista_check_offsets", "vista_dispatch_name", "vista_time_next_main_kernel", "vista_launch_counter",
     "summarize", "summarize_partial", "summarize_merge",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
@@ -88,7 +89,9 @@ def load():
     lib.vista_summarize_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
     lib.vista_summarize_fwd.argtypes = [DP, P, P, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_partial.argtypes = [DP, P, P, P, P, i64, P, P, P, sz, P]
-    lib.vista_summarize_merge.argtypes = [DP, i32, P, P, P, P, P, P, P]
+    lib.vista_summarize_merge.argtypes = [DP, i32, P, P, P, P, P, P, P, sz, P]
+    lib.vista_summarize_merge_workspace_size.argtypes = [DP, ctypes.POINTER(sz)]
+    lib.vista_summarize_merge_workspace_size.restype = ctypes.c_int
     lib.vista_check_offsets.argtypes = [P, i32, i64, P]
     lib.vista_time_next_main_kernel.argtypes = [P, P]
     lib.vista_time_next_main_kernel.restype = ctypes.c_int
@@ -160,10 +163,18 @@ def vista_summarize_partial(desc, q, k, v, offsets, total_len, part_o, part_lse,
                                           int(workspace_bytes), _stream(stream)), "vista_summarize_partial")
 
 
-def vista_summarize_merge(desc, num_parts, part_o, part_lse, q, user_len, out, lse, stream=None):
+def vista_summarize_merge_workspace_size(desc: Desc) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load().vista_summarize_merge_workspace_size(ctypes.byref(desc), ctypes.byref(n)),
+           "vista_summarize_merge_workspace_size")
+    return n.value
+
+
+def vista_summarize_merge(desc, num_parts, part_o, part_lse, q, user_len, out, lse, workspace=None,
+                          workspace_bytes=0, stream=None):
     _check(load().vista_summarize_merge(ctypes.byref(desc), int(num_parts), _ptr(part_o), _ptr(part_lse),
-                                        _ptr(q), _ptr(user_len), _ptr(out), _ptr(lse), _stream(stream)),
-           "vista_summarize_merge")
+                                        _ptr(q), _ptr(user_len), _ptr(out), _ptr(lse), _ptr(workspace),
+                                        int(workspace_bytes), _stream(stream)), "vista_summarize_merge")
 
 
 def vista_check_offsets(offsets, num_users, total_len, stream=None):
@@ -271,5 +282,7 @@ def summarize_merge(part_o, part_lse, *, q, attn=SOFTMAX, user_len=None, scale=N
     odt = torch.bfloat16 if desc.out_dtype == BF16 else torch.float32
     out = torch.empty((B, S, H, d), dtype=odt, device=part_o.device)
     lse = torch.empty((B, H, S), dtype=torch.float32, device=part_o.device) if attn == SOFTMAX else None
-    vista_summarize_merge(desc, P, part_o, part_lse, q, user_len, out, lse, stream)
+    need = vista_summarize_merge_workspace_size(desc)
+    ws = torch.empty(max(need, 16), dtype=torch.uint8, device=part_o.device) if need else None
+    vista_summarize_merge(desc, P, part_o, part_lse, q, user_len, out, lse, ws, need, stream)
     return out, lse

@@ -41,7 +41,7 @@ struct Problem {
 
 // Workspace carve-up (all offsets 256-B aligned).
 struct Workspace {
-    size_t uts_off, slot_unit_off, slot_o_off, slot_lse_off, zbuf_off, total;
+    size_t uts_off, slot_unit_off, slot_o_off, slot_lse_off, zbuf_off, fin_off, total;
     int num_ctas;      // persistent grid size used by the tiled kernels
     int rows_per_unit; // softmax: query rows per work unit (NQ * 128); QLA: d
 };
@@ -64,7 +64,12 @@ cudaError_t launch_simt_qla_state(const Problem& p, float* zbuf);
 // O = phi1(Q) phi2( (sum_{p<P} Z_p) / N_u ) ; Z parts at zparts + p * part_stride (floats),
 // N_u from offsets (user_len == NULL) or user_len[u].
 cudaError_t launch_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
-                                const int64_t* user_len);
+                                const int64_t* user_len, void* ws);
+bool qla_finalize_uses_tc(const Problem& p);
+// tensor-core finalize (bf16, d = 128); ws: sm100_qla_finalize_workspace(p) bytes
+size_t sm100_qla_finalize_workspace(const Problem& p);
+cudaError_t launch_sm100_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
+                                      const int64_t* user_len, void* ws);
 // Merge P stacked softmax partials [P,B,H,S,d] / [P,B,H,S] into outs.
 cudaError_t launch_merge_softmax_parts(const Problem& p, int P, const float* part_o, const float* part_lse);
 

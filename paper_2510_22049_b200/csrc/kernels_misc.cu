@@ -454,8 +454,12 @@ static cudaError_t finalize_d(const Problem& p, const float* zparts, int P, int6
         p.phi2, p.normalize, p.outs);
     return cudaGetLastError();
 }
+bool qla_finalize_uses_tc(const Problem& p) { return p.in_bf16 && p.d == 128 && (p.q_user_stride % 8) == 0; }
+
 cudaError_t launch_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
-                                const int64_t* user_len) {
+                                const int64_t* user_len, void* ws) {
+    if (qla_finalize_uses_tc(p))  // tensor-core finalize (sm100_qla_finalize.cu)
+        return launch_sm100_qla_finalize(p, zparts, P, part_stride, user_len, ws);
     if (p.in_bf16) {
         switch (p.d) {
             case 32: return finalize_d<32, __nv_bfloat16>(p, zparts, P, part_stride, user_len);

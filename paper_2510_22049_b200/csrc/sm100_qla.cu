@@ -65,6 +65,81 @@ __device__ __forceinline__ uint32_t phi_bf16x2(int kind, uint32_t w) {
     return ptx::pack_bf16x2(phi(kind, lo), phi(kind, hi));
 }
 
+// SiLU on a bf16x2 pair with packed bf16 math: x * (0.5 + 0.5 tanh(x / 2)) -- 4 instructions per
+// pair (HMUL2, MUFU.TANH bf16x2, HFMA2, HMUL2).  The result is bf16 anyway (it is the MMA operand).
+__device__ __forceinline__ uint32_t silu_bf16x2(uint32_t x) {
+    uint32_t h, t, s, y;
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(h) : "r"(x), "r"(0x3F003F00u));
+    asm("tanh.approx.bf16x2 %0, %1;" : "=r"(t) : "r"(h));
+    asm("fma.rn.bf16x2 %0, %1, %2, %2;" : "=r"(s) : "r"(t), "r"(0x3F003F00u));
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(y) : "r"(x), "r"(s));
+    return y;
+}
+
+template <int PHI>
+__device__ __forceinline__ uint32_t phi2x(uint32_t w) {
+    if constexpr (PHI == VISTA_ACT_SILU) return silu_bf16x2(w);
+    else if constexpr (PHI == VISTA_ACT_SHIFTED_ELU) return phi_bf16x2(VISTA_ACT_SHIFTED_ELU, w);
+    else return w;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// phi1 over one 128 x 128 bf16 K tile in shared memory (in place, layout-agnostic: the 128-B
+// swizzle only permutes 16-B chunks within a row), rows >= valid zeroed AFTER activation.
+// 256 threads x 8 chunks of 16 B; all loads first for ILP.
+template <int PHI>
+__device__ __forceinline__ void phi_tile(uint32_t tile, int xt, int64_t valid) {
+    uint4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = lds128(tile + (uint32_t)(xt + i * 256) * 16);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int c = xt + i * 256;
+        const int j = (c & 1023) >> 3;  // 128-B line = history row within the tile
+        if (j >= valid) {
+            v[i] = make_uint4(0, 0, 0, 0);
+        } else if constexpr (PHI != VISTA_ACT_IDENTITY) {
+            v[i].x = phi2x<PHI>(v[i].x);
+            v[i].y = phi2x<PHI>(v[i].y);
+            v[i].z = phi2x<PHI>(v[i].z);
+            v[i].w = phi2x<PHI>(v[i].w);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sts128(tile + (uint32_t)(xt + i * 256) * 16, v[i]);
+}
+
+// Z (+)= phi1(K)^T V for one staged tile: A = phi1(K) [j][c1] read as MN-major (M = c1),
+// B = V [j][c2] MN-major (N = c2); 8 k-steps of 16 history rows.  Compile-time stage / buffer so
+// the descriptors stay in uniform registers (see sm100_softmax.cu).
+template <int ZB, int ST>
+__device__ __forceinline__ void issue_Z_t(uint32_t tmem, uint32_t base, bool acc) {
+    constexpr uint32_t idZ = ptx::idesc_bf16_f32(128, 128, 1, 1);
+    const uint32_t ka = base + ST * kStageBytes, va = ka + kTileBytes;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+        ptx::mma_ss_w(tmem + ZB * 128, ptx::sdesc_sw128(ka + kk * 2048, kHalfBytes, 1024),
+                      ptx::sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), idZ, (acc || kk > 0) ? 1u : 0u);
+}
+template <int ZB>
+__device__ __forceinline__ void issue_Z_s(int st, uint32_t tmem, uint32_t base, bool acc) {
+    switch (st) {
+        case 0: issue_Z_t<ZB, 0>(tmem, base, acc); break;
+        case 1: issue_Z_t<ZB, 1>(tmem, base, acc); break;
+        default: issue_Z_t<ZB, 2>(tmem, base, acc); break;
+    }
+}
+
+template <int PHI1>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_qla_state_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                            const Params P) {
@@ -101,75 +176,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = bars->tmem_base;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
 
     ItemIter iter;
     iter.init(P.uts, P.B, HG, cta, num_ctas);
     Item it;
 
     if (warp == 0) {
-        if (lane == 0) {
-            ptx::tma_prefetch(&mapK);
-            ptx::tma_prefetch(&mapV);
-            const uint64_t pol = ptx::policy_evict_first();
-            int stage = 0;
-            uint32_t phase = 0;
-            while (iter.next(it)) {
-                const int h = it.hg;
-                const int64_t row0 = P.offsets[it.u];
-                for (int t = it.t0; t < it.t1; ++t) {
-                    ptx::mbar_wait(&bars->kv_empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&bars->kv_full[stage], kStageBytes);
-                    uint8_t* sk = smem + stage * kStageBytes;
-                    const int32_t row = (int32_t)(row0 + (int64_t)t * kTile);
-                    for (int half = 0; half < 2; ++half) {
-                        ptx::tma_load_3d(sk + half * kHalfBytes, &mapK, &bars->kv_full[stage], half * 64, h, row, pol);
-                        ptx::tma_load_3d(sk + kTileBytes + half * kHalfBytes, &mapV, &bars->kv_full[stage], half * 64,
-                                         h, row, pol);
-                    }
-                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+        // ============================ TMA producer (warp-wide, one elected lane issues) ============
+        ptx::tma_prefetch(&mapK);
+        ptx::tma_prefetch(&mapV);
+        const uint64_t pol = ptx::policy_evict_first();
+        int stage = 0;
+        uint32_t phase = 0;
+        while (iter.next(it)) {
+            const int h = it.hg;
+            const int64_t row0 = P.offsets[it.u];
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->kv_empty[stage], phase ^ 1);
+                ptx::mbar_arrive_expect_tx_w(&bars->kv_full[stage], kStageBytes);
+                uint8_t* sk = smem + stage * kStageBytes;
+                const int32_t row = (int32_t)(row0 + (int64_t)t * kTile);
+                for (int half = 0; half < 2; ++half) {
+                    ptx::tma_load_3d_w(sk + half * kHalfBytes, &mapK, &bars->kv_full[stage], half * 64, h, row, pol);
+                    ptx::tma_load_3d_w(sk + kTileBytes + half * kHalfBytes, &mapV, &bars->kv_full[stage], half * 64,
+                                       h, row, pol);
                 }
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
         }
-        __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idZ = ptx::idesc_bf16_f32(128, 128, 1, 1);  // A, B both MN-major
-            const uint32_t base = ptx::smem_u32(smem);
-            int stage = 0;
-            uint32_t phase = 0;
-            uint32_t zuse[2] = {0, 0};
-            int k = 0;
-            while (iter.next(it)) {
-                const int zb = k & 1;
-                ptx::mbar_wait(&bars->z_empty[zb], (zuse[zb] & 1) ^ 1);
-                ++zuse[zb];
-                const uint32_t dz = tmem + zb * 128;
-                for (int t = it.t0; t < it.t1; ++t) {
-                    ptx::mbar_wait(&bars->k_ready[stage], phase);
-                    ptx::tc_fence_after();
-                    const uint32_t ka = base + stage * kStageBytes, va = ka + kTileBytes;
+        // ============================ MMA issuer (warp-wide) ============================
+        const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+        int stage = 0;
+        uint32_t phase = 0;
+        uint32_t zuse[2] = {0, 0};
+        int k = 0;
+        while (iter.next(it)) {
+            const int zb = k & 1;
+            ptx::mbar_wait(&bars->z_empty[zb], (zuse[zb] & 1) ^ 1);
+            ++zuse[zb];
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->k_ready[stage], phase);
+                ptx::tc_fence_after();
 #ifndef VISTA_EXP_QLA_NOMMA
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk)
-                        ptx::mma_ss(dz, ptx::sdesc_sw128(ka + kk * 2048, kHalfBytes, 1024),
-                                    ptx::sdesc_sw128(va + kk * 2048, kHalfBytes, 1024), idZ,
-                                    (t > it.t0 || kk > 0) ? 1u : 0u);
+                if (zb == 0) issue_Z_s<0>(stage, tmem, base, t > it.t0);
+                else issue_Z_s<1>(stage, tmem, base, t > it.t0);
 #endif
-                    ptx::mma_commit(&bars->kv_empty[stage]);
-                    if (++stage == kStages) { stage = 0; phase ^= 1; }
-                }
-                ptx::mma_commit(&bars->z_full[zb]);
-                ++k;
+                ptx::mma_commit_w(&bars->kv_empty[stage]);
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
+            ptx::mma_commit_w(&bars->z_full[zb]);
+            ++k;
         }
-        __syncwarp();
     } else if (warp >= 4) {
         const int xt = threadIdx.x - 128;  // 0 .. 255
         const int wq = warp % 4;
         const int chalf = (warp - 4) / 4;  // epilogue: columns [64*chalf, 64*chalf + 64)
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
-        const int phi1 = P.phi1;
+        const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
         int stage = 0;
         uint32_t phase = 0;
         uint32_t zphase[2] = {0, 0};
@@ -179,26 +244,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->kv_full[stage], phase);
                 const int64_t valid = L - (int64_t)t * kTile;
-                uint4* sk = reinterpret_cast<uint4*>(smem + stage * kStageBytes);
 #ifdef VISTA_EXP_QLA_NOXFORM
                 if (false) {
 #else
-                if (phi1 != VISTA_ACT_IDENTITY || valid < kTile) {
+                if (PHI1 != VISTA_ACT_IDENTITY || valid < kTile) {
 #endif
-#pragma unroll 4
-                    for (int c = xt; c < kTileBytes / 16; c += kXformWarps * 32) {
-                        const int j = (c & 1023) >> 3;  // 128-B line = history row within the tile
-                        uint4 x = sk[c];
-                        if (j >= valid) {
-                            x = make_uint4(0, 0, 0, 0);
-                        } else if (phi1 != VISTA_ACT_IDENTITY) {
-                            x.x = phi_bf16x2(phi1, x.x);
-                            x.y = phi_bf16x2(phi1, x.y);
-                            x.z = phi_bf16x2(phi1, x.z);
-                            x.w = phi_bf16x2(phi1, x.w);
-                        }
-                        sk[c] = x;
-                    }
+                    phi_tile<PHI1>(base + stage * kStageBytes, xt, valid);
                     ptx::fence_proxy_async_smem();
                 }
                 ptx::mbar_arrive(&bars->k_ready[stage]);
@@ -235,6 +286,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
+template <int PHI1>
+static cudaError_t launch_phi(const Problem& p, const Workspace& w, const CUtensorMap& mk, const CUtensorMap& mv,
+                              const Params& P) {
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(sm100_qla_state_kernel<PHI1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (attr != cudaSuccess) return attr;
+    sm100_qla_state_kernel<PHI1><<<w.num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf) {
     CUtensorMap mk, mv;
     if (!make_kv_map(&mk, p.k, p.total_len, p.H) || !make_kv_map(&mv, p.v, p.total_len, p.H))
@@ -248,11 +309,9 @@ cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* w
     P.B = p.B;
     P.H = p.H;
     P.phi1 = p.phi1;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(sm100_qla_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (attr != cudaSuccess) return attr;
-    sm100_qla_state_kernel<<<w.num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P);
-    return cudaGetLastError();
+    return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU>(p, w, mk, mv, P)
+         : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU>(p, w, mk, mv, P)
+                                           : launch_phi<VISTA_ACT_IDENTITY>(p, w, mk, mv, P);
 }
 
 }  // namespace vista

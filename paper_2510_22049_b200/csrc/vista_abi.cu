@@ -126,6 +126,8 @@ Workspace plan_workspace(const Problem& p, bool partial) {
     off = align256(off + (size_t)2 * w.num_ctas * w.rows_per_unit * sizeof(float));
     w.zbuf_off = off;
     if (p.attn == VISTA_QLA) off = align256(off + (size_t)p.B * p.H * p.d * p.d * sizeof(float));
+    w.fin_off = off;
+    if (p.attn == VISTA_QLA && qla_finalize_uses_tc(p)) off = align256(off + sm100_qla_finalize_workspace(p));
     w.total = off;
     return w;
 }
@@ -213,7 +215,7 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
             if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), zbuf)) != cudaSuccess) break;
             if ((e = timed_main(p.stream, [&] { return launch_sm100_qla_state(p, w, ws, zbuf); })) != cudaSuccess) break;
             if ((e = launch_merge_qla_slots(p, w, ws, zbuf)) != cudaSuccess) break;
-            if (!partial) e = launch_qla_finalize(p, zbuf, 1, 0, nullptr);
+            if (!partial) e = launch_qla_finalize(p, zbuf, 1, 0, nullptr, ws + w.fin_off);
             nlaunch = partial ? 3 : 4;
             break;
         }
@@ -224,7 +226,7 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
         case PATH_SIMT_QLA: {
             float* zbuf = partial ? reinterpret_cast<float*>(outs.out) : reinterpret_cast<float*>(ws + w.zbuf_off);
             if ((e = timed_main(p.stream, [&] { return launch_simt_qla_state(p, zbuf); })) != cudaSuccess) break;
-            if (!partial) e = launch_qla_finalize(p, zbuf, 1, 0, nullptr);
+            if (!partial) e = launch_qla_finalize(p, zbuf, 1, 0, nullptr, ws + w.fin_off);
             nlaunch = partial ? 1 : 2;
             break;
         }
@@ -251,9 +253,21 @@ vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, 
     return run(desc, q, k, v, offsets, total_len, o, workspace, workspace_bytes, stream);
 }
 
+static size_t merge_ws_bytes(const Problem& p) {
+    return (p.attn == VISTA_QLA && qla_finalize_uses_tc(p)) ? sm100_qla_finalize_workspace(p) : 0;
+}
+
+vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (!bytes) return VISTA_ERR_NULL;
+    *bytes = merge_ws_bytes(make_problem(desc, 0));
+    return VISTA_OK;
+}
+
 vista_status_t vista_summarize_merge(const vista_desc_t* desc, int32_t num_parts, const float* part_o,
                                      const float* part_lse, const void* q, const int64_t* user_len, void* out,
-                                     float* lse, void* stream) {
+                                     float* lse, void* workspace, size_t workspace_bytes, void* stream) {
     vista_status_t st = validate_desc(desc);
     if (st != VISTA_OK) return st;
     if (num_parts < 1) return VISTA_ERR_INVALID;
@@ -266,11 +280,14 @@ vista_status_t vista_summarize_merge(const vista_desc_t* desc, int32_t num_parts
     p.outs = OutSpec{OUT_FINAL, desc->out_dtype == VISTA_BF16, out, desc->attn == VISTA_SOFTMAX ? lse : nullptr};
     p.stream = reinterpret_cast<cudaStream_t>(stream);
     if (p.B == 0) return VISTA_OK;
+    const size_t need = merge_ws_bytes(p);
+    if (need > 0 && (!workspace || workspace_bytes < need)) return VISTA_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
     cudaError_t e;
     if (desc->attn == VISTA_SOFTMAX) {
         e = launch_merge_softmax_parts(p, num_parts, part_o, part_lse);
     } else {
-        e = launch_qla_finalize(p, part_o, num_parts, (int64_t)p.B * p.H * p.d * p.d, user_len);
+        e = launch_qla_finalize(p, part_o, num_parts, (int64_t)p.B * p.H * p.d * p.d, user_len, workspace);
     }
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches += 1;

@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--attn", default="softmax", choices=["softmax", "qla"])
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--mode", default=None, choices=["by_user", "by_length", "flat"],
+                    help="multi-GPU partitioner (default per config: c2/c3 by_user, c4 by_length, c5 flat)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -132,26 +134,80 @@ def run_own(args, rank, world, local_rank):
     import synth
 
     vista.load()
+    from paper_2510_22049_b200 import dist as vdist
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
     attn = vista.SOFTMAX if args.attn == "softmax" else vista.QLA
-    # by-user sharding: rank r summarizes its own batch (seed r); identical shape on every rank
-    q, K, V, off = synth.make_batch(lens, S, H, d, seed=rank, backend="torch", device=dev)
-    total = int(off[-1])
-    off_t = torch.from_numpy(off).to(dev)
-    B = len(lens)
-    desc = vista.make_desc(B, S, H, d, in_dtype=vista.BF16, out_dtype=vista.BF16, attn=attn)
-    path = vista.vista_dispatch_name(desc)
-    ws_bytes = vista.vista_summarize_workspace_size(desc, total)
-    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
-    out = torch.empty((B, S, H, d), dtype=torch.bfloat16, device=dev)
-    lse = torch.empty((B, H, S), dtype=torch.float32, device=dev) if attn == vista.SOFTMAX else None
+    mode = args.mode or {"c2": "by_user", "c3": "by_user", "c4": "by_length", "c5": "flat"}[args.config]
+    if world == 1 and mode != "by_user":
+        mode = "by_user"  # one shard: the split-L paths degenerate to the plain forward
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
+    B_all = len(lens)
+    off_all = synth.offsets_from_lengths(lens)
+    if mode == "by_user":
+        # weak scaling: rank r summarizes its own batch of the configured shape (seed r)
+        q, K, V, off = synth.make_batch(lens, S, H, d, seed=rank, backend="torch", device=dev)
+        total = int(off[-1])
+        off_t = torch.from_numpy(off).to(dev)
+        B = len(lens)
+        desc = vista.make_desc(B, S, H, d, in_dtype=vista.BF16, out_dtype=vista.BF16, attn=attn)
+        ws_bytes = vista.vista_summarize_workspace_size(desc, total)
+        ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+        out = torch.empty((B, S, H, d), dtype=torch.bfloat16, device=dev)
+        lse = torch.empty((B, H, S), dtype=torch.float32, device=dev) if attn == vista.SOFTMAX else None
+        inputs = [q, K, V, off_t]
 
-    def step():
-        vista.vista_summarize_fwd(desc, q, K, V, off_t, total, out, lse, ws, ws_bytes, sh)
+        def step(ins=inputs):
+            vista.vista_summarize_fwd(desc, ins[0], ins[1], ins[2], ins[3], total, out, lse, ws, ws_bytes, sh)
+            return [out] + ([lse] if lse is not None else [])
+        items_per_step = world * total
+        scaling = "weak"
+        parallel = f"by_user x{world} (weak: a {args.config} batch per GPU, no data-path collective)"
+    else:
+        # strong scaling: one batch of the configured shape split across the ranks
+        q = synth.make_q(S, H, d, seed=0, backend="torch", device=dev)
+        if mode == "by_length":
+            cuts = vdist.partition_by_length(lens, world)
+            seg = [(u, int(cuts[rank, u]), int(cuts[rank + 1, u])) for u in range(B_all)]
+        else:
+            seg = [(s.user, s.start, s.end) for s in vdist.partition_flat(lens, world)[rank]]
+            all_segs = vdist.partition_flat(lens, world)
+        seg_len = np.array([e - a for _, a, e in seg], dtype=np.int64)
+        soff = synth.offsets_from_lengths(seg_len)
+        total = int(soff[-1])
+        tdt = torch.bfloat16
+        K = torch.empty((total, H, d), dtype=tdt, device=dev)
+        V = torch.empty((total, H, d), dtype=tdt, device=dev)
+        off_dev = torch.from_numpy(off_all).to(dev)
+        for n, (u, a0, e0) in enumerate(seg):  # generate this rank's rows (global row ids)
+            for r0 in range(a0, e0, 1 << 18):
+                r1 = min(e0, r0 + (1 << 18))
+                rows = torch.arange(int(off_all[u]) + r0, int(off_all[u]) + r1, dtype=torch.int64, device=dev)
+                users = torch.full_like(rows, u)
+                k, v = synth.make_kv(rows, users, H, d, seed=0, backend="torch", device=dev)
+                K[int(soff[n]) + r0 - a0:int(soff[n]) + r1 - a0] = k
+                V[int(soff[n]) + r0 - a0:int(soff[n]) + r1 - a0] = v
+        soff_t = torch.from_numpy(soff).to(dev)
+        ulen = torch.from_numpy(np.asarray(lens, dtype=np.int64)).to(dev)
+        inputs = [q, K, V, soff_t]
+        if mode == "by_length":
+            def step(ins=inputs):
+                out, lse = vdist.summarize_by_length(ins[0], ins[1], ins[2], ins[3], ulen, attn=args.attn,
+                                                     total_len=total)
+                return [out] + ([lse] if lse is not None else [])
+        else:
+            segs_obj = [vdist.Segment(u, a0, e0) for u, a0, e0 in seg]
+
+            def step(ins=inputs):
+                res = vdist.summarize_flat(ins[0], ins[1], ins[2], segs_obj, all_segs, lens, attn=args.attn)
+                return [o for o, _ in res.values()][:1] or [ins[0]]
+        items_per_step = int(off_all[-1])
+        scaling = "strong"
+        parallel = f"{mode} x{world} (strong: one {args.config} batch split; all_gather of partials over NCCL)"
+        B = B_all
+    path = vista.vista_dispatch_name(vista.make_desc(B, S, H, d, in_dtype=vista.BF16, attn=attn))
 
     # warm-up
     for _ in range(max(args.warmup, 3)):
@@ -190,27 +246,22 @@ def run_own(args, rank, world, local_rank):
         t = torch.tensor([elapsed_ms, kern_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed_ms, kern_ms = float(t[0]), float(t[1])
-    items_per_step = world * total
     value = items_per_step * K_steps / (elapsed_ms / 1e3)
 
     # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if args.e2e_steps > 0:
-        hq, hK, hV = q.cpu().pin_memory(), K.cpu().pin_memory(), V.cpu().pin_memory()
-        hoff = off_t.cpu().pin_memory()
-        hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-        hlse = torch.empty(lse.shape, dtype=lse.dtype).pin_memory() if lse is not None else None
-        dq, dK, dV, doff = torch.empty_like(q), torch.empty_like(K), torch.empty_like(V), torch.empty_like(off_t)
+        host_in = [x.cpu().pin_memory() for x in inputs]
+        dev_in = [torch.empty_like(x) for x in inputs]
+        outs0 = step()
+        host_out = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs0]
 
         def e2e_step():
-            dq.copy_(hq, non_blocking=True)
-            dK.copy_(hK, non_blocking=True)
-            dV.copy_(hV, non_blocking=True)
-            doff.copy_(hoff, non_blocking=True)
-            vista.vista_summarize_fwd(desc, dq, dK, dV, doff, total, out, lse, ws, ws_bytes, sh)
-            hout.copy_(out, non_blocking=True)
-            if hlse is not None:
-                hlse.copy_(lse, non_blocking=True)
+            for hx, dx in zip(host_in, dev_in):
+                dx.copy_(hx, non_blocking=True)
+            outs = step(dev_in)
+            for ho, o in zip(host_out, outs):
+                ho.copy_(o, non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -227,18 +278,20 @@ def run_own(args, rank, world, local_rank):
             t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e_ms = float(t[0])
-        h2d = sum(x.numel() * x.element_size() for x in (hq, hK, hV, hoff))
-        d2h = hout.numel() * hout.element_size() + (hlse.numel() * hlse.element_size() if hlse is not None else 0)
+        h2d = sum(x.numel() * x.element_size() for x in host_in)
+        d2h = sum(x.numel() * x.element_size() for x in host_out)
         e2e = {"value": items_per_step * args.e2e_steps / (e_ms / 1e3), "unit": "items/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "note": "pinned host buffers -> H2D copies -> vista_summarize_fwd -> D2H of out+lse, CUDA events"}
+               "note": "per rank: pinned host inputs -> H2D -> the step through the C ABI -> D2H of outputs; "
+                       "CUDA events, max over ranks"}
 
     if rank != 0:
         return None
     pk, pk_kind = peaks()
+    # algorithmic work of ONE launch of the dominant kernel on this rank (its `total` items)
     flops = 4.0 * S * d * H * total if attn == vista.SOFTMAX else 2.0 * d * d * H * total
     kv_bytes = 4.0 * d * H * total  # bf16 K + V, read once
-    io_bytes = kv_bytes + S * H * d * 2 + B * S * H * d * 2 + (B * H * S * 4 if lse is not None else 0)
+    io_bytes = kv_bytes + S * H * d * 2 + B * S * H * d * 2 + (B * H * S * 4 if attn == vista.SOFTMAX else 0)
     tflops = flops / (kern_ms / 1e3) / 1e12
     gbs = io_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
@@ -263,10 +316,10 @@ def run_own(args, rank, world, local_rank):
     res = {
         "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": world, "steps": K_steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / K_steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded counter-based generator, bf16-exact grid values; synth/)",
         "config": {"workload": wdesc, "users_per_gpu": B, "items_per_gpu": total, "S": S, "d": d, "H": H,
-                   "attn": args.attn, "parallelism": f"by_user x{world} (no data-path collective)",
+                   "attn": args.attn, "parallelism": parallel, "mode": mode,
                    "path": path, "l2": f"inputs {kv_bytes / 1e9:.2f} GB/GPU > 126 MB L2, no flush",
                    "pct_bf16_tensor_peak": round(100 * tflops / pk["bf16_tflops"], 2)},
         "roofline": roof,
@@ -395,8 +448,7 @@ def main():
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_own(args, rank, world, local_rank)
     if res is not None and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds,
-                                               rows=None if args.attn == "qla" else 32)
+        v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds, rows=None)
         res["cpu_baseline"] = {"value": v, "unit": "items/s", "cores": cores, "kind": "oracle",
                                "sample": sample, "seconds": round(t, 2)}
     elif res is not None:

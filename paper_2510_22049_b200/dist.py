@@ -1,0 +1,190 @@
+"""Multi-GPU sharding of VISTA stage-1 summarization (one process per GPU, torch.distributed).
+
+SURVEY.md §8(e).  Users are independent, and within a user the history splits with one exchange
+of O(B*H*S*d) partials whatever L is (the flash-decoding identity for softmax; the sum of states
+for QLA, "sum_j K[S]_j^T V[S]_j").  Three partitioners over the jagged histories:
+
+  by_user    whole users to ranks, longest-processing-time greedy on L_u (C3).  No collective on the
+             data path: every rank summarizes its own users.
+  by_length  each user's [0, L_u) cut into `world` equal contiguous ranges; rank g gets range g of
+             every user (C4, 1M-item histories).  Each rank computes partials with
+             vista_summarize_partial, one all_gather (NCCL over NVLink) exchanges them, and every
+             rank merges them in rank order with vista_summarize_merge (bitwise identical results on
+             all ranks; deterministic for a fixed world size).
+  flat       the concatenated item stream cut into `world` equal ranges (C5 power-law mix): at most
+             world - 1 users straddle ranks; only their boundary partials are exchanged.
+
+The per-shard compute is a `backend` object (default: CudaBackend, the C-ABI library); tests inject
+a CPU backend so the partition / exchange / merge logic runs under gloo without a GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["partition_by_user", "partition_by_length", "partition_flat", "CudaBackend",
+           "summarize_by_length", "summarize_flat", "Segment"]
+
+
+# ----------------------------------------------------------------------------- partitioners (host)
+def partition_by_user(lengths, world: int) -> list[list[int]]:
+    """LPT greedy: users by decreasing L_u (ties: lower index first) onto the least-loaded rank
+    (ties: lower rank).  Returns each rank's users in increasing user order."""
+    lengths = np.asarray(lengths, dtype=np.int64)
+    order = sorted(range(len(lengths)), key=lambda u: (-int(lengths[u]), u))
+    load = [0] * world
+    out: list[list[int]] = [[] for _ in range(world)]
+    for u in order:
+        r = min(range(world), key=lambda g: (load[g], g))
+        out[r].append(u)
+        load[r] += int(lengths[u])
+    return [sorted(x) for x in out]
+
+
+def partition_by_length(lengths, world: int) -> np.ndarray:
+    """Cut points: returns int64 [world + 1, B]; rank g owns items [cuts[g, u], cuts[g + 1, u]) of
+    user u (equal contiguous ranges, the first ranges one item shorter when L_u % world != 0)."""
+    lengths = np.asarray(lengths, dtype=np.int64)
+    g = np.arange(world + 1, dtype=np.int64)[:, None]
+    return (lengths[None, :] * g) // world
+
+
+@dataclass(frozen=True)
+class Segment:
+    user: int
+    start: int  # item offset within the user's history
+    end: int
+
+
+def partition_flat(lengths, world: int) -> list[list[Segment]]:
+    """Cut the concatenated item stream [0, sum L) into `world` equal ranges; each rank gets the
+    user segments overlapping its range (in user order).  Empty users belong to no segment."""
+    lengths = np.asarray(lengths, dtype=np.int64)
+    off = np.zeros(len(lengths) + 1, dtype=np.int64)
+    np.cumsum(lengths, out=off[1:])
+    total = int(off[-1])
+    out: list[list[Segment]] = []
+    for g in range(world):
+        a, b = total * g // world, total * (g + 1) // world
+        segs = []
+        u = int(np.searchsorted(off, a, side="right") - 1) if a < total else len(lengths)
+        while u < len(lengths) and off[u] < b:
+            s, e = max(a, int(off[u])), min(b, int(off[u + 1]))
+            if e > s:
+                segs.append(Segment(u, s - int(off[u]), e - int(off[u])))
+            u += 1
+        out.append(segs)
+    return out
+
+
+# ----------------------------------------------------------------------------- compute backends
+class CudaBackend:
+    """Per-shard compute through the C ABI (paper_2510_22049_b200)."""
+
+    def __init__(self, **kw):
+        import paper_2510_22049_b200 as vista
+        self.v = vista
+        self.kw = kw
+
+    def partial(self, q, k, v, offsets, total_len, attn):
+        return self.v.summarize_partial(q, k, v, offsets, total_len, attn=attn, **self.kw)
+
+    def merge(self, part_o, part_lse, q, attn, user_len):
+        return self.v.summarize_merge(part_o, part_lse, q=q, attn=attn, user_len=user_len, **self.kw)
+
+
+def _attn_code(attn):
+    return 0 if attn in (0, "softmax") else 1
+
+
+# ----------------------------------------------------------------------------- split-L paths
+def _all_gather(t, group):
+    """[*shape] on every rank -> [world, *shape] in rank order (one all_gather_into_tensor)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = t.contiguous()
+    out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out.view((world,) + tuple(t.shape))
+
+
+def summarize_by_length(q, k_shard, v_shard, shard_offsets, user_len, *, attn="softmax", group=None,
+                        backend=None, total_len=None):
+    """Rank-local shard (this rank's range of every user) -> merged summary of every user on every
+    rank.  shard_offsets: int64 [B+1] (device), user_len: int64 [B] total L_u (device, QLA 1/N).
+    One all_gather of the partials (softmax: O_p [B,H,S,d] + lse_p [B,H,S]; QLA: Z_p [B,H,d,d])."""
+    import torch
+    import torch.distributed as dist
+    backend = backend or CudaBackend()
+    a = _attn_code(attn)
+    world = dist.get_world_size(group)
+    if total_len is None:
+        total_len = k_shard.shape[0]
+    po, pl = backend.partial(q, k_shard, v_shard, shard_offsets, total_len, a)
+    go = _all_gather(po, group)
+    gl = _all_gather(pl, group) if a == 0 else None
+    return backend.merge(go, gl, q, a, user_len)
+
+
+def summarize_flat(q, k_local, v_local, segments: list[Segment], all_segments: list[list[Segment]], lengths, *,
+                   attn="softmax", group=None, backend=None):
+    """Flat (item-stream) sharding.  k_local / v_local hold this rank's segments back to back.
+    Returns {user: (out [S,H,d], lse [H,S] or None)} for the users this rank OWNS (a straddling user
+    is owned by the lowest rank holding part of it).  Only straddling users' partials are exchanged
+    (one all_gather of two fixed-size boundary slots per rank)."""
+    import torch
+    import torch.distributed as dist
+    backend = backend or CudaBackend()
+    a = _attn_code(attn)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    lengths = np.asarray(lengths, dtype=np.int64)
+    dev = k_local.device
+    seg_len = np.array([s.end - s.start for s in segments], dtype=np.int64)
+    off = np.zeros(len(segments) + 1, dtype=np.int64)
+    np.cumsum(seg_len, out=off[1:])
+    off_t = torch.as_tensor(off, device=dev)
+    po, pl = backend.partial(q, k_local, v_local, off_t, int(off[-1]), a)
+
+    def complete(s):
+        return s.start == 0 and s.end == int(lengths[s.user])
+
+    owner = {}
+    for g in range(world):
+        for s in all_segments[g]:
+            owner.setdefault(s.user, g)
+    # boundary slots: the first and last segment of every rank, if incomplete
+    slot_shape = tuple(po.shape[1:])
+    send_o = torch.zeros((2,) + slot_shape, dtype=po.dtype, device=dev)
+    send_l = torch.full((2,) + tuple(pl.shape[1:]), float("-inf"), dtype=pl.dtype, device=dev) if a == 0 else None
+    send_u = torch.full((2,), -1, dtype=torch.int64, device=dev)
+    ends = [0] if len(segments) == 1 else ([0, len(segments) - 1] if segments else [])
+    for slot, j in enumerate(ends):
+        if not complete(segments[j]):
+            send_o[slot] = po[j]
+            if a == 0:
+                send_l[slot] = pl[j]
+            send_u[slot] = segments[j].user
+    recv_o = _all_gather(send_o, group)
+    recv_u = _all_gather(send_u, group)
+    recv_l = _all_gather(send_l, group) if a == 0 else None
+    ru = recv_u.cpu().numpy()
+    results = {}
+    comp = [j for j, s in enumerate(segments) if complete(s)]  # complete -> owned here, merged in one call
+    if comp:
+        ci = torch.as_tensor(comp, device=dev)
+        ulen = torch.as_tensor([int(lengths[segments[j].user]) for j in comp], dtype=torch.int64, device=dev)
+        out, lse = backend.merge(po[ci][None], None if a else pl[ci][None], q, a, ulen)
+        for n, j in enumerate(comp):
+            results[segments[j].user] = (out[n], None if lse is None else lse[n])
+    for j, s in enumerate(segments):
+        if complete(s) or owner[s.user] != rank:
+            continue
+        sel = [(g, sl) for g in range(world) for sl in range(2) if ru[g, sl] == s.user]
+        parts_o = torch.stack([recv_o[g, sl] for g, sl in sel])
+        parts_l = torch.stack([recv_l[g, sl] for g, sl in sel]) if a == 0 else None
+        ulen = torch.as_tensor([int(lengths[s.user])], dtype=torch.int64, device=dev)
+        out, lse = backend.merge(parts_o[:, None], None if parts_l is None else parts_l[:, None], q, a, ulen)
+        results[s.user] = (out[0], None if lse is None else lse[0])
+    return results

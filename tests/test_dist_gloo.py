@@ -1,0 +1,157 @@
+"""Multi-process (world_size 2 and 3, gloo, CPU) tests of the sharding layer
+(paper_2510_22049_b200/dist.py): partitioners, the all_gather exchange and the merge order, with
+the per-shard compute injected as the float64 oracle (tests only).  The same code runs with the
+CUDA backend and NCCL on GPUs."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2510_22049_b200 import dist as vdist
+
+
+class OracleBackend:
+    """CPU float64 stand-in for CudaBackend with the same tensor contract."""
+
+    def partial(self, q, k, v, offsets, total_len, attn):
+        qn, kn, vn = q.numpy(), k.numpy(), v.numpy()
+        off = offsets.numpy()
+        if attn == 0:
+            out, lse = oracle.softmax_summarize(qn, kn, vn, off)
+            return torch.from_numpy(out.transpose(0, 2, 1, 3).copy()), torch.from_numpy(lse)
+        return torch.from_numpy(oracle.qla_state(kn, vn, off)), None
+
+    def merge(self, part_o, part_lse, q, attn, user_len):
+        po = part_o.numpy()
+        if attn == 0:
+            out, lse = oracle.merge_lse(po, part_lse.numpy())    # [B,H,S,d], [B,H,S]
+            return torch.from_numpy(out.transpose(0, 2, 1, 3).copy()), torch.from_numpy(lse)
+        z = oracle.merge_sum(po)
+        return torch.from_numpy(oracle.qla_finalize(q.numpy(), z, user_len.numpy())), None
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, mode, attn, lens, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        S, H, d = 6, 2, 8
+        lens = np.asarray(lens, dtype=np.int64)
+        off = synth.offsets_from_lengths(lens)
+        q = torch.from_numpy(synth.make_q(S, H, d, seed=3, tau=2)).double()
+        be = OracleBackend()
+        if mode == "by_length":
+            cuts = vdist.partition_by_length(lens, world)
+            rows = np.concatenate([np.arange(off[u] + cuts[rank, u], off[u] + cuts[rank + 1, u]) for u in range(len(lens))])
+            users = synth.row_users(off, rows)
+            k, v = synth.make_kv(rows.astype(np.int64), users, H, d, seed=3)
+            soff = synth.offsets_from_lengths(cuts[rank + 1] - cuts[rank])
+            out, lse = vdist.summarize_by_length(q, torch.from_numpy(k).double(), torch.from_numpy(v).double(),
+                                                 torch.from_numpy(soff), torch.from_numpy(lens), attn=attn,
+                                                 backend=be)
+            res = {u: (out[u].numpy(), None if lse is None else lse[u].numpy()) for u in range(len(lens))}
+        else:
+            segs = vdist.partition_flat(lens, world)
+            mine = segs[rank]
+            rows = np.concatenate([np.arange(off[s.user] + s.start, off[s.user] + s.end) for s in mine]) \
+                if mine else np.zeros(0, np.int64)
+            users = synth.row_users(off, rows)
+            k, v = synth.make_kv(rows.astype(np.int64), users, H, d, seed=3)
+            got = vdist.summarize_flat(q, torch.from_numpy(k).double(), torch.from_numpy(v).double(), mine, segs,
+                                       lens, attn=attn, backend=be)
+            res = {u: (o.numpy(), None if l is None else l.numpy()) for u, (o, l) in got.items()}
+        result_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(world, mode, attn, lens):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, attn, lens, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return dict(out)
+
+
+def reference(lens, attn):
+    S, H, d = 6, 2, 8
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=3, tau=2)
+    if attn == "softmax":
+        return oracle.softmax_summarize(q, k, v, off)
+    return oracle.qla_summarize(q, k, v, off), None
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_by_length_matches_unsplit(world, attn):
+    lens = [50, 0, 7, 129, 1]
+    res = run_world(world, "by_length", attn, lens)
+    ref, ref_lse = reference(lens, attn)
+    for r in range(world):  # every rank holds the merged result of every user
+        for u in range(len(lens)):
+            o, l = res[r][u]
+            np.testing.assert_allclose(o, ref[u], rtol=1e-11, atol=1e-12)
+            if attn == "softmax":
+                np.testing.assert_allclose(l, ref_lse[u], rtol=1e-12)
+    for u in range(len(lens)):  # identical on every rank (fixed merge order)
+        assert all(np.array_equal(res[0][u][0], res[r][u][0]) for r in range(world))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_flat_matches_unsplit(world, attn):
+    lens = [40, 3, 0, 90, 17, 5, 61]
+    res = run_world(world, "flat", attn, lens)
+    ref, ref_lse = reference(lens, attn)
+    owned = {}
+    for r in range(world):
+        for u, v in res[r].items():
+            assert u not in owned, "a user is owned by exactly one rank"
+            owned[u] = v
+    assert sorted(owned) == [u for u in range(len(lens)) if lens[u] > 0]
+    for u, (o, l) in owned.items():
+        np.testing.assert_allclose(o, ref[u], rtol=1e-11, atol=1e-12)
+        if attn == "softmax":
+            np.testing.assert_allclose(l, ref_lse[u], rtol=1e-12)
+
+
+def test_partitioners():
+    lens = np.array([5, 100, 0, 30, 30, 70])
+    parts = vdist.partition_by_user(lens, 3)
+    assert sorted(u for p in parts for u in p) == list(range(6))
+    loads = [int(lens[p].sum()) for p in parts]
+    assert max(loads) - min(loads) <= 100 and loads[0] == 100  # LPT: the 100-item user alone on rank 0
+    cuts = vdist.partition_by_length(lens, 4)
+    assert np.array_equal(cuts[0], np.zeros(6)) and np.array_equal(cuts[-1], lens)
+    assert np.all(np.diff(cuts, axis=0) >= 0) and np.all(np.diff(cuts, axis=0).max(0) - np.diff(cuts, axis=0).min(0) <= 1)
+    segs = vdist.partition_flat(lens, 4)
+    covered = {}
+    for rank in segs:
+        for s in rank:
+            covered.setdefault(s.user, []).append((s.start, s.end))
+    for u, ranges in covered.items():
+        ranges.sort()
+        assert ranges[0][0] == 0 and ranges[-1][1] == lens[u]
+        assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    sizes = [sum(s.end - s.start for s in r) for r in segs]
+    assert max(sizes) - min(sizes) <= 1

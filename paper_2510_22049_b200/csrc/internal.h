@@ -56,6 +56,9 @@ Workspace plan_workspace(const Problem& p, bool partial);
 // (softmax: zeros / -inf in outs; QLA: zeros in zbuf if non-NULL).
 cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf);
 cudaError_t launch_sm100_softmax(const Problem& p, const Workspace& w, char* ws);
+// 2-CTA (cta_group::2) variant for S % 256 == 0; w.num_ctas counts CTA PAIRS
+cudaError_t launch_sm100_softmax2(const Problem& p, const Workspace& w, char* ws);
+bool softmax_uses_pairs(const Problem& p);
 cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf);
 cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, char* ws);
 cudaError_t launch_merge_qla_slots(const Problem& p, const Workspace& w, char* ws, float* zbuf);

@@ -105,6 +105,15 @@ Path choose_path(const Problem& p) {
 
 int sm100_softmax_nq(int S);
 
+bool softmax_uses_pairs(const Problem& p) {
+#ifdef VISTA_SOFTMAX_PAIRS  // experimental 2-CTA kernel (sm100_softmax2.cu); see DESIGN.md §4.1
+    return p.S % 256 == 0 && p.num_sms >= 2;
+#else
+    (void)p;
+    return false;
+#endif
+}
+
 Workspace plan_workspace(const Problem& p, bool partial) {
     (void)partial;
     Workspace w{};
@@ -115,6 +124,10 @@ Workspace plan_workspace(const Problem& p, bool partial) {
     if (path == PATH_SM100_SOFTMAX || path == PATH_SM100_QLA) {
         w.num_ctas = p.num_sms;
         w.rows_per_unit = path == PATH_SM100_SOFTMAX ? sm100_softmax_nq(p.S) * 128 : 128;
+        if (path == PATH_SM100_SOFTMAX && softmax_uses_pairs(p)) {
+            w.num_ctas = p.num_sms / 2;  // CTA pairs
+            w.rows_per_unit = 256;
+        }
     }
     w.uts_off = off;
     off = align256(off + (size_t)(p.B + 1) * sizeof(int64_t));
@@ -205,7 +218,10 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
     switch (choose_path(p)) {
         case PATH_SM100_SOFTMAX: {
             if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), nullptr)) != cudaSuccess) break;
-            if ((e = timed_main(p.stream, [&] { return launch_sm100_softmax(p, w, ws); })) != cudaSuccess) break;
+            if ((e = timed_main(p.stream, [&] {
+                     return softmax_uses_pairs(p) ? launch_sm100_softmax2(p, w, ws) : launch_sm100_softmax(p, w, ws);
+                 })) != cudaSuccess)
+                break;
             e = launch_merge_softmax_slots(p, w, ws);
             nlaunch = 3;
             break;

@@ -41,7 +41,8 @@ struct Problem {
 
 // Workspace carve-up (all offsets 256-B aligned).
 struct Workspace {
-    size_t uts_off, slot_unit_off, slot_o_off, slot_lse_off, zbuf_off, fin_off, total;
+    size_t uts_off, cnt_off, slot_unit_off, slot_o_off, slot_lse_off, zbuf_off, fin_off, total;
+    int num_units;     // per-unit piece counters (fused split-L merge)
     int num_ctas;      // persistent grid size used by the tiled kernels
     int rows_per_unit; // softmax: query rows per work unit (NQ * 128); QLA: d
 };
@@ -54,7 +55,7 @@ Workspace plan_workspace(const Problem& p, bool partial);
 // ---- launchers (return cudaError_t of the launch) ----
 // user tile starts: uts[u] = sum_{u'<u} ceil(L_u' / 128); also fills the outputs of empty users
 // (softmax: zeros / -inf in outs; QLA: zeros in zbuf if non-NULL).
-cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf);
+cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf, int* cnt = nullptr, int ncnt = 0);
 cudaError_t launch_sm100_softmax(const Problem& p, const Workspace& w, char* ws);
 // 2-CTA (cta_group::2) variant for S % 256 == 0; w.num_ctas counts CTA PAIRS
 cudaError_t launch_sm100_softmax2(const Problem& p, const Workspace& w, char* ws);

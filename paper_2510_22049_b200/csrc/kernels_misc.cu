@@ -61,10 +61,12 @@ __device__ __forceinline__ void lse_store(const OutSpec& o, int S, int H, int u,
 
 // ---------------------------------------------------------------------------------------------
 __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, int64_t* __restrict__ uts, OutSpec outs,
-                                  int S, int H, int d, int softmax, float* __restrict__ zbuf) {
+                                  int S, int H, int d, int softmax, float* __restrict__ zbuf, int* __restrict__ cnt,
+                                  int ncnt) {
     __shared__ int64_t wsum[32];
     __shared__ int64_t carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < ncnt; e += blockDim.x) cnt[e] = 0;  // fused-merge piece counters
     if (tid == 0) {
         carry = 0;
         uts[0] = 0;
@@ -402,9 +404,9 @@ __global__ void __launch_bounds__(256) simt_qla_state_kernel(const T* __restrict
 }  // namespace
 
 // ============================================================================== launchers
-cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf) {
+cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf, int* cnt, int ncnt) {
     user_tiles_kernel<<<1, 1024, 0, p.stream>>>(p.offsets, p.B, uts, p.outs, p.S, p.H, p.d,
-                                                 p.attn == VISTA_SOFTMAX, zbuf);
+                                                 p.attn == VISTA_SOFTMAX, zbuf, cnt, ncnt);
     return cudaGetLastError();
 }
 

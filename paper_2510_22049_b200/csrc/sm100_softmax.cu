@@ -41,6 +41,13 @@ namespace {
 constexpr int kHalfBytes = 128 * 128;       // 128 rows x 64 bf16 (one 128-B swizzle column block)
 constexpr int kTileBytes = 2 * kHalfBytes;  // 128 x 128 bf16
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
+#ifdef VISTA_FUSED_MERGE
+// experimental: split-L merge in the epilogue of the last CTA finishing a unit (measured slower
+// than the separate merge kernel at c2/c3: the merging CTA's tail grows more than the launch saves)
+constexpr bool kFusedMerge = true;
+#else
+constexpr bool kFusedMerge = false;
+#endif
 #ifndef VISTA_SETMAXNREG
 #define VISTA_SETMAXNREG 1
 #endif
@@ -80,11 +87,13 @@ struct Bars {
     uint64_t s_full[2][2], p_full[2][2];  // [q tile][S buffer]
     uint64_t pv_done[2], o_full[2];
     uint32_t tmem_base;
+    int merge_last, merge_clo, merge_chi;  // fused split-L merge handshake (epilogue)
 };
 
 struct Params {
     const int64_t* offsets;
     const int64_t* uts;
+    int* unit_cnt;  // per unit: pieces finished (zeroed by the scan kernel every launch)
     int* slot_unit;
     float* slot_o;
     float* slot_lse;
@@ -536,6 +545,65 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 for (int j = 0; j < 32; ++j) of[j] = __uint_as_float(o[j]) * inv_l;
                 store_row(P, it, cta, wg * 128 + row, of, c * 32, lse, c == 0, kRows);
             }
+            if (kFusedMerge && !item_complete(it)) {
+                // Fused split-L merge: the last CTA to finish a piece of this unit combines all
+                // pieces (their slots, ascending CTA order) with the LSE merge and writes the row.
+                __threadfence();
+                ptx::named_bar_sync(1, NQ * 128);
+                const int T = HG * (int)P.uts[P.B];
+                const int u0 = HG * (int)P.uts[it.u] + it.hg * it.Tu;
+                if (threadIdx.x == 128) {
+                    const int c_lo = cta_of_tile(u0, T, num_ctas), c_hi = cta_of_tile(u0 + it.Tu - 1, T, num_ctas);
+                    int pieces = 0;  // CTAs with a non-empty range in [c_lo, c_hi] (T < C leaves empty ranges)
+                    for (int c = c_lo; c <= c_hi; ++c) pieces += range_begin(c, T, num_ctas) < range_begin(c + 1, T, num_ctas);
+                    const int prev = atomicAdd(&P.unit_cnt[it.u * HG + it.hg], 1);
+                    bars->merge_last = prev == pieces - 1;
+                    bars->merge_clo = c_lo;
+                    bars->merge_chi = c_hi;
+                }
+                ptx::named_bar_sync(1, NQ * 128);
+                if (bars->merge_last) {
+                    __threadfence();
+                    const int c_lo = bars->merge_clo, c_hi = bars->merge_chi;
+                    const int ri = wg * 128 + row;
+                    float M = -INFINITY;
+                    for (int c = c_lo; c <= c_hi; ++c) {
+                        if (range_begin(c, T, num_ctas) == range_begin(c + 1, T, num_ctas)) continue;  // empty range
+                        M = fmaxf(M, __ldcg(P.slot_lse + (size_t)slot_of(c, c_lo, u0, T, num_ctas) * kRows + ri));
+                    }
+                    float Ls = 0.f;
+                    for (int c = c_lo; c <= c_hi; ++c) {
+                        if (range_begin(c, T, num_ctas) == range_begin(c + 1, T, num_ctas)) continue;
+                        Ls += ptx::ex2((__ldcg(P.slot_lse + (size_t)slot_of(c, c_lo, u0, T, num_ctas) * kRows + ri) - M) *
+                                       kLog2e);
+                    }
+                    const float lse_all = M + __logf(Ls);
+                    Item whole = it;
+                    whole.t0 = 0;
+                    whole.t1 = it.Tu;
+#pragma unroll 1
+                    for (int cc = 0; cc < 4; ++cc) {
+                        float of[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) of[j] = 0.f;
+                        for (int c = c_lo; c <= c_hi; ++c) {
+                            if (range_begin(c, T, num_ctas) == range_begin(c + 1, T, num_ctas)) continue;
+                            const size_t sl = (size_t)slot_of(c, c_lo, u0, T, num_ctas) * kRows + ri;
+                            const float w = ptx::ex2((__ldcg(P.slot_lse + sl) - lse_all) * kLog2e);
+                            const float4* src = reinterpret_cast<const float4*>(P.slot_o + sl * 128 + cc * 32);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const float4 v = __ldcg(src + j);
+                                of[4 * j] += w * v.x;
+                                of[4 * j + 1] += w * v.y;
+                                of[4 * j + 2] += w * v.z;
+                                of[4 * j + 3] += w * v.w;
+                            }
+                        }
+                        store_row(P, whole, cta, ri, of, cc * 32, lse_all, cc == 0, kRows);
+                    }
+                }
+            }
         }
     }
     ptx::tc_fence_before();
@@ -606,6 +674,7 @@ static cudaError_t launch_nq(const Problem& p, const Workspace& w, char* ws) {
     Params P;
     P.offsets = p.offsets;
     P.uts = reinterpret_cast<const int64_t*>(ws + w.uts_off);
+    P.unit_cnt = reinterpret_cast<int*>(ws + w.cnt_off);
     P.slot_unit = reinterpret_cast<int*>(ws + w.slot_unit_off);
     P.slot_o = reinterpret_cast<float*>(ws + w.slot_o_off);
     P.slot_lse = reinterpret_cast<float*>(ws + w.slot_lse_off);

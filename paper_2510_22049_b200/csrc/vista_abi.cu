@@ -131,6 +131,9 @@ Workspace plan_workspace(const Problem& p, bool partial) {
     }
     w.uts_off = off;
     off = align256(off + (size_t)(p.B + 1) * sizeof(int64_t));
+    w.cnt_off = off;
+    w.num_units = (path == PATH_SM100_SOFTMAX) ? p.B * p.H * ((p.S + 127) / 128) : 0;
+    off = align256(off + (size_t)w.num_units * sizeof(int));
     w.slot_unit_off = off;
     off = align256(off + (size_t)2 * w.num_ctas * sizeof(int));
     w.slot_o_off = off;
@@ -217,13 +220,21 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
     int nlaunch = 0;
     switch (choose_path(p)) {
         case PATH_SM100_SOFTMAX: {
-            if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), nullptr)) != cudaSuccess) break;
-            if ((e = timed_main(p.stream, [&] {
-                     return softmax_uses_pairs(p) ? launch_sm100_softmax2(p, w, ws) : launch_sm100_softmax(p, w, ws);
-                 })) != cudaSuccess)
+            if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), nullptr,
+                                       reinterpret_cast<int*>(ws + w.cnt_off), w.num_units)) != cudaSuccess)
                 break;
-            e = launch_merge_softmax_slots(p, w, ws);
-            nlaunch = 3;
+            if (softmax_uses_pairs(p)) {
+                if ((e = timed_main(p.stream, [&] { return launch_sm100_softmax2(p, w, ws); })) != cudaSuccess) break;
+                e = launch_merge_softmax_slots(p, w, ws);
+                nlaunch = 3;
+            } else {
+                e = timed_main(p.stream, [&] { return launch_sm100_softmax(p, w, ws); });
+                nlaunch = 2;
+#ifndef VISTA_FUSED_MERGE
+                if (e == cudaSuccess) e = launch_merge_softmax_slots(p, w, ws);
+                nlaunch = 3;
+#endif
+            }
             break;
         }
         case PATH_SM100_QLA: {

@@ -234,3 +234,101 @@ def test_gpu_generator_matches_numpy(cuda_lib):
     qt, kt, vt, _ = synth.make_batch([100, 0, 300], 8, 2, 128, seed=4, category=True, backend="torch", device="cuda")
     assert np.array_equal(k, kt.float().cpu().numpy()) and np.array_equal(v, vt.float().cpu().numpy())
     assert np.array_equal(q, qt.float().cpu().numpy())
+
+
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_per_user_seeds_and_bf16_out(cuda_lib, attn):
+    """q_user_stride != 0 (personalized seeds, reading R12) and bf16 output."""
+    vista = cuda_lib
+    lens = [700, 0, 129]
+    S, H, d = 256, 2, 128
+    B = len(lens)
+    q = synth.make_q(S, H, d, seed=13, users=B, tau=2)
+    _, k, v, off = synth.make_batch(lens, S, H, d, seed=13)
+    qt, kt, vt = to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16")
+    a = vista.SOFTMAX if attn == "softmax" else vista.QLA
+    out, lse = vista.summarize(qt, kt, vt, torch.from_numpy(off).cuda(), int(off[-1]), attn=a, out_dtype=vista.BF16)
+    torch.cuda.synchronize()
+    if attn == "softmax":
+        ref, ref_lse = oracle.softmax_summarize(q, k, v, off, q_per_user=True)
+        check_softmax(out, lse, ref, ref_lse, lens, "bf16")
+    else:
+        ref = oracle.qla_summarize(q, k, v, off, q_per_user=True)
+        g = out.float().cpu().numpy()
+        for u in range(B):
+            for h in range(H):
+                assert block_err(g[u, :, h], ref[u, :, h]) <= 2e-2
+
+
+def test_qla_c2_full_size_sampled_users(cuda_lib):
+    """QLA at BASELINE config 2 size (bench launch configuration), three users checked."""
+    vista = cuda_lib
+    cfg = synth.CONFIGS["c2"]
+    lens = synth.user_lengths("c2")
+    S, H, d = cfg["S"], cfg["H"], cfg["d"]
+    q, K, V, off = synth.make_batch(lens, S, H, d, backend="torch", device="cuda")
+    out, _ = vista.summarize(q, K, V, torch.from_numpy(off).cuda(), int(off[-1]), attn=vista.QLA, out_dtype=vista.BF16)
+    torch.cuda.synchronize()
+    qn = q.float().cpu().numpy()
+    for u in (0, 40, 63):
+        a, b = int(off[u]), int(off[u + 1])
+        ref = oracle.qla_summarize(qn, K[a:b].float().cpu().numpy(), V[a:b].float().cpu().numpy(), [0, b - a])
+        g = out[u].float().cpu().numpy()
+        for h in range(H):
+            assert block_err(g[:, h], ref[0, :, h]) <= 2e-2
+
+
+def test_c5_full_size_sampled(cuda_lib):
+    """BASELINE config 5 (1,024 power-law users, S=512) at full size: the longest user, a median
+    one and the shortest, sampled rows of both 256-row groups, against the oracle."""
+    vista = cuda_lib
+    cfg = synth.CONFIGS["c5"]
+    lens = synth.user_lengths("c5")
+    S, H, d = cfg["S"], cfg["H"], cfg["d"]
+    q, K, V, off = synth.make_batch(lens, S, H, d, backend="torch", device="cuda")
+    out, lse = vista.summarize(q, K, V, torch.from_numpy(off).cuda(), int(off[-1]), out_dtype=vista.BF16)
+    torch.cuda.synchronize()
+    rows = np.array([0, 255, 256, 511])
+    qn = q.float().cpu().numpy()
+    order = np.argsort(lens)
+    for u in (int(order[-1]), int(order[len(order) // 2]), int(order[0])):
+        a, b = int(off[u]), int(off[u + 1])
+        ref, ref_lse = oracle.softmax_summarize(qn, K[a:b].float().cpu().numpy(), V[a:b].float().cpu().numpy(),
+                                                [0, b - a], rows=rows)
+        check_softmax(out[u:u + 1], lse[u:u + 1], ref, ref_lse, [b - a], "bf16", rows=rows)
+
+
+def test_c4_partial_shards_full_size(cuda_lib):
+    """BASELINE config 4 (8 users x 1M items): by_length split into 8 shards run on this GPU one
+    after another (the multi-GPU split-L data flow without NCCL), merged, sampled rows checked."""
+    vista = cuda_lib
+    cfg = synth.CONFIGS["c4"]
+    lens = synth.user_lengths("c4")
+    S, H, d = cfg["S"], cfg["H"], cfg["d"]
+    from paper_2510_22049_b200 import dist as vdist
+    world = 8
+    cuts = vdist.partition_by_length(lens, world)
+    off_all = synth.offsets_from_lengths(lens)
+    q = synth.make_q(S, H, d, backend="torch", device="cuda")
+    parts_o, parts_l = [], []
+    for g in range(world):
+        seg_len = cuts[g + 1] - cuts[g]
+        soff = synth.offsets_from_lengths(seg_len)
+        rows = torch.cat([torch.arange(int(off_all[u] + cuts[g, u]), int(off_all[u] + cuts[g + 1, u]), device="cuda")
+                          for u in range(len(lens))])
+        users = synth.row_users(torch.from_numpy(off_all).cuda(), rows, backend="torch")
+        k, v = synth.make_kv(rows, users, H, d, backend="torch", device="cuda")
+        po, pl = vista.summarize_partial(q, k.contiguous(), v.contiguous(), torch.from_numpy(soff).cuda(), int(soff[-1]))
+        parts_o.append(po)
+        parts_l.append(pl)
+        del k, v
+    out, lse = vista.summarize_merge(torch.stack(parts_o), torch.stack(parts_l), q=q, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    u = 3
+    a, b = int(off_all[u]), int(off_all[u + 1])
+    rows_u = torch.arange(a, b, device="cuda")
+    k, v = synth.make_kv(rows_u, torch.full_like(rows_u, u), H, d, backend="torch", device="cuda")
+    sel = np.array([0, 200])
+    ref, ref_lse = oracle.softmax_summarize(q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy(),
+                                            [0, b - a], rows=sel)
+    check_softmax(out[u:u + 1], lse[u:u + 1], ref, ref_lse, [b - a], "bf16", rows=sel)

@@ -51,6 +51,7 @@ def _load():
         lib.vo_qla_finalize.argtypes = [i64, i64, i64, i64, P, i64, P, P, i32, i32, i32, P, i32]
         lib.vo_merge_lse.argtypes = [i64, i64, i64, P, P, P, P]
         lib.vo_merge_sum.argtypes = [i64, i64, P, P]
+        lib.vo_quantize_rows_f32.argtypes = [i64, i64, P, P, P, P]
         lib.vo_act.argtypes = [i32, f64]
         lib.vo_act.restype = f64
         lib.vo_num_threads.restype = i32
@@ -169,3 +170,21 @@ def merge_sum(parts):
     out = np.empty(parts.shape[1:], np.float64)
     _load().vo_merge_sum(parts.shape[0], int(np.prod(parts.shape[1:])), _ptr(parts), _ptr(out))
     return out
+
+
+def quantize_rows_int8(x):
+    """Int8 export of token rows (scheme SPEC.md:339-347), float32 arithmetic.
+    x: [..., d] float32 -> (codes int8 [..., d], scale float32 [...], zero_point float32 [...])."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    d = x.shape[-1]
+    n = int(np.prod(x.shape[:-1]))
+    codes = np.empty(x.shape, np.int8)
+    scale = np.empty(x.shape[:-1], np.float32)
+    zp = np.empty(x.shape[:-1], np.float32)
+    _load().vo_quantize_rows_f32(n, d, _ptr(x), _ptr(codes), _ptr(scale), _ptr(zp))
+    return codes, scale, zp
+
+
+def dequantize_rows_int8(codes, scale, zp):
+    """x^ = code * scale + zero_point (SPEC.md:348-352), float64."""
+    return codes.astype(np.float64) * scale[..., None].astype(np.float64) + zp[..., None].astype(np.float64)

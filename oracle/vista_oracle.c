@@ -241,3 +241,35 @@ int vo_merge_sum(int64_t P, int64_t n, const double* parts, double* out) {
     }
     return 0;
 }
+
+/*
+ * Int8 export of summary tokens (NEXT-1): "quantized and exported to a large key-value cache ...
+ * dequantized with minimal distortion" (Sec. 3.1).  The scheme is SPEC.md:339-347
+ * (the paper gives none): per token row of d values, symmetric-range affine quantization
+ *   scale = max((max - min) / 254, 1e-12),  zero_point = (max + min) / 2,
+ *   code  = clamp(round_half_even((x - zero_point) / scale), -127, 127),  x^ = code * scale + zp.
+ * Computed in float32 (the kernel's precision, reading R18) with no FMA contraction
+ * (-std=c11 => -ffp-contract=off), so the integer decisions match bit for bit.
+ */
+int vo_quantize_rows_f32(int64_t n, int64_t d, const float* x, signed char* codes, float* scale, float* zp) {
+    for (int64_t r = 0; r < n; ++r) {
+        const float* xr = x + r * d;
+        float mx = xr[0], mn = xr[0];
+        for (int64_t c = 1; c < d; ++c) {
+            if (xr[c] > mx) mx = xr[c];
+            if (xr[c] < mn) mn = xr[c];
+        }
+        float s = (mx - mn) / 254.0f;
+        if (!(s > 1e-12f)) s = 1e-12f;
+        const float z = 0.5f * (mx + mn);
+        scale[r] = s;
+        zp[r] = z;
+        for (int64_t c = 0; c < d; ++c) {
+            float q = rintf((xr[c] - z) / s);
+            if (q > 127.0f) q = 127.0f;
+            if (q < -127.0f) q = -127.0f;
+            codes[r * d + c] = (signed char)q;
+        }
+    }
+    return 0;
+}

@@ -369,3 +369,27 @@ def test_synth_numpy_torch_identical_and_recipe():
     assert int(synth.user_lengths("c3").sum()) == 1_859_714
     L5 = synth.user_lengths("c5")
     assert int(L5.sum()) == 6_906_453 and int(L5.max()) == 667_490
+
+
+# ----------------------------------------------------------------------------- NEXT-1 int8 export
+def test_quantize_error_bound_and_special_rows():
+    """|dequant - x| <= scale/2 per entry (+ float32 rounding slack); all-zero row
+    -> scale at the floor and codes 0; a row on the 255-point grid round-trips exactly; codes stay in
+    [-127, 127] and the extremes map to -127 / +127."""
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-3, 3, size=(64, 128)).astype(np.float32)
+    x[0] = 0.0
+    kk = rng.integers(-127, 128, size=128)
+    kk[0], kk[1] = -127, 127
+    x[1] = (kk * 0.5 + 1.0).astype(np.float32)  # zero point 1, scale 0.5: on the 255-point grid
+    codes, scale, zp = oracle.quantize_rows_int8(x)
+    assert codes.min() >= -127 and codes.max() <= 127
+    deq = oracle.dequantize_rows_int8(codes, scale, zp)
+    err = np.abs(deq - x.astype(np.float64))
+    assert np.all(err <= scale[:, None] * (0.5 + 1e-5) + 1e-6)
+    assert scale[0] == np.float32(1e-12) and np.all(codes[0] == 0) and np.all(deq[0] == 0)
+    # grid row: max - min = 127 * 0.5 * 2 -> scale 0.5, exact round trip
+    assert scale[1] == np.float32(0.5) and zp[1] == np.float32(1.0)
+    assert np.array_equal(codes[1], kk) and np.array_equal(deq[1], x[1].astype(np.float64))
+    r = 5
+    assert codes[r, np.argmax(x[r])] == 127 and codes[r, np.argmin(x[r])] == -127

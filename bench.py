@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--mode", default=None, choices=["by_user", "by_length", "flat"],
                     help="multi-GPU partitioner (default per config: c2/c3 by_user, c4 by_length, c5 flat)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--export-int8", action="store_true",
+                    help="NEXT-1: the step also exports the summary tokens as int8 (vista_quantize_rows_int8)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -158,9 +160,19 @@ def run_own(args, rank, world, local_rank):
         out = torch.empty((B, S, H, d), dtype=torch.bfloat16, device=dev)
         lse = torch.empty((B, H, S), dtype=torch.float32, device=dev) if attn == vista.SOFTMAX else None
         inputs = [q, K, V, off_t]
+        nrows = B * S * H
+        codes = torch.empty((nrows, d), dtype=torch.int8, device=dev) if args.export_int8 else None
+        qscale = torch.empty(nrows, dtype=torch.float32, device=dev) if args.export_int8 else None
+        qzp = torch.empty(nrows, dtype=torch.float32, device=dev) if args.export_int8 else None
+
+        def export():
+            vista.vista_quantize_rows_int8(nrows, d, vista.BF16, out, codes, qscale, qzp, sh)
 
         def step(ins=inputs):
             vista.vista_summarize_fwd(desc, ins[0], ins[1], ins[2], ins[3], total, out, lse, ws, ws_bytes, sh)
+            if args.export_int8:
+                export()
+                return [codes, qscale, qzp] + ([lse] if lse is not None else [])
             return [out] + ([lse] if lse is not None else [])
         items_per_step = world * total
         scaling = "weak"
@@ -285,6 +297,19 @@ def run_own(args, rank, world, local_rank):
                "note": "per rank: pinned host inputs -> H2D -> the step through the C ABI -> D2H of outputs; "
                        "CUDA events, max over ranks"}
 
+    export_info = None
+    if args.export_int8 and mode == "by_user":
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(20):
+            export()
+        b.record(stream)
+        torch.cuda.synchronize()
+        xms = a.elapsed_time(b) / 20
+        xbytes = nrows * d * 2 + nrows * d + nrows * 8
+        export_info = {"kernel": "quantize_rows_kernel", "kernel_ms": round(xms, 5), "bytes_per_launch": xbytes,
+                       "achieved_gbs": round(xbytes / (xms / 1e3) / 1e9, 1), "rows": nrows,
+                       "scheme": "per-row affine int8, SPEC.md:339-347 (NEXT-1)"}
     if rank != 0:
         return None
     pk, pk_kind = peaks()
@@ -327,6 +352,8 @@ def run_own(args, rank, world, local_rank):
         "e2e": e2e,
         "gpu_launches": launches,
     }
+    if export_info is not None:
+        res["export_int8"] = export_info
     return res
 
 

@@ -163,6 +163,18 @@ vista_status_t vista_check_offsets(const int64_t* offsets, int32_t num_users, in
 const char* vista_dispatch_name(const vista_desc_t* desc);
 
 /*
+ * Int8 export of summary tokens (NEXT-1; "quantized and exported to a large key-value cache ...
+ * dequantized with minimal distortion").  The paper gives no scheme; this is
+ * per row of d values, scale = max((max - min) / 254, 1e-12),
+ * zero_point = (max + min) / 2, code = clamp(rint((x - zero_point) / scale), -127, 127), all in
+ * float32 without contraction, so |code * scale + zero_point - x| <= scale / 2.
+ *   x [n, d] (in_dtype bf16 or f32), codes int8 [n, d], scale / zero_point float32 [n]; device.
+ * Typical use: x = the out tensor of vista_summarize_fwd viewed as [B*S*H, d].  Async on stream.
+ */
+vista_status_t vista_quantize_rows_int8(int64_t n, int32_t d, int32_t in_dtype, const void* x,
+                                        int8_t* codes, float* scale, float* zero_point, void* stream);
+
+/*
  * Measurement hooks (used by bench.py; not needed for correctness).
  *
  * vista_time_next_main_kernel: arms a one-shot, per-thread hook: the next summarize call

@@ -24,6 +24,7 @@ __all__ = [
     "vista_summarize_fwd", "vista_summarize_partial", "vista_summarize_merge",
     "vista_summarize_merge_workspace_size",
     "vista_check_offsets", "vista_dispatch_name", "vista_time_next_main_kernel", "vista_launch_counter",
+    "vista_quantize_rows_int8", "quantize_int8",
     "summarize", "summarize_partial", "summarize_merge",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
@@ -93,6 +94,8 @@ def load():
     lib.vista_summarize_merge_workspace_size.argtypes = [DP, ctypes.POINTER(sz)]
     lib.vista_summarize_merge_workspace_size.restype = ctypes.c_int
     lib.vista_check_offsets.argtypes = [P, i32, i64, P]
+    lib.vista_quantize_rows_int8.argtypes = [i64, i32, i32, P, P, P, P, P]
+    lib.vista_quantize_rows_int8.restype = ctypes.c_int
     lib.vista_time_next_main_kernel.argtypes = [P, P]
     lib.vista_time_next_main_kernel.restype = ctypes.c_int
     lib.vista_launch_counter.restype = ctypes.c_uint64
@@ -180,6 +183,23 @@ def vista_summarize_merge(desc, num_parts, part_o, part_lse, q, user_len, out, l
 def vista_check_offsets(offsets, num_users, total_len, stream=None):
     _check(load().vista_check_offsets(_ptr(offsets), int(num_users), int(total_len), _stream(stream)),
            "vista_check_offsets")
+
+
+def vista_quantize_rows_int8(n, d, in_dtype, x, codes, scale, zero_point, stream=None):
+    _check(load().vista_quantize_rows_int8(int(n), int(d), int(in_dtype), _ptr(x), _ptr(codes), _ptr(scale),
+                                           _ptr(zero_point), _stream(stream)), "vista_quantize_rows_int8")
+
+
+def quantize_int8(x, stream=None):
+    """Int8 export of rows of x [..., d] (bf16 or f32, device) -> (codes int8, scale f32, zero_point f32)."""
+    import torch
+    d = x.shape[-1]
+    n = x.numel() // d
+    codes = torch.empty(x.shape, dtype=torch.int8, device=x.device)
+    scale = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
+    zp = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
+    vista_quantize_rows_int8(n, d, _dtype_code(x), x.contiguous(), codes, scale, zp, stream)
+    return codes, scale, zp
 
 
 def vista_time_next_main_kernel(start_event, stop_event):

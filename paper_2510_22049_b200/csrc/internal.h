@@ -74,6 +74,8 @@ bool qla_finalize_uses_tc(const Problem& p);
 size_t sm100_qla_finalize_workspace(const Problem& p);
 cudaError_t launch_sm100_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
                                       const int64_t* user_len, void* ws);
+cudaError_t launch_quantize_rows(int64_t n, int d, int in_bf16, const void* x, int8_t* codes, float* scale, float* zp,
+                                 cudaStream_t stream);
 // Merge P stacked softmax partials [P,B,H,S,d] / [P,B,H,S] into outs.
 cudaError_t launch_merge_softmax_parts(const Problem& p, int P, const float* part_o, const float* part_lse);
 

@@ -401,7 +401,117 @@ __global__ void __launch_bounds__(256) simt_qla_state_kernel(const T* __restrict
     for (int a = 0; a < NR; ++a) zbuf[((size_t)unit * D + r0 + a * RSTEP) * D + c2] = acc[a];
 }
 
+// Int8 export (NEXT-1): one warp per row; float32 arithmetic without contraction (matches the
+// oracle's decisions bit for bit): scale = max((mx - mn) / 254, 1e-12), zp = (mx + mn) / 2,
+// code = clamp(rint((x - zp) / scale), -127, 127).
+template <typename T>
+__global__ void quantize_rows_kernel(int64_t n, int d, const T* __restrict__ x, int8_t* __restrict__ codes,
+                                     float* __restrict__ scale, float* __restrict__ zp) {
+    const int64_t r = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    if (r >= n) return;
+    const T* xr = x + r * d;
+    float mx = -INFINITY, mn = INFINITY;
+    for (int c = lane; c < d; c += 32) {
+        const float v = ld<T>(xr + c);
+        mx = fmaxf(mx, v);
+        mn = fminf(mn, v);
+    }
+    mx = warp_max(mx);
+    mn = -warp_max(-mn);
+    float s = __fdiv_rn(__fsub_rn(mx, mn), 254.0f);
+    if (!(s > 1e-12f)) s = 1e-12f;
+    const float z = __fmul_rn(0.5f, __fadd_rn(mx, mn));
+    if (lane == 0) {
+        scale[r] = s;
+        zp[r] = z;
+    }
+    for (int c = lane; c < d; c += 32) {
+        float q = rintf(__fdiv_rn(__fsub_rn(ld<T>(xr + c), z), s));
+        q = fminf(fmaxf(q, -127.f), 127.f);
+        codes[r * d + c] = (int8_t)q;
+    }
+}
+
+// Vectorized variant for d = 128: 16 threads per row, 8 consecutive values per thread (one 16-B
+// load for bf16), 8-byte code stores; same float32 arithmetic as quantize_rows_kernel.
+template <typename T>
+__global__ void __launch_bounds__(256) quantize_rows128_kernel(int64_t n, const T* __restrict__ x,
+                                                               int8_t* __restrict__ codes, float* __restrict__ scale,
+                                                               float* __restrict__ zp) {
+    const int64_t r = (int64_t)blockIdx.x * 16 + threadIdx.x / 16;
+    const int sub = threadIdx.x % 16;
+    const bool ok = r < n;
+    float v[8];
+    if (ok) {
+        const T* xr = x + r * 128 + sub * 8;
+        if constexpr (sizeof(T) == 2) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(xr);
+            const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                v[2 * e] = __uint_as_float(w[e] << 16);
+                v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+            }
+        } else {
+            const float4 a = *reinterpret_cast<const float4*>(xr), b = *reinterpret_cast<const float4*>(xr + 4);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = 0.f;
+    }
+    float mx = v[0], mn = v[0];
+#pragma unroll
+    for (int e = 1; e < 8; ++e) {
+        mx = fmaxf(mx, v[e]);
+        mn = fminf(mn, v[e]);
+    }
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (!ok) return;
+    float s = __fdiv_rn(__fsub_rn(mx, mn), 254.0f);
+    if (!(s > 1e-12f)) s = 1e-12f;
+    const float z = __fmul_rn(0.5f, __fadd_rn(mx, mn));
+    if (sub == 0) {
+        scale[r] = s;
+        zp[r] = z;
+    }
+    uint32_t pk[2] = {0, 0};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float q = fminf(fmaxf(rintf(__fdiv_rn(__fsub_rn(v[e], z), s)), -127.f), 127.f);
+        pk[e >> 2] |= ((uint32_t)(uint8_t)(int8_t)q) << (8 * (e & 3));
+    }
+    *reinterpret_cast<uint2*>(codes + r * 128 + sub * 8) = make_uint2(pk[0], pk[1]);
+}
+
 }  // namespace
+
+cudaError_t launch_quantize_rows(int64_t n, int d, int in_bf16, const void* x, int8_t* codes, float* scale, float* zp,
+                                 cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(codes)) & 15) == 0;
+    if (d == 128 && aligned) {
+        const unsigned g = (unsigned)((n + 15) / 16);
+        if (in_bf16)
+            quantize_rows128_kernel<__nv_bfloat16><<<g, 256, 0, stream>>>(n, reinterpret_cast<const __nv_bfloat16*>(x),
+                                                                          codes, scale, zp);
+        else
+            quantize_rows128_kernel<float><<<g, 256, 0, stream>>>(n, reinterpret_cast<const float*>(x), codes, scale, zp);
+        return cudaGetLastError();
+    }
+    const unsigned grid = (unsigned)((n + 7) / 8);
+    if (in_bf16)
+        quantize_rows_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>(n, d, reinterpret_cast<const __nv_bfloat16*>(x),
+                                                                      codes, scale, zp);
+    else
+        quantize_rows_kernel<float><<<grid, 256, 0, stream>>>(n, d, reinterpret_cast<const float*>(x), codes, scale, zp);
+    return cudaGetLastError();
+}
 
 // ============================================================================== launchers
 cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf, int* cnt, int ncnt) {

@@ -321,6 +321,18 @@ vista_status_t vista_summarize_merge(const vista_desc_t* desc, int32_t num_parts
     return VISTA_OK;
 }
 
+vista_status_t vista_quantize_rows_int8(int64_t n, int32_t d, int32_t in_dtype, const void* x, int8_t* codes,
+                                        float* scale, float* zero_point, void* stream) {
+    if (n < 0 || d < 1) return VISTA_ERR_INVALID;
+    if (in_dtype != VISTA_F32 && in_dtype != VISTA_BF16) return VISTA_ERR_INVALID;
+    if (n > 0 && (!x || !codes || !scale || !zero_point)) return VISTA_ERR_NULL;
+    cudaError_t e = launch_quantize_rows(n, d, in_dtype == VISTA_BF16, x, codes, scale, zero_point,
+                                         reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (n > 0) g_launches += 1;
+    return VISTA_OK;
+}
+
 vista_status_t vista_time_next_main_kernel(void* start_event, void* stop_event) {
     g_ev_start = reinterpret_cast<cudaEvent_t>(start_event);
     g_ev_stop = reinterpret_cast<cudaEvent_t>(stop_event);

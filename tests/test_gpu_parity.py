@@ -332,3 +332,36 @@ def test_c4_partial_shards_full_size(cuda_lib):
     ref, ref_lse = oracle.softmax_summarize(q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy(),
                                             [0, b - a], rows=sel)
     check_softmax(out[u:u + 1], lse[u:u + 1], ref, ref_lse, [b - a], "bf16", rows=sel)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_int8_export_bit_exact(cuda_lib, dtype):
+    """NEXT-1: the CUDA quantizer takes the same float32 decisions as the oracle -> identical codes,
+    scales and zero points (bit-exact) on seeded rows, incl. a constant row and a zero row."""
+    vista = cuda_lib
+    q, k, v, off = synth.make_batch([1000], 8, 1, 128, dtype=dtype, seed=17)
+    x = np.concatenate([k[:, 0, :], v[:, 0, :]]).astype(np.float32)
+    x[3] = 0.0
+    x[4] = x[4, 0]
+    codes, scale, zp = oracle.quantize_rows_int8(x)
+    gc, gs, gz = vista.quantize_int8(to_dev(x, dtype))
+    torch.cuda.synchronize()
+    assert np.array_equal(gc.cpu().numpy(), codes)
+    assert np.array_equal(gs.cpu().numpy(), scale) and np.array_equal(gz.cpu().numpy(), zp)
+
+
+def test_int8_export_of_summary_tokens(cuda_lib):
+    """Summarize -> export: dequantized tokens stay within scale/2 of the exported bf16 tokens and
+    within the bf16 parity gate of the oracle summary."""
+    vista = cuda_lib
+    lens = [3000, 129]
+    (q, k, v, off), (out, lse) = run_case(vista, lens, 256, 2, 128, seed=19)
+    codes, scale, zp = vista.quantize_int8(out)
+    torch.cuda.synchronize()
+    deq = codes.float() * scale[..., None] + zp[..., None]
+    assert torch.all((deq - out).abs() <= scale[..., None] * 0.5 * (1 + 1e-5) + 1e-6)
+    ref, _ = oracle.softmax_summarize(q, k, v, off)
+    g = deq.cpu().numpy().astype(np.float64)
+    for u in range(len(lens)):
+        for h in range(2):
+            assert block_err(g[u, :, h], ref[u, :, h]) <= 2e-2

@@ -13,6 +13,29 @@ constexpr int kTile = 128;  // history items per tile (= TMA box rows = MMA N of
 
 enum OutMode : int { OUT_FINAL = 0, OUT_PARTIAL = 1 };
 
+// Launch with programmatic dependent launch (PDL): the kernel may begin while its predecessor on
+// the stream finishes; it must execute `griddepcontrol.wait` before touching the predecessor's
+// results.  Hides the launch latency of the short kernels around the main ones.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+#ifdef VISTA_NO_PDL
+    cfg.numAttrs = 0;
+#else
+    cfg.numAttrs = 1;
+#endif
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Where a finished (normalized) output row goes.
 struct OutSpec {
     int mode;            // OUT_FINAL: out[B,S,H,d] (out_dtype) + lse[B,H,S]; OUT_PARTIAL: part_o[B,H,S,d] f32 + part_lse[B,H,S]

@@ -66,6 +66,7 @@ __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, in
     __shared__ int64_t wsum[32];
     __shared__ int64_t carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    asm volatile("griddepcontrol.launch_dependents;");  // PDL: the main kernel may start its prologue
     for (int e = tid; e < ncnt; e += blockDim.x) cnt[e] = 0;  // fused-merge piece counters
     if (tid == 0) {
         carry = 0;

@@ -272,6 +272,11 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             ptx::mbar_init(&bars->o_full[q], 1);
         }
         ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, C::kTmemCols);
+    // PDL: everything above overlapped the scan kernel; its results (uts) are needed from here on
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) {
         // record which units this CTA's partial slots will hold (read by the merge kernel)
         ItemIter itr;
         itr.init(P.uts, P.B, HG, cta, num_ctas);
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
         P.slot_unit[2 * cta] = s0;
         P.slot_unit[2 * cta + 1] = s1;
     }
-    if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, C::kTmemCols);
+    asm volatile("griddepcontrol.launch_dependents;");
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -688,8 +693,7 @@ static cudaError_t launch_nq(const Problem& p, const Workspace& w, char* ws) {
     static const cudaError_t attr =
         cudaFuncSetAttribute(sm100_softmax_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (attr != cudaSuccess) return attr;
-    sm100_softmax_kernel<NQ><<<w.num_ctas, C::kThreads, C::kSmem, p.stream>>>(mq, mk, mv, P);
-    return cudaGetLastError();
+    return launch_pdl(sm100_softmax_kernel<NQ>, dim3(w.num_ctas), dim3(C::kThreads), C::kSmem, p.stream, mq, mk, mv, P);
 }
 
 int sm100_softmax_nq(int S) { return (S % 256 == 0) ? 2 : 1; }

@@ -101,26 +101,33 @@ __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, in
         if (tid == blockDim.x - 1) carry = incl;
         __syncthreads();
     }
-    // empty users: softmax out = 0, lse = -inf (identity of the LSE merge); QLA Z = 0
-    for (int u = 0; u < B; ++u) {
-        if (offsets[u + 1] != offsets[u]) continue;
-        if (softmax) {
-            const size_t n = (size_t)S * H * d;
-            if (outs.mode == OUT_PARTIAL) {
-                float* o = reinterpret_cast<float*>(outs.out) + (size_t)u * n;
-                for (size_t e = tid; e < n; e += blockDim.x) o[e] = 0.f;
-            } else if (outs.out_bf16) {
-                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(outs.out) + (size_t)u * n;
-                for (size_t e = tid; e < n; e += blockDim.x) o[e] = __float2bfloat16_rn(0.f);
-            } else {
-                float* o = reinterpret_cast<float*>(outs.out) + (size_t)u * n;
-                for (size_t e = tid; e < n; e += blockDim.x) o[e] = 0.f;
+    // empty users: softmax out = 0, lse = -inf (identity of the LSE merge); QLA Z = 0.
+    // One warp per empty user (found with a block-wide ballot scan; no serial pass over B).
+    const size_t n_sm = (size_t)S * H * d, n_z = (size_t)H * d * d;
+    for (int base = 0; base < B; base += blockDim.x) {
+        const int u = base + tid;
+        const bool empty = u < B && offsets[u + 1] == offsets[u];
+        if (!__syncthreads_or(empty)) continue;
+        unsigned m = __ballot_sync(0xffffffffu, empty);
+        while (m) {  // this warp fills its own empty users
+            const int uu = base + warp * 32 + __ffs(m) - 1;
+            m &= m - 1;
+            if (softmax) {
+                if (outs.mode == OUT_PARTIAL) {
+                    float* o = reinterpret_cast<float*>(outs.out) + (size_t)uu * n_sm;
+                    for (size_t e = lane; e < n_sm; e += 32) o[e] = 0.f;
+                } else if (outs.out_bf16) {
+                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(outs.out) + (size_t)uu * n_sm;
+                    for (size_t e = lane; e < n_sm; e += 32) o[e] = __float2bfloat16_rn(0.f);
+                } else {
+                    float* o = reinterpret_cast<float*>(outs.out) + (size_t)uu * n_sm;
+                    for (size_t e = lane; e < n_sm; e += 32) o[e] = 0.f;
+                }
+                if (outs.lse)
+                    for (int e = lane; e < H * S; e += 32) outs.lse[(size_t)uu * H * S + e] = -INFINITY;
+            } else if (zbuf) {
+                for (size_t e = lane; e < n_z; e += 32) zbuf[(size_t)uu * n_z + e] = 0.f;
             }
-            if (outs.lse)
-                for (int e = tid; e < H * S; e += blockDim.x) outs.lse[(size_t)u * H * S + e] = -INFINITY;
-        } else if (zbuf) {
-            const size_t n = (size_t)H * d * d;
-            for (size_t e = tid; e < n; e += blockDim.x) zbuf[(size_t)u * n + e] = 0.f;
         }
     }
 }

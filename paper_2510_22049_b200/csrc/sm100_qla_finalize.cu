@@ -18,7 +18,7 @@ constexpr int kHalf = 128 * 128;  // bytes of one [128 rows][64 bf16] swizzled h
 constexpr int kOp = 2 * kHalf;    // one 128 x 128 bf16 operand
 
 __device__ __forceinline__ float act(int kind, float x) {
-    if (kind == VISTA_ACT_SILU) return x / (1.f + __expf(-x));
+    if (kind == VISTA_ACT_SILU) return x * __frcp_rn(1.f + __expf(-x));
     if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? x : __expf(x - 1.f);
     return x;
 }
@@ -30,23 +30,25 @@ __device__ __forceinline__ uint32_t swz(int row, int col) {
     return half * kHalf + row * 128 + ((chunk ^ (row & 7)) << 4);
 }
 
-// Prep 1 (grid = units): W[unit] = phi2((sum_p Z_p) / N_u) as a bf16 [128][128] MN-major operand
-// (B[K = c1][N = c2], c2 contiguous), pre-swizzled so the MMA kernel can bulk-copy it.
-__global__ void __launch_bounds__(128) qla_prep_w_kernel(const float* __restrict__ zparts, int P, int64_t part_stride,
+// Prep 1 (grid = units x 4): W[unit] = phi2((sum_p Z_p) / N_u) as a bf16 [128][128] MN-major
+// operand (B[K = c1][N = c2], c2 contiguous), pre-swizzled so the MMA kernel can bulk-copy it.
+// 256 threads per block, each 8 consecutive values of one row (block = 32 rows).
+__global__ void __launch_bounds__(256) qla_prep_w_kernel(const float* __restrict__ zparts, int P, int64_t part_stride,
                                                          const int64_t* __restrict__ offsets,
                                                          const int64_t* __restrict__ user_len, int H, int phi2,
                                                          int normalize, uint8_t* __restrict__ wbuf) {
-    const int r = threadIdx.x, unit = blockIdx.x, u = unit / H;
+    const int unit = blockIdx.x >> 2, u = unit / H;
+    const int r = (blockIdx.x & 3) * 32 + threadIdx.x / 8, c = (threadIdx.x % 8) * 16;
     const int64_t N = user_len ? user_len[u] : (offsets[u + 1] - offsets[u]);
     const float inv = (normalize && N > 0) ? 1.f / (float)N : 1.f;
     const float* z0 = zparts + ((size_t)unit * 128 + r) * 128;
     uint8_t* dst = wbuf + (size_t)unit * kOp;
-#pragma unroll 2
-    for (int c = 0; c < 128; c += 8) {
-        float4 a = *reinterpret_cast<const float4*>(z0 + c), b = *reinterpret_cast<const float4*>(z0 + c + 4);
+#pragma unroll
+    for (int cc = c; cc < c + 16; cc += 8) {
+        float4 a = *reinterpret_cast<const float4*>(z0 + cc), b = *reinterpret_cast<const float4*>(z0 + cc + 4);
         for (int p = 1; p < P; ++p) {
             const float* zp = z0 + (size_t)p * part_stride;
-            const float4 a2 = *reinterpret_cast<const float4*>(zp + c), b2 = *reinterpret_cast<const float4*>(zp + c + 4);
+            const float4 a2 = *reinterpret_cast<const float4*>(zp + cc), b2 = *reinterpret_cast<const float4*>(zp + cc + 4);
             a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
             b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
         }
@@ -55,25 +57,26 @@ __global__ void __launch_bounds__(128) qla_prep_w_kernel(const float* __restrict
         pk.y = ptx::pack_bf16x2(act(phi2, a.z * inv), act(phi2, a.w * inv));
         pk.z = ptx::pack_bf16x2(act(phi2, b.x * inv), act(phi2, b.y * inv));
         pk.w = ptx::pack_bf16x2(act(phi2, b.z * inv), act(phi2, b.w * inv));
-        *reinterpret_cast<uint4*>(dst + swz(r, c)) = pk;
+        *reinterpret_cast<uint4*>(dst + swz(r, cc)) = pk;
     }
 }
 
-// Prep 2 (grid = Bq * H * ceil(S/128)): A block = phi1(Q rows) as a bf16 [128][128] K-major operand
-// (rows past S zero), pre-swizzled.  Bq = 1 for shared seeds, so this runs once per call.
-__global__ void __launch_bounds__(128) qla_prep_q_kernel(const __nv_bfloat16* __restrict__ q, int64_t q_user_stride,
+// Prep 2 (grid = Bq * H * ceil(S/128) * 4): A block = phi1(Q rows) as a bf16 [128][128] K-major
+// operand (rows past S zero), pre-swizzled.  Bq = 1 for shared seeds, so this runs once per call.
+__global__ void __launch_bounds__(256) qla_prep_q_kernel(const __nv_bfloat16* __restrict__ q, int64_t q_user_stride,
                                                          int S, int H, int phi1, uint8_t* __restrict__ abuf) {
-    const int r = threadIdx.x;
     const int nblk = (S + 127) / 128;
-    const int blk = blockIdx.x % nblk, h = (blockIdx.x / nblk) % H, uq = blockIdx.x / (nblk * H);
+    const int op = blockIdx.x >> 2;
+    const int blk = op % nblk, h = (op / nblk) % H, uq = op / (nblk * H);
+    const int r = (blockIdx.x & 3) * 32 + threadIdx.x / 8, c = (threadIdx.x % 8) * 16;
     const int i = blk * 128 + r;
     const __nv_bfloat16* qi = q + (size_t)uq * q_user_stride + ((size_t)i * H + h) * 128;
-    uint8_t* dst = abuf + (size_t)blockIdx.x * kOp;
-#pragma unroll 4
-    for (int c = 0; c < 128; c += 8) {
+    uint8_t* dst = abuf + (size_t)op * kOp;
+#pragma unroll
+    for (int cc = c; cc < c + 16; cc += 8) {
         uint4 pk = make_uint4(0, 0, 0, 0);
         if (i < S) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(qi + c);
+            const uint4 raw = *reinterpret_cast<const uint4*>(qi + cc);
             const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
             uint32_t o[4];
 #pragma unroll
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(128) qla_prep_q_kernel(const __nv_bfloat16* __
                 o[e] = ptx::pack_bf16x2(act(phi1, __uint_as_float(w[e] << 16)), act(phi1, __uint_as_float(w[e] & 0xFFFF0000u)));
             pk = make_uint4(o[0], o[1], o[2], o[3]);
         }
-        *reinterpret_cast<uint4*>(dst + swz(r, c)) = pk;
+        *reinterpret_cast<uint4*>(dst + swz(r, cc)) = pk;
     }
 }
 
@@ -173,10 +176,10 @@ cudaError_t launch_sm100_qla_finalize(const Problem& p, const float* zparts, int
     const int bq = p.q_user_stride ? p.B : 1;
     uint8_t* wbuf = reinterpret_cast<uint8_t*>(ws);
     uint8_t* abuf = wbuf + (size_t)p.B * p.H * kOp;
-    qla_prep_w_kernel<<<p.B * p.H, 128, 0, p.stream>>>(zparts, P, part_stride, p.offsets, user_len, p.H, p.phi2,
-                                                       p.normalize, wbuf);
-    qla_prep_q_kernel<<<bq * p.H * nblk, 128, 0, p.stream>>>(reinterpret_cast<const __nv_bfloat16*>(p.q),
-                                                             p.q_user_stride, p.S, p.H, p.phi1, abuf);
+    qla_prep_w_kernel<<<p.B * p.H * 4, 256, 0, p.stream>>>(zparts, P, part_stride, p.offsets, user_len, p.H, p.phi2,
+                                                           p.normalize, wbuf);
+    qla_prep_q_kernel<<<bq * p.H * nblk * 4, 256, 0, p.stream>>>(reinterpret_cast<const __nv_bfloat16*>(p.q),
+                                                                 p.q_user_stride, p.S, p.H, p.phi1, abuf);
     const int smem = 2 * kOp + 1024;
     static const cudaError_t attr =
         cudaFuncSetAttribute(sm100_qla_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

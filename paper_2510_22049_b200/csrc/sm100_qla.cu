@@ -161,14 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bars->z_empty[b], kXformWarps * 32);
         }
         ptx::fence_mbar_init();
-        ItemIter itr;
-        itr.init(P.uts, P.B, HG, cta, num_ctas);
-        Item it;
-        int s0 = -1, s1 = -1;
-        while (itr.next(it))
-            if (!item_complete(it)) {
-                if (it.first) s0 = it.u * HG + it.hg; else s1 = it.u * HG + it.hg;
-            }
+        int s0, s1;
+        partial_slots(P.uts, P.B, HG, cta, num_ctas, s0, s1);
         P.slot_unit[2 * cta] = s0;
         P.slot_unit[2 * cta + 1] = s1;
     }
@@ -189,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t pol = ptx::policy_evict_first();
         int stage = 0;
         uint32_t phase = 0;
-        while (iter.next(it)) {
+        while (iter.next(it, P.uts, P.B, HG)) {
             const int h = it.hg;
             const int64_t row0 = P.offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
@@ -212,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         uint32_t zuse[2] = {0, 0};
         int k = 0;
-        while (iter.next(it)) {
+        while (iter.next(it, P.uts, P.B, HG)) {
             const int zb = k & 1;
             ptx::mbar_wait(&bars->z_empty[zb], (zuse[zb] & 1) ^ 1);
             ++zuse[zb];
@@ -239,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         uint32_t zphase[2] = {0, 0};
         int k = 0;
-        while (iter.next(it)) {
+        while (iter.next(it, P.uts, P.B, HG)) {
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->kv_full[stage], phase);

@@ -32,8 +32,13 @@ namespace vista {
 __device__ unsigned long long g_vista_trace[12][64][2];
 #define VTRACE(ev, t, q) \
     do { if (blockIdx.x == 0 && (t) < 64) g_vista_trace[ev][t][q] = clock64(); } while (0)
+// per-item events of CTA 0 (first 64 items), see scripts/trace_items.py
+__device__ unsigned long long g_vista_itrace[12][64];
+#define ITRACE(ev, i) \
+    do { if (blockIdx.x == 0 && (i) < 64) g_vista_itrace[ev][i] = clock64(); } while (0)
 #else
 #define VTRACE(ev, t, q) do { } while (0)
+#define ITRACE(ev, i) do { } while (0)
 #endif
 
 namespace {
@@ -76,12 +81,23 @@ struct Cfg {
     static constexpr int kKOff = NQ * kTileBytes;
     static constexpr int kVOff = kKOff + kKStages * kTileBytes;
     static constexpr int kBarOff = kVOff + kVStages * kTileBytes;
-    static constexpr int kSmem = kBarOff + 512 + 1024;  // + alignment slack
+    static constexpr int kRingOff = kBarOff + 512;   // item ring (kItemRing x ItemEntry)
+    static constexpr int kSmem = kRingOff + 512 + 1024;  // + alignment slack
     static constexpr int kThreads = 128 + NQ * 128;     // control warpgroup + NQ softmax warpgroups
     static constexpr int kTmemCols = NQ == 2 ? 512 : 256;
 };
 
+// Item ring: the scheduler lane (warp 3) walks the CTA's tile range (ItemIter: uts / offsets
+// loads) up to kItemRing items ahead and publishes each item here, so no role has a global load
+// or a search on its per-item path.
+constexpr int kItemRing = 16;
+struct ItemEntry {
+    int u, hg, t0, t1, Tu, row0, len, flags;  // flags: 1 valid, 2 first, 4 last
+};
+static_assert(kItemRing * sizeof(ItemEntry) <= 512, "ring region");
+
 struct Bars {
+    uint64_t it_full[kItemRing], it_empty[kItemRing];
     uint64_t q_full, q_empty;
     uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
     uint64_t s_full[2][2], p_full[2][2];  // [q tile][S buffer]
@@ -101,7 +117,51 @@ struct Params {
     int B, S, H, G;
     float scale_log2;
     int q_per_user;
+    int out_v8, slot_v8;  // outputs / slots 32-B aligned: 256-bit stores
 };
+
+
+// Next item from the ring (all lanes of the calling warp; lane 0 releases the entry).
+__device__ __forceinline__ bool fetch_item(Bars* bars, const ItemEntry* ring, int k, Item& it) {
+    const int s = k % kItemRing;
+    ptx::mbar_wait(&bars->it_full[s], (uint32_t)(k / kItemRing) & 1u);
+    const volatile int* e = reinterpret_cast<const volatile int*>(ring + s);
+    it.u = e[0];
+    it.hg = e[1];
+    it.t0 = e[2];
+    it.t1 = e[3];
+    it.Tu = e[4];
+    it.row0 = e[5];
+    it.len = e[6];
+    const int f = e[7];
+    it.first = f & 2;
+    it.last = f & 4;
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(&bars->it_empty[s]);
+    return f & 1;
+}
+
+__device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+// 32 floats to global, 256-bit stores when aligned (V8), else 128-bit
+__device__ __forceinline__ void st_f32x32(float* dst, const float (&o)[32], bool v8) {
+    if (v8) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            const uint32_t w[8] = {__float_as_uint(o[j]),     __float_as_uint(o[j + 1]), __float_as_uint(o[j + 2]),
+                                   __float_as_uint(o[j + 3]), __float_as_uint(o[j + 4]), __float_as_uint(o[j + 5]),
+                                   __float_as_uint(o[j + 6]), __float_as_uint(o[j + 7])};
+            st_v8(dst + j, w);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+    }
+}
 
 __device__ __forceinline__ void store_row(const Params& P, const Item& it, int cta, int row_in_unit,
                                           const float (&o)[32], int c0, float lse, bool write_lse, int NQrows) {
@@ -109,39 +169,41 @@ __device__ __forceinline__ void store_row(const Params& P, const Item& it, int c
     const int h = it.hg / P.G, g = it.hg % P.G;
     if (!item_complete(it)) {
         const int slot = item_slot(it, cta);
-        float* dst = P.slot_o + ((size_t)slot * NQrows + row_in_unit) * 128 + c0;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+        st_f32x32(P.slot_o + ((size_t)slot * NQrows + row_in_unit) * 128 + c0, o, P.slot_v8);
         if (write_lse) P.slot_lse[(size_t)slot * NQrows + row_in_unit] = lse;
         return;
     }
     const int i = g * NQrows + row_in_unit;
     if (P.outs.mode == OUT_PARTIAL) {
-        float* dst = reinterpret_cast<float*>(P.outs.out) + (((size_t)it.u * P.H + h) * P.S + i) * 128 + c0;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+        st_f32x32(reinterpret_cast<float*>(P.outs.out) + (((size_t)it.u * P.H + h) * P.S + i) * 128 + c0, o,
+                  P.out_v8);
         if (write_lse) P.outs.lse[((size_t)it.u * P.H + h) * P.S + i] = lse;
         return;
     }
     const size_t base = (((size_t)it.u * P.S + i) * P.H + h) * 128 + c0;
     if (P.outs.out_bf16) {
         __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(P.outs.out) + base;
+        if (P.out_v8) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-            uint4 pk;
-            pk.x = ptx::pack_bf16x2(o[j], o[j + 1]);
-            pk.y = ptx::pack_bf16x2(o[j + 2], o[j + 3]);
-            pk.z = ptx::pack_bf16x2(o[j + 4], o[j + 5]);
-            pk.w = ptx::pack_bf16x2(o[j + 6], o[j + 7]);
-            *reinterpret_cast<uint4*>(dst + j) = pk;
+            for (int j = 0; j < 32; j += 16) {
+                uint32_t w[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) w[e] = ptx::pack_bf16x2(o[j + 2 * e], o[j + 2 * e + 1]);
+                st_v8(dst + j, w);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+                uint4 pk;
+                pk.x = ptx::pack_bf16x2(o[j], o[j + 1]);
+                pk.y = ptx::pack_bf16x2(o[j + 2], o[j + 3]);
+                pk.z = ptx::pack_bf16x2(o[j + 4], o[j + 5]);
+                pk.w = ptx::pack_bf16x2(o[j + 6], o[j + 7]);
+                *reinterpret_cast<uint4*>(dst + j) = pk;
+            }
         }
     } else {
-        float* dst = reinterpret_cast<float*>(P.outs.out) + base;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+        st_f32x32(reinterpret_cast<float*>(P.outs.out) + base, o, P.out_v8);
     }
     if (write_lse && P.outs.lse) P.outs.lse[((size_t)it.u * P.H + h) * P.S + i] = lse;
 }
@@ -246,6 +308,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     uint8_t* sK = smem + C::kKOff;
     uint8_t* sV = smem + C::kVOff;
     Bars* bars = reinterpret_cast<Bars*>(smem + C::kBarOff);
+    ItemEntry* ring = reinterpret_cast<ItemEntry*>(smem + C::kRingOff);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cta = blockIdx.x, num_ctas = gridDim.x;
@@ -253,6 +316,10 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     constexpr int kRows = NQ * 128;
 
     if (threadIdx.x == 0) {
+        for (int s = 0; s < kItemRing; ++s) {
+            ptx::mbar_init(&bars->it_full[s], 1);
+            ptx::mbar_init(&bars->it_empty[s], 3 + NQ * 4);
+        }
         ptx::mbar_init(&bars->q_full, 1);
         ptx::mbar_init(&bars->q_empty, 1);
         for (int s = 0; s < C::kKStages; ++s) {
@@ -278,15 +345,8 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) {
         // record which units this CTA's partial slots will hold (read by the merge kernel)
-        ItemIter itr;
-        itr.init(P.uts, P.B, HG, cta, num_ctas);
-        Item it;
-        int s0 = -1, s1 = -1;
-        while (itr.next(it)) {
-            if (!item_complete(it)) {
-                if (it.first) s0 = it.u * HG + it.hg; else s1 = it.u * HG + it.hg;
-            }
-        }
+        int s0, s1;
+        partial_slots(P.uts, P.B, HG, cta, num_ctas, s0, s1);
         P.slot_unit[2 * cta] = s0;
         P.slot_unit[2 * cta + 1] = s1;
     }
@@ -296,8 +356,6 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
 
-    ItemIter iter;
-    iter.init(P.uts, P.B, HG, cta, num_ctas);
     Item it;
 
     if (warp < 4) {
@@ -313,15 +371,17 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int k = 0;
-            while (iter.next(it)) {
+            while (fetch_item(bars, ring, k, it)) {
                 const int h = it.hg / P.G, g = it.hg % P.G;
+                if (lane == 0) ITRACE(8, k);
                 if (k > 0) ptx::mbar_wait(&bars->q_empty, (k - 1) & 1);
+                if (lane == 0) ITRACE(9, k);
                 ptx::mbar_arrive_expect_tx_w(&bars->q_full, NQ * kTileBytes);
                 for (int q = 0; q < NQ; ++q)
                     for (int half = 0; half < 2; ++half)
                         ptx::tma_load_4d_w(sQ + q * kTileBytes + half * kHalfBytes, &mapQ, &bars->q_full, half * 64, h,
                                          g * kRows + q * 128, P.q_per_user ? it.u : 0, pol_q);
-                const int64_t row0 = P.offsets[it.u];
+                const int row0 = it.row0;
                 for (int t = it.t0; t < it.t1; ++t) {
                     ptx::mbar_wait(&bars->k_empty[stage], phase ^ 1);
                     if (k == 0 && lane == 0) VTRACE(8, t - it.t0, 0);
@@ -333,8 +393,9 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                         continue;
                     }
 #endif
+                    if (lane == 0 && t == it.t0) ITRACE(10, k);
                     ptx::mbar_arrive_expect_tx_w(&bars->k_full[stage], kTileBytes);
-                    const int32_t row = (int32_t)(row0 + (int64_t)t * kTile);
+                    const int32_t row = row0 + t * kTile;
                     for (int half = 0; half < 2; ++half)
                         ptx::tma_load_3d_w(sK + stage * kTileBytes + half * kHalfBytes, &mapK, &bars->k_full[stage],
                                          half * 64, h, row, pol_kv);
@@ -349,9 +410,10 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             bool first_item = true;
-            while (iter.next(it)) {
+            int ki = 0;
+            while (fetch_item(bars, ring, ki++, it)) {
                 const int h = it.hg / P.G;
-                const int64_t row0 = P.offsets[it.u];
+                const int row0 = it.row0;
                 for (int t = it.t0; t < it.t1; ++t) {
                     ptx::mbar_wait(&bars->v_empty[stage], phase ^ 1);
                     if (first_item && lane == 0) VTRACE(9, t - it.t0, 0);
@@ -364,7 +426,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                     }
 #endif
                     ptx::mbar_arrive_expect_tx_w(&bars->v_full[stage], kTileBytes);
-                    const int32_t row = (int32_t)(row0 + (int64_t)t * kTile);
+                    const int32_t row = row0 + t * kTile;
                     for (int half = 0; half < 2; ++half)
                         ptx::tma_load_3d_w(sV + stage * kTileBytes + half * kHalfBytes, &mapV, &bars->v_full[stage],
                                          half * 64, h, row, pol_kv);
@@ -389,7 +451,8 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
 #ifdef VISTA_TRACE
             int item_no = 0;
 #endif
-            while (iter.next(it)) {
+            int ki = 0;
+            while (fetch_item(bars, ring, ki++, it)) {
                 const int ntiles = it.t1 - it.t0;
 #ifdef VISTA_TRACE
                 if (blockIdx.x == 0 && lane == 0 && item_no < 32) {
@@ -399,9 +462,12 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 }
                 ++item_no;
 #endif
+                if (lane == 0) ITRACE(0, item_no - 1);
                 ptx::mbar_wait(&bars->q_full, q_phase);
+                if (lane == 0) ITRACE(1, item_no - 1);
                 q_phase ^= 1;
                 ptx::mbar_wait(&bars->k_full[kst], kph);
+                if (lane == 0) ITRACE(2, item_no - 1);
                 ptx::tc_fence_after();
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
@@ -410,6 +476,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 }
                 ptx::mma_commit_w(&bars->k_empty[kst]);  // K tile t0 fully consumed once these complete
                 if (++kst == C::kKStages) { kst = 0; kph ^= 1; }
+                if (ntiles == 1) ptx::mma_commit_w(&bars->q_empty);  // last S of the item: Q free early
                 for (int t = 0; t < ntiles; ++t) {
                     const bool more = t + 1 < ntiles;
                     ptx::mbar_wait(&bars->v_full[vst], vph);
@@ -423,6 +490,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                         ptx::tc_fence_after();
                         issue_PV_d<NQ>(q, vst, t > 0, tmem, sVa);
                         if (!more) {
+                            if (lane == 0 && q == NQ - 1) ITRACE(3, item_no - 1);
                             ptx::mma_commit_w(&bars->o_full[q]);
                         } else {
                             if (q == 0) {
@@ -435,16 +503,42 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                             if (q == NQ - 1) {
                                 ptx::mma_commit_w(&bars->k_empty[kst]);
                                 if (++kst == C::kKStages) { kst = 0; kph ^= 1; }
+                                // last S of the item: the next item's Q load overlaps the last PVs
+                                if (t + 2 == ntiles) ptx::mma_commit_w(&bars->q_empty);
                             }
                         }
                     }
                     ptx::mma_commit_w(&bars->v_empty[vst]);
                     if (++vst == C::kVStages) { vst = 0; vph ^= 1; }
                 }
-                ptx::mma_commit_w(&bars->q_empty);
                 first_item = false;
             }
             (void)first_item;
+        } else if (warp == 3) {
+            // ============================ item scheduler ============================
+            if (lane == 0) {
+                ItemIter iter;
+                iter.init(P.uts, P.B, HG, cta, num_ctas);
+                for (int k = 0;; ++k) {
+                    const bool ok = iter.next(it, P.uts, P.B, HG);
+                    const int s = k % kItemRing;
+                    if (k >= kItemRing) ptx::mbar_wait(&bars->it_empty[s], (uint32_t)(k / kItemRing - 1) & 1u);
+                    volatile int* e = reinterpret_cast<volatile int*>(ring + s);
+                    if (ok) {
+                        const int64_t r0 = P.offsets[it.u], r1 = P.offsets[it.u + 1];
+                        e[0] = it.u;
+                        e[1] = it.hg;
+                        e[2] = it.t0;
+                        e[3] = it.t1;
+                        e[4] = it.Tu;
+                        e[5] = (int)r0;
+                        e[6] = (int)(r1 - r0);
+                    }
+                    e[7] = ok ? (1 | (it.first ? 2 : 0) | (it.last ? 4 : 0)) : 0;
+                    ptx::mbar_arrive(&bars->it_full[s]);  // release: the entry is visible to the waiters
+                    if (!ok) break;
+                }
+            }
         }
         __syncwarp();
     } else {
@@ -459,8 +553,16 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
         const float sl2 = P.scale_log2;
         uint32_t s_phase = 0, o_phase = 0;
         bool first_item = true;
-        while (iter.next(it)) {
-            const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
+#ifdef VISTA_TRACE
+        int sitem = 0;
+#endif
+        int ki = 0;
+        while (fetch_item(bars, ring, ki++, it)) {
+#ifdef VISTA_TRACE
+            const bool itr = row == 0 && wg == 0;
+            if (itr) ITRACE(4, sitem);
+#endif
+            const int L = it.len;
             float m_used = -INFINITY, l = 0.f;
             for (int t = it.t0; t < it.t1; ++t) {
                 const bool tr = first_item && row == 0;
@@ -468,6 +570,9 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 ptx::mbar_wait(&bars->s_full[wg][0], s_phase);
                 if (tr) VTRACE(4, t - it.t0, wg);
                 s_phase ^= 1;
+#ifdef VISTA_TRACE
+                if (itr && t == it.t0) ITRACE(5, sitem);
+#endif
                 ptx::tc_fence_after();
                 uint32_t r[4][32];
 #pragma unroll
@@ -485,7 +590,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                     continue;
                 }
 #endif
-                const int64_t valid = L - (int64_t)t * kTile;
+                const int valid = L - t * kTile;
                 const bool full = valid >= kTile;
                 if (!full) {
 #pragma unroll
@@ -537,6 +642,9 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             first_item = false;
             // epilogue: O / l, lse
             ptx::mbar_wait(&bars->o_full[wg], o_phase);
+#ifdef VISTA_TRACE
+            if (itr) ITRACE(6, sitem);
+#endif
             o_phase ^= 1;
             ptx::tc_fence_after();
             const float inv_l = 1.f / l;
@@ -550,6 +658,10 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 for (int j = 0; j < 32; ++j) of[j] = __uint_as_float(o[j]) * inv_l;
                 store_row(P, it, cta, wg * 128 + row, of, c * 32, lse, c == 0, kRows);
             }
+#ifdef VISTA_TRACE
+            if (itr) ITRACE(7, sitem);
+            ++sitem;
+#endif
             if (kFusedMerge && !item_complete(it)) {
                 // Fused split-L merge: the last CTA to finish a piece of this unit combines all
                 // pieces (their slots, ascending CTA order) with the LSE merge and writes the row.
@@ -690,6 +802,8 @@ static cudaError_t launch_nq(const Problem& p, const Workspace& w, char* ws) {
     P.G = p.S / (NQ * 128);
     P.scale_log2 = p.scale * kLog2e;
     P.q_per_user = p.q_user_stride != 0;
+    P.out_v8 = (reinterpret_cast<uintptr_t>(p.outs.out) & 31) == 0;
+    P.slot_v8 = (reinterpret_cast<uintptr_t>(P.slot_o) & 31) == 0;
     static const cudaError_t attr =
         cudaFuncSetAttribute(sm100_softmax_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (attr != cudaSuccess) return attr;
@@ -699,6 +813,9 @@ static cudaError_t launch_nq(const Problem& p, const Workspace& w, char* ws) {
 int sm100_softmax_nq(int S) { return (S % 256 == 0) ? 2 : 1; }
 
 #ifdef VISTA_TRACE
+extern "C" int vista_debug_itrace(void* host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, g_vista_itrace, bytes < sizeof(g_vista_itrace) ? bytes : sizeof(g_vista_itrace));
+}
 extern "C" int vista_debug_trace(void* host, size_t bytes) {
     return (int)cudaMemcpyFromSymbol(host, g_vista_trace, bytes < sizeof(g_vista_trace) ? bytes : sizeof(g_vista_trace));
 }

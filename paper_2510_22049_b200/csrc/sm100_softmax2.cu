@@ -232,14 +232,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         ptx::fence_mbar_init();
         if (rank == 0) {
-            ItemIter itr;
-            itr.init(P.uts, P.B, HG, pair, npairs);
-            Item it;
-            int s0 = -1, s1 = -1;
-            while (itr.next(it))
-                if (!item_complete(it)) {
-                    if (it.first) s0 = it.u * HG + it.hg; else s1 = it.u * HG + it.hg;
-                }
+            int s0, s1;
+            partial_slots(P.uts, P.B, HG, pair, npairs, s0, s1);
             P.slot_unit[2 * pair] = s0;
             P.slot_unit[2 * pair + 1] = s1;
         }
@@ -267,7 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t q_full_L = ptx::mapa(ptx::smem_u32(&bars->q_full), 0);
             Cursor cs;
             int k = 0;
-            while (iter.next(it)) {
+            while (iter.next(it, P.uts, P.B, HG)) {
                 const int h = it.hg / P.G, g = it.hg % P.G;
                 if (k > 0) ptx::mbar_wait(&bars->q_empty, (k - 1) & 1);
                 ptx::mbar_arrive_expect_tx_cluster_w(q_full_L, kQBytes);
@@ -296,7 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             bool first = true;
             uint32_t q_phase = 0;
             uint32_t p_phase[2] = {0, 0};
-            while (iter.next(it)) {
+            while (iter.next(it, P.uts, P.B, HG)) {
                 const int n = it.t1 - it.t0;
                 ptx::mbar_wait(&bars->q_full, q_phase);
                 q_phase ^= 1;
@@ -357,7 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float sl2 = P.scale_log2;
         uint32_t s_phase = 0, o_phase = 0;
         bool first = true;
-        while (iter.next(it)) {
+        while (iter.next(it, P.uts, P.B, HG)) {
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
             const int n = it.t1 - it.t0;
             float m_used = -INFINITY, l = 0.f;

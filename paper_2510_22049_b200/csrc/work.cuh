@@ -21,48 +21,87 @@ struct Item {
     int hg;       // h * G + g
     int t0, t1;   // tile range [t0, t1) within the unit
     int Tu;       // tiles of the unit
+    int row0;     // offsets[u] (history row of the unit's first item; < 2^31)
+    int len;      // L_u
     bool first, last;
 };
 
+// Largest u with HG * uts[u] <= t (t < HG * uts[B]); binary search, used once per walk.
+__device__ __forceinline__ int user_of_tile(const int64_t* uts, int B, int HG, int t) {
+    int lo = 0, hi = B - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (HG * (int)uts[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
 struct ItemIter {
     // Tile counts fit in 32 bits: sum L < 2^31 (TMA coordinates), so HG * sum T < 2^30.
-    const int64_t* uts;
-    int B, HG;
+    // One binary search at the first item; afterwards the walk advances user by user (a CTA's
+    // range is contiguous), one uts[] load per user boundary instead of a log2(B)-deep search.
+    // uts / B / HG come from the kernel parameters at every call (no registers held for them).
     int t, end;
-    bool started;
+    int u, base, Tu;  // current user (-1 before the first item), its first flat tile, tiles per unit
 
-    __device__ void init(const int64_t* uts_, int B_, int HG_, int cta, int num_ctas) {
-        uts = uts_;
-        B = B_;
-        HG = HG_;
+    __device__ void init(const int64_t* uts, int B, int HG, int cta, int num_ctas) {
         const int T = HG * (int)uts[B];
         t = (int)(((unsigned long long)cta * (unsigned)T) / (unsigned)num_ctas);
         end = (int)(((unsigned long long)(cta + 1) * (unsigned)T) / (unsigned)num_ctas);
-        started = false;
+        u = -1;
     }
-    __device__ bool next(Item& it) {
+    __device__ bool next(Item& it, const int64_t* uts, int B, int HG) {
         if (t >= end) return false;
-        int lo = 0, hi = B - 1;
-        while (lo < hi) {  // largest u with HG*uts[u] <= t
-            const int mid = (lo + hi + 1) >> 1;
-            if (HG * (int)uts[mid] <= t) lo = mid; else hi = mid - 1;
+        it.first = u < 0;
+        if (u < 0) {
+            u = user_of_tile(uts, B, HG, t);
+            const int a = (int)uts[u];
+            base = HG * a;
+            Tu = (int)uts[u + 1] - a;
         }
-        const int base = HG * (int)uts[lo];
-        const int Tu = (int)(uts[lo + 1] - uts[lo]);
+        while (t >= base + HG * Tu) {  // next non-empty user (t < end <= HG * uts[B] bounds this)
+            ++u;
+            base += HG * Tu;
+            Tu = (int)uts[u + 1] - base / HG;
+        }
         const unsigned r = (unsigned)(t - base);
-        it.u = lo;
+        it.u = u;
         it.hg = (int)(r / (unsigned)Tu);
         it.t0 = (int)(r - (unsigned)it.hg * (unsigned)Tu);
         const int n = min(end - t, Tu - it.t0);
         it.t1 = it.t0 + n;
         it.Tu = Tu;
-        it.first = !started;
-        started = true;
         t += n;
         it.last = (t >= end);
         return true;
     }
 };
+
+// Units held in CTA c's partial slots 2c (first item) / 2c+1 (last item), -1 if that item is a
+// whole unit or absent.  Only the first and the last item of a range can be partial, so this
+// looks at those two directly instead of walking the range.
+__device__ __forceinline__ void partial_slots(const int64_t* uts, int B, int HG, int cta, int num_ctas, int& s0,
+                                              int& s1) {
+    s0 = s1 = -1;
+    const int T = HG * (int)uts[B];
+    const int beg = (int)(((unsigned long long)cta * (unsigned)T) / (unsigned)num_ctas);
+    const int end = (int)(((unsigned long long)(cta + 1) * (unsigned)T) / (unsigned)num_ctas);
+    if (beg >= end) return;
+    // first item: unit holding tile beg
+    int u = user_of_tile(uts, B, HG, beg);
+    int a = (int)uts[u], Tu = (int)uts[u + 1] - a;
+    int r = beg - HG * a, hg = r / Tu;
+    const int f_start = HG * a + hg * Tu, f_end = f_start + Tu;
+    if (beg > f_start || end < f_end) s0 = u * HG + hg;
+    if (end <= f_end) return;  // one item only
+    // last item: unit holding tile end-1 (starts inside the range, so partial iff cut at end)
+    u = user_of_tile(uts, B, HG, end - 1);
+    a = (int)uts[u];
+    Tu = (int)uts[u + 1] - a;
+    r = end - 1 - HG * a;
+    hg = r / Tu;
+    if (end < HG * a + (hg + 1) * Tu) s1 = u * HG + hg;
+}
 
 __device__ __forceinline__ bool item_complete(const Item& it) { return it.t0 == 0 && it.t1 == it.Tu; }
 

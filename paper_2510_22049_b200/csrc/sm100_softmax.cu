@@ -208,6 +208,70 @@ __device__ __forceinline__ void store_row(const Params& P, const Item& it, int c
     if (write_lse && P.outs.lse) P.outs.lse[((size_t)it.u * P.H + h) * P.S + i] = lse;
 }
 
+// lse of one row (natural log): partial slot or the caller's lse output (if any)
+__device__ __forceinline__ void store_lse(const Params& P, const Item& it, int cta, int row, float lse, int NQrows) {
+    if (!item_complete(it)) {
+        P.slot_lse[(size_t)item_slot(it, cta) * NQrows + row] = lse;
+        return;
+    }
+    if (!P.outs.lse) return;
+    const int h = it.hg / P.G, g = it.hg % P.G;
+    P.outs.lse[((size_t)it.u * P.H + h) * P.S + g * NQrows + row] = lse;
+}
+
+// Start of output row `row` (row within the unit's NQ*128 rows) of item `it`: a partial slot row
+// (f32) for a split unit, else the final output row (bf16 or f32).
+__device__ __forceinline__ char* out_row_ptr(const Params& P, const Item& it, int cta, int row, int NQrows) {
+    if (!item_complete(it))
+        return reinterpret_cast<char*>(P.slot_o + ((size_t)item_slot(it, cta) * NQrows + row) * 128);
+    const int h = it.hg / P.G, g = it.hg % P.G;
+    const int i = g * NQrows + row;
+    if (P.outs.mode == OUT_PARTIAL)
+        return reinterpret_cast<char*>(P.outs.out) + ((((size_t)it.u * P.H + h) * P.S + i) * 128) * 4;
+    return reinterpret_cast<char*>(P.outs.out) +
+           ((((size_t)it.u * P.S + i) * P.H + h) * 128) * (P.outs.out_bf16 ? 2 : 4);
+}
+
+// Coalesced epilogue store of 256 bytes per row (64 32-bit words v[] of the calling thread's row,
+// byte offset `boff` in the row).  The row-per-thread layout of the accumulator would make every
+// warp store touch 32 rows (32 lines); instead the words go back to TMEM (the O columns at tcol,
+// already read) in a permuted column order and come out again with the 16x256b shape, where the 4
+// threads of a quad hold 128 contiguous bytes of one row: each warp store then writes 8 full
+// 128-B lines.  Column 8g + 2p + e holds word 8p + 2g + e (g < 4) or 32 + 8p + 2(g-4) + e (g >= 4).
+__device__ __forceinline__ void store_rows_coalesced(const Params& P, const Item& it, int cta, int row0, int NQrows,
+                                                     uint32_t tcol_warp, const uint32_t (&v)[64], int boff) {
+    const int lane = threadIdx.x & 31;
+    uint32_t a[32], b[32];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) {
+        const int g = c >> 3, p = (c & 7) >> 1, e = c & 1;
+        const int w = g < 4 ? 8 * p + 2 * g + e : 32 + 8 * p + 2 * (g - 4) + e;
+        if (c < 32) a[c] = v[w]; else b[c - 32] = v[w];
+    }
+    ptx::tmem_st32(tcol_warp, a);
+    ptx::tmem_st32(tcol_warp + 32, b);
+    ptx::tmem_wait_st();
+    const int p = lane & 3;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        uint32_t r[32];
+        ptx::tmem_ld16x256b_x8(tcol_warp + ((uint32_t)(16 * half) << 16), r);
+        ptx::tmem_wait_ld();
+        ptx::reg_fence(r);
+        const int ra = row0 + 16 * half + (lane >> 2);
+        char* pa = out_row_ptr(P, it, cta, ra, NQrows) + boff + 32 * p;
+        char* pb = out_row_ptr(P, it, cta, ra + 8, NQrows) + boff + 32 * p;
+        const uint32_t a0[8] = {r[0], r[1], r[4], r[5], r[8], r[9], r[12], r[13]};
+        const uint32_t a1[8] = {r[16], r[17], r[20], r[21], r[24], r[25], r[28], r[29]};
+        const uint32_t b0[8] = {r[2], r[3], r[6], r[7], r[10], r[11], r[14], r[15]};
+        const uint32_t b1[8] = {r[18], r[19], r[22], r[23], r[26], r[27], r[30], r[31]};
+        st_v8(pa, a0);
+        st_v8(pa + 128, a1);
+        st_v8(pb, b0);
+        st_v8(pb + 128, b1);
+    }
+}
+
 // p = 2^(s * scale * log2 e - m) for one 128-key row: packed FFMA2, exp2 on MUFU (ex2.approx) and,
 // for EMU of every 8 pairs, on the FMA pipe (exp2_emu2; only for tiles without masked keys);
 // bf16x2 pack; P overwrites the first 64 TMEM columns of S (16 columns per 32 keys).  Returns the
@@ -649,15 +713,46 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             ptx::tc_fence_after();
             const float inv_l = 1.f / l;
             const float lse = (m_used + __log2f(l)) * kLn2;
+            const bool complete = item_complete(it);
+            const bool coalesced = complete ? P.out_v8 : P.slot_v8;
+            const bool out16 = complete && P.outs.mode != OUT_PARTIAL && P.outs.out_bf16;
+            if (coalesced && out16) {
+                uint32_t v[64];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t o[32];
-                ptx::tmem_ld32_sync(tO + c * 32, o);
-                float of[32];
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t o[32];
+                    ptx::tmem_ld32_sync(tO + c * 32, o);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) of[j] = __uint_as_float(o[j]) * inv_l;
-                store_row(P, it, cta, wg * 128 + row, of, c * 32, lse, c == 0, kRows);
+                    for (int j = 0; j < 16; ++j)
+                        v[c * 16 + j] = ptx::pack_bf16x2(__uint_as_float(o[2 * j]) * inv_l,
+                                                         __uint_as_float(o[2 * j + 1]) * inv_l);
+                }
+                store_rows_coalesced(P, it, cta, wg * 128 + wq * 32, kRows, tO, v, 0);
+            } else if (coalesced) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    uint32_t v[64];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t o[32];
+                        ptx::tmem_ld32_sync(tO + hh * 64 + c * 32, o);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[c * 32 + j] = __float_as_uint(__uint_as_float(o[j]) * inv_l);
+                    }
+                    store_rows_coalesced(P, it, cta, wg * 128 + wq * 32, kRows, tO + hh * 64, v, hh * 256);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t o[32];
+                    ptx::tmem_ld32_sync(tO + c * 32, o);
+                    float of[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) of[j] = __uint_as_float(o[j]) * inv_l;
+                    store_row(P, it, cta, wg * 128 + row, of, c * 32, lse, false, kRows);
+                }
             }
+            store_lse(P, it, cta, wg * 128 + row, lse, kRows);
 #ifdef VISTA_TRACE
             if (itr) ITRACE(7, sitem);
             ++sitem;

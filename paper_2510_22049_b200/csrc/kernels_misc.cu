@@ -12,6 +12,7 @@
 #include <math.h>
 
 #include "internal.h"
+#include "sm100_ptx.cuh"
 
 namespace vista {
 
@@ -142,50 +143,154 @@ __device__ __forceinline__ bool slot_is_head(const int* slot_unit, int s, int n)
     return true;
 }
 
-// One warp per output row; lanes over 128 channels (float4).  rows = query rows per unit.
-__global__ void merge_softmax_slots_kernel(const int* __restrict__ slot_unit, int num_slots, const float* __restrict__ slot_o,
-                                           const float* __restrict__ slot_lse, int rows, OutSpec outs, int S, int H,
-                                           int G) {
+// Vectorized store of 4 consecutive channels [c, c+4) of one output row.
+__device__ __forceinline__ void out_store4(const OutSpec& o, int S, int H, int u, int h, int i, int c, float4 v) {
+    if (o.mode == OUT_PARTIAL) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(o.out) + (((size_t)u * H + h) * S + i) * 128 + c) = v;
+        return;
+    }
+    const size_t idx = (((size_t)u * S + i) * H + h) * 128 + c;
+    if (o.out_bf16) {
+        uint2 pk;
+        pk.x = ptx::pack_bf16x2(v.x, v.y);
+        pk.y = ptx::pack_bf16x2(v.z, v.w);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(o.out) + idx) = pk;
+    } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(o.out) + idx) = v;
+    }
+}
+
+// LSE merge of the run of partial slots of each split unit.  Block = (slot s, 32 rows), 8 warps x
+// 4 rows, lanes over 128 channels (float4); blocks whose slot does not start a run exit at once.
+// Warp 0 lists the run's slots (lane-parallel over 32 positions at a time: a run ends at the first
+// slot holding another unit, -1 slots are unused); then the members' 32-row slabs of o (16 KB
+// each, contiguous) and lse stream into shared memory by bulk copy, two members per stage,
+// double-buffered, and the rows are combined with an online max (any run length).
+constexpr int kMergeRows = 32;
+constexpr int kMergeMaxRun = 320;  // >= 2 * max CTAs a unit can span + 2
+struct MergeSmem {
+    float o[2][2][kMergeRows * 128];  // [stage][member][row * 128 + channel]
+    float lse[2][2][kMergeRows];
+    uint64_t full[2];
+    int list[kMergeMaxRun];
+    int count, n, head;
+};
+
+__global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __restrict__ slot_unit, int num_slots,
+                                                                  const float* __restrict__ slot_o,
+                                                                  const float* __restrict__ slot_lse, int rows,
+                                                                  OutSpec outs, int S, int H, int G) {
+    extern __shared__ __align__(128) uint8_t merge_smem_raw[];
+    MergeSmem& sm = *reinterpret_cast<MergeSmem*>(merge_smem_raw);
     const int s = blockIdx.x;
-    const int n = slot_unit[s];
-    if (n < 0 || !slot_is_head(slot_unit, s, n)) return;
-    const int row = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (row >= rows) return;
-    float M = -INFINITY;
-    for (int x = s; x < num_slots; ++x) {
-        const int m = slot_unit[x];
-        if (m < 0) continue;
-        if (m != n) break;
-        M = fmaxf(M, slot_lse[(size_t)x * rows + row]);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int row0 = blockIdx.y * kMergeRows;
+    if (warp == 0) {
+        // positions s-1 .. s+30 (lane 0 = the slot before s, for the run-head test)
+        const int x = s - 1 + lane;
+        int m = (x >= 0 && x < num_slots) ? slot_unit[x] : -2;
+        const int n = __shfl_sync(0xffffffffu, m, 1);
+        int prev = __shfl_sync(0xffffffffu, m, 0);
+        if (prev == -1) {  // walk back over unused slots (rare)
+            for (int p = s - 2; p >= 0; --p) {
+                prev = slot_unit[p];
+                if (prev >= 0) break;
+            }
+        }
+        const bool head = n >= 0 && prev != n;
+        int count = 0;
+        if (head) {
+            bool own = lane >= 1;
+            for (int c0 = s - 1;; c0 += 32) {
+                if (c0 != s - 1) {
+                    const int xx = c0 + lane;
+                    m = xx < num_slots ? slot_unit[xx] : -2;
+                    own = true;
+                }
+                const unsigned stop = __ballot_sync(0xffffffffu, own && (m == -2 || (m >= 0 && m != n)));
+                const int lim = stop ? __ffs(stop) - 1 : 32;
+                const bool mem = own && lane < lim && m == n;
+                const unsigned mask = __ballot_sync(0xffffffffu, mem);
+                if (mem && count + __popc(mask & ((1u << lane) - 1)) < kMergeMaxRun)
+                    sm.list[count + __popc(mask & ((1u << lane) - 1))] = c0 + lane;
+                count = min(count + __popc(mask), kMergeMaxRun);
+                if (stop) break;
+            }
+        }
+        if (lane == 0) {
+            sm.n = n;
+            sm.head = head && row0 < rows;
+            sm.count = count;
+            ptx::mbar_init(&sm.full[0], 1);
+            ptx::mbar_init(&sm.full[1], 1);
+            ptx::fence_mbar_init();
+        }
     }
-    float l = 0.f;
-    for (int x = s; x < num_slots; ++x) {
-        const int m = slot_unit[x];
-        if (m < 0) continue;
-        if (m != n) break;
-        l += expf(slot_lse[(size_t)x * rows + row] - M);
+    __syncthreads();
+    if (!sm.head) return;
+    const int n = sm.n, R = sm.count;
+    const int ngroups = (R + 1) / 2;
+    auto issue = [&](int gi) {  // thread 0: bulk copies of group gi (members 2 gi, 2 gi + 1)
+        const int st = gi & 1;
+        const int k = min(2, R - 2 * gi);
+        ptx::mbar_arrive_expect_tx(&sm.full[st], (uint32_t)k * (kMergeRows * 128 * 4 + kMergeRows * 4));
+        for (int j = 0; j < k; ++j) {
+            const int slot = sm.list[2 * gi + j];
+            ptx::bulk_g2s(ptx::smem_u32(sm.o[st][j]), slot_o + ((size_t)slot * rows + row0) * 128,
+                          kMergeRows * 128 * 4, &sm.full[st]);
+            ptx::bulk_g2s(ptx::smem_u32(sm.lse[st][j]), slot_lse + (size_t)slot * rows + row0, kMergeRows * 4,
+                          &sm.full[st]);
+        }
+    };
+    if (threadIdx.x == 0) {
+        issue(0);
+        if (ngroups > 1) issue(1);
     }
-    const float lse = M + logf(l);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int x = s; x < num_slots; ++x) {
-        const int m = slot_unit[x];
-        if (m < 0) continue;
-        if (m != n) break;
-        const float w = expf(slot_lse[(size_t)x * rows + row] - lse);
-        const float4 o = reinterpret_cast<const float4*>(slot_o + ((size_t)x * rows + row) * 128)[lane];
-        acc.x += w * o.x;
-        acc.y += w * o.y;
-        acc.z += w * o.z;
-        acc.w += w * o.w;
+    float M[4], l[4];
+    float4 acc[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        M[r] = -INFINITY;
+        l[r] = 0.f;
+        acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int gi = 0; gi < ngroups; ++gi) {
+        const int st = gi & 1;
+        const int k = min(2, R - 2 * gi);
+        ptx::mbar_wait(&sm.full[st], (uint32_t)(gi >> 1) & 1u);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int rl = warp * 4 + r;  // row within the block's 32
+            const float l0 = sm.lse[st][0][rl];
+            const float l1 = k > 1 ? sm.lse[st][1][rl] : -INFINITY;
+            const float Mn = fmaxf(M[r], fmaxf(l0, l1));
+            const float sc = __expf(M[r] - Mn);
+            const float w0 = __expf(l0 - Mn), w1 = k > 1 ? __expf(l1 - Mn) : 0.f;
+            const float4 o0 = reinterpret_cast<const float4*>(sm.o[st][0] + rl * 128)[lane];
+            const float4 o1 = k > 1 ? reinterpret_cast<const float4*>(sm.o[st][1] + rl * 128)[lane]
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            acc[r].x = acc[r].x * sc + w0 * o0.x + w1 * o1.x;
+            acc[r].y = acc[r].y * sc + w0 * o0.y + w1 * o1.y;
+            acc[r].z = acc[r].z * sc + w0 * o0.z + w1 * o1.z;
+            acc[r].w = acc[r].w * sc + w0 * o0.w + w1 * o1.w;
+            l[r] = l[r] * sc + w0 + w1;
+            M[r] = Mn;
+        }
+        __syncthreads();  // stage st free again
+        if (threadIdx.x == 0 && gi + 2 < ngroups) issue(gi + 2);
     }
     const int HG = H * G;
     const int u = n / HG, hg = n % HG, h = hg / G, g = hg % G;
-    const int i = g * rows + row;
-    out_store(outs, S, H, 128, u, h, i, lane * 4 + 0, acc.x);
-    out_store(outs, S, H, 128, u, h, i, lane * 4 + 1, acc.y);
-    out_store(outs, S, H, 128, u, h, i, lane * 4 + 2, acc.z);
-    out_store(outs, S, H, 128, u, h, i, lane * 4 + 3, acc.w);
-    if (lane == 0) lse_store(outs, S, H, u, h, i, lse);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int row = row0 + warp * 4 + r;
+        if (row >= rows) break;
+        const float inv = 1.f / l[r];
+        const float4 v = make_float4(acc[r].x * inv, acc[r].y * inv, acc[r].z * inv, acc[r].w * inv);
+        const int i = g * rows + row;
+        out_store4(outs, S, H, u, h, i, lane * 4, v);
+        if (lane == 0) lse_store(outs, S, H, u, h, i, M[r] + logf(l[r]));
+    }
 }
 
 // Sum the run of QLA state slots of each split unit into zbuf[unit] (d = 128 rows of 128).
@@ -530,8 +635,12 @@ cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf, int* 
 
 cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, char* ws) {
     const int num_slots = 2 * w.num_ctas;
-    dim3 grid(num_slots, (w.rows_per_unit + 7) / 8);
-    merge_softmax_slots_kernel<<<grid, 256, 0, p.stream>>>(
+    dim3 grid(num_slots, (w.rows_per_unit + kMergeRows - 1) / kMergeRows);
+    static const cudaError_t attr = cudaFuncSetAttribute(merge_softmax_slots_kernel,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)sizeof(MergeSmem));
+    if (attr != cudaSuccess) return attr;
+    merge_softmax_slots_kernel<<<grid, 256, sizeof(MergeSmem), p.stream>>>(
         reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots, reinterpret_cast<const float*>(ws + w.slot_o_off),
         reinterpret_cast<const float*>(ws + w.slot_lse_off), w.rows_per_unit, p.outs, p.S, p.H, p.S / w.rows_per_unit);
     return cudaGetLastError();

@@ -38,10 +38,35 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+#ifndef VISTA_WAIT_HINT_NS  // try_wait suspend-time hint (0: no hint operand, HW default window)
+#define VISTA_WAIT_HINT_NS 0
+#endif
+#ifndef VISTA_WAIT_SPIN  // non-blocking test_wait polls before the first (suspending) try_wait
+#define VISTA_WAIT_SPIN 0
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
+#if VISTA_WAIT_HINT_NS > 0
     asm volatile(
-        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, 10000000;\n\t"
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "n"(VISTA_WAIT_HINT_NS)
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+#endif
+    return ok != 0;
+}
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
         "selp.b32 %0, 1, 0, P;\n\t}"
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
@@ -56,6 +81,11 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // Wait until the phase with the given parity has completed.  A protocol bug would otherwise
 // hang the GPU: after 4 s of waiting (far beyond any legitimate wait) trap instead.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if VISTA_WAIT_SPIN > 0
+#pragma unroll 1
+    for (int i = 0; i < VISTA_WAIT_SPIN; ++i)
+        if (mbar_test_wait(bar, parity)) return;
+#endif
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
     while (!mbar_try_wait(bar, parity)) {
@@ -103,6 +133,13 @@ __device__ __forceinline__ void bulk_g2s_w(uint32_t dst_smem, const void* src, u
             dst_smem),
         "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+
+// Single-thread variant (the caller elects the issuing thread).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // Generic-proxy smem writes -> visible to the async proxy (tensor core / TMA).

@@ -59,7 +59,8 @@ constexpr bool kFusedMerge = false;
 #ifndef VISTA_EMU_PER_EIGHT
 #define VISTA_EMU_PER_EIGHT 0
 #endif
-constexpr int kEmuPerEight = VISTA_EMU_PER_EIGHT;  // exp2 on the FMA pipe for this many of every 8 score pairs
+constexpr int kEmuPerEight = VISTA_EMU_PER_EIGHT;
+  // exp2 on the FMA pipe for this many of every 8 score pairs
 #ifndef VISTA_CTL_REGS
 #define VISTA_CTL_REGS 152
 #endif

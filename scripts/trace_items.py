@@ -28,19 +28,19 @@ for _ in range(3):
     vista.summarize(q, K, V, ot, int(off[-1]))
 torch.cuda.synchronize()
 lib = vista.load()
-buf = np.zeros((12, 64), dtype=np.uint64)
+buf = np.zeros((16, 64), dtype=np.uint64)
 lib.vista_debug_itrace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert lib.vista_debug_itrace(buf.ctypes.data, buf.nbytes) == 0
 t0 = int(buf[0, 0])
 ev = buf.astype(np.int64) - t0
 names = ["mma_start", "mma_q", "mma_k", "mma_lastPV", "sm_start", "sm_S0", "sm_O", "sm_epi_done",
-         "pr_pre_qe", "pr_qe", "pr_K0"]
+         "pr_pre_qe", "pr_qe", "pr_K0", "mma_end", "sch_pub", "sch_pre_e", "sch_got_e"]
 print(f"L={L} S={S} H={H} B={B}")
 print("item " + " ".join(f"{n:>11s}" for n in names))
 for i in range(40):
     if buf[0, i] == 0:
         break
-    print(f"{i:4d} " + " ".join(f"{int(ev[e, i]):11d}" for e in range(11)))
+    print(f"{i:4d} " + " ".join(f"{int(ev[e, i]):11d}" for e in range(15)))
 n = 30
 if buf[0, n] != 0:
     per = np.diff(ev[0, 5:n]).mean()

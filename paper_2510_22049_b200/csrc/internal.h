@@ -83,9 +83,15 @@ cudaError_t launch_sm100_softmax(const Problem& p, const Workspace& w, char* ws)
 // 2-CTA (cta_group::2) variant for S % 256 == 0; w.num_ctas counts CTA PAIRS
 cudaError_t launch_sm100_softmax2(const Problem& p, const Workspace& w, char* ws);
 bool softmax_uses_pairs(const Problem& p);
-cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf);
+// wbuf != NULL: complete units write W = phi2(Z / N) (bf16 finalize operand) instead of Z to zbuf
+cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf,
+                                   uint8_t* wbuf = nullptr);
 cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, char* ws);
 cudaError_t launch_merge_qla_slots(const Problem& p, const Workspace& w, char* ws, float* zbuf);
+// split units' W = phi2(sum of slots / N) into wbuf (fused finalize path)
+cudaError_t launch_merge_qla_slots_w(const Problem& p, const Workspace& w, char* ws, uint8_t* wbuf);
+// finalize from the W operands already at ws (sm100_qla_finalize_workspace layout: W then phi1(Q))
+cudaError_t launch_sm100_qla_finalize_fused(const Problem& p, uint8_t* ws);
 cudaError_t launch_simt_softmax(const Problem& p);
 cudaError_t launch_simt_qla_state(const Problem& p, float* zbuf);
 // O = phi1(Q) phi2( (sum_{p<P} Z_p) / N_u ) ; Z parts at zparts + p * part_stride (floats),

@@ -12,6 +12,7 @@
 #include <math.h>
 
 #include "internal.h"
+#include "qla_common.cuh"
 #include "sm100_ptx.cuh"
 
 namespace vista {
@@ -312,6 +313,35 @@ __global__ void merge_qla_slots_kernel(const int* __restrict__ slot_unit, int nu
         acc.w += o.w;
     }
     reinterpret_cast<float4*>(zbuf + ((size_t)n * 128 + row) * 128)[lane] = acc;
+}
+
+// Fused-finalize variant: W[n] = phi2((sum of the run's Z) / N_u) as the bf16 swizzled operand.
+__global__ void merge_qla_slots_w_kernel(const int* __restrict__ slot_unit, int num_slots, const float* __restrict__ slot_o,
+                                         const int64_t* __restrict__ offsets, int H, int phi2, int normalize,
+                                         uint8_t* __restrict__ wbuf) {
+    const int s = blockIdx.x;
+    const int n = slot_unit[s];
+    if (n < 0 || !slot_is_head(slot_unit, s, n)) return;
+    const int row = blockIdx.y * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int x = s; x < num_slots; ++x) {
+        const int m = slot_unit[x];
+        if (m < 0) continue;
+        if (m != n) break;
+        const float4 o = reinterpret_cast<const float4*>(slot_o + ((size_t)x * 128 + row) * 128)[lane];
+        acc.x += o.x;
+        acc.y += o.y;
+        acc.z += o.z;
+        acc.w += o.w;
+    }
+    const int u = n / H;
+    const int64_t N = offsets[u + 1] - offsets[u];
+    const float inv = (normalize && N > 0) ? 1.f / (float)N : 1.f;
+    uint2 pk;
+    pk.x = ptx::pack_bf16x2(qla_act(phi2, acc.x * inv), qla_act(phi2, acc.y * inv));
+    pk.y = ptx::pack_bf16x2(qla_act(phi2, acc.z * inv), qla_act(phi2, acc.w * inv));
+    const int col = lane * 4;
+    *reinterpret_cast<uint2*>(wbuf + (size_t)n * (2 * 128 * 128) + qla_w_swz(row, col) + (col & 7) * 2) = pk;
 }
 
 // P stacked partials part_o [P,B,H,S,d] / part_lse [P,B,H,S] -> outs (FINAL).  One warp per row.
@@ -643,6 +673,15 @@ cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, cha
     merge_softmax_slots_kernel<<<grid, 256, sizeof(MergeSmem), p.stream>>>(
         reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots, reinterpret_cast<const float*>(ws + w.slot_o_off),
         reinterpret_cast<const float*>(ws + w.slot_lse_off), w.rows_per_unit, p.outs, p.S, p.H, p.S / w.rows_per_unit);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_qla_slots_w(const Problem& p, const Workspace& w, char* ws, uint8_t* wbuf) {
+    const int num_slots = 2 * w.num_ctas;
+    dim3 grid(num_slots, 128 / 8);
+    merge_qla_slots_w_kernel<<<grid, 256, 0, p.stream>>>(reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots,
+                                                         reinterpret_cast<const float*>(ws + w.slot_o_off), p.offsets,
+                                                         p.H, p.phi2, p.normalize, wbuf);
     return cudaGetLastError();
 }
 

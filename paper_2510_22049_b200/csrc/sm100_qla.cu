@@ -17,6 +17,7 @@
 
 #include "internal.h"
 #include "sm100_ptx.cuh"
+#include "qla_common.cuh"
 #include "work.cuh"
 
 namespace vista {
@@ -46,8 +47,9 @@ struct Params {
     const int64_t* uts;
     int* slot_unit;
     float* slot_o;
-    float* zbuf;
-    int B, H, phi1;
+    float* zbuf;      // complete units' Z (f32) -- unless wbuf is set
+    uint8_t* wbuf;    // fused finalize: complete units' W = phi2(Z / N) (bf16 MMA operand) instead
+    int B, H, phi1, phi2, normalize;
 };
 
 __device__ __forceinline__ float phi(int kind, float x) {
@@ -255,6 +257,36 @@ __global__ void __launch_bounds__(kThreads, 1)
             zphase[zb] ^= 1;
             ptx::tc_fence_after();
             const int c1 = wq * 32 + lane;
+            if (P.wbuf && item_complete(it)) {
+                // W[c1][c2] = phi2(Z[c1][c2] / N) as the bf16 B operand of the finalize GEMM
+                // (MN-major, 128-B swizzled halves of 64 columns: qla_w_swz)
+                const float inv = (P.normalize && L > 0) ? 1.f / (float)L : 1.f;
+                uint8_t* wdst = P.wbuf + (size_t)(it.u * HG + it.hg) * kTileBytes;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t r[32];
+                    ptx::tmem_ld32_sync(tmem + lane_bits + zb * 128 + chalf * 64 + c * 32, r);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 pk;
+                        uint32_t* pw = &pk.x;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            // same packed activation as the K transform (phi2x): W is a bf16 operand
+                            const uint32_t zz = ptx::pack_bf16x2(__uint_as_float(r[8 * q + 2 * e]) * inv,
+                                                                 __uint_as_float(r[8 * q + 2 * e + 1]) * inv);
+                            pw[e] = P.phi2 == VISTA_ACT_SILU ? silu_bf16x2(zz)
+                                  : P.phi2 == VISTA_ACT_SHIFTED_ELU ? phi_bf16x2(VISTA_ACT_SHIFTED_ELU, zz)
+                                                                    : zz;
+                        }
+                        *reinterpret_cast<uint4*>(wdst + qla_w_swz(c1, chalf * 64 + c * 32 + 8 * q)) = pk;
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bars->z_empty[zb]);
+                ++k;
+                continue;
+            }
             float* dst;
             if (item_complete(it)) dst = P.zbuf + ((size_t)(it.u * HG + it.hg) * 128 + c1) * 128;
             else dst = P.slot_o + ((size_t)item_slot(it, cta) * 128 + c1) * 128;
@@ -290,7 +322,7 @@ static cudaError_t launch_phi(const Problem& p, const Workspace& w, const CUtens
     return cudaGetLastError();
 }
 
-cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf) {
+cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf, uint8_t* wbuf) {
     CUtensorMap mk, mv;
     if (!make_kv_map(&mk, p.k, p.total_len, p.H) || !make_kv_map(&mv, p.v, p.total_len, p.H))
         return cudaErrorInvalidValue;
@@ -300,9 +332,12 @@ cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* w
     P.slot_unit = reinterpret_cast<int*>(ws + w.slot_unit_off);
     P.slot_o = reinterpret_cast<float*>(ws + w.slot_o_off);
     P.zbuf = zbuf;
+    P.wbuf = wbuf;
     P.B = p.B;
     P.H = p.H;
     P.phi1 = p.phi1;
+    P.phi2 = p.phi2;
+    P.normalize = p.normalize;
     return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU>(p, w, mk, mv, P)
          : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU>(p, w, mk, mv, P)
                                            : launch_phi<VISTA_ACT_IDENTITY>(p, w, mk, mv, P);

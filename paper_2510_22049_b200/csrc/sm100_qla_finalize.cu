@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 
 #include "internal.h"
+#include "qla_common.cuh"
 #include "sm100_ptx.cuh"
 
 namespace vista {
@@ -17,18 +18,8 @@ namespace {
 constexpr int kHalf = 128 * 128;  // bytes of one [128 rows][64 bf16] swizzled half
 constexpr int kOp = 2 * kHalf;    // one 128 x 128 bf16 operand
 
-__device__ __forceinline__ float act(int kind, float x) {
-    if (kind == VISTA_ACT_SILU) return x * __frcp_rn(1.f + __expf(-x));
-    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? x : __expf(x - 1.f);
-    return x;
-}
-
-// byte offset of element (row, col) in a [128][128] bf16 operand stored as two 128-B-swizzled
-// halves of 64 columns: 16-B chunk index XOR (row mod 8) within each 128-B row
-__device__ __forceinline__ uint32_t swz(int row, int col) {
-    const int half = col >> 6, chunk = (col & 63) >> 3;
-    return half * kHalf + row * 128 + ((chunk ^ (row & 7)) << 4);
-}
+__device__ __forceinline__ float act(int kind, float x) { return qla_act(kind, x); }
+__device__ __forceinline__ uint32_t swz(int row, int col) { return qla_w_swz(row, col); }
 
 // Prep 1 (grid = units x 4): W[unit] = phi2((sum_p Z_p) / N_u) as a bf16 [128][128] MN-major
 // operand (B[K = c1][N = c2], c2 contiguous), pre-swizzled so the MMA kernel can bulk-copy it.
@@ -90,9 +81,12 @@ __global__ void __launch_bounds__(256) qla_prep_q_kernel(const __nv_bfloat16* __
 
 // One CTA per (128 query rows, user, head): bulk-copy the two prepared operands, one 128x128x128
 // tcgen05 MMA chain into TMEM, rows out.
+// offsets != NULL (fused path, W written by the state kernel / slot merge): an empty user has no
+// W in wbuf and uses the constant W = phi2(0), the value the Z = 0 path gives.
 __global__ void __launch_bounds__(128) sm100_qla_finalize_kernel(const uint8_t* __restrict__ abuf,
                                                                  const uint8_t* __restrict__ wbuf, int q_per_user,
-                                                                 int S, int H, OutSpec outs) {
+                                                                 int S, int H, OutSpec outs,
+                                                                 const int64_t* __restrict__ offsets, int phi2) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
     __shared__ uint64_t bar_in, bar_mma;
@@ -102,6 +96,7 @@ __global__ void __launch_bounds__(128) sm100_qla_finalize_kernel(const uint8_t* 
     const int nblk = (S + 127) / 128;
     const int blk = blockIdx.x, unit = blockIdx.y, u = unit / H, h = unit % H;
     const int i = blk * 128 + r;
+    const bool empty = offsets && offsets[u + 1] == offsets[u];
     if (warp == 0) ptx::tmem_alloc(&tmem_slot, 128);
     if (r == 0) {
         ptx::mbar_init(&bar_in, 1);
@@ -112,12 +107,19 @@ __global__ void __launch_bounds__(128) sm100_qla_finalize_kernel(const uint8_t* 
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_slot, 0);
+    if (empty) {  // W = phi2(0) everywhere (a constant: layout-free)
+        uint8_t* sm = smem_raw + (base - ptx::smem_u32(smem_raw));
+        const uint32_t c2 = ptx::pack_bf16x2(act(phi2, 0.f), act(phi2, 0.f));
+        for (int e = r; e < kOp / 16; e += 128) *reinterpret_cast<uint4*>(sm + kOp + e * 16) = make_uint4(c2, c2, c2, c2);
+        ptx::fence_proxy_async_smem();
+        __syncthreads();
+    }
     if (warp == 0) {
         const uint8_t* a = abuf + ((size_t)((q_per_user ? u : 0) * H + h) * nblk + blk) * kOp;
         const uint8_t* w = wbuf + (size_t)unit * kOp;
-        ptx::mbar_arrive_expect_tx_w(&bar_in, 2 * kOp);
+        ptx::mbar_arrive_expect_tx_w(&bar_in, empty ? kOp : 2 * kOp);
         ptx::bulk_g2s_w(sA, a, kOp, &bar_in);
-        ptx::bulk_g2s_w(sB, w, kOp, &bar_in);
+        if (!empty) ptx::bulk_g2s_w(sB, w, kOp, &bar_in);
         ptx::mbar_wait(&bar_in, 0);
         ptx::tc_fence_after();
         constexpr uint32_t idO = ptx::idesc_bf16_f32(128, 128, 0, 1);  // A K-major, B MN-major
@@ -185,7 +187,26 @@ cudaError_t launch_sm100_qla_finalize(const Problem& p, const float* zparts, int
         cudaFuncSetAttribute(sm100_qla_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (attr != cudaSuccess) return attr;
     dim3 grid(nblk, p.B * p.H);
-    sm100_qla_finalize_kernel<<<grid, 128, smem, p.stream>>>(abuf, wbuf, p.q_user_stride != 0, p.S, p.H, p.outs);
+    sm100_qla_finalize_kernel<<<grid, 128, smem, p.stream>>>(abuf, wbuf, p.q_user_stride != 0, p.S, p.H, p.outs,
+                                                             nullptr, p.phi2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sm100_qla_finalize_fused(const Problem& p, uint8_t* ws) {
+    if (p.B == 0) return cudaSuccess;
+    const int nblk = (p.S + 127) / 128;
+    const int bq = p.q_user_stride ? p.B : 1;
+    uint8_t* wbuf = ws;
+    uint8_t* abuf = wbuf + (size_t)p.B * p.H * kOp;
+    qla_prep_q_kernel<<<bq * p.H * nblk * 4, 256, 0, p.stream>>>(reinterpret_cast<const __nv_bfloat16*>(p.q),
+                                                                 p.q_user_stride, p.S, p.H, p.phi1, abuf);
+    const int smem = 2 * kOp + 1024;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(sm100_qla_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) return attr;
+    dim3 grid(nblk, p.B * p.H);
+    sm100_qla_finalize_kernel<<<grid, 128, smem, p.stream>>>(abuf, wbuf, p.q_user_stride != 0, p.S, p.H, p.outs,
+                                                             p.offsets, p.phi2);
     return cudaGetLastError();
 }
 

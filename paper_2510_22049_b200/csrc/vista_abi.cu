@@ -238,6 +238,18 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
             break;
         }
         case PATH_SM100_QLA: {
+            if (!partial && qla_finalize_uses_tc(p)) {
+                // fused: state epilogue / slot merge write the finalize GEMM's W operand directly
+                uint8_t* wbuf = reinterpret_cast<uint8_t*>(ws + w.fin_off);
+                if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), nullptr)) != cudaSuccess) break;
+                if ((e = timed_main(p.stream, [&] { return launch_sm100_qla_state(p, w, ws, nullptr, wbuf); })) !=
+                    cudaSuccess)
+                    break;
+                if ((e = launch_merge_qla_slots_w(p, w, ws, wbuf)) != cudaSuccess) break;
+                e = launch_sm100_qla_finalize_fused(p, wbuf);
+                nlaunch = 4;
+                break;
+            }
             float* zbuf = partial ? reinterpret_cast<float*>(outs.out) : reinterpret_cast<float*>(ws + w.zbuf_off);
             if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), zbuf)) != cudaSuccess) break;
             if ((e = timed_main(p.stream, [&] { return launch_sm100_qla_state(p, w, ws, zbuf); })) != cudaSuccess) break;

@@ -68,6 +68,13 @@ constexpr int kEmuPerEight = VISTA_EMU_PER_EIGHT;
 constexpr int kCtlRegs = VISTA_CTL_REGS;
 constexpr int kSoftmaxRegs = ((64512 - 128 * kCtlRegs) / 256) & ~7;
 constexpr bool kSetMaxNReg = VISTA_SETMAXNREG;  // shift registers from the control warps to the softmax warps
+#ifndef VISTA_SPLIT_P
+#define VISTA_SPLIT_P 2
+#endif
+// P handed to the MMA in kSplitP parts of 128 / kSplitP keys (one arrive each; 1 = whole tile), so
+// the PV GEMM of a part overlaps the exponentials of the next parts
+constexpr int kSplitP = VISTA_SPLIT_P;
+static_assert(kSplitP == 1 || kSplitP == 2 || kSplitP == 4, "P split");
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -82,8 +89,10 @@ struct Cfg {
     static constexpr int kKOff = NQ * kTileBytes;
     static constexpr int kVOff = kKOff + kKStages * kTileBytes;
     static constexpr int kBarOff = kVOff + kVStages * kTileBytes;
-    static constexpr int kRingOff = kBarOff + 512;   // item ring (kItemRing x ItemEntry)
+    static constexpr int kBarBytes = 768;
+    static constexpr int kRingOff = kBarOff + kBarBytes;  // item ring (kItemRing x ItemEntry)
     static constexpr int kSmem = kRingOff + 512 + 1024;  // + alignment slack
+    static_assert(kSmem <= 232448, "shared memory");
     static constexpr int kThreads = 128 + NQ * 128;     // control warpgroup + NQ softmax warpgroups
     static constexpr int kTmemCols = NQ == 2 ? 512 : 256;
 };
@@ -101,11 +110,14 @@ struct Bars {
     uint64_t it_full[kItemRing], it_empty[kItemRing];
     uint64_t q_full, q_empty;
     uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
-    uint64_t s_full[2][2], p_full[2][2];  // [q tile][S buffer]
+    uint64_t s_full[2][2], p_full[2][2];  // [q tile][P part: 0 first, 1 last]
+    uint64_t p_part[2][2];                // [q tile][middle P parts] (kSplitP == 4)
     uint64_t pv_done[2], o_full[2];
     uint32_t tmem_base;
     int merge_last, merge_clo, merge_chi;  // fused split-L merge handshake (epilogue)
 };
+
+static_assert(sizeof(Bars) <= Cfg<2>::kBarBytes, "barrier region");
 
 struct Params {
     const int64_t* offsets;
@@ -310,6 +322,36 @@ __device__ __forceinline__ float exp_tile(const uint32_t (&r)[4][32], float sl2,
     return (la + lb) + (lc + ld);
 }
 
+// exp_tile for part PART of NP equal key ranges (32-key chunks [PART 4/NP, (PART+1) 4/NP)); P into
+// the matching TMEM columns
+template <int PART, int NP>
+__device__ __forceinline__ float exp_part(const uint32_t (&r)[4][32], float sl2, float neg, uint32_t tS) {
+    const uint64_t sl2x2 = ptx::f2_pack(sl2, sl2);
+    const uint64_t negx2 = ptx::f2_pack(neg, neg);
+    uint64_t acc[2] = {ptx::f2_pack(0.f, 0.f), ptx::f2_pack(0.f, 0.f)};
+#pragma unroll
+    for (int c = PART * (4 / NP); c < (PART + 1) * (4 / NP); ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t x2 = ptx::f2_fma(
+                ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
+            float x0, x1;
+            ptx::f2_unpack(x2, x0, x1);
+            const uint64_t p2 = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+            acc[j & 1] = ptx::f2_add(acc[j & 1], p2);
+            float p0, p1;
+            ptx::f2_unpack(p2, p0, p1);
+            pk[j] = ptx::pack_bf16x2(p0, p1);
+        }
+        ptx::tmem_st16(tS + c * 16, pk);
+    }
+    float la, lb, lc, ld;
+    ptx::f2_unpack(acc[0], la, lb);
+    ptx::f2_unpack(acc[1], lc, ld);
+    return (la + lb) + (lc + ld);
+}
+
 // ---- MMA issue with compile-time geometry (see the MMA role) ----
 template <int NQ, int Q, int ST>
 __device__ __forceinline__ void issue_S_t(uint32_t tmem, uint32_t sQa, uint32_t sKa) {
@@ -322,12 +364,12 @@ __device__ __forceinline__ void issue_S_t(uint32_t tmem, uint32_t sQa, uint32_t 
                       ptx::sdesc_sw128(sKa + ST * kTileBytes + off, 16, 1024), idS, kk > 0);
     }
 }
-template <int NQ, int Q, int ST, bool ACC>
+template <int NQ, int Q, int ST, bool ACC, int K0 = 0, int K1 = 8>
 __device__ __forceinline__ void issue_PV_t(uint32_t tmem, uint32_t sVa) {
-    // O_Q += P_Q V over the 128 keys of V stage ST; P (bf16) read from TMEM columns [128 Q, 128 Q + 64)
+    // O_Q += P_Q V over keys [16 K0, 16 K1) of V stage ST; P (bf16) read from TMEM columns [128 Q, 128 Q + 64)
     constexpr uint32_t idP = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM) x V (MN-major)
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
+    for (int kk = K0; kk < K1; ++kk)
         ptx::mma_ts_w(tmem + NQ * 128 + Q * 128, tmem + Q * 128 + kk * 8,
                       ptx::sdesc_sw128(sVa + ST * kTileBytes + kk * 2048, kHalfBytes, 1024), idP,
                       (ACC || kk > 0) ? 1u : 0u);
@@ -345,20 +387,20 @@ __device__ __forceinline__ void issue_S_d(int q, int st, uint32_t tmem, uint32_t
     if (q == 0) issue_S_q<NQ, 0>(st, tmem, sQa, sKa);
     else if constexpr (NQ > 1) issue_S_q<NQ, 1>(st, tmem, sQa, sKa);
 }
-template <int NQ, int Q, bool ACC>
+template <int NQ, int Q, bool ACC, int K0 = 0, int K1 = 8>
 __device__ __forceinline__ void issue_PV_q(int st, uint32_t tmem, uint32_t sVa) {
     switch (st) {
-        case 0: issue_PV_t<NQ, Q, 0, ACC>(tmem, sVa); break;
-        case 1: issue_PV_t<NQ, Q, 1, ACC>(tmem, sVa); break;
-        default: issue_PV_t<NQ, Q, 2, ACC>(tmem, sVa); break;
+        case 0: issue_PV_t<NQ, Q, 0, ACC, K0, K1>(tmem, sVa); break;
+        case 1: issue_PV_t<NQ, Q, 1, ACC, K0, K1>(tmem, sVa); break;
+        default: issue_PV_t<NQ, Q, 2, ACC, K0, K1>(tmem, sVa); break;
     }
 }
-template <int NQ>
+template <int NQ, int K0 = 0, int K1 = 8>
 __device__ __forceinline__ void issue_PV_d(int q, int st, bool acc, uint32_t tmem, uint32_t sVa) {
     if (q == 0) {
-        if (acc) issue_PV_q<NQ, 0, true>(st, tmem, sVa); else issue_PV_q<NQ, 0, false>(st, tmem, sVa);
+        if (acc) issue_PV_q<NQ, 0, true, K0, K1>(st, tmem, sVa); else issue_PV_q<NQ, 0, false, K0, K1>(st, tmem, sVa);
     } else if constexpr (NQ > 1) {
-        if (acc) issue_PV_q<NQ, 1, true>(st, tmem, sVa); else issue_PV_q<NQ, 1, false>(st, tmem, sVa);
+        if (acc) issue_PV_q<NQ, 1, true, K0, K1>(st, tmem, sVa); else issue_PV_q<NQ, 1, false, K0, K1>(st, tmem, sVa);
     }
 }
 
@@ -399,6 +441,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             for (int b = 0; b < 2; ++b) {
                 ptx::mbar_init(&bars->s_full[q][b], 1);
                 ptx::mbar_init(&bars->p_full[q][b], 128);
+                ptx::mbar_init(&bars->p_part[q][b], 128);
             }
             ptx::mbar_init(&bars->pv_done[q], 1);
             ptx::mbar_init(&bars->o_full[q], 1);
@@ -551,9 +594,28 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                         if (first_item && lane == 0) VTRACE(0, t, q);
                         ptx::mbar_wait(&bars->p_full[q][0], p_phase[q]);
                         if (first_item && lane == 0) VTRACE(1, t, q);
-                        p_phase[q] ^= 1;
                         ptx::tc_fence_after();
-                        issue_PV_d<NQ>(q, vst, t > 0, tmem, sVa);
+                        if constexpr (kSplitP == 2) {
+                            // keys 0-63 as soon as their P is in TMEM, keys 64-127 after the rest
+                            issue_PV_d<NQ, 0, 4>(q, vst, t > 0, tmem, sVa);
+                            ptx::mbar_wait(&bars->p_full[q][1], p_phase[q]);
+                            ptx::tc_fence_after();
+                            issue_PV_d<NQ, 4, 8>(q, vst, true, tmem, sVa);
+                        } else if constexpr (kSplitP == 4) {
+                            issue_PV_d<NQ, 0, 2>(q, vst, t > 0, tmem, sVa);
+                            ptx::mbar_wait(&bars->p_part[q][0], p_phase[q]);
+                            ptx::tc_fence_after();
+                            issue_PV_d<NQ, 2, 4>(q, vst, true, tmem, sVa);
+                            ptx::mbar_wait(&bars->p_part[q][1], p_phase[q]);
+                            ptx::tc_fence_after();
+                            issue_PV_d<NQ, 4, 6>(q, vst, true, tmem, sVa);
+                            ptx::mbar_wait(&bars->p_full[q][1], p_phase[q]);
+                            ptx::tc_fence_after();
+                            issue_PV_d<NQ, 6, 8>(q, vst, true, tmem, sVa);
+                        } else {
+                            issue_PV_d<NQ>(q, vst, t > 0, tmem, sVa);
+                        }
+                        p_phase[q] ^= 1;
                         if (!more) {
                             if (lane == 0 && q == NQ - 1) ITRACE(3, item_no - 1);
                             ptx::mma_commit_w(&bars->o_full[q]);
@@ -682,6 +744,45 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 const bool any = __any_sync(0xffffffffu, need);
                 const float m_old = m_used;
                 if (any) m_used = fmaxf(m_used, mxs);
+                if constexpr (kSplitP > 1) {
+                    const float lt0 = exp_part<0, kSplitP>(r, sl2, -m_used, tS);
+                    // O rescale before the first arrive (PV(t) accumulates into O right after it);
+                    // placed after the first part so its registers are free
+                    if (any && t > it.t0) {
+                        const float f = ptx::ex2(m_old - m_used);
+                        l *= f;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t o[32];
+                            ptx::tmem_ld32_sync(tO + c * 32, o);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
+                            ptx::tmem_st32(tO + c * 32, o);
+                        }
+                    }
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars->p_full[wg][0]);
+                    float lt = lt0;
+                    if constexpr (kSplitP == 4) {
+                        lt += exp_part<1, 4>(r, sl2, -m_used, tS);
+                        ptx::tmem_wait_st();
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(&bars->p_part[wg][0]);
+                        lt += exp_part<2, 4>(r, sl2, -m_used, tS);
+                        ptx::tmem_wait_st();
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(&bars->p_part[wg][1]);
+                        lt += exp_part<3, 4>(r, sl2, -m_used, tS);
+                    } else {
+                        lt += exp_part<1, 2>(r, sl2, -m_used, tS);
+                    }
+                    if (tr) VTRACE(6, t - it.t0, wg);
+                    l += lt;
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars->p_full[wg][1]);
+                } else {
                 // P = 2^(S scale log2e - m) over S_q (exp_tile); FMA-pipe exp2 only on unmasked tiles
                 const float lt = full ? exp_tile<kEmuPerEight>(r, sl2, -m_used, tS) : exp_tile<0>(r, sl2, -m_used, tS);
                 if (tr) VTRACE(6, t - it.t0, wg);
@@ -702,6 +803,7 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&bars->p_full[wg][0]);
+                }
                 if (tr) VTRACE(7, t - it.t0, wg);
             }
             first_item = false;

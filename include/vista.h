@@ -131,6 +131,32 @@ vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, 
                                        float* part_o, float* part_lse, void* workspace,
                                        size_t workspace_bytes, void* stream);
 
+/*
+ * Shared key prefix (optional; SURVEY.md 8(b) / DESIGN.md reading R18).  Every user additionally
+ * attends to the same prefix_len keys / values k_prefix, v_prefix [prefix_len, H, d] (e.g. the
+ * seeds' own keys in the self-attention over [seeds; UIH]):
+ *   softmax: out / lse are those of the attention over the union [prefix; history of u];
+ *   QLA:     Z = Z_prefix + Z_u and N_u = prefix_len + L_u (when qla_normalize).
+ * An empty user gets the prefix-only result.  prefix_len = 0 is exactly the plain call.  Requires
+ * shared seeds (q_user_stride = 0; else VISTA_ERR_UNSUPPORTED).  For split-L, pass the prefix to
+ * exactly ONE shard's vista_summarize_partial_prefix.  Workspace: at least
+ * vista_summarize_prefix_workspace_size bytes.
+ */
+vista_status_t vista_summarize_prefix_workspace_size(const vista_desc_t* desc, int64_t total_len,
+                                                     int64_t prefix_len, size_t* bytes);
+vista_status_t vista_summarize_fwd_prefix(const vista_desc_t* desc, const void* q, const void* k,
+                                          const void* v, const int64_t* offsets, int64_t total_len,
+                                          const void* k_prefix, const void* v_prefix,
+                                          int64_t prefix_len, void* out, float* lse, void* workspace,
+                                          size_t workspace_bytes, void* stream);
+vista_status_t vista_summarize_partial_prefix(const vista_desc_t* desc, const void* q,
+                                              const void* k, const void* v,
+                                              const int64_t* offsets, int64_t total_len,
+                                              const void* k_prefix, const void* v_prefix,
+                                              int64_t prefix_len, float* part_o, float* part_lse,
+                                              void* workspace, size_t workspace_bytes,
+                                              void* stream);
+
 /* Bytes of device workspace vista_summarize_merge needs for this descriptor (0 for softmax). */
 vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes);
 

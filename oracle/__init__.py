@@ -84,13 +84,38 @@ def act(kind: str, x: float) -> float:
     return float(_load().vo_act(ACT[kind], float(x)))
 
 
-def softmax_summarize(q, k, v, offsets, scale=None, rows=None, q_per_user=False, threads=0):
+def _with_prefix(k, v, offsets, k_prefix, v_prefix):
+    """Histories with a shared key prefix prepended to every user: the key set of user u is
+    [prefix; history of u] (reading R18; self-attention over [seeds; UIH]).
+    Returns (k', v', offsets') of the concatenated per-user histories."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    kp = np.asarray(k_prefix)
+    vp = np.asarray(v_prefix)
+    P = kp.shape[0]
+    B = len(offsets) - 1
+    ks, vs = [], []
+    for u in range(B):
+        ks += [kp, np.asarray(k[offsets[u]:offsets[u + 1]])]
+        vs += [vp, np.asarray(v[offsets[u]:offsets[u + 1]])]
+    lens = np.diff(offsets) + P
+    off2 = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    H, d = kp.shape[1:]
+    k2 = np.concatenate(ks) if ks else np.zeros((0, H, d), kp.dtype)
+    v2 = np.concatenate(vs) if vs else np.zeros((0, H, d), vp.dtype)
+    return k2, v2, off2
+
+
+def softmax_summarize(q, k, v, offsets, scale=None, rows=None, q_per_user=False, threads=0,
+                      k_prefix=None, v_prefix=None):
     """Seed-row softmax attention over each user's history.
 
     q: [S,H,d] (shared seeds) or [B,S,H,d] with q_per_user=True; k, v: [sumL,H,d];
     offsets: [B+1] int64.  rows: optional subset of query rows.
     Returns out [B, R, H, d] float64 and lse [B, H, R] float64 (natural log).
+    k_prefix, v_prefix: optional shared keys [P,H,d] attended by every user (see _with_prefix).
     """
+    if k_prefix is not None:
+        k, v, offsets = _with_prefix(k, v, offsets, k_prefix, v_prefix)
     q, k, v = _f32(q), _f32(k), _f32(v)
     offsets = np.ascontiguousarray(offsets, dtype=np.int64)
     B = len(offsets) - 1
@@ -144,8 +169,11 @@ def qla_finalize(q, z, n_items, phi1="silu", phi2="silu", normalize=True, q_per_
 
 
 def qla_summarize(q, k, v, offsets, phi1="silu", phi2="silu", normalize=True, q_per_user=False,
-                  threads=0):
-    """QLA source part at the seed rows: state then finalize.  Returns out [B,S,H,d]."""
+                  threads=0, k_prefix=None, v_prefix=None):
+    """QLA source part at the seed rows: state then finalize.  Returns out [B,S,H,d].
+    With a shared key prefix the state and N_u run over [prefix; history] (_with_prefix)."""
+    if k_prefix is not None:
+        k, v, offsets = _with_prefix(k, v, offsets, k_prefix, v_prefix)
     offsets = np.asarray(offsets, dtype=np.int64)
     z = qla_state(k, v, offsets, phi1, threads)
     return qla_finalize(q, z, np.diff(offsets), phi1, phi2, normalize, q_per_user, threads)

@@ -91,6 +91,9 @@ def load():
     lib.vista_summarize_fwd.argtypes = [DP, P, P, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_partial.argtypes = [DP, P, P, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge.argtypes = [DP, i32, P, P, P, P, P, P, P, sz, P]
+    lib.vista_summarize_prefix_workspace_size.argtypes = [DP, i64, i64, ctypes.POINTER(sz)]
+    lib.vista_summarize_fwd_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
+    lib.vista_summarize_partial_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge_workspace_size.argtypes = [DP, ctypes.POINTER(sz)]
     lib.vista_summarize_merge_workspace_size.restype = ctypes.c_int
     lib.vista_check_offsets.argtypes = [P, i32, i64, P]
@@ -100,7 +103,8 @@ def load():
     lib.vista_time_next_main_kernel.restype = ctypes.c_int
     lib.vista_launch_counter.restype = ctypes.c_uint64
     for f in ("vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
-              "vista_summarize_merge", "vista_check_offsets"):
+              "vista_summarize_merge", "vista_check_offsets", "vista_summarize_prefix_workspace_size",
+              "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix"):
         getattr(lib, f).restype = ctypes.c_int
     if lib.vista_abi_version() != ABI_VERSION:
         raise RuntimeError("libvista ABI version mismatch")
@@ -164,6 +168,30 @@ def vista_summarize_partial(desc, q, k, v, offsets, total_len, part_o, part_lse,
     _check(load().vista_summarize_partial(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
                                           int(total_len), _ptr(part_o), _ptr(part_lse), _ptr(workspace),
                                           int(workspace_bytes), _stream(stream)), "vista_summarize_partial")
+
+
+def vista_summarize_prefix_workspace_size(desc: Desc, total_len: int, prefix_len: int) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load().vista_summarize_prefix_workspace_size(ctypes.byref(desc), int(total_len), int(prefix_len),
+                                                        ctypes.byref(n)), "vista_summarize_prefix_workspace_size")
+    return n.value
+
+
+def vista_summarize_fwd_prefix(desc, q, k, v, offsets, total_len, k_prefix, v_prefix, prefix_len, out, lse,
+                               workspace, workspace_bytes, stream=None):
+    _check(load().vista_summarize_fwd_prefix(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                                             int(total_len), _ptr(k_prefix), _ptr(v_prefix), int(prefix_len),
+                                             _ptr(out), _ptr(lse), _ptr(workspace), int(workspace_bytes),
+                                             _stream(stream)), "vista_summarize_fwd_prefix")
+
+
+def vista_summarize_partial_prefix(desc, q, k, v, offsets, total_len, k_prefix, v_prefix, prefix_len, part_o,
+                                   part_lse, workspace, workspace_bytes, stream=None):
+    _check(load().vista_summarize_partial_prefix(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                                                 int(total_len), _ptr(k_prefix), _ptr(v_prefix), int(prefix_len),
+                                                 _ptr(part_o), _ptr(part_lse), _ptr(workspace),
+                                                 int(workspace_bytes), _stream(stream)),
+           "vista_summarize_partial_prefix")
 
 
 def vista_summarize_merge_workspace_size(desc: Desc) -> int:
@@ -238,20 +266,23 @@ def _desc_for(q, k, offsets, attn, scale, phi1, phi2, normalize, out_dtype):
                      phi1=phi1, phi2=phi2, normalize=normalize, q_user_stride=stride)
 
 
-def _workspace(desc, total_len, device, workspace=None):
+def _workspace(desc, total_len, device, workspace=None, prefix_len=0):
     import torch
-    need = vista_summarize_workspace_size(desc, total_len)
+    need = (vista_summarize_prefix_workspace_size(desc, total_len, prefix_len) if prefix_len
+            else vista_summarize_workspace_size(desc, total_len))
     if workspace is not None and workspace.numel() >= need:
         return workspace, need
     return torch.empty(max(need, 16), dtype=torch.uint8, device=device), need
 
 
 def summarize(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=None, phi1="silu", phi2="silu",
-              normalize=True, out_dtype=None, workspace=None, stream=None):
+              normalize=True, out_dtype=None, workspace=None, stream=None, k_prefix=None, v_prefix=None):
     """Summary tokens of every user: out [B,S,H,d] (+ lse [B,H,S] for softmax).
 
     q: [S,H,d] shared seeds or [B,S,H,d]; k, v: [total_len,H,d]; offsets: int64 [B+1] on device.
     total_len (host int) avoids a device read; pass it on the hot path.
+    k_prefix, v_prefix: optional shared key prefix [P,H,d] every user also attends to
+    (vista_summarize_fwd_prefix).
     """
     import torch
     if total_len is None:
@@ -261,13 +292,18 @@ def summarize(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=None, phi
     odt = torch.bfloat16 if desc.out_dtype == BF16 else torch.float32
     out = torch.empty((B, S, H, d), dtype=odt, device=q.device)
     lse = torch.empty((B, H, S), dtype=torch.float32, device=q.device) if attn == SOFTMAX else None
-    ws, need = _workspace(desc, total_len, q.device, workspace)
-    vista_summarize_fwd(desc, q, k, v, offsets, total_len, out, lse, ws, ws.numel(), stream)
+    P = 0 if k_prefix is None else int(k_prefix.shape[0])
+    ws, need = _workspace(desc, total_len, q.device, workspace, P)
+    if k_prefix is not None:
+        vista_summarize_fwd_prefix(desc, q, k, v, offsets, total_len, k_prefix, v_prefix, P, out, lse, ws,
+                                   ws.numel(), stream)
+    else:
+        vista_summarize_fwd(desc, q, k, v, offsets, total_len, out, lse, ws, ws.numel(), stream)
     return out, lse
 
 
 def summarize_partial(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=None, phi1="silu",
-                      phi2="silu", normalize=True, workspace=None, stream=None):
+                      phi2="silu", normalize=True, workspace=None, stream=None, k_prefix=None, v_prefix=None):
     """Partial over one history shard: softmax -> (part_o [B,H,S,d] f32, part_lse [B,H,S]);
     QLA -> (Z [B,H,d,d] f32, None)."""
     import torch
@@ -281,8 +317,13 @@ def summarize_partial(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=N
     else:
         po = torch.empty((B, H, d, d), dtype=torch.float32, device=q.device)
         pl = None
-    ws, need = _workspace(desc, total_len, q.device, workspace)
-    vista_summarize_partial(desc, q, k, v, offsets, total_len, po, pl, ws, ws.numel(), stream)
+    P = 0 if k_prefix is None else int(k_prefix.shape[0])
+    ws, need = _workspace(desc, total_len, q.device, workspace, P)
+    if k_prefix is not None:
+        vista_summarize_partial_prefix(desc, q, k, v, offsets, total_len, k_prefix, v_prefix, P, po, pl, ws,
+                                       ws.numel(), stream)
+    else:
+        vista_summarize_partial(desc, q, k, v, offsets, total_len, po, pl, ws, ws.numel(), stream)
     return po, pl
 
 

@@ -99,6 +99,11 @@ cudaError_t launch_simt_qla_state(const Problem& p, float* zbuf);
 cudaError_t launch_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
                                 const int64_t* user_len, void* ws);
 bool qla_finalize_uses_tc(const Problem& p);
+// shared key prefix (vista_summarize_*_prefix)
+cudaError_t launch_write_prefix_offsets(int64_t* off, int64_t P, cudaStream_t st);
+cudaError_t launch_merge_prefix(const Problem& p, const float* o, const float* lse, const float* opre,
+                                const float* lpre);
+cudaError_t launch_add_prefix_state(const Problem& p, float* z, const float* zpre, int64_t P, int64_t* user_len);
 // tensor-core finalize (bf16, d = 128); ws: sm100_qla_finalize_workspace(p) bytes
 size_t sm100_qla_finalize_workspace(const Problem& p);
 cudaError_t launch_sm100_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,

@@ -375,6 +375,55 @@ __global__ void merge_softmax_parts_kernel(int P, int B, int H, int S, const flo
     if (lane == 0) lse_store(outs, S, H, u, h, i, lse);
 }
 
+// Shared key prefix (softmax): LSE merge of each user's history result (o [B,H,S,D], lse [B,H,S])
+// with the prefix-only result of the same seeds (opre [H,S,D], lpre [H,S]) -> outs (FINAL or
+// PARTIAL layout).  Attention over the union of the two key sets (reading R18).
+template <int D>
+__global__ void merge_prefix_kernel(int B, int H, int S, const float* __restrict__ o, const float* __restrict__ lse,
+                                    const float* __restrict__ opre, const float* __restrict__ lpre, OutSpec outs) {
+    const int64_t r = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;  // row over (u, h, i)
+    const int lane = threadIdx.x % 32;
+    if (r >= (int64_t)B * H * S) return;
+    const int64_t rp = r % ((int64_t)H * S);  // (h, i) of the prefix row
+    const float l1 = lse[r], l2 = lpre[rp];
+    const float M = fmaxf(l1, l2);
+    constexpr int V = D / 32;
+    float acc[V];
+    float L = -INFINITY;
+    if (M == -INFINITY) {
+#pragma unroll
+        for (int t = 0; t < V; ++t) acc[t] = 0.f;
+    } else {
+        const float w1 = expf(l1 - M), w2 = expf(l2 - M);
+        const float inv = 1.f / (w1 + w2);
+        L = M + logf(w1 + w2);
+#pragma unroll
+        for (int t = 0; t < V; ++t)
+            acc[t] = (w1 * o[r * D + lane + 32 * t] + w2 * opre[rp * D + lane + 32 * t]) * inv;
+    }
+    const int u = (int)(r / ((int64_t)H * S)), h = (int)((r / S) % H), i = (int)(r % S);
+#pragma unroll
+    for (int t = 0; t < V; ++t) out_store(outs, S, H, D, u, h, i, lane + 32 * t, acc[t]);
+    if (lane == 0) lse_store(outs, S, H, u, h, i, L);
+}
+
+// Shared key prefix (QLA): Z[u,h] += Zpre[h] and user_len[u] = L_u + P (the prefix counts in N_u).
+__global__ void add_prefix_state_kernel(int B, int H, int D, float* __restrict__ z, const float* __restrict__ zpre,
+                                        const int64_t* __restrict__ offsets, int64_t P, int64_t* __restrict__ user_len) {
+    const int64_t n = (int64_t)B * H * D * D;
+    const int64_t per = (int64_t)H * D * D;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        z[e] += zpre[e % per];
+    if (user_len)
+        for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < B; u += (int64_t)gridDim.x * blockDim.x)
+            user_len[u] = offsets[u + 1] - offsets[u] + P;
+}
+
+__global__ void write_prefix_offsets_kernel(int64_t* off, int64_t P) {
+    off[0] = 0;
+    off[1] = P;
+}
+
 // ---------------------------------------------------------------------------------------------
 // O[u, i, h, :] = phi1(q_i) W,  W = phi2((sum_p Z_p[u,h]) * inv_N).  Block: 64 rows x D cols,
 // 256 threads, thread tile RT rows x 4 cols.
@@ -793,6 +842,31 @@ cudaError_t launch_simt_qla_state(const Problem& p, float* zbuf) {
         }
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_write_prefix_offsets(int64_t* off, int64_t P, cudaStream_t st) {
+    write_prefix_offsets_kernel<<<1, 1, 0, st>>>(off, P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_prefix(const Problem& p, const float* o, const float* lse, const float* opre,
+                                const float* lpre) {
+    const int64_t nrows = (int64_t)p.B * p.H * p.S;
+    if (nrows == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((nrows + 7) / 8);
+    switch (p.d) {
+        case 32: merge_prefix_kernel<32><<<grid, 256, 0, p.stream>>>(p.B, p.H, p.S, o, lse, opre, lpre, p.outs); break;
+        case 64: merge_prefix_kernel<64><<<grid, 256, 0, p.stream>>>(p.B, p.H, p.S, o, lse, opre, lpre, p.outs); break;
+        case 128: merge_prefix_kernel<128><<<grid, 256, 0, p.stream>>>(p.B, p.H, p.S, o, lse, opre, lpre, p.outs); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add_prefix_state(const Problem& p, float* z, const float* zpre, int64_t P, int64_t* user_len) {
+    if (p.B == 0) return cudaSuccess;
+    add_prefix_state_kernel<<<p.num_sms * 4, 256, 0, p.stream>>>(p.B, p.H, p.d, z, zpre, p.offsets, P, user_len);
+    return cudaGetLastError();
 }
 
 }  // namespace vista

@@ -6,6 +6,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -290,6 +291,130 @@ vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, 
     if (!desc) return VISTA_ERR_NULL;
     OutSpec o{OUT_PARTIAL, 0, part_o, desc->attn == VISTA_SOFTMAX ? part_lse : nullptr};
     return run(desc, q, k, v, offsets, total_len, o, workspace, workspace_bytes, stream);
+}
+
+// ---- shared key prefix: attention / state over [prefix keys; history] (reading R18).
+// Workspace: [sub-run workspace | prefix result | history result | QLA finalize workspace].
+namespace {
+struct PrefixPlan {
+    size_t sub_off, pre_off, preoff_off, main_off, main2_off, fin_off, total;
+};
+PrefixPlan plan_prefix(const vista_desc_t* desc, int64_t total_len, int64_t P) {
+    PrefixPlan pl{};
+    vista_desc_t d1 = *desc;
+    d1.num_users = 1;
+    const Problem pm = make_problem(desc, total_len), p1 = make_problem(&d1, P);
+    const size_t sub = std::max(plan_workspace(pm, true).total, plan_workspace(p1, true).total);
+    const bool softmax = desc->attn == VISTA_SOFTMAX;
+    const size_t B = (size_t)pm.B, H = (size_t)pm.H, S = (size_t)pm.S, d = (size_t)pm.d;
+    size_t off = 0;
+    pl.sub_off = off;
+    off = align256(off + sub);
+    pl.pre_off = off;  // softmax: opre [H,S,d] + lpre [H,S]; QLA: zpre [H,d,d]
+    off = align256(off + (softmax ? (H * S * d + H * S) : H * d * d) * sizeof(float));
+    pl.preoff_off = off;
+    off = align256(off + 2 * sizeof(int64_t));
+    pl.main_off = off;  // softmax: o [B,H,S,d]; QLA: z [B,H,d,d]
+    off = align256(off + (softmax ? B * H * S * d : B * H * d * d) * sizeof(float));
+    pl.main2_off = off;  // softmax: lse [B,H,S]; QLA: user_len [B]
+    off = align256(off + (softmax ? B * H * S * sizeof(float) : B * sizeof(int64_t)));
+    pl.fin_off = off;
+    if (!softmax && qla_finalize_uses_tc(pm)) off = align256(off + sm100_qla_finalize_workspace(pm));
+    pl.total = off;
+    return pl;
+}
+}  // namespace
+
+vista_status_t vista_summarize_prefix_workspace_size(const vista_desc_t* desc, int64_t total_len, int64_t prefix_len,
+                                                     size_t* bytes) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (!bytes) return VISTA_ERR_NULL;
+    if (total_len < 0 || prefix_len < 0) return VISTA_ERR_INVALID;
+    if (prefix_len == 0) return vista_summarize_workspace_size(desc, total_len, bytes);
+    *bytes = plan_prefix(desc, total_len, prefix_len).total;
+    return VISTA_OK;
+}
+
+static vista_status_t run_prefix(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                 const int64_t* offsets, int64_t total_len, const void* kp, const void* vp,
+                                 int64_t P, OutSpec outs, void* workspace, size_t workspace_bytes, void* stream) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (P < 0 || total_len < 0) return VISTA_ERR_INVALID;
+    if (P == 0) return run(desc, q, k, v, offsets, total_len, outs, workspace, workspace_bytes, stream);
+    if (!kp || !vp) return VISTA_ERR_NULL;
+    if (!aligned16(kp) || !aligned16(vp)) return VISTA_ERR_MISALIGNED;
+    if (desc->q_user_stride != 0) return VISTA_ERR_UNSUPPORTED;  // the prefix result is shared by all users
+    if (!q || !offsets || !outs.out) return VISTA_ERR_NULL;
+    if (outs.mode == OUT_PARTIAL && desc->attn == VISTA_SOFTMAX && !outs.lse) return VISTA_ERR_NULL;
+    if (desc->num_users == 0) return VISTA_OK;
+    const PrefixPlan pl = plan_prefix(desc, total_len, P);
+    if (!workspace || workspace_bytes < pl.total) return VISTA_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
+    char* ws = reinterpret_cast<char*>(workspace);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t sub_bytes = pl.pre_off - pl.sub_off;
+    vista_desc_t d1 = *desc;
+    d1.num_users = 1;
+    int64_t* pre_offsets = reinterpret_cast<int64_t*>(ws + pl.preoff_off);
+    cudaError_t e = launch_write_prefix_offsets(pre_offsets, P, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches += 1;
+    Problem pm = make_problem(desc, total_len);
+    pm.q = q;
+    pm.offsets = offsets;
+    pm.outs = outs;
+    pm.stream = s;
+    if (desc->attn == VISTA_SOFTMAX) {
+        float* opre = reinterpret_cast<float*>(ws + pl.pre_off);
+        float* lpre = opre + (size_t)pm.H * pm.S * pm.d;
+        float* o = reinterpret_cast<float*>(ws + pl.main_off);
+        float* l = reinterpret_cast<float*>(ws + pl.main2_off);
+        st = run(&d1, q, kp, vp, pre_offsets, P, OutSpec{OUT_PARTIAL, 0, opre, lpre}, ws + pl.sub_off, sub_bytes, stream);
+        if (st != VISTA_OK) return st;
+        st = run(desc, q, k, v, offsets, total_len, OutSpec{OUT_PARTIAL, 0, o, l}, ws + pl.sub_off, sub_bytes, stream);
+        if (st != VISTA_OK) return st;
+        e = launch_merge_prefix(pm, o, l, opre, lpre);
+    } else {
+        float* zpre = reinterpret_cast<float*>(ws + pl.pre_off);
+        const bool partial = outs.mode == OUT_PARTIAL;
+        float* z = partial ? reinterpret_cast<float*>(outs.out) : reinterpret_cast<float*>(ws + pl.main_off);
+        int64_t* user_len = partial ? nullptr : reinterpret_cast<int64_t*>(ws + pl.main2_off);
+        st = run(&d1, q, kp, vp, pre_offsets, P, OutSpec{OUT_PARTIAL, 0, zpre, nullptr}, ws + pl.sub_off, sub_bytes,
+                 stream);
+        if (st != VISTA_OK) return st;
+        st = run(desc, q, k, v, offsets, total_len, OutSpec{OUT_PARTIAL, 0, z, nullptr}, ws + pl.sub_off, sub_bytes,
+                 stream);
+        if (st != VISTA_OK) return st;
+        if ((e = launch_add_prefix_state(pm, z, zpre, P, user_len)) == cudaSuccess && !partial) {
+            g_launches += 1;
+            e = launch_qla_finalize(pm, z, 1, 0, user_len, ws + pl.fin_off);
+        }
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches += 1;
+    return VISTA_OK;
+}
+
+vista_status_t vista_summarize_fwd_prefix(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                          const int64_t* offsets, int64_t total_len, const void* k_prefix,
+                                          const void* v_prefix, int64_t prefix_len, void* out, float* lse,
+                                          void* workspace, size_t workspace_bytes, void* stream) {
+    if (!desc) return VISTA_ERR_NULL;
+    OutSpec o{OUT_FINAL, desc->out_dtype == VISTA_BF16, out, desc->attn == VISTA_SOFTMAX ? lse : nullptr};
+    return run_prefix(desc, q, k, v, offsets, total_len, k_prefix, v_prefix, prefix_len, o, workspace, workspace_bytes,
+                      stream);
+}
+
+vista_status_t vista_summarize_partial_prefix(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                              const int64_t* offsets, int64_t total_len, const void* k_prefix,
+                                              const void* v_prefix, int64_t prefix_len, float* part_o,
+                                              float* part_lse, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!desc) return VISTA_ERR_NULL;
+    OutSpec o{OUT_PARTIAL, 0, part_o, desc->attn == VISTA_SOFTMAX ? part_lse : nullptr};
+    return run_prefix(desc, q, k, v, offsets, total_len, k_prefix, v_prefix, prefix_len, o, workspace, workspace_bytes,
+                      stream);
 }
 
 static size_t merge_ws_bytes(const Problem& p) {

@@ -365,3 +365,84 @@ def test_int8_export_of_summary_tokens(cuda_lib):
     for u in range(len(lens)):
         for h in range(2):
             assert block_err(g[u, :, h], ref[u, :, h]) <= 2e-2
+
+
+# ----------------------------------------------------------------------------- shared key prefix (R18)
+def _prefix_inputs(lens, P, S, H, d, dtype="bf16", seed=0):
+    q, k, v, off = synth.make_batch(lens, S, H, d, dtype=dtype, seed=seed, tau=2)
+    _, kp, vp, _ = synth.make_batch([P], S, H, d, dtype=dtype, seed=seed + 1000)
+    return q, k, v, off, kp, vp
+
+
+@pytest.mark.parametrize("S,H,d,dtype,P", [(256, 2, 128, "bf16", 300), (256, 1, 128, "bf16", 1),
+                                          (33, 2, 64, "f32", 17)])
+def test_softmax_prefix(cuda_lib, S, H, d, dtype, P):
+    vista = cuda_lib
+    lens = [0, 129, 2049, 5]
+    q, k, v, off, kp, vp = _prefix_inputs(lens, P, S, H, d, dtype, seed=S + P)
+    out, lse = vista.summarize(to_dev(q, dtype), to_dev(k, dtype), to_dev(v, dtype), torch.from_numpy(off).cuda(),
+                               int(off[-1]), out_dtype=vista.F32, k_prefix=to_dev(kp, dtype),
+                               v_prefix=to_dev(vp, dtype))
+    torch.cuda.synchronize()
+    ref, ref_lse = oracle.softmax_summarize(q, k, v, off, k_prefix=kp, v_prefix=vp)
+    check_softmax(out, lse, ref, ref_lse, [n + P for n in lens], dtype)
+
+
+@pytest.mark.parametrize("phi1,phi2,normalize", [("silu", "silu", True), ("shifted_elu", "identity", False)])
+def test_qla_prefix(cuda_lib, phi1, phi2, normalize):
+    vista = cuda_lib
+    lens = [0, 129, 2049, 5]
+    P, S, H, d = 200, 256, 2, 128
+    q, k, v, off, kp, vp = _prefix_inputs(lens, P, S, H, d, seed=3)
+    out, _ = vista.summarize(to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16"), torch.from_numpy(off).cuda(),
+                             int(off[-1]), attn=vista.QLA, phi1=phi1, phi2=phi2, normalize=normalize,
+                             out_dtype=vista.F32, k_prefix=to_dev(kp, "bf16"), v_prefix=to_dev(vp, "bf16"))
+    torch.cuda.synchronize()
+    ref = oracle.qla_summarize(q, k, v, off, phi1, phi2, normalize, k_prefix=kp, v_prefix=vp)
+    g = out.cpu().numpy()
+    for u in range(len(lens)):
+        for h in range(H):
+            assert block_err(g[u, :, h], ref[u, :, h]) <= 2e-2, (u, h)
+
+
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_prefix_partial_then_merge(cuda_lib, attn):
+    """Split-L with a prefix: the prefix goes to exactly one shard's partial call."""
+    vista = cuda_lib
+    lens = [3000, 0, 700]
+    P, S, H, d = 64, 256, 1, 128
+    q, k, v, off, kp, vp = _prefix_inputs(lens, P, S, H, d, seed=8)
+    a = vista.SOFTMAX if attn == "softmax" else vista.QLA
+    cut = [n // 2 for n in lens]
+    shards = []
+    for si, (lo_f, hi_f) in enumerate([(lambda u: 0, lambda u: cut[u]), (lambda u: cut[u], lambda u: lens[u])]):
+        rows = np.concatenate([np.arange(off[u] + lo_f(u), off[u] + hi_f(u)) for u in range(len(lens))]).astype(np.int64)
+        soff = synth.offsets_from_lengths([hi_f(u) - lo_f(u) for u in range(len(lens))])
+        kw = dict(k_prefix=to_dev(kp, "bf16"), v_prefix=to_dev(vp, "bf16")) if si == 0 else {}
+        po, pl = vista.summarize_partial(to_dev(q, "bf16"), to_dev(k[rows], "bf16"), to_dev(v[rows], "bf16"),
+                                         torch.from_numpy(soff).cuda(), int(soff[-1]), attn=a, **kw)
+        shards.append((po, pl))
+    po = torch.stack([s[0] for s in shards])
+    pl = torch.stack([s[1] for s in shards]) if attn == "softmax" else None
+    ulen = torch.tensor([n + P for n in lens], dtype=torch.int64, device="cuda")
+    out, lse = vista.summarize_merge(po, pl, q=to_dev(q, "bf16"), attn=a, user_len=ulen, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    if attn == "softmax":
+        ref, ref_lse = oracle.softmax_summarize(q, k, v, off, k_prefix=kp, v_prefix=vp)
+        check_softmax(out, lse, ref, ref_lse, [n + P for n in lens], "bf16")
+    else:
+        ref = oracle.qla_summarize(q, k, v, off, k_prefix=kp, v_prefix=vp)
+        g = out.cpu().numpy()
+        for u in range(len(lens)):
+            assert block_err(g[u, :, 0], ref[u, :, 0]) <= 2e-2
+
+
+def test_prefix_requires_shared_seeds(cuda_lib):
+    vista = cuda_lib
+    d = vista.make_desc(2, 256, 1, 128, q_user_stride=256 * 128)
+    P = 4
+    n = 1 << 20
+    buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+    with pytest.raises(vista.VistaError) as e:
+        vista.vista_summarize_fwd_prefix(d, buf, buf, buf, buf, 0, buf, buf, P, buf, None, buf, n)
+    assert "UNSUPPORTED" in str(e.value)

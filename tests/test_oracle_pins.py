@@ -393,3 +393,48 @@ def test_quantize_error_bound_and_special_rows():
     assert np.array_equal(codes[1], kk) and np.array_equal(deq[1], x[1].astype(np.float64))
     r = 5
     assert codes[r, np.argmax(x[r])] == 127 and codes[r, np.argmin(x[r])] == -127
+
+
+# ----------------------------------------------------------------------------- prefix (R18)
+def _prefix_case(seed, lens, P, S=5, H=2, d=8):
+    rng = np.random.default_rng(seed)
+    q, k, v, off = _batch(seed, lens, S=S, H=H, d=d, tau=2)
+    kp = grid(rng, (P, H, d))
+    vp = grid(rng, (P, H, d))
+    return q, k, v, off, kp, vp
+
+
+def test_prefix_softmax_is_lse_merge_of_history_and_prefix():
+    """Attention over [prefix; history] == LSE merge of the history-only and prefix-only results
+    (the merge is pinned separately by P5).  Covers an empty user (= prefix-only result)."""
+    q, k, v, off, kp, vp = _prefix_case(21, [40, 0, 7], P=9)
+    o, l = oracle.softmax_summarize(q, k, v, off, k_prefix=kp, v_prefix=vp)
+    oh, lh = oracle.softmax_summarize(q, k, v, off)
+    op, lp = oracle.softmax_summarize(q, kp, vp, [0, 9])
+    B = len(off) - 1
+    for u in range(B):
+        po = np.stack([oh[u].transpose(1, 0, 2), op[0].transpose(1, 0, 2)])  # [2, H, S, d]
+        pl = np.stack([lh[u], lp[0]])                                        # [2, H, S]
+        mo, ml = oracle.merge_lse(po, pl)
+        np.testing.assert_allclose(o[u].transpose(1, 0, 2), mo, rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(l[u], ml, rtol=1e-13, atol=1e-13)
+
+
+def test_prefix_softmax_single_prefix_key_empty_user_closed_form():
+    """One prefix key, empty history: O = v_prefix, lse = scale q.k_prefix (P3(i) on the prefix)."""
+    q, k, v, off, kp, vp = _prefix_case(22, [0], P=1, S=3, H=1, d=8)
+    o, l = oracle.softmax_summarize(q, k, v, off, k_prefix=kp, v_prefix=vp, scale=0.5)
+    np.testing.assert_allclose(o[0, :, 0], np.broadcast_to(vp[0, 0].astype(np.float64), (3, 8)), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(l[0, 0], 0.5 * (q[:, 0].astype(np.float64) @ kp[0, 0].astype(np.float64)),
+                               rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("phi1,phi2,normalize", [("silu", "silu", True), ("shifted_elu", "identity", False)])
+def test_prefix_qla_state_is_additive(phi1, phi2, normalize):
+    """QLA over [prefix; history]: Z = Z_prefix + Z_u, N_u = P + L_u, then the finalize."""
+    q, k, v, off, kp, vp = _prefix_case(23, [30, 0, 4], P=6)
+    o = oracle.qla_summarize(q, k, v, off, phi1, phi2, normalize, k_prefix=kp, v_prefix=vp)
+    zh = oracle.qla_state(k, v, off, phi1)
+    zp = oracle.qla_state(kp, vp, [0, 6], phi1)
+    o2 = oracle.qla_finalize(q, zh + zp[0][None], np.diff(off) + 6, phi1, phi2, normalize)
+    np.testing.assert_allclose(o, o2, rtol=1e-12, atol=1e-12)

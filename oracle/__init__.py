@@ -54,6 +54,9 @@ def _load():
         lib.vo_quantize_rows_f32.argtypes = [i64, i64, P, P, P, P]
         lib.vo_act.argtypes = [i32, f64]
         lib.vo_act.restype = f64
+        lib.vo_act_prime.argtypes = [i32, f64]
+        lib.vo_act_prime.restype = f64
+        lib.vo_qla_backward.argtypes = [i64, i64, i64, i64, P, i64, P, P, P, P, i32, i32, i32, P, P, P, i32]
         lib.vo_num_threads.restype = i32
         _lib = lib
     return _lib
@@ -177,6 +180,37 @@ def qla_summarize(q, k, v, offsets, phi1="silu", phi2="silu", normalize=True, q_
     offsets = np.asarray(offsets, dtype=np.int64)
     z = qla_state(k, v, offsets, phi1, threads)
     return qla_finalize(q, z, np.diff(offsets), phi1, phi2, normalize, q_per_user, threads)
+
+
+def act_prime(kind: str, x: float) -> float:
+    """phi'(x) in float64 (shifted ELU PAPER.md:795-809)."""
+    return float(_load().vo_act_prime(ACT[kind], float(x)))
+
+
+def qla_backward(q, k, v, offsets, dout, phi1="silu", phi2="silu", normalize=True, q_per_user=False,
+                 threads=0, sum_users=None):
+    """QLA backward (NEXT-2; chain rule, vo_qla_backward).  dout [B,S,H,d].
+    Returns dq, dk [sumL,H,d], dv [sumL,H,d] (float64).  dq is [B,S,H,d] per user; with shared
+    seeds (q_per_user False) it is summed over users to [S,H,d] unless sum_users=False."""
+    q, k, v, dout = _f32(q), _f32(k), _f32(v), _f32(dout)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    B = len(offsets) - 1
+    S, H, d = q.shape[-3:]
+    T = k.shape[0]
+    dq = np.empty((B, S, H, d), np.float64)
+    dk = np.empty((T, H, d), np.float64)
+    dv = np.empty((T, H, d), np.float64)
+    kk, vv = (k, v) if T > 0 else (np.zeros((1, H, d), np.float32),) * 2
+    dkk, dvv = (dk, dv) if T > 0 else (np.zeros((1, H, d)), np.zeros((1, H, d)))
+    stride = S * H * d if q_per_user else 0
+    rc = _load().vo_qla_backward(B, S, H, d, _ptr(q), stride, _ptr(kk), _ptr(vv), _ptr(offsets), _ptr(dout),
+                                 ACT[phi1], ACT[phi2], int(bool(normalize)), _ptr(dq), _ptr(dkk), _ptr(dvv),
+                                 int(threads))
+    if rc != 0:
+        raise ValueError("vo_qla_backward failed")
+    if (sum_users if sum_users is not None else not q_per_user):
+        dq = dq.sum(axis=0)
+    return dq, dk, dv
 
 
 def merge_lse(part_o, part_lse):

@@ -28,6 +28,9 @@
  *  Merges used only to test split invariants: LSE merge of softmax partials and plain sum of
  *  QLA states.
  *
+ *  NEXT-2 (training): the QLA backward (vo_qla_backward) by the chain rule through
+ *  O = phi1(Q) phi2(Z / N), Z = phi1(K)^T V.
+ *
  * Inputs are float32 arrays whose values are exact (bf16 / f32 grid values from synth/); every
  * element is converted exactly to double and all arithmetic is double.  No blocking, no
  * reordering beyond the definitions above.  Compile: gcc -O2 -fopenmp (no -ffast-math).
@@ -198,6 +201,103 @@ int vo_qla_finalize(int64_t B, int64_t S, int64_t H, int64_t d, const float* q,
             }
         }
         free(w);
+    }
+    return 0;
+}
+
+/* phi' (derivatives of the activations above; shifted ELU: PAPER.md:795-809 gives
+ * phi'(x) = 1 if x >= 1 else e^{x-1}; SiLU: sigma(x) (1 + x (1 - sigma(x)))). */
+double vo_act_prime(int kind, double x) {
+    switch (kind) {
+        case VO_ACT_IDENTITY: return 1.0;
+        case VO_ACT_SILU: {
+            const double s = 1.0 / (1.0 + exp(-x));
+            return s * (1.0 + x * (1.0 - s));
+        }
+        case VO_ACT_SHIFTED_ELU: return x >= 1.0 ? 1.0 : exp(x - 1.0);
+        default: return NAN;
+    }
+}
+
+/*
+ * QLA backward (NEXT-2), source part at the seed rows.  Forward per (user u, head h):
+ *   A = phi1(Q) [S x d], Z = sum_j phi1(k_j)^T v_j [d x d], Zbar = Z / N_u (if normalize and
+ *   N_u > 0), W = phi2(Zbar), O = A W.
+ * Chain rule (the appendix derives the phi2 = identity, no-1/N case, PAPER.md:776-783 and the
+ * activated forms PAPER.md:817-829; phi2 and 1/N are composed around Z, reading R19):
+ *   dW = A^T dO;  dZ = (dW . phi2'(Zbar)) / N_u;  dA = dO W^T;  dQ = dA . phi1'(Q)
+ *   dV_j = phi1(k_j) dZ;  dK_j = (v_j dZ^T) . phi1'(k_j)
+ * dout: [B, S, H, d]; dq: [B, S, H, d] (per user, before any sum over users of shared seeds);
+ * dk, dv: [total, H, d].  All float64.
+ */
+int vo_qla_backward(int64_t B, int64_t S, int64_t H, int64_t d, const float* q, int64_t q_user_stride,
+                    const float* k, const float* v, const int64_t* offsets, const float* dout, int phi1,
+                    int phi2, int normalize, double* dq, double* dk, double* dv, int threads) {
+    if (B < 0 || S < 1 || H < 1 || d < 1) return -1;
+    set_threads(threads);
+#pragma omp parallel
+    {
+        double* z = (double*)malloc((size_t)(d * d) * sizeof(double));
+        double* w = (double*)malloc((size_t)(d * d) * sizeof(double));
+        double* dz = (double*)malloc((size_t)(d * d) * sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < B * H; ++t) {
+            const int64_t u = t / H, h = t % H;
+            const int64_t N = offsets[u + 1] - offsets[u];
+            const double inv = (normalize && N > 0) ? 1.0 / (double)N : 1.0;
+            for (int64_t e = 0; e < d * d; ++e) z[e] = 0.0;
+            for (int64_t j = offsets[u]; j < offsets[u + 1]; ++j) {
+                const float* kj = k + (j * H + h) * d;
+                const float* vj = v + (j * H + h) * d;
+                for (int64_t c1 = 0; c1 < d; ++c1) {
+                    const double a = vo_act(phi1, (double)kj[c1]);
+                    for (int64_t c2 = 0; c2 < d; ++c2) z[c1 * d + c2] += a * (double)vj[c2];
+                }
+            }
+            for (int64_t e = 0; e < d * d; ++e) w[e] = vo_act(phi2, z[e] * inv);
+            /* dW = A^T dO, then dZ */
+            for (int64_t e = 0; e < d * d; ++e) dz[e] = 0.0;
+            for (int64_t i = 0; i < S; ++i) {
+                const float* qi = q + u * q_user_stride + (i * H + h) * d;
+                const float* go = dout + ((u * S + i) * H + h) * d;
+                for (int64_t c1 = 0; c1 < d; ++c1) {
+                    const double a = vo_act(phi1, (double)qi[c1]);
+                    for (int64_t c2 = 0; c2 < d; ++c2) dz[c1 * d + c2] += a * (double)go[c2];
+                }
+            }
+            for (int64_t e = 0; e < d * d; ++e) dz[e] = dz[e] * vo_act_prime(phi2, z[e] * inv) * inv;
+            /* dQ = (dO W^T) . phi1'(Q) */
+            for (int64_t i = 0; i < S; ++i) {
+                const float* qi = q + u * q_user_stride + (i * H + h) * d;
+                const float* go = dout + ((u * S + i) * H + h) * d;
+                double* g = dq + ((u * S + i) * H + h) * d;
+                for (int64_t c1 = 0; c1 < d; ++c1) {
+                    double acc = 0.0;
+                    for (int64_t c2 = 0; c2 < d; ++c2) acc += (double)go[c2] * w[c1 * d + c2];
+                    g[c1] = acc * vo_act_prime(phi1, (double)qi[c1]);
+                }
+            }
+            /* dV_j = phi1(k_j) dZ;  dK_j = (v_j dZ^T) . phi1'(k_j) */
+            for (int64_t j = offsets[u]; j < offsets[u + 1]; ++j) {
+                const float* kj = k + (j * H + h) * d;
+                const float* vj = v + (j * H + h) * d;
+                double* gv = dv + (j * H + h) * d;
+                double* gk = dk + (j * H + h) * d;
+                for (int64_t c2 = 0; c2 < d; ++c2) gv[c2] = 0.0;
+                for (int64_t c1 = 0; c1 < d; ++c1) {
+                    const double a = vo_act(phi1, (double)kj[c1]);
+                    double acc = 0.0;
+                    for (int64_t c2 = 0; c2 < d; ++c2) {
+                        gv[c2] += a * dz[c1 * d + c2];
+                        acc += (double)vj[c2] * dz[c1 * d + c2];
+                    }
+                    gk[c1] = acc * vo_act_prime(phi1, (double)kj[c1]);
+                }
+            }
+        }
+        free(z);
+        free(w);
+        free(dz);
     }
     return 0;
 }

@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--mode", default=None, choices=["by_user", "by_length", "flat"],
                     help="multi-GPU partitioner (default per config: c2/c3 by_user, c4 by_length, c5 flat)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--backward", action="store_true",
+                    help="NEXT-2: the step is the QLA backward (vista_summarize_bwd: Z recompute, dQ, dK, dV)")
     ap.add_argument("--export-int8", action="store_true",
                     help="NEXT-1: the step also exports the summary tokens as int8 (vista_quantize_rows_int8)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
@@ -140,6 +142,8 @@ def run_own(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
+    if args.backward:
+        wdesc += " backward (NEXT-2)"
     attn = vista.SOFTMAX if args.attn == "softmax" else vista.QLA
     mode = args.mode or {"c2": "by_user", "c3": "by_user", "c4": "by_length", "c5": "flat"}[args.config]
     if world == 1 and mode != "by_user":
@@ -174,6 +178,23 @@ def run_own(args, rank, world, local_rank):
                 export()
                 return [codes, qscale, qzp] + ([lse] if lse is not None else [])
             return [out] + ([lse] if lse is not None else [])
+        if args.backward:
+            if attn != vista.QLA:
+                raise SystemExit("--backward: only the QLA backward is implemented (softmax backward is next)")
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(1234 + rank)
+            dout = (torch.randint(-128, 128, (B, S, H, d), device=dev, generator=gen).float() / 64).to(torch.bfloat16)
+            dq = torch.empty((S, H, d), dtype=torch.float32, device=dev)
+            dk = torch.empty_like(K)
+            dv = torch.empty_like(V)
+            bws_bytes = vista.vista_summarize_bwd_workspace_size(desc, total)
+            bws = torch.empty(max(bws_bytes, 16), dtype=torch.uint8, device=dev)
+            inputs = [q, K, V, off_t, dout]
+
+            def step(ins=inputs):
+                vista.vista_summarize_bwd(desc, ins[0], ins[1], ins[2], ins[3], total, None, None, ins[4], dq, dk,
+                                          dv, bws, bws_bytes, sh)
+                return [dq, dk, dv]
         items_per_step = world * total
         scaling = "weak"
         parallel = f"by_user x{world} (weak: a {args.config} batch per GPU, no data-path collective)"
@@ -317,6 +338,9 @@ def run_own(args, rank, world, local_rank):
     flops = 4.0 * S * d * H * total if attn == vista.SOFTMAX else 2.0 * d * d * H * total
     kv_bytes = 4.0 * d * H * total  # bf16 K + V, read once
     io_bytes = kv_bytes + S * H * d * 2 + B * S * H * d * 2 + (B * H * S * 4 if attn == vista.SOFTMAX else 0)
+    if args.backward:  # dK / dV kernel: K, V read, dK, dV written (bf16); dV = phi1(K) dZ and V dZ^T
+        flops = 4.0 * d * d * H * total
+        io_bytes = 2 * kv_bytes + B * H * d * d * 2
     tflops = flops / (kern_ms / 1e3) / 1e12
     gbs = io_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
@@ -334,7 +358,8 @@ def run_own(args, rank, world, local_rank):
     else:
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic, "peak_kind": f"{pk_kind} HBM copy",
-                "kernel": "sm100_qla_state_kernel", "kernel_ms": round(kern_ms, 5),
+                "kernel": "sm100_qla_bwd_kv_kernel" if args.backward else "sm100_qla_state_kernel",
+                "kernel_ms": round(kern_ms, 5),
                 "algorithmic_bytes_per_launch": io_bytes,
                 "tensor": {"achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                            "frac": round(tflops / pk["bf16_tflops"], 4)}}

@@ -157,6 +157,26 @@ vista_status_t vista_summarize_partial_prefix(const vista_desc_t* desc, const vo
                                               void* workspace, size_t workspace_bytes,
                                               void* stream);
 
+/*
+ * Backward (NEXT-2, stage-1 training) -- QLA only in this version (softmax: VISTA_ERR_UNSUPPORTED).
+ * Gradients of out = phi1(Q) phi2(Z / N_u), Z = sum_j phi1(k_j)^T v_j (the appendix derives the
+ * phi2 = identity, no-1/N case; phi2 and 1/N are composed by the
+ * chain rule, reading R19):
+ *   dW = phi1(Q)^T dO;  dZ = (dW . phi2'(Zbar)) / N_u;  dQ = (dO W^T) . phi1'(Q), W = phi2(Zbar);
+ *   dV_j = phi1(k_j) dZ;  dK_j = (v_j dZ^T) . phi1'(k_j).
+ *   dout [B,S,H,d] (out_dtype); dq float32: [S,H,d] summed over users (ascending u) for shared
+ *   seeds, [B,S,H,d] for per-user Q; dk, dv [total_len,H,d] in in_dtype.  out / lse are unused
+ *   for QLA (may be NULL).  Z is recomputed from k, v.  Workspace: at least
+ *   vista_summarize_bwd_workspace_size bytes.  Asynchronous on stream; deterministic.
+ */
+vista_status_t vista_summarize_bwd_workspace_size(const vista_desc_t* desc, int64_t total_len,
+                                                  size_t* bytes);
+vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, const void* k,
+                                   const void* v, const int64_t* offsets, int64_t total_len,
+                                   const void* out, const float* lse, const void* dout, float* dq,
+                                   void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
 /* Bytes of device workspace vista_summarize_merge needs for this descriptor (0 for softmax). */
 vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes);
 

@@ -25,7 +25,9 @@ __all__ = [
     "vista_summarize_merge_workspace_size",
     "vista_check_offsets", "vista_dispatch_name", "vista_time_next_main_kernel", "vista_launch_counter",
     "vista_quantize_rows_int8", "quantize_int8",
-    "summarize", "summarize_partial", "summarize_merge",
+    "vista_summarize_prefix_workspace_size", "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
+    "vista_summarize_bwd_workspace_size", "vista_summarize_bwd",
+    "summarize", "summarize_partial", "summarize_merge", "summarize_bwd",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
 
@@ -92,6 +94,8 @@ def load():
     lib.vista_summarize_partial.argtypes = [DP, P, P, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge.argtypes = [DP, i32, P, P, P, P, P, P, P, sz, P]
     lib.vista_summarize_prefix_workspace_size.argtypes = [DP, i64, i64, ctypes.POINTER(sz)]
+    lib.vista_summarize_bwd_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
+    lib.vista_summarize_bwd.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, P, sz, P]
     lib.vista_summarize_fwd_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_partial_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge_workspace_size.argtypes = [DP, ctypes.POINTER(sz)]
@@ -104,7 +108,8 @@ def load():
     lib.vista_launch_counter.restype = ctypes.c_uint64
     for f in ("vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
               "vista_summarize_merge", "vista_check_offsets", "vista_summarize_prefix_workspace_size",
-              "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix"):
+              "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
+              "vista_summarize_bwd_workspace_size", "vista_summarize_bwd"):
         getattr(lib, f).restype = ctypes.c_int
     if lib.vista_abi_version() != ABI_VERSION:
         raise RuntimeError("libvista ABI version mismatch")
@@ -192,6 +197,21 @@ def vista_summarize_partial_prefix(desc, q, k, v, offsets, total_len, k_prefix, 
                                                  _ptr(part_o), _ptr(part_lse), _ptr(workspace),
                                                  int(workspace_bytes), _stream(stream)),
            "vista_summarize_partial_prefix")
+
+
+def vista_summarize_bwd_workspace_size(desc: Desc, total_len: int) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load().vista_summarize_bwd_workspace_size(ctypes.byref(desc), int(total_len), ctypes.byref(n)),
+           "vista_summarize_bwd_workspace_size")
+    return n.value
+
+
+def vista_summarize_bwd(desc, q, k, v, offsets, total_len, out, lse, dout, dq, dk, dv, workspace, workspace_bytes,
+                        stream=None):
+    _check(load().vista_summarize_bwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets), int(total_len),
+                                      _ptr(out), _ptr(lse), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv),
+                                      _ptr(workspace), int(workspace_bytes), _stream(stream)),
+           "vista_summarize_bwd")
 
 
 def vista_summarize_merge_workspace_size(desc: Desc) -> int:
@@ -325,6 +345,24 @@ def summarize_partial(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=N
     else:
         vista_summarize_partial(desc, q, k, v, offsets, total_len, po, pl, ws, ws.numel(), stream)
     return po, pl
+
+
+def summarize_bwd(q, k, v, offsets, total_len, dout, *, attn=QLA, phi1="silu", phi2="silu", normalize=True,
+                  out=None, lse=None, workspace=None, stream=None):
+    """Backward of summarize (NEXT-2; QLA): returns (dq, dk, dv).  dq float32 [S,H,d] (shared seeds,
+    summed over users) or [B,S,H,d]; dk, dv like k, v."""
+    import torch
+    if total_len is None:
+        total_len = k.shape[0]
+    desc = _desc_for(q, k, offsets, attn, None, phi1, phi2, normalize, _dtype_code(dout))
+    dq = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    dk = torch.empty_like(k)
+    dv = torch.empty_like(v)
+    need = vista_summarize_bwd_workspace_size(desc, total_len)
+    ws = workspace if workspace is not None and workspace.numel() >= need else \
+        torch.empty(max(need, 16), dtype=torch.uint8, device=q.device)
+    vista_summarize_bwd(desc, q, k, v, offsets, total_len, out, lse, dout, dq, dk, dv, ws, ws.numel(), stream)
+    return dq, dk, dv
 
 
 def summarize_merge(part_o, part_lse, *, q, attn=SOFTMAX, user_len=None, scale=None, phi1="silu",

@@ -99,6 +99,15 @@ cudaError_t launch_simt_qla_state(const Problem& p, float* zbuf);
 cudaError_t launch_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
                                 const int64_t* user_len, void* ws);
 bool qla_finalize_uses_tc(const Problem& p);
+// QLA backward (NEXT-2)
+cudaError_t launch_qla_bwd_unit(const Problem& p, bool dout_bf16, const void* dout, const float* z, float* dz,
+                                uint8_t* dz_op, float* dqu);
+cudaError_t launch_qla_bwd_dq_sum(const Problem& p, const float* dqu, float* dq);
+cudaError_t launch_qla_bwd_kv_simt(const Problem& p, const float* dz, void* dk, void* dv);
+// tcgen05 dK / dV (bf16, d = 128): uts from the forward recompute's workspace; dz_op bf16 operands
+cudaError_t launch_sm100_qla_bwd_kv(const Problem& p, const Workspace& w, char* ws, const uint8_t* dz_op, void* dk,
+                                    void* dv);
+bool qla_bwd_uses_tc(const Problem& p);
 // shared key prefix (vista_summarize_*_prefix)
 cudaError_t launch_write_prefix_offsets(int64_t* off, int64_t P, cudaStream_t st);
 cudaError_t launch_merge_prefix(const Problem& p, const float* o, const float* lse, const float* opre,

@@ -1,0 +1,338 @@
+// sm100_qla_bwd.cu -- QLA backward dK / dV on B200 (NEXT-2; gradients in qla_bwd.cu's header):
+//     dV_j = phi1(k_j) dZ          dK_j = (v_j dZ^T) . phi1'(k_j)        (per user u, head h)
+// Two 128x128x128 tcgen05 GEMMs per 128-item tile, both with dZ (bf16, pre-swizzled by
+// qla_bwd_unit_kernel) as the B operand: MN-major ([K = c1][N = c2]) for dV, K-major
+// ([N = c1][K = c2]) for dK'.  HBM-bound: per item-head 512 B of K+V read, 512 B of dK+dV written
+// (bf16), 4 d^2 = 65,536 flop.
+//
+//   warp 0        TMA producer: K, V tiles (2 stages); dZ of the unit (bulk copy) on unit change
+//   warp 1        MMA issuer (warp-wide, one elected lane)
+//   warps 4..11   transform (phi1(K) -> its own buffer, phi1'(K) in place of K; bf16) and the
+//                 epilogue (TMEM -> bf16 rows of dV and dK . phi1'(K)); dK/dV double-buffered
+//                 in TMEM so the epilogue of tile t overlaps the GEMMs of tile t+1.
+// Tiles are independent (no split partials): a CTA walks its stream-K range (work.cuh).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "qla_common.cuh"
+#include "sm100_ptx.cuh"
+#include "work.cuh"
+
+namespace vista {
+
+bool make_kv_map(CUtensorMap* map, const void* base, int64_t total_len, int H);
+
+namespace {
+
+constexpr int kHalf = 128 * 128;       // one 64-column half of a 128 x 128 bf16 tile
+constexpr int kTile = 2 * kHalf;       // 32 KB
+constexpr int kStages = 2;
+constexpr int kStageBytes = 3 * kTile;  // raw K (-> phi1'(K)), V, phi1(K)
+constexpr int kDzOff = kStages * kStageBytes;
+constexpr int kBarOff = kDzOff + kTile;
+constexpr int kSmem = kBarOff + 256 + 1024;
+constexpr int kThreads = 384;
+constexpr int kXform = 256;  // threads of warps 4..11
+
+struct Bars {
+    uint64_t kv_full[kStages], k_ready[kStages], kv_empty[kStages];
+    uint64_t acc_full[2], acc_empty[2];
+    uint64_t dz_full, dz_empty;
+    uint32_t tmem_base;
+};
+
+struct Params {
+    const int64_t* offsets;
+    const int64_t* uts;
+    const uint8_t* dz_op;  // [B*H][32 KB]
+    __nv_bfloat16* dk;
+    __nv_bfloat16* dv;
+    int B, H;
+};
+
+__device__ __forceinline__ float phi_f(int kind, float x) {
+    if (kind == VISTA_ACT_SILU) return x * __frcp_rn(1.f + __expf(-x));
+    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? x : __expf(x - 1.f);
+    return x;
+}
+__device__ __forceinline__ float phi_prime_f(int kind, float x) {
+    if (kind == VISTA_ACT_SILU) {
+        const float s = __frcp_rn(1.f + __expf(-x));
+        return s * (1.f + x * (1.f - s));
+    }
+    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? 1.f : __expf(x - 1.f);
+    return 1.f;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// phi1(K) into the phi buffer and phi1'(K) over the raw K, 16-B chunk by chunk (the 128-B swizzle
+// only permutes chunks within a row, so the transform is layout-agnostic).
+template <int PHI>
+__device__ __forceinline__ void xform_tile(uint32_t kbuf, uint32_t pbuf, int xt) {
+#pragma unroll 2
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t off = (uint32_t)(xt + i * kXform) * 16;
+        const uint4 raw = lds128(kbuf + off);
+        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+        uint32_t ph[4], pr[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
+            ph[e] = ptx::pack_bf16x2(phi_f(PHI, lo), phi_f(PHI, hi));
+            pr[e] = ptx::pack_bf16x2(phi_prime_f(PHI, lo), phi_prime_f(PHI, hi));
+        }
+        sts128(pbuf + off, make_uint4(ph[0], ph[1], ph[2], ph[3]));
+        sts128(kbuf + off, make_uint4(pr[0], pr[1], pr[2], pr[3]));
+    }
+}
+
+template <int ST, int AB>
+__device__ __forceinline__ void issue_tile(uint32_t tmem, uint32_t base) {
+    const uint32_t kb = base + ST * kStageBytes, vb = kb + kTile, pb = vb + kTile, dz = base + kDzOff;
+    constexpr uint32_t idV = ptx::idesc_bf16_f32(128, 128, 0, 1);  // A K-major, B MN-major
+    constexpr uint32_t idK = ptx::idesc_bf16_f32(128, 128, 0, 0);  // both K-major
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t ak = (kk >> 2) * kHalf + (kk & 3) * 32;
+        // dV = phi1(K) dZ : A [item][c1] K-major, B = dZ [K = c1][N = c2] MN-major
+        ptx::mma_ss_w(tmem + AB * 256, ptx::sdesc_sw128(pb + ak, 16, 1024), ptx::sdesc_sw128(dz + kk * 2048, kHalf, 1024),
+                      idV, kk > 0);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t ak = (kk >> 2) * kHalf + (kk & 3) * 32;
+        // dK' = V dZ^T : A = V [item][c2] K-major, B = dZ [N = c1][K = c2] K-major
+        ptx::mma_ss_w(tmem + AB * 256 + 128, ptx::sdesc_sw128(vb + ak, 16, 1024), ptx::sdesc_sw128(dz + ak, 16, 1024),
+                      idK, kk > 0);
+    }
+}
+__device__ __forceinline__ void issue_tile_d(int st, int ab, uint32_t tmem, uint32_t base) {
+    if (st == 0) { if (ab == 0) issue_tile<0, 0>(tmem, base); else issue_tile<0, 1>(tmem, base); }
+    else { if (ab == 0) issue_tile<1, 0>(tmem, base); else issue_tile<1, 1>(tmem, base); }
+}
+
+__device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
+template <int PHI1>
+__global__ void __launch_bounds__(kThreads, 1)
+    sm100_qla_bwd_kv_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+                            const Params P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t base = ptx::smem_u32(smem);
+    Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int cta = blockIdx.x, num_ctas = gridDim.x;
+    const int HG = P.H;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&bars->kv_full[s], 1);
+            ptx::mbar_init(&bars->k_ready[s], kXform);
+            ptx::mbar_init(&bars->kv_empty[s], kXform);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bars->acc_full[b], 1);
+            ptx::mbar_init(&bars->acc_empty[b], kXform);
+        }
+        ptx::mbar_init(&bars->dz_full, 1);
+        ptx::mbar_init(&bars->dz_empty, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
+
+    ItemIter iter;
+    iter.init(P.uts, P.B, HG, cta, num_ctas);
+    Item it;
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        ptx::tma_prefetch(&mapK);
+        ptx::tma_prefetch(&mapV);
+        const uint64_t pol = ptx::policy_evict_first();
+        int stage = 0;
+        uint32_t phase = 0;
+        int k = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            const int h = it.hg;
+            // dZ of this unit (the MMAs of the previous unit must be done with the buffer)
+            if (k > 0) ptx::mbar_wait(&bars->dz_empty, (k - 1) & 1);
+            ptx::mbar_arrive_expect_tx_w(&bars->dz_full, kTile);
+            ptx::bulk_g2s_w(base + kDzOff, P.dz_op + (size_t)(it.u * HG + it.hg) * kTile, kTile, &bars->dz_full);
+            const int64_t row0 = P.offsets[it.u];
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->kv_empty[stage], phase ^ 1);
+                ptx::mbar_arrive_expect_tx_w(&bars->kv_full[stage], 2 * kTile);
+                uint8_t* sk = smem + stage * kStageBytes;
+                const int32_t row = (int32_t)(row0 + (int64_t)t * 128);
+                for (int half = 0; half < 2; ++half) {
+                    ptx::tma_load_3d_w(sk + half * kHalf, &mapK, &bars->kv_full[stage], half * 64, h, row, pol);
+                    ptx::tma_load_3d_w(sk + kTile + half * kHalf, &mapV, &bars->kv_full[stage], half * 64, h, row, pol);
+                }
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
+            }
+            ++k;
+        }
+    } else if (warp == 1) {
+        // ============================ MMA issuer ============================
+        int stage = 0;
+        uint32_t phase = 0;
+        int ab = 0;
+        uint32_t aph[2] = {0, 0};
+        int k = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            ptx::mbar_wait(&bars->dz_full, k & 1);
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->k_ready[stage], phase);
+                ptx::mbar_wait(&bars->acc_empty[ab], aph[ab] ^ 1);
+                aph[ab] ^= 1;
+                ptx::tc_fence_after();
+                issue_tile_d(stage, ab, tmem, base);
+                ptx::mma_commit_w(&bars->acc_full[ab]);
+                ab ^= 1;
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
+            }
+            ptx::mma_commit_w(&bars->dz_empty);  // dZ free once this unit's GEMMs complete
+            ++k;
+        }
+    } else if (warp >= 4) {
+        // ============================ transform + epilogue ============================
+        const int xt = threadIdx.x - 128;
+        const int wq = warp % 4;
+        const int chalf = (warp - 4) / 4;  // epilogue columns [64 chalf, 64 chalf + 64)
+        const int row = wq * 32 + lane;    // item row within the tile = TMEM lane
+        const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
+        int stage = 0;
+        uint32_t phase = 0;
+        int ab = 0;
+        uint32_t aph[2] = {0, 0};
+        // epilogue of the previous tile is deferred by one tile (after the next transform)
+        bool pend = false;
+        int p_stage = 0, p_ab = 0;
+        int64_t p_row0 = 0;
+        int p_valid = 0, p_h = 0;
+        auto epilogue = [&](int est, int eab, int64_t grow0, int valid, int h) {
+            ptx::mbar_wait(&bars->acc_full[eab], aph[eab]);
+            aph[eab] ^= 1;
+            ptx::tc_fence_after();
+            const bool ok = row < valid;
+            const size_t gidx = ((size_t)(grow0 + row) * P.H + h) * 128 + chalf * 64;
+            const uint32_t kb = base + est * kStageBytes;  // phi1'(K)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t rv[32], rk[32];
+                ptx::tmem_ld32(tmem + lane_bits + eab * 256 + chalf * 64 + c * 32, rv);
+                ptx::tmem_ld32(tmem + lane_bits + eab * 256 + 128 + chalf * 64 + c * 32, rk);
+                ptx::tmem_wait_ld();
+                ptx::reg_fence(rv);
+                ptx::reg_fence(rk);
+                // phi1'(k) for columns [64 chalf + 32 c, +32): 4 chunks of 8 bf16 in the swizzled row
+                uint32_t dp[16];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int col = chalf * 64 + c * 32 + q * 8;
+                    const uint4 pr = lds128(kb + qla_w_swz(row, col));
+                    dp[4 * q] = pr.x;
+                    dp[4 * q + 1] = pr.y;
+                    dp[4 * q + 2] = pr.z;
+                    dp[4 * q + 3] = pr.w;
+                }
+                if (ok) {
+                    uint32_t wv[16], wk[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        wv[j] = ptx::pack_bf16x2(__uint_as_float(rv[2 * j]), __uint_as_float(rv[2 * j + 1]));
+                        const float d0 = __uint_as_float(dp[j] << 16), d1 = __uint_as_float(dp[j] & 0xFFFF0000u);
+                        wk[j] = ptx::pack_bf16x2(__uint_as_float(rk[2 * j]) * d0, __uint_as_float(rk[2 * j + 1]) * d1);
+                    }
+                    const uint32_t v0[8] = {wv[0], wv[1], wv[2], wv[3], wv[4], wv[5], wv[6], wv[7]};
+                    const uint32_t v1[8] = {wv[8], wv[9], wv[10], wv[11], wv[12], wv[13], wv[14], wv[15]};
+                    const uint32_t k0[8] = {wk[0], wk[1], wk[2], wk[3], wk[4], wk[5], wk[6], wk[7]};
+                    const uint32_t k1[8] = {wk[8], wk[9], wk[10], wk[11], wk[12], wk[13], wk[14], wk[15]};
+                    st_v8(P.dv + gidx + c * 32, v0);
+                    st_v8(P.dv + gidx + c * 32 + 16, v1);
+                    st_v8(P.dk + gidx + c * 32, k0);
+                    st_v8(P.dk + gidx + c * 32 + 16, k1);
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&bars->acc_empty[eab]);
+            ptx::mbar_arrive(&bars->kv_empty[est]);
+        };
+        while (iter.next(it, P.uts, P.B, HG)) {
+            const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
+            const int64_t row0 = P.offsets[it.u];
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->kv_full[stage], phase);
+                xform_tile<PHI1>(base + stage * kStageBytes, base + stage * kStageBytes + 2 * kTile, xt);
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(&bars->k_ready[stage]);
+                if (pend) epilogue(p_stage, p_ab, p_row0, p_valid, p_h);
+                pend = true;
+                p_stage = stage;
+                p_ab = ab;
+                p_row0 = row0 + (int64_t)t * 128;
+                const int64_t rem = L - (int64_t)t * 128;
+                p_valid = rem < 128 ? (int)rem : 128;
+                p_h = it.hg;
+                ab ^= 1;
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
+            }
+        }
+        if (pend) epilogue(p_stage, p_ab, p_row0, p_valid, p_h);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+
+template <int PHI1>
+cudaError_t launch_phi(const Problem& p, int num_ctas, const CUtensorMap& mk, const CUtensorMap& mv, const Params& P) {
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(sm100_qla_bwd_kv_kernel<PHI1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (attr != cudaSuccess) return attr;
+    sm100_qla_bwd_kv_kernel<PHI1><<<num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool qla_bwd_uses_tc(const Problem& p) {
+    return p.in_bf16 && p.d == 128 && p.total_len < (int64_t(1) << 31);
+}
+
+cudaError_t launch_sm100_qla_bwd_kv(const Problem& p, const Workspace& w, char* ws, const uint8_t* dz_op, void* dk,
+                                    void* dv) {
+    CUtensorMap mk, mv;
+    if (!make_kv_map(&mk, p.k, p.total_len, p.H) || !make_kv_map(&mv, p.v, p.total_len, p.H))
+        return cudaErrorInvalidValue;
+    Params P;
+    P.offsets = p.offsets;
+    P.uts = reinterpret_cast<const int64_t*>(ws + w.uts_off);
+    P.dz_op = dz_op;
+    P.dk = reinterpret_cast<__nv_bfloat16*>(dk);
+    P.dv = reinterpret_cast<__nv_bfloat16*>(dv);
+    P.B = p.B;
+    P.H = p.H;
+    return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU>(p, w.num_ctas, mk, mv, P)
+         : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU>(p, w.num_ctas, mk, mv, P)
+                                           : launch_phi<VISTA_ACT_IDENTITY>(p, w.num_ctas, mk, mv, P);
+}
+
+}  // namespace vista

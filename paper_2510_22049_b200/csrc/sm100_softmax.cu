@@ -352,6 +352,19 @@ __device__ __forceinline__ float exp_part(const uint32_t (&r)[4][32], float sl2,
     return (la + lb) + (lc + ld);
 }
 
+#ifndef VISTA_MMA_SPIN
+#define VISTA_MMA_SPIN 0
+#endif
+// The MMA warp's waits for P: optionally poll (test_wait) before the suspending try_wait.
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t phase) {
+#if VISTA_MMA_SPIN > 0
+#pragma unroll 1
+    for (int i = 0; i < VISTA_MMA_SPIN; ++i)
+        if (ptx::mbar_test_wait(bar, phase)) return;
+#endif
+    ptx::mbar_wait(bar, phase);
+}
+
 // ---- MMA issue with compile-time geometry (see the MMA role) ----
 template <int NQ, int Q, int ST>
 __device__ __forceinline__ void issue_S_t(uint32_t tmem, uint32_t sQa, uint32_t sKa) {
@@ -592,13 +605,13 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
 #pragma unroll
                     for (int q = 0; q < NQ; ++q) {
                         if (first_item && lane == 0) VTRACE(0, t, q);
-                        ptx::mbar_wait(&bars->p_full[q][0], p_phase[q]);
+                        mma_wait(&bars->p_full[q][0], p_phase[q]);
                         if (first_item && lane == 0) VTRACE(1, t, q);
                         ptx::tc_fence_after();
                         if constexpr (kSplitP == 2) {
                             // keys 0-63 as soon as their P is in TMEM, keys 64-127 after the rest
                             issue_PV_d<NQ, 0, 4>(q, vst, t > 0, tmem, sVa);
-                            ptx::mbar_wait(&bars->p_full[q][1], p_phase[q]);
+                            mma_wait(&bars->p_full[q][1], p_phase[q]);
                             ptx::tc_fence_after();
                             issue_PV_d<NQ, 4, 8>(q, vst, true, tmem, sVa);
                         } else if constexpr (kSplitP == 4) {

@@ -417,6 +417,104 @@ vista_status_t vista_summarize_partial_prefix(const vista_desc_t* desc, const vo
                       stream);
 }
 
+// ---- backward (NEXT-2).  QLA: recompute Z (forward partial pass), per-unit dW / dZ / dQ, dK / dV.
+// Workspace: [forward sub-run | Z | dZ | dZ bf16 operands (tcgen05 path) | per-user dQ (shared seeds)].
+namespace {
+struct BwdPlan {
+    size_t sub_off, z_off, dz_off, dzop_off, dqu_off, total;
+};
+BwdPlan plan_bwd(const Problem& p) {
+    BwdPlan b{};
+    const size_t B = (size_t)p.B, H = (size_t)p.H, S = (size_t)p.S, d = (size_t)p.d;
+    size_t off = 0;
+    b.sub_off = off;
+    off = align256(off + plan_workspace(p, true).total);
+    b.z_off = off;
+    off = align256(off + B * H * d * d * sizeof(float));
+    b.dz_off = off;
+    off = align256(off + B * H * d * d * sizeof(float));
+    b.dzop_off = off;
+    if (qla_bwd_uses_tc(p)) off = align256(off + B * H * d * d * 2);
+    b.dqu_off = off;
+    if (p.q_user_stride == 0) off = align256(off + B * S * H * d * sizeof(float));
+    b.total = off;
+    return b;
+}
+}  // namespace
+
+vista_status_t vista_summarize_bwd_workspace_size(const vista_desc_t* desc, int64_t total_len, size_t* bytes) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (!bytes) return VISTA_ERR_NULL;
+    if (total_len < 0) return VISTA_ERR_INVALID;
+    if (desc->attn != VISTA_QLA) return VISTA_ERR_UNSUPPORTED;
+    *bytes = plan_bwd(make_problem(desc, total_len)).total;
+    return VISTA_OK;
+}
+
+vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                   const int64_t* offsets, int64_t total_len, const void* out, const float* lse,
+                                   const void* dout, float* dq, void* dk, void* dv, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+    (void)out;
+    (void)lse;
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (desc->attn != VISTA_QLA) return VISTA_ERR_UNSUPPORTED;  // softmax backward: not yet
+    if (total_len < 0) return VISTA_ERR_INVALID;
+    if (!q || !offsets || !dout || !dq) return VISTA_ERR_NULL;
+    if (total_len > 0 && (!k || !v || !dk || !dv)) return VISTA_ERR_NULL;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dq) || !aligned16(dk) ||
+        !aligned16(dv))
+        return VISTA_ERR_MISALIGNED;
+    Problem p = make_problem(desc, total_len);
+    p.q = q;
+    p.k = k;
+    p.v = v;
+    p.offsets = offsets;
+    p.stream = reinterpret_cast<cudaStream_t>(stream);
+    if (p.B == 0) return VISTA_OK;
+    const BwdPlan b = plan_bwd(p);
+    if (!workspace || workspace_bytes < b.total) return VISTA_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
+    char* ws = reinterpret_cast<char*>(workspace);
+    float* z = reinterpret_cast<float*>(ws + b.z_off);
+    float* dz = reinterpret_cast<float*>(ws + b.dz_off);
+    const bool tc = qla_bwd_uses_tc(p);
+    uint8_t* dz_op = tc ? reinterpret_cast<uint8_t*>(ws + b.dzop_off) : nullptr;
+    float* dqu = p.q_user_stride == 0 ? reinterpret_cast<float*>(ws + b.dqu_off) : dq;
+    // 1. Z = sum_j phi1(k_j)^T v_j (the forward state kernel, partial mode).  The timing hook, if
+    //    armed, is kept for the dK / dV kernel (the dominant one of the backward).
+    cudaEvent_t ev_a = g_ev_start, ev_b = g_ev_stop;
+    g_ev_start = g_ev_stop = nullptr;
+    st = run(desc, q, k, v, offsets, total_len, OutSpec{OUT_PARTIAL, 0, z, nullptr}, ws + b.sub_off,
+             b.z_off - b.sub_off, stream);
+    g_ev_start = ev_a;
+    g_ev_stop = ev_b;
+    if (st != VISTA_OK) return st;
+    // 2. per unit: dW, dZ, dA -> dQ_u
+    cudaError_t e = launch_qla_bwd_unit(p, desc->out_dtype == VISTA_BF16, dout, z, dz, dz_op, dqu);
+    int nl = 1;
+    // 3. shared seeds: dQ = sum_u dQ_u
+    if (e == cudaSuccess && p.q_user_stride == 0) {
+        e = launch_qla_bwd_dq_sum(p, dqu, dq);
+        ++nl;
+    }
+    // 4. dK, dV
+    if (e == cudaSuccess && total_len > 0) {
+        if (tc) {
+            const Workspace w = plan_workspace(p, true);
+            e = timed_main(p.stream, [&] { return launch_sm100_qla_bwd_kv(p, w, ws + b.sub_off, dz_op, dk, dv); });
+        } else {
+            e = timed_main(p.stream, [&] { return launch_qla_bwd_kv_simt(p, dz, dk, dv); });
+        }
+        ++nl;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches += (unsigned long long)nl;
+    return VISTA_OK;
+}
+
 static size_t merge_ws_bytes(const Problem& p) {
     return (p.attn == VISTA_QLA && qla_finalize_uses_tc(p)) ? sm100_qla_finalize_workspace(p) : 0;
 }

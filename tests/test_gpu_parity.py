@@ -446,3 +446,75 @@ def test_prefix_requires_shared_seeds(cuda_lib):
     with pytest.raises(vista.VistaError) as e:
         vista.vista_summarize_fwd_prefix(d, buf, buf, buf, buf, 0, buf, buf, P, buf, None, buf, n)
     assert "UNSUPPORTED" in str(e.value)
+
+
+# ----------------------------------------------------------------------------- QLA backward (NEXT-2)
+def _bwd_check(g, ref, tol, what):
+    g = g.float().cpu().numpy().astype(np.float64) if hasattr(g, "cpu") else g
+    den = np.abs(ref).max()
+    e = np.abs(g - ref).max() / (den if den > 0 else 1.0)
+    assert e <= tol, f"{what}: rel err {e:.3g} > {tol}"
+
+
+@pytest.mark.parametrize("phi1,phi2,normalize", [("silu", "silu", True), ("shifted_elu", "identity", False),
+                                                 ("identity", "shifted_elu", True)])
+def test_qla_backward_tcgen05(cuda_lib, phi1, phi2, normalize):
+    vista = cuda_lib
+    lens = [0, 129, 2049, 5, 300]
+    S, H, d = 256, 2, 128
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=21, tau=1)
+    rng = np.random.default_rng(4)
+    g = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    dq, dk, dv = vista.summarize_bwd(to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16"),
+                                     torch.from_numpy(off).cuda(), int(off[-1]), to_dev(g, "bf16"),
+                                     phi1=phi1, phi2=phi2, normalize=normalize)
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.qla_backward(q, k, v, off, g, phi1, phi2, normalize)
+    _bwd_check(dq, rq, 2e-2, "dq")
+    # dk / dv per user block (users' gradient scales differ by 1/N)
+    dkn = dk.float().cpu().numpy()
+    dvn = dv.float().cpu().numpy()
+    for u in range(len(lens)):
+        a, b = off[u], off[u + 1]
+        if b > a:
+            _bwd_check(dkn[a:b], rk[a:b], 2e-2, f"dk user {u}")
+            _bwd_check(dvn[a:b], rv[a:b], 2e-2, f"dv user {u}")
+
+
+@pytest.mark.parametrize("d,dtype", [(32, "f32"), (64, "bf16"), (128, "f32")])
+def test_qla_backward_simt(cuda_lib, d, dtype):
+    vista = cuda_lib
+    lens = [100, 0, 33]
+    S, H = 16, 2
+    q, k, v, off = synth.make_batch(lens, S, H, d, dtype=dtype, seed=d, tau=1)
+    rng = np.random.default_rng(5)
+    g = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    dq, dk, dv = vista.summarize_bwd(to_dev(q, dtype), to_dev(k, dtype), to_dev(v, dtype),
+                                     torch.from_numpy(off).cuda(), int(off[-1]), to_dev(g, dtype),
+                                     phi1="silu", phi2="silu", normalize=True)
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.qla_backward(q, k, v, off, g, "silu", "silu", True)
+    tol = 1e-4 if dtype == "f32" else 2e-2
+    _bwd_check(dq, rq, tol, "dq")
+    dkn, dvn = dk.float().cpu().numpy(), dv.float().cpu().numpy()
+    for u in range(len(lens)):
+        a, b = off[u], off[u + 1]
+        if b > a:
+            _bwd_check(dkn[a:b], rk[a:b], tol, f"dk user {u}")
+            _bwd_check(dvn[a:b], rv[a:b], tol, f"dv user {u}")
+
+
+def test_qla_backward_per_user_seeds(cuda_lib):
+    vista = cuda_lib
+    lens = [700, 3]
+    S, H, d = 128, 1, 128
+    rng = np.random.default_rng(6)
+    q = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    _, k, v, off = synth.make_batch(lens, S, H, d, seed=6)
+    g = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    dq, dk, dv = vista.summarize_bwd(to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16"),
+                                     torch.from_numpy(off).cuda(), int(off[-1]), to_dev(g, "bf16"))
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.qla_backward(q, k, v, off, g, "silu", "silu", True, q_per_user=True)
+    for u in range(len(lens)):
+        _bwd_check(dq[u], rq[u], 2e-2, f"dq user {u}")

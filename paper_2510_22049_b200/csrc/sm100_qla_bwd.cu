@@ -27,8 +27,8 @@ namespace {
 
 constexpr int kHalf = 128 * 128;       // one 64-column half of a 128 x 128 bf16 tile
 constexpr int kTile = 2 * kHalf;       // 32 KB
-constexpr int kStages = 2;
-constexpr int kStageBytes = 3 * kTile;  // raw K (-> phi1'(K)), V, phi1(K)
+constexpr int kStages = 3;
+constexpr int kStageBytes = 2 * kTile;  // K (-> phi1(K) in place), V
 constexpr int kDzOff = kStages * kStageBytes;
 constexpr int kBarOff = kDzOff + kTile;
 constexpr int kSmem = kBarOff + 256 + 1024;
@@ -45,24 +45,31 @@ struct Bars {
 struct Params {
     const int64_t* offsets;
     const int64_t* uts;
+    const __nv_bfloat16* k;  // raw K (the epilogue re-reads it for phi1'(K))
     const uint8_t* dz_op;  // [B*H][32 KB]
     __nv_bfloat16* dk;
     __nv_bfloat16* dv;
     int B, H;
 };
 
-__device__ __forceinline__ float phi_f(int kind, float x) {
-    if (kind == VISTA_ACT_SILU) return x * __frcp_rn(1.f + __expf(-x));
-    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? x : __expf(x - 1.f);
-    return x;
-}
-__device__ __forceinline__ float phi_prime_f(int kind, float x) {
-    if (kind == VISTA_ACT_SILU) {
-        const float s = __frcp_rn(1.f + __expf(-x));
-        return s * (1.f + x * (1.f - s));
+// phi1 and phi1' of one value with shared work: SiLU through sigma(x) = (1 + tanh(x/2)) / 2 (one
+// MUFU op), shifted ELU through one exp.
+template <int PHI>
+__device__ __forceinline__ void phi_and_prime(float x, float& f, float& fp) {
+    if constexpr (PHI == VISTA_ACT_SILU) {
+        float t;
+        asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+        const float sg = fmaf(0.5f, t, 0.5f);
+        f = x * sg;
+        fp = sg * fmaf(x, 1.f - sg, 1.f);
+    } else if constexpr (PHI == VISTA_ACT_SHIFTED_ELU) {
+        const float e = ptx::ex2((x - 1.f) * 1.4426950408889634f);
+        f = x >= 1.f ? x : e;
+        fp = x >= 1.f ? 1.f : e;
+    } else {
+        f = x;
+        fp = 1.f;
     }
-    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? 1.f : __expf(x - 1.f);
-    return 1.f;
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
@@ -75,30 +82,32 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
                  : "memory");
 }
 
-// phi1(K) into the phi buffer and phi1'(K) over the raw K, 16-B chunk by chunk (the 128-B swizzle
-// only permutes chunks within a row, so the transform is layout-agnostic).
+// phi1(K) in place, 16-B chunk by chunk (the 128-B swizzle only permutes chunks within a row, so
+// the transform is layout-agnostic).  phi1'(K) is recomputed in the epilogue from the raw K rows
+// (re-read through L2), so a stage is free as soon as its GEMMs complete.
 template <int PHI>
-__device__ __forceinline__ void xform_tile(uint32_t kbuf, uint32_t pbuf, int xt) {
-#pragma unroll 2
+__device__ __forceinline__ void xform_tile(uint32_t kbuf, int xt) {
+#pragma unroll 4
     for (int i = 0; i < 8; ++i) {
         const uint32_t off = (uint32_t)(xt + i * kXform) * 16;
         const uint4 raw = lds128(kbuf + off);
         const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-        uint32_t ph[4], pr[4];
+        uint32_t ph[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
-            ph[e] = ptx::pack_bf16x2(phi_f(PHI, lo), phi_f(PHI, hi));
-            pr[e] = ptx::pack_bf16x2(phi_prime_f(PHI, lo), phi_prime_f(PHI, hi));
+            float f0, p0, f1, p1;
+            phi_and_prime<PHI>(lo, f0, p0);
+            phi_and_prime<PHI>(hi, f1, p1);
+            ph[e] = ptx::pack_bf16x2(f0, f1);
         }
-        sts128(pbuf + off, make_uint4(ph[0], ph[1], ph[2], ph[3]));
-        sts128(kbuf + off, make_uint4(pr[0], pr[1], pr[2], pr[3]));
+        sts128(kbuf + off, make_uint4(ph[0], ph[1], ph[2], ph[3]));
     }
 }
 
 template <int ST, int AB>
 __device__ __forceinline__ void issue_tile(uint32_t tmem, uint32_t base) {
-    const uint32_t kb = base + ST * kStageBytes, vb = kb + kTile, pb = vb + kTile, dz = base + kDzOff;
+    const uint32_t kb = base + ST * kStageBytes, vb = kb + kTile, pb = kb, dz = base + kDzOff;
     constexpr uint32_t idV = ptx::idesc_bf16_f32(128, 128, 0, 1);  // A K-major, B MN-major
     constexpr uint32_t idK = ptx::idesc_bf16_f32(128, 128, 0, 0);  // both K-major
 #pragma unroll
@@ -118,7 +127,8 @@ __device__ __forceinline__ void issue_tile(uint32_t tmem, uint32_t base) {
 }
 __device__ __forceinline__ void issue_tile_d(int st, int ab, uint32_t tmem, uint32_t base) {
     if (st == 0) { if (ab == 0) issue_tile<0, 0>(tmem, base); else issue_tile<0, 1>(tmem, base); }
-    else { if (ab == 0) issue_tile<1, 0>(tmem, base); else issue_tile<1, 1>(tmem, base); }
+    else if (st == 1) { if (ab == 0) issue_tile<1, 0>(tmem, base); else issue_tile<1, 1>(tmem, base); }
+    else { if (ab == 0) issue_tile<2, 0>(tmem, base); else issue_tile<2, 1>(tmem, base); }
 }
 
 __device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&bars->kv_full[s], 1);
             ptx::mbar_init(&bars->k_ready[s], kXform);
-            ptx::mbar_init(&bars->kv_empty[s], kXform);
+            ptx::mbar_init(&bars->kv_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&bars->acc_full[b], 1);
@@ -166,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch(&mapK);
         ptx::tma_prefetch(&mapV);
         const uint64_t pol = ptx::policy_evict_first();
+        const uint64_t pol_k = ptx::policy_evict_last();  // re-read by the epilogue for phi1'(K)
         int stage = 0;
         uint32_t phase = 0;
         int k = 0;
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* sk = smem + stage * kStageBytes;
                 const int32_t row = (int32_t)(row0 + (int64_t)t * 128);
                 for (int half = 0; half < 2; ++half) {
-                    ptx::tma_load_3d_w(sk + half * kHalf, &mapK, &bars->kv_full[stage], half * 64, h, row, pol);
+                    ptx::tma_load_3d_w(sk + half * kHalf, &mapK, &bars->kv_full[stage], half * 64, h, row, pol_k);
                     ptx::tma_load_3d_w(sk + kTile + half * kHalf, &mapV, &bars->kv_full[stage], half * 64, h, row, pol);
                 }
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -205,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 issue_tile_d(stage, ab, tmem, base);
                 ptx::mma_commit_w(&bars->acc_full[ab]);
+                ptx::mma_commit_w(&bars->kv_empty[stage]);  // K, V stage free once the GEMMs complete
                 ab ^= 1;
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
@@ -227,60 +239,94 @@ __global__ void __launch_bounds__(kThreads, 1)
         int p_stage = 0, p_ab = 0;
         int64_t p_row0 = 0;
         int p_valid = 0, p_h = 0;
+        // Coalesced row stores (see sm100_softmax.cu store_rows_coalesced): the 32 packed words of a
+        // thread's 64-column row segment go back into the (already read) accumulator columns at
+        // tcol in a permuted order and come out with the 16x256b shape, a quad of threads then
+        // holding 128 contiguous bytes of one row: each warp store writes 8 full lines.
+        auto store32 = [&](uint32_t tcol, const uint32_t (&w)[32], __nv_bfloat16* gbase, int valid) {
+            uint32_t a[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const int g = c >> 3, p = (c & 7) >> 1, e = c & 1;
+                a[c] = w[8 * p + 2 * g + e];
+            }
+            ptx::tmem_st32(tcol, a);
+            ptx::tmem_wait_st();
+            const int p = lane & 3;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t r[16];
+                ptx::tmem_ld16x256b_x4(tcol + ((uint32_t)(16 * half) << 16), r);
+                ptx::tmem_wait_ld();
+                ptx::reg_fence(r);
+                const int ra = wq * 32 + 16 * half + (lane >> 2);
+                const uint32_t v0[8] = {r[0], r[1], r[4], r[5], r[8], r[9], r[12], r[13]};
+                const uint32_t v1[8] = {r[2], r[3], r[6], r[7], r[10], r[11], r[14], r[15]};
+                if (ra < valid) st_v8(gbase + (size_t)ra * P.H * 128 + 16 * p, v0);
+                if (ra + 8 < valid) st_v8(gbase + (size_t)(ra + 8) * P.H * 128 + 16 * p, v1);
+            }
+        };
         auto epilogue = [&](int est, int eab, int64_t grow0, int valid, int h) {
             ptx::mbar_wait(&bars->acc_full[eab], aph[eab]);
             aph[eab] ^= 1;
             ptx::tc_fence_after();
-            const bool ok = row < valid;
-            const size_t gidx = ((size_t)(grow0 + row) * P.H + h) * 128 + chalf * 64;
-            const uint32_t kb = base + est * kStageBytes;  // phi1'(K)
+            const size_t gcol = ((size_t)grow0 * P.H + h) * 128 + chalf * 64;  // row 0 of the tile
+            // raw k of this thread's row, columns [64 chalf, +64): 8 x 16 B through L2 (issued first)
+            uint4 kraw[8];
+            {
+                const int rr = row < valid ? row : 0;
+                const uint4* src = reinterpret_cast<const uint4*>(P.k + ((size_t)(grow0 + rr) * P.H + h) * 128 +
+                                                                  chalf * 64);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t rv[32], rk[32];
-                ptx::tmem_ld32(tmem + lane_bits + eab * 256 + chalf * 64 + c * 32, rv);
-                ptx::tmem_ld32(tmem + lane_bits + eab * 256 + 128 + chalf * 64 + c * 32, rk);
-                ptx::tmem_wait_ld();
-                ptx::reg_fence(rv);
-                ptx::reg_fence(rk);
-                // phi1'(k) for columns [64 chalf + 32 c, +32): 4 chunks of 8 bf16 in the swizzled row
-                uint32_t dp[16];
+                for (int q = 0; q < 8; ++q) kraw[q] = __ldg(src + q);
+            }
+            const uint32_t tv = tmem + lane_bits + eab * 256 + chalf * 64;
+            const uint32_t tk = tv + 128;
+            {  // dV
+                uint32_t w[32];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int col = chalf * 64 + c * 32 + q * 8;
-                    const uint4 pr = lds128(kb + qla_w_swz(row, col));
-                    dp[4 * q] = pr.x;
-                    dp[4 * q + 1] = pr.y;
-                    dp[4 * q + 2] = pr.z;
-                    dp[4 * q + 3] = pr.w;
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t rv[32];
+                    ptx::tmem_ld32_sync(tv + c * 32, rv);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        w[16 * c + j] = ptx::pack_bf16x2(__uint_as_float(rv[2 * j]), __uint_as_float(rv[2 * j + 1]));
                 }
-                if (ok) {
-                    uint32_t wv[16], wk[16];
+                store32(tv, w, P.dv + gcol, valid);
+            }
+            {  // dK = (V dZ^T) . phi1'(K)
+                uint32_t w[32];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        wv[j] = ptx::pack_bf16x2(__uint_as_float(rv[2 * j]), __uint_as_float(rv[2 * j + 1]));
-                        const float d0 = __uint_as_float(dp[j] << 16), d1 = __uint_as_float(dp[j] & 0xFFFF0000u);
-                        wk[j] = ptx::pack_bf16x2(__uint_as_float(rk[2 * j]) * d0, __uint_as_float(rk[2 * j + 1]) * d1);
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t rk[32];
+                    ptx::tmem_ld32_sync(tk + c * 32, rk);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 kr = kraw[4 * c + q];
+                        const uint32_t kw[4] = {kr.x, kr.y, kr.z, kr.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int j = 4 * q + e;
+                            float f, d0, d1;
+                            phi_and_prime<PHI1>(__uint_as_float(kw[e] << 16), f, d0);
+                            phi_and_prime<PHI1>(__uint_as_float(kw[e] & 0xFFFF0000u), f, d1);
+                            w[16 * c + j] = ptx::pack_bf16x2(__uint_as_float(rk[2 * j]) * d0,
+                                                             __uint_as_float(rk[2 * j + 1]) * d1);
+                        }
                     }
-                    const uint32_t v0[8] = {wv[0], wv[1], wv[2], wv[3], wv[4], wv[5], wv[6], wv[7]};
-                    const uint32_t v1[8] = {wv[8], wv[9], wv[10], wv[11], wv[12], wv[13], wv[14], wv[15]};
-                    const uint32_t k0[8] = {wk[0], wk[1], wk[2], wk[3], wk[4], wk[5], wk[6], wk[7]};
-                    const uint32_t k1[8] = {wk[8], wk[9], wk[10], wk[11], wk[12], wk[13], wk[14], wk[15]};
-                    st_v8(P.dv + gidx + c * 32, v0);
-                    st_v8(P.dv + gidx + c * 32 + 16, v1);
-                    st_v8(P.dk + gidx + c * 32, k0);
-                    st_v8(P.dk + gidx + c * 32 + 16, k1);
                 }
+                store32(tk, w, P.dk + gcol, valid);
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&bars->acc_empty[eab]);
-            ptx::mbar_arrive(&bars->kv_empty[est]);
+            (void)est;
         };
         while (iter.next(it, P.uts, P.B, HG)) {
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
             const int64_t row0 = P.offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->kv_full[stage], phase);
-                xform_tile<PHI1>(base + stage * kStageBytes, base + stage * kStageBytes + 2 * kTile, xt);
+                xform_tile<PHI1>(base + stage * kStageBytes, xt);
                 ptx::fence_proxy_async_smem();
                 ptx::mbar_arrive(&bars->k_ready[stage]);
                 if (pend) epilogue(p_stage, p_ab, p_row0, p_valid, p_h);
@@ -326,6 +372,7 @@ cudaError_t launch_sm100_qla_bwd_kv(const Problem& p, const Workspace& w, char* 
     P.offsets = p.offsets;
     P.uts = reinterpret_cast<const int64_t*>(ws + w.uts_off);
     P.dz_op = dz_op;
+    P.k = reinterpret_cast<const __nv_bfloat16*>(p.k);
     P.dk = reinterpret_cast<__nv_bfloat16*>(dk);
     P.dv = reinterpret_cast<__nv_bfloat16*>(dv);
     P.B = p.B;

@@ -108,6 +108,12 @@ cudaError_t launch_qla_bwd_kv_simt(const Problem& p, const float* dz, void* dk, 
 cudaError_t launch_sm100_qla_bwd_kv(const Problem& p, const Workspace& w, char* ws, const uint8_t* dz_op, void* dk,
                                     void* dv);
 bool qla_bwd_uses_tc(const Problem& p);
+// phi1(Q) as bf16 128-row MMA operand blocks (qla_prep_q_kernel); qla_prep_q_bytes of space
+size_t qla_prep_q_bytes(const Problem& p);
+cudaError_t launch_qla_prep_q(const Problem& p, uint8_t* abuf);
+// tcgen05 per-unit backward (dW -> dZ operand, dA -> per-user dQ); needs S % 128 == 0
+cudaError_t launch_sm100_qla_bwd_unit(const Problem& p, bool dout_bf16, const void* dout, const float* z,
+                                      const uint8_t* abuf, uint8_t* dz_op, float* dqu);
 // shared key prefix (vista_summarize_*_prefix)
 cudaError_t launch_write_prefix_offsets(int64_t* off, int64_t P, cudaStream_t st);
 cudaError_t launch_merge_prefix(const Problem& p, const float* o, const float* lse, const float* opre,

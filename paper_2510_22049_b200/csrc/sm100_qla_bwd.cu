@@ -359,6 +359,203 @@ cudaError_t launch_phi(const Problem& p, int num_ctas, const CUtensorMap& mk, co
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------------------
+// Per-unit backward on the tensor cores (one CTA of 128 threads per (u, h); S % 128 == 0):
+//   W = phi2(Zbar) (bf16, K-major [N = c1][K = c2]) built from Z by the threads,
+//   per 128-row block b:  dW += phi1(Q)_b^T dO_b  (both MN-major, K = the block's rows)
+//                         dA_b = dO_b W^T       (dO_b K-major [M = i][K = c2], W K-major)
+//                         dQ_u rows = dA_b . phi1'(Q)            -> f32 dqu
+//   then dZ = dW . phi2'(Zbar) / N_u -> the bf16 operand of the dK / dV kernel.
+namespace {
+namespace ub {
+constexpr int kW = 0, kA = kTile, kG = 2 * kTile;
+constexpr int kSmemU = 3 * kTile + 1024;
+}
+
+// 8 consecutive dO values as 4 packed bf16x2 words (16-B / 2 x 16-B vector loads)
+template <typename TO>
+__device__ __forceinline__ uint4 ld8_bf16(const TO* p);
+template <>
+__device__ __forceinline__ uint4 ld8_bf16<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+}
+template <>
+__device__ __forceinline__ uint4 ld8_bf16<float>(const float* p) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    return make_uint4(ptx::pack_bf16x2(a.x, a.y), ptx::pack_bf16x2(a.z, a.w), ptx::pack_bf16x2(b.x, b.y),
+                      ptx::pack_bf16x2(b.z, b.w));
+}
+
+__device__ __forceinline__ float act_any(int kind, float x) {
+    if (kind == VISTA_ACT_SILU) return x * __frcp_rn(1.f + __expf(-x));
+    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? x : __expf(x - 1.f);
+    return x;
+}
+__device__ __forceinline__ float act_prime_any(int kind, float x) {
+    if (kind == VISTA_ACT_SILU) {
+        const float s = __frcp_rn(1.f + __expf(-x));
+        return s * (1.f + x * (1.f - s));
+    }
+    if (kind == VISTA_ACT_SHIFTED_ELU) return x >= 1.f ? 1.f : __expf(x - 1.f);
+    return 1.f;
+}
+
+template <typename TO>
+__global__ void __launch_bounds__(128) sm100_qla_bwd_unit_kernel(const __nv_bfloat16* __restrict__ q,
+                                                                 int64_t q_user_stride, const TO* __restrict__ dout,
+                                                                 const float* __restrict__ z,
+                                                                 const uint8_t* __restrict__ abuf,
+                                                                 const int64_t* __restrict__ offsets, int S, int H,
+                                                                 int phi1, int phi2, int normalize,
+                                                                 uint8_t* __restrict__ dz_op, float* __restrict__ dqu) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* sm = smem_raw + (base - ptx::smem_u32(smem_raw));
+    __shared__ uint64_t bar_a, bar_mma;
+    __shared__ uint32_t tmem_slot;
+    const int r = threadIdx.x, warp = r / 32;
+    const int unit = blockIdx.x, u = unit / H, h = unit % H;
+    const int nblk = S / 128;
+    const int64_t N = offsets[u + 1] - offsets[u];
+    const float inv = (normalize && N > 0) ? 1.f / (float)N : 1.f;
+    if (warp == 0) ptx::tmem_alloc(&tmem_slot, 256);
+    if (r == 0) {
+        ptx::mbar_init(&bar_a, 1);
+        ptx::mbar_init(&bar_mma, 1);
+        ptx::fence_mbar_init();
+    }
+    // W = phi2(Zbar): thread r builds row c1 = r (K-major [N = c1][K = c2])
+    const float* zrow = z + ((size_t)unit * 128 + r) * 128;
+#pragma unroll 4
+    for (int c = 0; c < 128; c += 8) {
+        const float4 a = *reinterpret_cast<const float4*>(zrow + c), b = *reinterpret_cast<const float4*>(zrow + c + 4);
+        uint4 pk;
+        pk.x = ptx::pack_bf16x2(act_any(phi2, a.x * inv), act_any(phi2, a.y * inv));
+        pk.y = ptx::pack_bf16x2(act_any(phi2, a.z * inv), act_any(phi2, a.w * inv));
+        pk.z = ptx::pack_bf16x2(act_any(phi2, b.x * inv), act_any(phi2, b.y * inv));
+        pk.w = ptx::pack_bf16x2(act_any(phi2, b.z * inv), act_any(phi2, b.w * inv));
+        *reinterpret_cast<uint4*>(sm + ub::kW + qla_w_swz(r, c)) = pk;
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_slot, 0);
+    const uint32_t tdW = tmem, tdA = tmem + 128;
+    const uint32_t lane_bits = (uint32_t)(warp * 32) << 16;
+    const __nv_bfloat16* qu = q + (size_t)(q_user_stride ? u : 0) * q_user_stride;
+    const uint8_t* au = abuf + (size_t)((q_user_stride ? u : 0) * H + h) * nblk * kTile;
+    for (int b = 0; b < nblk; ++b) {
+        // phi1(Q) block by bulk copy; dO block (row i = 128 b + r) by the threads, swizzled
+        if (warp == 0) {
+            ptx::mbar_arrive_expect_tx_w(&bar_a, kTile);
+            ptx::bulk_g2s_w(base + ub::kA, au + (size_t)b * kTile, kTile, &bar_a);
+        }
+        const int i = b * 128 + r;
+        const TO* go = dout + (((size_t)u * S + i) * H + h) * 128;
+        uint4 gv[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) gv[c] = ld8_bf16<TO>(go + 8 * c);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) *reinterpret_cast<uint4*>(sm + ub::kG + qla_w_swz(r, 8 * c)) = gv[c];
+        ptx::fence_proxy_async_smem();
+        __syncthreads();
+        if (warp == 0) {
+            ptx::mbar_wait(&bar_a, b & 1);
+            ptx::tc_fence_after();
+            constexpr uint32_t idW = ptx::idesc_bf16_f32(128, 128, 1, 1);  // both MN-major
+            constexpr uint32_t idA = ptx::idesc_bf16_f32(128, 128, 0, 0);  // both K-major
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                ptx::mma_ss_w(tdW, ptx::sdesc_sw128(base + ub::kA + kk * 2048, kHalf, 1024),
+                              ptx::sdesc_sw128(base + ub::kG + kk * 2048, kHalf, 1024), idW, (b > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t ak = (kk >> 2) * kHalf + (kk & 3) * 32;
+                ptx::mma_ss_w(tdA, ptx::sdesc_sw128(base + ub::kG + ak, 16, 1024),
+                              ptx::sdesc_sw128(base + ub::kW + ak, 16, 1024), idA, kk > 0);
+            }
+            ptx::mma_commit_w(&bar_mma);
+        }
+        ptx::mbar_wait(&bar_mma, b & 1);
+        ptx::tc_fence_after();
+        // dQ rows of this block: dA . phi1'(q)
+        const __nv_bfloat16* qi = qu + ((size_t)i * H + h) * 128;
+        float* dst = dqu + (((size_t)u * S + i) * H + h) * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint4 qv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) qv[e] = __ldg(reinterpret_cast<const uint4*>(qi + c * 32) + e);
+            uint32_t o[32];
+            ptx::tmem_ld32_sync(tdA + lane_bits + c * 32, o);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t w[4] = {qv[e].x, qv[e].y, qv[e].z, qv[e].w};
+#pragma unroll
+                for (int f = 0; f < 4; f += 2) {
+                    const int j = 8 * e + 2 * f;
+                    float4 v;
+                    v.x = __uint_as_float(o[j]) * act_prime_any(phi1, __uint_as_float(w[f] << 16));
+                    v.y = __uint_as_float(o[j + 1]) * act_prime_any(phi1, __uint_as_float(w[f] & 0xFFFF0000u));
+                    v.z = __uint_as_float(o[j + 2]) * act_prime_any(phi1, __uint_as_float(w[f + 1] << 16));
+                    v.w = __uint_as_float(o[j + 3]) * act_prime_any(phi1, __uint_as_float(w[f + 1] & 0xFFFF0000u));
+                    *reinterpret_cast<float4*>(dst + c * 32 + j) = v;
+                }
+            }
+        }
+        ptx::tc_fence_before();
+        __syncthreads();  // smem blocks and the dA columns are reused by the next block
+        ptx::tc_fence_after();
+    }
+    // dZ = dW . phi2'(Zbar) / N -> bf16 operand row c1 = r
+    uint8_t* dzu = dz_op + (size_t)unit * kTile;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        ptx::tmem_ld32_sync(tdW + lane_bits + c * 32, o);
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            const float4 za = __ldg(reinterpret_cast<const float4*>(zrow + c * 32 + j));
+            const float4 zb = __ldg(reinterpret_cast<const float4*>(zrow + c * 32 + j + 4));
+            const float zz[8] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float g0 = __uint_as_float(o[j + 2 * e]) * act_prime_any(phi2, zz[2 * e] * inv) * inv;
+                const float g1 = __uint_as_float(o[j + 2 * e + 1]) * act_prime_any(phi2, zz[2 * e + 1] * inv) * inv;
+                w[e] = ptx::pack_bf16x2(g0, g1);
+            }
+            *reinterpret_cast<uint4*>(dzu + qla_w_swz(r, c * 32 + j)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tmem, 256);
+}
+}  // namespace
+
+cudaError_t launch_sm100_qla_bwd_unit(const Problem& p, bool dout_bf16, const void* dout, const float* z,
+                                      const uint8_t* abuf, uint8_t* dz_op, float* dqu) {
+    if (p.B == 0) return cudaSuccess;
+    const int smem = ub::kSmemU;
+    if (dout_bf16) {
+        static const cudaError_t attr = cudaFuncSetAttribute(sm100_qla_bwd_unit_kernel<__nv_bfloat16>,
+                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (attr != cudaSuccess) return attr;
+        sm100_qla_bwd_unit_kernel<__nv_bfloat16><<<p.B * p.H, 128, smem, p.stream>>>(
+            reinterpret_cast<const __nv_bfloat16*>(p.q), p.q_user_stride, reinterpret_cast<const __nv_bfloat16*>(dout),
+            z, abuf, p.offsets, p.S, p.H, p.phi1, p.phi2, p.normalize, dz_op, dqu);
+    } else {
+        static const cudaError_t attr = cudaFuncSetAttribute(sm100_qla_bwd_unit_kernel<float>,
+                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (attr != cudaSuccess) return attr;
+        sm100_qla_bwd_unit_kernel<float><<<p.B * p.H, 128, smem, p.stream>>>(
+            reinterpret_cast<const __nv_bfloat16*>(p.q), p.q_user_stride, reinterpret_cast<const float*>(dout), z, abuf,
+            p.offsets, p.S, p.H, p.phi1, p.phi2, p.normalize, dz_op, dqu);
+    }
+    return cudaGetLastError();
+}
+
 bool qla_bwd_uses_tc(const Problem& p) {
     return p.in_bf16 && p.d == 128 && p.total_len < (int64_t(1) << 31);
 }

@@ -210,4 +210,18 @@ cudaError_t launch_sm100_qla_finalize_fused(const Problem& p, uint8_t* ws) {
     return cudaGetLastError();
 }
 
+size_t qla_prep_q_bytes(const Problem& p) {
+    const int nblk = (p.S + 127) / 128;
+    const size_t bq = p.q_user_stride ? (size_t)p.B : 1;
+    return bq * p.H * nblk * kOp;
+}
+
+cudaError_t launch_qla_prep_q(const Problem& p, uint8_t* abuf) {
+    const int nblk = (p.S + 127) / 128;
+    const int bq = p.q_user_stride ? p.B : 1;
+    qla_prep_q_kernel<<<bq * p.H * nblk * 4, 256, 0, p.stream>>>(reinterpret_cast<const __nv_bfloat16*>(p.q),
+                                                                 p.q_user_stride, p.S, p.H, p.phi1, abuf);
+    return cudaGetLastError();
+}
+
 }  // namespace vista

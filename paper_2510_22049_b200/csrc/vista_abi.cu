@@ -421,7 +421,7 @@ vista_status_t vista_summarize_partial_prefix(const vista_desc_t* desc, const vo
 // Workspace: [forward sub-run | Z | dZ | dZ bf16 operands (tcgen05 path) | per-user dQ (shared seeds)].
 namespace {
 struct BwdPlan {
-    size_t sub_off, z_off, dz_off, dzop_off, dqu_off, total;
+    size_t sub_off, z_off, dz_off, dzop_off, abuf_off, dqu_off, total;
 };
 BwdPlan plan_bwd(const Problem& p) {
     BwdPlan b{};
@@ -435,6 +435,8 @@ BwdPlan plan_bwd(const Problem& p) {
     off = align256(off + B * H * d * d * sizeof(float));
     b.dzop_off = off;
     if (qla_bwd_uses_tc(p)) off = align256(off + B * H * d * d * 2);
+    b.abuf_off = off;
+    if (qla_bwd_uses_tc(p) && p.S % 128 == 0) off = align256(off + qla_prep_q_bytes(p));
     b.dqu_off = off;
     if (p.q_user_stride == 0) off = align256(off + B * S * H * d * sizeof(float));
     b.total = off;
@@ -492,9 +494,18 @@ vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, cons
     g_ev_start = ev_a;
     g_ev_stop = ev_b;
     if (st != VISTA_OK) return st;
-    // 2. per unit: dW, dZ, dA -> dQ_u
-    cudaError_t e = launch_qla_bwd_unit(p, desc->out_dtype == VISTA_BF16, dout, z, dz, dz_op, dqu);
+    // 2. per unit: dW, dZ, dA -> dQ_u (tensor cores when bf16, d = 128, S % 128 == 0)
+    cudaError_t e;
     int nl = 1;
+    if (tc && p.S % 128 == 0) {
+        uint8_t* abuf = reinterpret_cast<uint8_t*>(ws + b.abuf_off);
+        e = launch_qla_prep_q(p, abuf);
+        if (e == cudaSuccess)
+            e = launch_sm100_qla_bwd_unit(p, desc->out_dtype == VISTA_BF16, dout, z, abuf, dz_op, dqu);
+        ++nl;
+    } else {
+        e = launch_qla_bwd_unit(p, desc->out_dtype == VISTA_BF16, dout, z, dz, dz_op, dqu);
+    }
     // 3. shared seeds: dQ = sum_u dQ_u
     if (e == cudaSuccess && p.q_user_stride == 0) {
         e = launch_qla_bwd_dq_sum(p, dqu, dq);

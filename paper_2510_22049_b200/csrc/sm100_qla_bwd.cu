@@ -32,8 +32,9 @@ constexpr int kStageBytes = 2 * kTile;  // K (-> phi1(K) in place), V
 constexpr int kDzOff = kStages * kStageBytes;
 constexpr int kBarOff = kDzOff + kTile;
 constexpr int kSmem = kBarOff + 256 + 1024;
-constexpr int kThreads = 384;
-constexpr int kXform = 256;  // threads of warps 4..11
+constexpr int kThreads = 512;
+constexpr int kXform = 128;  // transform threads (warps 4..7)
+constexpr int kEpi = 256;    // epilogue threads (warps 8..15)
 
 struct Bars {
     uint64_t kv_full[kStages], k_ready[kStages], kv_empty[kStages];
@@ -88,7 +89,7 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
 template <int PHI>
 __device__ __forceinline__ void xform_tile(uint32_t kbuf, int xt) {
 #pragma unroll 4
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < (2 * kTile / 16) / kXform / 2; ++i) {
         const uint32_t off = (uint32_t)(xt + i * kXform) * 16;
         const uint4 raw = lds128(kbuf + off);
         const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&bars->acc_full[b], 1);
-            ptx::mbar_init(&bars->acc_empty[b], kXform);
+            ptx::mbar_init(&bars->acc_empty[b], kEpi);
         }
         ptx::mbar_init(&bars->dz_full, 1);
         ptx::mbar_init(&bars->dz_empty, 1);
@@ -223,22 +224,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mma_commit_w(&bars->dz_empty);  // dZ free once this unit's GEMMs complete
             ++k;
         }
-    } else if (warp >= 4) {
-        // ============================ transform + epilogue ============================
+    } else if (warp >= 4 && warp < 8) {
+        // ============================ transform ============================
         const int xt = threadIdx.x - 128;
-        const int wq = warp % 4;
-        const int chalf = (warp - 4) / 4;  // epilogue columns [64 chalf, 64 chalf + 64)
-        const int row = wq * 32 + lane;    // item row within the tile = TMEM lane
-        const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
         int stage = 0;
         uint32_t phase = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->kv_full[stage], phase);
+                xform_tile<PHI1>(base + stage * kStageBytes, xt);
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(&bars->k_ready[stage]);
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp >= 8) {
+        // ============================ epilogue ============================
+        const int wq = warp % 4;
+        const int chalf = (warp - 8) / 4;  // columns [64 chalf, 64 chalf + 64)
+        const int row = wq * 32 + lane;    // item row within the tile = TMEM lane
+        const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
         int ab = 0;
         uint32_t aph[2] = {0, 0};
-        // epilogue of the previous tile is deferred by one tile (after the next transform)
-        bool pend = false;
-        int p_stage = 0, p_ab = 0;
-        int64_t p_row0 = 0;
-        int p_valid = 0, p_h = 0;
         // Coalesced row stores (see sm100_softmax.cu store_rows_coalesced): the 32 packed words of a
         // thread's 64-column row segment go back into the (already read) accumulator columns at
         // tcol in a permuted order and come out with the 16x256b shape, a quad of threads then
@@ -325,23 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
             const int64_t row0 = P.offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
-                ptx::mbar_wait(&bars->kv_full[stage], phase);
-                xform_tile<PHI1>(base + stage * kStageBytes, xt);
-                ptx::fence_proxy_async_smem();
-                ptx::mbar_arrive(&bars->k_ready[stage]);
-                if (pend) epilogue(p_stage, p_ab, p_row0, p_valid, p_h);
-                pend = true;
-                p_stage = stage;
-                p_ab = ab;
-                p_row0 = row0 + (int64_t)t * 128;
                 const int64_t rem = L - (int64_t)t * 128;
-                p_valid = rem < 128 ? (int)rem : 128;
-                p_h = it.hg;
+                epilogue(0, ab, row0 + (int64_t)t * 128, rem < 128 ? (int)rem : 128, it.hg);
                 ab ^= 1;
-                if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
         }
-        if (pend) epilogue(p_stage, p_ab, p_row0, p_valid, p_h);
     }
     ptx::tc_fence_before();
     __syncthreads();

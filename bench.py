@@ -383,7 +383,7 @@ def run_own(args, rank, world, local_rank):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_sample(config, attn, seconds, rows=None):
+def oracle_sample(config, attn, seconds, rows=None, backward=False):
     """Time the float64 oracle on whole users (all rows, all heads) of the rank-0 batch until
     ~`seconds` of CPU work; returns (items/s, cores, sample description, equivalent items, s)."""
     import numpy as np
@@ -402,7 +402,10 @@ def oracle_sample(config, attn, seconds, rows=None):
         rr = np.arange(a, b, dtype=np.int64)
         k, v = synth.make_kv(rr, np.full(b - a, u), H, d, seed=0)
         t0 = time.perf_counter()
-        if attn == "softmax":
+        if backward:  # QLA backward (NEXT-2), dout grid values
+            g = (np.random.default_rng(u).integers(-128, 128, size=(1, S, H, d)) / 64.0).astype(np.float32)
+            oracle.qla_backward(q, k, v, [0, b - a], g, threads=cores)
+        elif attn == "softmax":
             oracle.softmax_summarize(q, k, v, [0, b - a], rows=rsel, threads=cores)
         else:
             oracle.qla_summarize(q, k, v, [0, b - a], threads=cores)
@@ -413,6 +416,8 @@ def oracle_sample(config, attn, seconds, rows=None):
             break
     rdesc = "all S rows" if rows is None else f"{rows} of {S} rows (items counted x {rows}/{S})"
     sample = f"{users} whole user(s) of {config} ({rdesc}, all {H} heads, full histories), float64 C oracle, OpenMP"
+    if backward:
+        sample += ", QLA backward (oracle.qla_backward)"
     return done_items / done_t, cores, sample, done_items, done_t
 
 
@@ -500,7 +505,8 @@ def main():
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_own(args, rank, world, local_rank)
     if res is not None and world == 1 and not args.no_cpu_baseline:
-        v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds, rows=None)
+        v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds, rows=None,
+                                               backward=args.backward)
         res["cpu_baseline"] = {"value": v, "unit": "items/s", "cores": cores, "kind": "oracle",
                                "sample": sample, "seconds": round(t, 2)}
     elif res is not None:

@@ -274,11 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         };
         auto epilogue = [&](int est, int eab, int64_t grow0, int valid, int h) {
-            ptx::mbar_wait(&bars->acc_full[eab], aph[eab]);
-            aph[eab] ^= 1;
-            ptx::tc_fence_after();
-            const size_t gcol = ((size_t)grow0 * P.H + h) * 128 + chalf * 64;  // row 0 of the tile
-            // raw k of this thread's row, columns [64 chalf, +64): 8 x 16 B through L2 (issued first)
+            // raw k of this thread's row, columns [64 chalf, +64): 8 x 16 B through L2 (issued before the wait for the GEMMs)
             uint4 kraw[8];
             {
                 const int rr = row < valid ? row : 0;
@@ -287,6 +283,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 8; ++q) kraw[q] = __ldg(src + q);
             }
+            ptx::mbar_wait(&bars->acc_full[eab], aph[eab]);
+            aph[eab] ^= 1;
+            ptx::tc_fence_after();
+            const size_t gcol = ((size_t)grow0 * P.H + h) * 128 + chalf * 64;  // row 0 of the tile
             const uint32_t tv = tmem + lane_bits + eab * 256 + chalf * 64;
             const uint32_t tk = tv + 128;
             {  // dV

@@ -5,11 +5,12 @@
 // ([N = c1][K = c2]) for dK'.  HBM-bound: per item-head 512 B of K+V read, 512 B of dK+dV written
 // (bf16), 4 d^2 = 65,536 flop.
 //
-//   warp 0        TMA producer: K, V tiles (2 stages); dZ of the unit (bulk copy) on unit change
-//   warp 1        MMA issuer (warp-wide, one elected lane)
-//   warps 4..11   transform (phi1(K) -> its own buffer, phi1'(K) in place of K; bf16) and the
-//                 epilogue (TMEM -> bf16 rows of dV and dK . phi1'(K)); dK/dV double-buffered
-//                 in TMEM so the epilogue of tile t overlaps the GEMMs of tile t+1.
+//   warp 0        TMA producer: K, V tiles (3 stages, freed by the MMA commit); dZ of the unit
+//                 (bulk copy) on unit change
+//   warp 1        MMA issuer (warp-wide, one elected lane); dV / dK' double-buffered in TMEM
+//   warps 4..7    transform: phi1(K) in place (bf16)
+//   warps 8..15   epilogue: TMEM -> bf16 rows of dV and of dK' . phi1'(K) (phi1' recomputed from
+//                 the raw K rows re-read through L2), coalesced through a TMEM round trip
 // Tiles are independent (no split partials): a CTA walks its stream-K range (work.cuh).
 #include <cuda.h>
 #include <cuda_bf16.h>

@@ -56,6 +56,7 @@ def _load():
         lib.vo_act.restype = f64
         lib.vo_act_prime.argtypes = [i32, f64]
         lib.vo_act_prime.restype = f64
+        lib.vo_softmax_backward.argtypes = [i64, i64, i64, i64, P, i64, P, P, P, f64, P, P, P, P, i32]
         lib.vo_qla_backward.argtypes = [i64, i64, i64, i64, P, i64, P, P, P, P, i32, i32, i32, P, P, P, i32]
         lib.vo_num_threads.restype = i32
         _lib = lib
@@ -211,6 +212,30 @@ def qla_backward(q, k, v, offsets, dout, phi1="silu", phi2="silu", normalize=Tru
     if (sum_users if sum_users is not None else not q_per_user):
         dq = dq.sum(axis=0)
     return dq, dk, dv
+
+
+def softmax_backward(q, k, v, offsets, dout, scale=None, q_per_user=False, threads=0, sum_users=None):
+    """Softmax backward (NEXT-2; vo_softmax_backward).  dout [B,S,H,d].  Returns dq (summed over
+    users for shared seeds unless sum_users=False; else [B,S,H,d]), dk, dv [sumL,H,d], float64."""
+    q, k, v, dout = _f32(q), _f32(k), _f32(v), _f32(dout)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    B = len(offsets) - 1
+    S, H, d = q.shape[-3:]
+    T = k.shape[0]
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    dq = np.empty((B, S, H, d), np.float64)
+    dk = np.empty((max(T, 1), H, d), np.float64)
+    dv = np.empty((max(T, 1), H, d), np.float64)
+    kk, vv = (k, v) if T > 0 else (np.zeros((1, H, d), np.float32),) * 2
+    stride = S * H * d if q_per_user else 0
+    rc = _load().vo_softmax_backward(B, S, H, d, _ptr(q), stride, _ptr(kk), _ptr(vv), _ptr(offsets), float(scale),
+                                     _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), int(threads))
+    if rc != 0:
+        raise ValueError("vo_softmax_backward failed")
+    if (sum_users if sum_users is not None else not q_per_user):
+        dq = dq.sum(axis=0)
+    return dq, dk[:T], dv[:T]
 
 
 def merge_lse(part_o, part_lse):

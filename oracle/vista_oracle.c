@@ -303,6 +303,82 @@ int vo_qla_backward(int64_t B, int64_t S, int64_t H, int64_t d, const float* q, 
 }
 
 /*
+ * Softmax backward (NEXT-2; "FA-style dQ/dK/dV for the S-query softmax"), the plain
+ * gradient of o_i = sum_j p_ij v_j, p_ij = softmax_j(s_ij), s_ij = scale q_i . k_j
+ * (PAPER.md:158-163), per user u, head h:
+ *   P = softmax rows;  dV_j = sum_i p_ij dO_i;  dP_ij = dO_i . v_j;  D_i = sum_j p_ij dP_ij
+ *   dS_ij = p_ij (dP_ij - D_i);  dQ_i = scale sum_j dS_ij k_j;  dK_j = scale sum_i dS_ij q_i.
+ * Two passes per row (max, then exp), sequential sums, float64.  dq [B,S,H,d] per user.
+ */
+int vo_softmax_backward(int64_t B, int64_t S, int64_t H, int64_t d, const float* q, int64_t q_user_stride,
+                        const float* k, const float* v, const int64_t* offsets, double scale, const float* dout,
+                        double* dq, double* dk, double* dv, int threads) {
+    if (B < 0 || S < 1 || H < 1 || d < 1) return -1;
+    set_threads(threads);
+    int64_t total = offsets[B];
+    for (int64_t e = 0; e < total * H * d; ++e) {
+        dk[e] = 0.0;
+        dv[e] = 0.0;
+    }
+    /* parallel over (u, h): each owns disjoint dk/dv rows and dq entries */
+#pragma omp parallel
+    {
+        int64_t maxL = 0;
+        for (int64_t u = 0; u < B; ++u) maxL = offsets[u + 1] - offsets[u] > maxL ? offsets[u + 1] - offsets[u] : maxL;
+        double* p = (double*)malloc((size_t)(maxL > 0 ? maxL : 1) * sizeof(double));
+        double* dp = (double*)malloc((size_t)(maxL > 0 ? maxL : 1) * sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < B * H; ++t) {
+            const int64_t u = t / H, h = t % H;
+            const int64_t j0 = offsets[u], L = offsets[u + 1] - offsets[u];
+            for (int64_t i = 0; i < S; ++i) {
+                const float* qi = q + u * q_user_stride + (i * H + h) * d;
+                const float* go = dout + ((u * S + i) * H + h) * d;
+                double* gq = dq + ((u * S + i) * H + h) * d;
+                for (int64_t c = 0; c < d; ++c) gq[c] = 0.0;
+                if (L == 0) continue;
+                double m = -INFINITY;
+                for (int64_t j = 0; j < L; ++j) {
+                    const float* kj = k + ((j0 + j) * H + h) * d;
+                    double s = 0.0;
+                    for (int64_t c = 0; c < d; ++c) s += (double)qi[c] * (double)kj[c];
+                    p[j] = scale * s;
+                    if (p[j] > m) m = p[j];
+                }
+                double l = 0.0;
+                for (int64_t j = 0; j < L; ++j) {
+                    p[j] = exp(p[j] - m);
+                    l += p[j];
+                }
+                double D = 0.0;
+                for (int64_t j = 0; j < L; ++j) {
+                    p[j] /= l;
+                    const float* vj = v + ((j0 + j) * H + h) * d;
+                    double s = 0.0;
+                    for (int64_t c = 0; c < d; ++c) s += (double)go[c] * (double)vj[c];
+                    dp[j] = s;
+                    D += p[j] * s;
+                }
+                for (int64_t j = 0; j < L; ++j) {
+                    const float* kj = k + ((j0 + j) * H + h) * d;
+                    double* gk = dk + ((j0 + j) * H + h) * d;
+                    double* gv = dv + ((j0 + j) * H + h) * d;
+                    const double ds = p[j] * (dp[j] - D);
+                    for (int64_t c = 0; c < d; ++c) {
+                        gv[c] += p[j] * (double)go[c];
+                        gk[c] += scale * ds * (double)qi[c];
+                        gq[c] += scale * ds * (double)kj[c];
+                    }
+                }
+            }
+        }
+        free(p);
+        free(dp);
+    }
+    return 0;
+}
+
+/*
  * LSE merge of P softmax partials over disjoint key sets, for n rows of width d
  * (flash-decoding style combination; the exact identity
  *   softmax over A u B = e^{lse_A - lse} O_A + e^{lse_B - lse} O_B,  lse = ln(e^{lse_A}+e^{lse_B})).

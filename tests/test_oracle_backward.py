@@ -150,3 +150,71 @@ def test_b4_user_independence():
     _, dk1, dv1 = oracle.qla_backward(q, k[4:], v[4:], [0, 3], g[1:], "silu", "silu", True)
     np.testing.assert_array_equal(dk[4:], dk1)
     np.testing.assert_array_equal(dv[4:], dv1)
+
+
+# ----------------------------------------------------------------------------- softmax backward
+def _torch_softmax_grads(q, k, v, off, g, scale, q_per_user):
+    qt = torch.tensor(q, dtype=torch.float64, requires_grad=True)
+    kt = torch.tensor(k, dtype=torch.float64, requires_grad=True)
+    vt = torch.tensor(v, dtype=torch.float64, requires_grad=True)
+    gt = torch.tensor(g, dtype=torch.float64)
+    loss = 0.0
+    for u in range(len(off) - 1):
+        a, b = int(off[u]), int(off[u + 1])
+        if b == a:
+            continue
+        qu = qt[u] if q_per_user else qt
+        for h in range(k.shape[1]):
+            att = torch.softmax(scale * qu[:, h] @ kt[a:b, h].T, dim=-1)
+            loss = loss + ((att @ vt[a:b, h]) * gt[u, :, h]).sum()
+    loss.backward()
+    z = lambda t: t.grad.numpy() if t.grad is not None else np.zeros(t.shape)
+    return z(qt), z(kt), z(vt)
+
+
+@pytest.mark.parametrize("q_per_user", [False, True])
+def test_b1_softmax_backward_vs_torch_autograd(q_per_user):
+    q, k, v, off, g = _case(31, [6, 0, 3, 1], q_per_user=q_per_user)
+    dq, dk, dv = oracle.softmax_backward(q, k, v, off, g, scale=0.7, q_per_user=q_per_user)
+    tq, tk, tv = _torch_softmax_grads(q, k, v, off, g, 0.7, q_per_user)
+    np.testing.assert_allclose(dq, tq, rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(dk, tk, rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(dv, tv, rtol=1e-11, atol=1e-12)
+
+
+def test_b2_softmax_backward_vs_finite_differences():
+    q, k, v, off, g = _case(32, [3, 2], S=2, H=1, d=3)
+    dq, dk, dv = oracle.softmax_backward(q, k, v, off, g, scale=0.5)
+    args = [q.astype(np.float64), k.astype(np.float64), v.astype(np.float64)]
+
+    def loss(qq, kk, vv):
+        tot = 0.0
+        for u in range(len(off) - 1):
+            a, b = off[u], off[u + 1]
+            s = 0.5 * qq[:, 0] @ kk[a:b, 0].T
+            p = np.exp(s - s.max(axis=1, keepdims=True))
+            p /= p.sum(axis=1, keepdims=True)
+            tot += np.sum((p @ vv[a:b, 0]) * g[u, :, 0])
+        return tot
+    eps = 1e-6
+    for which, ana in zip(range(3), (dq, dk, dv)):
+        num = np.zeros_like(args[which])
+        it = np.nditer(args[which], flags=["multi_index"])
+        for _ in it:
+            idx = it.multi_index
+            pl = [a.copy() for a in args]
+            mi = [a.copy() for a in args]
+            pl[which][idx] += eps
+            mi[which][idx] -= eps
+            num[idx] = (loss(*pl) - loss(*mi)) / (2 * eps)
+        np.testing.assert_allclose(ana, num, rtol=1e-6, atol=1e-8)
+
+
+def test_b4_softmax_backward_single_key_and_zero():
+    """One key: softmax = 1 so dV = sum_i dO_i, dK = dQ = 0 (dS = p (dP - D) = 0); dO = 0 -> 0."""
+    q, k, v, off, g = _case(33, [1], S=3, H=1, d=4)
+    dq, dk, dv = oracle.softmax_backward(q, k, v, off, g, scale=1.0)
+    np.testing.assert_allclose(dv[0, 0], g[0, :, 0].astype(np.float64).sum(axis=0), rtol=1e-14, atol=1e-14)
+    assert np.all(np.abs(dk) < 1e-15) and np.all(np.abs(dq) < 1e-15)
+    z = oracle.softmax_backward(q, k, v, off, np.zeros_like(g))
+    assert all(np.all(x == 0) for x in z)

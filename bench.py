@@ -179,8 +179,6 @@ def run_own(args, rank, world, local_rank):
                 return [codes, qscale, qzp] + ([lse] if lse is not None else [])
             return [out] + ([lse] if lse is not None else [])
         if args.backward:
-            if attn != vista.QLA:
-                raise SystemExit("--backward: only the QLA backward is implemented (softmax backward is next)")
             gen = torch.Generator(device=dev)
             gen.manual_seed(1234 + rank)
             dout = (torch.randint(-128, 128, (B, S, H, d), device=dev, generator=gen).float() / 64).to(torch.bfloat16)
@@ -191,9 +189,14 @@ def run_own(args, rank, world, local_rank):
             bws = torch.empty(max(bws_bytes, 16), dtype=torch.uint8, device=dev)
             inputs = [q, K, V, off_t, dout]
 
+            fwd_out, fwd_lse = (None, None)
+            if attn == vista.SOFTMAX:  # the forward's out / lse (computed once, outside the timed region)
+                vista.vista_summarize_fwd(desc, q, K, V, off_t, total, out, lse, ws, ws_bytes, sh)
+                fwd_out, fwd_lse = out.clone(), lse.clone()
+
             def step(ins=inputs):
-                vista.vista_summarize_bwd(desc, ins[0], ins[1], ins[2], ins[3], total, None, None, ins[4], dq, dk,
-                                          dv, bws, bws_bytes, sh)
+                vista.vista_summarize_bwd(desc, ins[0], ins[1], ins[2], ins[3], total, fwd_out, fwd_lse, ins[4], dq,
+                                          dk, dv, bws, bws_bytes, sh)
                 return [dq, dk, dv]
         items_per_step = world * total
         scaling = "weak"
@@ -338,9 +341,12 @@ def run_own(args, rank, world, local_rank):
     flops = 4.0 * S * d * H * total if attn == vista.SOFTMAX else 2.0 * d * d * H * total
     kv_bytes = 4.0 * d * H * total  # bf16 K + V, read once
     io_bytes = kv_bytes + S * H * d * 2 + B * S * H * d * 2 + (B * H * S * 4 if attn == vista.SOFTMAX else 0)
-    if args.backward:  # dK / dV kernel: K, V read, dK, dV written (bf16); dV = phi1(K) dZ and V dZ^T
+    if args.backward and attn == vista.QLA:  # dK / dV kernel: K, V read, dK, dV written (bf16)
         flops = 4.0 * d * d * H * total
         io_bytes = 2 * kv_bytes + B * H * d * d * 2
+    elif args.backward:  # softmax dK / dV kernel: S^T, dP^T, dV, dK GEMMs = 8 S d flop per item-head
+        flops = 8.0 * S * d * H * total
+        io_bytes = 2 * kv_bytes + 2 * B * S * H * d * 2
     tflops = flops / (kern_ms / 1e3) / 1e12
     gbs = io_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
@@ -351,7 +357,8 @@ def run_own(args, rank, world, local_rank):
         roof = {"bound": "tensor", "achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": round(tflops / pk["bf16_tflops"], 4), "traffic": traffic,
                 "peak_kind": f"{pk_kind} bf16 burst (kernel timed alone per launch)",
-                "kernel": "sm100_softmax_kernel", "kernel_ms": round(kern_ms, 5),
+                "kernel": "sm100_softmax_bwd_kv_kernel" if args.backward else "sm100_softmax_kernel",
+                "kernel_ms": round(kern_ms, 5),
                 "algorithmic_flop_per_launch": flops,
                 "hbm": {"achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                         "frac": round(gbs / pk["hbm_gbs"], 4), "algorithmic_bytes_per_launch": io_bytes}}
@@ -402,9 +409,12 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False):
         rr = np.arange(a, b, dtype=np.int64)
         k, v = synth.make_kv(rr, np.full(b - a, u), H, d, seed=0)
         t0 = time.perf_counter()
-        if backward:  # QLA backward (NEXT-2), dout grid values
+        if backward:  # backward (NEXT-2), dout grid values
             g = (np.random.default_rng(u).integers(-128, 128, size=(1, S, H, d)) / 64.0).astype(np.float32)
-            oracle.qla_backward(q, k, v, [0, b - a], g, threads=cores)
+            if attn == "softmax":
+                oracle.softmax_backward(q, k, v, [0, b - a], g, threads=cores)
+            else:
+                oracle.qla_backward(q, k, v, [0, b - a], g, threads=cores)
         elif attn == "softmax":
             oracle.softmax_summarize(q, k, v, [0, b - a], rows=rsel, threads=cores)
         else:
@@ -417,7 +427,7 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False):
     rdesc = "all S rows" if rows is None else f"{rows} of {S} rows (items counted x {rows}/{S})"
     sample = f"{users} whole user(s) of {config} ({rdesc}, all {H} heads, full histories), float64 C oracle, OpenMP"
     if backward:
-        sample += ", QLA backward (oracle.qla_backward)"
+        sample += f", {attn} backward (oracle.{attn}_backward)"
     return done_items / done_t, cores, sample, done_items, done_t
 
 

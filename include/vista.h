@@ -158,15 +158,19 @@ vista_status_t vista_summarize_partial_prefix(const vista_desc_t* desc, const vo
                                               void* stream);
 
 /*
- * Backward (NEXT-2, stage-1 training) -- QLA only in this version (softmax: VISTA_ERR_UNSUPPORTED).
- * Gradients of out = phi1(Q) phi2(Z / N_u), Z = sum_j phi1(k_j)^T v_j (the appendix derives the
+ * Backward (NEXT-2, stage-1 training).
+ * SOFTMAX: gradients of out_i = sum_j softmax_j(scale q_i . k_j) v_j, flash
+ *   style from the forward's out and lse (both required): dV = P^T dO, dK = scale dS^T Q,
+ *   dQ = scale dS K with dS = P . (dO V^T - rowsum(dO . out)).  This version: bf16, d = 128,
+ *   S % 128 == 0, S <= 256, bf16 dout (else VISTA_ERR_UNSUPPORTED).
+ * QLA: gradients of out = phi1(Q) phi2(Z / N_u), Z = sum_j phi1(k_j)^T v_j (the appendix derives the
  * phi2 = identity, no-1/N case; phi2 and 1/N are composed by the
  * chain rule, reading R19):
  *   dW = phi1(Q)^T dO;  dZ = (dW . phi2'(Zbar)) / N_u;  dQ = (dO W^T) . phi1'(Q), W = phi2(Zbar);
  *   dV_j = phi1(k_j) dZ;  dK_j = (v_j dZ^T) . phi1'(k_j).
  *   dout [B,S,H,d] (out_dtype); dq float32: [S,H,d] summed over users (ascending u) for shared
- *   seeds, [B,S,H,d] for per-user Q; dk, dv [total_len,H,d] in in_dtype.  out / lse are unused
- *   for QLA (may be NULL).  Z is recomputed from k, v.  Workspace: at least
+ *   seeds, [B,S,H,d] for per-user Q; dk, dv [total_len,H,d] in in_dtype.  out / lse: the
+ *   forward's outputs (softmax); unused for QLA (may be NULL; Z is recomputed).  Workspace: at least
  *   vista_summarize_bwd_workspace_size bytes.  Asynchronous on stream; deterministic.
  */
 vista_status_t vista_summarize_bwd_workspace_size(const vista_desc_t* desc, int64_t total_len,

@@ -349,8 +349,8 @@ def summarize_partial(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=N
 
 def summarize_bwd(q, k, v, offsets, total_len, dout, *, attn=QLA, phi1="silu", phi2="silu", normalize=True,
                   out=None, lse=None, workspace=None, stream=None):
-    """Backward of summarize (NEXT-2; QLA): returns (dq, dk, dv).  dq float32 [S,H,d] (shared seeds,
-    summed over users) or [B,S,H,d]; dk, dv like k, v."""
+    """Backward of summarize (NEXT-2): returns (dq, dk, dv).  dq float32 [S,H,d] (shared seeds,
+    summed over users) or [B,S,H,d]; dk, dv like k, v.  Softmax needs the forward's out and lse."""
     import torch
     if total_len is None:
         total_len = k.shape[0]

@@ -108,6 +108,11 @@ cudaError_t launch_qla_bwd_kv_simt(const Problem& p, const float* dz, void* dk, 
 cudaError_t launch_sm100_qla_bwd_kv(const Problem& p, const Workspace& w, char* ws, const uint8_t* dz_op, void* dk,
                                     void* dv);
 bool qla_bwd_uses_tc(const Problem& p);
+// softmax backward (NEXT-2): bf16, d = 128, S % 128 == 0, S <= 256, bf16 dout
+bool softmax_bwd_supported(const Problem& p, bool dout_bf16);
+size_t softmax_bwd_workspace(const Problem& p);
+cudaError_t launch_softmax_bwd(const Problem& p, const void* out, const float* lse, const void* dout, float* dq,
+                               void* dk, void* dv, char* ws, int* nlaunch, cudaEvent_t ev_a, cudaEvent_t ev_b);
 // phi1(Q) as bf16 128-row MMA operand blocks (qla_prep_q_kernel); qla_prep_q_bytes of space
 size_t qla_prep_q_bytes(const Problem& p);
 cudaError_t launch_qla_prep_q(const Problem& p, uint8_t* abuf);

@@ -1,0 +1,732 @@
+// sm100_softmax_bwd.cu -- softmax backward on B200 (NEXT-2, stage-1 training): the gradients of
+// o_i = sum_j p_ij v_j, p_ij = softmax_j(scale q_i . k_j) over each user's
+// history, flash-attention style (P recomputed from the forward's lse, never stored):
+//   P = exp(scale Q K^T - lse);  dP = dO V^T;  D_i = sum_c dO_ic O_ic;  dS = P . (dP - D)
+//   dV = P^T dO;   dK = scale dS^T Q;   dQ = scale dS K
+// Two passes, each a persistent TMA + tcgen05 kernel over the flat key tiles (work.cuh):
+//
+//   sm100_softmax_bwd_kv_kernel  (dK, dV; one work unit = (user, head), all S <= 256 seed rows
+//     resident in shared memory).  The key-major products are computed transposed so that the
+//     tensor core's M dimension is the 128 keys of a tile and every operand fits the TMEM / SMEM
+//     forms:  S^T = K Q_g^T,  dP^T = V dO_g^T  (SS);  P^T, dS^T go to TMEM as bf16 over S^T, dP^T
+//     and feed  dV += P^T dO_g,  dK += dS^T Q_g  as TS MMAs (A from TMEM), g over the 128-row
+//     query blocks.  The softmax is column-wise here (lse_i, D_i per query column; no reduction).
+//   sm100_softmax_bwd_dq_kernel  (dQ; one unit = (user, head, 128-row query block), like the
+//     forward with one Q tile):  S = Q_g K^T, dP = dO_g V^T (SS) -> dS (bf16 over S in TMEM) ->
+//     dQ += dS K (TS, K tile as the MN-major B operand).  Split units (stream-K) write partial
+//     slots, summed by the QLA slot merge into the [B, H, S, d] dQ buffer.
+//
+// TMEM (both): columns [0,128) S / S^T (bf16 P^T or dS over its first 64), [128,256) dP / dP^T
+// (bf16 dS^T over its first 64), then dV, dK (pass 1) or dQ (pass 2).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "internal.h"
+#include "qla_common.cuh"
+#include "sm100_ptx.cuh"
+#include "work.cuh"
+
+namespace vista {
+
+bool make_kv_map(CUtensorMap* map, const void* base, int64_t total_len, int H);
+bool make_q_map(CUtensorMap* map, const void* base, int S, int H, int B, int64_t q_user_stride);
+
+namespace {
+
+constexpr int kHalf = 128 * 128;
+constexpr int kTileB = 2 * kHalf;  // 32 KB: 128 rows x 128 bf16
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
+// Coalesced bf16 row store of 32 packed words (64 columns of this thread's TMEM lane row), through
+// a TMEM round trip at tcol (already read; see sm100_softmax.cu store_rows_coalesced).  Rows >= valid
+// are not stored.  gbase: element (row 0, first column); row stride in elements.
+__device__ __forceinline__ void store32_rows(uint32_t tcol, const uint32_t (&w)[32], __nv_bfloat16* gbase,
+                                             size_t row_stride, int valid, int wq, int lane) {
+    uint32_t a[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+        const int g = c >> 3, p = (c & 7) >> 1, e = c & 1;
+        a[c] = w[8 * p + 2 * g + e];
+    }
+    ptx::tmem_st32(tcol, a);
+    ptx::tmem_wait_st();
+    const int p = lane & 3;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        uint32_t r[16];
+        ptx::tmem_ld16x256b_x4(tcol + ((uint32_t)(16 * half) << 16), r);
+        ptx::tmem_wait_ld();
+        ptx::reg_fence(r);
+        const int ra = wq * 32 + 16 * half + (lane >> 2);
+        const uint32_t v0[8] = {r[0], r[1], r[4], r[5], r[8], r[9], r[12], r[13]};
+        const uint32_t v1[8] = {r[2], r[3], r[6], r[7], r[10], r[11], r[14], r[15]};
+        if (ra < valid) st_v8(gbase + (size_t)ra * row_stride + 16 * p, v0);
+        if (ra + 8 < valid) st_v8(gbase + (size_t)(ra + 8) * row_stride + 16 * p, v1);
+    }
+}
+
+// ============================================================================ pass 1: dK, dV
+namespace kv {
+constexpr int kMaxS = 256;
+constexpr int kQOff = 0;                            // Q: S/128 blocks of 32 KB
+constexpr int kGOff = kQOff + (kMaxS / 128) * kTileB;  // dO
+constexpr int kKOff = kGOff + (kMaxS / 128) * kTileB;  // K ring, 2 stages
+constexpr int kVOff = kKOff + 2 * kTileB;            // V, 1 stage
+constexpr int kBarOff = kVOff + kTileB;
+constexpr int kSmem = kBarOff + 256 + 1024;
+constexpr int kThreads = 384;
+
+struct Bars {
+    uint64_t q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty;
+    uint64_t sd_full, pds_ready, acc_full, acc_empty;
+    uint32_t tmem_base;
+};
+
+struct Params {
+    const int64_t* offsets;
+    const int64_t* uts;
+    const float* lse;  // [B, H, S] natural log
+    const float* dd;   // D [B, H, S]
+    __nv_bfloat16* dk;
+    __nv_bfloat16* dv;
+    int B, S, H;
+    float scale_log2, scale;
+    int q_per_user;
+};
+
+// S^T_g = K Q_g^T -> cols [0,128);  dP^T_g = V dO_g^T -> cols [128,256)   (all operands K-major)
+template <int KS>
+__device__ __forceinline__ void issue_sd(uint32_t tmem, uint32_t base, int g) {
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 0);
+    const uint32_t ka = base + kKOff + KS * kTileB, va = base + kVOff;
+    const uint32_t qa = base + kQOff + g * kTileB, ga = base + kGOff + g * kTileB;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+        ptx::mma_ss_w(tmem, ptx::sdesc_sw128(ka + off, 16, 1024), ptx::sdesc_sw128(qa + off, 16, 1024), id, kk > 0);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+        ptx::mma_ss_w(tmem + 128, ptx::sdesc_sw128(va + off, 16, 1024), ptx::sdesc_sw128(ga + off, 16, 1024), id,
+                      kk > 0);
+    }
+}
+// dV += P^T_g dO_g -> cols [256,384);  dK += dS^T_g Q_g -> cols [384,512)   (A from TMEM, B MN-major)
+__device__ __forceinline__ void issue_vk(uint32_t tmem, uint32_t base, int g) {
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);
+    const uint32_t qa = base + kQOff + g * kTileB, ga = base + kGOff + g * kTileB;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+        ptx::mma_ts_w(tmem + 256, tmem + kk * 8, ptx::sdesc_sw128(ga + kk * 2048, kHalf, 1024), id,
+                      (g > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+        ptx::mma_ts_w(tmem + 384, tmem + 128 + kk * 8, ptx::sdesc_sw128(qa + kk * 2048, kHalf, 1024), id,
+                      (g > 0 || kk > 0) ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    sm100_softmax_bwd_kv_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapG,
+                                const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+                                const Params P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t base = ptx::smem_u32(smem);
+    Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int cta = blockIdx.x, num_ctas = gridDim.x;
+    const int HG = P.H, G = P.S / 128;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bars->q_full, 1);
+        ptx::mbar_init(&bars->q_empty, 1);
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&bars->k_full[s], 1);
+            ptx::mbar_init(&bars->k_empty[s], 1);
+        }
+        ptx::mbar_init(&bars->v_full, 1);
+        ptx::mbar_init(&bars->v_empty, 1);
+        ptx::mbar_init(&bars->sd_full, 1);
+        ptx::mbar_init(&bars->pds_ready, 128);
+        ptx::mbar_init(&bars->acc_full, 1);
+        ptx::mbar_init(&bars->acc_empty, 128);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
+    ItemIter iter;
+    iter.init(P.uts, P.B, HG, cta, num_ctas);
+    Item it;
+    if (warp == 0) {
+        // ---------------- TMA producer: Q, dO of the unit; K (2 stages), V (1 stage) per tile
+        ptx::tma_prefetch(&mapQ);
+        ptx::tma_prefetch(&mapG);
+        ptx::tma_prefetch(&mapK);
+        ptx::tma_prefetch(&mapV);
+        const uint64_t pol = ptx::policy_evict_first(), pol_q = ptx::policy_evict_last();
+        int ks = 0;
+        uint32_t kph = 0, vph = 0;
+        int k = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            const int h = it.hg;
+            if (k > 0) ptx::mbar_wait(&bars->q_empty, (k - 1) & 1);
+            ptx::mbar_arrive_expect_tx_w(&bars->q_full, 2 * G * kTileB);
+            for (int g = 0; g < G; ++g)
+                for (int half = 0; half < 2; ++half) {
+                    ptx::tma_load_4d_w(smem + kQOff + g * kTileB + half * kHalf, &mapQ, &bars->q_full, half * 64, h,
+                                       g * 128, P.q_per_user ? it.u : 0, pol_q);
+                    ptx::tma_load_4d_w(smem + kGOff + g * kTileB + half * kHalf, &mapG, &bars->q_full, half * 64, h,
+                                       g * 128, it.u, pol);
+                }
+            const int64_t row0 = P.offsets[it.u];
+            for (int t = it.t0; t < it.t1; ++t) {
+                const int32_t row = (int32_t)(row0 + (int64_t)t * 128);
+                ptx::mbar_wait(&bars->k_empty[ks], kph ^ 1);
+                ptx::mbar_arrive_expect_tx_w(&bars->k_full[ks], kTileB);
+                for (int half = 0; half < 2; ++half)
+                    ptx::tma_load_3d_w(smem + kKOff + ks * kTileB + half * kHalf, &mapK, &bars->k_full[ks], half * 64,
+                                       h, row, pol);
+                if (++ks == 2) { ks = 0; kph ^= 1; }
+                ptx::mbar_wait(&bars->v_empty, vph ^ 1);
+                vph ^= 1;
+                ptx::mbar_arrive_expect_tx_w(&bars->v_full, kTileB);
+                for (int half = 0; half < 2; ++half)
+                    ptx::tma_load_3d_w(smem + kVOff + half * kHalf, &mapV, &bars->v_full, half * 64, h, row, pol);
+            }
+            ++k;
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        int ks = 0;
+        uint32_t kph = 0, vph = 0, pph = 0, aph = 0;
+        int k = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            ptx::mbar_wait(&bars->q_full, k & 1);
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->k_full[ks], kph);
+                ptx::mbar_wait(&bars->v_full, vph);
+                vph ^= 1;
+                ptx::mbar_wait(&bars->acc_empty, aph ^ 1);  // the epilogue has drained dV, dK of the last tile
+                aph ^= 1;
+                ptx::tc_fence_after();
+                for (int g = 0; g < G; ++g) {
+                    if (ks == 0) issue_sd<0>(tmem, base, g); else issue_sd<1>(tmem, base, g);
+                    ptx::mma_commit_w(&bars->sd_full);
+                    if (g == G - 1) {
+                        ptx::mma_commit_w(&bars->k_empty[ks]);  // K only feeds S^T
+                        ptx::mma_commit_w(&bars->v_empty);      // V only feeds dP^T
+                    }
+                    ptx::mbar_wait(&bars->pds_ready, pph);
+                    pph ^= 1;
+                    ptx::tc_fence_after();
+                    issue_vk(tmem, base, g);
+                }
+                ptx::mma_commit_w(&bars->acc_full);
+                if (++ks == 2) { ks = 0; kph ^= 1; }
+            }
+            ptx::mma_commit_w(&bars->q_empty);  // Q, dO free once this unit's GEMMs complete
+            ++k;
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------- column softmax: P^T = exp2(S^T scale log2e - lse_i log2e), dS^T = P^T (dP^T - D_i)
+        const int wq = warp % 4;
+        const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
+        uint32_t sph = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            const size_t lrow = ((size_t)it.u * P.H + it.hg) * P.S;
+            for (int t = it.t0; t < it.t1; ++t) {
+                for (int g = 0; g < G; ++g) {
+                    ptx::mbar_wait(&bars->sd_full, sph);
+                    sph ^= 1;
+                    ptx::tc_fence_after();
+#pragma unroll 1
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t sr[32], dr[32];
+                        ptx::tmem_ld32(tmem + lane_bits + c * 32, sr);
+                        ptx::tmem_ld32(tmem + lane_bits + 128 + c * 32, dr);
+                        const float4* lq = reinterpret_cast<const float4*>(P.lse + lrow + g * 128 + c * 32);
+                        const float4* dq = reinterpret_cast<const float4*>(P.dd + lrow + g * 128 + c * 32);
+                        float ls[32], dl[32];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const float4 a = __ldg(lq + e), b = __ldg(dq + e);
+                            ls[4 * e] = a.x * kLog2e;
+                            ls[4 * e + 1] = a.y * kLog2e;
+                            ls[4 * e + 2] = a.z * kLog2e;
+                            ls[4 * e + 3] = a.w * kLog2e;
+                            dl[4 * e] = b.x;
+                            dl[4 * e + 1] = b.y;
+                            dl[4 * e + 2] = b.z;
+                            dl[4 * e + 3] = b.w;
+                        }
+                        ptx::tmem_wait_ld();
+                        ptx::reg_fence(sr);
+                        ptx::reg_fence(dr);
+                        uint32_t pw[16], sw[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[2 * j]), P.scale_log2, -ls[2 * j]));
+                            const float p1 =
+                                ptx::ex2(fmaf(__uint_as_float(sr[2 * j + 1]), P.scale_log2, -ls[2 * j + 1]));
+                            pw[j] = ptx::pack_bf16x2(p0, p1);
+                            sw[j] = ptx::pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - dl[2 * j]),
+                                                     p1 * (__uint_as_float(dr[2 * j + 1]) - dl[2 * j + 1]));
+                        }
+                        ptx::tmem_st16(tmem + lane_bits + c * 16, pw);
+                        ptx::tmem_st16(tmem + lane_bits + 128 + c * 16, sw);
+                    }
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars->pds_ready);
+                }
+            }
+        }
+    } else if (warp >= 8) {
+        // ---------------- epilogue: dV, dK (x scale) rows -> bf16
+        const int wq = warp % 4;
+        const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
+        uint32_t aph = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->acc_full, aph);
+                aph ^= 1;
+                ptx::tc_fence_after();
+                const int64_t rem = L - (int64_t)t * 128;
+                const int valid = rem < 128 ? (int)rem : 128;
+                const size_t g0 = ((size_t)(P.offsets[it.u] + (int64_t)t * 128) * P.H + it.hg) * 128;
+                for (int m = 0; m < 2; ++m) {  // 0: dV, 1: dK
+                    const float sc = m ? P.scale : 1.f;
+                    __nv_bfloat16* dst = (m ? P.dk : P.dv) + g0;
+                    for (int hh = 0; hh < 2; ++hh) {  // 64-column halves
+                        const uint32_t tc = tmem + lane_bits + 256 + m * 128 + hh * 64;
+                        uint32_t w[32];
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            uint32_t r[32];
+                            ptx::tmem_ld32_sync(tc + c * 32, r);
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                w[16 * c + j] = ptx::pack_bf16x2(__uint_as_float(r[2 * j]) * sc,
+                                                                 __uint_as_float(r[2 * j + 1]) * sc);
+                        }
+                        store32_rows(tc, w, dst + hh * 64, (size_t)P.H * 128, valid, wq, lane);
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bars->acc_empty);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+}  // namespace kv
+
+// ============================================================================ pass 2: dQ
+namespace dq {
+constexpr int kQOff = 0, kGOff = kTileB, kKOff = 2 * kTileB, kVOff = kKOff + 2 * kTileB;
+constexpr int kBarOff = kVOff + 2 * kTileB;
+constexpr int kSmem = kBarOff + 256 + 1024;
+constexpr int kThreads = 256;
+
+struct Bars {
+    uint64_t q_full, q_empty, k_full[2], k_empty[2], v_full[2], v_empty[2];
+    uint64_t sd_full, ds_ready, dq_full, dq_empty;
+    uint32_t tmem_base;
+};
+
+struct Params {
+    const int64_t* offsets;
+    const int64_t* uts;
+    int* slot_unit;
+    float* slot_o;   // [2 C][128][128]
+    float* dqbuf;    // [B, H, S, d] (unit-major rows)
+    const float* lse;
+    const float* dd;
+    int B, S, H, G;
+    float scale_log2, scale;
+    int q_per_user;
+};
+
+template <int ST>
+__device__ __forceinline__ void issue_sd(uint32_t tmem, uint32_t base) {
+    // S = Q_g K^T -> [0,128);  dP = dO_g V^T -> [128,256)   (all K-major)
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 0);
+    const uint32_t ka = base + kKOff + ST * kTileB, va = base + kVOff + ST * kTileB;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+        ptx::mma_ss_w(tmem, ptx::sdesc_sw128(base + kQOff + off, 16, 1024), ptx::sdesc_sw128(ka + off, 16, 1024), id,
+                      kk > 0);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+        ptx::mma_ss_w(tmem + 128, ptx::sdesc_sw128(base + kGOff + off, 16, 1024), ptx::sdesc_sw128(va + off, 16, 1024),
+                      id, kk > 0);
+    }
+}
+template <int ST>
+__device__ __forceinline__ void issue_dq(uint32_t tmem, uint32_t base, bool acc) {
+    // dQ += dS K: A = dS (bf16, TMEM [0,64)), B = K tile MN-major [K = key][N = c]
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);
+    const uint32_t ka = base + kKOff + ST * kTileB;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+        ptx::mma_ts_w(tmem + 256, tmem + kk * 8, ptx::sdesc_sw128(ka + kk * 2048, kHalf, 1024), id,
+                      (acc || kk > 0) ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    sm100_softmax_bwd_dq_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapG,
+                                const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+                                const Params P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t base = ptx::smem_u32(smem);
+    Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int cta = blockIdx.x, num_ctas = gridDim.x;
+    const int HG = P.H * P.G;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bars->q_full, 1);
+        ptx::mbar_init(&bars->q_empty, 1);
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&bars->k_full[s], 1);
+            ptx::mbar_init(&bars->k_empty[s], 1);
+            ptx::mbar_init(&bars->v_full[s], 1);
+            ptx::mbar_init(&bars->v_empty[s], 1);
+        }
+        ptx::mbar_init(&bars->sd_full, 1);
+        ptx::mbar_init(&bars->ds_ready, 128);
+        ptx::mbar_init(&bars->dq_full, 1);
+        ptx::mbar_init(&bars->dq_empty, 128);
+        ptx::fence_mbar_init();
+        int s0, s1;
+        partial_slots(P.uts, P.B, HG, cta, num_ctas, s0, s1);
+        P.slot_unit[2 * cta] = s0;
+        P.slot_unit[2 * cta + 1] = s1;
+    }
+    if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
+    ItemIter iter;
+    iter.init(P.uts, P.B, HG, cta, num_ctas);
+    Item it;
+    if (warp == 0) {
+        ptx::tma_prefetch(&mapQ);
+        ptx::tma_prefetch(&mapG);
+        ptx::tma_prefetch(&mapK);
+        ptx::tma_prefetch(&mapV);
+        const uint64_t pol = ptx::policy_evict_first(), pol_q = ptx::policy_evict_last();
+        int st = 0;
+        uint32_t ph = 0;
+        int k = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            const int h = it.hg / P.G, g = it.hg % P.G;
+            if (k > 0) ptx::mbar_wait(&bars->q_empty, (k - 1) & 1);
+            ptx::mbar_arrive_expect_tx_w(&bars->q_full, 2 * kTileB);
+            for (int half = 0; half < 2; ++half) {
+                ptx::tma_load_4d_w(smem + kQOff + half * kHalf, &mapQ, &bars->q_full, half * 64, h, g * 128,
+                                   P.q_per_user ? it.u : 0, pol_q);
+                ptx::tma_load_4d_w(smem + kGOff + half * kHalf, &mapG, &bars->q_full, half * 64, h, g * 128, it.u, pol);
+            }
+            const int64_t row0 = P.offsets[it.u];
+            for (int t = it.t0; t < it.t1; ++t) {
+                const int32_t row = (int32_t)(row0 + (int64_t)t * 128);
+                ptx::mbar_wait(&bars->k_empty[st], ph ^ 1);
+                ptx::mbar_arrive_expect_tx_w(&bars->k_full[st], kTileB);
+                for (int half = 0; half < 2; ++half)
+                    ptx::tma_load_3d_w(smem + kKOff + st * kTileB + half * kHalf, &mapK, &bars->k_full[st], half * 64, h,
+                                       row, pol);
+                ptx::mbar_wait(&bars->v_empty[st], ph ^ 1);
+                ptx::mbar_arrive_expect_tx_w(&bars->v_full[st], kTileB);
+                for (int half = 0; half < 2; ++half)
+                    ptx::tma_load_3d_w(smem + kVOff + st * kTileB + half * kHalf, &mapV, &bars->v_full[st], half * 64, h,
+                                       row, pol);
+                if (++st == 2) { st = 0; ph ^= 1; }
+            }
+            ++k;
+        }
+    } else if (warp == 1) {
+        int st = 0;
+        uint32_t ph = 0, dph = 0, qeph = 0;
+        int k = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            ptx::mbar_wait(&bars->q_full, k & 1);
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->k_full[st], ph);
+                ptx::mbar_wait(&bars->v_full[st], ph);
+                ptx::tc_fence_after();
+                if (st == 0) issue_sd<0>(tmem, base); else issue_sd<1>(tmem, base);
+                ptx::mma_commit_w(&bars->sd_full);
+                ptx::mma_commit_w(&bars->v_empty[st]);
+                if (t + 1 == it.t1) ptx::mma_commit_w(&bars->q_empty);  // Q_g, dO_g feed only S, dP
+                ptx::mbar_wait(&bars->ds_ready, dph);
+                dph ^= 1;
+                if (t == it.t0) {  // dQ accumulator drained by the previous item's epilogue
+                    ptx::mbar_wait(&bars->dq_empty, qeph ^ 1);
+                    qeph ^= 1;
+                }
+                ptx::tc_fence_after();
+                if (st == 0) issue_dq<0>(tmem, base, t > it.t0); else issue_dq<1>(tmem, base, t > it.t0);
+                ptx::mma_commit_w(&bars->k_empty[st]);
+                if (++st == 2) { st = 0; ph ^= 1; }
+            }
+            ptx::mma_commit_w(&bars->dq_full);
+            ++k;
+        }
+    } else if (warp >= 4) {
+        // ---------------- row softmax: P = exp2(S scale log2e - lse_i log2e), dS = P (dP - D_i); epilogue dQ
+        const int wq = warp % 4;
+        const int r = wq * 32 + lane;  // query row within the block = TMEM lane
+        const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
+        uint32_t sph = 0, qph = 0;
+        while (iter.next(it, P.uts, P.B, HG)) {
+            const int h = it.hg / P.G, g = it.hg % P.G;
+            const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
+            const size_t li = ((size_t)it.u * P.H + h) * P.S + g * 128 + r;
+            const float lse2 = __ldg(P.lse + li) * kLog2e, dd = __ldg(P.dd + li);
+            for (int t = it.t0; t < it.t1; ++t) {
+                ptx::mbar_wait(&bars->sd_full, sph);
+                sph ^= 1;
+                ptx::tc_fence_after();
+                const int64_t remv = L - (int64_t)t * 128;
+                const int valid = remv < 128 ? (int)remv : 128;
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t sr[32], dr[32];
+                    ptx::tmem_ld32(tmem + lane_bits + c * 32, sr);
+                    ptx::tmem_ld32(tmem + lane_bits + 128 + c * 32, dr);
+                    ptx::tmem_wait_ld();
+                    ptx::reg_fence(sr);
+                    ptx::reg_fence(dr);
+                    uint32_t sw[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int col = c * 32 + 2 * j;
+                        const float p0 = col < valid ? ptx::ex2(fmaf(__uint_as_float(sr[2 * j]), P.scale_log2, -lse2)) : 0.f;
+                        const float p1 =
+                            col + 1 < valid ? ptx::ex2(fmaf(__uint_as_float(sr[2 * j + 1]), P.scale_log2, -lse2)) : 0.f;
+                        sw[j] = ptx::pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - dd),
+                                                 p1 * (__uint_as_float(dr[2 * j + 1]) - dd));
+                    }
+                    ptx::tmem_st16(tmem + lane_bits + c * 16, sw);
+                }
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bars->ds_ready);
+            }
+            // epilogue: dQ rows x scale -> final [B,H,S,d] row or a partial slot
+            ptx::mbar_wait(&bars->dq_full, qph);
+            qph ^= 1;
+            ptx::tc_fence_after();
+            float* dst = item_complete(it)
+                             ? P.dqbuf + ((size_t)(it.u * HG + it.hg) * 128 + r) * 128
+                             : P.slot_o + ((size_t)item_slot(it, cta) * 128 + r) * 128;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t o[32];
+                ptx::tmem_ld32_sync(tmem + lane_bits + 256 + c * 32, o);
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(dst + c * 32 + j) =
+                        make_float4(__uint_as_float(o[j]) * P.scale, __uint_as_float(o[j + 1]) * P.scale,
+                                    __uint_as_float(o[j + 2]) * P.scale, __uint_as_float(o[j + 3]) * P.scale);
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&bars->dq_empty);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+}  // namespace dq
+
+// D[u,h,i] = sum_c dO[u,i,h,c] O[u,i,h,c]   (one warp per row)
+template <typename TO>
+__global__ void softmax_bwd_d_kernel(const TO* __restrict__ out, const TO* __restrict__ dout, int B, int S, int H,
+                                     float* __restrict__ dd) {
+    const int64_t rrow = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;  // over (u, h, i)
+    const int lane = threadIdx.x % 32;
+    if (rrow >= (int64_t)B * H * S) return;
+    const int u = (int)(rrow / ((int64_t)H * S)), h = (int)((rrow / S) % H), i = (int)(rrow % S);
+    const size_t idx = (((size_t)u * S + i) * H + h) * 128;
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int c = lane + 32 * e;
+        float a, b;
+        if constexpr (sizeof(TO) == 2) {
+            a = __bfloat162float(out[idx + c]);
+            b = __bfloat162float(dout[idx + c]);
+        } else {
+            a = out[idx + c];
+            b = dout[idx + c];
+        }
+        s += a * b;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dd[rrow] = s;
+}
+
+// dq (final): shared seeds [S,H,d] = sum_u dqbuf[u,h,i,:] (ascending u); per-user [B,S,H,d]
+__global__ void softmax_bwd_dq_final_kernel(const float* __restrict__ dqbuf, int B, int S, int H, int per_user,
+                                            float* __restrict__ dq) {
+    const int64_t n = per_user ? (int64_t)B * S * H * 128 : (int64_t)S * H * 128;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % 128);
+        const int h = (int)((e / 128) % H);
+        const int i = (int)((e / (128 * H)) % S);
+        if (per_user) {
+            const int u = (int)(e / ((int64_t)128 * H * S));
+            dq[e] = dqbuf[(((size_t)u * H + h) * S + i) * 128 + c];
+        } else {
+            float s = 0.f;
+            for (int u = 0; u < B; ++u) s += dqbuf[(((size_t)u * H + h) * S + i) * 128 + c];
+            dq[e] = s;
+        }
+    }
+}
+
+}  // namespace
+
+bool softmax_bwd_supported(const Problem& p, bool dout_bf16) {
+    return p.in_bf16 && dout_bf16 && p.d == 128 && p.S % 128 == 0 && p.S <= kv::kMaxS &&
+           p.total_len < (int64_t(1) << 31) && (p.q_user_stride % 8) == 0;
+}
+
+size_t softmax_bwd_workspace(const Problem& p) {
+    const size_t C = (size_t)p.num_sms;
+    size_t off = 0;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    off = al(off + (size_t)(p.B + 1) * 8);           // uts
+    off = al(off + 2 * C * sizeof(int));             // slot_unit
+    off = al(off + 2 * C * 128 * 128 * 4);           // slots
+    off = al(off + (size_t)p.B * p.H * p.S * 4);     // D
+    off = al(off + (size_t)p.B * p.H * p.S * 128 * 4);  // dq buffer
+    return off;
+}
+
+cudaError_t launch_softmax_bwd(const Problem& p, const void* out, const float* lse, const void* dout, float* dq_out,
+                               void* dk, void* dv, char* ws, int* nlaunch, cudaEvent_t ev_a, cudaEvent_t ev_b) {
+    const size_t C = (size_t)p.num_sms;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    size_t off = 0;
+    int64_t* uts = reinterpret_cast<int64_t*>(ws + off);
+    off = al(off + (size_t)(p.B + 1) * 8);
+    int* slot_unit = reinterpret_cast<int*>(ws + off);
+    off = al(off + 2 * C * sizeof(int));
+    float* slots = reinterpret_cast<float*>(ws + off);
+    off = al(off + 2 * C * 128 * 128 * 4);
+    float* dd = reinterpret_cast<float*>(ws + off);
+    off = al(off + (size_t)p.B * p.H * p.S * 4);
+    float* dqbuf = reinterpret_cast<float*>(ws + off);
+    cudaError_t e;
+    int nl = 0;
+    // tile prefix (no output fill: nothing is written for empty users here)
+    Problem ps = p;
+    ps.outs = OutSpec{OUT_PARTIAL, 0, nullptr, nullptr};
+    ps.attn = VISTA_QLA;  // no softmax empty-fill
+    if ((e = launch_user_tiles(ps, uts, nullptr)) != cudaSuccess) return e;
+    ++nl;
+    // D
+    {
+        const int64_t rows = (int64_t)p.B * p.H * p.S;
+        const unsigned grid = (unsigned)((rows + 7) / 8);
+        softmax_bwd_d_kernel<__nv_bfloat16><<<grid, 256, 0, p.stream>>>(
+            reinterpret_cast<const __nv_bfloat16*>(out), reinterpret_cast<const __nv_bfloat16*>(dout), p.B, p.S, p.H, dd);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ++nl;
+    }
+    CUtensorMap mq, mg, mk, mv;
+    if (!make_q_map(&mq, p.q, p.S, p.H, p.B, p.q_user_stride) ||
+        !make_q_map(&mg, dout, p.S, p.H, p.B, (int64_t)p.S * p.H * 128) || !make_kv_map(&mk, p.k, p.total_len, p.H) ||
+        !make_kv_map(&mv, p.v, p.total_len, p.H))
+        return cudaErrorInvalidValue;
+    // pass 1: dK, dV
+    {
+        kv::Params P;
+        P.offsets = p.offsets;
+        P.uts = uts;
+        P.lse = lse;
+        P.dd = dd;
+        P.dk = reinterpret_cast<__nv_bfloat16*>(dk);
+        P.dv = reinterpret_cast<__nv_bfloat16*>(dv);
+        P.B = p.B;
+        P.S = p.S;
+        P.H = p.H;
+        P.scale_log2 = p.scale * kLog2e;
+        P.scale = p.scale;
+        P.q_per_user = p.q_user_stride != 0;
+        static const cudaError_t attr = cudaFuncSetAttribute(kv::sm100_softmax_bwd_kv_kernel,
+                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kv::kSmem);
+        if (attr != cudaSuccess) return attr;
+        if (ev_a && (e = cudaEventRecord(ev_a, p.stream)) != cudaSuccess) return e;
+        kv::sm100_softmax_bwd_kv_kernel<<<(unsigned)C, kv::kThreads, kv::kSmem, p.stream>>>(mq, mg, mk, mv, P);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (ev_b && (e = cudaEventRecord(ev_b, p.stream)) != cudaSuccess) return e;
+        ++nl;
+    }
+    // pass 2: dQ (stream-K over (u, h, g) units, partial slots summed into dqbuf)
+    {
+        if ((e = cudaMemsetAsync(dqbuf, 0, (size_t)p.B * p.H * p.S * 128 * 4, p.stream)) != cudaSuccess) return e;
+        dq::Params P;
+        P.offsets = p.offsets;
+        P.uts = uts;
+        P.slot_unit = slot_unit;
+        P.slot_o = slots;
+        P.dqbuf = dqbuf;
+        P.lse = lse;
+        P.dd = dd;
+        P.B = p.B;
+        P.S = p.S;
+        P.H = p.H;
+        P.G = p.S / 128;
+        P.scale_log2 = p.scale * kLog2e;
+        P.scale = p.scale;
+        P.q_per_user = p.q_user_stride != 0;
+        static const cudaError_t attr = cudaFuncSetAttribute(dq::sm100_softmax_bwd_dq_kernel,
+                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, dq::kSmem);
+        if (attr != cudaSuccess) return attr;
+        dq::sm100_softmax_bwd_dq_kernel<<<(unsigned)C, dq::kThreads, dq::kSmem, p.stream>>>(mq, mg, mk, mv, P);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ++nl;
+        // split units: sum the run of slots (the QLA slot merge; units of 128 rows)
+        Workspace w{};
+        w.num_ctas = (int)C;
+        w.slot_unit_off = (size_t)(reinterpret_cast<char*>(slot_unit) - ws);
+        w.slot_o_off = (size_t)(reinterpret_cast<char*>(slots) - ws);
+        if ((e = launch_merge_qla_slots(p, w, ws, dqbuf)) != cudaSuccess) return e;
+        ++nl;
+    }
+    {
+        const bool per_user = p.q_user_stride != 0;
+        const int64_t n = per_user ? (int64_t)p.B * p.S * p.H * 128 : (int64_t)p.S * p.H * 128;
+        softmax_bwd_dq_final_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, p.stream>>>(
+            dqbuf, p.B, p.S, p.H, per_user, dq_out);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ++nl;
+    }
+    *nlaunch = nl;
+    return cudaSuccess;
+}
+
+}  // namespace vista

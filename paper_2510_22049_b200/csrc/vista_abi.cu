@@ -449,8 +449,13 @@ vista_status_t vista_summarize_bwd_workspace_size(const vista_desc_t* desc, int6
     if (st != VISTA_OK) return st;
     if (!bytes) return VISTA_ERR_NULL;
     if (total_len < 0) return VISTA_ERR_INVALID;
-    if (desc->attn != VISTA_QLA) return VISTA_ERR_UNSUPPORTED;
-    *bytes = plan_bwd(make_problem(desc, total_len)).total;
+    const Problem p = make_problem(desc, total_len);
+    if (desc->attn == VISTA_SOFTMAX) {
+        if (!softmax_bwd_supported(p, desc->out_dtype == VISTA_BF16)) return VISTA_ERR_UNSUPPORTED;
+        *bytes = softmax_bwd_workspace(p);
+        return VISTA_OK;
+    }
+    *bytes = plan_bwd(p).total;
     return VISTA_OK;
 }
 
@@ -458,12 +463,35 @@ vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, cons
                                    const int64_t* offsets, int64_t total_len, const void* out, const float* lse,
                                    const void* dout, float* dq, void* dk, void* dv, void* workspace,
                                    size_t workspace_bytes, void* stream) {
-    (void)out;
-    (void)lse;
     vista_status_t st = validate_desc(desc);
     if (st != VISTA_OK) return st;
-    if (desc->attn != VISTA_QLA) return VISTA_ERR_UNSUPPORTED;  // softmax backward: not yet
     if (total_len < 0) return VISTA_ERR_INVALID;
+    if (desc->attn == VISTA_SOFTMAX) {
+        if (!q || !offsets || !dout || !dq || !out || !lse) return VISTA_ERR_NULL;
+        if (total_len > 0 && (!k || !v || !dk || !dv)) return VISTA_ERR_NULL;
+        if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(out) ||
+            !aligned16(lse) || !aligned16(dq) || !aligned16(dk) || !aligned16(dv))
+            return VISTA_ERR_MISALIGNED;
+        Problem p = make_problem(desc, total_len);
+        p.q = q;
+        p.k = k;
+        p.v = v;
+        p.offsets = offsets;
+        p.stream = reinterpret_cast<cudaStream_t>(stream);
+        if (!softmax_bwd_supported(p, desc->out_dtype == VISTA_BF16)) return VISTA_ERR_UNSUPPORTED;
+        if (p.B == 0) return VISTA_OK;
+        const size_t need = softmax_bwd_workspace(p);
+        if (!workspace || workspace_bytes < need) return VISTA_ERR_WORKSPACE;
+        if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
+        cudaEvent_t ev_a = g_ev_start, ev_b = g_ev_stop;
+        g_ev_start = g_ev_stop = nullptr;
+        int nl = 0;
+        cudaError_t e = launch_softmax_bwd(p, out, lse, dout, dq, dk, dv, reinterpret_cast<char*>(workspace), &nl,
+                                           ev_a, ev_b);
+        if (e != cudaSuccess) return cuda_fail(e);
+        g_launches += (unsigned long long)nl;
+        return VISTA_OK;
+    }
     if (!q || !offsets || !dout || !dq) return VISTA_ERR_NULL;
     if (total_len > 0 && (!k || !v || !dk || !dv)) return VISTA_ERR_NULL;
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dq) || !aligned16(dk) ||

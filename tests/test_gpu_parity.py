@@ -518,3 +518,44 @@ def test_qla_backward_per_user_seeds(cuda_lib):
     rq, rk, rv = oracle.qla_backward(q, k, v, off, g, "silu", "silu", True, q_per_user=True)
     for u in range(len(lens)):
         _bwd_check(dq[u], rq[u], 2e-2, f"dq user {u}")
+
+
+# ----------------------------------------------------------------------------- softmax backward (NEXT-2)
+@pytest.mark.parametrize("S,H,lens,per_user", [(256, 2, [0, 1, 127, 129, 300, 2049, 5], False),
+                                               (128, 1, [10_000, 3, 640], False),
+                                               (256, 1, [700, 129], True)])
+def test_softmax_backward_tcgen05(cuda_lib, S, H, lens, per_user):
+    vista = cuda_lib
+    d = 128
+    rng = np.random.default_rng(S + len(lens))
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=41, tau=1)
+    if per_user:
+        q = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    g = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    qt, kt, vt = to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16")
+    ot = torch.from_numpy(off).cuda()
+    out, lse = vista.summarize(qt, kt, vt, ot, int(off[-1]), out_dtype=vista.BF16)
+    dq, dk, dv = vista.summarize_bwd(qt, kt, vt, ot, int(off[-1]), to_dev(g, "bf16"), attn=vista.SOFTMAX,
+                                     out=out, lse=lse)
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.softmax_backward(q, k, v, off, g, q_per_user=per_user)
+    if per_user:
+        for u in range(len(lens)):
+            if lens[u]:
+                _bwd_check(dq[u], rq[u], 2e-2, f"dq user {u}")
+    else:
+        _bwd_check(dq, rq, 2e-2, "dq")
+    dkn, dvn = dk.float().cpu().numpy(), dv.float().cpu().numpy()
+    for u in range(len(lens)):
+        a, b = off[u], off[u + 1]
+        if b > a:
+            _bwd_check(dkn[a:b], rk[a:b], 2e-2, f"dk user {u}")
+            _bwd_check(dvn[a:b], rv[a:b], 2e-2, f"dv user {u}")
+
+
+def test_softmax_backward_unsupported_shape(cuda_lib):
+    vista = cuda_lib
+    d = vista.make_desc(2, 512, 1, 128)
+    with pytest.raises(vista.VistaError) as e:
+        vista.vista_summarize_bwd_workspace_size(d, 100)
+    assert "UNSUPPORTED" in str(e.value)

@@ -217,8 +217,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(&bars->k_full[ks], kph);
                 ptx::mbar_wait(&bars->v_full, vph);
                 vph ^= 1;
-                ptx::mbar_wait(&bars->acc_empty, aph ^ 1);  // the epilogue has drained dV, dK of the last tile
-                aph ^= 1;
                 ptx::tc_fence_after();
                 for (int g = 0; g < G; ++g) {
                     if (ks == 0) issue_sd<0>(tmem, base, g); else issue_sd<1>(tmem, base, g);
@@ -229,6 +227,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::mbar_wait(&bars->pds_ready, pph);
                     pph ^= 1;
+                    if (g == 0) {  // the epilogue has drained dV, dK of the last tile (overlaps S^T, softmax)
+                        ptx::mbar_wait(&bars->acc_empty, aph ^ 1);
+                        aph ^= 1;
+                    }
                     ptx::tc_fence_after();
                     issue_vk(tmem, base, g);
                 }

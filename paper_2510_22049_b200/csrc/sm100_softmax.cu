@@ -324,7 +324,7 @@ __device__ __forceinline__ float exp_tile(const uint32_t (&r)[4][32], float sl2,
 
 // exp_tile for part PART of NP equal key ranges (32-key chunks [PART 4/NP, (PART+1) 4/NP)); P into
 // the matching TMEM columns
-template <int PART, int NP>
+template <int PART, int NP, int EMU = 0>
 __device__ __forceinline__ float exp_part(const uint32_t (&r)[4][32], float sl2, float neg, uint32_t tS) {
     const uint64_t sl2x2 = ptx::f2_pack(sl2, sl2);
     const uint64_t negx2 = ptx::f2_pack(neg, neg);
@@ -336,9 +336,14 @@ __device__ __forceinline__ float exp_part(const uint32_t (&r)[4][32], float sl2,
         for (int j = 0; j < 16; ++j) {
             const uint64_t x2 = ptx::f2_fma(
                 ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
-            float x0, x1;
-            ptx::f2_unpack(x2, x0, x1);
-            const uint64_t p2 = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+            uint64_t p2;
+            if (EMU > 0 && (j & 7) >= 8 - EMU) {
+                p2 = ptx::exp2_emu2(x2);
+            } else {
+                float x0, x1;
+                ptx::f2_unpack(x2, x0, x1);
+                p2 = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+            }
             acc[j & 1] = ptx::f2_add(acc[j & 1], p2);
             float p0, p1;
             ptx::f2_unpack(p2, p0, p1);
@@ -758,7 +763,8 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 const float m_old = m_used;
                 if (any) m_used = fmaxf(m_used, mxs);
                 if constexpr (kSplitP > 1) {
-                    const float lt0 = exp_part<0, kSplitP>(r, sl2, -m_used, tS);
+                    const float lt0 = full ? exp_part<0, kSplitP, kEmuPerEight>(r, sl2, -m_used, tS)
+                                           : exp_part<0, kSplitP>(r, sl2, -m_used, tS);
                     // O rescale before the first arrive (PV(t) accumulates into O right after it);
                     // placed after the first part so its registers are free
                     if (any && t > it.t0) {
@@ -788,7 +794,8 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                         ptx::mbar_arrive(&bars->p_part[wg][1]);
                         lt += exp_part<3, 4>(r, sl2, -m_used, tS);
                     } else {
-                        lt += exp_part<1, 2>(r, sl2, -m_used, tS);
+                        lt += full ? exp_part<1, 2, kEmuPerEight>(r, sl2, -m_used, tS)
+                                   : exp_part<1, 2>(r, sl2, -m_used, tS);
                     }
                     if (tr) VTRACE(6, t - it.t0, wg);
                     l += lt;

@@ -121,6 +121,19 @@ vista_status_t vista_summarize_fwd(const vista_desc_t* desc, const void* q, cons
                                    void* stream);
 
 /*
+ * vista_summarize_fwd plus the int8 export of the summary rows (NEXT-1; scheme of
+ * vista_quantize_rows_int8 below, applied to out as stored): codes [B,S,H,d] int8 (16-B aligned),
+ * scale / zero_point [B,S,H] float32.  On the tcgen05 softmax path with a bf16, 32-B aligned out
+ * the export is fused into the epilogues (no second pass over out); otherwise it runs after.
+ * Results equal vista_quantize_rows_int8(out) bit for bit.
+ */
+vista_status_t vista_summarize_fwd_int8(const vista_desc_t* desc, const void* q, const void* k,
+                                        const void* v, const int64_t* offsets, int64_t total_len,
+                                        void* out, float* lse, int8_t* codes, float* scale,
+                                        float* zero_point, void* workspace, size_t workspace_bytes,
+                                        void* stream);
+
+/*
  * Partial pass over one shard of every user's history (split-L across GPUs, flash-decoding
  * style).  Same inputs as vista_summarize_fwd; here offsets describe THIS shard's rows of each
  * user.  Writes part_o and (softmax) part_lse, laid out as described above.  Combine the shards

@@ -26,7 +26,7 @@ __all__ = [
     "vista_check_offsets", "vista_dispatch_name", "vista_time_next_main_kernel", "vista_launch_counter",
     "vista_quantize_rows_int8", "quantize_int8",
     "vista_summarize_prefix_workspace_size", "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
-    "vista_summarize_bwd_workspace_size", "vista_summarize_bwd",
+    "vista_summarize_bwd_workspace_size", "vista_summarize_bwd", "vista_summarize_fwd_int8",
     "summarize", "summarize_partial", "summarize_merge", "summarize_bwd",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
@@ -95,6 +95,7 @@ def load():
     lib.vista_summarize_merge.argtypes = [DP, i32, P, P, P, P, P, P, P, sz, P]
     lib.vista_summarize_prefix_workspace_size.argtypes = [DP, i64, i64, ctypes.POINTER(sz)]
     lib.vista_summarize_bwd_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
+    lib.vista_summarize_fwd_int8.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, sz, P]
     lib.vista_summarize_bwd.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, P, sz, P]
     lib.vista_summarize_fwd_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_partial_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
@@ -109,7 +110,7 @@ def load():
     for f in ("vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
               "vista_summarize_merge", "vista_check_offsets", "vista_summarize_prefix_workspace_size",
               "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
-              "vista_summarize_bwd_workspace_size", "vista_summarize_bwd"):
+              "vista_summarize_bwd_workspace_size", "vista_summarize_bwd", "vista_summarize_fwd_int8"):
         getattr(lib, f).restype = ctypes.c_int
     if lib.vista_abi_version() != ABI_VERSION:
         raise RuntimeError("libvista ABI version mismatch")
@@ -166,6 +167,14 @@ def vista_summarize_fwd(desc, q, k, v, offsets, total_len, out, lse, workspace, 
     _check(load().vista_summarize_fwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
                                       int(total_len), _ptr(out), _ptr(lse), _ptr(workspace),
                                       int(workspace_bytes), _stream(stream)), "vista_summarize_fwd")
+
+
+def vista_summarize_fwd_int8(desc, q, k, v, offsets, total_len, out, lse, codes, scale, zero_point, workspace,
+                             workspace_bytes, stream=None):
+    _check(load().vista_summarize_fwd_int8(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                                           int(total_len), _ptr(out), _ptr(lse), _ptr(codes), _ptr(scale),
+                                           _ptr(zero_point), _ptr(workspace), int(workspace_bytes), _stream(stream)),
+           "vista_summarize_fwd_int8")
 
 
 def vista_summarize_partial(desc, q, k, v, offsets, total_len, part_o, part_lse, workspace,

@@ -42,6 +42,11 @@ struct OutSpec {
     int out_bf16;        // OUT_FINAL only: 1 -> bf16, 0 -> f32
     void* out;           // FINAL: out;  PARTIAL: part_o (float*)
     float* lse;          // may be NULL in FINAL mode
+    // NEXT-1 fused int8 export of the out rows (FINAL mode; NULL = none): codes [B,S,H,d] int8,
+    // qscale / qzp [B,S,H] float32 (int8_export.cuh)
+    int8_t* codes;
+    float* qscale;
+    float* qzp;
 };
 
 // Everything a launch needs (filled by the ABI layer after validation).

@@ -12,6 +12,7 @@
 #include <math.h>
 
 #include "internal.h"
+#include "int8_export.cuh"
 #include "qla_common.cuh"
 #include "sm100_ptx.cuh"
 
@@ -127,6 +128,13 @@ __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, in
                 }
                 if (outs.lse)
                     for (int e = lane; e < H * S; e += 32) outs.lse[(size_t)uu * H * S + e] = -INFINITY;
+                if (outs.codes) {  // zero rows export as code 0, scale 1e-12, zero point 0
+                    for (size_t e = lane; e < n_sm; e += 32) outs.codes[(size_t)uu * n_sm + e] = 0;
+                    for (int e = lane; e < S * H; e += 32) {
+                        outs.qscale[(size_t)uu * S * H + e] = 1e-12f;
+                        outs.qzp[(size_t)uu * S * H + e] = 0.f;
+                    }
+                }
             } else if (zbuf) {
                 for (size_t e = lane; e < n_z; e += 32) zbuf[(size_t)uu * n_z + e] = 0.f;
             }
@@ -290,6 +298,27 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
         const float4 v = make_float4(acc[r].x * inv, acc[r].y * inv, acc[r].z * inv, acc[r].w * inv);
         const int i = g * rows + row;
         out_store4(outs, S, H, u, h, i, lane * 4, v);
+        if (outs.codes) {  // NEXT-1 fused int8 export of the merged row, as stored
+            float x[4] = {v.x, v.y, v.z, v.w};
+            if (outs.out_bf16)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x[e] = __bfloat162float(__float2bfloat16_rn(x[e]));
+            float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3])), mn = fminf(fminf(x[0], x[1]), fminf(x[2], x[3]));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            }
+            float sc, z;
+            i8_scale_zp(mx, mn, sc, z);
+            const size_t orow = ((size_t)u * S + i) * H + h;
+            reinterpret_cast<uint32_t*>(outs.codes + orow * 128)[lane] =
+                i8_pack4(x[0], x[1], x[2], x[3], sc, z, i8_recip(sc));
+            if (lane == 0) {
+                outs.qscale[orow] = sc;
+                outs.qzp[orow] = z;
+            }
+        }
         if (lane == 0) lse_store(outs, S, H, u, h, i, M[r] + logf(l[r]));
     }
 }

@@ -23,6 +23,7 @@
 #include <math.h>
 
 #include "internal.h"
+#include "int8_export.cuh"
 #include "sm100_ptx.cuh"
 #include "work.cuh"
 
@@ -849,6 +850,11 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                     for (int j = 0; j < 16; ++j)
                         v[c * 16 + j] = ptx::pack_bf16x2(__uint_as_float(o[2 * j]) * inv_l,
                                                          __uint_as_float(o[2 * j + 1]) * inv_l);
+                }
+                if (P.outs.codes) {  // NEXT-1: int8 export of the row, as stored (bf16)
+                    const int h = it.hg / P.G, g = it.hg % P.G;
+                    const size_t orow = ((size_t)it.u * P.S + g * kRows + wg * 128 + row) * P.H + h;
+                    i8_export_row_bf16(v, P.outs.codes + orow * 128, P.outs.qscale + orow, P.outs.qzp + orow);
                 }
                 store_rows_coalesced(P, it, cta, wg * 128 + wq * 32, kRows, tO, v, 0);
             } else if (coalesced) {

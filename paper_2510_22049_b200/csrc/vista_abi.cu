@@ -285,6 +285,36 @@ vista_status_t vista_summarize_fwd(const vista_desc_t* desc, const void* q, cons
     return run(desc, q, k, v, offsets, total_len, o, workspace, workspace_bytes, stream);
 }
 
+vista_status_t vista_summarize_fwd_int8(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                        const int64_t* offsets, int64_t total_len, void* out, float* lse,
+                                        int8_t* codes, float* scale, float* zero_point, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+    if (!desc) return VISTA_ERR_NULL;
+    if (desc->num_users > 0 && (!codes || !scale || !zero_point)) return VISTA_ERR_NULL;
+    if (!aligned16(codes) || (reinterpret_cast<uintptr_t>(scale) & 3) || (reinterpret_cast<uintptr_t>(zero_point) & 3))
+        return VISTA_ERR_MISALIGNED;
+    OutSpec o{OUT_FINAL, desc->out_dtype == VISTA_BF16, out, desc->attn == VISTA_SOFTMAX ? lse : nullptr};
+    // fused into the epilogues (softmax epilogue, slot merge, empty-user fill) on the tcgen05 softmax
+    // path with a bf16, 32-B aligned out; otherwise the export kernel runs after the summarization
+    Problem pp = validate_desc(desc) == VISTA_OK ? make_problem(desc, total_len) : Problem{};
+    const bool fused = validate_desc(desc) == VISTA_OK && choose_path(pp) == PATH_SM100_SOFTMAX &&
+                       desc->out_dtype == VISTA_BF16 && (reinterpret_cast<uintptr_t>(out) & 31) == 0 &&
+                       !softmax_uses_pairs(pp);
+    if (fused) {
+        o.codes = codes;
+        o.qscale = scale;
+        o.qzp = zero_point;
+    }
+    vista_status_t st = run(desc, q, k, v, offsets, total_len, o, workspace, workspace_bytes, stream);
+    if (st != VISTA_OK || fused || desc->num_users == 0) return st;
+    const int64_t n = (int64_t)desc->num_users * desc->num_summary * desc->num_heads;
+    cudaError_t e = launch_quantize_rows(n, desc->head_dim, desc->out_dtype == VISTA_BF16, out, codes, scale,
+                                         zero_point, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches += 1;
+    return VISTA_OK;
+}
+
 vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, const void* k, const void* v,
                                        const int64_t* offsets, int64_t total_len, float* part_o, float* part_lse,
                                        void* workspace, size_t workspace_bytes, void* stream) {

@@ -559,3 +559,41 @@ def test_softmax_backward_unsupported_shape(cuda_lib):
     with pytest.raises(vista.VistaError) as e:
         vista.vista_summarize_bwd_workspace_size(d, 100)
     assert "UNSUPPORTED" in str(e.value)
+
+
+# ----------------------------------------------------------------------------- NEXT-1 fused export
+@pytest.mark.parametrize("S,H,out_bf16,attn", [(256, 2, True, "softmax"), (512, 1, True, "softmax"),
+                                               (256, 1, False, "softmax"), (256, 2, True, "qla")])
+def test_int8_export_fused_equals_separate(cuda_lib, S, H, out_bf16, attn):
+    """vista_summarize_fwd_int8 (fused into the softmax epilogue / slot merge / empty-user fill on
+    the tcgen05 path, a separate pass otherwise) == vista_quantize_rows_int8 of the output == the
+    oracle's quantizer applied to that output, bit for bit; many users force stream-K splits."""
+    vista = cuda_lib
+    rng = np.random.default_rng(S + H)
+    lens = [int(x) for x in rng.integers(0, 3000, size=160)]
+    lens[3] = 0
+    lens[10] = 129
+    d = 128
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=23)
+    qt, kt, vt = to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16")
+    ot = torch.from_numpy(off).cuda()
+    a = vista.SOFTMAX if attn == "softmax" else vista.QLA
+    desc = vista.make_desc(len(lens), S, H, d, in_dtype=vista.BF16, out_dtype=vista.BF16 if out_bf16 else vista.F32,
+                           attn=a)
+    total = int(off[-1])
+    need = vista.vista_summarize_workspace_size(desc, total)
+    ws = torch.empty(max(need, 16), dtype=torch.uint8, device="cuda")
+    B = len(lens)
+    out = torch.empty((B, S, H, d), dtype=torch.bfloat16 if out_bf16 else torch.float32, device="cuda")
+    lse = torch.empty((B, H, S), dtype=torch.float32, device="cuda") if attn == "softmax" else None
+    codes = torch.empty((B, S, H, d), dtype=torch.int8, device="cuda")
+    sc = torch.empty((B, S, H), dtype=torch.float32, device="cuda")
+    zp = torch.empty((B, S, H), dtype=torch.float32, device="cuda")
+    vista.vista_summarize_fwd_int8(desc, qt, kt, vt, ot, total, out, lse, codes, sc, zp, ws, need)
+    c2, s2, z2 = vista.quantize_int8(out)
+    torch.cuda.synchronize()
+    assert torch.equal(codes, c2.view(codes.shape)), "codes"
+    assert torch.equal(sc, s2.view(sc.shape)) and torch.equal(zp, z2.view(zp.shape)), "scale / zero point"
+    rc, rs, rz = oracle.quantize_rows_int8(out.float().cpu().numpy().reshape(-1, d))
+    assert np.array_equal(codes.cpu().numpy().reshape(-1, d), rc)
+    assert np.array_equal(sc.cpu().numpy().reshape(-1), rs) and np.array_equal(zp.cpu().numpy().reshape(-1), rz)

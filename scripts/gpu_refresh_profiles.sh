@@ -7,13 +7,16 @@ O=gpurun_out/refresh
 mkdir -p $O
 python bench.py > $O/bench_c2_softmax.json 2> $O/bench_c2_softmax.err
 python bench.py --attn qla > $O/bench_c2_qla.json 2> $O/bench_c2_qla.err
+python bench.py --backward --steps 100 > $O/bench_c2_softmax_bwd.json 2> $O/bench_c2_softmax_bwd.err
+python bench.py --attn qla --backward --steps 100 > $O/bench_c2_qla_bwd.json 2> $O/bench_c2_qla_bwd.err
+python bench.py --export-int8 --steps 100 --no-cpu-baseline > $O/bench_c2_softmax_int8.json 2> $O/bench_c2_softmax_int8.err
 STEPS=100 bash scripts/ab_configs.sh > $O/configs.txt 2>&1
 cp gpurun_out/cfg_*.json $O/ 2>/dev/null
 for cfg in c2 c5; do
   for attn in softmax qla; do
     CMD="python bench.py --config $cfg --attn $attn --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
     $CMD > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none \
-      -k regex:"sm100|merge_|user_tiles|qla_|quantize|simt_" --csv --log-file $O/launches_${cfg}_${attn}.csv $CMD > /dev/null 2>&1
+      -k regex:"sm100|merge_|user_tiles|qla_|quantize|simt_|softmax_bwd" --csv --log-file $O/launches_${cfg}_${attn}.csv $CMD > /dev/null 2>&1
     python scripts/ncu_summary.py launches $O/launches_${cfg}_${attn}.csv > $O/launches_${cfg}_${attn}.txt
   done
 done

@@ -191,6 +191,8 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
                                                                   OutSpec outs, int S, int H, int G) {
     extern __shared__ __align__(128) uint8_t merge_smem_raw[];
     MergeSmem& sm = *reinterpret_cast<MergeSmem*>(merge_smem_raw);
+    // PDL: launched while the summarization kernel runs; its slots are complete after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int s = blockIdx.x;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int row0 = blockIdx.y * kMergeRows;
@@ -748,10 +750,11 @@ cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, cha
                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)sizeof(MergeSmem));
     if (attr != cudaSuccess) return attr;
-    merge_softmax_slots_kernel<<<grid, 256, sizeof(MergeSmem), p.stream>>>(
-        reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots, reinterpret_cast<const float*>(ws + w.slot_o_off),
-        reinterpret_cast<const float*>(ws + w.slot_lse_off), w.rows_per_unit, p.outs, p.S, p.H, p.S / w.rows_per_unit);
-    return cudaGetLastError();
+    return launch_pdl(merge_softmax_slots_kernel, grid, dim3(256), sizeof(MergeSmem), p.stream,
+                      reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots,
+                      reinterpret_cast<const float*>(ws + w.slot_o_off),
+                      reinterpret_cast<const float*>(ws + w.slot_lse_off), w.rows_per_unit, p.outs, p.S, p.H,
+                      p.S / w.rows_per_unit);
 }
 
 cudaError_t launch_merge_qla_slots_w(const Problem& p, const Workspace& w, char* ws, uint8_t* wbuf) {

@@ -113,7 +113,7 @@ cudaError_t launch_qla_bwd_kv_simt(const Problem& p, const float* dz, void* dk, 
 cudaError_t launch_sm100_qla_bwd_kv(const Problem& p, const Workspace& w, char* ws, const uint8_t* dz_op, void* dk,
                                     void* dv);
 bool qla_bwd_uses_tc(const Problem& p);
-// softmax backward (NEXT-2): bf16, d = 128, S % 128 == 0, S <= 256, bf16 dout
+// softmax backward (NEXT-2): bf16, d = 128, S % 128 == 0, S <= 1024, bf16 dout
 bool softmax_bwd_supported(const Problem& p, bool dout_bf16);
 size_t softmax_bwd_workspace(const Problem& p);
 cudaError_t launch_softmax_bwd(const Problem& p, const void* out, const float* lse, const void* dout, float* dq,

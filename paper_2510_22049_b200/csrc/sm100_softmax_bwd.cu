@@ -75,10 +75,14 @@ __device__ __forceinline__ void store32_rows(uint32_t tcol, const uint32_t (&w)[
 
 // ============================================================================ pass 1: dK, dV
 namespace kv {
-constexpr int kMaxS = 256;
-constexpr int kQOff = 0;                            // Q: S/128 blocks of 32 KB
-constexpr int kGOff = kQOff + (kMaxS / 128) * kTileB;  // dO
-constexpr int kKOff = kGOff + (kMaxS / 128) * kTileB;  // K ring, 2 stages
+// S <= 256 (RESIDENT): Q and dO of the unit stay in shared memory, [0, 64 KB) and [64, 128 KB).
+// S > 256 (STREAM): the (Q_g, dO_g) pairs of each 128-row block stream through a 2-stage ring of
+// 64 KB in the same 128 KB (L2-resident reloads per key tile).
+constexpr int kResidentMaxS = 256;
+constexpr int kMaxS = 1024;
+constexpr int kQOff = 0;                            // Q blocks (RESIDENT) / ring stages (STREAM)
+constexpr int kGOff = kQOff + 2 * kTileB;            // dO blocks (RESIDENT)
+constexpr int kKOff = 4 * kTileB;                    // K ring, 2 stages
 constexpr int kVOff = kKOff + 2 * kTileB;            // V, 1 stage
 constexpr int kBarOff = kVOff + kTileB;
 constexpr int kSmem = kBarOff + 256 + 1024;
@@ -87,6 +91,7 @@ constexpr int kThreads = 384;
 struct Bars {
     uint64_t q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty;
     uint64_t sd_full, pds_ready, acc_full, acc_empty;
+    uint64_t qg_full[2], qg_empty[2];
     uint32_t tmem_base;
 };
 
@@ -104,10 +109,9 @@ struct Params {
 
 // S^T_g = K Q_g^T -> cols [0,128);  dP^T_g = V dO_g^T -> cols [128,256)   (all operands K-major)
 template <int KS>
-__device__ __forceinline__ void issue_sd(uint32_t tmem, uint32_t base, int g) {
+__device__ __forceinline__ void issue_sd(uint32_t tmem, uint32_t base, uint32_t qa, uint32_t ga) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 0);
     const uint32_t ka = base + kKOff + KS * kTileB, va = base + kVOff;
-    const uint32_t qa = base + kQOff + g * kTileB, ga = base + kGOff + g * kTileB;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
@@ -121,9 +125,8 @@ __device__ __forceinline__ void issue_sd(uint32_t tmem, uint32_t base, int g) {
     }
 }
 // dV += P^T_g dO_g -> cols [256,384);  dK += dS^T_g Q_g -> cols [384,512)   (A from TMEM, B MN-major)
-__device__ __forceinline__ void issue_vk(uint32_t tmem, uint32_t base, int g) {
+__device__ __forceinline__ void issue_vk(uint32_t tmem, uint32_t qa, uint32_t ga, int g) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);
-    const uint32_t qa = base + kQOff + g * kTileB, ga = base + kGOff + g * kTileB;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
         ptx::mma_ts_w(tmem + 256, tmem + kk * 8, ptx::sdesc_sw128(ga + kk * 2048, kHalf, 1024), id,
@@ -134,6 +137,7 @@ __device__ __forceinline__ void issue_vk(uint32_t tmem, uint32_t base, int g) {
                       (g > 0 || kk > 0) ? 1u : 0u);
 }
 
+template <bool STREAM>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_softmax_bwd_kv_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapG,
                                 const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
@@ -158,6 +162,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_init(&bars->pds_ready, 128);
         ptx::mbar_init(&bars->acc_full, 1);
         ptx::mbar_init(&bars->acc_empty, 128);
+        for (int s2 = 0; s2 < 2; ++s2) {
+            ptx::mbar_init(&bars->qg_full[s2], 1);
+            ptx::mbar_init(&bars->qg_empty[s2], 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
@@ -169,7 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     iter.init(P.uts, P.B, HG, cta, num_ctas);
     Item it;
     if (warp == 0) {
-        // ---------------- TMA producer: Q, dO of the unit; K (2 stages), V (1 stage) per tile
+        // ---------------- TMA producer: Q, dO (resident per unit, or streamed per block);
+        //                  K (2 stages), V (1 stage) per tile
         ptx::tma_prefetch(&mapQ);
         ptx::tma_prefetch(&mapG);
         ptx::tma_prefetch(&mapK);
@@ -178,17 +187,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         int ks = 0;
         uint32_t kph = 0, vph = 0;
         int k = 0;
+        int qs = 0;
+        uint32_t qph = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             const int h = it.hg;
-            if (k > 0) ptx::mbar_wait(&bars->q_empty, (k - 1) & 1);
-            ptx::mbar_arrive_expect_tx_w(&bars->q_full, 2 * G * kTileB);
-            for (int g = 0; g < G; ++g)
-                for (int half = 0; half < 2; ++half) {
-                    ptx::tma_load_4d_w(smem + kQOff + g * kTileB + half * kHalf, &mapQ, &bars->q_full, half * 64, h,
-                                       g * 128, P.q_per_user ? it.u : 0, pol_q);
-                    ptx::tma_load_4d_w(smem + kGOff + g * kTileB + half * kHalf, &mapG, &bars->q_full, half * 64, h,
-                                       g * 128, it.u, pol);
-                }
+            if constexpr (!STREAM) {
+                if (k > 0) ptx::mbar_wait(&bars->q_empty, (k - 1) & 1);
+                ptx::mbar_arrive_expect_tx_w(&bars->q_full, 2 * G * kTileB);
+                for (int g = 0; g < G; ++g)
+                    for (int half = 0; half < 2; ++half) {
+                        ptx::tma_load_4d_w(smem + kQOff + g * kTileB + half * kHalf, &mapQ, &bars->q_full, half * 64,
+                                           h, g * 128, P.q_per_user ? it.u : 0, pol_q);
+                        ptx::tma_load_4d_w(smem + kGOff + g * kTileB + half * kHalf, &mapG, &bars->q_full, half * 64,
+                                           h, g * 128, it.u, pol_q);
+                    }
+            }
             const int64_t row0 = P.offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
                 const int32_t row = (int32_t)(row0 + (int64_t)t * 128);
@@ -203,6 +216,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_arrive_expect_tx_w(&bars->v_full, kTileB);
                 for (int half = 0; half < 2; ++half)
                     ptx::tma_load_3d_w(smem + kVOff + half * kHalf, &mapV, &bars->v_full, half * 64, h, row, pol);
+                if constexpr (STREAM) {  // (Q_g, dO_g) for every 128-row block of this tile
+                    for (int g = 0; g < G; ++g) {
+                        ptx::mbar_wait(&bars->qg_empty[qs], qph ^ 1);
+                        ptx::mbar_arrive_expect_tx_w(&bars->qg_full[qs], 2 * kTileB);
+                        for (int half = 0; half < 2; ++half) {
+                            ptx::tma_load_4d_w(smem + kQOff + qs * 2 * kTileB + half * kHalf, &mapQ, &bars->qg_full[qs],
+                                               half * 64, h, g * 128, P.q_per_user ? it.u : 0, pol_q);
+                            ptx::tma_load_4d_w(smem + kQOff + qs * 2 * kTileB + kTileB + half * kHalf, &mapG,
+                                               &bars->qg_full[qs], half * 64, h, g * 128, it.u, pol_q);
+                        }
+                        if (++qs == 2) { qs = 0; qph ^= 1; }
+                    }
+                }
             }
             ++k;
         }
@@ -210,16 +236,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- MMA issuer
         int ks = 0;
         uint32_t kph = 0, vph = 0, pph = 0, aph = 0;
+        int qs = 0;
+        uint32_t qph = 0;
         int k = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
-            ptx::mbar_wait(&bars->q_full, k & 1);
+            if constexpr (!STREAM) ptx::mbar_wait(&bars->q_full, k & 1);
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->k_full[ks], kph);
                 ptx::mbar_wait(&bars->v_full, vph);
                 vph ^= 1;
                 ptx::tc_fence_after();
                 for (int g = 0; g < G; ++g) {
-                    if (ks == 0) issue_sd<0>(tmem, base, g); else issue_sd<1>(tmem, base, g);
+                    uint32_t qa, ga;
+                    if constexpr (STREAM) {
+                        ptx::mbar_wait(&bars->qg_full[qs], qph);
+                        ptx::tc_fence_after();
+                        qa = base + kQOff + qs * 2 * kTileB;
+                        ga = qa + kTileB;
+                    } else {
+                        qa = base + kQOff + g * kTileB;
+                        ga = base + kGOff + g * kTileB;
+                    }
+                    if (ks == 0) issue_sd<0>(tmem, base, qa, ga); else issue_sd<1>(tmem, base, qa, ga);
                     ptx::mma_commit_w(&bars->sd_full);
                     if (g == G - 1) {
                         ptx::mma_commit_w(&bars->k_empty[ks]);  // K only feeds S^T
@@ -232,12 +270,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         aph ^= 1;
                     }
                     ptx::tc_fence_after();
-                    issue_vk(tmem, base, g);
+                    issue_vk(tmem, qa, ga, g);
+                    if constexpr (STREAM) {
+                        ptx::mma_commit_w(&bars->qg_empty[qs]);
+                        if (++qs == 2) { qs = 0; qph ^= 1; }
+                    }
                 }
                 ptx::mma_commit_w(&bars->acc_full);
                 if (++ks == 2) { ks = 0; kph ^= 1; }
             }
-            ptx::mma_commit_w(&bars->q_empty);  // Q, dO free once this unit's GEMMs complete
+            if constexpr (!STREAM) ptx::mma_commit_w(&bars->q_empty);  // Q, dO free once the unit's GEMMs complete
             ++k;
         }
     } else if (warp >= 4 && warp < 8) {
@@ -678,11 +720,18 @@ cudaError_t launch_softmax_bwd(const Problem& p, const void* out, const float* l
         P.scale_log2 = p.scale * kLog2e;
         P.scale = p.scale;
         P.q_per_user = p.q_user_stride != 0;
-        static const cudaError_t attr = cudaFuncSetAttribute(kv::sm100_softmax_bwd_kv_kernel,
-                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kv::kSmem);
-        if (attr != cudaSuccess) return attr;
+        const bool stream = p.S > kv::kResidentMaxS;
+        static const cudaError_t attr0 = cudaFuncSetAttribute(kv::sm100_softmax_bwd_kv_kernel<false>,
+                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kv::kSmem);
+        static const cudaError_t attr1 = cudaFuncSetAttribute(kv::sm100_softmax_bwd_kv_kernel<true>,
+                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kv::kSmem);
+        if (attr0 != cudaSuccess) return attr0;
+        if (attr1 != cudaSuccess) return attr1;
         if (ev_a && (e = cudaEventRecord(ev_a, p.stream)) != cudaSuccess) return e;
-        kv::sm100_softmax_bwd_kv_kernel<<<(unsigned)C, kv::kThreads, kv::kSmem, p.stream>>>(mq, mg, mk, mv, P);
+        if (stream)
+            kv::sm100_softmax_bwd_kv_kernel<true><<<(unsigned)C, kv::kThreads, kv::kSmem, p.stream>>>(mq, mg, mk, mv, P);
+        else
+            kv::sm100_softmax_bwd_kv_kernel<false><<<(unsigned)C, kv::kThreads, kv::kSmem, p.stream>>>(mq, mg, mk, mv, P);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (ev_b && (e = cudaEventRecord(ev_b, p.stream)) != cudaSuccess) return e;
         ++nl;

@@ -523,7 +523,9 @@ def test_qla_backward_per_user_seeds(cuda_lib):
 # ----------------------------------------------------------------------------- softmax backward (NEXT-2)
 @pytest.mark.parametrize("S,H,lens,per_user", [(256, 2, [0, 1, 127, 129, 300, 2049, 5], False),
                                                (128, 1, [10_000, 3, 640], False),
-                                               (256, 1, [700, 129], True)])
+                                               (256, 1, [700, 129], True),
+                                               (512, 1, [0, 1500, 129, 3], False),
+                                               (384, 2, [260, 1], True)])
 def test_softmax_backward_tcgen05(cuda_lib, S, H, lens, per_user):
     vista = cuda_lib
     d = 128
@@ -555,7 +557,7 @@ def test_softmax_backward_tcgen05(cuda_lib, S, H, lens, per_user):
 
 def test_softmax_backward_unsupported_shape(cuda_lib):
     vista = cuda_lib
-    d = vista.make_desc(2, 512, 1, 128)
+    d = vista.make_desc(2, 200, 1, 128)
     with pytest.raises(vista.VistaError) as e:
         vista.vista_summarize_bwd_workspace_size(d, 100)
     assert "UNSUPPORTED" in str(e.value)

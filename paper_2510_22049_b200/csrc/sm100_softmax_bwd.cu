@@ -73,6 +73,8 @@ __device__ __forceinline__ void store32_rows(uint32_t tcol, const uint32_t (&w)[
     }
 }
 
+__device__ __forceinline__ void named_sync_sm() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 // ============================================================================ pass 1: dK, dV
 namespace kv {
 // S <= 256 (RESIDENT): Q and dO of the unit stay in shared memory, [0, 64 KB) and [64, 128 KB).
@@ -84,8 +86,11 @@ constexpr int kQOff = 0;                            // Q blocks (RESIDENT) / rin
 constexpr int kGOff = kQOff + 2 * kTileB;            // dO blocks (RESIDENT)
 constexpr int kKOff = 4 * kTileB;                    // K ring, 2 stages
 constexpr int kVOff = kKOff + 2 * kTileB;            // V, 1 stage
-constexpr int kBarOff = kVOff + kTileB;
-constexpr int kSmem = kBarOff + 256 + 1024;
+constexpr int kTiles = kVOff + kTileB;               // 224 KB of 1024-B aligned operand tiles
+// Barriers and the unit's lse*log2e / D rows (RESIDENT, 2 x 256 floats) sit in front of the tiles:
+// with the dynamic shared memory base 1024-B aligned this is exactly the 227 KB maximum.
+constexpr int kHead = 3072;
+constexpr int kSmem = kHead + kTiles;
 constexpr int kThreads = 384;
 
 struct Bars {
@@ -143,9 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                                 const Params P) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Bars* bars = reinterpret_cast<Bars*>(smem_raw);
+    float* lsd = reinterpret_cast<float*>(smem_raw + 256);  // [2][256]: lse * log2e, D
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + kHead + 1023) & ~uintptr_t(1023));
+    if (smem + kTiles > smem_raw + kSmem) __trap();  // dynamic smem base not 1024-B aligned
     const uint32_t base = ptx::smem_u32(smem);
-    Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cta = blockIdx.x, num_ctas = gridDim.x;
     const int HG = P.H, G = P.S / 128;
@@ -289,8 +296,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t sph = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             const size_t lrow = ((size_t)it.u * P.H + it.hg) * P.S;
+            if constexpr (!STREAM) {  // the unit's lse * log2e and D rows into shared memory
+                named_sync_sm();      // the previous unit's chunks are done with them
+                for (int e = threadIdx.x - 128; e < P.S; e += 128) {
+                    lsd[e] = __ldg(P.lse + lrow + e) * kLog2e;
+                    lsd[256 + e] = __ldg(P.dd + lrow + e);
+                }
+                named_sync_sm();
+            }
             for (int t = it.t0; t < it.t1; ++t) {
                 for (int g = 0; g < G; ++g) {
+                    if constexpr (STREAM) {  // this block's 128 lse * log2e and D values into shared memory
+                        const int e = threadIdx.x - 128;
+                        const float lv = __ldg(P.lse + lrow + g * 128 + e) * kLog2e;
+                        const float dv = __ldg(P.dd + lrow + g * 128 + e);
+                        named_sync_sm();
+                        lsd[g * 0 + e] = lv;
+                        lsd[256 + e] = dv;
+                        named_sync_sm();
+                    }
                     ptx::mbar_wait(&bars->sd_full, sph);
                     sph ^= 1;
                     ptx::tc_fence_after();
@@ -299,20 +323,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t sr[32], dr[32];
                         ptx::tmem_ld32(tmem + lane_bits + c * 32, sr);
                         ptx::tmem_ld32(tmem + lane_bits + 128 + c * 32, dr);
-                        const float4* lq = reinterpret_cast<const float4*>(P.lse + lrow + g * 128 + c * 32);
-                        const float4* dq = reinterpret_cast<const float4*>(P.dd + lrow + g * 128 + c * 32);
                         float ls[32], dl[32];
+                        {  // shared-memory broadcast reads (the whole unit, or this block when streaming)
+                            const int col0 = (STREAM ? 0 : g * 128) + c * 32;
+                            const float4* lq = reinterpret_cast<const float4*>(lsd + col0);
+                            const float4* dq = reinterpret_cast<const float4*>(lsd + 256 + col0);
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const float4 a = __ldg(lq + e), b = __ldg(dq + e);
-                            ls[4 * e] = a.x * kLog2e;
-                            ls[4 * e + 1] = a.y * kLog2e;
-                            ls[4 * e + 2] = a.z * kLog2e;
-                            ls[4 * e + 3] = a.w * kLog2e;
-                            dl[4 * e] = b.x;
-                            dl[4 * e + 1] = b.y;
-                            dl[4 * e + 2] = b.z;
-                            dl[4 * e + 3] = b.w;
+                            for (int e = 0; e < 8; ++e) {
+                                const float4 a = lq[e], b = dq[e];
+                                ls[4 * e] = a.x;
+                                ls[4 * e + 1] = a.y;
+                                ls[4 * e + 2] = a.z;
+                                ls[4 * e + 3] = a.w;
+                                dl[4 * e] = b.x;
+                                dl[4 * e + 1] = b.y;
+                                dl[4 * e + 2] = b.z;
+                                dl[4 * e + 3] = b.w;
+                            }
                         }
                         ptx::tmem_wait_ld();
                         ptx::reg_fence(sr);

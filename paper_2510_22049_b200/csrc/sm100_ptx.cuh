@@ -213,6 +213,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx_w(uint64_t* bar, uint32_t 
         "r"(bytes)
         : "memory");
 }
+// Prefetch a tensor tile into L2 (no shared memory destination, no completion).
+__device__ __forceinline__ void tma_prefetch_l2_3d_w(const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n\t}" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_w(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
                                               int32_t c1, int32_t c2, uint64_t policy) {
     asm volatile(

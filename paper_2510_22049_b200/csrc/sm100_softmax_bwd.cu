@@ -16,12 +16,15 @@
 //     dQ += dS K (TS, K tile as the MN-major B operand).  Split units (stream-K) write partial
 //     slots, summed by the QLA slot merge into the [B, H, S, d] dQ buffer.
 //
-// TMEM (both): columns [0,128) S / S^T (bf16 P^T or dS over its first 64), [128,256) dP / dP^T
-// (bf16 dS^T over its first 64), then dV, dK (pass 1) or dQ (pass 2).
+// TMEM, pass 1: two buffers of 128 columns, each a 64-query half block (S^T in its first 64
+// columns with bf16 P^T over the first 32; dP^T in the last 64 with bf16 dS^T over its first 32),
+// then dV [256,384), dK [384,512).  Pass 2: [0,128) S (bf16 dS over its first 64), [128,256) dP,
+// [256,384) dQ.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "internal.h"
 #include "qla_common.cuh"
@@ -73,10 +76,22 @@ __device__ __forceinline__ void store32_rows(uint32_t tcol, const uint32_t (&w)[
     }
 }
 
-__device__ __forceinline__ void named_sync_sm() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void named_sync_sm() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the softmax warps
 
 // ============================================================================ pass 1: dK, dV
 namespace kv {
+#ifdef VISTA_BWD_PROF  // cycles each role waits per barrier, averaged per CTA, printed by the last CTA
+__device__ unsigned long long g_bwd_prof[16];
+__device__ unsigned int g_bwd_done;
+#define PWAIT(i, x)                            \
+    do {                                       \
+        const long long _t0 = clock64();       \
+        x;                                     \
+        prof[i] += clock64() - _t0;            \
+    } while (0)
+#else
+#define PWAIT(i, x) x
+#endif
 // S <= 256 (RESIDENT): Q and dO of the unit stay in shared memory, [0, 64 KB) and [64, 128 KB).
 // S > 256 (STREAM): the (Q_g, dO_g) pairs of each 128-row block stream through a 2-stage ring of
 // 64 KB in the same 128 KB (L2-resident reloads per key tile).
@@ -91,14 +106,16 @@ constexpr int kTiles = kVOff + kTileB;               // 224 KB of 1024-B aligned
 // with the dynamic shared memory base 1024-B aligned this is exactly the 227 KB maximum.
 constexpr int kHead = 3072;
 constexpr int kSmem = kHead + kTiles;
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;  // 0 TMA, 1 MMA, 4-11 softmax (two column halves), 12-15 epilogue
 
 struct Bars {
     uint64_t q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty;
-    uint64_t sd_full, pds_ready, acc_full, acc_empty;
+    uint64_t s_full, dp_full, p_ready, ds_ready;
+    uint64_t dv_full, dv_empty, dk_full, dk_empty;
     uint64_t qg_full[2], qg_empty[2];
     uint32_t tmem_base;
 };
+static_assert(sizeof(Bars) <= 256, "barriers overlap the lse / D rows");
 
 struct Params {
     const int64_t* offsets;
@@ -112,16 +129,24 @@ struct Params {
     int q_per_user;
 };
 
-// S^T_g = K Q_g^T -> cols [0,128);  dP^T_g = V dO_g^T -> cols [128,256)   (all operands K-major)
+// One 128-query block g of a 128-key tile: S^T = K Q_g^T -> cols [0,128), dP^T = V dO_g^T ->
+// [128,256) (SS, all operands K-major).  The softmax warpgroup of query half sg writes bf16 P^T of
+// its 64 queries over [64 sg, 64 sg + 32) (the start of the S^T columns it read itself), dS^T
+// likewise over [128 + 64 sg, ...); dV += P^T dO_g -> [256,384), dK += dS^T Q_g -> [384,512) (A from
+// TMEM: K steps 0-3 at columns 0-31, 4-7 at 64-95; B MN-major).
 template <int KS>
-__device__ __forceinline__ void issue_sd(uint32_t tmem, uint32_t base, uint32_t qa, uint32_t ga) {
+__device__ __forceinline__ void issue_s(uint32_t tmem, uint32_t base, uint32_t qa) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 0);
-    const uint32_t ka = base + kKOff + KS * kTileB, va = base + kVOff;
+    const uint32_t ka = base + kKOff + KS * kTileB;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
         ptx::mma_ss_w(tmem, ptx::sdesc_sw128(ka + off, 16, 1024), ptx::sdesc_sw128(qa + off, 16, 1024), id, kk > 0);
     }
+}
+__device__ __forceinline__ void issue_dp(uint32_t tmem, uint32_t base, uint32_t ga) {
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 0);
+    const uint32_t va = base + kVOff;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
@@ -129,17 +154,20 @@ __device__ __forceinline__ void issue_sd(uint32_t tmem, uint32_t base, uint32_t 
                       kk > 0);
     }
 }
-// dV += P^T_g dO_g -> cols [256,384);  dK += dS^T_g Q_g -> cols [384,512)   (A from TMEM, B MN-major)
-__device__ __forceinline__ void issue_vk(uint32_t tmem, uint32_t qa, uint32_t ga, int g) {
+// acc: accumulate onto the tile's earlier blocks
+__device__ __forceinline__ void issue_dv(uint32_t tmem, uint32_t ga, bool acc) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
-        ptx::mma_ts_w(tmem + 256, tmem + kk * 8, ptx::sdesc_sw128(ga + kk * 2048, kHalf, 1024), id,
-                      (g > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_ts_w(tmem + 256, tmem + kk * 8 + (kk >> 2) * 32, ptx::sdesc_sw128(ga + kk * 2048, kHalf, 1024), id,
+                      (acc || kk > 0) ? 1u : 0u);
+}
+__device__ __forceinline__ void issue_dk(uint32_t tmem, uint32_t qa, bool acc) {
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
-        ptx::mma_ts_w(tmem + 384, tmem + 128 + kk * 8, ptx::sdesc_sw128(qa + kk * 2048, kHalf, 1024), id,
-                      (g > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_ts_w(tmem + 384, tmem + 128 + kk * 8 + (kk >> 2) * 32, ptx::sdesc_sw128(qa + kk * 2048, kHalf, 1024),
+                      id, (acc || kk > 0) ? 1u : 0u);
 }
 
 template <bool STREAM>
@@ -162,17 +190,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&bars->k_full[s], 1);
             ptx::mbar_init(&bars->k_empty[s], 1);
+            ptx::mbar_init(&bars->qg_full[s], 1);
+            ptx::mbar_init(&bars->qg_empty[s], 1);
         }
         ptx::mbar_init(&bars->v_full, 1);
         ptx::mbar_init(&bars->v_empty, 1);
-        ptx::mbar_init(&bars->sd_full, 1);
-        ptx::mbar_init(&bars->pds_ready, 128);
-        ptx::mbar_init(&bars->acc_full, 1);
-        ptx::mbar_init(&bars->acc_empty, 128);
-        for (int s2 = 0; s2 < 2; ++s2) {
-            ptx::mbar_init(&bars->qg_full[s2], 1);
-            ptx::mbar_init(&bars->qg_empty[s2], 1);
-        }
+        ptx::mbar_init(&bars->s_full, 1);
+        ptx::mbar_init(&bars->dp_full, 1);
+        ptx::mbar_init(&bars->p_ready, 256);
+        ptx::mbar_init(&bars->ds_ready, 256);
+        ptx::mbar_init(&bars->dv_full, 1);
+        ptx::mbar_init(&bars->dv_empty, 128);
+        ptx::mbar_init(&bars->dk_full, 1);
+        ptx::mbar_init(&bars->dk_empty, 128);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
@@ -180,6 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
+#ifdef VISTA_BWD_PROF
+    long long prof[16] = {};
+    const long long tstart = clock64();
+#endif
     ItemIter iter;
     iter.init(P.uts, P.B, HG, cta, num_ctas);
     Item it;
@@ -199,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (iter.next(it, P.uts, P.B, HG)) {
             const int h = it.hg;
             if constexpr (!STREAM) {
-                if (k > 0) ptx::mbar_wait(&bars->q_empty, (k - 1) & 1);
+                if (k > 0) PWAIT(3, ptx::mbar_wait(&bars->q_empty, (k - 1) & 1));
                 ptx::mbar_arrive_expect_tx_w(&bars->q_full, 2 * G * kTileB);
                 for (int g = 0; g < G; ++g)
                     for (int half = 0; half < 2; ++half) {
@@ -212,20 +246,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t row0 = P.offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
                 const int32_t row = (int32_t)(row0 + (int64_t)t * 128);
-                ptx::mbar_wait(&bars->k_empty[ks], kph ^ 1);
+                PWAIT(0, ptx::mbar_wait(&bars->k_empty[ks], kph ^ 1));
                 ptx::mbar_arrive_expect_tx_w(&bars->k_full[ks], kTileB);
                 for (int half = 0; half < 2; ++half)
                     ptx::tma_load_3d_w(smem + kKOff + ks * kTileB + half * kHalf, &mapK, &bars->k_full[ks], half * 64,
                                        h, row, pol);
                 if (++ks == 2) { ks = 0; kph ^= 1; }
-                ptx::mbar_wait(&bars->v_empty, vph ^ 1);
+                PWAIT(1, ptx::mbar_wait(&bars->v_empty, vph ^ 1));
                 vph ^= 1;
                 ptx::mbar_arrive_expect_tx_w(&bars->v_full, kTileB);
                 for (int half = 0; half < 2; ++half)
                     ptx::tma_load_3d_w(smem + kVOff + half * kHalf, &mapV, &bars->v_full, half * 64, h, row, pol);
+                // V has one stage: pull the next tile's V into L2 now so its load after this tile's
+                // last dP^T MMA is an L2 hit
+                if (t + 1 < it.t1)
+                    for (int half = 0; half < 2; ++half) ptx::tma_prefetch_l2_3d_w(&mapV, half * 64, h, row + 128);
                 if constexpr (STREAM) {  // (Q_g, dO_g) for every 128-row block of this tile
                     for (int g = 0; g < G; ++g) {
-                        ptx::mbar_wait(&bars->qg_empty[qs], qph ^ 1);
+                        PWAIT(2, ptx::mbar_wait(&bars->qg_empty[qs], qph ^ 1));
                         ptx::mbar_arrive_expect_tx_w(&bars->qg_full[qs], 2 * kTileB);
                         for (int half = 0; half < 2; ++half) {
                             ptx::tma_load_4d_w(smem + kQOff + qs * 2 * kTileB + half * kHalf, &mapQ, &bars->qg_full[qs],
@@ -240,23 +278,61 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++k;
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
+        // ---------------- MMA issuer, software-pipelined over the (tile, block) sequence:
+        //   S(n) dP(n) | P(n) ready: dV(n) S(n+1) | dS(n) ready: dK(n) dP(n+1) | ...
+        // so the tensor core computes the next block's S^T / dP^T while the softmax warps turn this
+        // block's into P^T / dS^T.  S(n+1) overwrites P^T(n) only after dV(n) (MMAs execute in order);
+        // dP(n+1) overwrites dS^T(n) only after dK(n).
         int ks = 0;
-        uint32_t kph = 0, vph = 0, pph = 0, aph = 0;
+        uint32_t kph = 0, vph = 0, pph = 0, dsph = 0, dvph = 0, dkph = 0;
         int qs = 0;
         uint32_t qph = 0;
         int k = 0;
+        bool pend = false, p_first = false, p_last = false;
+        uint32_t p_qa = 0, p_ga = 0;
+        int p_qs = 0;
+        // TS MMAs of the pending block: dV, then (optionally) the next block's S^T, then dK
+        auto pend_dv = [&]() {
+            PWAIT(4, ptx::mbar_wait(&bars->p_ready, pph));
+            pph ^= 1;
+            if (p_first) {  // the epilogue has drained dV of the previous tile
+                PWAIT(6, ptx::mbar_wait(&bars->dv_empty, dvph ^ 1));
+                dvph ^= 1;
+            }
+            ptx::tc_fence_after();
+            issue_dv(tmem, p_ga, !p_first);
+            if (p_last) ptx::mma_commit_w(&bars->dv_full);
+        };
+        auto pend_dk = [&]() {
+            PWAIT(5, ptx::mbar_wait(&bars->ds_ready, dsph));
+            dsph ^= 1;
+            if (p_first) {
+                PWAIT(6, ptx::mbar_wait(&bars->dk_empty, dkph ^ 1));
+                dkph ^= 1;
+            }
+            ptx::tc_fence_after();
+            issue_dk(tmem, p_qa, !p_first);
+            if (p_last) ptx::mma_commit_w(&bars->dk_full);
+            if constexpr (STREAM) ptx::mma_commit_w(&bars->qg_empty[p_qs]);  // Q_g, dO_g fully consumed
+            pend = false;
+        };
         while (iter.next(it, P.uts, P.B, HG)) {
-            if constexpr (!STREAM) ptx::mbar_wait(&bars->q_full, k & 1);
+            if constexpr (!STREAM) {
+                if (k > 0) {  // Q, dO of the previous unit are free once its last TS MMAs complete
+                    if (pend) { pend_dv(); pend_dk(); }
+                    ptx::mma_commit_w(&bars->q_empty);
+                }
+                PWAIT(7, ptx::mbar_wait(&bars->q_full, k & 1));
+            }
             for (int t = it.t0; t < it.t1; ++t) {
-                ptx::mbar_wait(&bars->k_full[ks], kph);
-                ptx::mbar_wait(&bars->v_full, vph);
-                vph ^= 1;
-                ptx::tc_fence_after();
+                // K (2 stages) is loaded well ahead; V (1 stage) only after the previous tile's last
+                // dP^T, so it is waited for just before this tile's first dP^T
+                PWAIT(7, ptx::mbar_wait(&bars->k_full[ks], kph));
+#pragma unroll 1
                 for (int g = 0; g < G; ++g) {
                     uint32_t qa, ga;
                     if constexpr (STREAM) {
-                        ptx::mbar_wait(&bars->qg_full[qs], qph);
+                        PWAIT(8, ptx::mbar_wait(&bars->qg_full[qs], qph));
                         ptx::tc_fence_after();
                         qa = base + kQOff + qs * 2 * kTileB;
                         ga = qa + kTileB;
@@ -264,120 +340,136 @@ __global__ void __launch_bounds__(kThreads, 1)
                         qa = base + kQOff + g * kTileB;
                         ga = base + kGOff + g * kTileB;
                     }
-                    if (ks == 0) issue_sd<0>(tmem, base, qa, ga); else issue_sd<1>(tmem, base, qa, ga);
-                    ptx::mma_commit_w(&bars->sd_full);
-                    if (g == G - 1) {
-                        ptx::mma_commit_w(&bars->k_empty[ks]);  // K only feeds S^T
-                        ptx::mma_commit_w(&bars->v_empty);      // V only feeds dP^T
-                    }
-                    ptx::mbar_wait(&bars->pds_ready, pph);
-                    pph ^= 1;
-                    if (g == 0) {  // the epilogue has drained dV, dK of the last tile (overlaps S^T, softmax)
-                        ptx::mbar_wait(&bars->acc_empty, aph ^ 1);
-                        aph ^= 1;
-                    }
+                    if (pend) pend_dv();
                     ptx::tc_fence_after();
-                    issue_vk(tmem, qa, ga, g);
-                    if constexpr (STREAM) {
-                        ptx::mma_commit_w(&bars->qg_empty[qs]);
-                        if (++qs == 2) { qs = 0; qph ^= 1; }
+                    if (ks == 0) issue_s<0>(tmem, base, qa); else issue_s<1>(tmem, base, qa);
+                    ptx::mma_commit_w(&bars->s_full);
+                    if (g == G - 1) ptx::mma_commit_w(&bars->k_empty[ks]);  // K only feeds S^T
+                    if (pend) pend_dk();
+                    if (g == 0) {
+                        PWAIT(12, ptx::mbar_wait(&bars->v_full, vph));
+                        vph ^= 1;
+                        ptx::tc_fence_after();
                     }
+                    issue_dp(tmem, base, ga);
+                    ptx::mma_commit_w(&bars->dp_full);
+                    if (g == G - 1) ptx::mma_commit_w(&bars->v_empty);  // V only feeds dP^T
+                    pend = true;
+                    p_qa = qa;
+                    p_ga = ga;
+                    p_first = g == 0;
+                    p_last = g == G - 1;
+                    p_qs = qs;
+                    if constexpr (STREAM)
+                        if (++qs == 2) { qs = 0; qph ^= 1; }
                 }
-                ptx::mma_commit_w(&bars->acc_full);
                 if (++ks == 2) { ks = 0; kph ^= 1; }
             }
-            if constexpr (!STREAM) ptx::mma_commit_w(&bars->q_empty);  // Q, dO free once the unit's GEMMs complete
             ++k;
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ---------------- column softmax: P^T = exp2(S^T scale log2e - lse_i log2e), dS^T = P^T (dP^T - D_i)
-        const int wq = warp % 4;
+        if (pend) { pend_dv(); pend_dk(); }
+    } else if (warp >= 4 && warp < 12) {
+        // ---------------- column softmax, in two phases per block:
+        //   P^T = exp2(S^T scale log2e - lse_i log2e)  (-> bf16 in TMEM, kept in registers)
+        //   dS^T = P^T (dP^T - D_i)
+        // warpgroup sg = 0, 1 handles query columns [64 sg, 64 sg + 64) of each block
+        const int wq = warp % 4, sg = (warp - 4) / 4, st = threadIdx.x - 128;  // st: 0..255
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
-        uint32_t sph = 0;
+        const uint32_t ts = tmem + lane_bits;
+        uint32_t sph = 0, dph = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             const size_t lrow = ((size_t)it.u * P.H + it.hg) * P.S;
             if constexpr (!STREAM) {  // the unit's lse * log2e and D rows into shared memory
                 named_sync_sm();      // the previous unit's chunks are done with them
-                for (int e = threadIdx.x - 128; e < P.S; e += 128) {
+                for (int e = st; e < P.S; e += 256) {
                     lsd[e] = __ldg(P.lse + lrow + e) * kLog2e;
                     lsd[256 + e] = __ldg(P.dd + lrow + e);
                 }
                 named_sync_sm();
             }
             for (int t = it.t0; t < it.t1; ++t) {
+#pragma unroll 1
                 for (int g = 0; g < G; ++g) {
                     if constexpr (STREAM) {  // this block's 128 lse * log2e and D values into shared memory
-                        const int e = threadIdx.x - 128;
+                        const int e = st & 127;
                         const float lv = __ldg(P.lse + lrow + g * 128 + e) * kLog2e;
                         const float dv = __ldg(P.dd + lrow + g * 128 + e);
                         named_sync_sm();
-                        lsd[g * 0 + e] = lv;
-                        lsd[256 + e] = dv;
+                        if (st < 128) lsd[e] = lv; else lsd[256 + e] = dv;
                         named_sync_sm();
                     }
-                    ptx::mbar_wait(&bars->sd_full, sph);
+                    const float* ls = lsd + (STREAM ? 0 : g * 128) + sg * 64;
+                    const float* dl = lsd + 256 + (STREAM ? 0 : g * 128) + sg * 64;
+                    const uint32_t tsp = ts + sg * 64, tsd = ts + 128 + sg * 64;  // this half's S^T / dP^T columns
+                    uint32_t pk[32];  // bf16x2 P^T of this warpgroup's 64 query columns
+                    PWAIT(9, ptx::mbar_wait(&bars->s_full, sph));
                     sph ^= 1;
                     ptx::tc_fence_after();
-#pragma unroll 1
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t sr[32], dr[32];
-                        ptx::tmem_ld32(tmem + lane_bits + c * 32, sr);
-                        ptx::tmem_ld32(tmem + lane_bits + 128 + c * 32, dr);
-                        float ls[32], dl[32];
-                        {  // shared-memory broadcast reads (the whole unit, or this block when streaming)
-                            const int col0 = (STREAM ? 0 : g * 128) + c * 32;
-                            const float4* lq = reinterpret_cast<const float4*>(lsd + col0);
-                            const float4* dq = reinterpret_cast<const float4*>(lsd + 256 + col0);
 #pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                const float4 a = lq[e], b = dq[e];
-                                ls[4 * e] = a.x;
-                                ls[4 * e + 1] = a.y;
-                                ls[4 * e + 2] = a.z;
-                                ls[4 * e + 3] = a.w;
-                                dl[4 * e] = b.x;
-                                dl[4 * e + 1] = b.y;
-                                dl[4 * e + 2] = b.z;
-                                dl[4 * e + 3] = b.w;
-                            }
-                        }
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t sr[32];
+                        ptx::tmem_ld32(tsp + c * 32, sr);
                         ptx::tmem_wait_ld();
                         ptx::reg_fence(sr);
-                        ptx::reg_fence(dr);
-                        uint32_t pw[16], sw[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[2 * j]), P.scale_log2, -ls[2 * j]));
-                            const float p1 =
-                                ptx::ex2(fmaf(__uint_as_float(sr[2 * j + 1]), P.scale_log2, -ls[2 * j + 1]));
-                            pw[j] = ptx::pack_bf16x2(p0, p1);
-                            sw[j] = ptx::pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - dl[2 * j]),
-                                                     p1 * (__uint_as_float(dr[2 * j + 1]) - dl[2 * j + 1]));
+                            const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + 2 * j);
+                            const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[2 * j]), P.scale_log2, -l2.x));
+                            const float p1 = ptx::ex2(fmaf(__uint_as_float(sr[2 * j + 1]), P.scale_log2, -l2.y));
+                            pk[16 * c + j] = ptx::pack_bf16x2(p0, p1);
                         }
-                        ptx::tmem_st16(tmem + lane_bits + c * 16, pw);
-                        ptx::tmem_st16(tmem + lane_bits + 128 + c * 16, sw);
+                        ptx::tmem_st16(tsp + c * 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16 * c));
                     }
                     ptx::tmem_wait_st();
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive(&bars->pds_ready);
+                    ptx::mbar_arrive(&bars->p_ready);
+                    PWAIT(10, ptx::mbar_wait(&bars->dp_full, dph));
+                    dph ^= 1;
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t dr[32];
+                        ptx::tmem_ld32(tsd + c * 32, dr);
+                        ptx::tmem_wait_ld();
+                        ptx::reg_fence(dr);
+                        uint32_t sw[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float2 d2 = *reinterpret_cast<const float2*>(dl + c * 32 + 2 * j);
+                            const uint32_t pw = pk[16 * c + j];
+                            const float p0 = __uint_as_float(pw << 16), p1 = __uint_as_float(pw & 0xffff0000u);
+                            sw[j] = ptx::pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - d2.x),
+                                                     p1 * (__uint_as_float(dr[2 * j + 1]) - d2.y));
+                        }
+                        ptx::tmem_st16(tsd + c * 16, sw);
+                    }
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars->ds_ready);
                 }
             }
         }
-    } else if (warp >= 8) {
-        // ---------------- epilogue: dV, dK (x scale) rows -> bf16
+    } else if (warp >= 12) {
+        // ---------------- epilogue: dV, then dK (x scale) rows -> bf16; each accumulator is released
+        // as soon as it is drained, so the next tile's dV MMAs need not wait for the dK drain
         const int wq = warp % 4;
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
-        uint32_t aph = 0;
+        uint32_t vph = 0, kph = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
-                ptx::mbar_wait(&bars->acc_full, aph);
-                aph ^= 1;
-                ptx::tc_fence_after();
                 const int64_t rem = L - (int64_t)t * 128;
                 const int valid = rem < 128 ? (int)rem : 128;
                 const size_t g0 = ((size_t)(P.offsets[it.u] + (int64_t)t * 128) * P.H + it.hg) * 128;
                 for (int m = 0; m < 2; ++m) {  // 0: dV, 1: dK
+                    if (m == 0) {
+                        PWAIT(11, ptx::mbar_wait(&bars->dv_full, vph));
+                        vph ^= 1;
+                    } else {
+                        PWAIT(11, ptx::mbar_wait(&bars->dk_full, kph));
+                        kph ^= 1;
+                    }
+                    ptx::tc_fence_after();
                     const float sc = m ? P.scale : 1.f;
                     __nv_bfloat16* dst = (m ? P.dk : P.dv) + g0;
                     for (int hh = 0; hh < 2; ++hh) {  // 64-column halves
@@ -394,15 +486,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         store32_rows(tc, w, dst + hh * 64, (size_t)P.H * 128, valid, wq, lane);
                     }
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(m ? &bars->dk_empty : &bars->dv_empty);
                 }
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&bars->acc_empty);
             }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+#ifdef VISTA_BWD_PROF
+    if (lane == 0 && (warp == 0 || warp == 1 || warp == 4 || warp == 12))
+        for (int i = 0; i < 15; ++i)
+            if (prof[i]) atomicAdd(&g_bwd_prof[i], (unsigned long long)prof[i]);
+    if (threadIdx.x == 0) {
+        atomicAdd(&g_bwd_prof[15], (unsigned long long)(clock64() - tstart));
+        __threadfence();
+        if (atomicAdd(&g_bwd_done, 1u) == gridDim.x - 1) {
+            __threadfence();
+            const char* nm[16] = {"k_empty", "v_empty",  "qg_empty", "q_empty", "p_ready", "ds_ready",
+                                  "acc_empty", "k_full",  "qg_full", "s_full",  "dp_full", "acc_full",
+                                  "v_full",   "-",        "-",       "total"};
+            for (int i = 0; i < 16; ++i)
+                printf("bwdprof %-10s %12.0f\n", nm[i], (double)atomicExch(&g_bwd_prof[i], 0ull) / gridDim.x);
+            g_bwd_done = 0;
+        }
+    }
+#endif
 }
 }  // namespace kv
 

@@ -521,11 +521,11 @@ namespace dq {
 constexpr int kQOff = 0, kGOff = kTileB, kKOff = 2 * kTileB, kVOff = kKOff + 2 * kTileB;
 constexpr int kBarOff = kVOff + 2 * kTileB;
 constexpr int kSmem = kBarOff + 256 + 1024;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 0 TMA, 1 MMA, 4-11 row softmax (two key halves) + dQ epilogue
 
 struct Bars {
     uint64_t q_full, q_empty, k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t sd_full, ds_ready, dq_full, dq_empty;
+    uint64_t s_full, dp_full, p_ready, ds_ready, dq_full, dq_empty;
     uint32_t tmem_base;
 };
 
@@ -542,32 +542,36 @@ struct Params {
     int q_per_user;
 };
 
-template <int ST>
-__device__ __forceinline__ void issue_sd(uint32_t tmem, uint32_t base) {
-    // S = Q_g K^T -> [0,128);  dP = dO_g V^T -> [128,256)   (all K-major)
+// TMEM: S of key tile n in buffer n % 2 (cols [128 b, 128 b + 128); the softmax writes bf16 dS over
+// [128 b + 64 sg, 128 b + 64 sg + 32) for key half sg), dP [256,384), dQ [384,512).
+// S = Q_g K^T -> buffer b;  dP = dO_g V^T -> [256,384)   (SS, all K-major)
+__device__ __forceinline__ void issue_s(uint32_t ts, uint32_t base, int st) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 0);
-    const uint32_t ka = base + kKOff + ST * kTileB, va = base + kVOff + ST * kTileB;
+    const uint32_t ka = base + kKOff + st * kTileB;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-        ptx::mma_ss_w(tmem, ptx::sdesc_sw128(base + kQOff + off, 16, 1024), ptx::sdesc_sw128(ka + off, 16, 1024), id,
+        ptx::mma_ss_w(ts, ptx::sdesc_sw128(base + kQOff + off, 16, 1024), ptx::sdesc_sw128(ka + off, 16, 1024), id,
                       kk > 0);
     }
+}
+__device__ __forceinline__ void issue_dp(uint32_t tmem, uint32_t base, int st) {
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 0);
+    const uint32_t va = base + kVOff + st * kTileB;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-        ptx::mma_ss_w(tmem + 128, ptx::sdesc_sw128(base + kGOff + off, 16, 1024), ptx::sdesc_sw128(va + off, 16, 1024),
+        ptx::mma_ss_w(tmem + 256, ptx::sdesc_sw128(base + kGOff + off, 16, 1024), ptx::sdesc_sw128(va + off, 16, 1024),
                       id, kk > 0);
     }
 }
-template <int ST>
-__device__ __forceinline__ void issue_dq(uint32_t tmem, uint32_t base, bool acc) {
-    // dQ += dS K: A = dS (bf16, TMEM [0,64)), B = K tile MN-major [K = key][N = c]
+// dQ += dS K: A = dS (bf16 in buffer ts: K steps 0-3 at +0..31, 4-7 at +64..95), B = K tile MN-major
+__device__ __forceinline__ void issue_dq(uint32_t tmem, uint32_t ts, uint32_t base, int st, bool acc) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);
-    const uint32_t ka = base + kKOff + ST * kTileB;
+    const uint32_t ka = base + kKOff + st * kTileB;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
-        ptx::mma_ts_w(tmem + 256, tmem + kk * 8, ptx::sdesc_sw128(ka + kk * 2048, kHalf, 1024), id,
+        ptx::mma_ts_w(tmem + 384, ts + kk * 8 + (kk >> 2) * 32, ptx::sdesc_sw128(ka + kk * 2048, kHalf, 1024), id,
                       (acc || kk > 0) ? 1u : 0u);
 }
 
@@ -591,10 +595,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bars->v_full[s], 1);
             ptx::mbar_init(&bars->v_empty[s], 1);
         }
-        ptx::mbar_init(&bars->sd_full, 1);
-        ptx::mbar_init(&bars->ds_ready, 128);
+        ptx::mbar_init(&bars->s_full, 1);
+        ptx::mbar_init(&bars->dp_full, 1);
+        ptx::mbar_init(&bars->p_ready, 256);
+        ptx::mbar_init(&bars->ds_ready, 256);
         ptx::mbar_init(&bars->dq_full, 1);
-        ptx::mbar_init(&bars->dq_empty, 128);
+        ptx::mbar_init(&bars->dq_empty, 256);
         ptx::fence_mbar_init();
         int s0, s1;
         partial_slots(P.uts, P.B, HG, cta, num_ctas, s0, s1);
@@ -645,85 +651,133 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++k;
         }
     } else if (warp == 1) {
-        int st = 0;
-        uint32_t ph = 0, dph = 0, qeph = 0;
+        // ---------------- MMA issuer, software-pipelined over the key tiles n of all items:
+        //   S(n) dP(n) | P(n) ready: S(n+1) | dS(n) ready: dQ(n) dP(n+1) | ...
+        // S alternates between two TMEM buffers, so S(n+1) runs while the softmax computes P(n) -> dS(n);
+        // S(n+2) reuses dS(n)'s buffer only after dQ(n) (MMAs execute in order).
+        int st = 0, sb = 0;
+        uint32_t ph = 0, pph = 0, dsph = 0, qeph = 0;
         int k = 0;
+        bool pend = false, p_first = false, p_last = false;
+        int p_st = 0, p_sb = 0;
+        auto pend_dq = [&]() {
+            ptx::mbar_wait(&bars->ds_ready, dsph);
+            dsph ^= 1;
+            if (p_first) {  // dQ accumulator drained by the previous item's epilogue
+                ptx::mbar_wait(&bars->dq_empty, qeph ^ 1);
+                qeph ^= 1;
+            }
+            ptx::tc_fence_after();
+            issue_dq(tmem, tmem + p_sb * 128, base, p_st, !p_first);
+            ptx::mma_commit_w(&bars->k_empty[p_st]);  // K feeds S and dQ
+            if (p_last) ptx::mma_commit_w(&bars->dq_full);
+            pend = false;
+        };
         while (iter.next(it, P.uts, P.B, HG)) {
             ptx::mbar_wait(&bars->q_full, k & 1);
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->k_full[st], ph);
-                ptx::mbar_wait(&bars->v_full[st], ph);
-                ptx::tc_fence_after();
-                if (st == 0) issue_sd<0>(tmem, base); else issue_sd<1>(tmem, base);
-                ptx::mma_commit_w(&bars->sd_full);
-                ptx::mma_commit_w(&bars->v_empty[st]);
-                if (t + 1 == it.t1) ptx::mma_commit_w(&bars->q_empty);  // Q_g, dO_g feed only S, dP
-                ptx::mbar_wait(&bars->ds_ready, dph);
-                dph ^= 1;
-                if (t == it.t0) {  // dQ accumulator drained by the previous item's epilogue
-                    ptx::mbar_wait(&bars->dq_empty, qeph ^ 1);
-                    qeph ^= 1;
+                if (pend) {
+                    ptx::mbar_wait(&bars->p_ready, pph);
+                    pph ^= 1;
                 }
                 ptx::tc_fence_after();
-                if (st == 0) issue_dq<0>(tmem, base, t > it.t0); else issue_dq<1>(tmem, base, t > it.t0);
-                ptx::mma_commit_w(&bars->k_empty[st]);
+                issue_s(tmem + sb * 128, base, st);
+                ptx::mma_commit_w(&bars->s_full);
+                if (pend) pend_dq();
+                ptx::mbar_wait(&bars->v_full[st], ph);
+                ptx::tc_fence_after();
+                issue_dp(tmem, base, st);
+                ptx::mma_commit_w(&bars->dp_full);
+                ptx::mma_commit_w(&bars->v_empty[st]);                  // V only feeds dP
+                if (t + 1 == it.t1) ptx::mma_commit_w(&bars->q_empty);  // Q_g, dO_g feed only S, dP
+                pend = true;
+                p_first = t == it.t0;
+                p_last = t + 1 == it.t1;
+                p_st = st;
+                p_sb = sb;
+                sb ^= 1;
                 if (++st == 2) { st = 0; ph ^= 1; }
             }
-            ptx::mma_commit_w(&bars->dq_full);
             ++k;
         }
+        if (pend) {
+            ptx::mbar_wait(&bars->p_ready, pph);
+            pend_dq();
+        }
     } else if (warp >= 4) {
-        // ---------------- row softmax: P = exp2(S scale log2e - lse_i log2e), dS = P (dP - D_i); epilogue dQ
-        const int wq = warp % 4;
+        // ---------------- row softmax: P = exp2(S scale log2e - lse_i log2e), dS = P (dP - D_i); epilogue dQ.
+        // Warpgroup sg handles keys [64 sg, 64 sg + 64) of each tile and dQ columns [64 sg, 64 sg + 64).
+        const int wq = warp % 4, sg = (warp - 4) / 4;
         const int r = wq * 32 + lane;  // query row within the block = TMEM lane
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
-        uint32_t sph = 0, qph = 0;
+        uint32_t sph = 0, dph = 0, qph = 0;
+        int sb = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             const int h = it.hg / P.G, g = it.hg % P.G;
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
             const size_t li = ((size_t)it.u * P.H + h) * P.S + g * 128 + r;
             const float lse2 = __ldg(P.lse + li) * kLog2e, dd = __ldg(P.dd + li);
             for (int t = it.t0; t < it.t1; ++t) {
-                ptx::mbar_wait(&bars->sd_full, sph);
+                const int64_t remv = L - (int64_t)t * 128 - sg * 64;
+                const int valid = remv < 64 ? (int)remv : 64;  // keys of this half (may be <= 0)
+                const uint32_t tsb = tmem + lane_bits + sb * 128 + sg * 64, tdp = tmem + lane_bits + 256 + sg * 64;
+                uint32_t pk[32];
+                ptx::mbar_wait(&bars->s_full, sph);
                 sph ^= 1;
                 ptx::tc_fence_after();
-                const int64_t remv = L - (int64_t)t * 128;
-                const int valid = remv < 128 ? (int)remv : 128;
-#pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t sr[32], dr[32];
-                    ptx::tmem_ld32(tmem + lane_bits + c * 32, sr);
-                    ptx::tmem_ld32(tmem + lane_bits + 128 + c * 32, dr);
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t sr[32];
+                    ptx::tmem_ld32(tsb + c * 32, sr);
                     ptx::tmem_wait_ld();
                     ptx::reg_fence(sr);
-                    ptx::reg_fence(dr);
-                    uint32_t sw[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         const int col = c * 32 + 2 * j;
                         const float p0 = col < valid ? ptx::ex2(fmaf(__uint_as_float(sr[2 * j]), P.scale_log2, -lse2)) : 0.f;
                         const float p1 =
                             col + 1 < valid ? ptx::ex2(fmaf(__uint_as_float(sr[2 * j + 1]), P.scale_log2, -lse2)) : 0.f;
+                        pk[16 * c + j] = ptx::pack_bf16x2(p0, p1);
+                    }
+                }
+                ptx::tc_fence_before();  // S read: the buffer may take S(n+2) after dQ(n)
+                ptx::mbar_arrive(&bars->p_ready);
+                ptx::mbar_wait(&bars->dp_full, dph);
+                dph ^= 1;
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t dr[32];
+                    ptx::tmem_ld32(tdp + c * 32, dr);
+                    ptx::tmem_wait_ld();
+                    ptx::reg_fence(dr);
+                    uint32_t sw[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t pw = pk[16 * c + j];
+                        const float p0 = __uint_as_float(pw << 16), p1 = __uint_as_float(pw & 0xffff0000u);
                         sw[j] = ptx::pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - dd),
                                                  p1 * (__uint_as_float(dr[2 * j + 1]) - dd));
                     }
-                    ptx::tmem_st16(tmem + lane_bits + c * 16, sw);
+                    ptx::tmem_st16(tsb + c * 16, sw);
                 }
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&bars->ds_ready);
+                sb ^= 1;
             }
-            // epilogue: dQ rows x scale -> final [B,H,S,d] row or a partial slot
+            // epilogue: dQ rows x scale (this warpgroup's 64 columns) -> final [B,H,S,d] row or a slot
             ptx::mbar_wait(&bars->dq_full, qph);
             qph ^= 1;
             ptx::tc_fence_after();
-            float* dst = item_complete(it)
-                             ? P.dqbuf + ((size_t)(it.u * HG + it.hg) * 128 + r) * 128
-                             : P.slot_o + ((size_t)item_slot(it, cta) * 128 + r) * 128;
+            float* dst = (item_complete(it) ? P.dqbuf + ((size_t)(it.u * HG + it.hg) * 128 + r) * 128
+                                            : P.slot_o + ((size_t)item_slot(it, cta) * 128 + r) * 128) +
+                         sg * 64;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 uint32_t o[32];
-                ptx::tmem_ld32_sync(tmem + lane_bits + 256 + c * 32, o);
+                ptx::tmem_ld32_sync(tmem + lane_bits + 384 + sg * 64 + c * 32, o);
 #pragma unroll
                 for (int j = 0; j < 32; j += 4)
                     *reinterpret_cast<float4*>(dst + c * 32 + j) =

@@ -822,21 +822,44 @@ __global__ void softmax_bwd_d_kernel(const TO* __restrict__ out, const TO* __res
     if (lane == 0) dd[rrow] = s;
 }
 
-// dq (final): shared seeds [S,H,d] = sum_u dqbuf[u,h,i,:] (ascending u); per-user [B,S,H,d]
+// dq (final): shared seeds [S,H,d] = sum_u dqbuf[u,h,i,:] (ascending u); per-user [B,S,H,d].
+// Four columns per thread; the loads of 8 users are issued before their (in-order) additions.
 __global__ void softmax_bwd_dq_final_kernel(const float* __restrict__ dqbuf, int B, int S, int H, int per_user,
                                             float* __restrict__ dq) {
-    const int64_t n = per_user ? (int64_t)B * S * H * 128 : (int64_t)S * H * 128;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(e % 128);
-        const int h = (int)((e / 128) % H);
-        const int i = (int)((e / (128 * H)) % S);
+    const int64_t n4 = (per_user ? (int64_t)B * S * H * 128 : (int64_t)S * H * 128) / 4;
+    const size_t ustride = (size_t)H * S * 128 / 4;  // one user's rows, in float4
+    const float4* src = reinterpret_cast<const float4*>(dqbuf);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c4 = (int)(e % 32);
+        const int h = (int)((e / 32) % H);
+        const int i = (int)((e / (32 * H)) % S);
+        const size_t hi = ((size_t)h * S + i) * 32 + c4;  // within a user
         if (per_user) {
-            const int u = (int)(e / ((int64_t)128 * H * S));
-            dq[e] = dqbuf[(((size_t)u * H + h) * S + i) * 128 + c];
+            const int u = (int)(e / ((int64_t)32 * H * S));
+            reinterpret_cast<float4*>(dq)[e] = src[(size_t)u * ustride + hi];
         } else {
-            float s = 0.f;
-            for (int u = 0; u < B; ++u) s += dqbuf[(((size_t)u * H + h) * S + i) * 128 + c];
-            dq[e] = s;
+            float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+            int u = 0;
+            for (; u + 8 <= B; u += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (size_t)(u + j) * ustride + hi);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    s.x += v[j].x;
+                    s.y += v[j].y;
+                    s.z += v[j].z;
+                    s.w += v[j].w;
+                }
+            }
+            for (; u < B; ++u) {
+                const float4 v = __ldg(src + (size_t)u * ustride + hi);
+                s.x += v.x;
+                s.y += v.y;
+                s.z += v.z;
+                s.w += v.w;
+            }
+            reinterpret_cast<float4*>(dq)[e] = s;
         }
     }
 }
@@ -962,7 +985,7 @@ cudaError_t launch_softmax_bwd(const Problem& p, const void* out, const float* l
     {
         const bool per_user = p.q_user_stride != 0;
         const int64_t n = per_user ? (int64_t)p.B * p.S * p.H * 128 : (int64_t)p.S * p.H * 128;
-        softmax_bwd_dq_final_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, p.stream>>>(
+        softmax_bwd_dq_final_kernel<<<(unsigned)std::min<int64_t>((n / 4 + 255) / 256, 4096), 256, 0, p.stream>>>(
             dqbuf, p.B, p.S, p.H, per_user, dq_out);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         ++nl;

@@ -525,7 +525,8 @@ def test_qla_backward_per_user_seeds(cuda_lib):
                                                (128, 1, [10_000, 3, 640], False),
                                                (256, 1, [700, 129], True),
                                                (512, 1, [0, 1500, 129, 3], False),
-                                               (384, 2, [260, 1], True)])
+                                               (384, 2, [260, 1], True),
+                                               (128, 2, [50, 0, 131, 7, 256, 1, 90, 3, 129, 64, 1], False)])
 def test_softmax_backward_tcgen05(cuda_lib, S, H, lens, per_user):
     vista = cuda_lib
     d = 128

@@ -49,6 +49,7 @@ def _load():
         lib.vo_softmax.argtypes = [i64, i64, i64, i64, P, i64, P, P, P, f64, P, i64, P, P, i32]
         lib.vo_qla_state.argtypes = [i64, i64, i64, P, P, P, i32, P, i32]
         lib.vo_qla_finalize.argtypes = [i64, i64, i64, i64, P, i64, P, P, i32, i32, i32, P, i32]
+        lib.vo_qla_rows.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, P, i32]
         lib.vo_merge_lse.argtypes = [i64, i64, i64, P, P, P, P]
         lib.vo_merge_sum.argtypes = [i64, i64, P, P]
         lib.vo_quantize_rows_f32.argtypes = [i64, i64, P, P, P, P]
@@ -181,6 +182,32 @@ def qla_summarize(q, k, v, offsets, phi1="silu", phi2="silu", normalize=True, q_
     offsets = np.asarray(offsets, dtype=np.int64)
     z = qla_state(k, v, offsets, phi1, threads)
     return qla_finalize(q, z, np.diff(offsets), phi1, phi2, normalize, q_per_user, threads)
+
+
+def qla_rows(q_rows, row_offsets, k, v, offsets, phi1="silu", phi2="silu", normalize=True,
+             k_self=None, v_self=None, threads=0):
+    """QLA at per-user query rows (NEXT-3 history rows; NEXT-4 target rows with
+    the Delta self term): out[r] = phi1(q_r) phi2(Zbar_u) [+ (phi1(q_r) .
+    phi1(k_self_r)) v_self_r] for r in [row_offsets[u], row_offsets[u+1]).  Returns [R,H,d]."""
+    q_rows = _f32(q_rows)
+    row_offsets = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    offsets = np.asarray(offsets, dtype=np.int64)
+    z = qla_state(k, v, offsets, phi1, threads)
+    B, H, d, _ = z.shape
+    R = q_rows.shape[0]
+    out = np.empty((R, H, d), np.float64)
+    if R == 0:
+        return out
+    ks = vs = None
+    if k_self is not None:
+        ks, vs = _f32(k_self), _f32(v_self)
+    n_items = np.ascontiguousarray(np.diff(offsets), dtype=np.int64)
+    rc = _load().vo_qla_rows(B, H, d, _ptr(z), _ptr(n_items), _ptr(q_rows), _ptr(row_offsets),
+                             _ptr(ks) if ks is not None else None, _ptr(vs) if vs is not None else None,
+                             ACT[phi1], ACT[phi2], int(bool(normalize)), _ptr(out), int(threads))
+    if rc != 0:
+        raise ValueError("vo_qla_rows failed")
+    return out
 
 
 def act_prime(kind: str, x: float) -> float:

@@ -28,6 +28,9 @@
  *  Merges used only to test split invariants: LSE merge of softmax partials and plain sum of
  *  QLA states.
  *
+ *  NEXT-3 / NEXT-4: QLA at arbitrary per-user query rows (history rows of a deeper layer, or
+ *  target rows with the Delta self term), vo_qla_rows.
+ *
  *  NEXT-2 (training): the QLA backward (vo_qla_backward) by the chain rule through
  *  O = phi1(Q) phi2(Z / N), Z = phi1(K)^T V.
  *
@@ -197,6 +200,53 @@ int vo_qla_finalize(int64_t B, int64_t S, int64_t H, int64_t d, const float* q,
                 for (int64_t c1 = 0; c1 < d; ++c1) {
                     const double a = vo_act(phi1, (double)qi[c1]);
                     for (int64_t c2 = 0; c2 < d; ++c2) o[c2] += a * w[c1 * d + c2];
+                }
+            }
+        }
+        free(w);
+    }
+    return 0;
+}
+
+/*
+ * QLA at arbitrary per-user query rows (NEXT-3 / NEXT-4):
+ *   history rows  O[S] = phi(Q[S]) phi(phi(K[S])^T V[S])
+ *   target rows   O[T] = phi(Q[T]) phi(phi(K[S])^T V[S])
+ *                        + Delta(phi(Q[T]), phi(K[T])) V[T]
+ * with Delta(X, Y)_ij = sum_k X_ik Y_ik delta_ij, i.e. row r gains
+ * (phi1(q_r) . phi1(k_self_r)) v_self_r.  Rows r in [row_offsets[u], row_offsets[u+1]) belong to
+ * user u and use its state Zbar_u (as in vo_qla_finalize: Z / N_u when normalizing, DESIGN.md
+ * reading R10); the Delta term carries no 1/N (reading R20).  k_self = v_self = NULL: no Delta term.
+ * q_rows, k_self, v_self: [R, H, d]; z: [B, H, d, d]; out: [R, H, d].
+ */
+int vo_qla_rows(int64_t B, int64_t H, int64_t d, const double* z, const int64_t* n_items,
+                const float* q_rows, const int64_t* row_offsets, const float* k_self,
+                const float* v_self, int phi1, int phi2, int normalize, double* out, int threads) {
+    if (B < 0 || H < 1 || d < 1) return -1;
+    set_threads(threads);
+#pragma omp parallel
+    {
+        double* w = (double*)malloc((size_t)(d * d) * sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < B * H; ++t) {
+            const int64_t u = t / H, h = t % H;
+            const double* zu = z + t * d * d;
+            const double inv = (normalize && n_items[u] > 0) ? 1.0 / (double)n_items[u] : 1.0;
+            for (int64_t e = 0; e < d * d; ++e) w[e] = vo_act(phi2, zu[e] * inv);
+            for (int64_t r = row_offsets[u]; r < row_offsets[u + 1]; ++r) {
+                const float* qr = q_rows + (r * H + h) * d;
+                double* o = out + (r * H + h) * d;
+                for (int64_t c2 = 0; c2 < d; ++c2) o[c2] = 0.0;
+                for (int64_t c1 = 0; c1 < d; ++c1) {
+                    const double a = vo_act(phi1, (double)qr[c1]);
+                    for (int64_t c2 = 0; c2 < d; ++c2) o[c2] += a * w[c1 * d + c2];
+                }
+                if (k_self) {
+                    const float* kr = k_self + (r * H + h) * d;
+                    const float* vr = v_self + (r * H + h) * d;
+                    double dot = 0.0;
+                    for (int64_t c = 0; c < d; ++c) dot += vo_act(phi1, (double)qr[c]) * vo_act(phi1, (double)kr[c]);
+                    for (int64_t c = 0; c < d; ++c) o[c] += dot * (double)vr[c];
                 }
             }
         }

@@ -194,6 +194,32 @@ vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, cons
                                    void* dk, void* dv, void* workspace, size_t workspace_bytes,
                                    void* stream);
 
+/*
+ * QLA at arbitrary per-user query rows (NEXT-3 / NEXT-4; desc->attn must be VISTA_QLA):
+ *   history rows (a deeper summarizer layer)  O[S] = phi(Q[S]) phi(phi(K[S])^T V[S])
+ *   target rows (stage 2)  O[T] = phi(Q[T]) phi(phi(K[S])^T V[S]) + Delta(phi(Q[T]), phi(K[T])) V[T]
+ *                          with Delta(X, Y)_ij = sum_k X_ik Y_ik delta_ij
+ * Row r of user u (r in [row_offsets[u], row_offsets[u+1])) gets
+ *   out[r,h,:] = phi1(q_rows[r,h,:]) phi2(Z_uh / N_u)  [+ (phi1(q_r) . phi1(k_self_r)) v_self_r]
+ * where Z_uh = sum_j phi1(k_j)^T v_j over the user's history [offsets[u], offsets[u+1]) and N_u its
+ * length when desc->qla_normalize (reading R10; the Delta term carries no 1/N, R20).
+ *   k, v        [total_len, H, d] (in_dtype), history; offsets int64 [B+1] as for summarize.
+ *   q_rows      [total_rows, H, d] (in_dtype); row_offsets int64 [B+1] on the device, row_offsets[0]
+ *               = 0, non-decreasing, row_offsets[B] = total_rows (a precondition, like offsets).
+ *   k_self, v_self  [total_rows, H, d] (in_dtype), both NULL for no Delta term (history rows).
+ *   out         [total_rows, H, d] in out_dtype.  desc->num_summary and q_user_stride are unused.
+ * Users without history have Z = 0 (out = phi1(q) phi2(0) [+ Delta]).  tcgen05 path for bf16, d =
+ * 128; CUDA cores otherwise.  Workspace: at least vista_qla_rows_workspace_size bytes, caller-owned.
+ * All pointers 16-byte aligned (VISTA_ERR_MISALIGNED).  Asynchronous on stream; deterministic.
+ */
+vista_status_t vista_qla_rows_workspace_size(const vista_desc_t* desc, int64_t total_len,
+                                             int64_t total_rows, size_t* bytes);
+vista_status_t vista_qla_rows(const vista_desc_t* desc, const void* k, const void* v,
+                              const int64_t* offsets, int64_t total_len, const void* q_rows,
+                              const int64_t* row_offsets, int64_t total_rows, const void* k_self,
+                              const void* v_self, void* out, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
 /* Bytes of device workspace vista_summarize_merge needs for this descriptor (0 for softmax). */
 vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes);
 

@@ -27,7 +27,8 @@ __all__ = [
     "vista_quantize_rows_int8", "quantize_int8",
     "vista_summarize_prefix_workspace_size", "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
     "vista_summarize_bwd_workspace_size", "vista_summarize_bwd", "vista_summarize_fwd_int8",
-    "summarize", "summarize_partial", "summarize_merge", "summarize_bwd",
+    "vista_qla_rows_workspace_size", "vista_qla_rows",
+    "summarize", "summarize_partial", "summarize_merge", "summarize_bwd", "qla_rows",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
 
@@ -97,6 +98,8 @@ def load():
     lib.vista_summarize_bwd_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
     lib.vista_summarize_fwd_int8.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, sz, P]
     lib.vista_summarize_bwd.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, P, sz, P]
+    lib.vista_qla_rows_workspace_size.argtypes = [DP, i64, i64, ctypes.POINTER(sz)]
+    lib.vista_qla_rows.argtypes = [DP, P, P, P, i64, P, P, i64, P, P, P, P, sz, P]
     lib.vista_summarize_fwd_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_partial_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge_workspace_size.argtypes = [DP, ctypes.POINTER(sz)]
@@ -221,6 +224,21 @@ def vista_summarize_bwd(desc, q, k, v, offsets, total_len, out, lse, dout, dq, d
                                       _ptr(out), _ptr(lse), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv),
                                       _ptr(workspace), int(workspace_bytes), _stream(stream)),
            "vista_summarize_bwd")
+
+
+def vista_qla_rows_workspace_size(desc, total_len, total_rows) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load().vista_qla_rows_workspace_size(ctypes.byref(desc), int(total_len), int(total_rows), ctypes.byref(n)),
+           "vista_qla_rows_workspace_size")
+    return n.value
+
+
+def vista_qla_rows(desc, k, v, offsets, total_len, q_rows, row_offsets, total_rows, k_self, v_self, out, workspace,
+                   workspace_bytes, stream=None):
+    _check(load().vista_qla_rows(ctypes.byref(desc), _ptr(k), _ptr(v), _ptr(offsets), int(total_len), _ptr(q_rows),
+                                 _ptr(row_offsets), int(total_rows), _ptr(k_self), _ptr(v_self), _ptr(out),
+                                 _ptr(workspace), int(workspace_bytes), _stream(stream)),
+           "vista_qla_rows")
 
 
 def vista_summarize_merge_workspace_size(desc: Desc) -> int:
@@ -372,6 +390,30 @@ def summarize_bwd(q, k, v, offsets, total_len, dout, *, attn=QLA, phi1="silu", p
         torch.empty(max(need, 16), dtype=torch.uint8, device=q.device)
     vista_summarize_bwd(desc, q, k, v, offsets, total_len, out, lse, dout, dq, dk, dv, ws, ws.numel(), stream)
     return dq, dk, dv
+
+
+def qla_rows(k, v, offsets, total_len, q_rows, row_offsets, total_rows=None, *, k_self=None, v_self=None,
+             phi1="silu", phi2="silu", normalize=True, out_dtype=None, workspace=None, stream=None):
+    """QLA at per-user query rows (NEXT-3 / NEXT-4): out [R,H,d] with out[r] = phi1(q_r) phi2(Z_u / N_u)
+    (+ (phi1(q_r) . phi1(k_self_r)) v_self_r when k_self, v_self are given: the target rows' Delta
+    term).  Rows [row_offsets[u], row_offsets[u+1]) belong to user u; Z_u is its history's state."""
+    import torch
+    if total_len is None:
+        total_len = k.shape[0]
+    if total_rows is None:
+        total_rows = q_rows.shape[0]
+    B = offsets.numel() - 1
+    H, d = q_rows.shape[-2:]
+    desc = make_desc(B, 1, H, d, in_dtype=_dtype_code(q_rows), out_dtype=out_dtype, attn=QLA, phi1=phi1, phi2=phi2,
+                     normalize=normalize)
+    odt = torch.bfloat16 if desc.out_dtype == BF16 else torch.float32
+    out = torch.empty((q_rows.shape[0], H, d), dtype=odt, device=q_rows.device)
+    need = vista_qla_rows_workspace_size(desc, total_len, total_rows)
+    ws = workspace if workspace is not None and workspace.numel() >= need else \
+        torch.empty(max(need, 16), dtype=torch.uint8, device=q_rows.device)
+    vista_qla_rows(desc, k, v, offsets, total_len, q_rows, row_offsets, total_rows, k_self, v_self, out, ws,
+                   ws.numel(), stream)
+    return out
 
 
 def summarize_merge(part_o, part_lse, *, q, attn=SOFTMAX, user_len=None, scale=None, phi1="silu",

@@ -165,6 +165,12 @@ __global__ void __launch_bounds__(128) sm100_qla_finalize_kernel(const uint8_t* 
 
 }  // namespace
 
+// W_u operands for the rows path (sm100_qla_rows.cu): W = phi2(Z / N_u) from one state [B,H,d,d]
+cudaError_t launch_qla_prep_w(const Problem& p, const float* z, uint8_t* wbuf) {
+    qla_prep_w_kernel<<<p.B * p.H * 4, 256, 0, p.stream>>>(z, 1, 0, p.offsets, nullptr, p.H, p.phi2, p.normalize, wbuf);
+    return cudaGetLastError();
+}
+
 size_t sm100_qla_finalize_workspace(const Problem& p) {
     const int nblk = (p.S + 127) / 128;
     const size_t bq = p.q_user_stride ? (size_t)p.B : 1;

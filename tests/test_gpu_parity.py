@@ -600,3 +600,62 @@ def test_int8_export_fused_equals_separate(cuda_lib, S, H, out_bf16, attn):
     rc, rs, rz = oracle.quantize_rows_int8(out.float().cpu().numpy().reshape(-1, d))
     assert np.array_equal(codes.cpu().numpy().reshape(-1, d), rc)
     assert np.array_equal(sc.cpu().numpy().reshape(-1), rs) and np.array_equal(zp.cpu().numpy().reshape(-1), rz)
+
+
+# ----------------------------------------------------------------------------- QLA at per-user rows (NEXT-3/4)
+def _rows_case(lens, rows, H, d, dtype, seed, delta):
+    rng = np.random.default_rng(seed)
+    _, k, v, off = synth.make_batch(lens, 1, H, d, seed=seed)
+    roff = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    R = int(roff[-1])
+    q = ((rng.integers(-128, 128, size=(R, H, d)) / 64.0)).astype(np.float32)
+    ks = vs = None
+    if delta:
+        ks = ((rng.integers(-128, 128, size=(R, H, d)) / 64.0)).astype(np.float32)
+        vs = ((rng.integers(-128, 128, size=(R, H, d)) / 64.0)).astype(np.float32)
+    return q, roff, k, v, off, ks, vs
+
+
+def _rows_check(vista, lens, rows, H, d, dtype, seed, delta, phi1, phi2, normalize, out_dtype, tol):
+    q, roff, k, v, off, ks, vs = _rows_case(lens, rows, H, d, dtype, seed, delta)
+    dev = lambda x: None if x is None else to_dev(x, dtype)  # noqa: E731
+    out = vista.qla_rows(dev(k), dev(v), torch.from_numpy(off).cuda(), int(off[-1]), dev(q),
+                         torch.from_numpy(roff).cuda(), int(roff[-1]), k_self=dev(ks), v_self=dev(vs), phi1=phi1,
+                         phi2=phi2, normalize=normalize, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    ref = oracle.qla_rows(q, roff, k, v, off, phi1, phi2, normalize, k_self=ks, v_self=vs)
+    g = out.float().cpu().numpy()
+    for u in range(len(lens)):
+        a, b = roff[u], roff[u + 1]
+        for h in range(H):
+            if b > a:
+                e = block_err(g[a:b, h], ref[a:b, h])
+                assert e <= tol, f"user {u} head {h} ({phi1},{phi2},{normalize},delta={delta}): {e:.3g}"
+
+
+@pytest.mark.parametrize("phi1,phi2,normalize,delta", [("silu", "silu", True, False), ("silu", "silu", True, True),
+                                                       ("shifted_elu", "identity", False, True),
+                                                       ("identity", "shifted_elu", True, False)])
+def test_qla_rows_tcgen05(cuda_lib, phi1, phi2, normalize, delta):
+    """History rows (no Delta) and target rows (Delta) against the oracle: ragged rows per user
+    (empty, 1, tile tails, several tiles), users without history, bf16 and f32 out."""
+    vista = cuda_lib
+    lens = [300, 0, 129, 2049, 5, 1]
+    rows = [130, 3, 0, 257, 1, 128]
+    for out_dtype in (vista.BF16, vista.F32):
+        _rows_check(vista, lens, rows, 2, 128, "bf16", 61, delta, phi1, phi2, normalize, out_dtype, 2e-2)
+
+
+def test_qla_rows_history_rows_are_the_histories(cuda_lib):
+    """NEXT-3 form: every history item as a query row of its own user (rows = offsets), many units
+    per CTA so the stream-K ranges split users."""
+    vista = cuda_lib
+    lens = [5000, 1, 0, 777, 12_000]
+    _rows_check(vista, lens, lens, 1, 128, "bf16", 62, False, "silu", "silu", True, vista.BF16, 2e-2)
+
+
+@pytest.mark.parametrize("d,dtype", [(32, "f32"), (64, "bf16"), (128, "f32")])
+def test_qla_rows_simt(cuda_lib, d, dtype):
+    vista = cuda_lib
+    tol = 1e-4 if dtype == "f32" else 2e-2
+    _rows_check(vista, [40, 0, 3], [5, 2, 7], 2, d, dtype, 63, True, "silu", "silu", True, None, tol)

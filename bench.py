@@ -29,6 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "history items summarized/sec (S=256,d=128) + % bf16 tensor peak, 1/2/4/8 GPU"
+TARGETS_PER_USER = 256  # --qla-rows target: candidate rows per user (NEXT-4)
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 
 
@@ -43,6 +44,9 @@ def parse():
     ap.add_argument("--mode", default=None, choices=["by_user", "by_length", "flat"],
                     help="multi-GPU partitioner (default per config: c2/c3 by_user, c4 by_length, c5 flat)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--qla-rows", choices=["history", "target"], default=None,
+                    help="NEXT-3/4 (QLA): the step is vista_qla_rows -- every history item as a query row of its "
+                         "own user (history), or 256 target rows per user with the Delta self term (target)")
     ap.add_argument("--backward", action="store_true",
                     help="NEXT-2: the step is the QLA backward (vista_summarize_bwd: Z recompute, dQ, dK, dV)")
     ap.add_argument("--export-int8", action="store_true",
@@ -144,10 +148,13 @@ def run_own(args, rank, world, local_rank):
     cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
     if args.backward:
         wdesc += " backward (NEXT-2)"
+    if args.qla_rows:
+        wdesc += (" QLA history rows (NEXT-3: every item a query row of its user)" if args.qla_rows == "history"
+                  else f" QLA target rows (NEXT-4: {TARGETS_PER_USER} targets per user, Delta self term)")
     attn = vista.SOFTMAX if args.attn == "softmax" else vista.QLA
     mode = args.mode or {"c2": "by_user", "c3": "by_user", "c4": "by_length", "c5": "flat"}[args.config]
-    if world == 1 and mode != "by_user":
-        mode = "by_user"  # one shard: the split-L paths degenerate to the plain forward
+    if (world == 1 or args.qla_rows) and mode != "by_user":
+        mode = "by_user"  # one shard: the split-L paths degenerate to the plain forward; rows: per-user batches
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
     B_all = len(lens)
@@ -199,6 +206,28 @@ def run_own(args, rank, world, local_rank):
                 vista.vista_summarize_bwd(desc, ins[0], ins[1], ins[2], ins[3], total, fwd_out, fwd_lse, ins[4], dq,
                                           dk, dv, bws, bws_bytes, sh)
                 return [dq, dk, dv]
+        if args.qla_rows:
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(4321 + rank)
+            grid = lambda shape: (torch.randint(-128, 128, shape, device=dev, generator=gen).float() / 64  # noqa: E731
+                                  ).to(torch.bfloat16)
+            if args.qla_rows == "history":
+                roff_t, n_rows = off_t, total
+                q_rows, k_self, v_self = grid((total, H, d)), None, None
+            else:
+                n_rows = TARGETS_PER_USER * B
+                roff_t = torch.arange(B + 1, dtype=torch.int64, device=dev) * TARGETS_PER_USER
+                q_rows, k_self, v_self = grid((n_rows, H, d)), grid((n_rows, H, d)), grid((n_rows, H, d))
+            rows_out = torch.empty((n_rows, H, d), dtype=torch.bfloat16, device=dev)
+            rws_bytes = vista.vista_qla_rows_workspace_size(desc, total, n_rows)
+            rws = torch.empty(max(rws_bytes, 16), dtype=torch.uint8, device=dev)
+            inputs = [K, V, off_t, q_rows, roff_t] + ([k_self, v_self] if k_self is not None else [])
+
+            def step(ins=inputs):
+                ks, vs = (ins[5], ins[6]) if len(ins) > 5 else (None, None)
+                vista.vista_qla_rows(desc, ins[0], ins[1], ins[2], total, ins[3], ins[4], n_rows, ks, vs, rows_out,
+                                     rws, rws_bytes, sh)
+                return [rows_out]
         items_per_step = world * total
         scaling = "weak"
         parallel = f"by_user x{world} (weak: a {args.config} batch per GPU, no data-path collective)"
@@ -350,6 +379,9 @@ def run_own(args, rank, world, local_rank):
     elif args.backward:  # softmax dK / dV kernel: S^T, dP^T, dV, dK GEMMs = 8 S d flop per item-head
         flops = 8.0 * S * d * H * total
         io_bytes = 2 * kv_bytes + 2 * B * S * H * d * 2
+    if args.qla_rows:  # rows kernel: q read, out written (bf16) [+ k_self, v_self read], W_u per unit
+        flops = 2.0 * d * d * H * n_rows
+        io_bytes = 4.0 * d * H * n_rows * (2 if args.qla_rows == "target" else 1) + B * H * d * d * 2
     tflops = flops / (kern_ms / 1e3) / 1e12
     gbs = io_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
@@ -368,7 +400,8 @@ def run_own(args, rank, world, local_rank):
     else:
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic, "peak_kind": f"{pk_kind} HBM copy",
-                "kernel": "sm100_qla_bwd_kv_kernel" if args.backward else "sm100_qla_state_kernel",
+                "kernel": ("sm100_qla_rows_kernel" if args.qla_rows else
+                           "sm100_qla_bwd_kv_kernel" if args.backward else "sm100_qla_state_kernel"),
                 "kernel_ms": round(kern_ms, 5),
                 "algorithmic_bytes_per_launch": io_bytes,
                 "tensor": {"achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
@@ -393,7 +426,7 @@ def run_own(args, rank, world, local_rank):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_sample(config, attn, seconds, rows=None, backward=False):
+def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=None):
     """Time the float64 oracle on whole users (all rows, all heads) of the rank-0 batch until
     ~`seconds` of CPU work; returns (items/s, cores, sample description, equivalent items, s)."""
     import numpy as np
@@ -412,7 +445,16 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False):
         rr = np.arange(a, b, dtype=np.int64)
         k, v = synth.make_kv(rr, np.full(b - a, u), H, d, seed=0)
         t0 = time.perf_counter()
-        if backward:  # backward (NEXT-2), dout grid values
+        if qla_rows:  # NEXT-3/4: QLA at per-user query rows
+            rng = np.random.default_rng(u)
+            n = (b - a) if qla_rows == "history" else TARGETS_PER_USER
+            qr = (rng.integers(-128, 128, size=(n, H, d)) / 64.0).astype(np.float32)
+            ks = vs = None
+            if qla_rows == "target":
+                ks = (rng.integers(-128, 128, size=(n, H, d)) / 64.0).astype(np.float32)
+                vs = (rng.integers(-128, 128, size=(n, H, d)) / 64.0).astype(np.float32)
+            oracle.qla_rows(qr, [0, n], k, v, [0, b - a], k_self=ks, v_self=vs, threads=cores)
+        elif backward:  # backward (NEXT-2), dout grid values
             g = (np.random.default_rng(u).integers(-128, 128, size=(1, S, H, d)) / 64.0).astype(np.float32)
             if attn == "softmax":
                 oracle.softmax_backward(q, k, v, [0, b - a], g, threads=cores)
@@ -431,6 +473,8 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False):
     sample = f"{users} whole user(s) of {config} ({rdesc}, all {H} heads, full histories), float64 C oracle, OpenMP"
     if backward:
         sample += f", {attn} backward (oracle.{attn}_backward)"
+    if qla_rows:
+        sample += f", QLA {qla_rows} rows (oracle.qla_rows)"
     return done_items / done_t, cores, sample, done_items, done_t
 
 
@@ -504,6 +548,10 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    if args.qla_rows:
+        args.attn = "qla"  # the rows path is QLA's
+        if args.backward or args.export_int8:
+            raise SystemExit("--qla-rows excludes --backward / --export-int8")
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -519,7 +567,7 @@ def main():
     res = run_own(args, rank, world, local_rank)
     if res is not None and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds, rows=None,
-                                               backward=args.backward)
+                                               backward=args.backward, qla_rows=args.qla_rows)
         res["cpu_baseline"] = {"value": v, "unit": "items/s", "cores": cores, "kind": "oracle",
                                "sample": sample, "seconds": round(t, 2)}
     elif res is not None:

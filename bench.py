@@ -387,7 +387,9 @@ def run_own(args, rank, world, local_rank):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(f"{args.config}_{args.attn}")
+        tkey = f"{args.config}_{args.attn}" + ("_bwd" if args.backward else "") + \
+            (f"_rows_{args.qla_rows}" if args.qla_rows else "")
+        traffic = json.load(open(tpath)).get(tkey)
     if attn == vista.SOFTMAX:
         roof = {"bound": "tensor", "achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": round(tflops / pk["bf16_tflops"], 4), "traffic": traffic,

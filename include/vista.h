@@ -174,8 +174,8 @@ vista_status_t vista_summarize_partial_prefix(const vista_desc_t* desc, const vo
  * Backward (NEXT-2, stage-1 training).
  * SOFTMAX: gradients of out_i = sum_j softmax_j(scale q_i . k_j) v_j, flash
  *   style from the forward's out and lse (both required): dV = P^T dO, dK = scale dS^T Q,
- *   dQ = scale dS K with dS = P . (dO V^T - rowsum(dO . out)).  This version: bf16, d = 128,
- *   S % 128 == 0, S <= 1024, bf16 dout (else VISTA_ERR_UNSUPPORTED).
+ *   dQ = scale dS K with dS = P . (dO V^T - rowsum(dO . out)).  tcgen05 kernels for bf16, d = 128,
+ *   S % 128 == 0, S <= 1024, bf16 dout; CUDA cores (fp32) for every other shape.
  * QLA: gradients of out = phi1(Q) phi2(Z / N_u), Z = sum_j phi1(k_j)^T v_j (the appendix derives the
  * phi2 = identity, no-1/N case; phi2 and 1/N are composed by the
  * chain rule, reading R19):

@@ -116,6 +116,10 @@ bool qla_bwd_uses_tc(const Problem& p);
 // softmax backward (NEXT-2): bf16, d = 128, S % 128 == 0, S <= 1024, bf16 dout
 bool softmax_bwd_supported(const Problem& p, bool dout_bf16);
 size_t softmax_bwd_workspace(const Problem& p);
+// CUDA-core softmax backward for the other shapes (softmax_bwd_simt.cu)
+size_t softmax_bwd_simt_workspace(const Problem& p);
+cudaError_t launch_softmax_bwd_simt(const Problem& p, bool dout_bf16, const void* out, const float* lse,
+                                    const void* dout, float* dq, void* dk, void* dv, char* ws);
 cudaError_t launch_softmax_bwd(const Problem& p, const void* out, const float* lse, const void* dout, float* dq,
                                void* dk, void* dv, char* ws, int* nlaunch, cudaEvent_t ev_a, cudaEvent_t ev_b);
 // phi1(Q) as bf16 128-row MMA operand blocks (qla_prep_q_kernel); qla_prep_q_bytes of space

@@ -481,8 +481,8 @@ vista_status_t vista_summarize_bwd_workspace_size(const vista_desc_t* desc, int6
     if (total_len < 0) return VISTA_ERR_INVALID;
     const Problem p = make_problem(desc, total_len);
     if (desc->attn == VISTA_SOFTMAX) {
-        if (!softmax_bwd_supported(p, desc->out_dtype == VISTA_BF16)) return VISTA_ERR_UNSUPPORTED;
-        *bytes = softmax_bwd_workspace(p);
+        *bytes = softmax_bwd_supported(p, desc->out_dtype == VISTA_BF16) ? softmax_bwd_workspace(p)
+                                                                         : softmax_bwd_simt_workspace(p);
         return VISTA_OK;
     }
     *bytes = plan_bwd(p).total;
@@ -508,16 +508,22 @@ vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, cons
         p.v = v;
         p.offsets = offsets;
         p.stream = reinterpret_cast<cudaStream_t>(stream);
-        if (!softmax_bwd_supported(p, desc->out_dtype == VISTA_BF16)) return VISTA_ERR_UNSUPPORTED;
+        const bool dout_bf16 = desc->out_dtype == VISTA_BF16;
+        const bool tc = softmax_bwd_supported(p, dout_bf16);
         if (p.B == 0) return VISTA_OK;
-        const size_t need = softmax_bwd_workspace(p);
+        const size_t need = tc ? softmax_bwd_workspace(p) : softmax_bwd_simt_workspace(p);
         if (!workspace || workspace_bytes < need) return VISTA_ERR_WORKSPACE;
         if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
         cudaEvent_t ev_a = g_ev_start, ev_b = g_ev_stop;
         g_ev_start = g_ev_stop = nullptr;
         int nl = 0;
-        cudaError_t e = launch_softmax_bwd(p, out, lse, dout, dq, dk, dv, reinterpret_cast<char*>(workspace), &nl,
-                                           ev_a, ev_b);
+        cudaError_t e;
+        if (tc) {
+            e = launch_softmax_bwd(p, out, lse, dout, dq, dk, dv, reinterpret_cast<char*>(workspace), &nl, ev_a, ev_b);
+        } else {  // CUDA cores: D, dK/dV (timed), dQ
+            e = launch_softmax_bwd_simt(p, dout_bf16, out, lse, dout, dq, dk, dv, reinterpret_cast<char*>(workspace));
+            nl = p.total_len > 0 ? 3 : 2;
+        }
         if (e != cudaSuccess) return cuda_fail(e);
         g_launches += (unsigned long long)nl;
         return VISTA_OK;

@@ -556,12 +556,41 @@ def test_softmax_backward_tcgen05(cuda_lib, S, H, lens, per_user):
             _bwd_check(dvn[a:b], rv[a:b], 2e-2, f"dv user {u}")
 
 
-def test_softmax_backward_unsupported_shape(cuda_lib):
+@pytest.mark.parametrize("S,H,d,dtype,out_dtype,per_user", [(200, 1, 128, "bf16", "bf16", False),
+                                                             (16, 2, 32, "f32", "f32", False),
+                                                             (64, 1, 64, "bf16", "f32", True),
+                                                             (1100, 1, 128, "bf16", "bf16", False)])
+def test_softmax_backward_simt(cuda_lib, S, H, d, dtype, out_dtype, per_user):
+    """Shapes outside the tcgen05 backward (S % 128 != 0, f32, d < 128, f32 dout, S > 1024): the
+    CUDA-core path, against the oracle."""
     vista = cuda_lib
-    d = vista.make_desc(2, 200, 1, 128)
-    with pytest.raises(vista.VistaError) as e:
-        vista.vista_summarize_bwd_workspace_size(d, 100)
-    assert "UNSUPPORTED" in str(e.value)
+    lens = [300, 0, 17, 129]
+    rng = np.random.default_rng(S + d)
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=43, tau=1)
+    if per_user:
+        q = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    g = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    qt, kt, vt = to_dev(q, dtype), to_dev(k, dtype), to_dev(v, dtype)
+    ot = torch.from_numpy(off).cuda()
+    odt = vista.BF16 if out_dtype == "bf16" else vista.F32
+    out, lse = vista.summarize(qt, kt, vt, ot, int(off[-1]), out_dtype=odt)
+    dq, dk, dv = vista.summarize_bwd(qt, kt, vt, ot, int(off[-1]), to_dev(g, out_dtype), attn=vista.SOFTMAX,
+                                     out=out, lse=lse)
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.softmax_backward(q, k, v, off, g, q_per_user=per_user)
+    tol = 1e-4 if (dtype == "f32" and out_dtype == "f32") else 2e-2
+    if per_user:
+        for u in range(len(lens)):
+            if lens[u]:
+                _bwd_check(dq[u], rq[u], tol, f"dq user {u}")
+    else:
+        _bwd_check(dq, rq, tol, "dq")
+    dkn, dvn = dk.float().cpu().numpy(), dv.float().cpu().numpy()
+    for u in range(len(lens)):
+        a, b = off[u], off[u + 1]
+        if b > a:
+            _bwd_check(dkn[a:b], rk[a:b], tol, f"dk user {u}")
+            _bwd_check(dvn[a:b], rv[a:b], tol, f"dv user {u}")
 
 
 # ----------------------------------------------------------------------------- NEXT-1 fused export

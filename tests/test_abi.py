@@ -81,6 +81,36 @@ def test_validation_errors_before_launch(lib):
     assert vista.vista_status_string(5) == "VISTA_ERR_WORKSPACE"
 
 
+def test_qla_rows_and_bwd_validation_before_launch(lib):
+    """NEXT-2/3/4 entry points: argument errors are returned before any launch."""
+    import paper_2510_22049_b200 as vista
+    dq = vista.make_desc(2, 1, 1, 128, attn=vista.QLA)
+    n = vista.vista_qla_rows_workspace_size(dq, 1000, 500)
+    assert n > 0
+    with pytest.raises(vista.VistaError) as e:  # rows need the QLA form
+        vista.vista_qla_rows_workspace_size(vista.make_desc(2, 1, 1, 128), 1000, 500)
+    assert e.value.status == 2
+    with pytest.raises(vista.VistaError) as e:  # negative row count
+        vista.vista_qla_rows_workspace_size(dq, 1000, -1)
+    assert e.value.status == 2
+    with pytest.raises(vista.VistaError) as e:  # NULL row offsets
+        vista.vista_qla_rows(dq, 4096, 4096, 4096, 10, 4096, 0, 5, 0, 0, 4096, 4096, n, stream=0)
+    assert e.value.status == 1
+    with pytest.raises(vista.VistaError) as e:  # k_self without v_self
+        vista.vista_qla_rows(dq, 4096, 4096, 4096, 10, 4096, 4096, 5, 4096, 0, 4096, 4096, n, stream=0)
+    assert e.value.status == 1
+    with pytest.raises(vista.VistaError) as e:  # misaligned q rows
+        vista.vista_qla_rows(dq, 4096, 4096, 4096, 10, 4104, 4096, 5, 0, 0, 4096, 4096, n, stream=0)
+    assert e.value.status == 4
+    with pytest.raises(vista.VistaError) as e:  # short workspace
+        vista.vista_qla_rows(dq, 4096, 4096, 4096, 10, 4096, 4096, 5, 0, 0, 4096, 4096, 1, stream=0)
+    assert e.value.status == 5
+    # the softmax backward takes every shape the forward takes (tcgen05 or CUDA cores)
+    for desc in (vista.make_desc(2, 200, 1, 128), vista.make_desc(2, 16, 1, 32, in_dtype=vista.F32),
+                 vista.make_desc(2, 256, 1, 128)):
+        assert vista.vista_summarize_bwd_workspace_size(desc, 100) > 0
+
+
 def test_dispatch_by_shape(lib):
     import paper_2510_22049_b200 as vista
     assert vista.vista_dispatch_name(vista.make_desc(8, 256, 4, 128)) == "sm100_softmax"

@@ -112,7 +112,8 @@ struct Bars {
     uint64_t q_full, q_empty, k_full[2], k_empty[2], v_full, v_empty;
     uint64_t s_full, dp_full, p_ready, ds_ready;
     uint64_t dv_full, dv_empty, dk_full, dk_empty;
-    uint64_t qg_full[2], qg_empty[2];
+    uint64_t qg_full[2], qg_empty[2];  // STREAM: Q_g of a ring stage
+    uint64_t go_full[2], go_empty[2];  // STREAM: dO_g of a ring stage
     uint32_t tmem_base;
 };
 static_assert(sizeof(Bars) <= 256, "barriers overlap the lse / D rows");
@@ -192,6 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bars->k_empty[s], 1);
             ptx::mbar_init(&bars->qg_full[s], 1);
             ptx::mbar_init(&bars->qg_empty[s], 1);
+            ptx::mbar_init(&bars->go_full[s], 1);
+            ptx::mbar_init(&bars->go_empty[s], 1);
         }
         ptx::mbar_init(&bars->v_full, 1);
         ptx::mbar_init(&bars->v_empty, 1);
@@ -261,16 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // last dP^T MMA is an L2 hit
                 if (t + 1 < it.t1)
                     for (int half = 0; half < 2; ++half) ptx::tma_prefetch_l2_3d_w(&mapV, half * 64, h, row + 128);
-                if constexpr (STREAM) {  // (Q_g, dO_g) for every 128-row block of this tile
-                    for (int g = 0; g < G; ++g) {
+                if constexpr (STREAM) {  // (Q_g, dO_g) for every 128-row block of this tile, each half
+                    for (int g = 0; g < G; ++g) {  // freed separately (Q_g after dK, dO_g after dV)
                         PWAIT(2, ptx::mbar_wait(&bars->qg_empty[qs], qph ^ 1));
-                        ptx::mbar_arrive_expect_tx_w(&bars->qg_full[qs], 2 * kTileB);
-                        for (int half = 0; half < 2; ++half) {
+                        ptx::mbar_arrive_expect_tx_w(&bars->qg_full[qs], kTileB);
+                        for (int half = 0; half < 2; ++half)
                             ptx::tma_load_4d_w(smem + kQOff + qs * 2 * kTileB + half * kHalf, &mapQ, &bars->qg_full[qs],
                                                half * 64, h, g * 128, P.q_per_user ? it.u : 0, pol_q);
+                        PWAIT(2, ptx::mbar_wait(&bars->go_empty[qs], qph ^ 1));
+                        ptx::mbar_arrive_expect_tx_w(&bars->go_full[qs], kTileB);
+                        for (int half = 0; half < 2; ++half)
                             ptx::tma_load_4d_w(smem + kQOff + qs * 2 * kTileB + kTileB + half * kHalf, &mapG,
-                                               &bars->qg_full[qs], half * 64, h, g * 128, it.u, pol_q);
-                        }
+                                               &bars->go_full[qs], half * 64, h, g * 128, it.u, pol_q);
                         if (++qs == 2) { qs = 0; qph ^= 1; }
                     }
                 }
@@ -302,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             issue_dv(tmem, p_ga, !p_first);
             if (p_last) ptx::mma_commit_w(&bars->dv_full);
+            if constexpr (STREAM) ptx::mma_commit_w(&bars->go_empty[p_qs]);  // dO_g consumed (dP, dV)
         };
         auto pend_dk = [&]() {
             PWAIT(5, ptx::mbar_wait(&bars->ds_ready, dsph));
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             issue_dk(tmem, p_qa, !p_first);
             if (p_last) ptx::mma_commit_w(&bars->dk_full);
-            if constexpr (STREAM) ptx::mma_commit_w(&bars->qg_empty[p_qs]);  // Q_g, dO_g fully consumed
+            if constexpr (STREAM) ptx::mma_commit_w(&bars->qg_empty[p_qs]);  // Q_g consumed (S, dK)
             pend = false;
         };
         while (iter.next(it, P.uts, P.B, HG)) {
@@ -349,6 +355,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (g == 0) {
                         PWAIT(12, ptx::mbar_wait(&bars->v_full, vph));
                         vph ^= 1;
+                        ptx::tc_fence_after();
+                    }
+                    if constexpr (STREAM) {
+                        PWAIT(8, ptx::mbar_wait(&bars->go_full[qs], qph));
                         ptx::tc_fence_after();
                     }
                     issue_dp(tmem, base, ga);

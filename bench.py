@@ -147,7 +147,7 @@ def run_own(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
     if args.backward:
-        wdesc += " backward (NEXT-2)"
+        wdesc += " backward (NEXT-2, from the forward's saved " + ("out, lse)" if args.attn == "softmax" else "state Z)")
     if args.qla_rows:
         wdesc += (" QLA history rows (NEXT-3: every item a query row of its user)" if args.qla_rows == "history"
                   else f" QLA target rows (NEXT-4: {TARGETS_PER_USER} targets per user, Delta self term)")
@@ -197,14 +197,21 @@ def run_own(args, rank, world, local_rank):
             bws = torch.empty(max(bws_bytes, 16), dtype=torch.uint8, device=dev)
             inputs = [q, K, V, off_t, dout]
 
-            fwd_out, fwd_lse = (None, None)
+            fwd_out, fwd_lse, fwd_z = (None, None, None)
             if attn == vista.SOFTMAX:  # the forward's out / lse (computed once, outside the timed region)
                 vista.vista_summarize_fwd(desc, q, K, V, off_t, total, out, lse, ws, ws_bytes, sh)
                 fwd_out, fwd_lse = out.clone(), lse.clone()
+            else:  # the forward's saved state Z (partial mode; computed once, outside the timed region)
+                fwd_z = torch.empty((B, H, d, d), dtype=torch.float32, device=dev)
+                vista.vista_summarize_partial(desc, q, K, V, off_t, total, fwd_z, None, ws, ws_bytes, sh)
 
             def step(ins=inputs):
-                vista.vista_summarize_bwd(desc, ins[0], ins[1], ins[2], ins[3], total, fwd_out, fwd_lse, ins[4], dq,
-                                          dk, dv, bws, bws_bytes, sh)
+                if fwd_z is not None:
+                    vista.vista_summarize_bwd_qla_saved(desc, ins[0], ins[1], ins[2], ins[3], total, fwd_z, ins[4],
+                                                        dq, dk, dv, bws, bws_bytes, sh)
+                else:
+                    vista.vista_summarize_bwd(desc, ins[0], ins[1], ins[2], ins[3], total, fwd_out, fwd_lse, ins[4],
+                                              dq, dk, dv, bws, bws_bytes, sh)
                 return [dq, dk, dv]
         if args.qla_rows:
             gen = torch.Generator(device=dev)

@@ -220,6 +220,18 @@ vista_status_t vista_qla_rows(const vista_desc_t* desc, const void* k, const voi
                               const void* v_self, void* out, void* workspace,
                               size_t workspace_bytes, void* stream);
 
+/*
+ * QLA backward from the forward's saved state (saves the Z recompute): z_saved = Z_u = sum_j
+ * phi1(k_j)^T v_j, float32 [B, H, d, d], not divided by N_u -- exactly what vista_summarize_partial
+ * returns for QLA on the same k, v, offsets.  Everything else as vista_summarize_bwd (QLA);
+ * desc->attn must be VISTA_QLA.  Workspace: vista_summarize_bwd_workspace_size bytes.
+ */
+vista_status_t vista_summarize_bwd_qla_saved(const vista_desc_t* desc, const void* q, const void* k,
+                                             const void* v, const int64_t* offsets, int64_t total_len,
+                                             const float* z_saved, const void* dout, float* dq,
+                                             void* dk, void* dv, void* workspace,
+                                             size_t workspace_bytes, void* stream);
+
 /* Bytes of device workspace vista_summarize_merge needs for this descriptor (0 for softmax). */
 vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes);
 

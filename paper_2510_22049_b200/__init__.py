@@ -27,7 +27,7 @@ __all__ = [
     "vista_quantize_rows_int8", "quantize_int8",
     "vista_summarize_prefix_workspace_size", "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
     "vista_summarize_bwd_workspace_size", "vista_summarize_bwd", "vista_summarize_fwd_int8",
-    "vista_qla_rows_workspace_size", "vista_qla_rows",
+    "vista_qla_rows_workspace_size", "vista_qla_rows", "vista_summarize_bwd_qla_saved",
     "summarize", "summarize_partial", "summarize_merge", "summarize_bwd", "qla_rows",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
@@ -98,6 +98,7 @@ def load():
     lib.vista_summarize_bwd_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
     lib.vista_summarize_fwd_int8.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, sz, P]
     lib.vista_summarize_bwd.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, P, sz, P]
+    lib.vista_summarize_bwd_qla_saved.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, sz, P]
     lib.vista_qla_rows_workspace_size.argtypes = [DP, i64, i64, ctypes.POINTER(sz)]
     lib.vista_qla_rows.argtypes = [DP, P, P, P, i64, P, P, i64, P, P, P, P, sz, P]
     lib.vista_summarize_fwd_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
@@ -224,6 +225,14 @@ def vista_summarize_bwd(desc, q, k, v, offsets, total_len, out, lse, dout, dq, d
                                       _ptr(out), _ptr(lse), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv),
                                       _ptr(workspace), int(workspace_bytes), _stream(stream)),
            "vista_summarize_bwd")
+
+
+def vista_summarize_bwd_qla_saved(desc, q, k, v, offsets, total_len, z_saved, dout, dq, dk, dv, workspace,
+                                  workspace_bytes, stream=None):
+    _check(load().vista_summarize_bwd_qla_saved(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                                                int(total_len), _ptr(z_saved), _ptr(dout), _ptr(dq), _ptr(dk),
+                                                _ptr(dv), _ptr(workspace), int(workspace_bytes), _stream(stream)),
+           "vista_summarize_bwd_qla_saved")
 
 
 def vista_qla_rows_workspace_size(desc, total_len, total_rows) -> int:
@@ -375,9 +384,11 @@ def summarize_partial(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=N
 
 
 def summarize_bwd(q, k, v, offsets, total_len, dout, *, attn=QLA, phi1="silu", phi2="silu", normalize=True,
-                  out=None, lse=None, workspace=None, stream=None):
+                  out=None, lse=None, z=None, workspace=None, stream=None):
     """Backward of summarize (NEXT-2): returns (dq, dk, dv).  dq float32 [S,H,d] (shared seeds,
-    summed over users) or [B,S,H,d]; dk, dv like k, v.  Softmax needs the forward's out and lse."""
+    summed over users) or [B,S,H,d]; dk, dv like k, v.  Softmax needs the forward's out and lse;
+    QLA may take the forward's saved state z ([B,H,d,d] f32 from summarize_partial) instead of
+    recomputing it."""
     import torch
     if total_len is None:
         total_len = k.shape[0]
@@ -388,7 +399,10 @@ def summarize_bwd(q, k, v, offsets, total_len, dout, *, attn=QLA, phi1="silu", p
     need = vista_summarize_bwd_workspace_size(desc, total_len)
     ws = workspace if workspace is not None and workspace.numel() >= need else \
         torch.empty(max(need, 16), dtype=torch.uint8, device=q.device)
-    vista_summarize_bwd(desc, q, k, v, offsets, total_len, out, lse, dout, dq, dk, dv, ws, ws.numel(), stream)
+    if attn == QLA and z is not None:
+        vista_summarize_bwd_qla_saved(desc, q, k, v, offsets, total_len, z, dout, dq, dk, dv, ws, ws.numel(), stream)
+    else:
+        vista_summarize_bwd(desc, q, k, v, offsets, total_len, out, lse, dout, dq, dk, dv, ws, ws.numel(), stream)
     return dq, dk, dv
 
 

@@ -489,6 +489,22 @@ vista_status_t vista_summarize_bwd_workspace_size(const vista_desc_t* desc, int6
     return VISTA_OK;
 }
 
+static vista_status_t qla_bwd(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                              const int64_t* offsets, int64_t total_len, const float* z_saved, const void* dout,
+                              float* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, void* stream);
+
+vista_status_t vista_summarize_bwd_qla_saved(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                             const int64_t* offsets, int64_t total_len, const float* z_saved,
+                                             const void* dout, float* dq, void* dk, void* dv, void* workspace,
+                                             size_t workspace_bytes, void* stream) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (desc->attn != VISTA_QLA) return VISTA_ERR_INVALID;
+    if (!z_saved) return VISTA_ERR_NULL;
+    if (!aligned16(z_saved)) return VISTA_ERR_MISALIGNED;
+    return qla_bwd(desc, q, k, v, offsets, total_len, z_saved, dout, dq, dk, dv, workspace, workspace_bytes, stream);
+}
+
 vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, const void* k, const void* v,
                                    const int64_t* offsets, int64_t total_len, const void* out, const float* lse,
                                    const void* dout, float* dq, void* dk, void* dv, void* workspace,
@@ -528,6 +544,14 @@ vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, cons
         g_launches += (unsigned long long)nl;
         return VISTA_OK;
     }
+    return qla_bwd(desc, q, k, v, offsets, total_len, nullptr, dout, dq, dk, dv, workspace, workspace_bytes, stream);
+}
+
+static vista_status_t qla_bwd(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                              const int64_t* offsets, int64_t total_len, const float* z_saved, const void* dout,
+                              float* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, void* stream) {
+    vista_status_t st = VISTA_OK;
+    if (total_len < 0) return VISTA_ERR_INVALID;
     if (!q || !offsets || !dout || !dq) return VISTA_ERR_NULL;
     if (total_len > 0 && (!k || !v || !dk || !dv)) return VISTA_ERR_NULL;
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dq) || !aligned16(dk) ||
@@ -544,17 +568,27 @@ vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, cons
     if (!workspace || workspace_bytes < b.total) return VISTA_ERR_WORKSPACE;
     if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
     char* ws = reinterpret_cast<char*>(workspace);
-    float* z = reinterpret_cast<float*>(ws + b.z_off);
+    const float* z = z_saved ? z_saved : reinterpret_cast<float*>(ws + b.z_off);
     float* dz = reinterpret_cast<float*>(ws + b.dz_off);
     const bool tc = qla_bwd_uses_tc(p);
     uint8_t* dz_op = tc ? reinterpret_cast<uint8_t*>(ws + b.dzop_off) : nullptr;
     float* dqu = p.q_user_stride == 0 ? reinterpret_cast<float*>(ws + b.dqu_off) : dq;
-    // 1. Z = sum_j phi1(k_j)^T v_j (the forward state kernel, partial mode).  The timing hook, if
-    //    armed, is kept for the dK / dV kernel (the dominant one of the backward).
+    // 1. Z = sum_j phi1(k_j)^T v_j (the forward state kernel, partial mode), unless the forward's
+    //    state was saved.  The timing hook, if armed, is kept for the dK / dV kernel (the dominant
+    //    one of the backward).  The tile starts of the dK / dV kernel come from this run too.
     cudaEvent_t ev_a = g_ev_start, ev_b = g_ev_stop;
     g_ev_start = g_ev_stop = nullptr;
-    st = run(desc, q, k, v, offsets, total_len, OutSpec{OUT_PARTIAL, 0, z, nullptr}, ws + b.sub_off,
-             b.z_off - b.sub_off, stream);
+    if (!z_saved) {
+        st = run(desc, q, k, v, offsets, total_len, OutSpec{OUT_PARTIAL, 0, const_cast<float*>(z), nullptr},
+                 ws + b.sub_off, b.z_off - b.sub_off, stream);
+    } else if (qla_bwd_uses_tc(p) && total_len > 0) {
+        const Workspace w = plan_workspace(p, true);
+        Problem pt = p;
+        pt.outs = OutSpec{OUT_PARTIAL, 0, nullptr, nullptr};
+        const cudaError_t e0 = launch_user_tiles(pt, reinterpret_cast<int64_t*>(ws + b.sub_off + w.uts_off), nullptr);
+        if (e0 != cudaSuccess) st = cuda_fail(e0);
+        else g_launches += 1;
+    }
     g_ev_start = ev_a;
     g_ev_stop = ev_b;
     if (st != VISTA_OK) return st;

@@ -481,6 +481,34 @@ def test_qla_backward_tcgen05(cuda_lib, phi1, phi2, normalize):
             _bwd_check(dvn[a:b], rv[a:b], 2e-2, f"dv user {u}")
 
 
+@pytest.mark.parametrize("d,dtype", [(128, "bf16"), (64, "f32")])
+def test_qla_backward_from_saved_state(cuda_lib, d, dtype):
+    """vista_summarize_bwd_qla_saved with the forward's partial state Z == the recomputing backward,
+    bit for bit (same kernels after the state), and both match the oracle."""
+    vista = cuda_lib
+    lens = [0, 129, 2049, 5, 300]
+    S, H = 256, 2
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=22, tau=1)
+    rng = np.random.default_rng(7)
+    g = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    qt, kt, vt, gt = to_dev(q, dtype), to_dev(k, dtype), to_dev(v, dtype), to_dev(g, dtype)
+    ot = torch.from_numpy(off).cuda()
+    z, _ = vista.summarize_partial(qt, kt, vt, ot, int(off[-1]), attn=vista.QLA)
+    a = vista.summarize_bwd(qt, kt, vt, ot, int(off[-1]), gt, z=z)
+    b = vista.summarize_bwd(qt, kt, vt, ot, int(off[-1]), gt)
+    torch.cuda.synchronize()
+    for x, y, what in zip(a, b, ("dq", "dk", "dv")):
+        assert torch.equal(x, y), what
+    rq, rk, rv = oracle.qla_backward(q, k, v, off, g, "silu", "silu", True)
+    tol = 1e-4 if dtype == "f32" else 2e-2
+    _bwd_check(a[0], rq, tol, "dq")
+    dkn = a[1].float().cpu().numpy()
+    for u in range(len(lens)):
+        lo, hi = off[u], off[u + 1]
+        if hi > lo:
+            _bwd_check(dkn[lo:hi], rk[lo:hi], tol, f"dk user {u}")
+
+
 @pytest.mark.parametrize("d,dtype", [(32, "f32"), (64, "bf16"), (128, "f32")])
 def test_qla_backward_simt(cuda_lib, d, dtype):
     vista = cuda_lib

@@ -716,3 +716,61 @@ def test_qla_rows_simt(cuda_lib, d, dtype):
     vista = cuda_lib
     tol = 1e-4 if dtype == "f32" else 2e-2
     _rows_check(vista, [40, 0, 3], [5, 2, 7], 2, d, dtype, 63, True, "silu", "silu", True, None, tol)
+
+
+# ----------------------------------------------------------------------------- full-size sampled (NEXT-2..4)
+def _c2_full():
+    cfg = synth.CONFIGS["c2"]
+    lens = synth.user_lengths("c2")
+    S, H, d = cfg["S"], cfg["H"], cfg["d"]
+    q, K, V, off = synth.make_batch(lens, S, H, d, backend="torch", device="cuda")
+    return lens, S, H, d, q, K, V, off
+
+
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_backward_c2_full_size_sampled_users(cuda_lib, attn):
+    """The backward at BASELINE config 2 size in the bench's launch configuration (softmax from the
+    forward's out / lse, QLA from the forward's saved state); dK, dV of three users against the
+    oracle run on those users alone (their gradients depend on their own history only)."""
+    vista = cuda_lib
+    lens, S, H, d, q, K, V, off = _c2_full()
+    ot = torch.from_numpy(off).cuda()
+    rng = np.random.default_rng(11)
+    g = ((rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0)).astype(np.float32)
+    gt = torch.from_numpy(g).cuda().to(torch.bfloat16)
+    if attn == "softmax":
+        out, lse = vista.summarize(q, K, V, ot, int(off[-1]), out_dtype=vista.BF16)
+        dq, dk, dv = vista.summarize_bwd(q, K, V, ot, int(off[-1]), gt, attn=vista.SOFTMAX, out=out, lse=lse)
+    else:
+        z, _ = vista.summarize_partial(q, K, V, ot, int(off[-1]), attn=vista.QLA)
+        dq, dk, dv = vista.summarize_bwd(q, K, V, ot, int(off[-1]), gt, z=z)
+    torch.cuda.synchronize()
+    qn = q.float().cpu().numpy()
+    for u in (0, 40, 63):
+        a, b = int(off[u]), int(off[u + 1])
+        kn, vn = K[a:b].float().cpu().numpy(), V[a:b].float().cpu().numpy()
+        if attn == "softmax":
+            _, rk, rv = oracle.softmax_backward(qn, kn, vn, [0, b - a], g[u:u + 1])
+        else:
+            _, rk, rv = oracle.qla_backward(qn, kn, vn, [0, b - a], g[u:u + 1])
+        _bwd_check(dk[a:b], rk, 2e-2, f"{attn} dk user {u}")
+        _bwd_check(dv[a:b], rv, 2e-2, f"{attn} dv user {u}")
+
+
+def test_qla_rows_c2_full_size_sampled_users(cuda_lib):
+    """QLA history rows (NEXT-3) at config 2 size, bench launch configuration; three users' rows."""
+    vista = cuda_lib
+    lens, S, H, d, q, K, V, off = _c2_full()
+    ot = torch.from_numpy(off).cuda()
+    rng = np.random.default_rng(12)
+    qr = ((rng.integers(-128, 128, size=(int(off[-1]), H, d)) / 64.0)).astype(np.float32)
+    out = vista.qla_rows(K, V, ot, int(off[-1]), torch.from_numpy(qr).cuda().to(torch.bfloat16), ot, int(off[-1]),
+                         out_dtype=vista.BF16)
+    torch.cuda.synchronize()
+    for u in (0, 40, 63):
+        a, b = int(off[u]), int(off[u + 1])
+        ref = oracle.qla_rows(qr[a:b], [0, b - a], K[a:b].float().cpu().numpy(), V[a:b].float().cpu().numpy(),
+                              [0, b - a])
+        gq = out[a:b].float().cpu().numpy()
+        for h in range(H):
+            assert block_err(gq[:, h], ref[:, h]) <= 2e-2, f"user {u} head {h}"

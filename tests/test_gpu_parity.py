@@ -774,3 +774,17 @@ def test_qla_rows_c2_full_size_sampled_users(cuda_lib):
         gq = out[a:b].float().cpu().numpy()
         for h in range(H):
             assert block_err(gq[:, h], ref[:, h]) <= 2e-2, f"user {u} head {h}"
+
+
+def test_qla_rows_edge_cases(cuda_lib):
+    """No history at all (Z = 0 for every user: out = phi1(q) phi2(0) + Delta), no rows at all, and
+    a single row."""
+    vista = cuda_lib
+    for phi2 in ("silu", "shifted_elu"):
+        _rows_check(vista, [0, 0, 0], [3, 0, 129], 2, 128, "bf16", 64, True, "silu", phi2, True, vista.F32, 2e-2)
+    _rows_check(vista, [70, 2], [0, 1], 1, 128, "bf16", 65, False, "silu", "silu", True, vista.BF16, 2e-2)
+    k = torch.zeros((5, 1, 128), dtype=torch.bfloat16, device="cuda")
+    off = torch.tensor([0, 5], dtype=torch.int64, device="cuda")
+    q = torch.zeros((0, 1, 128), dtype=torch.bfloat16, device="cuda")
+    out = vista.qla_rows(k, k, off, 5, q, torch.tensor([0, 0], dtype=torch.int64, device="cuda"), 0)
+    assert out.shape == (0, 1, 128)

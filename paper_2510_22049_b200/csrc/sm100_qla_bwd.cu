@@ -28,8 +28,14 @@ namespace {
 
 constexpr int kHalf = 128 * 128;       // one 64-column half of a 128 x 128 bf16 tile
 constexpr int kTile = 2 * kHalf;       // 32 KB
-constexpr int kStages = 3;
-constexpr int kStageBytes = 2 * kTile;  // K (-> phi1(K) in place), V
+#ifndef VISTA_QLA_BWD_KP
+#define VISTA_QLA_BWD_KP 1
+#endif
+// kKp: the transform also writes phi1'(K) (bf16) into a third tile of the stage, which the epilogue
+// reads from shared memory (2 stages); else 3 stages and the epilogue re-reads raw K through L2
+constexpr bool kKp = VISTA_QLA_BWD_KP;
+constexpr int kStages = kKp ? 2 : 3;
+constexpr int kStageBytes = (kKp ? 3 : 2) * kTile;  // K (-> phi1(K) in place), V [, phi1'(K)]
 constexpr int kDzOff = kStages * kStageBytes;
 constexpr int kBarOff = kDzOff + kTile;
 constexpr int kSmem = kBarOff + 256 + 1024;
@@ -94,7 +100,7 @@ __device__ __forceinline__ void xform_tile(uint32_t kbuf, int xt) {
         const uint32_t off = (uint32_t)(xt + i * kXform) * 16;
         const uint4 raw = lds128(kbuf + off);
         const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-        uint32_t ph[4];
+        uint32_t ph[4], pp[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const float lo = __uint_as_float(w[e] << 16), hi = __uint_as_float(w[e] & 0xFFFF0000u);
@@ -102,8 +108,10 @@ __device__ __forceinline__ void xform_tile(uint32_t kbuf, int xt) {
             phi_and_prime<PHI>(lo, f0, p0);
             phi_and_prime<PHI>(hi, f1, p1);
             ph[e] = ptx::pack_bf16x2(f0, f1);
+            pp[e] = ptx::pack_bf16x2(p0, p1);
         }
         sts128(kbuf + off, make_uint4(ph[0], ph[1], ph[2], ph[3]));
+        if constexpr (kKp) sts128(kbuf + 2 * kTile + off, make_uint4(pp[0], pp[1], pp[2], pp[3]));
     }
 }
 
@@ -129,7 +137,7 @@ __device__ __forceinline__ void issue_tile(uint32_t tmem, uint32_t base) {
 }
 __device__ __forceinline__ void issue_tile_d(int st, int ab, uint32_t tmem, uint32_t base) {
     if (st == 0) { if (ab == 0) issue_tile<0, 0>(tmem, base); else issue_tile<0, 1>(tmem, base); }
-    else if (st == 1) { if (ab == 0) issue_tile<1, 0>(tmem, base); else issue_tile<1, 1>(tmem, base); }
+    else if (kStages == 2 || st == 1) { if (ab == 0) issue_tile<1, 0>(tmem, base); else issue_tile<1, 1>(tmem, base); }
     else { if (ab == 0) issue_tile<2, 0>(tmem, base); else issue_tile<2, 1>(tmem, base); }
 }
 
@@ -154,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&bars->kv_full[s], 1);
             ptx::mbar_init(&bars->k_ready[s], kXform);
-            ptx::mbar_init(&bars->kv_empty[s], 1);
+            ptx::mbar_init(&bars->kv_empty[s], kKp ? 1 + kEpi : 1);  // MMA commit [+ epilogue read phi1'(K)]
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&bars->acc_full[b], 1);
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch(&mapK);
         ptx::tma_prefetch(&mapV);
         const uint64_t pol = ptx::policy_evict_first();
-        const uint64_t pol_k = ptx::policy_evict_last();  // re-read by the epilogue for phi1'(K)
+        const uint64_t pol_k = kKp ? pol : ptx::policy_evict_last();  // !kKp: re-read by the epilogue for phi1'(K)
         int stage = 0;
         uint32_t phase = 0;
         int k = 0;
@@ -277,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto epilogue = [&](int est, int eab, int64_t grow0, int valid, int h) {
             // raw k of this thread's row, columns [64 chalf, +64): 8 x 16 B through L2 (issued before the wait for the GEMMs)
             uint4 kraw[8];
-            {
+            if constexpr (!kKp) {
                 const int rr = row < valid ? row : 0;
                 const uint4* src = reinterpret_cast<const uint4*>(P.k + ((size_t)(grow0 + rr) * P.H + h) * 128 +
                                                                   chalf * 64);
@@ -287,6 +295,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&bars->acc_full[eab], aph[eab]);
             aph[eab] ^= 1;
             ptx::tc_fence_after();
+            if constexpr (kKp) {  // phi1'(K) of this row's 64 columns from the stage (swizzled 16-B chunks)
+                const uint32_t kp = base + est * kStageBytes + 2 * kTile + chalf * kHalf + row * 128;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) kraw[q] = lds128(kp + ((q ^ (row & 7)) << 4));
+                ptx::mbar_arrive(&bars->kv_empty[est]);
+            }
             const size_t gcol = ((size_t)grow0 * P.H + h) * 128 + chalf * 64;  // row 0 of the tile
             const uint32_t tv = tmem + lane_bits + eab * 256 + chalf * 64;
             const uint32_t tk = tv + 128;
@@ -316,8 +330,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int e = 0; e < 4; ++e) {
                             const int j = 4 * q + e;
                             float f, d0, d1;
-                            phi_and_prime<PHI1>(__uint_as_float(kw[e] << 16), f, d0);
-                            phi_and_prime<PHI1>(__uint_as_float(kw[e] & 0xFFFF0000u), f, d1);
+                            if constexpr (kKp) {  // phi1'(k) (bf16) from the transform
+                                d0 = __uint_as_float(kw[e] << 16);
+                                d1 = __uint_as_float(kw[e] & 0xFFFF0000u);
+                            } else {
+                                phi_and_prime<PHI1>(__uint_as_float(kw[e] << 16), f, d0);
+                                phi_and_prime<PHI1>(__uint_as_float(kw[e] & 0xFFFF0000u), f, d1);
+                            }
                             w[16 * c + j] = ptx::pack_bf16x2(__uint_as_float(rk[2 * j]) * d0,
                                                              __uint_as_float(rk[2 * j + 1]) * d1);
                         }
@@ -329,13 +348,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_arrive(&bars->acc_empty[eab]);
             (void)est;
         };
+        int est = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
             const int64_t row0 = P.offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
                 const int64_t rem = L - (int64_t)t * 128;
-                epilogue(0, ab, row0 + (int64_t)t * 128, rem < 128 ? (int)rem : 128, it.hg);
+                epilogue(est, ab, row0 + (int64_t)t * 128, rem < 128 ? (int)rem : 128, it.hg);
                 ab ^= 1;
+                if (++est == kStages) est = 0;
             }
         }
     }

@@ -212,6 +212,8 @@ def run_own(args, rank, world, local_rank):
                 else:
                     vista.vista_summarize_bwd(desc, ins[0], ins[1], ins[2], ins[3], total, fwd_out, fwd_lse, ins[4],
                                               dq, dk, dv, bws, bws_bytes, sh)
+                if world > 1:  # data parallel: the shared seeds' gradient is summed over the ranks (NCCL)
+                    torch.distributed.all_reduce(dq)
                 return [dq, dk, dv]
         if args.qla_rows:
             gen = torch.Generator(device=dev)
@@ -238,6 +240,8 @@ def run_own(args, rank, world, local_rank):
         items_per_step = world * total
         scaling = "weak"
         parallel = f"by_user x{world} (weak: a {args.config} batch per GPU, no data-path collective)"
+        if args.backward:
+            parallel = f"by_user x{world} (weak: a {args.config} batch per GPU; NCCL all_reduce of the seed gradient)"
     else:
         # strong scaling: one batch of the configured shape split across the ranks
         q = synth.make_q(S, H, d, seed=0, backend="torch", device=dev)

@@ -93,6 +93,22 @@ class CudaBackend:
     def merge(self, part_o, part_lse, q, attn, user_len):
         return self.v.summarize_merge(part_o, part_lse, q=q, attn=attn, user_len=user_len, **self.kw)
 
+    def bwd(self, q, k, v, offsets, total_len, dout, attn, **kw):
+        return self.v.summarize_bwd(q, k, v, offsets, total_len, dout, attn=attn, **self.kw, **kw)
+
+
+def summarize_bwd_by_user(q, k, v, offsets, total_len, dout, *, attn="softmax", group=None, backend=None, **kw):
+    """Data-parallel backward (NEXT-2) of a by_user shard: the local gradients from the backend, then
+    the one exchange the path has -- the shared seeds' gradient dq [S,H,d] summed over the ranks
+    (all_reduce; per-user seeds have no exchange).  dk, dv stay local (the rank's own items).
+    kw: forwarded to the backend's bwd (out / lse for softmax, z for QLA)."""
+    import torch.distributed as dist
+    be = backend or CudaBackend()
+    dq, dk, dv = be.bwd(q, k, v, offsets, total_len, dout, _attn_code(attn), **kw)
+    if q.dim() == 3 and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(dq, group=group)
+    return dq, dk, dv
+
 
 def _attn_code(attn):
     return 0 if attn in (0, "softmax") else 1

@@ -36,6 +36,15 @@ class OracleBackend:
         return torch.from_numpy(oracle.qla_finalize(q.numpy(), z, user_len.numpy())), None
 
 
+    def bwd(self, q, k, v, offsets, total_len, dout, attn, **kw):
+        qn, kn, vn, gn, off = q.numpy(), k.numpy(), v.numpy(), dout.numpy(), offsets.numpy()
+        if attn == 0:
+            g = oracle.softmax_backward(qn, kn, vn, off, gn)
+        else:
+            g = oracle.qla_backward(qn, kn, vn, off, gn)
+        return tuple(torch.from_numpy(np.ascontiguousarray(x)) for x in g)
+
+
 def free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -155,3 +164,50 @@ def test_partitioners():
         assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
     sizes = [sum(s.end - s.start for s in r) for r in segs]
     assert max(sizes) - min(sizes) <= 1
+
+
+def _bwd_worker(rank, world, port, attn, lens, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        S, H, d = 6, 2, 8
+        q, k, v, off = synth.make_batch(lens, S, H, d, seed=5, tau=1)
+        mine = vdist.partition_by_user(lens, world)[rank]
+        rng = np.random.default_rng(9)
+        g = (rng.integers(-128, 128, size=(len(lens), S, H, d)) / 64.0).astype(np.float32)
+        kk = np.concatenate([k[off[u]:off[u + 1]] for u in mine]) if mine else np.zeros((0, H, d), np.float32)
+        vv = np.concatenate([v[off[u]:off[u + 1]] for u in mine]) if mine else np.zeros((0, H, d), np.float32)
+        soff = synth.offsets_from_lengths(np.asarray([lens[u] for u in mine], dtype=np.int64))
+        dq, dk, dv = vdist.summarize_bwd_by_user(torch.from_numpy(q), torch.from_numpy(kk), torch.from_numpy(vv),
+                                                 torch.from_numpy(soff), int(soff[-1]), torch.from_numpy(g[mine]),
+                                                 attn=attn, backend=OracleBackend())
+        result_q.put((rank, (dq.numpy(), mine, dk.numpy(), soff)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_backward_by_user_all_reduces_seed_gradient(attn):
+    """Data-parallel backward over 2 ranks (gloo): the seed gradient after the all_reduce equals the
+    unsplit one on every rank; each rank's dK covers exactly its own users."""
+    lens = [30, 0, 12, 45, 7]
+    ctx = mp.get_context("spawn")
+    rq = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_bwd_worker, args=(r, 2, port, attn, lens, rq)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(rq.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    S, H, d = 6, 2, 8
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=5, tau=1)
+    g = (np.random.default_rng(9).integers(-128, 128, size=(len(lens), S, H, d)) / 64.0).astype(np.float32)
+    ref = (oracle.softmax_backward if attn == "softmax" else oracle.qla_backward)(q, k, v, off, g)
+    for r in range(2):
+        dq, mine, dk, soff = res[r]
+        np.testing.assert_allclose(dq, ref[0], rtol=0, atol=1e-12 * max(1.0, np.abs(ref[0]).max()))
+        for n, u in enumerate(mine):
+            np.testing.assert_allclose(dk[soff[n]:soff[n + 1]], ref[1][off[u]:off[u + 1]], rtol=0, atol=1e-12)

@@ -33,7 +33,10 @@ namespace {
 
 constexpr int kHalf = 128 * 128;  // one 64-column half of a 128 x 128 bf16 tile
 constexpr int kTile = 2 * kHalf;  // 32 KB
-constexpr int kStages = 3;
+#ifndef VISTA_ROWS_STAGES
+#define VISTA_ROWS_STAGES 3
+#endif
+constexpr int kStages = VISTA_ROWS_STAGES;
 constexpr int kWOff = kStages * kTile;
 constexpr int kBarOff = kWOff + kTile;
 constexpr int kSmem = kBarOff + 256 + 1024;
@@ -115,6 +118,16 @@ __device__ __forceinline__ void issue_tile(uint32_t tacc, uint32_t base) {
                       ptx::sdesc_sw128(wb + kk * 2048, kHalf, 1024), id, kk > 0);
 }
 
+__device__ __forceinline__ void issue_tile_d(int stage, uint32_t tacc, uint32_t base) {
+    switch (stage) {
+        case 0: issue_tile<0>(tacc, base); break;
+        case 1: issue_tile<1 % kStages>(tacc, base); break;
+        case 2: issue_tile<2 % kStages>(tacc, base); break;
+        case 3: issue_tile<3 % kStages>(tacc, base); break;
+        default: issue_tile<4 % kStages>(tacc, base); break;
+    }
+}
+
 template <int PHI1>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_qla_rows_kernel(const __grid_constant__ CUtensorMap mapQ, const Params P) {
@@ -185,9 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 aph[ab] ^= 1;
                 ptx::tc_fence_after();
                 const uint32_t tacc = tmem + ab * 128;
-                if (stage == 0) issue_tile<0>(tacc, base);
-                else if (stage == 1) issue_tile<1>(tacc, base);
-                else issue_tile<2>(tacc, base);
+                issue_tile_d(stage, tacc, base);
                 ptx::mma_commit_w(&bars->acc_full[ab]);
                 ptx::mma_commit_w(&bars->q_empty[stage]);
                 ab ^= 1;

@@ -407,6 +407,11 @@ def run_own(args, rank, world, local_rank):
                 "peak_kind": f"{pk_kind} bf16 burst (kernel timed alone per launch)",
                 "kernel": "sm100_softmax_bwd_kv_kernel" if args.backward else "sm100_softmax_kernel",
                 "kernel_ms": round(kern_ms, 5),
+                # context: the same against the power-capped sustained GEMM figure, the denominator for
+                # a kernel inside a long run (this run's clocks say whether sw_power_cap was active)
+                "sustained": ({"peak": pk["bf16_tflops_sustained"],
+                               "frac": round(tflops / pk["bf16_tflops_sustained"], 4)}
+                              if pk.get("bf16_tflops_sustained") else None),
                 "algorithmic_flop_per_launch": flops,
                 "hbm": {"achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                         "frac": round(gbs / pk["hbm_gbs"], 4), "algorithmic_bytes_per_launch": io_bytes}}

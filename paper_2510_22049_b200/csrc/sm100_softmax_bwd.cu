@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_init(&bars->dq_empty, 256);
         ptx::fence_mbar_init();
         int s0, s1;
-        partial_slots(P.uts, P.B, HG, cta, num_ctas, s0, s1);
+        partial_slots_g(P.uts, P.B, HG, cta, num_ctas, s0, s1, gmajor_groups(P.G, num_ctas));
         P.slot_unit[2 * cta] = s0;
         P.slot_unit[2 * cta + 1] = s1;
     }
@@ -622,8 +622,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
-    ItemIter iter;
-    iter.init(P.uts, P.B, HG, cta, num_ctas);
+    ItemIterG iter;
+    iter.init(P.uts, P.B, HG, cta, num_ctas, gmajor_groups(P.G, num_ctas));
     Item it;
     if (warp == 0) {
         ptx::tma_prefetch(&mapQ);

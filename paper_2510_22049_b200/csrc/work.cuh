@@ -103,6 +103,105 @@ __device__ __forceinline__ void partial_slots(const int64_t* uts, int B, int HG,
     if (end < HG * a + (hg + 1) * Tu) s1 = u * HG + hg;
 }
 
+#ifndef VISTA_GMAJOR
+#define VISTA_GMAJOR 1
+#endif
+// Query-group-major work order for a kernel whose units re-read a user's K/V once per query group
+// (the softmax backward dQ pass, G = S / 128); 0 = unit-major.  Measured on the forward at S = 512
+// too: +1% at c5, but the generic iterator cost 2% at c2 (G = 1), so the forward keeps ItemIter.
+constexpr int kGMajor = VISTA_GMAJOR;
+__device__ __forceinline__ int gmajor_groups(int G, int num_ctas) { return (kGMajor && G > 1 && num_ctas % G == 0) ? G : 1; }
+
+struct ItemIterG {
+    // ItemIter with an optional query-group-major order.
+    // G > 1 (query-group-major order, "g-major"): the flat space is G blocks of H * uts[B] tiles,
+    // block g holding the units (u, h, g) user-major.  With C divisible by G, CTAs c and
+    // c + C/G, ... walk the same (user, head, tile) sequence for the G query groups at the same
+    // time, so each K/V tile is fetched from HBM once and hit in L2 by the other groups.
+    int t, end;
+    int u, base, Tu;  // current user (-1 before the first item), its first flat tile, tiles per unit
+    int G, g;         // query groups per head (1: unit-major order), current group
+
+    __device__ void init(const int64_t* uts, int B, int HG, int cta, int num_ctas, int groups = 1) {
+        const int T = HG * (int)uts[B];
+        t = (int)(((unsigned long long)cta * (unsigned)T) / (unsigned)num_ctas);
+        end = (int)(((unsigned long long)(cta + 1) * (unsigned)T) / (unsigned)num_ctas);
+        u = -1;
+        G = groups;
+        g = 0;
+    }
+    __device__ bool next(Item& it, const int64_t* uts, int B, int HG) {
+        if (t >= end) return false;
+        const int H = G > 1 ? HG / G : HG;
+        it.first = u < 0;
+        if (u < 0) {
+            int tl = t;
+            if (G > 1) {
+                const int TH = H * (int)uts[B];
+                g = t / TH;
+                tl = t - g * TH;
+            }
+            u = user_of_tile(uts, B, H, tl);
+            const int a = (int)uts[u];
+            base = (t - tl) + H * a;
+            Tu = (int)uts[u + 1] - a;
+        }
+        while (t >= base + H * Tu) {  // next non-empty user (t < end <= HG * uts[B] bounds this)
+            base += H * Tu;
+            if (++u == B) {  // g-major: wrap to the next query group's block
+                u = 0;
+                ++g;
+            }
+            Tu = (int)(uts[u + 1] - uts[u]);
+        }
+        const unsigned r = (unsigned)(t - base);
+        const int h = (int)(r / (unsigned)Tu);
+        it.u = u;
+        it.hg = G > 1 ? h * G + g : h;
+        it.t0 = (int)(r - (unsigned)h * (unsigned)Tu);
+        const int n = min(end - t, Tu - it.t0);
+        it.t1 = it.t0 + n;
+        it.Tu = Tu;
+        t += n;
+        it.last = (t >= end);
+        return true;
+    }
+};
+
+// Units held in CTA c's partial slots 2c (first item) / 2c+1 (last item), -1 if that item is a
+// whole unit or absent.  Only the first and the last item of a range can be partial, so this
+// looks at those two directly instead of walking the range.  G as in ItemIterG.
+__device__ __forceinline__ void unit_at(const int64_t* uts, int B, int HG, int G, int x, int& n, int& f_start,
+                                        int& f_end) {
+    const int H = G > 1 ? HG / G : HG;
+    int g = 0, tl = x;
+    if (G > 1) {
+        const int TH = H * (int)uts[B];
+        g = x / TH;
+        tl = x - g * TH;
+    }
+    const int u = user_of_tile(uts, B, H, tl);
+    const int a = (int)uts[u], Tu = (int)uts[u + 1] - a;
+    const int h = (tl - H * a) / Tu;
+    f_start = (x - tl) + H * a + h * Tu;
+    f_end = f_start + Tu;
+    n = u * HG + (G > 1 ? h * G + g : h);
+}
+__device__ __forceinline__ void partial_slots_g(const int64_t* uts, int B, int HG, int cta, int num_ctas, int& s0,
+                                              int& s1, int G) {
+    s0 = s1 = -1;
+    const int T = HG * (int)uts[B];
+    const int beg = (int)(((unsigned long long)cta * (unsigned)T) / (unsigned)num_ctas);
+    const int end = (int)(((unsigned long long)(cta + 1) * (unsigned)T) / (unsigned)num_ctas);
+    if (beg >= end) return;
+    int n, f_start, f_end;
+    unit_at(uts, B, HG, G, beg, n, f_start, f_end);  // first item: the unit holding tile beg
+    if (beg > f_start || end < f_end) s0 = n;
+    if (end <= f_end) return;  // one item only
+    unit_at(uts, B, HG, G, end - 1, n, f_start, f_end);  // last item: starts inside the range
+    if (end < f_end) s1 = n;
+}
+
 __device__ __forceinline__ bool item_complete(const Item& it) { return it.t0 == 0 && it.t1 == it.Tu; }
 
 // First flat tile of CTA c's range, and the CTA whose range holds flat tile x (ranges as in ItemIter).

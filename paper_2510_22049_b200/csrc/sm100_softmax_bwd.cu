@@ -391,9 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const size_t lrow = ((size_t)it.u * P.H + it.hg) * P.S;
             if constexpr (!STREAM) {  // the unit's lse * log2e and D rows into shared memory
                 named_sync_sm();      // the previous unit's chunks are done with them
-                for (int e = st; e < P.S; e += 256) {
-                    lsd[e] = __ldg(P.lse + lrow + e) * kLog2e;
-                    lsd[256 + e] = __ldg(P.dd + lrow + e);
+                for (int e = st; e < P.S; e += 256) {  // negated: the FFMA2 / FADD2 addends below
+                    lsd[e] = -__ldg(P.lse + lrow + e) * kLog2e;
+                    lsd[256 + e] = -__ldg(P.dd + lrow + e);
                 }
                 named_sync_sm();
             }
@@ -402,12 +402,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int g = 0; g < G; ++g) {
                     if constexpr (STREAM) {  // this block's 128 lse * log2e and D values into shared memory
                         const int e = st & 127;
-                        const float lv = __ldg(P.lse + lrow + g * 128 + e) * kLog2e;
-                        const float dv = __ldg(P.dd + lrow + g * 128 + e);
+                        const float lv = -__ldg(P.lse + lrow + g * 128 + e) * kLog2e;
+                        const float dv = -__ldg(P.dd + lrow + g * 128 + e);
                         named_sync_sm();
                         if (st < 128) lsd[e] = lv; else lsd[256 + e] = dv;
                         named_sync_sm();
                     }
+                    const uint64_t sl2x2 = ptx::f2_pack(P.scale_log2, P.scale_log2), zero2 = ptx::f2_pack(0.f, 0.f);
                     const float* ls = lsd + (STREAM ? 0 : g * 128) + sg * 64;
                     const float* dl = lsd + 256 + (STREAM ? 0 : g * 128) + sg * 64;
                     const uint32_t tsp = ts + sg * 64, tsd = ts + 128 + sg * 64;  // this half's S^T / dP^T columns
@@ -422,11 +423,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tmem_wait_ld();
                         ptx::reg_fence(sr);
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + 2 * j);
-                            const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[2 * j]), P.scale_log2, -l2.x));
-                            const float p1 = ptx::ex2(fmaf(__uint_as_float(sr[2 * j + 1]), P.scale_log2, -l2.y));
-                            pk[16 * c + j] = ptx::pack_bf16x2(p0, p1);
+                        for (int j = 0; j < 16; ++j) {  // x = s scale log2e - lse log2e (FFMA2), p = 2^x
+                            const uint64_t nl2 = *reinterpret_cast<const uint64_t*>(ls + c * 32 + 2 * j);
+                            float x0, x1;
+                            ptx::f2_unpack(ptx::f2_fma(ptx::f2_pack(__uint_as_float(sr[2 * j]), __uint_as_float(sr[2 * j + 1])),
+                                                       sl2x2, nl2),
+                                           x0, x1);
+                            pk[16 * c + j] = ptx::pack_bf16x2(ptx::ex2(x0), ptx::ex2(x1));
                         }
                         ptx::tmem_st16(tsp + c * 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16 * c));
                     }
@@ -444,12 +447,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::reg_fence(dr);
                         uint32_t sw[16];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const float2 d2 = *reinterpret_cast<const float2*>(dl + c * 32 + 2 * j);
+                        for (int j = 0; j < 16; ++j) {  // dS = P (dP - D): FADD2 then FFMA2 (+0)
+                            const uint64_t nd2 = *reinterpret_cast<const uint64_t*>(dl + c * 32 + 2 * j);
                             const uint32_t pw = pk[16 * c + j];
-                            const float p0 = __uint_as_float(pw << 16), p1 = __uint_as_float(pw & 0xffff0000u);
-                            sw[j] = ptx::pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - d2.x),
-                                                     p1 * (__uint_as_float(dr[2 * j + 1]) - d2.y));
+                            const uint64_t t2 =
+                                ptx::f2_add(ptx::f2_pack(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])), nd2);
+                            float d0, d1;
+                            ptx::f2_unpack(ptx::f2_fma(ptx::f2_pack(__uint_as_float(pw << 16), __uint_as_float(pw & 0xffff0000u)),
+                                                       t2, zero2),
+                                           d0, d1);
+                            sw[j] = ptx::pack_bf16x2(d0, d1);
                         }
                         ptx::tmem_st16(tsd + c * 16, sw);
                     }
@@ -728,6 +735,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t L = P.offsets[it.u + 1] - P.offsets[it.u];
             const size_t li = ((size_t)it.u * P.H + h) * P.S + g * 128 + r;
             const float lse2 = __ldg(P.lse + li) * kLog2e, dd = __ldg(P.dd + li);
+            const uint64_t sl2x2 = ptx::f2_pack(P.scale_log2, P.scale_log2), nlse2x2 = ptx::f2_pack(-lse2, -lse2),
+                           ndd2 = ptx::f2_pack(-dd, -dd), zero2 = ptx::f2_pack(0.f, 0.f);
             for (int t = it.t0; t < it.t1; ++t) {
                 const int64_t remv = L - (int64_t)t * 128 - sg * 64;
                 const int valid = remv < 64 ? (int)remv : 64;  // keys of this half (may be <= 0)
@@ -743,11 +752,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tmem_wait_ld();
                     ptx::reg_fence(sr);
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
+                    for (int j = 0; j < 16; ++j) {  // x = s scale log2e - lse log2e (FFMA2), p = 2^x
                         const int col = c * 32 + 2 * j;
-                        const float p0 = col < valid ? ptx::ex2(fmaf(__uint_as_float(sr[2 * j]), P.scale_log2, -lse2)) : 0.f;
-                        const float p1 =
-                            col + 1 < valid ? ptx::ex2(fmaf(__uint_as_float(sr[2 * j + 1]), P.scale_log2, -lse2)) : 0.f;
+                        float x0, x1;
+                        ptx::f2_unpack(ptx::f2_fma(ptx::f2_pack(__uint_as_float(sr[2 * j]), __uint_as_float(sr[2 * j + 1])),
+                                                   sl2x2, nlse2x2),
+                                       x0, x1);
+                        const float p0 = col < valid ? ptx::ex2(x0) : 0.f;
+                        const float p1 = col + 1 < valid ? ptx::ex2(x1) : 0.f;
                         pk[16 * c + j] = ptx::pack_bf16x2(p0, p1);
                     }
                 }
@@ -765,10 +777,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t sw[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const uint32_t pw = pk[16 * c + j];
-                        const float p0 = __uint_as_float(pw << 16), p1 = __uint_as_float(pw & 0xffff0000u);
-                        sw[j] = ptx::pack_bf16x2(p0 * (__uint_as_float(dr[2 * j]) - dd),
-                                                 p1 * (__uint_as_float(dr[2 * j + 1]) - dd));
+                        const uint32_t pw = pk[16 * c + j];  // dS = P (dP - D): FADD2 then FFMA2 (+0)
+                        const uint64_t t2 =
+                            ptx::f2_add(ptx::f2_pack(__uint_as_float(dr[2 * j]), __uint_as_float(dr[2 * j + 1])), ndd2);
+                        float d0, d1;
+                        ptx::f2_unpack(ptx::f2_fma(ptx::f2_pack(__uint_as_float(pw << 16), __uint_as_float(pw & 0xffff0000u)),
+                                                   t2, zero2),
+                                       d0, d1);
+                        sw[j] = ptx::pack_bf16x2(d0, d1);
                     }
                     ptx::tmem_st16(tsb + c * 16, sw);
                 }

@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 }  // namespace dq
 
-// D[u,h,i] = sum_c dO[u,i,h,c] O[u,i,h,c]   (one warp per row)
+// D[u,h,i] = sum_c dO[u,i,h,c] O[u,i,h,c]   (one warp per row; 4 consecutive channels per lane)
 template <typename TO>
 __global__ void softmax_bwd_d_kernel(const TO* __restrict__ out, const TO* __restrict__ dout, int B, int S, int H,
                                      float* __restrict__ dd) {
@@ -828,20 +828,21 @@ __global__ void softmax_bwd_d_kernel(const TO* __restrict__ out, const TO* __res
     const int lane = threadIdx.x % 32;
     if (rrow >= (int64_t)B * H * S) return;
     const int u = (int)(rrow / ((int64_t)H * S)), h = (int)((rrow / S) % H), i = (int)(rrow % S);
-    const size_t idx = (((size_t)u * S + i) * H + h) * 128;
+    const size_t idx = (((size_t)u * S + i) * H + h) * 128 + 4 * lane;
     float s = 0.f;
+    if constexpr (sizeof(TO) == 2) {
+        const uint2 a = __ldg(reinterpret_cast<const uint2*>(out + idx));
+        const uint2 b = __ldg(reinterpret_cast<const uint2*>(dout + idx));
+        const uint32_t aw[2] = {a.x, a.y}, bw[2] = {b.x, b.y};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const int c = lane + 32 * e;
-        float a, b;
-        if constexpr (sizeof(TO) == 2) {
-            a = __bfloat162float(out[idx + c]);
-            b = __bfloat162float(dout[idx + c]);
-        } else {
-            a = out[idx + c];
-            b = dout[idx + c];
+        for (int e = 0; e < 2; ++e) {
+            s = fmaf(__uint_as_float(aw[e] << 16), __uint_as_float(bw[e] << 16), s);
+            s = fmaf(__uint_as_float(aw[e] & 0xffff0000u), __uint_as_float(bw[e] & 0xffff0000u), s);
         }
-        s += a * b;
+    } else {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(out + idx));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(dout + idx));
+        s = a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);

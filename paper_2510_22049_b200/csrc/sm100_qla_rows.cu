@@ -239,22 +239,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t grow0 = row0 + (int64_t)t * 128;
                 const size_t e0 = ((size_t)grow0 * P.H + it.hg) * 128;  // element (row 0, col 0) of the tile
                 // Delta: d_r = phi1(q_r) . phi1(k_self_r) over all 128 columns (both column warps
-                // compute it), issued before the wait for the GEMM
+                // compute it), issued before the wait for the GEMM. Coalesced: the warp walks its 32
+                // rows, lane l holding channels [4l, 4l + 4) of each (one 256 B row per load), then a
+                // transpose-reduce (31 shuffles) leaves row wq * 32 + l's sum in lane l.
                 float dr = 0.f;
-                if (P.k_self && row < valid) {
-                    const uint4* qs = reinterpret_cast<const uint4*>(P.q + e0 + (size_t)row * rstride);
-                    const uint4* ks = reinterpret_cast<const uint4*>(P.k_self + e0 + (size_t)row * rstride);
-#pragma unroll 4
-                    for (int c = 0; c < 16; ++c) {
-                        const uint4 a = __ldg(qs + c), b = __ldg(ks + c);
-                        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+                if (P.k_self) {
+                    float part[32];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            dr = fmaf(phi<PHI1>(__uint_as_float(aw[e] << 16)), phi<PHI1>(__uint_as_float(bw[e] << 16)), dr);
-                            dr = fmaf(phi<PHI1>(__uint_as_float(aw[e] & 0xFFFF0000u)),
-                                      phi<PHI1>(__uint_as_float(bw[e] & 0xFFFF0000u)), dr);
+                    for (int rr = 0; rr < 32; ++rr) {
+                        float s = 0.f;
+                        {  // rows past the tail re-read the last valid row; their sums are never used
+                            const int r = min(wq * 32 + rr, valid - 1);
+                            const size_t off = e0 + (size_t)r * rstride + 4 * lane;
+                            const uint2 a = __ldg(reinterpret_cast<const uint2*>(P.q + off));
+                            const uint2 b = __ldg(reinterpret_cast<const uint2*>(P.k_self + off));
+                            const uint32_t aw[2] = {a.x, a.y}, bw[2] = {b.x, b.y};
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                s = fmaf(phi<PHI1>(__uint_as_float(aw[e] << 16)), phi<PHI1>(__uint_as_float(bw[e] << 16)), s);
+                                s = fmaf(phi<PHI1>(__uint_as_float(aw[e] & 0xFFFF0000u)),
+                                         phi<PHI1>(__uint_as_float(bw[e] & 0xFFFF0000u)), s);
+                            }
+                        }
+                        part[rr] = s;
+                    }
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) {
+                        const bool upper = (lane & o) != 0;
+#pragma unroll
+                        for (int i = 0; i < o; ++i) {
+                            const float send = upper ? part[i] : part[i + o];
+                            const float keep = upper ? part[i + o] : part[i];
+                            part[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                         }
                     }
+                    dr = part[0];
                 }
                 ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
                 aph[ab] ^= 1;

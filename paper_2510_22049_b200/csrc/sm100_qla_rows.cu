@@ -39,7 +39,8 @@ constexpr int kTile = 2 * kHalf;  // 32 KB
 constexpr int kStages = VISTA_ROWS_STAGES;
 constexpr int kWOff = kStages * kTile;
 constexpr int kBarOff = kWOff + kTile;
-constexpr int kSmem = kBarOff + 256 + 1024;
+constexpr int kDrOff = kBarOff + 256;  // float [2 tile parities][2 column halves][128 rows]: Delta halves
+constexpr int kSmem = kDrOff + 2048 + 1024;
 constexpr int kThreads = 512;
 constexpr int kXform = 128;
 constexpr int kEpi = 256;
@@ -238,29 +239,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int valid = rem < 128 ? (int)rem : 128;
                 const int64_t grow0 = row0 + (int64_t)t * 128;
                 const size_t e0 = ((size_t)grow0 * P.H + it.hg) * 128;  // element (row 0, col 0) of the tile
-                // Delta: d_r = phi1(q_r) . phi1(k_self_r) over all 128 columns (both column warps
-                // compute it), issued before the wait for the GEMM. Coalesced: the warp walks its 32
-                // rows, lane l holding channels [4l, 4l + 4) of each (one 256 B row per load), then a
-                // transpose-reduce (31 shuffles) leaves row wq * 32 + l's sum in lane l.
+                // Delta: d_r = phi1(q_r) . phi1(k_self_r), issued before the wait for the GEMM. Each
+                // column warp sums its 64 columns, coalesced: the warp walks its 32 rows, lane l
+                // holding channels 64 chalf + [2l, 2l + 2) of each (one 128 B line per load), then a
+                // transpose-reduce (31 shuffles) leaves row wq * 32 + l's half sum in lane l; the two
+                // halves meet through shared memory (named barrier per warp pair, buffer per tile
+                // parity so the next tile's write cannot overtake the partner's read).
                 float dr = 0.f;
                 if (P.k_self) {
                     float part[32];
 #pragma unroll
                     for (int rr = 0; rr < 32; ++rr) {
-                        float s = 0.f;
-                        {  // rows past the tail re-read the last valid row; their sums are never used
-                            const int r = min(wq * 32 + rr, valid - 1);
-                            const size_t off = e0 + (size_t)r * rstride + 4 * lane;
-                            const uint2 a = __ldg(reinterpret_cast<const uint2*>(P.q + off));
-                            const uint2 b = __ldg(reinterpret_cast<const uint2*>(P.k_self + off));
-                            const uint32_t aw[2] = {a.x, a.y}, bw[2] = {b.x, b.y};
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                s = fmaf(phi<PHI1>(__uint_as_float(aw[e] << 16)), phi<PHI1>(__uint_as_float(bw[e] << 16)), s);
-                                s = fmaf(phi<PHI1>(__uint_as_float(aw[e] & 0xFFFF0000u)),
-                                         phi<PHI1>(__uint_as_float(bw[e] & 0xFFFF0000u)), s);
-                            }
-                        }
+                        // rows past the tail re-read the last valid row; their sums are never used
+                        const int r = min(wq * 32 + rr, valid - 1);
+                        const size_t off = e0 + (size_t)r * rstride + chalf * 64 + 2 * lane;
+                        const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(P.q + off));
+                        const uint32_t b = __ldg(reinterpret_cast<const uint32_t*>(P.k_self + off));
+                        float s = phi<PHI1>(__uint_as_float(a << 16)) * phi<PHI1>(__uint_as_float(b << 16));
+                        s = fmaf(phi<PHI1>(__uint_as_float(a & 0xFFFF0000u)), phi<PHI1>(__uint_as_float(b & 0xFFFF0000u)), s);
                         part[rr] = s;
                     }
 #pragma unroll
@@ -273,7 +269,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                             part[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                         }
                     }
-                    dr = part[0];
+                    float* xch = reinterpret_cast<float*>(smem + kDrOff) + ab * 256;
+                    xch[chalf * 128 + row] = part[0];
+                    ptx::named_bar_sync(1 + wq, 64);
+                    // fixed order (columns 0-63 first) so both warps hold the same d_r
+                    dr = chalf == 0 ? part[0] + xch[128 + row] : xch[row] + part[0];
                 }
                 ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
                 aph[ab] ^= 1;

@@ -51,6 +51,13 @@ def parse():
                     help="NEXT-2: the step is the QLA backward (vista_summarize_bwd: Z recompute, dQ, dK, dV)")
     ap.add_argument("--export-int8", action="store_true",
                     help="NEXT-1: the step also exports the summary tokens as int8 (vista_quantize_rows_int8)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="run the K timed steps eagerly instead of as one captured CUDA graph")
+    ap.add_argument("--no-sustained", dest="sustained", action="store_false",
+                    help="skip the SURVEY 8(d) protocol block (>= 200 ms graph replays, median of 5)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group for N > 1 (gloo: host-staged exchange; a dry run of the multi-rank "
+                         "path when fewer GPUs than ranks are visible)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -143,7 +150,7 @@ def run_own(args, rank, world, local_rank):
 
     vista.load()
     from paper_2510_22049_b200 import dist as vdist
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % max(torch.cuda.device_count(), 1))
     torch.cuda.set_device(dev)
     cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
     if args.backward:
@@ -177,14 +184,14 @@ def run_own(args, rank, world, local_rank):
         qzp = torch.empty(nrows, dtype=torch.float32, device=dev) if args.export_int8 else None
 
         def export():
-            vista.vista_quantize_rows_int8(nrows, d, vista.BF16, out, codes, qscale, qzp, sh)
+            vista.vista_quantize_rows_int8(nrows, d, vista.BF16, out, codes, qscale, qzp, None)
 
         def step(ins=inputs):
             if args.export_int8:  # NEXT-1: the export fused into the summarization's epilogues
                 vista.vista_summarize_fwd_int8(desc, ins[0], ins[1], ins[2], ins[3], total, out, lse, codes, qscale,
-                                               qzp, ws, ws_bytes, sh)
+                                               qzp, ws, ws_bytes, None)
                 return [codes, qscale, qzp] + ([lse] if lse is not None else [])
-            vista.vista_summarize_fwd(desc, ins[0], ins[1], ins[2], ins[3], total, out, lse, ws, ws_bytes, sh)
+            vista.vista_summarize_fwd(desc, ins[0], ins[1], ins[2], ins[3], total, out, lse, ws, ws_bytes, None)
             return [out] + ([lse] if lse is not None else [])
         if args.backward:
             gen = torch.Generator(device=dev)
@@ -208,10 +215,10 @@ def run_own(args, rank, world, local_rank):
             def step(ins=inputs):
                 if fwd_z is not None:
                     vista.vista_summarize_bwd_qla_saved(desc, ins[0], ins[1], ins[2], ins[3], total, fwd_z, ins[4],
-                                                        dq, dk, dv, bws, bws_bytes, sh)
+                                                        dq, dk, dv, bws, bws_bytes, None)
                 else:
                     vista.vista_summarize_bwd(desc, ins[0], ins[1], ins[2], ins[3], total, fwd_out, fwd_lse, ins[4],
-                                              dq, dk, dv, bws, bws_bytes, sh)
+                                              dq, dk, dv, bws, bws_bytes, None)
                 if world > 1:  # data parallel: the shared seeds' gradient is summed over the ranks (NCCL)
                     torch.distributed.all_reduce(dq)
                 return [dq, dk, dv]
@@ -235,7 +242,7 @@ def run_own(args, rank, world, local_rank):
             def step(ins=inputs):
                 ks, vs = (ins[5], ins[6]) if len(ins) > 5 else (None, None)
                 vista.vista_qla_rows(desc, ins[0], ins[1], ins[2], total, ins[3], ins[4], n_rows, ks, vs, rows_out,
-                                     rws, rws_bytes, sh)
+                                     rws, rws_bytes, None)
                 return [rows_out]
         items_per_step = world * total
         scaling = "weak"
@@ -276,9 +283,11 @@ def run_own(args, rank, world, local_rank):
                 return [out] + ([lse] if lse is not None else [])
         else:
             segs_obj = [vdist.Segment(u, a0, e0) for u, a0, e0 in seg]
+            fplan = vdist.FlatPlan(all_segs, lens, rank, dev)
 
             def step(ins=inputs):
-                res = vdist.summarize_flat(ins[0], ins[1], ins[2], segs_obj, all_segs, lens, attn=args.attn)
+                res = vdist.summarize_flat(ins[0], ins[1], ins[2], segs_obj, all_segs, lens, attn=args.attn,
+                                           plan=fplan)
                 return [o for o, _ in res.values()][:1] or [ins[0]]
         items_per_step = int(off_all[-1])
         scaling = "strong"
@@ -286,19 +295,47 @@ def run_own(args, rank, world, local_rank):
         B = B_all
     path = vista.vista_dispatch_name(vista.make_desc(B, S, H, d, in_dtype=vista.BF16, attn=attn))
 
-    # warm-up
+    # warm-up (eager: also initializes NCCL communicators and the library's per-device state)
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
 
     K_steps = args.steps
     ev_k = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K_steps)]
-    for a, b in ev_k:  # materialize the event handles
-        a.record(stream)
-        b.record(stream)
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    gpu_index = os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[local_rank] \
-        if "CUDA_VISIBLE_DEVICES" in os.environ else str(local_rank)
+
+    def run_steps(n, evs=None):
+        for i in range(n):
+            if evs is not None:
+                vista.vista_time_next_main_kernel(evs[i][0], evs[i][1])
+            step()
+
+    # The K timed steps are captured once into a CUDA graph (one launch per replay: no host gaps
+    # between the steps' kernels); eager if capture is unavailable (gloo host staging) or fails.
+    graph, graph_note = None, None
+    if args.graph and args.dist_backend != "gloo":
+        try:
+            graph = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(stream)
+            with torch.cuda.stream(cs):
+                run_steps(1)  # warm the capture stream
+                graph.capture_begin()
+                c0 = vista.vista_launch_counter()
+                run_steps(K_steps, ev_k)
+                captured_launches = vista.vista_launch_counter() - c0
+                graph.capture_end()
+            stream.wait_stream(cs)
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001 -- recorded in the JSON line
+            graph, graph_note = None, f"eager (capture failed: {type(exc).__name__}: {str(exc)[:120]})"
+            torch.cuda.synchronize()
+    elif not args.graph:
+        graph_note = "eager (--no-graph)"
+    else:
+        graph_note = "eager (gloo exchange is host-staged, not capturable)"
+    gpu_index = os.environ.get("CUDA_VISIBLE_DEVICES", str(dev.index)).split(",")[dev.index] \
+        if "CUDA_VISIBLE_DEVICES" in os.environ else str(dev.index)
     sampler = ClockSampler(gpu_index)
     time.sleep(0.3)  # let nvidia-smi start sampling
     if world > 1:
@@ -307,15 +344,18 @@ def run_own(args, rank, world, local_rank):
     launches0 = vista.vista_launch_counter()
     w0 = time.time()
     t_start.record(stream)
-    for i in range(K_steps):
-        vista.vista_time_next_main_kernel(ev_k[i][0], ev_k[i][1])
-        step()
+    if graph is not None:
+        graph.replay()
+    else:
+        run_steps(K_steps, ev_k)
     t_stop.record(stream)
     torch.cuda.synchronize()
     w1 = time.time()
     if world > 1:
         torch.distributed.barrier()
-    launches = vista.vista_launch_counter() - launches0
+    # library launches inside the timed region: counted at capture time for a graph (one replay
+    # runs exactly the captured launches), live otherwise
+    launches = (captured_launches if graph is not None else vista.vista_launch_counter() - launches0)
     clocks = sampler.stop(w0, w1)
     elapsed_ms = t_start.elapsed_time(t_stop)
     kern_ms = sum(a.elapsed_time(b) for a, b in ev_k) / K_steps
@@ -324,6 +364,32 @@ def run_own(args, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed_ms, kern_ms = float(t[0]), float(t[1])
     value = items_per_step * K_steps / (elapsed_ms / 1e3)
+
+    # ---- SURVEY 8(d) protocol, beside the K-step number: R graph-replayed steps with R * t >= 200 ms,
+    # median of 5 runs, with the clocks of those runs (the sustained, power-capped regime)
+    sustained = None
+    if args.sustained and world == 1 and graph is not None:
+        R = max(1, int(math.ceil(200.0 / max(elapsed_ms / K_steps, 1e-3))))
+        reps = max(1, int(math.ceil(R / K_steps)))
+        sampler2 = ClockSampler(gpu_index)
+        time.sleep(0.3)
+        runs = []
+        w2 = time.time()
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                graph.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            runs.append(a.elapsed_time(b) / (reps * K_steps))
+        w3 = time.time()
+        # the last replay's per-step kernel events are those of the sustained regime
+        kern_sus = sum(a.elapsed_time(b) for a, b in ev_k) / K_steps
+        runs.sort()
+        sustained = {"ms_per_step_median": runs[2], "ms_per_step_runs": [round(x, 5) for x in runs],
+                     "steps_per_run": reps * K_steps, "value": items_per_step / (runs[2] / 1e3),
+                     "kernel_ms": round(kern_sus, 5), "clocks": sampler2.stop(w2, w3)}
 
     # ---- end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -437,7 +503,26 @@ def run_own(args, rank, world, local_rank):
         "clocks": clocks,
         "e2e": e2e,
         "gpu_launches": launches,
+        "timing": {"steps": graph_note or f"the {K_steps} timed steps replayed as one captured CUDA graph",
+                   "kernel_events": "per-step CUDA events around the dominant kernel (vista_time_next_main_kernel), "
+                                    "on the launching stream"},
     }
+    if sustained is not None:
+        sp = pk.get("bf16_tflops_sustained") if attn == vista.SOFTMAX else pk["hbm_gbs"]
+        if attn == vista.SOFTMAX:
+            ach = flops / (sustained["kernel_ms"] / 1e3) / 1e12
+        else:
+            ach = io_bytes / (sustained["kernel_ms"] / 1e3) / 1e9
+        sustained["roofline"] = {"achieved": round(ach, 2), "unit": roof["unit"], "peak": sp,
+                                 "frac": round(ach / sp, 4) if sp else None,
+                                 "peak_kind": ("measured bf16 sustained (power-capped GEMM)" if attn == vista.SOFTMAX
+                                               else "measured HBM copy")}
+        sustained["note"] = ("SURVEY 8(d) protocol: R graph-replayed steps per run (>= 200 ms), median of 5 runs; "
+                             "the sustained regime the K-step burst number sits above")
+        res["sustained"] = sustained
+    if world > 1 and args.dist_backend == "gloo":
+        res["dry_run"] = ("gloo process group: the exchange is staged through host memory and the ranks may share "
+                          "one GPU -- a functional run of the multi-rank path, not a scaling measurement")
     if export_info is not None:
         res["export_int8"] = export_info
     return res
@@ -570,9 +655,27 @@ def main():
         args.attn = "qla"  # the rows path is QLA's
         if args.backward or args.export_int8:
             raise SystemExit("--qla-rows excludes --backward / --export-int8")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: start N ranks (one process per GPU) under torch.distributed.run
+        if args.dist_backend == "nccl" and args.impl == "own":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                raise SystemExit(f"--gpus {args.gpus}: only {have} CUDA device(s) visible; NCCL needs one GPU per "
+                                 f"rank (use --dist-backend gloo for a functional dry run)")
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and args.impl == "own":
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         res = run_reference(args, rank, world)
         if res is not None:
@@ -580,8 +683,12 @@ def main():
         return
     if world > 1:
         import torch
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "gloo":  # dry run: ranks may share the visible GPU(s)
+            torch.cuda.set_device(local_rank % max(torch.cuda.device_count(), 1))
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_own(args, rank, world, local_rank)
     if res is not None and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds, rows=None,

@@ -200,9 +200,11 @@ vista_status_t vista_summarize_bwd(const vista_desc_t* desc, const void* q, cons
  *   target rows (stage 2)  O[T] = phi(Q[T]) phi(phi(K[S])^T V[S]) + Delta(phi(Q[T]), phi(K[T])) V[T]
  *                          with Delta(X, Y)_ij = sum_k X_ik Y_ik delta_ij
  * Row r of user u (r in [row_offsets[u], row_offsets[u+1])) gets
- *   out[r,h,:] = phi1(q_rows[r,h,:]) phi2(Z_uh / N_u)  [+ (phi1(q_r) . phi1(k_self_r)) v_self_r]
+ *   out[r,h,:] = phi1(q_rows[r,h,:]) phi2(Z_uh / N_u)  [+ (phi1(q_r) . phi1(k_self_r)) v_self_r / N_u]
  * where Z_uh = sum_j phi1(k_j)^T v_j over the user's history [offsets[u], offsets[u+1]) and N_u its
- * length when desc->qla_normalize (reading R10; the Delta term carries no 1/N, R20).
+ * length when desc->qla_normalize (else 1; also 1 when N_u = 0).  The Delta term sits under the same
+ * 1/N_u as the state: App. B's mixed form O = (Q K^T (.) M) V / N, M = [[1,0],[1,I_m]]
+ * (readings R10, R20).
  *   k, v        [total_len, H, d] (in_dtype), history; offsets int64 [B+1] as for summarize.
  *   q_rows      [total_rows, H, d] (in_dtype); row_offsets int64 [B+1] on the device, row_offsets[0]
  *               = 0, non-decreasing, row_offsets[B] = total_rows (a precondition, like offsets).

@@ -216,7 +216,11 @@ int vo_qla_finalize(int64_t B, int64_t S, int64_t H, int64_t d, const float* q,
  * with Delta(X, Y)_ij = sum_k X_ik Y_ik delta_ij, i.e. row r gains
  * (phi1(q_r) . phi1(k_self_r)) v_self_r.  Rows r in [row_offsets[u], row_offsets[u+1]) belong to
  * user u and use its state Zbar_u (as in vo_qla_finalize: Z / N_u when normalizing, DESIGN.md
- * reading R10); the Delta term carries no 1/N (reading R20).  k_self = v_self = NULL: no Delta term.
+ * reading R10).  When normalizing, the Delta term is divided by the SAME N_u: App. B writes the
+ * mixed form as one product under one scalar, O = (Q K^T (.) M) V / N with M = [[1,0],[1,I_m]]
+ * (PAPER.md:644-654), so the target's own diagonal term sits under the same /N as its source
+ * term (reading R20).  N_u = 0 (no history): no division, as for the state.
+ * k_self = v_self = NULL: no Delta term.
  * q_rows, k_self, v_self: [R, H, d]; z: [B, H, d, d]; out: [R, H, d].
  */
 int vo_qla_rows(int64_t B, int64_t H, int64_t d, const double* z, const int64_t* n_items,
@@ -246,6 +250,7 @@ int vo_qla_rows(int64_t B, int64_t H, int64_t d, const double* z, const int64_t*
                     const float* vr = v_self + (r * H + h) * d;
                     double dot = 0.0;
                     for (int64_t c = 0; c < d; ++c) dot += vo_act(phi1, (double)qr[c]) * vo_act(phi1, (double)kr[c]);
+                    dot *= inv; /* App. B: the diagonal term under the same 1/N */
                     for (int64_t c = 0; c < d; ++c) o[c] += dot * (double)vr[c];
                 }
             }
@@ -474,8 +479,12 @@ int vo_merge_sum(int64_t P, int64_t n, const double* parts, double* out) {
  * (the paper gives none): per token row of d values, symmetric-range affine quantization
  *   scale = max((max - min) / 254, 1e-12),  zero_point = (max + min) / 2,
  *   code  = clamp(round_half_even((x - zero_point) / scale), -127, 127),  x^ = code * scale + zp.
- * Computed in float32 (the kernel's precision, reading R18) with no FMA contraction
- * (-std=c11 => -ffp-contract=off), so the integer decisions match bit for bit.
+ * Reading R21: the codes are an integer decision taken from floating point, so they
+ * are decided in float32 -- the precision of the stored scale and zero point, the only values a
+ * consumer ever dequantizes with -- with no FMA contraction (-std=c11 => -ffp-contract=off):
+ * t = (x - zp) / s with the stored s, zp.  SPEC.md:342 says only "round"; an exact tie
+ * t = k + 1/2 goes to the even k (round-half-to-even, rintf, the IEEE default).  Both choices are
+ * pinned by tests/test_oracle_pins.py (exact .5 ties; |code s + zp - x| <= s/2 with the stored s).
  */
 int vo_quantize_rows_f32(int64_t n, int64_t d, const float* x, signed char* codes, float* scale, float* zp) {
     for (int64_t r = 0; r < n; ++r) {

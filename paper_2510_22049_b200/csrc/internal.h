@@ -10,6 +10,9 @@
 namespace vista {
 
 constexpr int kTile = 128;  // history items per tile (= TMA box rows = MMA N of the score GEMM)
+// Upper bound on every persistent grid (one CTA per SM): the split-L merge lists a unit's run of
+// partial slots in a fixed array of 2 * kMaxPersistentCtas + 2 entries (kernels_misc.cu).
+constexpr int kMaxPersistentCtas = 159;
 
 enum OutMode : int { OUT_FINAL = 0, OUT_PARTIAL = 1 };
 
@@ -35,6 +38,11 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 #endif
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the CURRENT device, set once per
+// (function, device, bytes) under a lock (function attributes are per device: a process-wide
+// once-only set would leave a second device at the 48 KB default).  vista_abi.cu.
+cudaError_t set_smem_attr(const void* fn, int bytes);
 
 // Where a finished (normalized) output row goes.
 struct OutSpec {
@@ -69,8 +77,7 @@ struct Problem {
 
 // Workspace carve-up (all offsets 256-B aligned).
 struct Workspace {
-    size_t uts_off, cnt_off, slot_unit_off, slot_o_off, slot_lse_off, zbuf_off, fin_off, total;
-    int num_units;     // per-unit piece counters (fused split-L merge)
+    size_t uts_off, slot_unit_off, slot_o_off, slot_lse_off, zbuf_off, fin_off, total;
     int num_ctas;      // persistent grid size used by the tiled kernels
     int rows_per_unit; // softmax: query rows per work unit (NQ * 128); QLA: d
 };
@@ -83,11 +90,8 @@ Workspace plan_workspace(const Problem& p, bool partial);
 // ---- launchers (return cudaError_t of the launch) ----
 // user tile starts: uts[u] = sum_{u'<u} ceil(L_u' / 128); also fills the outputs of empty users
 // (softmax: zeros / -inf in outs; QLA: zeros in zbuf if non-NULL).
-cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf, int* cnt = nullptr, int ncnt = 0);
+cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf);
 cudaError_t launch_sm100_softmax(const Problem& p, const Workspace& w, char* ws);
-// 2-CTA (cta_group::2) variant for S % 256 == 0; w.num_ctas counts CTA PAIRS
-cudaError_t launch_sm100_softmax2(const Problem& p, const Workspace& w, char* ws);
-bool softmax_uses_pairs(const Problem& p);
 // wbuf != NULL: complete units write W = phi2(Z / N) (bf16 finalize operand) instead of Z to zbuf
 cudaError_t launch_sm100_qla_state(const Problem& p, const Workspace& w, char* ws, float* zbuf,
                                    uint8_t* wbuf = nullptr);

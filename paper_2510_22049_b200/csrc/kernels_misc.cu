@@ -64,13 +64,11 @@ __device__ __forceinline__ void lse_store(const OutSpec& o, int S, int H, int u,
 
 // ---------------------------------------------------------------------------------------------
 __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, int64_t* __restrict__ uts, OutSpec outs,
-                                  int S, int H, int d, int softmax, float* __restrict__ zbuf, int* __restrict__ cnt,
-                                  int ncnt) {
+                                  int S, int H, int d, int softmax, float* __restrict__ zbuf) {
     __shared__ int64_t wsum[32];
     __shared__ int64_t carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     asm volatile("griddepcontrol.launch_dependents;");  // PDL: the main kernel may start its prologue
-    for (int e = tid; e < ncnt; e += blockDim.x) cnt[e] = 0;  // fused-merge piece counters
     if (tid == 0) {
         carry = 0;
         uts[0] = 0;
@@ -177,6 +175,7 @@ __device__ __forceinline__ void out_store4(const OutSpec& o, int S, int H, int u
 // double-buffered, and the rows are combined with an online max (any run length).
 constexpr int kMergeRows = 32;
 constexpr int kMergeMaxRun = 320;  // >= 2 * max CTAs a unit can span + 2
+static_assert(kMergeMaxRun >= 2 * kMaxPersistentCtas + 2, "merge run list");
 struct MergeSmem {
     float o[2][2][kMergeRows * 128];  // [stage][member][row * 128 + channel]
     float lse[2][2][kMergeRows];
@@ -737,18 +736,16 @@ cudaError_t launch_quantize_rows(int64_t n, int d, int in_bf16, const void* x, i
 }
 
 // ============================================================================== launchers
-cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf, int* cnt, int ncnt) {
+cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf) {
     user_tiles_kernel<<<1, 1024, 0, p.stream>>>(p.offsets, p.B, uts, p.outs, p.S, p.H, p.d,
-                                                 p.attn == VISTA_SOFTMAX, zbuf, cnt, ncnt);
+                                                 p.attn == VISTA_SOFTMAX, zbuf);
     return cudaGetLastError();
 }
 
 cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, char* ws) {
     const int num_slots = 2 * w.num_ctas;
     dim3 grid(num_slots, (w.rows_per_unit + kMergeRows - 1) / kMergeRows);
-    static const cudaError_t attr = cudaFuncSetAttribute(merge_softmax_slots_kernel,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)sizeof(MergeSmem));
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(merge_softmax_slots_kernel), (int)sizeof(MergeSmem));
     if (attr != cudaSuccess) return attr;
     return launch_pdl(merge_softmax_slots_kernel, grid, dim3(256), sizeof(MergeSmem), p.stream,
                       reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots,
@@ -794,8 +791,7 @@ template <int D, typename TQ>
 static cudaError_t finalize_d(const Problem& p, const float* zparts, int P, int64_t part_stride, const int64_t* user_len) {
     if (p.B == 0) return cudaSuccess;
     const size_t smem = (size_t)(D * D + D * 64) * sizeof(float);
-    static const cudaError_t attr = cudaFuncSetAttribute(qla_finalize_kernel<D, TQ>,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(qla_finalize_kernel<D, TQ>), (int)smem);
     if (attr != cudaSuccess) return attr;
     dim3 grid((p.S + 63) / 64, p.B * p.H);
     qla_finalize_kernel<D, TQ><<<grid, 256, smem, p.stream>>>(

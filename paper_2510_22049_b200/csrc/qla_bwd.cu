@@ -199,8 +199,7 @@ __global__ void __launch_bounds__(256) qla_bwd_kv_kernel(const T* __restrict__ k
 template <int D, typename TQ, typename TO>
 cudaError_t unit_launch(const Problem& p, const void* dout, const float* z, float* dz, uint8_t* dz_op, float* dqu) {
     const size_t smem = (size_t)(D * (D + 1) + 2 * kChunk * D) * sizeof(float);
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(qla_bwd_unit_kernel<D, TQ, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(qla_bwd_unit_kernel<D, TQ, TO>), (int)smem);
     if (attr != cudaSuccess) return attr;
     qla_bwd_unit_kernel<D, TQ, TO><<<p.B * p.H, 256, smem, p.stream>>>(
         reinterpret_cast<const TQ*>(p.q), p.q_user_stride, reinterpret_cast<const TO*>(dout), z, p.offsets, p.S, p.H,
@@ -211,8 +210,7 @@ cudaError_t unit_launch(const Problem& p, const void* dout, const float* z, floa
 template <int D, typename T>
 cudaError_t kv_launch(const Problem& p, const float* dz, void* dk, void* dv) {
     const size_t smem = (size_t)(D * (D + 1) + 2 * kChunk * D) * sizeof(float);
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(qla_bwd_kv_kernel<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(qla_bwd_kv_kernel<D, T>), (int)smem);
     if (attr != cudaSuccess) return attr;
     qla_bwd_kv_kernel<D, T><<<p.B * p.H, 256, smem, p.stream>>>(reinterpret_cast<const T*>(p.k),
                                                                 reinterpret_cast<const T*>(p.v), p.offsets, p.H,

@@ -315,8 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int PHI1>
 static cudaError_t launch_phi(const Problem& p, const Workspace& w, const CUtensorMap& mk, const CUtensorMap& mv,
                               const Params& P) {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(sm100_qla_state_kernel<PHI1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_state_kernel<PHI1>), kSmem);
     if (attr != cudaSuccess) return attr;
     sm100_qla_state_kernel<PHI1><<<w.num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P);
     return cudaGetLastError();

@@ -367,8 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int PHI1>
 cudaError_t launch_phi(const Problem& p, int num_ctas, const CUtensorMap& mk, const CUtensorMap& mv, const Params& P) {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(sm100_qla_bwd_kv_kernel<PHI1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_bwd_kv_kernel<PHI1>), kSmem);
     if (attr != cudaSuccess) return attr;
     sm100_qla_bwd_kv_kernel<PHI1><<<num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P);
     return cudaGetLastError();
@@ -556,15 +555,13 @@ cudaError_t launch_sm100_qla_bwd_unit(const Problem& p, bool dout_bf16, const vo
     if (p.B == 0) return cudaSuccess;
     const int smem = ub::kSmemU;
     if (dout_bf16) {
-        static const cudaError_t attr = cudaFuncSetAttribute(sm100_qla_bwd_unit_kernel<__nv_bfloat16>,
-                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_bwd_unit_kernel<__nv_bfloat16>), smem);
         if (attr != cudaSuccess) return attr;
         sm100_qla_bwd_unit_kernel<__nv_bfloat16><<<p.B * p.H, 128, smem, p.stream>>>(
             reinterpret_cast<const __nv_bfloat16*>(p.q), p.q_user_stride, reinterpret_cast<const __nv_bfloat16*>(dout),
             z, abuf, p.offsets, p.S, p.H, p.phi1, p.phi2, p.normalize, dz_op, dqu);
     } else {
-        static const cudaError_t attr = cudaFuncSetAttribute(sm100_qla_bwd_unit_kernel<float>,
-                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_bwd_unit_kernel<float>), smem);
         if (attr != cudaSuccess) return attr;
         sm100_qla_bwd_unit_kernel<float><<<p.B * p.H, 128, smem, p.stream>>>(
             reinterpret_cast<const __nv_bfloat16*>(p.q), p.q_user_stride, reinterpret_cast<const float*>(dout), z, abuf,

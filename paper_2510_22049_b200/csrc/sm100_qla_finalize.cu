@@ -189,8 +189,7 @@ cudaError_t launch_sm100_qla_finalize(const Problem& p, const float* zparts, int
     qla_prep_q_kernel<<<bq * p.H * nblk * 4, 256, 0, p.stream>>>(reinterpret_cast<const __nv_bfloat16*>(p.q),
                                                                  p.q_user_stride, p.S, p.H, p.phi1, abuf);
     const int smem = 2 * kOp + 1024;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(sm100_qla_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_finalize_kernel), smem);
     if (attr != cudaSuccess) return attr;
     dim3 grid(nblk, p.B * p.H);
     sm100_qla_finalize_kernel<<<grid, 128, smem, p.stream>>>(abuf, wbuf, p.q_user_stride != 0, p.S, p.H, p.outs,
@@ -207,8 +206,7 @@ cudaError_t launch_sm100_qla_finalize_fused(const Problem& p, uint8_t* ws) {
     qla_prep_q_kernel<<<bq * p.H * nblk * 4, 256, 0, p.stream>>>(reinterpret_cast<const __nv_bfloat16*>(p.q),
                                                                  p.q_user_stride, p.S, p.H, p.phi1, abuf);
     const int smem = 2 * kOp + 1024;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(sm100_qla_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_finalize_kernel), smem);
     if (attr != cudaSuccess) return attr;
     dim3 grid(nblk, p.B * p.H);
     sm100_qla_finalize_kernel<<<grid, 128, smem, p.stream>>>(abuf, wbuf, p.q_user_stride != 0, p.S, p.H, p.outs,

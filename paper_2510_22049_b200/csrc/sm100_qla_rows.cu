@@ -3,9 +3,10 @@
 //   target rows    O[T] = phi(Q[T]) phi(phi(K[S])^T V[S]) + Delta(phi(Q[T]), phi(K[T])) V[T]
 //                  Delta(X, Y)_ij = sum_k X_ik Y_ik delta_ij
 // Row r of user u (r in [row_offsets[u], row_offsets[u+1])):
-//   o_r = phi1(q_r) W_u  [+ (phi1(q_r) . phi1(k_self_r)) v_self_r],   W_u = phi2(Z_u / N_u)
+//   o_r = phi1(q_r) W_u  [+ (phi1(q_r) . phi1(k_self_r)) v_self_r / N_u],   W_u = phi2(Z_u / N_u)
 // with Z_u the user's state (the forward state kernel, partial mode) and W_u its bf16 MN-major
-// operand (qla_prep_w_kernel).  DESIGN.md readings R10 (1/N) and R20 (Delta without 1/N).
+// operand (qla_prep_w_kernel).  DESIGN.md readings R10 (1/N) and R20: with normalization the Delta
+// term is divided by the same N_u (App. B, O = (Q K^T (.) M) V / N).
 //
 // sm100_qla_rows_kernel: persistent, one CTA per SM, stream-K over the flat 128-row tiles of the
 // rows' jagged layout (work.cuh), one 128x128x128 tcgen05 GEMM per tile with W_u as the B operand.
@@ -60,7 +61,9 @@ struct Params {
     const __nv_bfloat16* k_self;  // NULL: no Delta term
     const __nv_bfloat16* v_self;
     void* out;                    // [R, H, 128] bf16 or f32
+    const int64_t* offsets;       // history offsets [B+1]: N_u for the Delta term's 1/N
     int out_bf16;
+    int normalize;
     int B, H;
 };
 
@@ -234,6 +237,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (iter.next(it, P.uts, P.B, HG)) {
             const int64_t R = P.row_offsets[it.u + 1] - P.row_offsets[it.u];
             const int64_t row0 = P.row_offsets[it.u];
+            float inv_n = 1.f;  // App. B: the Delta term under the state's 1/N_u (reading R20)
+            if (P.k_self && P.normalize) {
+                const int64_t N = P.offsets[it.u + 1] - P.offsets[it.u];
+                if (N > 0) inv_n = 1.f / (float)N;
+            }
             for (int t = it.t0; t < it.t1; ++t) {
                 const int64_t rem = R - (int64_t)t * 128;
                 const int valid = rem < 128 ? (int)rem : 128;
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     xch[chalf * 128 + row] = part[0];
                     ptx::named_bar_sync(1 + wq, 64);
                     // fixed order (columns 0-63 first) so both warps hold the same d_r
-                    dr = chalf == 0 ? part[0] + xch[128 + row] : xch[row] + part[0];
+                    dr = (chalf == 0 ? part[0] + xch[128 + row] : xch[row] + part[0]) * inv_n;
                 }
                 ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
                 aph[ab] ^= 1;
@@ -346,8 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int PHI1>
 cudaError_t launch_phi(const Problem& p, const CUtensorMap& mq, const Params& P) {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(sm100_qla_rows_kernel<PHI1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_rows_kernel<PHI1>), kSmem);
     if (attr != cudaSuccess) return attr;
     sm100_qla_rows_kernel<PHI1><<<p.num_sms, kThreads, kSmem, p.stream>>>(mq, P);
     return cudaGetLastError();
@@ -392,6 +399,7 @@ __global__ void qla_rows_simt_kernel(const float* __restrict__ z, const int64_t*
     if (c >= d) return;
     const int64_t N = offsets[u + 1] - offsets[u];
     const float inv = (normalize && N > 0) ? 1.f / (float)N : 1.f;
+    dr *= inv;  // App. B: the Delta term under the same 1/N_u (reading R20)
     const float* zu = z + (size_t)(u * H + h) * d * d;
     float acc = 0.f;
     for (int c1 = 0; c1 < d; ++c1) acc = fmaf(fq[c1], qla_act(phi2, zu[(size_t)c1 * d + c] * inv), acc);
@@ -421,6 +429,8 @@ cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, 
     P.k_self = reinterpret_cast<const __nv_bfloat16*>(k_self);
     P.v_self = reinterpret_cast<const __nv_bfloat16*>(v_self);
     P.out = out;
+    P.offsets = p.offsets;
+    P.normalize = p.normalize;
     P.out_bf16 = out_bf16;
     P.B = p.B;
     P.H = p.H;

@@ -47,13 +47,6 @@ namespace {
 constexpr int kHalfBytes = 128 * 128;       // 128 rows x 64 bf16 (one 128-B swizzle column block)
 constexpr int kTileBytes = 2 * kHalfBytes;  // 128 x 128 bf16
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
-#ifdef VISTA_FUSED_MERGE
-// experimental: split-L merge in the epilogue of the last CTA finishing a unit (measured slower
-// than the separate merge kernel at c2/c3: the merging CTA's tail grows more than the launch saves)
-constexpr bool kFusedMerge = true;
-#else
-constexpr bool kFusedMerge = false;
-#endif
 #ifndef VISTA_SETMAXNREG
 #define VISTA_SETMAXNREG 1
 #endif
@@ -115,7 +108,6 @@ struct Bars {
     uint64_t p_part[2][2];                // [q tile][middle P parts] (kSplitP == 4)
     uint64_t pv_done[2], o_full[2];
     uint32_t tmem_base;
-    int merge_last, merge_clo, merge_chi;  // fused split-L merge handshake (epilogue)
 };
 
 static_assert(sizeof(Bars) <= Cfg<2>::kBarBytes, "barrier region");
@@ -123,7 +115,6 @@ static_assert(sizeof(Bars) <= Cfg<2>::kBarBytes, "barrier region");
 struct Params {
     const int64_t* offsets;
     const int64_t* uts;
-    int* unit_cnt;  // per unit: pieces finished (zeroed by the scan kernel every launch)
     int* slot_unit;
     float* slot_o;
     float* slot_lse;
@@ -512,14 +503,6 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 for (int t = it.t0; t < it.t1; ++t) {
                     ptx::mbar_wait(&bars->k_empty[stage], phase ^ 1);
                     if (k == 0 && lane == 0) VTRACE(8, t - it.t0, 0);
-#ifdef VISTA_EXP_NOLOAD  // experiment: keep re-using resident tiles (no HBM traffic after the first ones)
-                    if (t >= it.t0 + C::kKStages) {
-                        if (ptx::elect_one()) ptx::mbar_arrive(&bars->k_full[stage]);
-                        __syncwarp();
-                        if (++stage == C::kKStages) { stage = 0; phase ^= 1; }
-                        continue;
-                    }
-#endif
                     if (lane == 0 && t == it.t0) ITRACE(10, k);
                     ptx::mbar_arrive_expect_tx_w(&bars->k_full[stage], kTileBytes);
                     const int32_t row = row0 + t * kTile;
@@ -544,14 +527,6 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
                 for (int t = it.t0; t < it.t1; ++t) {
                     ptx::mbar_wait(&bars->v_empty[stage], phase ^ 1);
                     if (first_item && lane == 0) VTRACE(9, t - it.t0, 0);
-#ifdef VISTA_EXP_NOLOAD
-                    if (t >= it.t0 + C::kVStages) {
-                        if (ptx::elect_one()) ptx::mbar_arrive(&bars->v_full[stage]);
-                        __syncwarp();
-                        if (++stage == C::kVStages) { stage = 0; phase ^= 1; }
-                        continue;
-                    }
-#endif
                     ptx::mbar_arrive_expect_tx_w(&bars->v_full[stage], kTileBytes);
                     const int32_t row = row0 + t * kTile;
                     for (int half = 0; half < 2; ++half)
@@ -727,15 +702,6 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) ptx::reg_fence(r[c]);
                 if (tr) VTRACE(5, t - it.t0, wg);
-#ifdef VISTA_EXP_NOSOFTMAX  // experiment: skip the softmax math (P = stale TMEM contents)
-                if (true) {
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive(&bars->p_full[wg][0]);
-                    l = 1.f;
-                    m_used = 0.f;
-                    continue;
-                }
-#endif
                 const int valid = L - t * kTile;
                 const bool full = valid >= kTile;
                 if (!full) {
@@ -886,65 +852,6 @@ __global__ void __launch_bounds__(Cfg<NQ>::kThreads, 1)
             if (itr) ITRACE(7, sitem);
             ++sitem;
 #endif
-            if (kFusedMerge && !item_complete(it)) {
-                // Fused split-L merge: the last CTA to finish a piece of this unit combines all
-                // pieces (their slots, ascending CTA order) with the LSE merge and writes the row.
-                __threadfence();
-                ptx::named_bar_sync(1, NQ * 128);
-                const int T = HG * (int)P.uts[P.B];
-                const int u0 = HG * (int)P.uts[it.u] + it.hg * it.Tu;
-                if (threadIdx.x == 128) {
-                    const int c_lo = cta_of_tile(u0, T, num_ctas), c_hi = cta_of_tile(u0 + it.Tu - 1, T, num_ctas);
-                    int pieces = 0;  // CTAs with a non-empty range in [c_lo, c_hi] (T < C leaves empty ranges)
-                    for (int c = c_lo; c <= c_hi; ++c) pieces += range_begin(c, T, num_ctas) < range_begin(c + 1, T, num_ctas);
-                    const int prev = atomicAdd(&P.unit_cnt[it.u * HG + it.hg], 1);
-                    bars->merge_last = prev == pieces - 1;
-                    bars->merge_clo = c_lo;
-                    bars->merge_chi = c_hi;
-                }
-                ptx::named_bar_sync(1, NQ * 128);
-                if (bars->merge_last) {
-                    __threadfence();
-                    const int c_lo = bars->merge_clo, c_hi = bars->merge_chi;
-                    const int ri = wg * 128 + row;
-                    float M = -INFINITY;
-                    for (int c = c_lo; c <= c_hi; ++c) {
-                        if (range_begin(c, T, num_ctas) == range_begin(c + 1, T, num_ctas)) continue;  // empty range
-                        M = fmaxf(M, __ldcg(P.slot_lse + (size_t)slot_of(c, c_lo, u0, T, num_ctas) * kRows + ri));
-                    }
-                    float Ls = 0.f;
-                    for (int c = c_lo; c <= c_hi; ++c) {
-                        if (range_begin(c, T, num_ctas) == range_begin(c + 1, T, num_ctas)) continue;
-                        Ls += ptx::ex2((__ldcg(P.slot_lse + (size_t)slot_of(c, c_lo, u0, T, num_ctas) * kRows + ri) - M) *
-                                       kLog2e);
-                    }
-                    const float lse_all = M + __logf(Ls);
-                    Item whole = it;
-                    whole.t0 = 0;
-                    whole.t1 = it.Tu;
-#pragma unroll 1
-                    for (int cc = 0; cc < 4; ++cc) {
-                        float of[32];
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) of[j] = 0.f;
-                        for (int c = c_lo; c <= c_hi; ++c) {
-                            if (range_begin(c, T, num_ctas) == range_begin(c + 1, T, num_ctas)) continue;
-                            const size_t sl = (size_t)slot_of(c, c_lo, u0, T, num_ctas) * kRows + ri;
-                            const float w = ptx::ex2((__ldcg(P.slot_lse + sl) - lse_all) * kLog2e);
-                            const float4* src = reinterpret_cast<const float4*>(P.slot_o + sl * 128 + cc * 32);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                const float4 v = __ldcg(src + j);
-                                of[4 * j] += w * v.x;
-                                of[4 * j + 1] += w * v.y;
-                                of[4 * j + 2] += w * v.z;
-                                of[4 * j + 3] += w * v.w;
-                            }
-                        }
-                        store_row(P, whole, cta, ri, of, cc * 32, lse_all, cc == 0, kRows);
-                    }
-                }
-            }
         }
     }
     ptx::tc_fence_before();
@@ -1015,7 +922,6 @@ static cudaError_t launch_nq(const Problem& p, const Workspace& w, char* ws) {
     Params P;
     P.offsets = p.offsets;
     P.uts = reinterpret_cast<const int64_t*>(ws + w.uts_off);
-    P.unit_cnt = reinterpret_cast<int*>(ws + w.cnt_off);
     P.slot_unit = reinterpret_cast<int*>(ws + w.slot_unit_off);
     P.slot_o = reinterpret_cast<float*>(ws + w.slot_o_off);
     P.slot_lse = reinterpret_cast<float*>(ws + w.slot_lse_off);
@@ -1028,8 +934,7 @@ static cudaError_t launch_nq(const Problem& p, const Workspace& w, char* ws) {
     P.q_per_user = p.q_user_stride != 0;
     P.out_v8 = (reinterpret_cast<uintptr_t>(p.outs.out) & 31) == 0;
     P.slot_v8 = (reinterpret_cast<uintptr_t>(P.slot_o) & 31) == 0;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(sm100_softmax_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_softmax_kernel<NQ>), C::kSmem);
     if (attr != cudaSuccess) return attr;
     return launch_pdl(sm100_softmax_kernel<NQ>, dim3(w.num_ctas), dim3(C::kThreads), C::kSmem, p.stream, mq, mk, mv, P);
 }

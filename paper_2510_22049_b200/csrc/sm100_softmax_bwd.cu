@@ -962,10 +962,8 @@ cudaError_t launch_softmax_bwd(const Problem& p, const void* out, const float* l
         P.scale = p.scale;
         P.q_per_user = p.q_user_stride != 0;
         const bool stream = p.S > kv::kResidentMaxS;
-        static const cudaError_t attr0 = cudaFuncSetAttribute(kv::sm100_softmax_bwd_kv_kernel<false>,
-                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kv::kSmem);
-        static const cudaError_t attr1 = cudaFuncSetAttribute(kv::sm100_softmax_bwd_kv_kernel<true>,
-                                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kv::kSmem);
+        const cudaError_t attr0 = set_smem_attr(reinterpret_cast<const void*>(kv::sm100_softmax_bwd_kv_kernel<false>), kv::kSmem);
+        const cudaError_t attr1 = set_smem_attr(reinterpret_cast<const void*>(kv::sm100_softmax_bwd_kv_kernel<true>), kv::kSmem);
         if (attr0 != cudaSuccess) return attr0;
         if (attr1 != cudaSuccess) return attr1;
         if (ev_a && (e = cudaEventRecord(ev_a, p.stream)) != cudaSuccess) return e;
@@ -995,8 +993,7 @@ cudaError_t launch_softmax_bwd(const Problem& p, const void* out, const float* l
         P.scale_log2 = p.scale * kLog2e;
         P.scale = p.scale;
         P.q_per_user = p.q_user_stride != 0;
-        static const cudaError_t attr = cudaFuncSetAttribute(dq::sm100_softmax_bwd_dq_kernel,
-                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, dq::kSmem);
+        const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(dq::sm100_softmax_bwd_dq_kernel), dq::kSmem);
         if (attr != cudaSuccess) return attr;
         dq::sm100_softmax_bwd_dq_kernel<<<(unsigned)C, dq::kThreads, dq::kSmem, p.stream>>>(mq, mg, mk, mv, P);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <vector>
 
 #include "internal.h"
@@ -90,13 +92,27 @@ Problem make_problem(const vista_desc_t* d, int64_t total_len) {
     p.normalize = d->qla_normalize;
     p.q_user_stride = d->q_user_stride;
     p.total_len = total_len;
-    p.num_sms = device_sms();
+    p.num_sms = std::min(device_sms(), kMaxPersistentCtas);  // bounds the merge's slot run list
     return p;
 }
 
 }  // namespace
 
 namespace vista {
+
+cudaError_t set_smem_attr(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const auto key = std::make_tuple(fn, dev, bytes);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
+}
 
 Path choose_path(const Problem& p) {
     const bool tma_ok = p.in_bf16 && p.d == 128 && p.total_len < (int64_t(1) << 31) && (p.q_user_stride % 8) == 0;
@@ -105,15 +121,6 @@ Path choose_path(const Problem& p) {
 }
 
 int sm100_softmax_nq(int S);
-
-bool softmax_uses_pairs(const Problem& p) {
-#ifdef VISTA_SOFTMAX_PAIRS  // experimental 2-CTA kernel (sm100_softmax2.cu); see DESIGN.md §4.1
-    return p.S % 256 == 0 && p.num_sms >= 2;
-#else
-    (void)p;
-    return false;
-#endif
-}
 
 Workspace plan_workspace(const Problem& p, bool partial) {
     (void)partial;
@@ -125,16 +132,9 @@ Workspace plan_workspace(const Problem& p, bool partial) {
     if (path == PATH_SM100_SOFTMAX || path == PATH_SM100_QLA) {
         w.num_ctas = p.num_sms;
         w.rows_per_unit = path == PATH_SM100_SOFTMAX ? sm100_softmax_nq(p.S) * 128 : 128;
-        if (path == PATH_SM100_SOFTMAX && softmax_uses_pairs(p)) {
-            w.num_ctas = p.num_sms / 2;  // CTA pairs
-            w.rows_per_unit = 256;
-        }
     }
     w.uts_off = off;
     off = align256(off + (size_t)(p.B + 1) * sizeof(int64_t));
-    w.cnt_off = off;
-    w.num_units = (path == PATH_SM100_SOFTMAX) ? p.B * p.H * ((p.S + 127) / 128) : 0;
-    off = align256(off + (size_t)w.num_units * sizeof(int));
     w.slot_unit_off = off;
     off = align256(off + (size_t)2 * w.num_ctas * sizeof(int));
     w.slot_o_off = off;
@@ -221,21 +221,11 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
     int nlaunch = 0;
     switch (choose_path(p)) {
         case PATH_SM100_SOFTMAX: {
-            if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), nullptr,
-                                       reinterpret_cast<int*>(ws + w.cnt_off), w.num_units)) != cudaSuccess)
+            if ((e = launch_user_tiles(p, reinterpret_cast<int64_t*>(ws + w.uts_off), nullptr)) != cudaSuccess)
                 break;
-            if (softmax_uses_pairs(p)) {
-                if ((e = timed_main(p.stream, [&] { return launch_sm100_softmax2(p, w, ws); })) != cudaSuccess) break;
-                e = launch_merge_softmax_slots(p, w, ws);
-                nlaunch = 3;
-            } else {
-                e = timed_main(p.stream, [&] { return launch_sm100_softmax(p, w, ws); });
-                nlaunch = 2;
-#ifndef VISTA_FUSED_MERGE
-                if (e == cudaSuccess) e = launch_merge_softmax_slots(p, w, ws);
-                nlaunch = 3;
-#endif
-            }
+            if ((e = timed_main(p.stream, [&] { return launch_sm100_softmax(p, w, ws); })) != cudaSuccess) break;
+            e = launch_merge_softmax_slots(p, w, ws);
+            nlaunch = 3;
             break;
         }
         case PATH_SM100_QLA: {
@@ -298,8 +288,7 @@ vista_status_t vista_summarize_fwd_int8(const vista_desc_t* desc, const void* q,
     // path with a bf16, 32-B aligned out; otherwise the export kernel runs after the summarization
     Problem pp = validate_desc(desc) == VISTA_OK ? make_problem(desc, total_len) : Problem{};
     const bool fused = validate_desc(desc) == VISTA_OK && choose_path(pp) == PATH_SM100_SOFTMAX &&
-                       desc->out_dtype == VISTA_BF16 && (reinterpret_cast<uintptr_t>(out) & 31) == 0 &&
-                       !softmax_uses_pairs(pp);
+                       desc->out_dtype == VISTA_BF16 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
     if (fused) {
         o.codes = codes;
         o.qscale = scale;

@@ -204,20 +204,6 @@ __device__ __forceinline__ void partial_slots_g(const int64_t* uts, int B, int H
 
 __device__ __forceinline__ bool item_complete(const Item& it) { return it.t0 == 0 && it.t1 == it.Tu; }
 
-// First flat tile of CTA c's range, and the CTA whose range holds flat tile x (ranges as in ItemIter).
-__device__ __forceinline__ int range_begin(int c, int T, int C) {
-    return (int)(((unsigned long long)c * (unsigned)T) / (unsigned)C);
-}
-__device__ __forceinline__ int cta_of_tile(int x, int T, int C) {
-    int c = (int)(((unsigned long long)x * (unsigned)C) / (unsigned)T);
-    while (c + 1 < C && range_begin(c + 1, T, C) <= x) ++c;
-    while (c > 0 && range_begin(c, T, C) > x) --c;
-    return c;
-}
-// Workspace slot in which CTA c holds its partial of the unit whose flat tiles start at u0.
-__device__ __forceinline__ int slot_of(int c, int c_lo, int u0, int T, int C) {
-    return (c > c_lo || range_begin(c, T, C) >= u0) ? 2 * c : 2 * c + 1;
-}
 __device__ __forceinline__ int item_slot(const Item& it, int cta) { return it.first ? 2 * cta : 2 * cta + 1; }
 
 }  // namespace vista

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = ["partition_by_user", "partition_by_length", "partition_flat", "CudaBackend",
-           "summarize_by_length", "summarize_flat", "Segment"]
+           "summarize_by_length", "summarize_flat", "summarize_bwd_by_user", "FlatPlan", "Segment"]
 
 
 # ----------------------------------------------------------------------------- partitioners (host)
@@ -116,26 +116,30 @@ def _attn_code(attn):
 
 # ----------------------------------------------------------------------------- split-L paths
 def _all_gather(t, group):
-    """[*shape] on every rank -> [world, *shape] in rank order (one all_gather_into_tensor)."""
+    """[*shape] on every rank -> [world, *shape] in rank order (one all_gather_into_tensor).
+
+    NCCL gathers device tensors directly (NVLink / NVSwitch).  Under gloo (CPU tests, or a
+    single-GPU dry run of several ranks) a device tensor is staged through host memory."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     t = t.contiguous()
-    out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-    dist.all_gather_into_tensor(out, t, group=group)
-    return out.view((world,) + tuple(t.shape))
+    staged = t.is_cuda and dist.get_backend(group) == "gloo"
+    src = t.cpu() if staged else t
+    out = torch.empty((world * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    out = out.view((world,) + tuple(src.shape))
+    return out.to(t.device, non_blocking=True) if staged else out
 
 
 def summarize_by_length(q, k_shard, v_shard, shard_offsets, user_len, *, attn="softmax", group=None,
                         backend=None, total_len=None):
     """Rank-local shard (this rank's range of every user) -> merged summary of every user on every
     rank.  shard_offsets: int64 [B+1] (device), user_len: int64 [B] total L_u (device, QLA 1/N).
-    One all_gather of the partials (softmax: O_p [B,H,S,d] + lse_p [B,H,S]; QLA: Z_p [B,H,d,d])."""
-    import torch
-    import torch.distributed as dist
+    One all_gather of the partials (softmax: O_p [B,H,S,d] + lse_p [B,H,S]; QLA: Z_p [B,H,d,d]).
+    No host synchronization: the step is capturable in a CUDA graph (NCCL)."""
     backend = backend or CudaBackend()
     a = _attn_code(attn)
-    world = dist.get_world_size(group)
     if total_len is None:
         total_len = k_shard.shape[0]
     po, pl = backend.partial(q, k_shard, v_shard, shard_offsets, total_len, a)
@@ -144,63 +148,113 @@ def summarize_by_length(q, k_shard, v_shard, shard_offsets, user_len, *, attn="s
     return backend.merge(go, gl, q, a, user_len)
 
 
+class FlatPlan:
+    """Host-side plan of the flat (item-stream) exchange for one rank, built once per partition.
+
+    Every rank knows the whole partition, so it knows -- without communicating -- which boundary
+    slot of which rank carries which straddling user: rank g sends its first segment in slot 0 and
+    its last in slot 1 when they are incomplete.  The plan holds the device index tensors that
+    (1) gather the rank's complete segments for one merge call and (2) gather each owned
+    straddling user's parts from the all_gathered slots, padded to the largest part count with a
+    null slot (lse = -inf / Z = 0, the identity of either merge), for a second merge call.  No
+    step ever reads a device value on the host."""
+
+    def __init__(self, all_segments: list[list[Segment]], lengths, rank: int, device, q_per_user: bool = False):
+        import torch
+        lengths = np.asarray(lengths, dtype=np.int64)
+        world = len(all_segments)
+        self.world, self.rank = world, rank
+        self.segments = segs = all_segments[rank]
+        seg_len = np.array([s.end - s.start for s in segs], dtype=np.int64)
+        off = np.zeros(len(segs) + 1, dtype=np.int64)
+        np.cumsum(seg_len, out=off[1:])
+        self.total_len = int(off[-1])
+        self.offsets = torch.as_tensor(off, device=device)
+        self.seg_users = torch.as_tensor([s.user for s in segs], dtype=torch.int64, device=device)
+        self.q_per_user = q_per_user
+
+        def complete(s):
+            return s.start == 0 and s.end == int(lengths[s.user])
+
+        def slots_of(g):  # [(slot, local segment index)] rank g sends
+            sg = all_segments[g]
+            ends = [0] if len(sg) == 1 else ([0, len(sg) - 1] if sg else [])
+            return [(sl, j) for sl, j in enumerate(ends) if not complete(sg[j])]
+
+        self.send = slots_of(rank)
+        owner = {}
+        for g in range(world):
+            for s in all_segments[g]:
+                owner.setdefault(s.user, g)
+        comp = [j for j, s in enumerate(segs) if complete(s)]
+        self.comp_users = [segs[j].user for j in comp]
+        self.comp_idx = torch.as_tensor(comp, dtype=torch.int64, device=device)
+        self.comp_len = torch.as_tensor([int(lengths[u]) for u in self.comp_users], dtype=torch.int64, device=device)
+        parts: dict[int, list[int]] = {}
+        for g in range(world):
+            for sl, j in slots_of(g):
+                u = all_segments[g][j].user
+                if owner[u] == rank:
+                    parts.setdefault(u, []).append(2 * g + sl)  # ascending rank order
+        self.str_users = sorted(parts)
+        pmax = max((len(v) for v in parts.values()), default=0)
+        null = 2 * world
+        gidx = np.full((pmax, len(self.str_users)), null, dtype=np.int64)
+        for n, u in enumerate(self.str_users):
+            gidx[:len(parts[u]), n] = parts[u]
+        self.str_gidx = torch.as_tensor(gidx, device=device)
+        self.str_users_t = torch.as_tensor(self.str_users, dtype=torch.int64, device=device)
+        self.str_len = torch.as_tensor([int(lengths[u]) for u in self.str_users], dtype=torch.int64, device=device)
+
+
 def summarize_flat(q, k_local, v_local, segments: list[Segment], all_segments: list[list[Segment]], lengths, *,
-                   attn="softmax", group=None, backend=None):
+                   attn="softmax", group=None, backend=None, plan: FlatPlan | None = None):
     """Flat (item-stream) sharding.  k_local / v_local hold this rank's segments back to back.
     Returns {user: (out [S,H,d], lse [H,S] or None)} for the users this rank OWNS (a straddling user
     is owned by the lowest rank holding part of it).  Only straddling users' partials are exchanged
-    (one all_gather of two fixed-size boundary slots per rank)."""
+    (one all_gather of two fixed-size boundary slots per rank).  q: shared seeds [S,H,d] or
+    per-user seeds [B,S,H,d] (each segment then uses its own user's seeds).  Pass a prebuilt
+    `plan` (FlatPlan) on the hot path; the step then does no host-side work beyond launches."""
     import torch
     import torch.distributed as dist
     backend = backend or CudaBackend()
     a = _attn_code(attn)
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    lengths = np.asarray(lengths, dtype=np.int64)
-    dev = k_local.device
-    seg_len = np.array([s.end - s.start for s in segments], dtype=np.int64)
-    off = np.zeros(len(segments) + 1, dtype=np.int64)
-    np.cumsum(seg_len, out=off[1:])
-    off_t = torch.as_tensor(off, device=dev)
-    po, pl = backend.partial(q, k_local, v_local, off_t, int(off[-1]), a)
-
-    def complete(s):
-        return s.start == 0 and s.end == int(lengths[s.user])
-
-    owner = {}
-    for g in range(world):
-        for s in all_segments[g]:
-            owner.setdefault(s.user, g)
-    # boundary slots: the first and last segment of every rank, if incomplete
+    rank = dist.get_rank(group)
+    per_user = q.dim() == 4
+    if plan is None:
+        plan = FlatPlan(all_segments, lengths, rank, k_local.device, per_user)
+    q_seg = q.index_select(0, plan.seg_users.to(q.device)) if per_user else q
+    po, pl = backend.partial(q_seg, k_local, v_local, plan.offsets.to(k_local.device), plan.total_len, a)
+    dev = po.device
     slot_shape = tuple(po.shape[1:])
     send_o = torch.zeros((2,) + slot_shape, dtype=po.dtype, device=dev)
     send_l = torch.full((2,) + tuple(pl.shape[1:]), float("-inf"), dtype=pl.dtype, device=dev) if a == 0 else None
-    send_u = torch.full((2,), -1, dtype=torch.int64, device=dev)
-    ends = [0] if len(segments) == 1 else ([0, len(segments) - 1] if segments else [])
-    for slot, j in enumerate(ends):
-        if not complete(segments[j]):
-            send_o[slot] = po[j]
-            if a == 0:
-                send_l[slot] = pl[j]
-            send_u[slot] = segments[j].user
-    recv_o = _all_gather(send_o, group)
-    recv_u = _all_gather(send_u, group)
-    recv_l = _all_gather(send_l, group) if a == 0 else None
-    ru = recv_u.cpu().numpy()
+    for slot, j in plan.send:
+        send_o[slot] = po[j]
+        if a == 0:
+            send_l[slot] = pl[j]
+    recv_o = _all_gather(send_o, group).reshape((-1,) + slot_shape)
+    recv_l = _all_gather(send_l, group).reshape((-1,) + tuple(pl.shape[1:])) if a == 0 else None
     results = {}
-    comp = [j for j, s in enumerate(segments) if complete(s)]  # complete -> owned here, merged in one call
-    if comp:
-        ci = torch.as_tensor(comp, device=dev)
-        ulen = torch.as_tensor([int(lengths[segments[j].user]) for j in comp], dtype=torch.int64, device=dev)
-        out, lse = backend.merge(po[ci][None], None if a else pl[ci][None], q, a, ulen)
-        for n, j in enumerate(comp):
-            results[segments[j].user] = (out[n], None if lse is None else lse[n])
-    for j, s in enumerate(segments):
-        if complete(s) or owner[s.user] != rank:
-            continue
-        sel = [(g, sl) for g in range(world) for sl in range(2) if ru[g, sl] == s.user]
-        parts_o = torch.stack([recv_o[g, sl] for g, sl in sel])
-        parts_l = torch.stack([recv_l[g, sl] for g, sl in sel]) if a == 0 else None
-        ulen = torch.as_tensor([int(lengths[s.user])], dtype=torch.int64, device=dev)
-        out, lse = backend.merge(parts_o[:, None], None if parts_l is None else parts_l[:, None], q, a, ulen)
-        results[s.user] = (out[0], None if lse is None else lse[0])
+    if plan.comp_users:
+        ci = plan.comp_idx.to(dev)
+        qc = q_seg.index_select(0, ci) if per_user else q
+        out, lse = backend.merge(po.index_select(0, ci)[None], None if a else pl.index_select(0, ci)[None], qc, a,
+                                 plan.comp_len.to(dev))
+        for n, u in enumerate(plan.comp_users):
+            results[u] = (out[n], None if lse is None else lse[n])
+    if plan.str_users:
+        # null slot (index 2 * world): the identity of the merge (lse -inf / Z = 0)
+        flat_o = torch.cat([recv_o, torch.zeros((1,) + slot_shape, dtype=recv_o.dtype, device=dev)])
+        gidx = plan.str_gidx.to(dev)
+        parts_o = flat_o[gidx]
+        parts_l = None
+        if a == 0:
+            flat_l = torch.cat([recv_l, torch.full((1,) + tuple(recv_l.shape[1:]), float("-inf"), dtype=recv_l.dtype,
+                                                   device=dev)])
+            parts_l = flat_l[gidx]
+        qs = q.index_select(0, plan.str_users_t.to(q.device)) if per_user else q
+        out, lse = backend.merge(parts_o, parts_l, qs, a, plan.str_len.to(dev))
+        for n, u in enumerate(plan.str_users):
+            results[u] = (out[n], None if lse is None else lse[n])
     return results

@@ -23,7 +23,7 @@ class OracleBackend:
         qn, kn, vn = q.numpy(), k.numpy(), v.numpy()
         off = offsets.numpy()
         if attn == 0:
-            out, lse = oracle.softmax_summarize(qn, kn, vn, off)
+            out, lse = oracle.softmax_summarize(qn, kn, vn, off, q_per_user=q.dim() == 4)
             return torch.from_numpy(out.transpose(0, 2, 1, 3).copy()), torch.from_numpy(lse)
         return torch.from_numpy(oracle.qla_state(kn, vn, off)), None
 
@@ -33,7 +33,7 @@ class OracleBackend:
             out, lse = oracle.merge_lse(po, part_lse.numpy())    # [B,H,S,d], [B,H,S]
             return torch.from_numpy(out.transpose(0, 2, 1, 3).copy()), torch.from_numpy(lse)
         z = oracle.merge_sum(po)
-        return torch.from_numpy(oracle.qla_finalize(q.numpy(), z, user_len.numpy())), None
+        return torch.from_numpy(oracle.qla_finalize(q.numpy(), z, user_len.numpy(), q_per_user=q.dim() == 4)), None
 
 
     def bwd(self, q, k, v, offsets, total_len, dout, attn, **kw):
@@ -53,7 +53,11 @@ def free_port():
     return p
 
 
-def _worker(rank, world, port, mode, attn, lens, result_q):
+def _per_user_q(B, S, H, d):
+    return (np.random.default_rng(77).integers(-128, 128, size=(B, S, H, d)) / 64.0).astype(np.float32)
+
+
+def _worker(rank, world, port, mode, attn, lens, result_q, per_user=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -62,6 +66,8 @@ def _worker(rank, world, port, mode, attn, lens, result_q):
         lens = np.asarray(lens, dtype=np.int64)
         off = synth.offsets_from_lengths(lens)
         q = torch.from_numpy(synth.make_q(S, H, d, seed=3, tau=2)).double()
+        if per_user:
+            q = torch.from_numpy(_per_user_q(len(lens), S, H, d)).double()
         be = OracleBackend()
         if mode == "by_length":
             cuts = vdist.partition_by_length(lens, world)
@@ -88,11 +94,11 @@ def _worker(rank, world, port, mode, attn, lens, result_q):
         dist.destroy_process_group()
 
 
-def run_world(world, mode, attn, lens):
+def run_world(world, mode, attn, lens, per_user=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, attn, lens, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, attn, lens, q, per_user)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=240) for _ in range(world)]
@@ -137,6 +143,27 @@ def test_flat_matches_unsplit(world, attn):
         for u, v in res[r].items():
             assert u not in owned, "a user is owned by exactly one rank"
             owned[u] = v
+    assert sorted(owned) == [u for u in range(len(lens)) if lens[u] > 0]
+    for u, (o, l) in owned.items():
+        np.testing.assert_allclose(o, ref[u], rtol=1e-11, atol=1e-12)
+        if attn == "softmax":
+            np.testing.assert_allclose(l, ref_lse[u], rtol=1e-12)
+
+
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_flat_per_user_seeds(attn):
+    """Flat sharding with per-user seeds q [B,S,H,d]: every segment (and every straddling user's
+    merge) uses its own user's seeds; 3 ranks so a user can straddle two boundaries."""
+    lens = [40, 3, 0, 90, 17, 5, 61]
+    res = run_world(3, "flat", attn, lens, per_user=True)
+    S, H, d = 6, 2, 8
+    _, k, v, off = synth.make_batch(lens, S, H, d, seed=3, tau=2)
+    q = _per_user_q(len(lens), S, H, d)
+    if attn == "softmax":
+        ref, ref_lse = oracle.softmax_summarize(q, k, v, off, q_per_user=True)
+    else:
+        ref, ref_lse = oracle.qla_summarize(q, k, v, off, q_per_user=True), None
+    owned = {u: v_ for r in range(3) for u, v_ in res[r].items()}
     assert sorted(owned) == [u for u in range(len(lens)) if lens[u] > 0]
     for u, (o, l) in owned.items():
         np.testing.assert_allclose(o, ref[u], rtol=1e-11, atol=1e-12)

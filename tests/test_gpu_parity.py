@@ -788,3 +788,130 @@ def test_qla_rows_edge_cases(cuda_lib):
     q = torch.zeros((0, 1, 128), dtype=torch.bfloat16, device="cuda")
     out = vista.qla_rows(k, k, off, 5, q, torch.tensor([0, 0], dtype=torch.int64, device="cuda"), 0)
     assert out.shape == (0, 1, 128)
+
+
+# ----------------------------------------------------------------------------- invariants / robustness (SURVEY §4 tier 3)
+def test_int8_exact_ties_bit_exact(cuda_lib):
+    """DESIGN.md R21 on the GPU: exact .5 ties (stored scale 1, zero point 0) round half to even, the
+    same codes as the oracle, through the separate quantizer and the bf16 path."""
+    vista = cuda_lib
+    x = np.zeros((4, 128), np.float32)
+    x[:, :2] = [-127.0, 127.0]
+    x[:, 2:12] = [0.5, 1.5, 2.5, 3.5, -0.5, -1.5, -2.5, -3.5, 126.5, -126.5]
+    want = np.zeros(128, np.int8)
+    want[:12] = [-127, 127, 0, 2, 2, 4, 0, -2, -2, -4, 126, -126]
+    rc, rs, rz = oracle.quantize_rows_int8(x)
+    for dtype in ("bf16", "f32"):
+        gc, gs, gz = vista.quantize_int8(to_dev(x, dtype))
+        torch.cuda.synchronize()
+        assert np.array_equal(gc.cpu().numpy(), rc) and np.all(rc == want[None])
+        assert np.all(gs.cpu().numpy() == 1.0) and np.all(gz.cpu().numpy() == 0.0)
+
+
+def _grid8(rng, shape, lo=-8, hi=9):
+    return (rng.integers(lo, hi, size=shape) / 8.0).astype(np.float32)
+
+
+def test_softmax_key_shift_large_logits(cuda_lib):
+    """Key shift K + 1 c^T (c = 8 in every channel, values exact in bf16): every row's logits move by
+    the constant scale q.c (~ +1000 with scale 1 and positive seeds), so O is unchanged and
+    lse moves by scale q.c.  Exercises the first-tile rescale of the online softmax with huge
+    logits; checked against the oracle on the shifted inputs and against the unshifted GPU run."""
+    vista = cuda_lib
+    rng = np.random.default_rng(71)
+    lens, S, H, d = [3000, 1, 129, 700], 256, 1, 128
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    q = (rng.integers(0, 17, size=(S, H, d)) / 8.0).astype(np.float32)   # >= 0: q.c ~ 8 * 128
+    k = _grid8(rng, (off[-1], H, d))
+    v = _grid8(rng, (off[-1], H, d)) + _grid8(rng, (1, H, d))
+    ks = k + 8.0
+    ot = torch.from_numpy(off).cuda()
+    o0, l0 = vista.summarize(to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16"), ot, int(off[-1]),
+                             scale=1.0, out_dtype=vista.F32)
+    o1, l1 = vista.summarize(to_dev(q, "bf16"), to_dev(ks, "bf16"), to_dev(v, "bf16"), ot, int(off[-1]),
+                             scale=1.0, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    ref, ref_lse = oracle.softmax_summarize(q, ks, v, off, scale=1.0)
+    check_softmax(o1, l1, ref, ref_lse, lens, "bf16")
+    shift = (q[:, 0].astype(np.float64) @ np.full(d, 8.0))  # [S]
+    assert shift.min() > 500
+    for u in range(len(lens)):
+        assert block_err(o1[u].cpu().numpy(), o0[u].cpu().numpy()) <= 2e-2
+        dl = l1[u, 0].double().cpu().numpy() - l0[u, 0].double().cpu().numpy()
+        # lse is float32 near 1000: its own rounding is ~6e-5; the shift is exact in float64
+        assert np.abs(dl - shift).max() <= 2e-3
+
+
+def test_softmax_duplication_adds_ln2(cuda_lib):
+    """Duplicating every history item leaves O unchanged and adds ln 2 to lse (P4(ii))."""
+    vista = cuda_lib
+    lens = [2500, 129, 1, 0]
+    q, k, v, off = synth.make_batch(lens, 256, 2, 128, seed=72)
+    lens2 = [2 * L for L in lens]
+    off2 = np.concatenate([[0], np.cumsum(lens2)]).astype(np.int64)
+    idx = np.concatenate([np.concatenate([np.arange(off[u], off[u + 1])] * 2) for u in range(len(lens))]).astype(np.int64)
+    ot, ot2 = torch.from_numpy(off).cuda(), torch.from_numpy(off2).cuda()
+    o1, l1 = vista.summarize(to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16"), ot, int(off[-1]), out_dtype=vista.F32)
+    o2, l2 = vista.summarize(to_dev(q, "bf16"), to_dev(k[idx], "bf16"), to_dev(v[idx], "bf16"), ot2, int(off2[-1]),
+                             out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    for u in range(3):
+        assert block_err(o2[u].cpu().numpy(), o1[u].cpu().numpy()) <= 2e-2
+        assert (l2[u] - l1[u] - np.log(2.0)).abs().max().item() <= 1e-3
+    assert torch.all(o2[3] == 0) and torch.all(l2[3] == -np.inf)
+
+
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_user_and_row_independence_bitwise(cuda_lib, attn):
+    """No leakage across users or seed rows: with the lengths (hence the stream-K partition) fixed,
+    replacing every OTHER user's history values, or one seed row's values, leaves the remaining
+    outputs bitwise unchanged (P4(iv), (v))."""
+    vista = cuda_lib
+    a = vista.SOFTMAX if attn == "softmax" else vista.QLA
+    lens = [4000, 300, 0, 9000, 128]
+    q, k, v, off = synth.make_batch(lens, 256, 2, 128, seed=73)
+    ot = torch.from_numpy(off).cuda()
+    run = lambda qq, kk, vv: vista.summarize(to_dev(qq, "bf16"), to_dev(kk, "bf16"), to_dev(vv, "bf16"), ot,  # noqa
+                                             int(off[-1]), attn=a, out_dtype=vista.F32)
+    o1, l1 = run(q, k, v)
+    _, k2, v2, _ = synth.make_batch(lens, 256, 2, 128, seed=74)
+    keep = slice(off[3], off[4])
+    k2[keep], v2[keep] = k[keep], v[keep]
+    o2, l2 = run(q, k2, v2)
+    q3 = q.copy()
+    q3[17] = q3[17][::-1].copy() * 0.5 + 0.25
+    o3, l3 = run(q3, k, v)
+    torch.cuda.synchronize()
+    assert torch.equal(o1[3], o2[3])
+    if attn == "softmax":
+        assert torch.equal(l1[3], l2[3])
+    rows = [i for i in range(256) if i != 17]
+    if attn == "qla":
+        assert torch.equal(o1[:, rows], o3[:, rows])
+    else:
+        # rows of other warps are bitwise unchanged; the 31 rows sharing row 17's warp share its
+        # warp-uniform rescale decision (DESIGN.md 4.1), so their p are taken against a possibly
+        # different running max: equal within rounding, not bitwise
+        other = [i for i in range(256) if i // 32 != 17 // 32]
+        assert torch.equal(o1[:, other], o3[:, other]) and torch.equal(l1[:, :, other], l3[:, :, other])
+        for u in (0, 1, 3, 4):
+            assert block_err(o3[u, rows].cpu().numpy(), o1[u, rows].cpu().numpy()) <= 1e-2
+
+
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_all_empty_batch_and_zero_users(cuda_lib, attn):
+    """Every user empty: softmax O = 0 and lse = -inf (R6); QLA O = phi1(Q) phi2(0) = 0 for SiLU.
+    B = 0: a valid no-op (no launch, VISTA_OK)."""
+    vista = cuda_lib
+    a = vista.SOFTMAX if attn == "softmax" else vista.QLA
+    q = to_dev(synth.make_q(256, 2, 128, seed=5), "bf16")
+    k = torch.zeros((0, 2, 128), dtype=torch.bfloat16, device="cuda")
+    off = torch.zeros(5, dtype=torch.int64, device="cuda")
+    o, l = vista.summarize(q, k, k, off, 0, attn=a, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    assert o.shape == (4, 256, 2, 128) and torch.all(o == 0)
+    if attn == "softmax":
+        assert torch.all(l == -np.inf)
+    o0, l0 = vista.summarize(q, k, k, torch.zeros(1, dtype=torch.int64, device="cuda"), 0, attn=a, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    assert o0.shape == (0, 256, 2, 128)

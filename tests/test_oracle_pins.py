@@ -395,6 +395,43 @@ def test_quantize_error_bound_and_special_rows():
     assert codes[r, np.argmax(x[r])] == 127 and codes[r, np.argmin(x[r])] == -127
 
 
+def _tie_row(d=128):
+    """A row with min -127, max +127 -> stored scale exactly 1.0 and zero point exactly 0.0, so
+    t = (x - zp) / s = x: the half-integers below are exact ties in float32 (R21)."""
+    x = np.zeros(d, np.float32)
+    x[:2] = [-127.0, 127.0]
+    ties = np.array([0.5, 1.5, 2.5, 3.5, -0.5, -1.5, -2.5, -3.5, 126.5, -126.5], np.float32)
+    x[2:2 + len(ties)] = ties
+    want = np.zeros(d, np.int64)
+    want[:2] = [-127, 127]
+    want[2:2 + len(ties)] = [0, 2, 2, 4, 0, -2, -2, -4, 126, -126]  # half to even
+    return x, want
+
+
+def test_quantize_exact_ties_round_half_to_even():
+    """R21 tie rule: an exact .5 goes to the even code (SPEC.md:342 says only "round"); values
+    exact in bf16 and f32, and the stored scale / zero point are exactly 1 and 0."""
+    x, want = _tie_row()
+    codes, scale, zp = oracle.quantize_rows_int8(x[None])
+    assert scale[0] == np.float32(1.0) and zp[0] == np.float32(0.0)
+    assert np.array_equal(codes[0].astype(np.int64), want)
+    # the bound with the STORED scale holds with equality at a tie (|2 - 2.5| = s/2)
+    deq = oracle.dequantize_rows_int8(codes, scale, zp)
+    assert np.max(np.abs(deq[0] - x)) == 0.5
+
+
+def test_quantize_bound_with_stored_scale():
+    """R21: the codes are decided from the stored float32 scale / zero point, so the SPEC.md:346
+    bound |code s + zp - x| <= s/2 holds for the values a consumer actually dequantizes with (up to
+    one float32 rounding of the dequantization itself), on rows with awkward ranges."""
+    rng = np.random.default_rng(9)
+    x = (rng.standard_normal((256, 128)) * rng.uniform(1e-3, 1e3, size=(256, 1))).astype(np.float32)
+    codes, scale, zp = oracle.quantize_rows_int8(x)
+    deq = codes.astype(np.float64) * scale.astype(np.float64)[:, None] + zp.astype(np.float64)[:, None]
+    slack = np.abs(x).max(1, keepdims=True) * 2.0 ** -23
+    assert np.all(np.abs(deq - x) <= scale[:, None] * 0.5 + slack)
+
+
 # ----------------------------------------------------------------------------- prefix (R18)
 def _prefix_case(seed, lens, P, S=5, H=2, d=8):
     rng = np.random.default_rng(seed)

@@ -7,6 +7,8 @@ target rows with the Delta self term), CPU only.
   R4 rows = the seeds of every user reproduces the seed-row summary (qla_summarize)
   R5 empty history: Z = 0, W = phi2(0) (0 for SiLU; e^-1 for shifted ELU, a closed form)
   R6 invariants: permutation of a user's history; linearity of the Delta term in v_self
+  R7 App. B's dense mixed form: phi = Id, 1/N -> source and target rows together equal
+     (Q K^T (.) M) V / N with M = [[1,0],[1,I_m]], one N for both kinds of row
 A dropped Delta term, a Delta without phi1 on either side, a transposed state or rows assigned to
 the wrong user fails at least one of them.
 """
@@ -63,6 +65,13 @@ def test_r2_delta_is_attention_to_itself():
 def test_r3_worked_scalars():
     for e in json.load(open(GOLDEN))["qla_target_scalar"]:
         one = lambda x: np.array([[[x]]], np.float32)  # noqa: E731
+        if "k_hist" in e:  # several source items, App. B's 1/N
+            col = lambda xs: np.array(xs, np.float32).reshape(-1, 1, 1)  # noqa: E731
+            n = len(e["k_hist"])
+            got = oracle.qla_rows(one(e["q_t"]), [0, 1], col(e["k_hist"]), col(e["v_hist"]), [0, n], e["phi1"],
+                                  e["phi2"], e["normalize"], k_self=one(e["k_t"]), v_self=one(e["v_t"]))
+            assert abs(got[0, 0, 0] - e["value"]) <= 1e-12, (e, got)
+            continue
         got = oracle.qla_rows(one(e["q_t"]), [0, 1], one(e["k"]), one(e["v"]), [0, 1], e["phi1"], e["phi2"],
                               e["normalize"], k_self=one(e["k_t"]), v_self=one(e["v_t"]))
         assert abs(got[0, 0, 0] - e["value"]) <= 1e-12, (e, got)
@@ -77,7 +86,13 @@ def test_r3_silu_scalar_closed_form():
     one = lambda x: np.array([[[x]]], np.float32)  # noqa: E731
     got = oracle.qla_rows(one(2.0), [0, 1], one(3.0), one(5.0), [0, 1], "silu", "silu", True,
                           k_self=one(3.0), v_self=one(5.0))
-    want = silu(2.0) * silu(silu(3.0) * 5.0 / 1.0) + silu(2.0) * silu(3.0) * 5.0
+    want = silu(2.0) * silu(silu(3.0) * 5.0 / 1.0) + silu(2.0) * silu(3.0) * 5.0 / 1.0
+    assert abs(got[0, 0, 0] - want) <= 1e-12 * abs(want)
+    # two source items (N = 2): the Delta term is halved with the state (App. B)
+    k2, v2 = np.array([3.0, -1.0], np.float32).reshape(2, 1, 1), np.array([5.0, 2.0], np.float32).reshape(2, 1, 1)
+    got = oracle.qla_rows(one(2.0), [0, 1], k2, v2, [0, 2], "silu", "silu", True, k_self=one(3.0), v_self=one(5.0))
+    z = (silu(3.0) * 5.0 + silu(-1.0) * 2.0) / 2.0
+    want = silu(2.0) * silu(z) + silu(2.0) * silu(3.0) * 5.0 / 2.0
     assert abs(got[0, 0, 0] - want) <= 1e-12 * abs(want)
 
 
@@ -123,3 +138,29 @@ def test_r6_invariants():
     no_delta = oracle.qla_rows(q, roff, k, v, off, "silu", "silu", True)
     twice = oracle.qla_rows(q, roff, k, v, off, "silu", "silu", True, k_self=ks, v_self=2 * vs)
     np.testing.assert_allclose(twice - no_delta, 2 * (base - no_delta), rtol=0, atol=1e-12)
+
+
+def test_r7_appendix_b_dense_mixed_form():
+    """SPEC.md:186's kernel equivalence: phi = Id with 1/N, every user's source rows (no Delta) and
+    target rows (Delta) equal the dense (Q K^T (.) M) V / N of App. B, M = [[1_nn, 0], [1_mn, I_m]],
+    N = n = the user's source length (one scalar for the whole product)."""
+    rng = np.random.default_rng(7)
+    lens, ntgt, H, d = [6, 3, 11], [4, 1, 5], 2, 8
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    toff = np.concatenate([[0], np.cumsum(ntgt)]).astype(np.int64)
+    ks, vs, qs = grid(rng, (off[-1], H, d)), grid(rng, (off[-1], H, d)), grid(rng, (off[-1], H, d))
+    qt, kt, vt = grid(rng, (toff[-1], H, d)), grid(rng, (toff[-1], H, d)), grid(rng, (toff[-1], H, d))
+    src = oracle.qla_rows(qs, off, ks, vs, off, "identity", "identity", True)
+    tgt = oracle.qla_rows(qt, toff, ks, vs, off, "identity", "identity", True, k_self=kt, v_self=vt)
+    for u in range(len(lens)):
+        n, m = lens[u], ntgt[u]
+        M = np.zeros((n + m, n + m))
+        M[:, :n] = 1.0
+        M[n:, n:] = np.eye(m)
+        for h in range(H):
+            Q = np.concatenate([qs[off[u]:off[u + 1], h], qt[toff[u]:toff[u + 1], h]]).astype(np.float64)
+            K = np.concatenate([ks[off[u]:off[u + 1], h], kt[toff[u]:toff[u + 1], h]]).astype(np.float64)
+            V = np.concatenate([vs[off[u]:off[u + 1], h], vt[toff[u]:toff[u + 1], h]]).astype(np.float64)
+            O = ((Q @ K.T) * M) @ V / n
+            np.testing.assert_allclose(src[off[u]:off[u + 1], h], O[:n], rtol=0, atol=1e-12)
+            np.testing.assert_allclose(tgt[toff[u]:toff[u + 1], h], O[n:], rtol=0, atol=1e-12)

@@ -28,10 +28,17 @@ template <typename F>
 cudaError_t timed_main(cudaStream_t s, F&& launch) {
     cudaEvent_t a = g_ev_start, b = g_ev_stop;
     g_ev_start = g_ev_stop = nullptr;
+    // under stream capture the records become external event nodes: the graph records them at
+    // every replay (a plain record in a capture is only an internal dependency)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    const unsigned flags =
+        (a || b) && cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive
+            ? cudaEventRecordExternal
+            : cudaEventRecordDefault;
     cudaError_t e;
-    if (a && (e = cudaEventRecord(a, s)) != cudaSuccess) return e;
+    if (a && (e = cudaEventRecordWithFlags(a, s, flags)) != cudaSuccess) return e;
     e = launch();
-    if (e == cudaSuccess && b) e = cudaEventRecord(b, s);
+    if (e == cudaSuccess && b) e = cudaEventRecordWithFlags(b, s, flags);
     return e;
 }
 
@@ -120,7 +127,8 @@ Path choose_path(const Problem& p) {
     return tma_ok ? PATH_SM100_QLA : PATH_SIMT_QLA;
 }
 
-int sm100_softmax_nq(int S);
+int sm100_softmax_cluster(int S);
+int sm100_softmax_num_clusters(const Problem& p);
 
 Workspace plan_workspace(const Problem& p, bool partial) {
     (void)partial;
@@ -131,7 +139,11 @@ Workspace plan_workspace(const Problem& p, bool partial) {
     w.rows_per_unit = 0;
     if (path == PATH_SM100_SOFTMAX || path == PATH_SM100_QLA) {
         w.num_ctas = p.num_sms;
-        w.rows_per_unit = path == PATH_SM100_SOFTMAX ? sm100_softmax_nq(p.S) * 128 : 128;
+        w.rows_per_unit = 128;
+        if (path == PATH_SM100_SOFTMAX) {  // persistent grid of clusters, C * 128 query rows per unit
+            w.num_ctas = sm100_softmax_num_clusters(p);
+            w.rows_per_unit = sm100_softmax_cluster(p.S) * 128;
+        }
     }
     w.uts_off = off;
     off = align256(off + (size_t)(p.B + 1) * sizeof(int64_t));
@@ -199,9 +211,10 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
     vista_status_t st = validate_desc(desc);
     if (st != VISTA_OK) return st;
     if (total_len < 0) return VISTA_ERR_INVALID;
-    if (!q || !offsets || !outs.out) return VISTA_ERR_NULL;
+    if (!q || !offsets || (!outs.out && desc->num_users > 0)) return VISTA_ERR_NULL;  // B = 0: nothing to write
     if (total_len > 0 && (!k || !v)) return VISTA_ERR_NULL;
-    if (outs.mode == OUT_PARTIAL && desc->attn == VISTA_SOFTMAX && !outs.lse) return VISTA_ERR_NULL;
+    if (outs.mode == OUT_PARTIAL && desc->attn == VISTA_SOFTMAX && !outs.lse && desc->num_users > 0)
+        return VISTA_ERR_NULL;
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(outs.out)) return VISTA_ERR_MISALIGNED;
     if (outs.lse && (reinterpret_cast<uintptr_t>(outs.lse) & 3)) return VISTA_ERR_MISALIGNED;
     Problem p = make_problem(desc, total_len);

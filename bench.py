@@ -156,8 +156,9 @@ def run_own(args, rank, world, local_rank):
     if args.backward:
         wdesc += " backward (NEXT-2, from the forward's saved " + ("out, lse)" if args.attn == "softmax" else "state Z)")
     if args.qla_rows:
-        wdesc += (" QLA history rows (NEXT-3: every item a query row of its user)" if args.qla_rows == "history"
-                  else f" QLA target rows (NEXT-4: {TARGETS_PER_USER} targets per user, Delta self term)")
+        wdesc += (" QLA history rows from the saved state (NEXT-3: every item a query row of its user)"
+                  if args.qla_rows == "history"
+                  else f" QLA target rows from the saved state (NEXT-4: {TARGETS_PER_USER} targets per user, Delta self term)")
     attn = vista.SOFTMAX if args.attn == "softmax" else vista.QLA
     mode = args.mode or {"c2": "by_user", "c3": "by_user", "c4": "by_length", "c5": "flat"}[args.config]
     if (world == 1 or args.qla_rows) and mode != "by_user":
@@ -235,14 +236,19 @@ def run_own(args, rank, world, local_rank):
                 roff_t = torch.arange(B + 1, dtype=torch.int64, device=dev) * TARGETS_PER_USER
                 q_rows, k_self, v_self = grid((n_rows, H, d)), grid((n_rows, H, d)), grid((n_rows, H, d))
             rows_out = torch.empty((n_rows, H, d), dtype=torch.bfloat16, device=dev)
-            rws_bytes = vista.vista_qla_rows_workspace_size(desc, total, n_rows)
+            # the layer's state is computed once (the summarization pass, outside the timed step) and
+            # reused by the rows: "can be computed first, then multiplied with Q[S]_l, Q[T]_l"
+            z_state = torch.empty((B, H, d, d), dtype=torch.float32, device=dev)
+            vista.vista_summarize_partial(desc, q, K, V, off_t, total, z_state, None, ws, ws_bytes, None)
+            ulen_t = torch.from_numpy(np.asarray(lens, dtype=np.int64)).to(dev)
+            rws_bytes = vista.vista_qla_rows_from_state_workspace_size(desc, n_rows)
             rws = torch.empty(max(rws_bytes, 16), dtype=torch.uint8, device=dev)
-            inputs = [K, V, off_t, q_rows, roff_t] + ([k_self, v_self] if k_self is not None else [])
+            inputs = [z_state, ulen_t, q_rows, roff_t] + ([k_self, v_self] if k_self is not None else [])
 
             def step(ins=inputs):
-                ks, vs = (ins[5], ins[6]) if len(ins) > 5 else (None, None)
-                vista.vista_qla_rows(desc, ins[0], ins[1], ins[2], total, ins[3], ins[4], n_rows, ks, vs, rows_out,
-                                     rws, rws_bytes, None)
+                ks, vs = (ins[4], ins[5]) if len(ins) > 4 else (None, None)
+                vista.vista_qla_rows_from_state(desc, ins[0], ins[1], ins[2], ins[3], n_rows, ks, vs, rows_out,
+                                                rws, rws_bytes, None)
                 return [rows_out]
         items_per_step = world * total
         scaling = "weak"

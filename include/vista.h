@@ -223,6 +223,26 @@ vista_status_t vista_qla_rows(const vista_desc_t* desc, const void* k, const voi
                               size_t workspace_bytes, void* stream);
 
 /*
+ * QLA rows from a state computed once (App. B: "sum_j K[S]_j^T V[S]_j can be computed
+ * first, then multiplied with Q[S]_l, Q[T]_l"): exactly vista_qla_rows, but the user states come in
+ * instead of the histories, so one state pass (vista_summarize_partial, QLA; or an all-reduced sum
+ * of shards' states) serves the seed rows, the history rows and the target rows of a layer.
+ *   z          float32 [B, H, d, d], Z_u = sum_j phi1(k_j)^T v_j, NOT divided by N_u (DEVICE)
+ *   user_len   int64 [B] (DEVICE): N_u, the 1/N of the state and of the Delta term when
+ *              desc->qla_normalize (readings R10, R20)
+ *   q_rows, row_offsets, total_rows, k_self, v_self, out: as vista_qla_rows.
+ * Workspace: at least vista_qla_rows_from_state_workspace_size bytes (W_u operands and tile starts).
+ * B = 0 or total_rows = 0: no-op.  Asynchronous on stream; deterministic.
+ */
+vista_status_t vista_qla_rows_from_state_workspace_size(const vista_desc_t* desc, int64_t total_rows,
+                                                        size_t* bytes);
+vista_status_t vista_qla_rows_from_state(const vista_desc_t* desc, const float* z, const int64_t* user_len,
+                                         const void* q_rows, const int64_t* row_offsets,
+                                         int64_t total_rows, const void* k_self, const void* v_self,
+                                         void* out, void* workspace, size_t workspace_bytes,
+                                         void* stream);
+
+/*
  * QLA backward from the forward's saved state (saves the Z recompute): z_saved = Z_u = sum_j
  * phi1(k_j)^T v_j, float32 [B, H, d, d], not divided by N_u -- exactly what vista_summarize_partial
  * returns for QLA on the same k, v, offsets.  Everything else as vista_summarize_bwd (QLA);

@@ -28,6 +28,7 @@ __all__ = [
     "vista_summarize_prefix_workspace_size", "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
     "vista_summarize_bwd_workspace_size", "vista_summarize_bwd", "vista_summarize_fwd_int8",
     "vista_qla_rows_workspace_size", "vista_qla_rows", "vista_summarize_bwd_qla_saved",
+    "vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state", "qla_rows_from_state",
     "summarize", "summarize_partial", "summarize_merge", "summarize_bwd", "qla_rows",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
@@ -101,6 +102,8 @@ def load():
     lib.vista_summarize_bwd_qla_saved.argtypes = [DP, P, P, P, P, i64, P, P, P, P, P, P, sz, P]
     lib.vista_qla_rows_workspace_size.argtypes = [DP, i64, i64, ctypes.POINTER(sz)]
     lib.vista_qla_rows.argtypes = [DP, P, P, P, i64, P, P, i64, P, P, P, P, sz, P]
+    lib.vista_qla_rows_from_state_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
+    lib.vista_qla_rows_from_state.argtypes = [DP, P, P, P, P, i64, P, P, P, P, sz, P]
     lib.vista_summarize_fwd_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_partial_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge_workspace_size.argtypes = [DP, ctypes.POINTER(sz)]
@@ -111,7 +114,8 @@ def load():
     lib.vista_time_next_main_kernel.argtypes = [P, P]
     lib.vista_time_next_main_kernel.restype = ctypes.c_int
     lib.vista_launch_counter.restype = ctypes.c_uint64
-    for f in ("vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
+    for f in ("vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state",
+              "vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
               "vista_summarize_merge", "vista_check_offsets", "vista_summarize_prefix_workspace_size",
               "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
               "vista_summarize_bwd_workspace_size", "vista_summarize_bwd", "vista_summarize_fwd_int8"):
@@ -248,6 +252,21 @@ def vista_qla_rows(desc, k, v, offsets, total_len, q_rows, row_offsets, total_ro
                                  _ptr(row_offsets), int(total_rows), _ptr(k_self), _ptr(v_self), _ptr(out),
                                  _ptr(workspace), int(workspace_bytes), _stream(stream)),
            "vista_qla_rows")
+
+
+def vista_qla_rows_from_state_workspace_size(desc, total_rows) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load().vista_qla_rows_from_state_workspace_size(ctypes.byref(desc), int(total_rows), ctypes.byref(n)),
+           "vista_qla_rows_from_state_workspace_size")
+    return n.value
+
+
+def vista_qla_rows_from_state(desc, z, user_len, q_rows, row_offsets, total_rows, k_self, v_self, out, workspace,
+                              workspace_bytes, stream=None):
+    _check(load().vista_qla_rows_from_state(ctypes.byref(desc), _ptr(z), _ptr(user_len), _ptr(q_rows),
+                                            _ptr(row_offsets), int(total_rows), _ptr(k_self), _ptr(v_self), _ptr(out),
+                                            _ptr(workspace), int(workspace_bytes), _stream(stream)),
+           "vista_qla_rows_from_state")
 
 
 def vista_summarize_merge_workspace_size(desc: Desc) -> int:
@@ -427,6 +446,27 @@ def qla_rows(k, v, offsets, total_len, q_rows, row_offsets, total_rows=None, *, 
         torch.empty(max(need, 16), dtype=torch.uint8, device=q_rows.device)
     vista_qla_rows(desc, k, v, offsets, total_len, q_rows, row_offsets, total_rows, k_self, v_self, out, ws,
                    ws.numel(), stream)
+    return out
+
+
+def qla_rows_from_state(z, user_len, q_rows, row_offsets, total_rows=None, *, k_self=None, v_self=None,
+                        phi1="silu", phi2="silu", normalize=True, out_dtype=None, workspace=None, stream=None):
+    """QLA rows from saved states z [B,H,d,d] (f32, unnormalized; e.g. summarize_partial(..., attn=QLA)[0])
+    and user_len [B] (int64 N_u): the same rows as qla_rows without re-reading the histories."""
+    import torch
+    if total_rows is None:
+        total_rows = q_rows.shape[0]
+    B = z.shape[0]
+    H, d = q_rows.shape[-2:]
+    desc = make_desc(B, 1, H, d, in_dtype=_dtype_code(q_rows), out_dtype=out_dtype, attn=QLA, phi1=phi1, phi2=phi2,
+                     normalize=normalize)
+    odt = torch.bfloat16 if desc.out_dtype == BF16 else torch.float32
+    out = torch.empty((q_rows.shape[0], H, d), dtype=odt, device=q_rows.device)
+    need = vista_qla_rows_from_state_workspace_size(desc, total_rows)
+    ws = workspace if workspace is not None and workspace.numel() >= need else \
+        torch.empty(max(need, 16), dtype=torch.uint8, device=q_rows.device)
+    vista_qla_rows_from_state(desc, z, user_len, q_rows, row_offsets, total_rows, k_self, v_self, out, ws, ws.numel(),
+                              stream)
     return out
 
 

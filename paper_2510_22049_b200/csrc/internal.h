@@ -140,13 +140,15 @@ cudaError_t launch_add_prefix_state(const Problem& p, float* z, const float* zpr
 // tensor-core finalize (bf16, d = 128); ws: sm100_qla_finalize_workspace(p) bytes
 size_t sm100_qla_finalize_workspace(const Problem& p);
 // QLA at per-user query rows (NEXT-3 / NEXT-4, sm100_qla_rows.cu)
-cudaError_t launch_qla_prep_w(const Problem& p, const float* z, uint8_t* wbuf);
+// W_u = phi2(Z_u / N_u) operands; N_u = user_len[u] if given, else from p.offsets
+cudaError_t launch_qla_prep_w(const Problem& p, const float* z, uint8_t* wbuf, const int64_t* user_len = nullptr);
 bool qla_rows_uses_tc(const Problem& p, int64_t total_rows);
 cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, int64_t total_rows, const int64_t* uts,
                                   const uint8_t* w_op, const void* q, const void* k_self, const void* v_self,
-                                  int out_bf16, void* out);
+                                  int out_bf16, void* out, const int64_t* user_len = nullptr);
 cudaError_t launch_qla_rows_simt(const Problem& p, const float* z, const int64_t* row_offsets, int64_t total_rows,
-                                 const void* q, const void* k_self, const void* v_self, int out_bf16, void* out);
+                                 const void* q, const void* k_self, const void* v_self, int out_bf16, void* out,
+                                 const int64_t* user_len = nullptr);
 cudaError_t launch_sm100_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
                                       const int64_t* user_len, void* ws);
 cudaError_t launch_quantize_rows(int64_t n, int d, int in_bf16, const void* x, int8_t* codes, float* scale, float* zp,

@@ -15,6 +15,18 @@ __device__ __forceinline__ float qla_act(int kind, float x) {
     return x;
 }
 
+// SiLU on a bf16x2 pair with packed bf16 math: x * (0.5 + 0.5 tanh(x / 2)) -- 4 instructions per
+// pair (HMUL2, MUFU.TANH bf16x2, HFMA2, HMUL2), one MUFU op for two values.  Used where the result is
+// a bf16 MMA operand anyway (phi1 of K and of query rows).
+__device__ __forceinline__ uint32_t qla_silu_bf16x2(uint32_t x) {
+    uint32_t h, t, s, y;
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(h) : "r"(x), "r"(0x3F003F00u));
+    asm("tanh.approx.bf16x2 %0, %1;" : "=r"(t) : "r"(h));
+    asm("fma.rn.bf16x2 %0, %1, %2, %2;" : "=r"(s) : "r"(t), "r"(0x3F003F00u));
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(y) : "r"(x), "r"(s));
+    return y;
+}
+
 // byte offset of element (row, col) of a [128][128] bf16 operand in two swizzled halves: 16-B chunk
 // index XOR (row mod 8) within each 128-B row
 __device__ __forceinline__ uint32_t qla_w_swz(int row, int col) {

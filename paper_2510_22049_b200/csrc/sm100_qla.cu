@@ -67,20 +67,9 @@ __device__ __forceinline__ uint32_t phi_bf16x2(int kind, uint32_t w) {
     return ptx::pack_bf16x2(phi(kind, lo), phi(kind, hi));
 }
 
-// SiLU on a bf16x2 pair with packed bf16 math: x * (0.5 + 0.5 tanh(x / 2)) -- 4 instructions per
-// pair (HMUL2, MUFU.TANH bf16x2, HFMA2, HMUL2).  The result is bf16 anyway (it is the MMA operand).
-__device__ __forceinline__ uint32_t silu_bf16x2(uint32_t x) {
-    uint32_t h, t, s, y;
-    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(h) : "r"(x), "r"(0x3F003F00u));
-    asm("tanh.approx.bf16x2 %0, %1;" : "=r"(t) : "r"(h));
-    asm("fma.rn.bf16x2 %0, %1, %2, %2;" : "=r"(s) : "r"(t), "r"(0x3F003F00u));
-    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(y) : "r"(x), "r"(s));
-    return y;
-}
-
 template <int PHI>
 __device__ __forceinline__ uint32_t phi2x(uint32_t w) {
-    if constexpr (PHI == VISTA_ACT_SILU) return silu_bf16x2(w);
+    if constexpr (PHI == VISTA_ACT_SILU) return qla_silu_bf16x2(w);
     else if constexpr (PHI == VISTA_ACT_SHIFTED_ELU) return phi_bf16x2(VISTA_ACT_SHIFTED_ELU, w);
     else return w;
 }
@@ -275,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // same packed activation as the K transform (phi2x): W is a bf16 operand
                             const uint32_t zz = ptx::pack_bf16x2(__uint_as_float(r[8 * q + 2 * e]) * inv,
                                                                  __uint_as_float(r[8 * q + 2 * e + 1]) * inv);
-                            pw[e] = P.phi2 == VISTA_ACT_SILU ? silu_bf16x2(zz)
+                            pw[e] = P.phi2 == VISTA_ACT_SILU ? qla_silu_bf16x2(zz)
                                   : P.phi2 == VISTA_ACT_SHIFTED_ELU ? phi_bf16x2(VISTA_ACT_SHIFTED_ELU, zz)
                                                                     : zz;
                         }

@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(128) sm100_qla_finalize_kernel(const uint8_t* 
 }  // namespace
 
 // W_u operands for the rows path (sm100_qla_rows.cu): W = phi2(Z / N_u) from one state [B,H,d,d]
-cudaError_t launch_qla_prep_w(const Problem& p, const float* z, uint8_t* wbuf) {
-    qla_prep_w_kernel<<<p.B * p.H * 4, 256, 0, p.stream>>>(z, 1, 0, p.offsets, nullptr, p.H, p.phi2, p.normalize, wbuf);
+cudaError_t launch_qla_prep_w(const Problem& p, const float* z, uint8_t* wbuf, const int64_t* user_len) {
+    qla_prep_w_kernel<<<p.B * p.H * 4, 256, 0, p.stream>>>(z, 1, 0, p.offsets, user_len, p.H, p.phi2, p.normalize, wbuf);
     return cudaGetLastError();
 }
 

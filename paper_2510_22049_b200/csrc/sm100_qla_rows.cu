@@ -12,11 +12,13 @@
 // rows' jagged layout (work.cuh), one 128x128x128 tcgen05 GEMM per tile with W_u as the B operand.
 // HBM-bound: per row-head 256 B of q read and 256 B (bf16) of o written (+ 512 B of k_self, v_self
 // with the Delta term), 2 d^2 = 32,768 flop.
-//   warp 0        TMA producer: Q tiles (3 stages, freed by the MMA commit); W_u (bulk copy) per unit
+//   warp 0        TMA producer: q tiles (history rows: 3 stages of 32 KB) or q, k_self, v_self tiles
+//                 (target rows: 2 stages of 96 KB); W_u (bulk copy) per unit
 //   warp 1        MMA issuer; O double-buffered in TMEM
-//   warps 4..7    transform: phi1(Q) in place (bf16)
-//   warps 8..15   epilogue: TMEM -> (+ Delta) -> rows (bf16 coalesced through a TMEM round trip, or
-//                 f32); two warps per TMEM lane quarter, 64 columns each
+//   warps 4..7    transform: phi1(Q) in place (bf16), one row per thread; with Delta also the row dot
+//                 phi1(q) . phi1(k_self) (/ N_u) from the staged k tile, into shared memory
+//   warps 8..15   epilogue: TMEM (+ d_r v_self_r from the staged v tile) -> rows (bf16 coalesced
+//                 through a TMEM round trip, or f32); two warps per TMEM lane quarter, 64 columns each
 // qla_rows_simt_kernel: CUDA-core path for f32 inputs or d in {32, 64} (one block per (row, head)).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -34,20 +36,26 @@ namespace {
 
 constexpr int kHalf = 128 * 128;  // one 64-column half of a 128 x 128 bf16 tile
 constexpr int kTile = 2 * kHalf;  // 32 KB
-#ifndef VISTA_ROWS_STAGES
-#define VISTA_ROWS_STAGES 3
-#endif
-constexpr int kStages = VISTA_ROWS_STAGES;
-constexpr int kWOff = kStages * kTile;
-constexpr int kBarOff = kWOff + kTile;
-constexpr int kDrOff = kBarOff + 256;  // float [2 tile parities][2 column halves][128 rows]: Delta halves
-constexpr int kSmem = kDrOff + 2048 + 1024;
 constexpr int kThreads = 512;
 constexpr int kXform = 128;
 constexpr int kEpi = 256;
 
+// Shared-memory geometry: history rows stage q only (3 x 32 KB); target rows stage q, k_self and
+// v_self of a tile together (2 x 96 KB), so the Delta dot and the + d v_self of the epilogue read
+// shared memory instead of re-reading rows from global memory on the tile's critical path.
+template <bool DELTA>
+struct Geo {
+    static constexpr int kStages = DELTA ? 2 : 3;
+    static constexpr int kStageBytes = DELTA ? 3 * kTile : kTile;
+    static constexpr int kWOff = kStages * kStageBytes;
+    static constexpr int kBarOff = kWOff + kTile;
+    static constexpr int kDrOff = kBarOff + 256;  // float [stage][128 rows]: the Delta dot of each row
+    static constexpr int kSmem = kDrOff + kStages * 128 * 4 + 1024;
+    static_assert(kSmem <= 232448, "shared memory");
+};
+
 struct Bars {
-    uint64_t q_full[kStages], q_ready[kStages], q_empty[kStages];
+    uint64_t q_full[3], q_ready[3], q_empty[3];
     uint64_t acc_full[2], acc_empty[2];
     uint64_t w_full, w_empty;
     uint32_t tmem_base;
@@ -57,11 +65,9 @@ struct Params {
     const int64_t* row_offsets;
     const int64_t* uts;           // tile starts of the rows' layout
     const uint8_t* w_op;          // [B*H][32 KB] W_u operands
-    const __nv_bfloat16* q;       // raw q rows (re-read by the epilogue for the Delta term)
-    const __nv_bfloat16* k_self;  // NULL: no Delta term
-    const __nv_bfloat16* v_self;
     void* out;                    // [R, H, 128] bf16 or f32
-    const int64_t* offsets;       // history offsets [B+1]: N_u for the Delta term's 1/N
+    const int64_t* offsets;       // history offsets [B+1]: N_u for the Delta term's 1/N ...
+    const int64_t* user_len;      // ... or N_u given directly ([B], may be NULL)
     int out_bf16;
     int normalize;
     int B, H;
@@ -80,6 +86,18 @@ __device__ __forceinline__ float phi(float x) {
     }
 }
 
+// phi on a packed bf16x2 pair -> packed bf16x2 (SiLU in packed bf16 math, one MUFU op per pair)
+template <int PHI>
+__device__ __forceinline__ uint32_t phi2x(uint32_t w) {
+    if constexpr (PHI == VISTA_ACT_SILU) {
+        return qla_silu_bf16x2(w);
+    } else if constexpr (PHI == VISTA_ACT_SHIFTED_ELU) {
+        return ptx::pack_bf16x2(phi<PHI>(__uint_as_float(w << 16)), phi<PHI>(__uint_as_float(w & 0xFFFF0000u)));
+    } else {
+        return w;
+    }
+}
+
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 v;
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -94,8 +112,41 @@ __device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
                  "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                  : "memory");
 }
+// byte offset of 16-B chunk c (of 8) of row r in a 128-row, 128-B-row SWIZZLE_128B half tile
+__device__ __forceinline__ uint32_t swz_chunk(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
-// phi1(Q) in place, 16-B chunk by chunk (the swizzle only permutes chunks within a row)
+// phi1 in place over a q tile, one row per thread (16 chunks of 8 values); with DELTA also the row
+// dot phi1(q_r) . phi1(k_self_r) from the k tile of the stage.  Returns the dot (0 without DELTA).
+template <int PHI, bool DELTA>
+__device__ __forceinline__ float xform_row(uint32_t qbuf, uint32_t kbuf, int r) {
+    float dot = 0.f;
+#pragma unroll
+    for (int half = 0; half < 2; ++half)
+#pragma unroll 4
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t off = half * kHalf + swz_chunk(r, c);
+            const uint4 raw = lds128(qbuf + off);
+            const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+            uint32_t ph[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ph[e] = phi2x<PHI>(w[e]);
+            sts128(qbuf + off, make_uint4(ph[0], ph[1], ph[2], ph[3]));
+            if constexpr (DELTA) {
+                const uint4 kr = lds128(kbuf + off);
+                const uint32_t kw[4] = {kr.x, kr.y, kr.z, kr.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {  // the dot of the bf16 phi1 values (those the MMA sees), in f32
+                    const uint32_t pk = phi2x<PHI>(kw[e]);
+                    dot = fmaf(__uint_as_float(ph[e] << 16), __uint_as_float(pk << 16), dot);
+                    dot = fmaf(__uint_as_float(ph[e] & 0xFFFF0000u), __uint_as_float(pk & 0xFFFF0000u), dot);
+                }
+            }
+        }
+    return dot;
+}
+
+// phi1(Q) in place without the Delta dot, 16-B chunk by chunk (the swizzle only permutes chunks
+// within a row): consecutive threads take consecutive chunks
 template <int PHI>
 __device__ __forceinline__ void xform_tile(uint32_t qbuf, int xt) {
 #pragma unroll 4
@@ -105,16 +156,15 @@ __device__ __forceinline__ void xform_tile(uint32_t qbuf, int xt) {
         const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
         uint32_t ph[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-            ph[e] = ptx::pack_bf16x2(phi<PHI>(__uint_as_float(w[e] << 16)), phi<PHI>(__uint_as_float(w[e] & 0xFFFF0000u)));
+        for (int e = 0; e < 4; ++e) ph[e] = phi2x<PHI>(w[e]);
         sts128(qbuf + off, make_uint4(ph[0], ph[1], ph[2], ph[3]));
     }
 }
 
 // O = phi1(Q) W: A = phi1(Q) [row][c1] K-major, B = W [K = c1][N = c2] MN-major
-template <int ST>
+template <int SB, int ST, int WOFF>
 __device__ __forceinline__ void issue_tile(uint32_t tacc, uint32_t base) {
-    const uint32_t qb = base + ST * kTile, wb = base + kWOff;
+    const uint32_t qb = base + ST * SB, wb = base + WOFF;
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
@@ -122,23 +172,27 @@ __device__ __forceinline__ void issue_tile(uint32_t tacc, uint32_t base) {
                       ptx::sdesc_sw128(wb + kk * 2048, kHalf, 1024), id, kk > 0);
 }
 
+template <bool DELTA>
 __device__ __forceinline__ void issue_tile_d(int stage, uint32_t tacc, uint32_t base) {
+    using G = Geo<DELTA>;
     switch (stage) {
-        case 0: issue_tile<0>(tacc, base); break;
-        case 1: issue_tile<1 % kStages>(tacc, base); break;
-        case 2: issue_tile<2 % kStages>(tacc, base); break;
-        case 3: issue_tile<3 % kStages>(tacc, base); break;
-        default: issue_tile<4 % kStages>(tacc, base); break;
+        case 0: issue_tile<G::kStageBytes, 0, G::kWOff>(tacc, base); break;
+        case 1: issue_tile<G::kStageBytes, 1 % G::kStages, G::kWOff>(tacc, base); break;
+        default: issue_tile<G::kStageBytes, 2 % G::kStages, G::kWOff>(tacc, base); break;
     }
 }
 
-template <int PHI1>
+template <int PHI1, bool DELTA>
 __global__ void __launch_bounds__(kThreads, 1)
-    sm100_qla_rows_kernel(const __grid_constant__ CUtensorMap mapQ, const Params P) {
+    sm100_qla_rows_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+                          const __grid_constant__ CUtensorMap mapV, const Params P) {
+    using G = Geo<DELTA>;
+    constexpr int kStages = G::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t base = ptx::smem_u32(smem);
-    Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
+    Bars* bars = reinterpret_cast<Bars*>(smem + G::kBarOff);
+    float* dr_smem = reinterpret_cast<float*>(smem + G::kDrOff);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cta = blockIdx.x, num_ctas = gridDim.x;
     const int HG = P.H;
@@ -146,7 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&bars->q_full[s], 1);
             ptx::mbar_init(&bars->q_ready[s], kXform);
-            ptx::mbar_init(&bars->q_empty[s], 1);
+            // freed by the MMA commit (q consumed) and, with DELTA, by the epilogue (v_self consumed)
+            ptx::mbar_init(&bars->q_empty[s], DELTA ? 1 + kEpi : 1);
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&bars->acc_full[b], 1);
@@ -166,24 +221,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     iter.init(P.uts, P.B, HG, cta, num_ctas);
     Item it;
     if (warp == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer: q tiles (+ k_self, v_self tiles); W_u per unit
         ptx::tma_prefetch(&mapQ);
-        const uint64_t pol = P.k_self ? ptx::policy_evict_last() : ptx::policy_evict_first();  // Delta re-reads q
+        if constexpr (DELTA) {
+            ptx::tma_prefetch(&mapK);
+            ptx::tma_prefetch(&mapV);
+        }
+        const uint64_t pol = ptx::policy_evict_first();
         int stage = 0;
         uint32_t phase = 0;
         int k = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             if (k > 0) ptx::mbar_wait(&bars->w_empty, (k - 1) & 1);  // the previous unit's GEMMs are done with W
             ptx::mbar_arrive_expect_tx_w(&bars->w_full, kTile);
-            ptx::bulk_g2s_w(base + kWOff, P.w_op + (size_t)(it.u * HG + it.hg) * kTile, kTile, &bars->w_full);
+            ptx::bulk_g2s_w(base + G::kWOff, P.w_op + (size_t)(it.u * HG + it.hg) * kTile, kTile, &bars->w_full);
             const int64_t row0 = P.row_offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->q_empty[stage], phase ^ 1);
-                ptx::mbar_arrive_expect_tx_w(&bars->q_full[stage], kTile);
+                ptx::mbar_arrive_expect_tx_w(&bars->q_full[stage], G::kStageBytes);
                 const int32_t row = (int32_t)(row0 + (int64_t)t * 128);
-                for (int half = 0; half < 2; ++half)
-                    ptx::tma_load_3d_w(smem + stage * kTile + half * kHalf, &mapQ, &bars->q_full[stage], half * 64,
-                                       it.hg, row, pol);
+                uint8_t* st = smem + stage * G::kStageBytes;
+                for (int half = 0; half < 2; ++half) {
+                    ptx::tma_load_3d_w(st + half * kHalf, &mapQ, &bars->q_full[stage], half * 64, it.hg, row, pol);
+                    if constexpr (DELTA) {
+                        ptx::tma_load_3d_w(st + kTile + half * kHalf, &mapK, &bars->q_full[stage], half * 64, it.hg,
+                                           row, pol);
+                        ptx::tma_load_3d_w(st + 2 * kTile + half * kHalf, &mapV, &bars->q_full[stage], half * 64,
+                                           it.hg, row, pol);
+                    }
+                }
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
             ++k;
@@ -202,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 aph[ab] ^= 1;
                 ptx::tc_fence_after();
                 const uint32_t tacc = tmem + ab * 128;
-                issue_tile_d(stage, tacc, base);
+                issue_tile_d<DELTA>(stage, tacc, base);
                 ptx::mma_commit_w(&bars->acc_full[ab]);
                 ptx::mma_commit_w(&bars->q_empty[stage]);
                 ab ^= 1;
@@ -212,14 +278,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++k;
         }
     } else if (warp >= 4 && warp < 8) {
-        // ---------------- transform: phi1(Q) in place
-        const int xt = threadIdx.x - 128;
+        // ---------------- transform: phi1(Q) in place, one row per thread (+ the Delta dot)
+        const int r = threadIdx.x - 128;
         int stage = 0;
         uint32_t phase = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
+            float inv_n = 1.f;  // App. B: the Delta term under the state's 1/N_u (reading R20)
+            if (DELTA && P.normalize) {
+                const int64_t N = P.user_len ? P.user_len[it.u] : P.offsets[it.u + 1] - P.offsets[it.u];
+                if (N > 0) inv_n = 1.f / (float)N;
+            }
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->q_full[stage], phase);
-                xform_tile<PHI1>(base + stage * kTile, xt);
+                const uint32_t sb = base + stage * G::kStageBytes;
+                if constexpr (DELTA) dr_smem[stage * 128 + r] = xform_row<PHI1, true>(sb, sb + kTile, r) * inv_n;
+                else xform_tile<PHI1>(sb, r);
                 ptx::fence_proxy_async_smem();
                 ptx::mbar_arrive(&bars->q_ready[stage]);
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -232,57 +305,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = wq * 32 + lane;    // row within the tile = TMEM lane
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
         const size_t rstride = (size_t)P.H * 128;  // elements between rows
-        int ab = 0;
+        int ab = 0, stage = 0;
         uint32_t aph[2] = {0, 0};
+        uint32_t phase = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             const int64_t R = P.row_offsets[it.u + 1] - P.row_offsets[it.u];
             const int64_t row0 = P.row_offsets[it.u];
-            float inv_n = 1.f;  // App. B: the Delta term under the state's 1/N_u (reading R20)
-            if (P.k_self && P.normalize) {
-                const int64_t N = P.offsets[it.u + 1] - P.offsets[it.u];
-                if (N > 0) inv_n = 1.f / (float)N;
-            }
             for (int t = it.t0; t < it.t1; ++t) {
                 const int64_t rem = R - (int64_t)t * 128;
                 const int valid = rem < 128 ? (int)rem : 128;
                 const int64_t grow0 = row0 + (int64_t)t * 128;
                 const size_t e0 = ((size_t)grow0 * P.H + it.hg) * 128;  // element (row 0, col 0) of the tile
-                // Delta: d_r = phi1(q_r) . phi1(k_self_r), issued before the wait for the GEMM. Each
-                // column warp sums its 64 columns, coalesced: the warp walks its 32 rows, lane l
-                // holding channels 64 chalf + [2l, 2l + 2) of each (one 128 B line per load), then a
-                // transpose-reduce (31 shuffles) leaves row wq * 32 + l's half sum in lane l; the two
-                // halves meet through shared memory (named barrier per warp pair, buffer per tile
-                // parity so the next tile's write cannot overtake the partner's read).
-                float dr = 0.f;
-                if (P.k_self) {
-                    float part[32];
-#pragma unroll
-                    for (int rr = 0; rr < 32; ++rr) {
-                        // rows past the tail re-read the last valid row; their sums are never used
-                        const int r = min(wq * 32 + rr, valid - 1);
-                        const size_t off = e0 + (size_t)r * rstride + chalf * 64 + 2 * lane;
-                        const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(P.q + off));
-                        const uint32_t b = __ldg(reinterpret_cast<const uint32_t*>(P.k_self + off));
-                        float s = phi<PHI1>(__uint_as_float(a << 16)) * phi<PHI1>(__uint_as_float(b << 16));
-                        s = fmaf(phi<PHI1>(__uint_as_float(a & 0xFFFF0000u)), phi<PHI1>(__uint_as_float(b & 0xFFFF0000u)), s);
-                        part[rr] = s;
-                    }
-#pragma unroll
-                    for (int o = 16; o >= 1; o >>= 1) {
-                        const bool upper = (lane & o) != 0;
-#pragma unroll
-                        for (int i = 0; i < o; ++i) {
-                            const float send = upper ? part[i] : part[i + o];
-                            const float keep = upper ? part[i + o] : part[i];
-                            part[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                        }
-                    }
-                    float* xch = reinterpret_cast<float*>(smem + kDrOff) + ab * 256;
-                    xch[chalf * 128 + row] = part[0];
-                    ptx::named_bar_sync(1 + wq, 64);
-                    // fixed order (columns 0-63 first) so both warps hold the same d_r
-                    dr = (chalf == 0 ? part[0] + xch[128 + row] : xch[row] + part[0]) * inv_n;
-                }
                 ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
                 aph[ab] ^= 1;
                 ptx::tc_fence_after();
@@ -295,12 +328,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[32 * c + j] = __uint_as_float(r[j]);
                 }
-                if (P.k_self && row < valid) {  // + d_r v_self_r
-                    const uint4* vs =
-                        reinterpret_cast<const uint4*>(P.v_self + e0 + (size_t)row * rstride + chalf * 64);
+                if constexpr (DELTA) {  // + d_r v_self_r, both from shared memory
+                    ptx::mbar_wait(&bars->q_ready[stage], phase);  // orders the transform's d_r writes
+                    const float dr = dr_smem[stage * 128 + row];
+                    const uint32_t vb = base + stage * G::kStageBytes + 2 * kTile + chalf * kHalf;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
-                        const uint4 b = __ldg(vs + c);
+                        const uint4 b = lds128(vb + swz_chunk(row, c));
                         const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
@@ -308,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             o[8 * c + 2 * e + 1] = fmaf(dr, __uint_as_float(bw[e] & 0xFFFF0000u), o[8 * c + 2 * e + 1]);
                         }
                     }
+                    ptx::mbar_arrive(&bars->q_empty[stage]);  // v_self read: the stage may be refilled
                 }
                 if (P.out_bf16) {
                     // coalesced: permuted 32x32b store into the (read) accumulator columns, 16x256b load
@@ -344,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&bars->acc_empty[ab]);
                 ab ^= 1;
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
         }
     }
@@ -352,11 +388,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) ptx::tmem_dealloc(tmem, 256);
 }
 
-template <int PHI1>
-cudaError_t launch_phi(const Problem& p, const CUtensorMap& mq, const Params& P) {
-    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_rows_kernel<PHI1>), kSmem);
+template <int PHI1, bool DELTA>
+cudaError_t launch_phi(const Problem& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                       const Params& P) {
+    using G = Geo<DELTA>;
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_rows_kernel<PHI1, DELTA>), G::kSmem);
     if (attr != cudaSuccess) return attr;
-    sm100_qla_rows_kernel<PHI1><<<p.num_sms, kThreads, kSmem, p.stream>>>(mq, P);
+    sm100_qla_rows_kernel<PHI1, DELTA><<<p.num_sms, kThreads, G::kSmem, p.stream>>>(mq, mk, mv, P);
     return cudaGetLastError();
 }
 
@@ -370,7 +408,7 @@ __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p, size
 
 template <typename T>
 __global__ void qla_rows_simt_kernel(const float* __restrict__ z, const int64_t* __restrict__ offsets,
-                                     const int64_t* __restrict__ row_offsets, int B, int H, int d, int phi1, int phi2,
+                                     const int64_t* __restrict__ user_len, const int64_t* __restrict__ row_offsets, int B, int H, int d, int phi1, int phi2,
                                      int normalize, const T* __restrict__ q, const T* __restrict__ k_self,
                                      const T* __restrict__ v_self, int out_bf16, void* __restrict__ out) {
     __shared__ float fq[128];
@@ -397,7 +435,7 @@ __global__ void qla_rows_simt_kernel(const float* __restrict__ z, const int64_t*
     if (k_self)
         for (int w = 0; w < (d + 31) / 32; ++w) dr += red[w];
     if (c >= d) return;
-    const int64_t N = offsets[u + 1] - offsets[u];
+    const int64_t N = user_len ? user_len[u] : offsets[u + 1] - offsets[u];
     const float inv = (normalize && N > 0) ? 1.f / (float)N : 1.f;
     dr *= inv;  // App. B: the Delta term under the same 1/N_u (reading R20)
     const float* zu = z + (size_t)(u * H + h) * d * d;
@@ -415,43 +453,50 @@ bool qla_rows_uses_tc(const Problem& p, int64_t total_rows) {
 }
 
 // p: the history problem (B, H, d, phi, normalize, stream); uts: tile starts of the rows' layout;
-// w_op: the W_u operands (qla_prep_w)
+// w_op: the W_u operands (qla_prep_w); user_len: N_u per user (NULL: from p.offsets)
 cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, int64_t total_rows, const int64_t* uts,
                                   const uint8_t* w_op, const void* q, const void* k_self, const void* v_self,
-                                  int out_bf16, void* out) {
-    CUtensorMap mq;
+                                  int out_bf16, void* out, const int64_t* user_len) {
+    CUtensorMap mq, mk, mv;
     if (!make_kv_map(&mq, q, total_rows, p.H)) return cudaErrorInvalidValue;
+    const bool delta = k_self != nullptr;
+    if (delta && (!make_kv_map(&mk, k_self, total_rows, p.H) || !make_kv_map(&mv, v_self, total_rows, p.H)))
+        return cudaErrorInvalidValue;
+    if (!delta) mk = mv = mq;
     Params P;
     P.row_offsets = row_offsets;
     P.uts = uts;
     P.w_op = w_op;
-    P.q = reinterpret_cast<const __nv_bfloat16*>(q);
-    P.k_self = reinterpret_cast<const __nv_bfloat16*>(k_self);
-    P.v_self = reinterpret_cast<const __nv_bfloat16*>(v_self);
     P.out = out;
     P.offsets = p.offsets;
+    P.user_len = user_len;
     P.normalize = p.normalize;
     P.out_bf16 = out_bf16;
     P.B = p.B;
     P.H = p.H;
-    return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU>(p, mq, P)
-         : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU>(p, mq, P)
-                                           : launch_phi<VISTA_ACT_IDENTITY>(p, mq, P);
+    if (delta)
+        return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU, true>(p, mq, mk, mv, P)
+             : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU, true>(p, mq, mk, mv, P)
+                                               : launch_phi<VISTA_ACT_IDENTITY, true>(p, mq, mk, mv, P);
+    return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU, false>(p, mq, mk, mv, P)
+         : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU, false>(p, mq, mk, mv, P)
+                                           : launch_phi<VISTA_ACT_IDENTITY, false>(p, mq, mk, mv, P);
 }
 
 cudaError_t launch_qla_rows_simt(const Problem& p, const float* z, const int64_t* row_offsets, int64_t total_rows,
-                                 const void* q, const void* k_self, const void* v_self, int out_bf16, void* out) {
+                                 const void* q, const void* k_self, const void* v_self, int out_bf16, void* out,
+                                 const int64_t* user_len) {
     if (total_rows == 0) return cudaSuccess;
     const unsigned grid = (unsigned)(total_rows * p.H);
     const int threads = p.d < 32 ? 32 : p.d;
     if (p.in_bf16)
         qla_rows_simt_kernel<__nv_bfloat16><<<grid, threads, 0, p.stream>>>(
-            z, p.offsets, row_offsets, p.B, p.H, p.d, p.phi1, p.phi2, p.normalize,
+            z, p.offsets, user_len, row_offsets, p.B, p.H, p.d, p.phi1, p.phi2, p.normalize,
             reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k_self),
             reinterpret_cast<const __nv_bfloat16*>(v_self), out_bf16, out);
     else
         qla_rows_simt_kernel<float><<<grid, threads, 0, p.stream>>>(
-            z, p.offsets, row_offsets, p.B, p.H, p.d, p.phi1, p.phi2, p.normalize, reinterpret_cast<const float*>(q),
+            z, p.offsets, user_len, row_offsets, p.B, p.H, p.d, p.phi1, p.phi2, p.normalize, reinterpret_cast<const float*>(q),
             reinterpret_cast<const float*>(k_self), reinterpret_cast<const float*>(v_self), out_bf16, out);
     return cudaGetLastError();
 }

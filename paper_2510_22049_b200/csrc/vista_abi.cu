@@ -631,21 +631,67 @@ namespace {
 struct RowsPlan {
     size_t sub_off, z_off, w_off, uts_off, total;
 };
-RowsPlan plan_rows(const Problem& p, int64_t total_rows) {
+// with_state: workspace for the Z pass too (vista_qla_rows); else only W_u and the rows' tile starts
+RowsPlan plan_rows(const Problem& p, int64_t total_rows, bool with_state) {
     RowsPlan r{};
     const size_t B = (size_t)p.B, H = (size_t)p.H, d = (size_t)p.d;
     const bool tc = qla_rows_uses_tc(p, total_rows);
     size_t off = 0;
     r.sub_off = off;
-    off = align256(off + plan_workspace(p, true).total);
+    if (with_state) off = align256(off + plan_workspace(p, true).total);
     r.z_off = off;
-    off = align256(off + B * H * d * d * sizeof(float));
+    if (with_state) off = align256(off + B * H * d * d * sizeof(float));
     r.w_off = off;
     if (tc) off = align256(off + B * H * d * d * 2);
     r.uts_off = off;
     if (tc) off = align256(off + (B + 1) * sizeof(int64_t));
     r.total = off;
     return r;
+}
+
+// Rows from a state: W_u = phi2(Z_u / N_u) operands, the rows' tile starts, the rows kernel (or the
+// SIMT kernel).  N_u from user_len (if given) or p.offsets.
+vista_status_t rows_from_z(const vista_desc_t* desc, const Problem& p, const RowsPlan& r, char* ws, const float* z,
+                           const int64_t* user_len, const void* q_rows, const int64_t* row_offsets, int64_t total_rows,
+                           const void* k_self, const void* v_self, void* out) {
+    const int out_bf16 = desc->out_dtype == VISTA_BF16;
+    cudaError_t e;
+    int nl = 0;
+    if (qla_rows_uses_tc(p, total_rows)) {
+        uint8_t* w_op = reinterpret_cast<uint8_t*>(ws + r.w_off);
+        int64_t* uts = reinterpret_cast<int64_t*>(ws + r.uts_off);
+        Problem pr = p;
+        pr.offsets = row_offsets;
+        pr.total_len = total_rows;
+        pr.attn = VISTA_QLA;
+        pr.outs = OutSpec{OUT_PARTIAL, 0, nullptr, nullptr};
+        e = launch_qla_prep_w(p, z, w_op, user_len);
+        if (e == cudaSuccess) e = launch_user_tiles(pr, uts, nullptr);
+        if (e == cudaSuccess)
+            e = timed_main(p.stream, [&] {
+                return launch_sm100_qla_rows(p, row_offsets, total_rows, uts, w_op, q_rows, k_self, v_self, out_bf16,
+                                             out, user_len);
+            });
+        nl = 3;
+    } else {
+        e = timed_main(p.stream, [&] {
+            return launch_qla_rows_simt(p, z, row_offsets, total_rows, q_rows, k_self, v_self, out_bf16, out, user_len);
+        });
+        nl = 1;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches += (unsigned long long)nl;
+    return VISTA_OK;
+}
+
+vista_status_t check_rows_args(const vista_desc_t* desc, int64_t total_rows, const void* q_rows,
+                               const int64_t* row_offsets, const void* k_self, const void* v_self, const void* out) {
+    if (desc->attn != VISTA_QLA || total_rows < 0) return VISTA_ERR_INVALID;
+    if (!row_offsets) return VISTA_ERR_NULL;
+    if (total_rows > 0 && (!q_rows || !out)) return VISTA_ERR_NULL;
+    if ((k_self == nullptr) != (v_self == nullptr)) return VISTA_ERR_NULL;
+    if (!aligned16(q_rows) || !aligned16(k_self) || !aligned16(v_self) || !aligned16(out)) return VISTA_ERR_MISALIGNED;
+    return VISTA_OK;
 }
 }  // namespace
 
@@ -655,7 +701,7 @@ vista_status_t vista_qla_rows_workspace_size(const vista_desc_t* desc, int64_t t
     if (st != VISTA_OK) return st;
     if (!bytes) return VISTA_ERR_NULL;
     if (desc->attn != VISTA_QLA || total_len < 0 || total_rows < 0) return VISTA_ERR_INVALID;
-    *bytes = plan_rows(make_problem(desc, total_len), total_rows).total;
+    *bytes = plan_rows(make_problem(desc, total_len), total_rows, true).total;
     return VISTA_OK;
 }
 
@@ -665,21 +711,18 @@ vista_status_t vista_qla_rows(const vista_desc_t* desc, const void* k, const voi
                               size_t workspace_bytes, void* stream) {
     vista_status_t st = validate_desc(desc);
     if (st != VISTA_OK) return st;
-    if (desc->attn != VISTA_QLA || total_len < 0 || total_rows < 0) return VISTA_ERR_INVALID;
-    if (!offsets || !row_offsets) return VISTA_ERR_NULL;
+    if (total_len < 0) return VISTA_ERR_INVALID;
+    if ((st = check_rows_args(desc, total_rows, q_rows, row_offsets, k_self, v_self, out)) != VISTA_OK) return st;
+    if (!offsets) return VISTA_ERR_NULL;
     if (total_len > 0 && (!k || !v)) return VISTA_ERR_NULL;
-    if (total_rows > 0 && (!q_rows || !out)) return VISTA_ERR_NULL;
-    if ((k_self == nullptr) != (v_self == nullptr)) return VISTA_ERR_NULL;
-    if (!aligned16(k) || !aligned16(v) || !aligned16(q_rows) || !aligned16(k_self) || !aligned16(v_self) ||
-        !aligned16(out))
-        return VISTA_ERR_MISALIGNED;
+    if (!aligned16(k) || !aligned16(v)) return VISTA_ERR_MISALIGNED;
     Problem p = make_problem(desc, total_len);
     p.k = k;
     p.v = v;
     p.offsets = offsets;
     p.stream = reinterpret_cast<cudaStream_t>(stream);
     if (p.B == 0 || total_rows == 0) return VISTA_OK;
-    const RowsPlan r = plan_rows(p, total_rows);
+    const RowsPlan r = plan_rows(p, total_rows, true);
     if (!workspace || workspace_bytes < r.total) return VISTA_ERR_WORKSPACE;
     if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
     char* ws = reinterpret_cast<char*>(workspace);
@@ -693,35 +736,36 @@ vista_status_t vista_qla_rows(const vista_desc_t* desc, const void* k, const voi
     g_ev_start = ev_a;
     g_ev_stop = ev_b;
     if (st != VISTA_OK) return st;
-    const int out_bf16 = desc->out_dtype == VISTA_BF16;
-    cudaError_t e;
-    int nl = 0;
-    if (qla_rows_uses_tc(p, total_rows)) {
-        // 2. W_u = phi2(Z_u / N_u) as bf16 MMA operands; tile starts of the rows' jagged layout
-        uint8_t* w_op = reinterpret_cast<uint8_t*>(ws + r.w_off);
-        int64_t* uts = reinterpret_cast<int64_t*>(ws + r.uts_off);
-        Problem pr = p;
-        pr.offsets = row_offsets;
-        pr.total_len = total_rows;
-        pr.attn = VISTA_QLA;
-        pr.outs = OutSpec{OUT_PARTIAL, 0, nullptr, nullptr};
-        e = launch_qla_prep_w(p, z, w_op);
-        if (e == cudaSuccess) e = launch_user_tiles(pr, uts, nullptr);
-        // 3. O rows = phi1(Q) W_u (+ Delta)
-        if (e == cudaSuccess)
-            e = timed_main(p.stream, [&] {
-                return launch_sm100_qla_rows(p, row_offsets, total_rows, uts, w_op, q_rows, k_self, v_self, out_bf16, out);
-            });
-        nl = 3;
-    } else {
-        e = timed_main(p.stream, [&] {
-            return launch_qla_rows_simt(p, z, row_offsets, total_rows, q_rows, k_self, v_self, out_bf16, out);
-        });
-        nl = 1;
-    }
-    if (e != cudaSuccess) return cuda_fail(e);
-    g_launches += (unsigned long long)nl;
+    // 2.-3. W_u, tile starts, rows
+    return rows_from_z(desc, p, r, ws, z, nullptr, q_rows, row_offsets, total_rows, k_self, v_self, out);
+}
+
+vista_status_t vista_qla_rows_from_state_workspace_size(const vista_desc_t* desc, int64_t total_rows, size_t* bytes) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (!bytes) return VISTA_ERR_NULL;
+    if (desc->attn != VISTA_QLA || total_rows < 0) return VISTA_ERR_INVALID;
+    *bytes = plan_rows(make_problem(desc, 0), total_rows, false).total;
     return VISTA_OK;
+}
+
+vista_status_t vista_qla_rows_from_state(const vista_desc_t* desc, const float* z, const int64_t* user_len,
+                                         const void* q_rows, const int64_t* row_offsets, int64_t total_rows,
+                                         const void* k_self, const void* v_self, void* out, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if ((st = check_rows_args(desc, total_rows, q_rows, row_offsets, k_self, v_self, out)) != VISTA_OK) return st;
+    if (desc->num_users > 0 && (!z || !user_len)) return VISTA_ERR_NULL;
+    if (!aligned16(z)) return VISTA_ERR_MISALIGNED;
+    Problem p = make_problem(desc, 0);
+    p.stream = reinterpret_cast<cudaStream_t>(stream);
+    if (p.B == 0 || total_rows == 0) return VISTA_OK;
+    const RowsPlan r = plan_rows(p, total_rows, false);
+    if (r.total > 0 && (!workspace || workspace_bytes < r.total)) return VISTA_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
+    return rows_from_z(desc, p, r, reinterpret_cast<char*>(workspace), z, user_len, q_rows, row_offsets, total_rows,
+                       k_self, v_self, out);
 }
 
 static size_t merge_ws_bytes(const Problem& p) {

@@ -915,3 +915,61 @@ def test_all_empty_batch_and_zero_users(cuda_lib, attn):
     o0, l0 = vista.summarize(q, k, k, torch.zeros(1, dtype=torch.int64, device="cuda"), 0, attn=a, out_dtype=vista.F32)
     torch.cuda.synchronize()
     assert o0.shape == (0, 256, 2, 128)
+
+
+# ----------------------------------------------------------------------------- QLA rows from a saved state
+@pytest.mark.parametrize("delta,normalize,dtype", [(True, True, "bf16"), (False, True, "bf16"), (True, False, "bf16"),
+                                                   (True, True, "f32")])
+def test_qla_rows_from_state(cuda_lib, delta, normalize, dtype):
+    """vista_qla_rows_from_state on the state of vista_summarize_partial (QLA) and N_u = L_u gives
+    the rows of vista_qla_rows bitwise (same W_u operands, same rows kernel) and matches the oracle
+    (the state computed first, then multiplied with Q[S]_l, Q[T]_l)."""
+    vista = cuda_lib
+    lens = [300, 0, 129, 2049, 5, 1]
+    rows = [130, 3, 0, 257, 1, 128]
+    H, d = 2, 128 if dtype == "bf16" else 64
+    q, roff, k, v, off, ks, vs = _rows_case(lens, rows, H, d, dtype, 66, delta)
+    dev = lambda x: None if x is None else to_dev(x, dtype)  # noqa: E731
+    kt, vt, ot, rt = dev(k), dev(v), torch.from_numpy(off).cuda(), torch.from_numpy(roff).cuda()
+    seeds = dev(q[:1])  # any q: the partial state does not read it
+    z, _ = vista.summarize_partial(seeds, kt, vt, ot, int(off[-1]), attn=vista.QLA, normalize=normalize)
+    ulen = torch.from_numpy(np.diff(off)).cuda()
+    a = vista.qla_rows_from_state(z, ulen, dev(q), rt, int(roff[-1]), k_self=dev(ks), v_self=dev(vs),
+                                  normalize=normalize, out_dtype=vista.F32)
+    b = vista.qla_rows(kt, vt, ot, int(off[-1]), dev(q), rt, int(roff[-1]), k_self=dev(ks), v_self=dev(vs),
+                       normalize=normalize, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    ref = oracle.qla_rows(q, roff, k, v, off, "silu", "silu", normalize, k_self=ks, v_self=vs)
+    g = a.cpu().numpy()
+    tol = 2e-2 if dtype == "bf16" else 1e-4
+    for u in range(len(lens)):
+        for h in range(H):
+            if roff[u + 1] > roff[u]:
+                assert block_err(g[roff[u]:roff[u + 1], h], ref[roff[u]:roff[u + 1], h]) <= tol
+
+
+def test_qla_target_rows_c2_full_size_from_state(cuda_lib):
+    """The bench's --qla-rows target step at config 2 size: 256 target rows per user with the Delta
+    term from the users' saved states; three users against the oracle."""
+    vista = cuda_lib
+    lens, S, H, d, q, K, V, off = _c2_full()
+    ot = torch.from_numpy(off).cuda()
+    B = len(lens)
+    z, _ = vista.summarize_partial(q, K, V, ot, int(off[-1]), attn=vista.QLA)
+    rng = np.random.default_rng(13)
+    n = 256 * B
+    qr, ks, vs = [(rng.integers(-128, 128, size=(n, H, d)) / 64.0).astype(np.float32) for _ in range(3)]
+    roff = np.arange(B + 1, dtype=np.int64) * 256
+    out = vista.qla_rows_from_state(z, torch.from_numpy(np.asarray(lens, np.int64)).cuda(), to_dev(qr, "bf16"),
+                                    torch.from_numpy(roff).cuda(), n, k_self=to_dev(ks, "bf16"),
+                                    v_self=to_dev(vs, "bf16"), out_dtype=vista.BF16)
+    torch.cuda.synchronize()
+    for u in (0, 31, 63):
+        a, b = int(off[u]), int(off[u + 1])
+        ref = oracle.qla_rows(qr[256 * u:256 * (u + 1)], [0, 256], K[a:b].float().cpu().numpy(),
+                              V[a:b].float().cpu().numpy(), [0, b - a], k_self=ks[256 * u:256 * (u + 1)],
+                              v_self=vs[256 * u:256 * (u + 1)])
+        g = out[256 * u:256 * (u + 1)].float().cpu().numpy()
+        for h in range(H):
+            assert block_err(g[:, h], ref[:, h]) <= 2e-2, f"user {u} head {h}"

@@ -60,6 +60,7 @@ def _load():
         lib.vo_softmax_backward.argtypes = [i64, i64, i64, i64, P, i64, P, P, P, f64, P, P, P, P, i32]
         lib.vo_qla_backward.argtypes = [i64, i64, i64, i64, P, i64, P, P, P, P, i32, i32, i32, P, P, P, i32]
         lib.vo_num_threads.restype = i32
+        lib.vo_target_attend.argtypes = [i64, i64, i64, i64, P, P, P, P, P, P, P, P, f64, P, P, i32]
         _lib = lib
     return _lib
 
@@ -302,3 +303,28 @@ def quantize_rows_int8(x):
 def dequantize_rows_int8(codes, scale, zp):
     """x^ = code * scale + zero_point (SPEC.md:348-352), float64."""
     return codes.astype(np.float64) * scale[..., None].astype(np.float64) + zp[..., None].astype(np.float64)
+
+
+def target_attend(codes, tscale, tzp, q, k_self, v_self, row_offsets, scale=None, resid=None, threads=0):
+    """Stage-2 target-aware attention (NEXT-4, vo_target_attend): every candidate row attends to the
+    dequantized summary tokens of its user and to itself.  codes [B,S,H,d] int8, tscale / tzp
+    [B,S,H]; q, k_self, v_self (, resid) [R,H,d].  Returns out [R,H,d], lse [R,H] (float64)."""
+    codes = np.ascontiguousarray(codes, dtype=np.int8)
+    tscale, tzp = _f32(tscale), _f32(tzp)
+    q, k_self, v_self = _f32(q), _f32(k_self), _f32(v_self)
+    rz = None if resid is None else _f32(resid)
+    row_offsets = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    B, S, H, d = codes.shape
+    R = q.shape[0]
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    out = np.empty((R, H, d), np.float64)
+    lse = np.empty((R, H), np.float64)
+    if R == 0:
+        return out, lse
+    rc = _load().vo_target_attend(B, S, H, d, _ptr(codes), _ptr(tscale), _ptr(tzp), _ptr(q), _ptr(k_self),
+                                  _ptr(v_self), _ptr(rz) if rz is not None else None, _ptr(row_offsets), float(scale),
+                                  _ptr(out), _ptr(lse), int(threads))
+    if rc != 0:
+        raise ValueError("vo_target_attend failed")
+    return out, lse

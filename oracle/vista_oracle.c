@@ -31,6 +31,9 @@
  *  NEXT-3 / NEXT-4: QLA at arbitrary per-user query rows (history rows of a deeper layer, or
  *  target rows with the Delta self term), vo_qla_rows.
  *
+ *  NEXT-4: stage-2 target-aware attention of candidates over the cached (int8-exported) summary
+ *  tokens, vo_target_attend.
+ *
  *  NEXT-2 (training): the QLA backward (vo_qla_backward) by the chain rule through
  *  O = phi1(Q) phi2(Z / N), Z = phi1(K)^T V.
  *
@@ -505,6 +508,68 @@ int vo_quantize_rows_f32(int64_t n, int64_t d, const float* x, signed char* code
             if (q < -127.0f) q = -127.0f;
             codes[r * d + c] = (signed char)q;
         }
+    }
+    return 0;
+}
+
+/*
+ * Stage-2 target-aware attention (NEXT-4): "any attention network can technically be used for the
+ * target-aware attention stage ... we selected a standard O(N^2) transformer block, which delivers
+ * excellent performance on the compact summary sequences" (Sec. 3.3), over the
+ * summary tokens "retrieved from the cache and dequantized" (Sec. 3.1), with
+ * candidates never attending each other ("the candidates cannot attend each other").
+ * Reading R22: each candidate attends to [the S tokens of its user; itself]
+ * (SPEC.md:264-272 target_attend), keys = values = the dequantized tokens (a block's W_k / W_v fold
+ * into the query and the output by linearity), the candidate's own key / value given.
+ * For candidate c in [row_offsets[u], row_offsets[u+1]) and head h:
+ *   t_i    = codes[u,i,h,:] * tscale[u,i,h] + tzp[u,i,h]            (dequantization)
+ *   s_i    = scale q_c . t_i,   s_self = scale q_c . k_c,   m = max(s_i, s_self)
+ *   o_c    = (sum_i e^{s_i - m} t_i + e^{s_self - m} v_c) / (sum_i e^{s_i - m} + e^{s_self - m})
+ *   out_c  = o_c + resid_c (resid may be NULL);   lse_c = m + ln(sum ...)  (lse may be NULL)
+ * codes [B,S,H,d] int8; tscale, tzp [B,S,H]; q, k_self, v_self, resid, out [R,H,d]; lse [R,H].
+ */
+int vo_target_attend(int64_t B, int64_t S, int64_t H, int64_t d, const signed char* codes, const float* tscale,
+                     const float* tzp, const float* q, const float* k_self, const float* v_self, const float* resid,
+                     const int64_t* row_offsets, double scale, double* out, double* lse, int threads) {
+    if (B < 0 || S < 1 || H < 1 || d < 1) return -1;
+    set_threads(threads);
+    const int64_t R = row_offsets[B];
+#pragma omp parallel
+    {
+        double* t = (double*)malloc((size_t)(S * d) * sizeof(double));
+        double* sc = (double*)malloc((size_t)(S + 1) * sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t x = 0; x < R * H; ++x) {
+            const int64_t c = x / H, h = x % H;
+            int64_t u = 0;
+            while (row_offsets[u + 1] <= c) ++u;
+            for (int64_t i = 0; i < S; ++i) {
+                const double a = (double)tscale[(u * S + i) * H + h], b = (double)tzp[(u * S + i) * H + h];
+                for (int64_t e = 0; e < d; ++e) t[i * d + e] = (double)codes[((u * S + i) * H + h) * d + e] * a + b;
+            }
+            const float* qc = q + (c * H + h) * d;
+            const float* kc = k_self + (c * H + h) * d;
+            const float* vc = v_self + (c * H + h) * d;
+            double m = -INFINITY;
+            for (int64_t i = 0; i <= S; ++i) {
+                double acc = 0.0;
+                for (int64_t e = 0; e < d; ++e) acc += (double)qc[e] * (i < S ? t[i * d + e] : (double)kc[e]);
+                sc[i] = scale * acc;
+                if (sc[i] > m) m = sc[i];
+            }
+            double l = 0.0;
+            double* o = out + (c * H + h) * d;
+            for (int64_t e = 0; e < d; ++e) o[e] = 0.0;
+            for (int64_t i = 0; i <= S; ++i) {
+                const double p = exp(sc[i] - m);
+                l += p;
+                for (int64_t e = 0; e < d; ++e) o[e] += p * (i < S ? t[i * d + e] : (double)vc[e]);
+            }
+            for (int64_t e = 0; e < d; ++e) o[e] = o[e] / l + (resid ? (double)resid[(c * H + h) * d + e] : 0.0);
+            if (lse) lse[c * H + h] = m + log(l);
+        }
+        free(t);
+        free(sc);
     }
     return 0;
 }

@@ -29,6 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "history items summarized/sec (S=256,d=128) + % bf16 tensor peak, 1/2/4/8 GPU"
+METRIC_STAGE2 = "stage-2 candidates scored/sec over the cached int8 summary tokens (NEXT-4; not the headline metric)"
 TARGETS_PER_USER = 256  # --qla-rows target: candidate rows per user (NEXT-4)
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 
@@ -47,6 +48,9 @@ def parse():
     ap.add_argument("--qla-rows", choices=["history", "target"], default=None,
                     help="NEXT-3/4 (QLA): the step is vista_qla_rows -- every history item as a query row of its "
                          "own user (history), or 256 target rows per user with the Delta self term (target)")
+    ap.add_argument("--stage2", action="store_true",
+                    help="NEXT-4: the step is stage-2 target-aware attention (vista_target_attend) of "
+                         f"{TARGETS_PER_USER} candidates per user over the int8 export of the batch's summary tokens")
     ap.add_argument("--backward", action="store_true",
                     help="NEXT-2: the step is the QLA backward (vista_summarize_bwd: Z recompute, dQ, dK, dV)")
     ap.add_argument("--export-int8", action="store_true",
@@ -155,6 +159,9 @@ def run_own(args, rank, world, local_rank):
     cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
     if args.backward:
         wdesc += " backward (NEXT-2, from the forward's saved " + ("out, lse)" if args.attn == "softmax" else "state Z)")
+    if args.stage2:
+        wdesc += (f" stage-2 target-aware attention (NEXT-4: {TARGETS_PER_USER} candidates per user over the "
+                  f"{S} int8 summary tokens of the user + itself)")
     if args.qla_rows:
         wdesc += (" QLA history rows from the saved state (NEXT-3: every item a query row of its user)"
                   if args.qla_rows == "history"
@@ -250,7 +257,31 @@ def run_own(args, rank, world, local_rank):
                 vista.vista_qla_rows_from_state(desc, ins[0], ins[1], ins[2], ins[3], n_rows, ks, vs, rows_out,
                                                 rws, rws_bytes, None)
                 return [rows_out]
-        items_per_step = world * total
+        if args.stage2:
+            # the batch's summary tokens as the int8 export (vista_summarize_fwd_int8, outside the step)
+            codes = torch.empty((B, S, H, d), dtype=torch.int8, device=dev)
+            tsc = torch.empty((B, S, H), dtype=torch.float32, device=dev)
+            tzp = torch.empty((B, S, H), dtype=torch.float32, device=dev)
+            vista.vista_summarize_fwd_int8(desc, q, K, V, off_t, total, out, lse, codes, tsc, tzp, ws, ws_bytes, None)
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(5678 + rank)
+            grid = lambda shape: (torch.randint(-128, 128, shape, device=dev, generator=gen).float() / 64  # noqa: E731
+                                  ).to(torch.bfloat16)
+            n_rows = TARGETS_PER_USER * B
+            roff_t = torch.arange(B + 1, dtype=torch.int64, device=dev) * TARGETS_PER_USER
+            cq, ck, cv = grid((n_rows, H, d)), grid((n_rows, H, d)), grid((n_rows, H, d))
+            sdesc = vista.make_desc(B, S, H, d, in_dtype=vista.BF16, out_dtype=vista.BF16, attn=vista.SOFTMAX)
+            s2_out = torch.empty((n_rows, H, d), dtype=torch.bfloat16, device=dev)
+            s2_lse = torch.empty((n_rows, H), dtype=torch.float32, device=dev)
+            s2_bytes = vista.vista_target_attend_workspace_size(sdesc, n_rows)
+            s2_ws = torch.empty(max(s2_bytes, 16), dtype=torch.uint8, device=dev)
+            inputs = [codes, tsc, tzp, cq, ck, cv, roff_t]
+
+            def step(ins=inputs):
+                vista.vista_target_attend(sdesc, ins[0], ins[1], ins[2], ins[3], ins[4], ins[5], None, ins[6], n_rows,
+                                          s2_out, s2_lse, s2_ws, s2_bytes, None)
+                return [s2_out, s2_lse]
+        items_per_step = world * (n_rows if args.stage2 else total)
         scaling = "weak"
         parallel = f"by_user x{world} (weak: a {args.config} batch per GPU, no data-path collective)"
         if args.backward:
@@ -447,7 +478,7 @@ def run_own(args, rank, world, local_rank):
             e_ms = float(t[0])
         h2d = sum(x.numel() * x.element_size() for x in host_in)
         d2h = sum(x.numel() * x.element_size() for x in host_out)
-        e2e = {"value": items_per_step * args.e2e_steps / (e_ms / 1e3), "unit": "items/s",
+        e2e = {"value": items_per_step * args.e2e_steps / (e_ms / 1e3), "unit": "candidates/s" if args.stage2 else "items/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "note": "per rank: pinned host inputs -> H2D -> the step through the C ABI -> D2H of outputs; "
                        "CUDA events, max over ranks"}
@@ -483,15 +514,25 @@ def run_own(args, rank, world, local_rank):
     if args.qla_rows:  # rows kernel: q read, out written (bf16) [+ k_self, v_self read], W_u per unit
         flops = 2.0 * d * d * H * n_rows
         io_bytes = 4.0 * d * H * n_rows * (2 if args.qla_rows == "target" else 1) + B * H * d * d * 2
+    if args.stage2:  # target attention: q, k_c, v_c read, out written (bf16), lse; int8 tokens + scales
+        flops = 4.0 * S * d * H * n_rows
+        io_bytes = 4.0 * 2 * d * H * n_rows + 4.0 * H * n_rows + B * S * H * (d + 8)
     tflops = flops / (kern_ms / 1e3) / 1e12
     gbs = io_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         tkey = f"{args.config}_{args.attn}" + ("_bwd" if args.backward else "") + \
-            (f"_rows_{args.qla_rows}" if args.qla_rows else "")
+            (f"_rows_{args.qla_rows}" if args.qla_rows else "") + ("_stage2" if args.stage2 else "")
         traffic = json.load(open(tpath)).get(tkey)
-    if attn == vista.SOFTMAX:
+    if args.stage2:
+        roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic, "peak_kind": f"{pk_kind} HBM copy",
+                "kernel": "sm100_target_attend_kernel", "kernel_ms": round(kern_ms, 5),
+                "algorithmic_bytes_per_launch": io_bytes,
+                "tensor": {"achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                           "frac": round(tflops / pk["bf16_tflops"], 4)}}
+    elif attn == vista.SOFTMAX:
         roof = {"bound": "tensor", "achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": round(tflops / pk["bf16_tflops"], 4), "traffic": traffic,
                 "peak_kind": f"{pk_kind} bf16 burst (kernel timed alone per launch)",
@@ -515,7 +556,8 @@ def run_own(args, rank, world, local_rank):
                 "tensor": {"achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                            "frac": round(tflops / pk["bf16_tflops"], 4)}}
     res = {
-        "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": world, "steps": K_steps,
+        "metric": METRIC_STAGE2 if args.stage2 else METRIC, "value": value,
+        "unit": "candidates/s" if args.stage2 else "items/s", "n_gpus": world, "steps": K_steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / K_steps, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded counter-based generator, bf16-exact grid values; synth/)",
@@ -553,7 +595,7 @@ def run_own(args, rank, world, local_rank):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=None):
+def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=None, stage2=False):
     """Time the float64 oracle on whole users (all rows, all heads) of the rank-0 batch until
     ~`seconds` of CPU work; returns (items/s, cores, sample description, equivalent items, s)."""
     import numpy as np
@@ -572,7 +614,16 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=Non
         rr = np.arange(a, b, dtype=np.int64)
         k, v = synth.make_kv(rr, np.full(b - a, u), H, d, seed=0)
         t0 = time.perf_counter()
-        if qla_rows:  # NEXT-3/4: QLA at per-user query rows
+        if stage2:  # NEXT-4: target attention of the user's candidates over its int8 tokens
+            rng = np.random.default_rng(u)
+            n = TARGETS_PER_USER
+            cds = rng.integers(-127, 128, size=(1, S, H, d)).astype(np.int8)
+            tsc = (rng.integers(1, 64, size=(1, S, H)) / 1024.0).astype(np.float32)
+            tzp = (rng.integers(-64, 64, size=(1, S, H)) / 128.0).astype(np.float32)
+            cq, ck, cv = [(rng.integers(-128, 128, size=(n, H, d)) / 64.0).astype(np.float32) for _ in range(3)]
+            t0 = time.perf_counter()
+            oracle.target_attend(cds, tsc, tzp, cq, ck, cv, [0, n], threads=cores)
+        elif qla_rows:  # NEXT-3/4: QLA at per-user query rows
             rng = np.random.default_rng(u)
             n = (b - a) if qla_rows == "history" else TARGETS_PER_USER
             qr = (rng.integers(-128, 128, size=(n, H, d)) / 64.0).astype(np.float32)
@@ -592,7 +643,7 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=Non
         else:
             oracle.qla_summarize(q, k, v, [0, b - a], threads=cores)
         done_t += time.perf_counter() - t0
-        done_items += (b - a) * frac
+        done_items += TARGETS_PER_USER if stage2 else (b - a) * frac
         users += 1
         if done_t >= seconds:
             break
@@ -602,6 +653,9 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=Non
         sample += f", {attn} backward (oracle.{attn}_backward)"
     if qla_rows:
         sample += f", QLA {qla_rows} rows (oracle.qla_rows)"
+    if stage2:
+        sample = (f"{users} user(s) x {TARGETS_PER_USER} candidates over {S} int8 tokens, all {H} heads, "
+                  "float64 C oracle (oracle.target_attend), OpenMP; unit candidates/s")
     return done_items / done_t, cores, sample, done_items, done_t
 
 
@@ -675,6 +729,10 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    if args.stage2:
+        args.attn = "softmax"  # stage 2 reads the softmax summary's int8 export
+        if args.backward or args.export_int8 or args.qla_rows:
+            raise SystemExit("--stage2 excludes --backward / --export-int8 / --qla-rows")
     if args.qla_rows:
         args.attn = "qla"  # the rows path is QLA's
         if args.backward or args.export_int8:
@@ -716,8 +774,9 @@ def main():
     res = run_own(args, rank, world, local_rank)
     if res is not None and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds, rows=None,
-                                               backward=args.backward, qla_rows=args.qla_rows)
-        res["cpu_baseline"] = {"value": v, "unit": "items/s", "cores": cores, "kind": "oracle",
+                                               backward=args.backward, qla_rows=args.qla_rows, stage2=args.stage2)
+        res["cpu_baseline"] = {"value": v, "unit": "candidates/s" if args.stage2 else "items/s", "cores": cores,
+                               "kind": "oracle",
                                "sample": sample, "seconds": round(t, 2)}
     elif res is not None:
         res["cpu_baseline"] = None

@@ -254,6 +254,35 @@ vista_status_t vista_summarize_bwd_qla_saved(const vista_desc_t* desc, const voi
                                              void* dk, void* dv, void* workspace,
                                              size_t workspace_bytes, void* stream);
 
+/*
+ * Stage-2 target-aware attention over the cached summary tokens (NEXT-4).  "any attention network can
+ * technically be used for the target-aware attention stage ... a standard O(N^2) transformer block"
+ * (Sec. 3.3), over the summary tokens "retrieved from the cache and dequantized"
+ * -- the int8 export of vista_summarize_fwd_int8 read directly.  DESIGN.md reading
+ * R22: candidate c of user u attends to [the S tokens of u; itself], never to another candidate
+ * (PAPER.md:156); keys = values = the dequantized tokens (a block's W_k, W_v fold into q and into the
+ * output by linearity); the candidate's own key k_c and value v_c are given:
+ *   t_i = codes[u,i,h,:] * token_scale[u,i,h] + token_zero_point[u,i,h]
+ *   out[c,h,:] = softmax over {scale q_c.t_i, scale q_c.k_c} of [t_i ; v_c]  (+ resid[c,h,:])
+ *   lse[c,h]   = ln sum of the exponentials                                  (natural log)
+ * desc: num_users B, num_summary S (tokens per user), num_heads H, head_dim d; in_dtype of q, k_self,
+ *   v_self, resid; out_dtype; softmax_scale (NaN -> 1/sqrt(d)); attn must be VISTA_SOFTMAX.
+ *   codes       int8 [B, S, H, d]; token_scale, token_zero_point float32 [B, S, H]   (DEVICE)
+ *   q, k_self, v_self [total_rows, H, d]; resid [total_rows, H, d] or NULL          (DEVICE)
+ *   row_offsets int64 [B+1] (DEVICE): user u's candidates are rows [row_offsets[u], row_offsets[u+1])
+ *   out [total_rows, H, d] (out_dtype); lse float32 [total_rows, H] or NULL
+ * tcgen05 kernel for bf16, d = 128, S in {128, 256}; CUDA cores otherwise.  Workspace: at least
+ * vista_target_attend_workspace_size bytes.  Results of a candidate do not depend on the other
+ * candidates.  Asynchronous on stream; deterministic.
+ */
+vista_status_t vista_target_attend_workspace_size(const vista_desc_t* desc, int64_t total_rows,
+                                                  size_t* bytes);
+vista_status_t vista_target_attend(const vista_desc_t* desc, const int8_t* codes, const float* token_scale,
+                                   const float* token_zero_point, const void* q, const void* k_self,
+                                   const void* v_self, const void* resid, const int64_t* row_offsets,
+                                   int64_t total_rows, void* out, float* lse, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
 /* Bytes of device workspace vista_summarize_merge needs for this descriptor (0 for softmax). */
 vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes);
 

@@ -29,6 +29,7 @@ __all__ = [
     "vista_summarize_bwd_workspace_size", "vista_summarize_bwd", "vista_summarize_fwd_int8",
     "vista_qla_rows_workspace_size", "vista_qla_rows", "vista_summarize_bwd_qla_saved",
     "vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state", "qla_rows_from_state",
+    "vista_target_attend_workspace_size", "vista_target_attend", "target_attend",
     "summarize", "summarize_partial", "summarize_merge", "summarize_bwd", "qla_rows",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
@@ -104,6 +105,8 @@ def load():
     lib.vista_qla_rows.argtypes = [DP, P, P, P, i64, P, P, i64, P, P, P, P, sz, P]
     lib.vista_qla_rows_from_state_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
     lib.vista_qla_rows_from_state.argtypes = [DP, P, P, P, P, i64, P, P, P, P, sz, P]
+    lib.vista_target_attend_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
+    lib.vista_target_attend.argtypes = [DP, P, P, P, P, P, P, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_fwd_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_partial_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge_workspace_size.argtypes = [DP, ctypes.POINTER(sz)]
@@ -115,6 +118,7 @@ def load():
     lib.vista_time_next_main_kernel.restype = ctypes.c_int
     lib.vista_launch_counter.restype = ctypes.c_uint64
     for f in ("vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state",
+              "vista_target_attend_workspace_size", "vista_target_attend",
               "vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
               "vista_summarize_merge", "vista_check_offsets", "vista_summarize_prefix_workspace_size",
               "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
@@ -267,6 +271,21 @@ def vista_qla_rows_from_state(desc, z, user_len, q_rows, row_offsets, total_rows
                                             _ptr(row_offsets), int(total_rows), _ptr(k_self), _ptr(v_self), _ptr(out),
                                             _ptr(workspace), int(workspace_bytes), _stream(stream)),
            "vista_qla_rows_from_state")
+
+
+def vista_target_attend_workspace_size(desc, total_rows) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load().vista_target_attend_workspace_size(ctypes.byref(desc), int(total_rows), ctypes.byref(n)),
+           "vista_target_attend_workspace_size")
+    return n.value
+
+
+def vista_target_attend(desc, codes, token_scale, token_zero_point, q, k_self, v_self, resid, row_offsets, total_rows,
+                        out, lse, workspace, workspace_bytes, stream=None):
+    _check(load().vista_target_attend(ctypes.byref(desc), _ptr(codes), _ptr(token_scale), _ptr(token_zero_point),
+                                      _ptr(q), _ptr(k_self), _ptr(v_self), _ptr(resid), _ptr(row_offsets),
+                                      int(total_rows), _ptr(out), _ptr(lse), _ptr(workspace), int(workspace_bytes),
+                                      _stream(stream)), "vista_target_attend")
 
 
 def vista_summarize_merge_workspace_size(desc: Desc) -> int:
@@ -468,6 +487,27 @@ def qla_rows_from_state(z, user_len, q_rows, row_offsets, total_rows=None, *, k_
     vista_qla_rows_from_state(desc, z, user_len, q_rows, row_offsets, total_rows, k_self, v_self, out, ws, ws.numel(),
                               stream)
     return out
+
+
+def target_attend(codes, token_scale, token_zero_point, q, k_self, v_self, row_offsets, total_rows=None, *,
+                  resid=None, scale=None, out_dtype=None, with_lse=True, workspace=None, stream=None):
+    """Stage-2 target-aware attention (NEXT-4): candidates q, k_self, v_self [R,H,d] attend to the int8
+    summary tokens of their user (codes [B,S,H,d], token_scale / token_zero_point [B,S,H], e.g. the
+    outputs of vista_summarize_fwd_int8) and to themselves.  Returns (out [R,H,d], lse [R,H] or None)."""
+    import torch
+    if total_rows is None:
+        total_rows = q.shape[0]
+    B, S, H, d = codes.shape
+    desc = make_desc(B, S, H, d, in_dtype=_dtype_code(q), out_dtype=out_dtype, attn=SOFTMAX, scale=scale)
+    odt = torch.bfloat16 if desc.out_dtype == BF16 else torch.float32
+    out = torch.empty((q.shape[0], H, d), dtype=odt, device=q.device)
+    lse = torch.empty((q.shape[0], H), dtype=torch.float32, device=q.device) if with_lse else None
+    need = vista_target_attend_workspace_size(desc, total_rows)
+    ws = workspace if workspace is not None and workspace.numel() >= need else \
+        torch.empty(max(need, 16), dtype=torch.uint8, device=q.device)
+    vista_target_attend(desc, codes, token_scale, token_zero_point, q, k_self, v_self, resid, row_offsets, total_rows,
+                        out, lse, ws, ws.numel(), stream)
+    return out, lse
 
 
 def summarize_merge(part_o, part_lse, *, q, attn=SOFTMAX, user_len=None, scale=None, phi1="silu",

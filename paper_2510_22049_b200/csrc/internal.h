@@ -149,6 +149,16 @@ cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, 
 cudaError_t launch_qla_rows_simt(const Problem& p, const float* z, const int64_t* row_offsets, int64_t total_rows,
                                  const void* q, const void* k_self, const void* v_self, int out_bf16, void* out,
                                  const int64_t* user_len = nullptr);
+// stage-2 target-aware attention over the cached int8 summary tokens (NEXT-4, sm100_target_attend.cu)
+bool target_attend_uses_tc(const Problem& p);
+cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offsets, int64_t total_rows,
+                                       const int64_t* uts, const int8_t* codes, const float* tscale, const float* tzp,
+                                       const void* q, const void* k_self, const void* v_self, const void* resid,
+                                       int out_bf16, void* out, float* lse);
+cudaError_t launch_simt_target_attend(const Problem& p, const int64_t* row_offsets, int64_t total_rows,
+                                      const int8_t* codes, const float* tscale, const float* tzp, const void* q,
+                                      const void* k_self, const void* v_self, const void* resid, int out_bf16,
+                                      void* out, float* lse);
 cudaError_t launch_sm100_qla_finalize(const Problem& p, const float* zparts, int P, int64_t part_stride,
                                       const int64_t* user_len, void* ws);
 cudaError_t launch_quantize_rows(int64_t n, int d, int in_bf16, const void* x, int8_t* codes, float* scale, float* zp,

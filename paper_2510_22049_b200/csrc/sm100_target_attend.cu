@@ -1,0 +1,423 @@
+// sm100_target_attend.cu -- stage-2 target-aware attention over the cached summary tokens (NEXT-4).
+//
+// "any attention network can technically be used for the target-aware attention stage ... we selected
+// a standard O(N^2) transformer block, which delivers excellent performance on the compact summary
+// sequences" (Sec. 3.3).  The stage-1 summary tokens are "retrieved from the cache
+// and dequantized": this kernel reads the int8 export of vista_summarize_fwd_int8
+// directly and dequantizes it in the load path.  Reading R22: candidate c of user u
+// attends to [the S tokens of u; itself] and never to another candidate:
+//   t_i = code * scale + zp,  s_i = scale q_c . t_i,  s_self = scale q_c . k_c
+//   out_c = (sum_i e^{s_i} t_i + e^{s_self} v_c) / (sum_i e^{s_i} + e^{s_self})  [+ resid_c]
+//
+// sm100_target_attend_kernel (bf16, d = 128, S in {128, 256}): persistent, stream-K over the flat
+// 128-candidate tiles of the candidates' jagged layout (work.cuh).  Per item (user, head) the S x 128
+// tokens are dequantized once into shared memory (bf16, 128-B swizzle) and serve as the B operand of
+// both GEMMs: K-major for S = Q T^T, MN-major for O = P T.  Per tile: TMA of the q, k_self, v_self
+// rows; S on tcgen05 into TMEM; row softmax (one thread per candidate row, the self logit from shared
+// memory) writing P (bf16) over the S columns; O on tcgen05 (P from TMEM); epilogue adds the self term.
+// simt_target_attend_kernel: CUDA cores, one warp per (candidate, head), any S >= 1, d <= 128, f32 or
+// bf16 -- the shapes the tcgen05 kernel does not take.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "internal.h"
+#include "sm100_ptx.cuh"
+#include "work.cuh"
+
+namespace vista {
+
+bool make_kv_map(CUtensorMap* map, const void* base, int64_t total_len, int H);
+
+namespace {
+
+constexpr int kHalf = 128 * 128;  // one 64-column half of a 128-row bf16 tile
+constexpr int kTileB = 2 * kHalf;  // 32 KB
+constexpr int kThreads = 256;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+// smem: q, k_self, v_self tiles (96 KB), tokens T (S x 128 bf16, <= 64 KB), barriers
+constexpr int kQOff = 0, kKOff = kTileB, kVOff = 2 * kTileB, kTOff = 3 * kTileB;
+constexpr int kBarOff = kTOff + 2 * kTileB;
+constexpr int kSmem = kBarOff + 64 + 1024;
+
+struct TAParams {
+    const int64_t* row_offsets;
+    const int64_t* uts;
+    const int8_t* codes;  // [B, S, H, 128]
+    const float* tscale;  // [B, S, H]
+    const float* tzp;
+    const void* resid;  // [R, H, 128] (in dtype bf16) or NULL
+    void* out;          // [R, H, 128]
+    float* lse;         // [R, H] or NULL
+    int B, S, H, out_bf16;
+    float scale_log2;
+};
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+// 16-B chunk c (of 8) of row r in a SWIZZLE_128B half tile of 128-B rows
+__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+template <int NS>  // N = S tokens
+__device__ __forceinline__ void issue_scores(uint32_t tS, uint32_t sQ, uint32_t sT) {
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, NS, 0, 0);  // Q, T both K-major
+    constexpr int halfT = NS * 128;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+        ptx::mma_ss_w(tS, ptx::sdesc_sw128(sQ + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024),
+                      ptx::sdesc_sw128(sT + (kk >> 2) * halfT + (kk & 3) * 32, 16, 1024), id, kk > 0);
+}
+template <int NS>
+__device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t sT) {
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM) x T (MN-major)
+    constexpr int halfT = NS * 128;
+#pragma unroll
+    for (int kk = 0; kk < NS / 16; ++kk)
+        ptx::mma_ts_w(tO, tP + kk * 8, ptx::sdesc_sw128(sT + kk * 2048, halfT, 1024), id, kk > 0);
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kThreads, 1)
+    sm100_target_attend_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+                               const __grid_constant__ CUtensorMap mapV, const TAParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t base = ptx::smem_u32(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kBarOff);  // 0 tiles full, 1 S done, 2 P ready, 3 O done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kBarOff + 32);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar[0], 1);
+        ptx::mbar_init(&bar[1], 1);
+        ptx::mbar_init(&bar[2], 128);
+        ptx::mbar_init(&bar[3], 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 4) ptx::tmem_alloc(tmem_slot, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tO = tmem + 256;  // S (and P over its first NS/2 columns) | O
+    const int H = P.H;
+    const size_t rstride = (size_t)H * 128;
+    uint32_t ph = 0;  // phase of the per-tile barriers (each completes once per tile)
+    ItemIter iter;
+    iter.init(P.uts, P.B, H, blockIdx.x, gridDim.x);
+    Item it;
+    while (iter.next(it, P.uts, P.B, H)) {
+        const int u = it.u, h = it.hg;
+        // ---- tokens of (u, h): int8 codes * scale + zero point -> bf16, swizzled, both halves
+        for (int x = threadIdx.x; x < NS * 8; x += kThreads) {  // x = (token i, 16-B chunk of codes)
+            const int i = x >> 3, cc = x & 7;                    // codes [16 cc, 16 cc + 16) of token i
+            const size_t tix = ((size_t)u * NS + i) * H + h;
+            const float a = __ldg(P.tscale + tix), b = __ldg(P.tzp + tix);
+            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(P.codes + tix * 128) + cc);
+            const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+            uint32_t o[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int32_t v = (int32_t)w[e];
+                const float f0 = (float)(int8_t)(v & 0xFF), f1 = (float)(int8_t)((v >> 8) & 0xFF);
+                const float f2 = (float)(int8_t)((v >> 16) & 0xFF), f3 = (float)(v >> 24);
+                o[2 * e] = ptx::pack_bf16x2(fmaf(f0, a, b), fmaf(f1, a, b));
+                o[2 * e + 1] = ptx::pack_bf16x2(fmaf(f2, a, b), fmaf(f3, a, b));
+            }
+            // channels 16 cc .. 16 cc + 15 = 16-B bf16 chunks 2 cc, 2 cc + 1 of the row (half = cc / 4)
+            const uint32_t hb = base + kTOff + (cc >> 2) * (NS * 128);
+            const int c0 = (2 * cc) & 7;
+            sts128(hb + swz(i, c0), make_uint4(o[0], o[1], o[2], o[3]));
+            sts128(hb + swz(i, c0 + 1), make_uint4(o[4], o[5], o[6], o[7]));
+        }
+        ptx::fence_proxy_async_smem();
+        __syncthreads();
+        const int64_t R = P.row_offsets[u + 1] - P.row_offsets[u];
+        for (int t = it.t0; t < it.t1; ++t) {
+            const int64_t row0 = P.row_offsets[u] + (int64_t)t * 128;
+            const int64_t remr = R - (int64_t)t * 128;
+            const int valid = remr < 128 ? (int)remr : 128;
+            if (warp == 0) {
+                ptx::mbar_arrive_expect_tx_w(&bar[0], 3 * kTileB);
+                for (int half = 0; half < 2; ++half) {
+                    ptx::tma_load_3d_w(smem + kQOff + half * kHalf, &mapQ, &bar[0], half * 64, h, (int32_t)row0,
+                                       ptx::policy_evict_first());
+                    ptx::tma_load_3d_w(smem + kKOff + half * kHalf, &mapK, &bar[0], half * 64, h, (int32_t)row0,
+                                       ptx::policy_evict_first());
+                    ptx::tma_load_3d_w(smem + kVOff + half * kHalf, &mapV, &bar[0], half * 64, h, (int32_t)row0,
+                                       ptx::policy_evict_first());
+                }
+            }
+            ptx::mbar_wait(&bar[0], ph);
+            if (warp == 4) {
+                ptx::tc_fence_after();
+                issue_scores<NS>(tS, base + kQOff, base + kTOff);
+                ptx::mma_commit_w(&bar[1]);
+            }
+            if (warp < 4) {
+                // ---- softmax over [tokens; self], one thread per candidate row (= TMEM lane)
+                const int row = warp * 32 + lane;
+                const uint32_t lb = (uint32_t)(warp * 32) << 16;
+                float self = 0.f;  // q_c . k_c from the staged tiles
+#pragma unroll
+                for (int half = 0; half < 2; ++half)
+#pragma unroll 4
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 qa = lds128(base + kQOff + half * kHalf + swz(row, c));
+                        const uint4 ka = lds128(base + kKOff + half * kHalf + swz(row, c));
+                        const uint32_t qw[4] = {qa.x, qa.y, qa.z, qa.w}, kw[4] = {ka.x, ka.y, ka.z, ka.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            self = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(kw[e] << 16), self);
+                            self = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(kw[e] & 0xFFFF0000u), self);
+                        }
+                    }
+                self *= P.scale_log2;
+                ptx::mbar_wait(&bar[1], ph);
+                ptx::tc_fence_after();
+                float m = self;
+#pragma unroll 1
+                for (int c = 0; c < NS / 32; ++c) {
+                    uint32_t r[32];
+                    ptx::tmem_ld32_sync(tS + lb + c * 32, r);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]) * P.scale_log2);
+                }
+                float l = 0.f;
+#pragma unroll 1
+                for (int c = 0; c < NS / 32; ++c) {
+                    uint32_t r[32], pk[16];
+                    ptx::tmem_ld32_sync(tS + lb + c * 32, r);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float p0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), P.scale_log2, -m));
+                        const float p1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), P.scale_log2, -m));
+                        l += p0 + p1;
+                        pk[j] = ptx::pack_bf16x2(p0, p1);
+                    }
+                    ptx::tmem_st16(tS + lb + c * 16, pk);  // P over the first NS / 2 S columns (already read)
+                }
+                const float pself = ptx::ex2(self - m);
+                l += pself;
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bar[2]);
+                // ---- epilogue: (O + p_self v_c) / l [+ resid]
+                ptx::mbar_wait(&bar[3], ph);
+                ptx::tc_fence_after();
+                const float inv = 1.f / l;
+#pragma unroll 1
+                for (int half = 0; half < 2; ++half) {
+                    float o[64];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t r[32];
+                        ptx::tmem_ld32_sync(tO + lb + half * 64 + c * 32, r);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) o[32 * c + j] = __uint_as_float(r[j]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 va = lds128(base + kVOff + half * kHalf + swz(row, c));
+                        const uint32_t vw[4] = {va.x, va.y, va.z, va.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            o[8 * c + 2 * e] = fmaf(pself, __uint_as_float(vw[e] << 16), o[8 * c + 2 * e]) * inv;
+                            o[8 * c + 2 * e + 1] =
+                                fmaf(pself, __uint_as_float(vw[e] & 0xFFFF0000u), o[8 * c + 2 * e + 1]) * inv;
+                        }
+                    }
+                    if (row < valid) {
+                        const size_t e0 = (size_t)(row0 + row) * rstride + (size_t)h * 128 + half * 64;
+                        if (P.resid) {
+                            const uint4* rs = reinterpret_cast<const uint4*>(
+                                reinterpret_cast<const __nv_bfloat16*>(P.resid) + e0);
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {
+                                const uint4 ra = __ldg(rs + c);
+                                const uint32_t rw[4] = {ra.x, ra.y, ra.z, ra.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    o[8 * c + 2 * e] += __uint_as_float(rw[e] << 16);
+                                    o[8 * c + 2 * e + 1] += __uint_as_float(rw[e] & 0xFFFF0000u);
+                                }
+                            }
+                        }
+                        if (P.out_bf16) {
+                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + e0);
+#pragma unroll
+                            for (int c = 0; c < 8; ++c)
+                                dst[c] = make_uint4(ptx::pack_bf16x2(o[8 * c], o[8 * c + 1]),
+                                                    ptx::pack_bf16x2(o[8 * c + 2], o[8 * c + 3]),
+                                                    ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]),
+                                                    ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7]));
+                        } else {
+                            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + e0);
+#pragma unroll
+                            for (int c = 0; c < 16; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                        }
+                    }
+                }
+                if (P.lse && row < valid) P.lse[(size_t)(row0 + row) * H + h] = (m + __log2f(l)) * kLn2;
+            } else if (warp == 4) {
+                ptx::mbar_wait(&bar[2], ph);
+                ptx::tc_fence_after();
+                issue_pv<NS>(tO, tS, base + kTOff);
+                ptx::mma_commit_w(&bar[3]);
+            }
+            ph ^= 1;
+            ptx::tc_fence_before();
+            __syncthreads();  // tiles, TMEM and the barriers are reused by the next tile
+            ptx::tc_fence_after();
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 4) ptx::tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------- SIMT: one warp per (candidate, head)
+template <typename T>
+__device__ __forceinline__ float ldv(const T* p, size_t i);
+template <>
+__device__ __forceinline__ float ldv<float>(const float* p, size_t i) { return p[i]; }
+template <>
+__device__ __forceinline__ float ldv<__nv_bfloat16>(const __nv_bfloat16* p, size_t i) { return __bfloat162float(p[i]); }
+
+template <typename T>
+__global__ void simt_target_attend_kernel(const int64_t* __restrict__ row_offsets, const int8_t* __restrict__ codes,
+                                          const float* __restrict__ tscale, const float* __restrict__ tzp,
+                                          const T* __restrict__ q, const T* __restrict__ k_self,
+                                          const T* __restrict__ v_self, const T* __restrict__ resid, int B, int S,
+                                          int H, int d, float scale, int out_bf16, void* __restrict__ out,
+                                          float* __restrict__ lse, int64_t total) {
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (gw >= total * H) return;
+    const int lane = threadIdx.x % 32;
+    const int64_t c = gw / H;
+    const int h = (int)(gw % H);
+    int lo = 0, hi = B;  // user u: row_offsets[u] <= c < row_offsets[u+1]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) / 2;
+        if (row_offsets[mid] <= c) lo = mid; else hi = mid;
+    }
+    const int u = lo;
+    const size_t e0 = ((size_t)c * H + h) * d;
+    float qv[4], acc[4], vv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int e = lane + 32 * j;
+        qv[j] = e < d ? ldv(q, e0 + e) : 0.f;
+        acc[j] = 0.f;
+    }
+    // self logit first, then the tokens, online softmax (natural-log domain, f32)
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int e = lane + 32 * j;
+        if (e < d) s = fmaf(qv[j], ldv(k_self, e0 + e), s);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    float m = s * scale, l = 1.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int e = lane + 32 * j;
+        acc[j] = e < d ? ldv(v_self, e0 + e) : 0.f;
+    }
+    for (int i = 0; i < S; ++i) {
+        const size_t tix = ((size_t)u * S + i) * H + h;
+        const float a = tscale[tix], b = tzp[tix];
+        float dot = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int e = lane + 32 * j;
+            vv[j] = e < d ? fmaf((float)codes[tix * d + e], a, b) : 0.f;
+            dot = fmaf(qv[j], vv[j], dot);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        const float x = dot * scale;
+        const float mn = fmaxf(m, x);
+        const float f = __expf(m - mn), p = __expf(x - mn);
+        l = l * f + p;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = fmaf(acc[j], f, p * vv[j]);
+        m = mn;
+    }
+    const float inv = 1.f / l;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int e = lane + 32 * j;
+        if (e >= d) continue;
+        float y = acc[j] * inv;
+        if (resid) y += ldv(resid, e0 + e);
+        if (out_bf16) reinterpret_cast<__nv_bfloat16*>(out)[e0 + e] = __float2bfloat16_rn(y);
+        else reinterpret_cast<float*>(out)[e0 + e] = y;
+    }
+    if (lse && lane == 0) lse[(size_t)c * H + h] = m + __logf(l);
+}
+
+}  // namespace
+
+bool target_attend_uses_tc(const Problem& p) { return p.in_bf16 && p.d == 128 && (p.S == 128 || p.S == 256); }
+
+cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offsets, int64_t total_rows,
+                                       const int64_t* uts, const int8_t* codes, const float* tscale, const float* tzp,
+                                       const void* q, const void* k_self, const void* v_self, const void* resid,
+                                       int out_bf16, void* out, float* lse) {
+    CUtensorMap mq, mk, mv;
+    if (!make_kv_map(&mq, q, total_rows, p.H) || !make_kv_map(&mk, k_self, total_rows, p.H) ||
+        !make_kv_map(&mv, v_self, total_rows, p.H))
+        return cudaErrorInvalidValue;
+    TAParams P;
+    P.row_offsets = row_offsets;
+    P.uts = uts;
+    P.codes = codes;
+    P.tscale = tscale;
+    P.tzp = tzp;
+    P.resid = resid;
+    P.out = out;
+    P.lse = lse;
+    P.B = p.B;
+    P.S = p.S;
+    P.H = p.H;
+    P.out_bf16 = out_bf16;
+    P.scale_log2 = p.scale * kLog2e;
+    const void* fn = p.S == 256 ? reinterpret_cast<const void*>(sm100_target_attend_kernel<256>)
+                                : reinterpret_cast<const void*>(sm100_target_attend_kernel<128>);
+    const cudaError_t attr = set_smem_attr(fn, kSmem);
+    if (attr != cudaSuccess) return attr;
+    if (p.S == 256) sm100_target_attend_kernel<256><<<p.num_sms, kThreads, kSmem, p.stream>>>(mq, mk, mv, P);
+    else sm100_target_attend_kernel<128><<<p.num_sms, kThreads, kSmem, p.stream>>>(mq, mk, mv, P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_simt_target_attend(const Problem& p, const int64_t* row_offsets, int64_t total_rows,
+                                      const int8_t* codes, const float* tscale, const float* tzp, const void* q,
+                                      const void* k_self, const void* v_self, const void* resid, int out_bf16,
+                                      void* out, float* lse) {
+    if (total_rows == 0) return cudaSuccess;
+    const int64_t warps = total_rows * p.H;
+    const unsigned grid = (unsigned)((warps + 7) / 8);
+    if (p.in_bf16)
+        simt_target_attend_kernel<__nv_bfloat16><<<grid, 256, 0, p.stream>>>(
+            row_offsets, codes, tscale, tzp, reinterpret_cast<const __nv_bfloat16*>(q),
+            reinterpret_cast<const __nv_bfloat16*>(k_self), reinterpret_cast<const __nv_bfloat16*>(v_self),
+            reinterpret_cast<const __nv_bfloat16*>(resid), p.B, p.S, p.H, p.d, p.scale, out_bf16, out, lse, total_rows);
+    else
+        simt_target_attend_kernel<float><<<grid, 256, 0, p.stream>>>(
+            row_offsets, codes, tscale, tzp, reinterpret_cast<const float*>(q), reinterpret_cast<const float*>(k_self),
+            reinterpret_cast<const float*>(v_self), reinterpret_cast<const float*>(resid), p.B, p.S, p.H, p.d, p.scale,
+            out_bf16, out, lse, total_rows);
+    return cudaGetLastError();
+}
+
+}  // namespace vista

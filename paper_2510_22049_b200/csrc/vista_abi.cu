@@ -768,6 +768,67 @@ vista_status_t vista_qla_rows_from_state(const vista_desc_t* desc, const float* 
                        k_self, v_self, out);
 }
 
+// ---------------------------------------------------------------- stage-2 target-aware attention
+vista_status_t vista_target_attend_workspace_size(const vista_desc_t* desc, int64_t total_rows, size_t* bytes) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (!bytes) return VISTA_ERR_NULL;
+    if (total_rows < 0) return VISTA_ERR_INVALID;
+    const Problem p = make_problem(desc, 0);
+    *bytes = target_attend_uses_tc(p) ? align256((size_t)(p.B + 1) * sizeof(int64_t)) : 0;
+    return VISTA_OK;
+}
+
+vista_status_t vista_target_attend(const vista_desc_t* desc, const int8_t* codes, const float* token_scale,
+                                   const float* token_zero_point, const void* q, const void* k_self,
+                                   const void* v_self, const void* resid, const int64_t* row_offsets,
+                                   int64_t total_rows, void* out, float* lse, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (total_rows < 0) return VISTA_ERR_INVALID;
+    if (!row_offsets) return VISTA_ERR_NULL;
+    if (desc->num_users > 0 && (!codes || !token_scale || !token_zero_point)) return VISTA_ERR_NULL;
+    if (total_rows > 0 && (!q || !k_self || !v_self || !out)) return VISTA_ERR_NULL;
+    if (!aligned16(codes) || !aligned16(q) || !aligned16(k_self) || !aligned16(v_self) || !aligned16(resid) ||
+        !aligned16(out) || (reinterpret_cast<uintptr_t>(token_scale) & 3) ||
+        (reinterpret_cast<uintptr_t>(token_zero_point) & 3) || (reinterpret_cast<uintptr_t>(lse) & 3))
+        return VISTA_ERR_MISALIGNED;
+    Problem p = make_problem(desc, 0);
+    p.stream = reinterpret_cast<cudaStream_t>(stream);
+    if (p.B == 0 || total_rows == 0) return VISTA_OK;
+    const int out_bf16 = desc->out_dtype == VISTA_BF16;
+    cudaError_t e;
+    int nl;
+    if (target_attend_uses_tc(p) && total_rows < (int64_t(1) << 31)) {
+        const size_t need = align256((size_t)(p.B + 1) * sizeof(int64_t));
+        if (!workspace || workspace_bytes < need) return VISTA_ERR_WORKSPACE;
+        if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
+        int64_t* uts = reinterpret_cast<int64_t*>(workspace);
+        Problem pr = p;  // tile starts of the candidates' jagged layout
+        pr.offsets = row_offsets;
+        pr.total_len = total_rows;
+        pr.attn = VISTA_QLA;
+        pr.outs = OutSpec{OUT_PARTIAL, 0, nullptr, nullptr};
+        e = launch_user_tiles(pr, uts, nullptr);
+        if (e == cudaSuccess)
+            e = timed_main(p.stream, [&] {
+                return launch_sm100_target_attend(p, row_offsets, total_rows, uts, codes, token_scale, token_zero_point,
+                                                  q, k_self, v_self, resid, out_bf16, out, lse);
+            });
+        nl = 2;
+    } else {
+        e = timed_main(p.stream, [&] {
+            return launch_simt_target_attend(p, row_offsets, total_rows, codes, token_scale, token_zero_point, q,
+                                             k_self, v_self, resid, out_bf16, out, lse);
+        });
+        nl = 1;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches += (unsigned long long)nl;
+    return VISTA_OK;
+}
+
 static size_t merge_ws_bytes(const Problem& p) {
     return (p.attn == VISTA_QLA && qla_finalize_uses_tc(p)) ? sm100_qla_finalize_workspace(p) : 0;
 }

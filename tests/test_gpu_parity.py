@@ -973,3 +973,109 @@ def test_qla_target_rows_c2_full_size_from_state(cuda_lib):
         g = out[256 * u:256 * (u + 1)].float().cpu().numpy()
         for h in range(H):
             assert block_err(g[:, h], ref[:, h]) <= 2e-2, f"user {u} head {h}"
+
+
+# ----------------------------------------------------------------------------- stage-2 target-aware attention (NEXT-4)
+def _ta_case(rng, B, S, H, d, rows, dtype):
+    codes = rng.integers(-127, 128, size=(B, S, H, d)).astype(np.int8)
+    ts = (rng.integers(1, 64, size=(B, S, H)) / 1024.0).astype(np.float32)
+    tz = (rng.integers(-64, 64, size=(B, S, H)) / 128.0).astype(np.float32)
+    roff = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    R = int(roff[-1])
+    g = lambda: (rng.integers(-128, 128, size=(R, H, d)) / 64.0).astype(np.float32)  # noqa: E731
+    return codes, ts, tz, g(), g(), g(), g(), roff
+
+
+def _ta_check(vista, B, S, H, d, rows, dtype, seed, resid, out_dtype, tol, ltol):
+    rng = np.random.default_rng(seed)
+    codes, ts, tz, q, k, v, rs, roff = _ta_case(rng, B, S, H, d, rows, dtype)
+    dev = lambda x: to_dev(x, dtype)  # noqa: E731
+    out, lse = vista.target_attend(torch.from_numpy(codes).cuda(), torch.from_numpy(ts).cuda(),
+                                   torch.from_numpy(tz).cuda(), dev(q), dev(k), dev(v), torch.from_numpy(roff).cuda(),
+                                   resid=dev(rs) if resid else None, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    ref, ref_lse = oracle.target_attend(codes, ts, tz, q, k, v, roff, resid=rs if resid else None)
+    g = out.float().cpu().numpy()
+    # lse gate: the tensor-core path rounds the dequantized tokens to bf16 (relative 2^-9), so a logit
+    # moves by at most scale * sum_e |q_e| * max |t| * 2^-9 (2^-8 with the f32 accumulation slack)
+    t = codes.astype(np.float64) * ts[..., None] + tz[..., None]
+    tmax = np.abs(t).max(axis=(1, 3))  # [B, H]
+    for u in range(B):
+        a, b = roff[u], roff[u + 1]
+        for h in range(H):
+            if b > a:
+                e = block_err(g[a:b, h], ref[a:b, h])
+                assert e <= tol, f"user {u} head {h}: {e:.3g}"
+                bound = np.abs(q[a:b, h]).sum(-1) * tmax[u, h] * 2.0 ** -8 / np.sqrt(d) if dtype == "bf16" else 0.0
+                assert np.all(np.abs(lse[a:b, h].cpu().numpy() - ref_lse[a:b, h]) <= ltol + bound)
+    return out
+
+
+@pytest.mark.parametrize("S,resid,out_bf16", [(256, False, True), (128, True, False), (256, True, True)])
+def test_target_attend_tcgen05(cuda_lib, S, resid, out_bf16):
+    """Ragged candidates per user (none, 1, a tile tail, several tiles), int8 tokens dequantized in
+    the load path, the self key / value, an optional residual; bf16 and f32 out."""
+    vista = cuda_lib
+    _ta_check(vista, 5, S, 2, 128, [130, 0, 1, 300, 128], "bf16", 81, resid, vista.BF16 if out_bf16 else vista.F32,
+              2e-2, 1e-3)
+
+
+@pytest.mark.parametrize("S,d,dtype", [(17, 64, "bf16"), (256, 128, "f32"), (40, 32, "f32")])
+def test_target_attend_simt(cuda_lib, S, d, dtype):
+    vista = cuda_lib
+    tol, ltol = (1e-4, 1e-5) if dtype == "f32" else (2e-2, 1e-3)
+    _ta_check(vista, 3, S, 2, d, [5, 0, 9], dtype, 82, True, vista.F32, tol, ltol)
+
+
+def test_target_attend_candidate_independence_bitwise(cuda_lib):
+    """PAPER.md:156 "the candidates cannot attend each other": a candidate's output is bitwise the same
+    whatever the other candidates of the batch (here: their values replaced), on the tcgen05 path."""
+    vista = cuda_lib
+    rng = np.random.default_rng(83)
+    codes, ts, tz, q, k, v, rs, roff = _ta_case(rng, 2, 256, 2, 128, [200, 57], "bf16")
+    q2, k2, v2 = q.copy(), k.copy(), v.copy()
+    keep = [3, 150, 230]
+    others = np.setdiff1d(np.arange(257), keep)
+    q2[others] = -q2[others]
+    k2[others] = 0.5 * k2[others]
+    v2[others] = v2[others][::-1]
+    args = lambda qq, kk, vv: (torch.from_numpy(codes).cuda(), torch.from_numpy(ts).cuda(),  # noqa: E731
+                               torch.from_numpy(tz).cuda(), to_dev(qq, "bf16"), to_dev(kk, "bf16"), to_dev(vv, "bf16"),
+                               torch.from_numpy(roff).cuda())
+    o1, l1 = vista.target_attend(*args(q, k, v), out_dtype=vista.F32)
+    o2, l2 = vista.target_attend(*args(q2, k2, v2), out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    assert torch.equal(o1[keep], o2[keep]) and torch.equal(l1[keep], l2[keep])
+
+
+def test_target_attend_reads_the_summarize_int8_export(cuda_lib):
+    """Stage 1 -> export -> stage 2 on the device: vista_summarize_fwd_int8's codes / scales feed
+    vista_target_attend directly; checked against the oracle applied to the same exported codes."""
+    vista = cuda_lib
+    lens = [3000, 129, 700]
+    S, H, d = 256, 2, 128
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=84)
+    qt, kt, vt = to_dev(q, "bf16"), to_dev(k, "bf16"), to_dev(v, "bf16")
+    ot = torch.from_numpy(off).cuda()
+    B = len(lens)
+    desc = vista.make_desc(B, S, H, d, in_dtype=vista.BF16, out_dtype=vista.BF16)
+    need = vista.vista_summarize_workspace_size(desc, int(off[-1]))
+    ws = torch.empty(max(need, 16), dtype=torch.uint8, device="cuda")
+    out = torch.empty((B, S, H, d), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((B, H, S), dtype=torch.float32, device="cuda")
+    codes = torch.empty((B, S, H, d), dtype=torch.int8, device="cuda")
+    sc = torch.empty((B, S, H), dtype=torch.float32, device="cuda")
+    zp = torch.empty((B, S, H), dtype=torch.float32, device="cuda")
+    vista.vista_summarize_fwd_int8(desc, qt, kt, vt, ot, int(off[-1]), out, lse, codes, sc, zp, ws, need)
+    rng = np.random.default_rng(85)
+    rows = [64, 200, 1]
+    roff = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    cq, ck, cv = [(rng.integers(-128, 128, size=(int(roff[-1]), H, d)) / 64.0).astype(np.float32) for _ in range(3)]
+    o, l = vista.target_attend(codes, sc, zp, to_dev(cq, "bf16"), to_dev(ck, "bf16"), to_dev(cv, "bf16"),
+                               torch.from_numpy(roff).cuda(), out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    ref, _ = oracle.target_attend(codes.cpu().numpy(), sc.cpu().numpy(), zp.cpu().numpy(), cq, ck, cv, roff)
+    g = o.cpu().numpy()
+    for u in range(B):
+        for h in range(H):
+            assert block_err(g[roff[u]:roff[u + 1], h], ref[roff[u]:roff[u + 1], h]) <= 2e-2

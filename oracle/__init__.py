@@ -61,6 +61,7 @@ def _load():
         lib.vo_qla_backward.argtypes = [i64, i64, i64, i64, P, i64, P, P, P, P, i32, i32, i32, P, P, P, i32]
         lib.vo_num_threads.restype = i32
         lib.vo_target_attend.argtypes = [i64, i64, i64, i64, P, P, P, P, P, P, P, P, f64, P, P, i32]
+        lib.vo_summarize_layers.argtypes = [i64, i64, i64, i64, i64, P, P, P, i32, i32, i32, P, i32]
         _lib = lib
     return _lib
 
@@ -328,3 +329,21 @@ def target_attend(codes, tscale, tzp, q, k_self, v_self, row_offsets, scale=None
     if rc != 0:
         raise ValueError("vo_target_attend failed")
     return out, lse
+
+
+def summarize_layers(x, offsets, weights, S, H, phi1="silu", phi2="silu", normalize=True, threads=0):
+    """Multi-layer summarizer (NEXT-3, vo_summarize_layers): x [R, D] (user u = rows [offsets[u],
+    offsets[u+1]), its first S rows the seed rows), weights [L, 5, D, D] (q, k, v, g, o; row = output).
+    Returns x after the layers [R, D] float64; the summary tokens are each user's first S rows."""
+    x = _f32(x)
+    weights = _f32(weights)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    R, D = x.shape
+    L = weights.shape[0]
+    assert weights.shape[1:] == (5, D, D) and D % H == 0
+    out = np.empty((R, D), np.float64)
+    rc = _load().vo_summarize_layers(len(offsets) - 1, S, H, D // H, L, _ptr(weights), _ptr(x), _ptr(offsets),
+                                     ACT[phi1], ACT[phi2], int(bool(normalize)), _ptr(out), int(threads))
+    if rc != 0:
+        raise ValueError("vo_summarize_layers failed")
+    return out

@@ -31,6 +31,9 @@
  *  NEXT-3 / NEXT-4: QLA at arbitrary per-user query rows (history rows of a deeper layer, or
  *  target rows with the Delta self term), vo_qla_rows.
  *
+ *  NEXT-3: the multi-layer summarizer (projections, QLA over [seeds; history], SGLU gate, output
+ *  projection, residual), vo_summarize_layers.
+ *
  *  NEXT-4: stage-2 target-aware attention of candidates over the cached (int8-exported) summary
  *  tokens, vo_target_attend.
  *
@@ -571,5 +574,91 @@ int vo_target_attend(int64_t B, int64_t S, int64_t H, int64_t d, const signed ch
         free(t);
         free(sc);
     }
+    return 0;
+}
+
+/*
+ * Multi-layer summarizer (NEXT-3).  "self-attention with virtual seed embeddings to summarize
+ * ultra-long UIH sequences" (Sec. 3.2) with "the QLU module and the SGLU module"
+ * (Sec. 3.2.2), full (not causal) self-attention, 3 -> 5 layers in
+ * production.  Reading R23: user u's sequence
+ * X = [S seed rows; L_u history rows] (rows [offsets[u], offsets[u+1]) of x, width D = H d); per layer
+ *   Q = X Wq^T, K = X Wk^T, V = X Wv^T, G = X Wg^T                     (W* [D][D], row = output)
+ *   per head h (columns [h d, h d + d)):  Z = sum_{rows j of u} phi1(K_jh)^T V_jh,
+ *        W_h = phi2(Z / N_u) (N_u = S + L_u when normalizing),  O_rh = phi1(Q_rh) W_h
+ *   Y = (O (.) sigmoid(G)) Wo^T,   X <- X + Y
+ * After the layers, the summary tokens are the first S rows of every user.
+ * weights: [L][5][D][D] (q, k, v, g, o); x: [R][D] input; x_out: [R][D] after the layers (float64).
+ */
+int vo_summarize_layers(int64_t B, int64_t S, int64_t H, int64_t d, int64_t n_layers, const float* weights,
+                        const float* x, const int64_t* offsets, int phi1, int phi2, int normalize, double* x_out,
+                        int threads) {
+    if (B < 0 || S < 1 || H < 1 || d < 1 || n_layers < 0) return -1;
+    set_threads(threads);
+    const int64_t D = H * d, R = offsets[B];
+    for (int64_t e = 0; e < R * D; ++e) x_out[e] = (double)x[e];
+    double* qkvg = (double*)malloc((size_t)(R * 4 * D) * sizeof(double));
+    double* o = (double*)malloc((size_t)(R * D) * sizeof(double));
+    if (!qkvg || !o) {
+        free(qkvg);
+        free(o);
+        return -1;
+    }
+    for (int64_t layer = 0; layer < n_layers; ++layer) {
+        const float* W = weights + layer * 5 * D * D;
+        /* projections: qkvg[r][t*D + c] = sum_i x[r][i] W_t[c][i] */
+#pragma omp parallel for schedule(static)
+        for (int64_t r = 0; r < R; ++r)
+            for (int64_t t = 0; t < 4; ++t)
+                for (int64_t c = 0; c < D; ++c) {
+                    double acc = 0.0;
+                    for (int64_t i = 0; i < D; ++i) acc += x_out[r * D + i] * (double)W[(t * D + c) * D + i];
+                    qkvg[r * 4 * D + t * D + c] = acc;
+                }
+        /* QLA over all rows of the user, per head */
+#pragma omp parallel
+        {
+            double* z = (double*)malloc((size_t)(d * d) * sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+            for (int64_t t = 0; t < B * H; ++t) {
+                const int64_t u = t / H, h = t % H;
+                const int64_t N = offsets[u + 1] - offsets[u];
+                const double inv = (normalize && N > 0) ? 1.0 / (double)N : 1.0;
+                for (int64_t e = 0; e < d * d; ++e) z[e] = 0.0;
+                for (int64_t j = offsets[u]; j < offsets[u + 1]; ++j)
+                    for (int64_t c1 = 0; c1 < d; ++c1) {
+                        const double a = vo_act(phi1, qkvg[j * 4 * D + D + h * d + c1]);
+                        for (int64_t c2 = 0; c2 < d; ++c2) z[c1 * d + c2] += a * qkvg[j * 4 * D + 2 * D + h * d + c2];
+                    }
+                for (int64_t e = 0; e < d * d; ++e) z[e] = vo_act(phi2, z[e] * inv);
+                for (int64_t r = offsets[u]; r < offsets[u + 1]; ++r)
+                    for (int64_t c2 = 0; c2 < d; ++c2) {
+                        double acc = 0.0;
+                        for (int64_t c1 = 0; c1 < d; ++c1) acc += vo_act(phi1, qkvg[r * 4 * D + h * d + c1]) * z[c1 * d + c2];
+                        o[r * D + h * d + c2] = acc;
+                    }
+            }
+            free(z);
+        }
+        /* SGLU gate, output projection, residual */
+        const float* Wo = W + 4 * D * D;
+#pragma omp parallel
+        {
+            double* gated = (double*)malloc((size_t)D * sizeof(double));
+#pragma omp for schedule(static)
+            for (int64_t r = 0; r < R; ++r) {
+                for (int64_t i = 0; i < D; ++i)
+                    gated[i] = o[r * D + i] / (1.0 + exp(-qkvg[r * 4 * D + 3 * D + i]));
+                for (int64_t c = 0; c < D; ++c) {
+                    double acc = 0.0;
+                    for (int64_t i = 0; i < D; ++i) acc += gated[i] * (double)Wo[c * D + i];
+                    x_out[r * D + c] += acc;
+                }
+            }
+            free(gated);
+        }
+    }
+    free(qkvg);
+    free(o);
     return 0;
 }

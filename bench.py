@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--qla-rows", choices=["history", "target"], default=None,
                     help="NEXT-3/4 (QLA): the step is vista_qla_rows -- every history item as a query row of its "
                          "own user (history), or 256 target rows per user with the Delta self term (target)")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="NEXT-3: the step is an N-layer summarizer (vista_summarize_layers: projections, QLA over "
+                         "[seeds; history], SGLU, output projection, residual) over the batch")
     ap.add_argument("--stage2", action="store_true",
                     help="NEXT-4: the step is stage-2 target-aware attention (vista_target_attend) of "
                          f"{TARGETS_PER_USER} candidates per user over the int8 export of the batch's summary tokens")
@@ -159,6 +162,9 @@ def run_own(args, rank, world, local_rank):
     cfg, lens, S, H, d, wdesc = workload(args.config, args.attn)
     if args.backward:
         wdesc += " backward (NEXT-2, from the forward's saved " + ("out, lse)" if args.attn == "softmax" else "state Z)")
+    if args.layers:
+        wdesc += (f" {args.layers}-layer summarizer (NEXT-3: X = [S seeds; history] per user, D = H d; per layer the "
+                  "QKVG projection GEMM, QLA state + rows over all rows, SGLU-gated output GEMM + residual)")
     if args.stage2:
         wdesc += (f" stage-2 target-aware attention (NEXT-4: {TARGETS_PER_USER} candidates per user over the "
                   f"{S} int8 summary tokens of the user + itself)")
@@ -281,6 +287,29 @@ def run_own(args, rank, world, local_rank):
                 vista.vista_target_attend(sdesc, ins[0], ins[1], ins[2], ins[3], ins[4], ins[5], None, ins[6], n_rows,
                                           s2_out, s2_lse, s2_ws, s2_bytes, None)
                 return [s2_out, s2_lse]
+        if args.layers:
+            D = H * d
+            seg = np.asarray([S + int(L) for L in lens], dtype=np.int64)
+            x_off = synth.offsets_from_lengths(seg)
+            R_rows = int(x_off[-1])
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(999 + rank)
+            x0 = (torch.randint(-128, 128, (R_rows, D), device=dev, generator=gen).float() / 64).to(torch.bfloat16)
+            wl = (torch.randint(-128, 128, (args.layers, 5, D, D), device=dev, generator=gen).float()
+                  / (128.0 * math.sqrt(D))).to(torch.bfloat16)
+            xw = torch.empty_like(x0)
+            xoff_t = torch.from_numpy(x_off).to(dev)
+            ldesc = vista.make_desc(B, S, H, d, in_dtype=vista.BF16, out_dtype=vista.BF16, attn=vista.QLA)
+            l_bytes = vista.vista_summarize_layers_workspace_size(ldesc, args.layers, R_rows)
+            l_ws = torch.empty(max(l_bytes, 16), dtype=torch.uint8, device=dev)
+            tokens = torch.empty((B, S, H, d), dtype=torch.bfloat16, device=dev)
+            inputs = [x0, wl, xoff_t]
+
+            def step(ins=inputs):
+                xw.copy_(ins[0])  # the layers update X in place: every step starts from the embeddings
+                vista.vista_summarize_layers(ldesc, args.layers, ins[1], xw, ins[2], R_rows, tokens, l_ws, l_bytes,
+                                             None)
+                return [tokens]
         items_per_step = world * (n_rows if args.stage2 else total)
         scaling = "weak"
         parallel = f"by_user x{world} (weak: a {args.config} batch per GPU, no data-path collective)"
@@ -514,6 +543,9 @@ def run_own(args, rank, world, local_rank):
     if args.qla_rows:  # rows kernel: q read, out written (bf16) [+ k_self, v_self read], W_u per unit
         flops = 2.0 * d * d * H * n_rows
         io_bytes = 4.0 * d * H * n_rows * (2 if args.qla_rows == "target" else 1) + B * H * d * d * 2
+    if args.layers:  # projection GEMM of the first layer: X [R, D] x [Wq|Wk|Wv|Wg]^T [4D, D]
+        flops = 2.0 * R_rows * D * 4 * D
+        io_bytes = 2.0 * R_rows * D * 5 + 4 * D * D * 2
     if args.stage2:  # target attention: q, k_c, v_c read, out written (bf16), lse; int8 tokens + scales
         flops = 4.0 * S * d * H * n_rows
         io_bytes = 4.0 * 2 * d * H * n_rows + 4.0 * H * n_rows + B * S * H * (d + 8)
@@ -523,9 +555,17 @@ def run_own(args, rank, world, local_rank):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         tkey = f"{args.config}_{args.attn}" + ("_bwd" if args.backward else "") + \
-            (f"_rows_{args.qla_rows}" if args.qla_rows else "") + ("_stage2" if args.stage2 else "")
+            (f"_rows_{args.qla_rows}" if args.qla_rows else "") + ("_stage2" if args.stage2 else "") + \
+            (f"_layers{args.layers}" if args.layers else "")
         traffic = json.load(open(tpath)).get(tkey)
-    if args.stage2:
+    if args.layers:
+        roof = {"bound": "tensor", "achieved": round(tflops, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": round(tflops / pk["bf16_tflops"], 4), "traffic": traffic,
+                "peak_kind": f"{pk_kind} bf16 burst", "kernel": "sm100_gemm_kernel (QKVG projection)",
+                "kernel_ms": round(kern_ms, 5), "algorithmic_flop_per_launch": flops,
+                "hbm": {"achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": round(gbs / pk["hbm_gbs"], 4), "algorithmic_bytes_per_launch": io_bytes}}
+    elif args.stage2:
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic, "peak_kind": f"{pk_kind} HBM copy",
                 "kernel": "sm100_target_attend_kernel", "kernel_ms": round(kern_ms, 5),
@@ -595,7 +635,7 @@ def run_own(args, rank, world, local_rank):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=None, stage2=False):
+def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=None, stage2=False, layers=0):
     """Time the float64 oracle on whole users (all rows, all heads) of the rank-0 batch until
     ~`seconds` of CPU work; returns (items/s, cores, sample description, equivalent items, s)."""
     import numpy as np
@@ -614,7 +654,14 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=Non
         rr = np.arange(a, b, dtype=np.int64)
         k, v = synth.make_kv(rr, np.full(b - a, u), H, d, seed=0)
         t0 = time.perf_counter()
-        if stage2:  # NEXT-4: target attention of the user's candidates over its int8 tokens
+        if layers:  # NEXT-3: the multi-layer summarizer over [seeds; history] of one user
+            rng = np.random.default_rng(u)
+            D = H * d
+            xu = (rng.integers(-128, 128, size=(S + b - a, D)) / 64.0).astype(np.float32)
+            wl = (rng.integers(-128, 128, size=(layers, 5, D, D)) / (128.0 * np.sqrt(D))).astype(np.float32)
+            t0 = time.perf_counter()
+            oracle.summarize_layers(xu, [0, S + b - a], wl, S, H, threads=cores)
+        elif stage2:  # NEXT-4: target attention of the user's candidates over its int8 tokens
             rng = np.random.default_rng(u)
             n = TARGETS_PER_USER
             cds = rng.integers(-127, 128, size=(1, S, H, d)).astype(np.int8)
@@ -653,6 +700,8 @@ def oracle_sample(config, attn, seconds, rows=None, backward=False, qla_rows=Non
         sample += f", {attn} backward (oracle.{attn}_backward)"
     if qla_rows:
         sample += f", QLA {qla_rows} rows (oracle.qla_rows)"
+    if layers:
+        sample += f", {layers}-layer summarizer (oracle.summarize_layers)"
     if stage2:
         sample = (f"{users} user(s) x {TARGETS_PER_USER} candidates over {S} int8 tokens, all {H} heads, "
                   "float64 C oracle (oracle.target_attend), OpenMP; unit candidates/s")
@@ -729,6 +778,10 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    if args.layers:
+        args.attn = "qla"  # the summarizer layers are QLA layers
+        if args.backward or args.export_int8 or args.qla_rows or args.stage2:
+            raise SystemExit("--layers excludes --backward / --export-int8 / --qla-rows / --stage2")
     if args.stage2:
         args.attn = "softmax"  # stage 2 reads the softmax summary's int8 export
         if args.backward or args.export_int8 or args.qla_rows:
@@ -774,7 +827,8 @@ def main():
     res = run_own(args, rank, world, local_rank)
     if res is not None and world == 1 and not args.no_cpu_baseline:
         v, cores, sample, _, t = oracle_sample(args.config, args.attn, args.cpu_seconds, rows=None,
-                                               backward=args.backward, qla_rows=args.qla_rows, stage2=args.stage2)
+                                               backward=args.backward, qla_rows=args.qla_rows, stage2=args.stage2,
+                                               layers=args.layers)
         res["cpu_baseline"] = {"value": v, "unit": "candidates/s" if args.stage2 else "items/s", "cores": cores,
                                "kind": "oracle",
                                "sample": sample, "seconds": round(t, 2)}

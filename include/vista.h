@@ -255,6 +255,33 @@ vista_status_t vista_summarize_bwd_qla_saved(const vista_desc_t* desc, const voi
                                              size_t workspace_bytes, void* stream);
 
 /*
+ * Multi-layer summarizer (NEXT-3): "self-attention with virtual seed embeddings to summarize
+ * ultra-long UIH sequences" built from "the QLU module and the SGLU module"
+ * (PAPER.md:214), full self-attention, several layers.
+ * DESIGN.md reading R23: user u's sequence is X_u = [S seed rows; L_u history rows]
+ * = rows [x_offsets[u], x_offsets[u+1]) of x (the caller lays them out; the first S rows of every
+ * segment are the seed rows), width D = H d.  Each layer, on tcgen05:
+ *   [Q | K | V | G] = X [Wq | Wk | Wv | Wg]^T                       (one GEMM, four outputs)
+ *   Z_uh = sum_{rows j of u} phi1(K_jh)^T V_jh;  O_rh = phi1(Q_rh) phi2(Z_uh / N_u), N_u = S + L_u
+ *   X <- X + (O (.) sigmoid(G)) Wo^T                                (gate fused into the GEMM's load
+ *                                                                     path, residual into its epilogue)
+ * The summary tokens are the first S rows of every user after the layers.
+ * desc: B, S, H, d = 128, in_dtype VISTA_BF16, attn VISTA_QLA (phi1, phi2, qla_normalize), shared
+ *   seeds (q_user_stride = 0); out_dtype is the dtype of tokens.
+ *   weights  bf16 [num_layers][5][D][D]: Wq, Wk, Wv, Wg, Wo, each [out][in] (row-major)   (DEVICE)
+ *   x        bf16 [total_rows, D], updated IN PLACE through the layers                   (DEVICE)
+ *   x_offsets int64 [B+1] (DEVICE); every segment at least S rows (a precondition)
+ *   tokens   [B, S, H, d] (out_dtype) or NULL: the summary tokens after the last layer
+ * Workspace: at least vista_summarize_layers_workspace_size bytes.  Other dtypes / d:
+ * VISTA_ERR_UNSUPPORTED.  Asynchronous on stream; deterministic.
+ */
+vista_status_t vista_summarize_layers_workspace_size(const vista_desc_t* desc, int32_t num_layers,
+                                                     int64_t total_rows, size_t* bytes);
+vista_status_t vista_summarize_layers(const vista_desc_t* desc, int32_t num_layers, const void* weights,
+                                      void* x, const int64_t* x_offsets, int64_t total_rows, void* tokens,
+                                      void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Stage-2 target-aware attention over the cached summary tokens (NEXT-4).  "any attention network can
  * technically be used for the target-aware attention stage ... a standard O(N^2) transformer block"
  * (Sec. 3.3), over the summary tokens "retrieved from the cache and dequantized"

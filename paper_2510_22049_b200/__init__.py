@@ -30,6 +30,7 @@ __all__ = [
     "vista_qla_rows_workspace_size", "vista_qla_rows", "vista_summarize_bwd_qla_saved",
     "vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state", "qla_rows_from_state",
     "vista_target_attend_workspace_size", "vista_target_attend", "target_attend",
+    "vista_summarize_layers_workspace_size", "vista_summarize_layers", "summarize_layers",
     "summarize", "summarize_partial", "summarize_merge", "summarize_bwd", "qla_rows",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
@@ -107,6 +108,8 @@ def load():
     lib.vista_qla_rows_from_state.argtypes = [DP, P, P, P, P, i64, P, P, P, P, sz, P]
     lib.vista_target_attend_workspace_size.argtypes = [DP, i64, ctypes.POINTER(sz)]
     lib.vista_target_attend.argtypes = [DP, P, P, P, P, P, P, P, P, i64, P, P, P, sz, P]
+    lib.vista_summarize_layers_workspace_size.argtypes = [DP, i32, i64, ctypes.POINTER(sz)]
+    lib.vista_summarize_layers.argtypes = [DP, i32, P, P, P, i64, P, P, sz, P]
     lib.vista_summarize_fwd_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_partial_prefix.argtypes = [DP, P, P, P, P, i64, P, P, i64, P, P, P, sz, P]
     lib.vista_summarize_merge_workspace_size.argtypes = [DP, ctypes.POINTER(sz)]
@@ -119,6 +122,7 @@ def load():
     lib.vista_launch_counter.restype = ctypes.c_uint64
     for f in ("vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state",
               "vista_target_attend_workspace_size", "vista_target_attend",
+              "vista_summarize_layers_workspace_size", "vista_summarize_layers",
               "vista_summarize_workspace_size", "vista_summarize_fwd", "vista_summarize_partial",
               "vista_summarize_merge", "vista_check_offsets", "vista_summarize_prefix_workspace_size",
               "vista_summarize_fwd_prefix", "vista_summarize_partial_prefix",
@@ -286,6 +290,20 @@ def vista_target_attend(desc, codes, token_scale, token_zero_point, q, k_self, v
                                       _ptr(q), _ptr(k_self), _ptr(v_self), _ptr(resid), _ptr(row_offsets),
                                       int(total_rows), _ptr(out), _ptr(lse), _ptr(workspace), int(workspace_bytes),
                                       _stream(stream)), "vista_target_attend")
+
+
+def vista_summarize_layers_workspace_size(desc, num_layers, total_rows) -> int:
+    n = ctypes.c_size_t(0)
+    _check(load().vista_summarize_layers_workspace_size(ctypes.byref(desc), int(num_layers), int(total_rows),
+                                                        ctypes.byref(n)), "vista_summarize_layers_workspace_size")
+    return n.value
+
+
+def vista_summarize_layers(desc, num_layers, weights, x, x_offsets, total_rows, tokens, workspace, workspace_bytes,
+                           stream=None):
+    _check(load().vista_summarize_layers(ctypes.byref(desc), int(num_layers), _ptr(weights), _ptr(x), _ptr(x_offsets),
+                                         int(total_rows), _ptr(tokens), _ptr(workspace), int(workspace_bytes),
+                                         _stream(stream)), "vista_summarize_layers")
 
 
 def vista_summarize_merge_workspace_size(desc: Desc) -> int:
@@ -508,6 +526,29 @@ def target_attend(codes, token_scale, token_zero_point, q, k_self, v_self, row_o
     vista_target_attend(desc, codes, token_scale, token_zero_point, q, k_self, v_self, resid, row_offsets, total_rows,
                         out, lse, ws, ws.numel(), stream)
     return out, lse
+
+
+def summarize_layers(x, x_offsets, weights, S, H, total_rows=None, *, phi1="silu", phi2="silu", normalize=True,
+                     out_dtype=None, workspace=None, stream=None):
+    """Multi-layer summarizer (NEXT-3): x [R, D] bf16 (user u = rows [x_offsets[u], x_offsets[u+1]), its
+    first S rows the seed rows), weights [L, 5, D, D] bf16 (Wq, Wk, Wv, Wg, Wo as [out][in]).  x is
+    updated in place; returns the summary tokens [B, S, H, d]."""
+    import torch
+    if total_rows is None:
+        total_rows = x.shape[0]
+    B = x_offsets.numel() - 1
+    D = x.shape[1]
+    d = D // H
+    L = weights.shape[0]
+    desc = make_desc(B, S, H, d, in_dtype=BF16, out_dtype=out_dtype, attn=QLA, phi1=phi1, phi2=phi2,
+                     normalize=normalize)
+    odt = torch.bfloat16 if desc.out_dtype == BF16 else torch.float32
+    tokens = torch.empty((B, S, H, d), dtype=odt, device=x.device)
+    need = vista_summarize_layers_workspace_size(desc, L, total_rows)
+    ws = workspace if workspace is not None and workspace.numel() >= need else \
+        torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
+    vista_summarize_layers(desc, L, weights, x, x_offsets, total_rows, tokens, ws, ws.numel(), stream)
+    return tokens
 
 
 def summarize_merge(part_o, part_lse, *, q, attn=SOFTMAX, user_len=None, scale=None, phi1="silu",

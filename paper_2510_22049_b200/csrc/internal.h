@@ -145,10 +145,16 @@ cudaError_t launch_qla_prep_w(const Problem& p, const float* z, uint8_t* wbuf, c
 bool qla_rows_uses_tc(const Problem& p, int64_t total_rows);
 cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, int64_t total_rows, const int64_t* uts,
                                   const uint8_t* w_op, const void* q, const void* k_self, const void* v_self,
-                                  int out_bf16, void* out, const int64_t* user_len = nullptr);
+                                  int out_bf16, void* out, const int64_t* user_len = nullptr,
+                                  const void* gate = nullptr);
 cudaError_t launch_qla_rows_simt(const Problem& p, const float* z, const int64_t* row_offsets, int64_t total_rows,
                                  const void* q, const void* k_self, const void* v_self, int out_bf16, void* out,
                                  const int64_t* user_len = nullptr);
+// multi-layer summarizer (NEXT-3): tcgen05 GEMM C = A B^T (sm100_gemm.cu) and the seed-row gather
+cudaError_t launch_sm100_gemm(int M, int N, int K, const void* A, int64_t lda, const void* Bw, int nsplit,
+                              void* const* outs, const void* resid, int num_sms, cudaStream_t stream);
+cudaError_t launch_gather_seed_rows(const void* x, const int64_t* x_offsets, int B, int S, int D, int out_bf16,
+                                    void* tokens, cudaStream_t stream);
 // stage-2 target-aware attention over the cached int8 summary tokens (NEXT-4, sm100_target_attend.cu)
 bool target_attend_uses_tc(const Problem& p);
 cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offsets, int64_t total_rows,

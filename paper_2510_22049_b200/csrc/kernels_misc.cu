@@ -735,6 +735,20 @@ cudaError_t launch_quantize_rows(int64_t n, int d, int in_bf16, const void* x, i
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Summary tokens of the multi-layer summarizer: the first S rows of every user's segment of x
+// [R, D] (bf16) -> tokens [B, S, D] (bf16 or f32).  One block per (user, seed row).
+__global__ void gather_seed_rows_kernel(const __nv_bfloat16* __restrict__ x, const int64_t* __restrict__ x_offsets,
+                                        int S, int D, int out_bf16, void* __restrict__ tokens) {
+    const int u = blockIdx.x / S, i = blockIdx.x % S;
+    const __nv_bfloat16* src = x + (size_t)(x_offsets[u] + i) * D;
+    const size_t dst = ((size_t)u * S + i) * D;
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+        if (out_bf16) reinterpret_cast<__nv_bfloat16*>(tokens)[dst + c] = src[c];
+        else reinterpret_cast<float*>(tokens)[dst + c] = __bfloat162float(src[c]);
+    }
+}
+
 // ============================================================================== launchers
 cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf) {
     user_tiles_kernel<<<1, 1024, 0, p.stream>>>(p.offsets, p.B, uts, p.outs, p.S, p.H, p.d,
@@ -897,4 +911,14 @@ cudaError_t launch_add_prefix_state(const Problem& p, float* z, const float* zpr
     return cudaGetLastError();
 }
 
+}  // namespace vista
+
+namespace vista {
+cudaError_t launch_gather_seed_rows(const void* x, const int64_t* x_offsets, int B, int S, int D, int out_bf16,
+                                    void* tokens, cudaStream_t stream) {
+    if (B == 0) return cudaSuccess;
+    gather_seed_rows_kernel<<<B * S, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(x), x_offsets, S, D,
+                                                       out_bf16, tokens);
+    return cudaGetLastError();
+}
 }  // namespace vista

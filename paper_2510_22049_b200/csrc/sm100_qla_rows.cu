@@ -68,6 +68,7 @@ struct Params {
     void* out;                    // [R, H, 128] bf16 or f32
     const int64_t* offsets;       // history offsets [B+1]: N_u for the Delta term's 1/N ...
     const int64_t* user_len;      // ... or N_u given directly ([B], may be NULL)
+    const __nv_bfloat16* gate;    // [R, H, 128] or NULL: out = o (.) sigmoid(gate) (the summarizer's SGLU gate)
     int out_bf16;
     int normalize;
     int B, H;
@@ -344,6 +345,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::mbar_arrive(&bars->q_empty[stage]);  // v_self read: the stage may be refilled
                 }
+                if (P.gate && row < valid) {  // SGLU gate (reading R23): o (.) sigmoid(g), sigmoid via one tanh
+                    const uint4* gs = reinterpret_cast<const uint4*>(P.gate + e0 + (size_t)row * rstride + chalf * 64);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 b = __ldg(gs + c);
+                        const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            float t0, t1;
+                            asm("tanh.approx.f32 %0, %1;" : "=f"(t0) : "f"(0.5f * __uint_as_float(bw[e] << 16)));
+                            asm("tanh.approx.f32 %0, %1;" : "=f"(t1) : "f"(0.5f * __uint_as_float(bw[e] & 0xFFFF0000u)));
+                            o[8 * c + 2 * e] *= fmaf(0.5f, t0, 0.5f);
+                            o[8 * c + 2 * e + 1] *= fmaf(0.5f, t1, 0.5f);
+                        }
+                    }
+                }
                 if (P.out_bf16) {
                     // coalesced: permuted 32x32b store into the (read) accumulator columns, 16x256b load
                     // back, so a quad of threads holds 128 contiguous bytes of one row
@@ -456,7 +473,7 @@ bool qla_rows_uses_tc(const Problem& p, int64_t total_rows) {
 // w_op: the W_u operands (qla_prep_w); user_len: N_u per user (NULL: from p.offsets)
 cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, int64_t total_rows, const int64_t* uts,
                                   const uint8_t* w_op, const void* q, const void* k_self, const void* v_self,
-                                  int out_bf16, void* out, const int64_t* user_len) {
+                                  int out_bf16, void* out, const int64_t* user_len, const void* gate) {
     CUtensorMap mq, mk, mv;
     if (!make_kv_map(&mq, q, total_rows, p.H)) return cudaErrorInvalidValue;
     const bool delta = k_self != nullptr;
@@ -470,6 +487,7 @@ cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, 
     P.out = out;
     P.offsets = p.offsets;
     P.user_len = user_len;
+    P.gate = reinterpret_cast<const __nv_bfloat16*>(gate);
     P.normalize = p.normalize;
     P.out_bf16 = out_bf16;
     P.B = p.B;

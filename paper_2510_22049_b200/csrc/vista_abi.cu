@@ -1,6 +1,7 @@
 // vista_abi.cu -- the C ABI of libvista (include/vista.h): validation, workspace planning,
 // dispatch by shape, launch sequencing.  All device work is enqueued on the caller's stream;
 // nothing here synchronizes (except the debug entry vista_check_offsets).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -653,7 +654,7 @@ RowsPlan plan_rows(const Problem& p, int64_t total_rows, bool with_state) {
 // SIMT kernel).  N_u from user_len (if given) or p.offsets.
 vista_status_t rows_from_z(const vista_desc_t* desc, const Problem& p, const RowsPlan& r, char* ws, const float* z,
                            const int64_t* user_len, const void* q_rows, const int64_t* row_offsets, int64_t total_rows,
-                           const void* k_self, const void* v_self, void* out) {
+                           const void* k_self, const void* v_self, void* out, const void* gate = nullptr) {
     const int out_bf16 = desc->out_dtype == VISTA_BF16;
     cudaError_t e;
     int nl = 0;
@@ -670,7 +671,7 @@ vista_status_t rows_from_z(const vista_desc_t* desc, const Problem& p, const Row
         if (e == cudaSuccess)
             e = timed_main(p.stream, [&] {
                 return launch_sm100_qla_rows(p, row_offsets, total_rows, uts, w_op, q_rows, k_self, v_self, out_bf16,
-                                             out, user_len);
+                                             out, user_len, gate);
             });
         nl = 3;
     } else {
@@ -766,6 +767,115 @@ vista_status_t vista_qla_rows_from_state(const vista_desc_t* desc, const float* 
     if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
     return rows_from_z(desc, p, r, reinterpret_cast<char*>(workspace), z, user_len, q_rows, row_offsets, total_rows,
                        k_self, v_self, out);
+}
+
+// ---------------------------------------------------------------- multi-layer summarizer (NEXT-3)
+namespace {
+struct LayersPlan {
+    size_t qkvg_off, o_off, z_off, sub_off, rows_off, total;
+};
+LayersPlan plan_layers(const Problem& p, int64_t R) {
+    LayersPlan l{};
+    const size_t D = (size_t)p.H * p.d;
+    size_t off = 0;
+    l.qkvg_off = off;
+    off = align256(off + 4 * (size_t)R * D * 2);
+    l.o_off = off;
+    off = align256(off + (size_t)R * D * 2);
+    l.z_off = off;
+    off = align256(off + (size_t)p.B * p.H * p.d * p.d * sizeof(float));
+    l.sub_off = off;
+    Problem ps = p;
+    ps.total_len = R;
+    ps.attn = VISTA_QLA;
+    off = align256(off + plan_workspace(ps, true).total);
+    l.rows_off = off;
+    off = align256(off + plan_rows(ps, R, false).total);
+    l.total = off;
+    return l;
+}
+bool layers_supported(const vista_desc_t* d) {
+    return d->in_dtype == VISTA_BF16 && d->head_dim == 128 && d->attn == VISTA_QLA && d->q_user_stride == 0;
+}
+}  // namespace
+
+vista_status_t vista_summarize_layers_workspace_size(const vista_desc_t* desc, int32_t num_layers, int64_t total_rows,
+                                                     size_t* bytes) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (!bytes) return VISTA_ERR_NULL;
+    if (num_layers < 0 || total_rows < 0) return VISTA_ERR_INVALID;
+    if (!layers_supported(desc)) return VISTA_ERR_UNSUPPORTED;
+    *bytes = plan_layers(make_problem(desc, total_rows), total_rows).total;
+    return VISTA_OK;
+}
+
+vista_status_t vista_summarize_layers(const vista_desc_t* desc, int32_t num_layers, const void* weights, void* x,
+                                      const int64_t* x_offsets, int64_t total_rows, void* tokens, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    if (num_layers < 0 || total_rows < 0) return VISTA_ERR_INVALID;
+    if (!layers_supported(desc)) return VISTA_ERR_UNSUPPORTED;
+    if (!x_offsets || (total_rows > 0 && !x) || (num_layers > 0 && !weights)) return VISTA_ERR_NULL;
+    if (!aligned16(weights) || !aligned16(x) || !aligned16(tokens)) return VISTA_ERR_MISALIGNED;
+    if (total_rows >= (int64_t(1) << 31)) return VISTA_ERR_UNSUPPORTED;
+    Problem p = make_problem(desc, total_rows);
+    p.stream = reinterpret_cast<cudaStream_t>(stream);
+    if (p.B == 0) return VISTA_OK;
+    const LayersPlan l = plan_layers(p, total_rows);
+    if (!workspace || workspace_bytes < l.total) return VISTA_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return VISTA_ERR_MISALIGNED;
+    char* ws = reinterpret_cast<char*>(workspace);
+    const int R = (int)total_rows, D = p.H * p.d;
+    const size_t RD = (size_t)R * D;
+    __nv_bfloat16* qkvg = reinterpret_cast<__nv_bfloat16*>(ws + l.qkvg_off);
+    void* outs[4] = {qkvg, qkvg + RD, qkvg + 2 * RD, qkvg + 3 * RD};  // Q, K, V, G [R, D] each
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(ws + l.o_off);
+    float* z = reinterpret_cast<float*>(ws + l.z_off);
+    vista_desc_t dq = *desc;  // the QLA state / rows over all rows of every user's segment
+    dq.attn = VISTA_QLA;
+    dq.in_dtype = VISTA_BF16;
+    dq.out_dtype = VISTA_BF16;
+    Problem pr = make_problem(&dq, total_rows);
+    pr.offsets = x_offsets;
+    pr.stream = p.stream;
+    const RowsPlan rp = plan_rows(pr, total_rows, false);
+    cudaError_t e = cudaSuccess;
+    for (int layer = 0; layer < num_layers && R > 0; ++layer) {
+        const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(weights) + (size_t)layer * 5 * D * D;
+        // 1. [Q | K | V | G] = X [Wq | Wk | Wv | Wg]^T
+        // (the timing hook, if armed, brackets the first layer's projection GEMM, the dominant kernel)
+        if ((e = timed_main(p.stream, [&] {
+                 return launch_sm100_gemm(R, 4 * D, D, x, D, W, 4, outs, nullptr, p.num_sms, p.stream);
+             })) != cudaSuccess)
+            break;
+        g_launches += 1;
+        // 2. Z_u = sum over the user's rows of phi1(K)^T V (the state kernel, partial mode)
+        cudaEvent_t ev_a = g_ev_start, ev_b = g_ev_stop;
+        g_ev_start = g_ev_stop = nullptr;
+        st = run(&dq, outs[0], outs[1], outs[2], x_offsets, total_rows, OutSpec{OUT_PARTIAL, 0, z, nullptr},
+                 ws + l.sub_off, l.rows_off - l.sub_off, stream);
+        g_ev_start = ev_a;
+        g_ev_stop = ev_b;
+        if (st != VISTA_OK) return st;
+        // 3. O_r = (phi1(Q_r) phi2(Z_u / N_u)) (.) sigmoid(G_r) for every row (N_u = the segment's length;
+        //    the SGLU gate applied in the rows kernel's epilogue, so O is written once, gated)
+        st = rows_from_z(&dq, pr, rp, ws + l.rows_off, z, nullptr, outs[0], x_offsets, total_rows, nullptr, nullptr, o,
+                         outs[3]);
+        if (st != VISTA_OK) return st;
+        // 4. X <- X + O Wo^T (the residual in the GEMM's epilogue)
+        void* xo[4] = {x, x, x, x};
+        if ((e = launch_sm100_gemm(R, D, D, o, D, W + 4 * (size_t)D * D, 1, xo, x, p.num_sms, p.stream)) != cudaSuccess)
+            break;
+        g_launches += 1;
+    }
+    if (e == cudaSuccess && tokens) {
+        e = launch_gather_seed_rows(x, x_offsets, p.B, p.S, D, desc->out_dtype == VISTA_BF16, tokens, p.stream);
+        g_launches += 1;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    return VISTA_OK;
 }
 
 // ---------------------------------------------------------------- stage-2 target-aware attention

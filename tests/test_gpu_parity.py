@@ -1079,3 +1079,39 @@ def test_target_attend_reads_the_summarize_int8_export(cuda_lib):
     for u in range(B):
         for h in range(H):
             assert block_err(g[roff[u]:roff[u + 1], h], ref[roff[u]:roff[u + 1], h]) <= 2e-2
+
+
+# ----------------------------------------------------------------------------- multi-layer summarizer (NEXT-3)
+def _layers_case(rng, lens, S, H, n_layers, d=128):
+    D = H * d
+    off = np.concatenate([[0], np.cumsum([S + L for L in lens])]).astype(np.int64)
+    x = ((rng.integers(-128, 128, size=(int(off[-1]), D)) / 64.0)).astype(np.float32)
+    # weights ~ U(-1, 1) / sqrt(D) / 2: activations stay O(1) through the layers (with twice that
+    # scale they grow ~10^4-fold over three layers and bf16 rounding of the intermediates dominates)
+    W = (rng.integers(-128, 128, size=(n_layers, 5, D, D)) / (128.0 * np.sqrt(D))).astype(np.float32)
+    return x, off, W
+
+
+@pytest.mark.parametrize("lens,S,H,n_layers", [([300, 0, 1000], 128, 1, 3), ([129, 2000], 256, 2, 2)])
+def test_summarize_layers(cuda_lib, lens, S, H, n_layers):
+    """3 (2) summarizer layers (projections, QLA over [seeds; history], SGLU, output projection,
+    residual) on tcgen05 against the float64 oracle of the per-layer definition: the tokens (each
+    user's first S rows) and every updated row, per (user, head-column block)."""
+    vista = cuda_lib
+    rng = np.random.default_rng(91)
+    x, off, W = _layers_case(rng, lens, S, H, n_layers)
+    xt = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    x_bf = xt.float().cpu().numpy()  # the bf16-rounded input the GPU sees
+    Wt = torch.from_numpy(W).cuda().to(torch.bfloat16)
+    W_bf = Wt.float().cpu().numpy()
+    tok = vista.summarize_layers(xt, torch.from_numpy(off).cuda(), Wt, S, H, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    ref = oracle.summarize_layers(x_bf, off, W_bf, S, H)
+    g = xt.float().cpu().numpy()
+    d = 128
+    for u in range(len(lens)):
+        a, b = off[u], off[u + 1]
+        for h in range(H):
+            c = slice(h * d, (h + 1) * d)
+            assert block_err(g[a:b, c], ref[a:b, c]) <= 2e-2, f"user {u} head {h}"
+            assert block_err(tok[u, :, h].cpu().numpy(), ref[a:a + S, c]) <= 2e-2

@@ -614,14 +614,16 @@ def run_own(args, rank, world, local_rank):
                                     "on the launching stream"},
     }
     if sustained is not None:
-        sp = pk.get("bf16_tflops_sustained") if attn == vista.SOFTMAX else pk["hbm_gbs"]
-        if attn == vista.SOFTMAX:
+        # same bound and unit as the burst roofline above, against the sustained denominator
+        tensor_bound = roof["bound"] == "tensor"
+        sp = pk.get("bf16_tflops_sustained") if tensor_bound else pk["hbm_gbs"]
+        if tensor_bound:
             ach = flops / (sustained["kernel_ms"] / 1e3) / 1e12
         else:
             ach = io_bytes / (sustained["kernel_ms"] / 1e3) / 1e9
-        sustained["roofline"] = {"achieved": round(ach, 2), "unit": roof["unit"], "peak": sp,
-                                 "frac": round(ach / sp, 4) if sp else None,
-                                 "peak_kind": ("measured bf16 sustained (power-capped GEMM)" if attn == vista.SOFTMAX
+        sustained["roofline"] = {"bound": roof["bound"], "achieved": round(ach, 2), "unit": roof["unit"],
+                                 "peak": sp, "frac": round(ach / sp, 4) if sp else None,
+                                 "peak_kind": ("measured bf16 sustained (power-capped GEMM)" if tensor_bound
                                                else "measured HBM copy")}
         sustained["note"] = ("SURVEY 8(d) protocol: R graph-replayed steps per run (>= 200 ms), median of 5 runs; "
                              "the sustained regime the K-step burst number sits above")

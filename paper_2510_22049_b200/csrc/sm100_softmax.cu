@@ -37,6 +37,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "internal.h"
 #include "int8_export.cuh"
@@ -53,7 +54,11 @@ __device__ unsigned long long g_vista_trace[28][64];
 #define VTRACE(ev, g) \
     do { if (blockIdx.x == 0 && (g) < 64) g_vista_trace[ev][g] = clock64(); } while (0)
 __device__ unsigned long long g_vista_cta[256][4];  // per CTA: globaltimer start / end, clock64 start / end
+__device__ int g_vista_probe[2][64];  // CTA 0 softmax: s_full / p_free already complete at the first probe
+#define VPROBE(i, g, bar, par) \
+    do { if (blockIdx.x == 0 && (g) < 64) g_vista_probe[i][g] = ptx::mbar_test_wait(bar, par) ? 1 : 0; } while (0)
 #else
+#define VPROBE(i, g, bar, par) do { } while (0)
 #define VTRACE(ev, g) do { } while (0)
 #endif
 
@@ -68,10 +73,17 @@ constexpr float kLn2 = 0.6931471805599453f;
 #define VISTA_KSTAGES 3
 #endif
 constexpr int kKStages = VISTA_KSTAGES, kVStages = 5 - VISTA_KSTAGES;
+// CTA-pair mode (cta_group::2): a stage holds this CTA's half of a tile (K: 64 keys x 128
+// channels, V: 128 keys x 64 channels), so the same 160 KB of rings hold more stages
+constexpr int kPairBytes = kTileBytes / 2;
+constexpr int kPairKStages = 6, kPairVStages = 4;
+constexpr int kMaxStages = 6;
 
 constexpr int kQOff = 0;
 constexpr int kKOff = kQOff + kTileBytes;
 constexpr int kVOff = kKOff + kKStages * kTileBytes;
+constexpr int kPairVOff = kKOff + kPairKStages * kPairBytes;
+static_assert(kPairVOff + kPairVStages * kPairBytes == kVOff + kVStages * kTileBytes, "same ring footprint");
 constexpr int kThreads = 512;
 constexpr int kTmemCols = 512;
 constexpr int kItemRing = 16;
@@ -93,7 +105,7 @@ struct ItemEntry {
 struct Bars {
     uint64_t it_full[kItemRing], it_empty[kItemRing];
     uint64_t q_full, q_empty;  // the item's Q tile in smem / its last S done
-    uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
+    uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages];
     uint64_t s_full[2], s_free[2];  // S(g) in buffer g % 2 complete / loaded by both softmax halves
     uint64_t p_full[2], p_free[2];  // P(g) in buffer g % 2 written (256 arrivals) / read by PV(g)
     uint64_t pv_done;               // one completion per PV (the rescale waits for the previous one)
@@ -293,6 +305,47 @@ __device__ __forceinline__ float exp_half(const uint32_t (&r)[2][32], float sl2,
     return (la + lb) + (lc + ld);
 }
 
+// The same exponentials into registers (pk: the bf16x2 P words of this thread's 64 keys); the
+// caller stores them once the exponent offset is known to stand.
+__device__ __forceinline__ float exp_regs(const uint32_t (&r)[2][32], float sl2, float neg, uint32_t (&pk)[2][16]) {
+    const uint64_t sl2x2 = ptx::f2_pack(sl2, sl2);
+    const uint64_t negx2 = ptx::f2_pack(neg, neg);
+    uint64_t acc[2] = {ptx::f2_pack(0.f, 0.f), ptx::f2_pack(0.f, 0.f)};
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t x2 = ptx::f2_fma(
+                ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
+            float x0, x1;
+            ptx::f2_unpack(x2, x0, x1);
+            const uint64_t p2 = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+            acc[j & 1] = ptx::f2_add(acc[j & 1], p2);
+            float p0, p1;
+            ptx::f2_unpack(p2, p0, p1);
+            pk[c][j] = ptx::pack_bf16x2(p0, p1);
+        }
+    float la, lb, lc, ld;
+    ptx::f2_unpack(acc[0], la, lb);
+    ptx::f2_unpack(acc[1], lc, ld);
+    return (la + lb) + (lc + ld);
+}
+
+// max of this thread's 64 raw scores (4 independent FMNMX3 chains), then with the row's other thread
+__device__ __forceinline__ float row_max(const uint32_t (&r)[2][32]) {
+    float m4[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int c = a >> 1, o = (a & 1) * 16;
+        float m = ptx::max3(__uint_as_float(r[c][o]), __uint_as_float(r[c][o + 1]), __uint_as_float(r[c][o + 2]));
+#pragma unroll
+        for (int j = 3; j < 15; j += 2) m = ptx::max3(m, __uint_as_float(r[c][o + j]), __uint_as_float(r[c][o + j + 1]));
+        m4[a] = fmaxf(m, __uint_as_float(r[c][o + 15]));
+    }
+    const float mh = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    return fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, 16));
+}
+
 // ---- MMA issue with compile-time geometry (descriptors stay in uniform registers) ----
 template <int KS>
 __device__ __forceinline__ void issue_S_t(uint32_t tS, uint32_t sQa, uint32_t sKa) {
@@ -331,7 +384,60 @@ __device__ __forceinline__ void issue_PV(int vs, uint32_t tO, uint32_t tP, uint3
     }
 }
 
-template <int C>
+// ---- CTA pair (cta_group::2, M = 256; issued by the leader CTA for both) ----
+template <int KS>
+__device__ __forceinline__ void issue_S2_t(uint32_t tS, uint32_t sQa, uint32_t sKa) {
+    // S = Q K^T: A = Q (each CTA its 128 rows), B = K tile split along N: each CTA holds 64 keys x
+    // 128 channels (two 8 KB channel halves)
+    constexpr uint32_t idS = ptx::idesc_bf16_f32(256, 128, 0, 0);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+        ptx::mma2_ss_w(tS, ptx::sdesc_sw128(sQa + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024),
+                       ptx::sdesc_sw128(sKa + KS * kPairBytes + (kk >> 2) * (kPairBytes / 2) + (kk & 3) * 32, 16, 1024),
+                       idS, kk > 0);
+}
+template <int VS>
+__device__ __forceinline__ void issue_PV2_t(uint32_t tO, uint32_t tP, uint32_t sVa, bool acc) {
+    // O += P V: A = P from each CTA's TMEM, B = V tile split along N = channels: each CTA holds all
+    // 128 keys x 64 channels (one 128-B swizzle column)
+    constexpr uint32_t idP = ptx::idesc_bf16_f32(256, 128, 0, 1);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+        ptx::mma2_ts_w(tO, tP + kk * 8, ptx::sdesc_sw128(sVa + VS * kPairBytes + kk * 2048, kHalfBytes, 1024), idP,
+                       (acc || kk > 0) ? 1u : 0u);
+}
+__device__ __forceinline__ void issue_S2(int ks, uint32_t tS, uint32_t sQa, uint32_t sKa) {
+    static_assert(kPairKStages == 6, "stage switch");
+    switch (ks) {
+        case 0: issue_S2_t<0>(tS, sQa, sKa); break;
+        case 1: issue_S2_t<1>(tS, sQa, sKa); break;
+        case 2: issue_S2_t<2>(tS, sQa, sKa); break;
+        case 3: issue_S2_t<3>(tS, sQa, sKa); break;
+        case 4: issue_S2_t<4>(tS, sQa, sKa); break;
+        default: issue_S2_t<5>(tS, sQa, sKa); break;
+    }
+}
+__device__ __forceinline__ void issue_PV2(int vs, uint32_t tO, uint32_t tP, uint32_t sVa, bool acc) {
+    static_assert(kPairVStages == 4, "stage switch");
+    switch (vs) {
+        case 0: issue_PV2_t<0>(tO, tP, sVa, acc); break;
+        case 1: issue_PV2_t<1>(tO, tP, sVa, acc); break;
+        case 2: issue_PV2_t<2>(tO, tP, sVa, acc); break;
+        default: issue_PV2_t<3>(tO, tP, sVa, acc); break;
+    }
+}
+
+// arrive of one warp (lane 0, after the warp's own tcgen05 accesses are fenced) on a barrier of
+// the pair's leader CTA: local for the leader, through the cluster window for the peer
+__device__ __forceinline__ void warp_arrive_leader(uint64_t* bar, int rank) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        if (rank == 0) ptx::mbar_arrive(bar);
+        else ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(bar), 0), 1);
+    }
+}
+
+template <int C, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_softmax_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
                          const __grid_constant__ CUtensorMap mapV, const Params P) {
@@ -339,11 +445,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem + kQOff;
     uint8_t* sK = smem + kKOff;
-    uint8_t* sV = smem + kVOff;
+    uint8_t* sV = smem + (PAIR ? kPairVOff : kVOff);
     Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
     ItemEntry* ring = reinterpret_cast<ItemEntry*>(smem + kRingOff);
 
+    static_assert(!PAIR || C == 2, "a CTA pair is a cluster of two");
     constexpr uint16_t kMask = (uint16_t)((1u << C) - 1u);
+    constexpr int KST = PAIR ? kPairKStages : kKStages, VST = PAIR ? kPairVStages : kVStages;
     constexpr int kSlice = 128 / C;  // K/V rows this CTA loads (and multicasts) per tile
     constexpr int kRows = C * 128;   // query rows per unit
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -363,30 +471,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bars->it_full[s], 1);
             ptx::mbar_init(&bars->it_empty[s], kRingConsumers);
         }
+        // pair mode: the full barriers of the leader count its producer's expect_tx (both halves'
+        // bytes) and the TMA completions of both CTAs; the leader's MMA commits arrive on the
+        // barriers of both CTAs (count 1); the consumers of both CTAs arrive once per warp on the
+        // leader's s_free / p_full / o_empty
         ptx::mbar_init(&bars->q_full, 1);
         ptx::mbar_init(&bars->q_empty, 1);
-        for (int s = 0; s < kKStages; ++s) {
+        for (int s = 0; s < KST; ++s) {
             ptx::mbar_init(&bars->k_full[s], 1);
-            ptx::mbar_init(&bars->k_empty[s], C);  // released by every CTA of the cluster
+            ptx::mbar_init(&bars->k_empty[s], PAIR ? 1 : C);  // multicast mode: released by every CTA
         }
-        for (int s = 0; s < kVStages; ++s) {
+        for (int s = 0; s < VST; ++s) {
             ptx::mbar_init(&bars->v_full[s], 1);
-            ptx::mbar_init(&bars->v_empty[s], C);
+            ptx::mbar_init(&bars->v_empty[s], PAIR ? 1 : C);
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&bars->s_full[b], 1);
-            ptx::mbar_init(&bars->s_free[b], 256);
-            ptx::mbar_init(&bars->p_full[b], 256);
+            ptx::mbar_init(&bars->s_free[b], PAIR ? 16 : 256);
+            ptx::mbar_init(&bars->p_full[b], PAIR ? 16 : 256);
             ptx::mbar_init(&bars->p_free[b], 1);
         }
         ptx::mbar_init(&bars->pv_done, 1);
         ptx::mbar_init(&bars->o_full, 1);
-        ptx::mbar_init(&bars->o_empty, 128);
+        ptx::mbar_init(&bars->o_empty, PAIR ? 8 : 128);
         ptx::mbar_init(&bars->ml_full, 256);
         ptx::mbar_init(&bars->ml_empty, 128);
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, kTmemCols);
+    if (warp == 1) {
+        if constexpr (PAIR) ptx::tmem_alloc2(&bars->tmem_base, kTmemCols);
+        else ptx::tmem_alloc(&bars->tmem_base, kTmemCols);
+    }
     // PDL: everything above overlapped the scan kernel; its results (uts) are needed from here on
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0 && rank == 0) {
@@ -446,24 +561,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int h = it.hg / P.G, g = it.hg % P.G;
                 if (k >= 1) ptx::mbar_wait(&bars->q_empty, (uint32_t)(k - 1) & 1u);  // previous item's S done
                 if (lane == 0) VTRACE(17, k);
-                ptx::mbar_arrive_expect_tx_w(&bars->q_full, kTileBytes);
-                for (int half = 0; half < 2; ++half)
-                    ptx::tma_load_4d_w(sQ + half * kHalfBytes, &mapQ, &bars->q_full, half * 64, h,
-                                       g * kRows + rank * 128, P.q_per_user ? it.u : 0, pol_q);
+                if constexpr (PAIR) {
+                    // this CTA's Q rows; completion on the leader's q_full (armed for both CTAs)
+                    const uint32_t qf = ptx::mapa(ptx::smem_u32(&bars->q_full), 0);
+                    if (rank == 0) ptx::mbar_arrive_expect_tx_w(&bars->q_full, 2 * kTileBytes);
+                    for (int half = 0; half < 2; ++half)
+                        ptx::tma_load_4d_2sm_w(ptx::smem_u32(sQ + half * kHalfBytes), &mapQ, qf, half * 64, h,
+                                               g * kRows + rank * 128, P.q_per_user ? it.u : 0, pol_q);
+                } else {
+                    ptx::mbar_arrive_expect_tx_w(&bars->q_full, kTileBytes);
+                    for (int half = 0; half < 2; ++half)
+                        ptx::tma_load_4d_w(sQ + half * kHalfBytes, &mapQ, &bars->q_full, half * 64, h,
+                                           g * kRows + rank * 128, P.q_per_user ? it.u : 0, pol_q);
+                }
                 for (int t = it.t0; t < it.t1; ++t) {
                     ptx::mbar_wait(&bars->k_empty[stage], phase ^ 1);
                     if (lane == 0) VTRACE(5, gk);
                     ++gk;
-                    ptx::mbar_arrive_expect_tx_w(&bars->k_full[stage], kTileBytes);
-                    const int32_t row = row0 + t * kTile + rank * kSlice;
-                    for (int half = 0; half < 2; ++half) {
-                        uint8_t* dst = sK + stage * kTileBytes + half * kHalfBytes + rank * kSlice * 128;
-                        if constexpr (C > 1)
-                            ptx::tma_load_3d_mc_w(dst, &mapK, &bars->k_full[stage], half * 64, h, row, kMask, pol_kv);
-                        else
-                            ptx::tma_load_3d_w(dst, &mapK, &bars->k_full[stage], half * 64, h, row, pol_kv);
+                    if constexpr (PAIR) {
+                        // keys [64 rank, 64 rank + 64) of the tile, both channel halves
+                        const uint32_t kf = ptx::mapa(ptx::smem_u32(&bars->k_full[stage]), 0);
+                        if (rank == 0) ptx::mbar_arrive_expect_tx_w(&bars->k_full[stage], 2 * kPairBytes);
+                        const int32_t row = row0 + t * kTile + rank * 64;
+                        for (int half = 0; half < 2; ++half)
+                            ptx::tma_load_3d_2sm_w(ptx::smem_u32(sK + stage * kPairBytes + half * (kPairBytes / 2)), &mapK,
+                                                   kf, half * 64, h, row, pol_kv);
+                    } else {
+                        ptx::mbar_arrive_expect_tx_w(&bars->k_full[stage], kTileBytes);
+                        const int32_t row = row0 + t * kTile + rank * kSlice;
+                        for (int half = 0; half < 2; ++half) {
+                            uint8_t* dst = sK + stage * kTileBytes + half * kHalfBytes + rank * kSlice * 128;
+                            if constexpr (C > 1)
+                                ptx::tma_load_3d_mc_w(dst, &mapK, &bars->k_full[stage], half * 64, h, row, kMask, pol_kv);
+                            else
+                                ptx::tma_load_3d_w(dst, &mapK, &bars->k_full[stage], half * 64, h, row, pol_kv);
+                        }
                     }
-                    if (++stage == kKStages) { stage = 0; phase ^= 1; }
+                    if (++stage == KST) { stage = 0; phase ^= 1; }
                 }
             }
         } else if (warp == 2) {
@@ -478,17 +612,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&bars->v_empty[stage], phase ^ 1);
                     if (lane == 0) VTRACE(6, gv);
                     ++gv;
-                    ptx::mbar_arrive_expect_tx_w(&bars->v_full[stage], kTileBytes);
-                    const int32_t row = it.row0 + t * kTile + rank * kSlice;
-                    for (int half = 0; half < 2; ++half) {
-                        uint8_t* dst = sV + stage * kTileBytes + half * kHalfBytes + rank * kSlice * 128;
-                        if constexpr (C > 1)
-                            ptx::tma_load_3d_mc_w(dst, &mapV, &bars->v_full[stage], half * 64, h, row, kMask, pol_kv);
-                        else
-                            ptx::tma_load_3d_w(dst, &mapV, &bars->v_full[stage], half * 64, h, row, pol_kv);
+                    if constexpr (PAIR) {
+                        // all 128 keys of the tile, channels [64 rank, 64 rank + 64)
+                        const uint32_t vf = ptx::mapa(ptx::smem_u32(&bars->v_full[stage]), 0);
+                        if (rank == 0) ptx::mbar_arrive_expect_tx_w(&bars->v_full[stage], 2 * kPairBytes);
+                        ptx::tma_load_3d_2sm_w(ptx::smem_u32(sV + stage * kPairBytes), &mapV, vf, rank * 64, h,
+                                               it.row0 + t * kTile, pol_kv);
+                    } else {
+                        ptx::mbar_arrive_expect_tx_w(&bars->v_full[stage], kTileBytes);
+                        const int32_t row = it.row0 + t * kTile + rank * kSlice;
+                        for (int half = 0; half < 2; ++half) {
+                            uint8_t* dst = sV + stage * kTileBytes + half * kHalfBytes + rank * kSlice * 128;
+                            if constexpr (C > 1)
+                                ptx::tma_load_3d_mc_w(dst, &mapV, &bars->v_full[stage], half * 64, h, row, kMask, pol_kv);
+                            else
+                                ptx::tma_load_3d_w(dst, &mapV, &bars->v_full[stage], half * 64, h, row, pol_kv);
+                        }
                     }
-                    if (++stage == kVStages) { stage = 0; phase ^= 1; }
+                    if (++stage == VST) { stage = 0; phase ^= 1; }
                 }
+            }
+        } else if (PAIR && rank != 0) {
+            // pair mode: the peer CTA's MMA warps only drain the item ring (the leader issues for both)
+            for (int k = 0; fetch_item(bars, ring, k, it); ++k) {
             }
         } else if (warp == 1) {
             // ============================ score MMAs ============================
@@ -506,18 +652,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&bars->k_full[kst], kph);
                     VTRACE(8, g);
                     ptx::tc_fence_after();
-                    issue_S(kst, tmem + b * 128, sQa, sKa);
-                    ptx::mma_commit_w(&bars->s_full[b]);
-                    if constexpr (C > 1) ptx::mma_commit_mc_w(&bars->k_empty[kst], kMask);
-                    else ptx::mma_commit_w(&bars->k_empty[kst]);
-                    if (t == it.t1 - 1) ptx::mma_commit_w(&bars->q_empty);  // Q free once its last S completes
+                    if constexpr (PAIR) {
+                        issue_S2(kst, tmem + b * 128, sQa, sKa);
+                        ptx::mma2_commit_mc_w(&bars->s_full[b]);
+                        ptx::mma2_commit_mc_w(&bars->k_empty[kst]);
+                        if (t == it.t1 - 1) ptx::mma2_commit_mc_w(&bars->q_empty);
+                    } else {
+                        issue_S(kst, tmem + b * 128, sQa, sKa);
+                        ptx::mma_commit_w(&bars->s_full[b]);
+                        if constexpr (C > 1) ptx::mma_commit_mc_w(&bars->k_empty[kst], kMask);
+                        else ptx::mma_commit_w(&bars->k_empty[kst]);
+                        if (t == it.t1 - 1) ptx::mma_commit_w(&bars->q_empty);  // Q free once its last S completes
+                    }
                     VTRACE(0, g);
-                    if (++kst == kKStages) { kst = 0; kph ^= 1; }
+                    if (++kst == KST) { kst = 0; kph ^= 1; }
                 }
             }
         } else {
             // ============================ PV MMAs ============================
-            const uint32_t sVa = base + kVOff;
+            const uint32_t sVa = base + (PAIR ? kPairVOff : kVOff);
             int vst = 0, g = 0;
             uint32_t vph = 0;
             for (int k = 0; fetch_item(bars, ring, k, it); ++k) {
@@ -532,14 +685,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&bars->p_full[b], (uint32_t)(g >> 1) & 1u);
                     VTRACE(1, g);
                     ptx::tc_fence_after();
-                    issue_PV(vst, tmem + 256, tmem + 384 + b * 64, sVa, t > it.t0);
-                    ptx::mma_commit_w(&bars->p_free[b]);
-                    ptx::mma_commit_w(&bars->pv_done);
-                    if constexpr (C > 1) ptx::mma_commit_mc_w(&bars->v_empty[vst], kMask);
-                    else ptx::mma_commit_w(&bars->v_empty[vst]);
-                    if (t == it.t1 - 1) ptx::mma_commit_w(&bars->o_full);
+                    if constexpr (PAIR) {
+                        issue_PV2(vst, tmem + 256, tmem + 384 + b * 64, sVa, t > it.t0);
+                        ptx::mma2_commit_mc_w(&bars->p_free[b]);
+                        ptx::mma2_commit_mc_w(&bars->pv_done);
+                        ptx::mma2_commit_mc_w(&bars->v_empty[vst]);
+                        if (t == it.t1 - 1) ptx::mma2_commit_mc_w(&bars->o_full);
+                    } else {
+                        issue_PV(vst, tmem + 256, tmem + 384 + b * 64, sVa, t > it.t0);
+                        ptx::mma_commit_w(&bars->p_free[b]);
+                        ptx::mma_commit_w(&bars->pv_done);
+                        if constexpr (C > 1) ptx::mma_commit_mc_w(&bars->v_empty[vst], kMask);
+                        else ptx::mma_commit_w(&bars->v_empty[vst]);
+                        if (t == it.t1 - 1) ptx::mma_commit_w(&bars->o_full);
+                    }
                     VTRACE(2, g);
-                    if (++vst == kVStages) { vst = 0; vph ^= 1; }
+                    if (++vst == VST) { vst = 0; vph ^= 1; }
                 }
             }
         }
@@ -561,6 +722,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int b = g & 1;
                 const uint32_t tS = tmem + lane_bits + b * 128;
                 const uint32_t tP = tmem + lane_bits + 384 + b * 64;
+                if (row == 0 && ch == 0) {
+                    VTRACE(26, g);
+                    VPROBE(0, g, &bars->s_full[b], (uint32_t)(g >> 1) & 1u);
+                }
                 ptx::mbar_wait(&bars->s_full[b], (uint32_t)(g >> 1) & 1u);
                 if (row == 0 && ch == 0) VTRACE(3, g);
                 ptx::tc_fence_after();
@@ -571,7 +736,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::reg_fence(r[0]);
                 ptx::reg_fence(r[1]);
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&bars->s_free[b]);  // S buffer b may take S(g + 2)
+                if constexpr (PAIR) warp_arrive_leader(&bars->s_free[b], rank);
+                else ptx::mbar_arrive(&bars->s_free[b]);  // S buffer b may take S(g + 2)
                 if (row == 0 && ch == 0) VTRACE(12, g);
                 const int valid = L - t * kTile - ch * 64;  // valid keys among this thread's 64
                 if (valid < 64) {
@@ -581,6 +747,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j)
                             if (c * 32 + j >= valid) r[c][j] = __float_as_uint(-INFINITY);
                 }
+#ifdef VISTA_SPEC_MAX
+                // Speculative offset: past an item's first tile the exponentials run with the running
+                // offset m_used while the row max is computed alongside (independent instructions the
+                // scheduler interleaves with the MUFU ops, so the max leaves the critical path).  Only
+                // when a row max exceeds m_used + 8 (p > 2^8, rare once the first tiles have set the
+                // offset) are they redone with the new offset, before any P is stored.
+                if (g >= 2) {
+                    if (row == 0 && ch == 0) {
+                        VTRACE(27, g);
+                        VPROBE(1, g, &bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
+                    }
+                    ptx::mbar_wait(&bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
+                }
+                if (row == 0 && ch == 0) VTRACE(14, g);
+                uint32_t pk[2][16];
+                float lt = 0.f;
+                const bool spec = t > it.t0;
+                if (spec) lt = exp_regs(r, sl2, -m_used, pk);
+                const float mxs = row_max(r) * sl2;
+                if (row == 0 && ch == 0) VTRACE(13, g);
+                const bool need = mxs > m_used + kRescaleThreshold;
+                const bool any = __any_sync(0xffffffffu, need);
+                const float m_old = m_used;
+                if (any) {
+                    m_used = fmaxf(m_used, mxs);
+                    lt = exp_regs(r, sl2, -m_used, pk);
+                }
+                ptx::tc_fence_after();
+                if (lane == 0 && wq == 0) VTRACE(22 + 2 * rh, g);
+                ptx::tmem_st16x32bx2_x16<32>(tP, pk[0]);
+                ptx::tmem_st16x32bx2_x16<32>(tP + 16, pk[1]);
+                if (lane == 0 && wq == 0) VTRACE(23 + 2 * rh, g);
+#else
                 // row max: 4 independent FMNMX3 chains over this thread's keys, then the row's other thread
                 float m4[4];
 #pragma unroll
@@ -602,12 +801,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float m_old = m_used;
                 if (any) m_used = fmaxf(m_used, mxs);
                 // P buffer b is free once PV(g - 2) has read it
+                if (row == 0 && ch == 0 && g >= 2) {
+                    VTRACE(27, g);
+                    VPROBE(1, g, &bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
+                }
                 if (g >= 2) ptx::mbar_wait(&bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
                 if (row == 0 && ch == 0) VTRACE(14, g);
                 ptx::tc_fence_after();
                 if (lane == 0 && wq == 0) VTRACE(22 + 2 * rh, g);
                 const float lt = exp_half(r, sl2, -m_used, tP);
                 if (lane == 0 && wq == 0) VTRACE(23 + 2 * rh, g);
+#endif
                 if (any && t > it.t0) {
                     // O holds this item's sum up to PV(g - 1): wait for it, then rescale this row's
                     // 128 columns in place, 64 per thread (PV(g) cannot start before the p_full arrive)
@@ -630,7 +834,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l += lt;
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&bars->p_full[b]);
+                if constexpr (PAIR) warp_arrive_leader(&bars->p_full[b], rank);
+                else ptx::mbar_arrive(&bars->p_full[b]);
                 if (row == 0 && ch == 0) VTRACE(4, g);
             }
             // the row's sum (both threads) and running max to the epilogue (single buffer: wait until
@@ -707,7 +912,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             store_lse(P, it, cid, urow, lse, kRows);
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&bars->o_empty);
+            if constexpr (PAIR) warp_arrive_leader(&bars->o_empty, rank);
+            else ptx::mbar_arrive(&bars->o_empty);
             if (row == 0) VTRACE(19, k);
         }
     }
@@ -720,7 +926,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         g_vista_cta[blockIdx.x][3] = clock64();
     }
 #endif
-    if (warp == 1) ptx::tmem_dealloc(tmem, kTmemCols);
+    if (warp == 1) {
+        if constexpr (PAIR) ptx::tmem_dealloc2(tmem, kTmemCols);
+        else ptx::tmem_dealloc(tmem, kTmemCols);
+    }
 }
 
 }  // namespace
@@ -752,24 +961,33 @@ static cudaLaunchConfig_t cluster_config(dim3 grid, cudaStream_t stream, cudaLau
     return cfg;
 }
 
+// CTA-pair mode (cta_group::2) for clusters of two (S = 256 per unit): VISTA_SOFTMAX_PAIR=1 selects it
+// instead of the multicast kernel.  Parity-green, but measured 4% slower at c2, so
+// it is off by default.
+static bool use_pair() {
+    static const int v = [] {
+        const char* e = getenv("VISTA_SOFTMAX_PAIR");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 // Persistent grid: the number of clusters of C CTAs that can be co-resident on this device.
-template <int C>
+template <int C, bool PAIR>
 static int max_clusters(int num_sms) {
     if (C == 1) return num_sms;
     static int cache[64] = {0};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
     if (!cache[dev]) {
-        if (set_smem_attr(reinterpret_cast<const void*>(sm100_softmax_kernel<C>), kSmem) != cudaSuccess)
+        const void* fn = reinterpret_cast<const void*>(sm100_softmax_kernel<C, PAIR>);
+        if (set_smem_attr(fn, kSmem) != cudaSuccess)
             return num_sms / C;  // no device (host-only sizing): the upper bound
         cudaLaunchAttribute attrs[2];
         cudaLaunchConfig_t cfg = cluster_config<C>(dim3(C * (num_sms / C)), nullptr, attrs);
         cfg.numAttrs = 1;  // cluster dimension only
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(sm100_softmax_kernel<C>), &cfg) !=
-                cudaSuccess ||
-            n <= 0)
-            n = num_sms / C;
+        if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n <= 0) n = num_sms / C;
         cache[dev] = std::min(n, num_sms / C);
     }
     return cache[dev];
@@ -777,17 +995,21 @@ static int max_clusters(int num_sms) {
 
 int sm100_softmax_num_clusters(const Problem& p) {
     switch (sm100_softmax_cluster(p.S)) {
-        case 8: return max_clusters<8>(p.num_sms);
-        case 4: return max_clusters<4>(p.num_sms);
-        case 2: return max_clusters<2>(p.num_sms);
-        default: return max_clusters<1>(p.num_sms);
+        case 8: return max_clusters<8, false>(p.num_sms);
+        case 4: return max_clusters<4, false>(p.num_sms);
+        case 2: return use_pair() ? max_clusters<2, true>(p.num_sms) : max_clusters<2, false>(p.num_sms);
+        default: return max_clusters<1, false>(p.num_sms);
     }
 }
 
-template <int C>
+template <int C, bool PAIR>
 static cudaError_t launch_c(const Problem& p, const Workspace& w, char* ws) {
     CUtensorMap mq, mk, mv;
-    if (!make_q_map(&mq, p.q, p.S, p.H, p.B, p.q_user_stride) || !make_kv_map_rows(&mk, p.k, p.total_len, p.H, 128 / C) || !make_kv_map_rows(&mv, p.v, p.total_len, p.H, 128 / C))
+    // K / V boxes: the rows one CTA loads per tile (pair: 64 keys of K, all 128 keys of V for its
+    // 64 channels; multicast: 128 / C rows of each)
+    const int krows = PAIR ? 64 : 128 / C, vrows = PAIR ? 128 : 128 / C;
+    if (!make_q_map(&mq, p.q, p.S, p.H, p.B, p.q_user_stride) || !make_kv_map_rows(&mk, p.k, p.total_len, p.H, krows) ||
+        !make_kv_map_rows(&mv, p.v, p.total_len, p.H, vrows))
         return cudaErrorInvalidValue;
     Params P;
     P.offsets = p.offsets;
@@ -804,7 +1026,7 @@ static cudaError_t launch_c(const Problem& p, const Workspace& w, char* ws) {
     P.q_per_user = p.q_user_stride != 0;
     P.out_v8 = (reinterpret_cast<uintptr_t>(p.outs.out) & 31) == 0;
     P.slot_v8 = (reinterpret_cast<uintptr_t>(P.slot_o) & 31) == 0;
-    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_softmax_kernel<C>), kSmem);
+    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_softmax_kernel<C, PAIR>), kSmem);
     if (attr != cudaSuccess) return attr;
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = cluster_config<C>(dim3(C * w.num_ctas), p.stream, attrs);
@@ -812,7 +1034,7 @@ static cudaError_t launch_c(const Problem& p, const Workspace& w, char* ws) {
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
 #endif
-    return cudaLaunchKernelEx(&cfg, sm100_softmax_kernel<C>, mq, mk, mv, P);
+    return cudaLaunchKernelEx(&cfg, sm100_softmax_kernel<C, PAIR>, mq, mk, mv, P);
 }
 
 #ifdef VISTA_TRACE
@@ -823,16 +1045,19 @@ extern "C" int vista_debug_trace(void* host, size_t bytes) {
 
 cudaError_t launch_sm100_softmax(const Problem& p, const Workspace& w, char* ws) {
     switch (sm100_softmax_cluster(p.S)) {
-        case 8: return launch_c<8>(p, w, ws);
-        case 4: return launch_c<4>(p, w, ws);
-        case 2: return launch_c<2>(p, w, ws);
-        default: return launch_c<1>(p, w, ws);
+        case 8: return launch_c<8, false>(p, w, ws);
+        case 4: return launch_c<4, false>(p, w, ws);
+        case 2: return use_pair() ? launch_c<2, true>(p, w, ws) : launch_c<2, false>(p, w, ws);
+        default: return launch_c<1, false>(p, w, ws);
     }
 }
 
 }  // namespace vista
 
 #ifdef VISTA_TRACE
+extern "C" int vista_debug_probe(void* host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, vista::g_vista_probe, bytes < sizeof(vista::g_vista_probe) ? bytes : sizeof(vista::g_vista_probe));
+}
 extern "C" int vista_debug_cta_times(void* host, size_t bytes) {
     return (int)cudaMemcpyFromSymbol(host, vista::g_vista_cta, bytes < sizeof(vista::g_vista_cta) ? bytes : sizeof(vista::g_vista_cta));
 }

@@ -51,6 +51,17 @@ print("median V request -> PV got V:", int(np.median(rel[10, 8:48] - rel[6, 8:48
 print("softmax phases: got_S->loaded", int(np.median(rel[12, 8:48] - rel[3, 8:48])), " loaded->max exchanged",
       int(np.median(rel[13, 8:48] - rel[12, 8:48])), " ->p_free", int(np.median(rel[14, 8:48] - rel[13, 8:48])),
       " ->exps done", int(np.median(rel[15, 8:48] - rel[14, 8:48])), " ->arrived", int(np.median(rel[4, 8:48] - rel[15, 8:48])))
+pr = np.zeros((2, 64), dtype=np.int32)
+if hasattr(lib, "vista_debug_probe"):
+    lib.vista_debug_probe.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    lib.vista_debug_probe(pr.ctypes.data, pr.nbytes)
+    ws = rel[3, 8:48] - rel[26, 8:48]
+    wp = rel[14, 8:48] - rel[27, 8:48]
+    print("s_full: ready at first probe", int(pr[0, 8:48].sum()), "/ 40; wait (probe -> passed) median",
+          int(np.median(ws)), "ready-only median", int(np.median(ws[pr[0, 8:48] == 1])) if pr[0, 8:48].any() else None)
+    print("p_free: ready at first probe", int(pr[1, 8:48].sum()), "/ 40; wait median", int(np.median(wp)),
+          "ready-only median", int(np.median(wp[pr[1, 8:48] == 1])) if pr[1, 8:48].any() else None)
+    print("arrive(g-1) -> s_full probe(g):", int(np.median(rel[26, 9:48] - rel[4, 8:47])))
 print("items (k: producer Q issued, S got Q, PV got O free, epi got ml, epi got O, epi done):")
 for k in range(6):
     print(k, [int(rel[e, k]) for e in (17, 16, 18, 20, 21, 19)])

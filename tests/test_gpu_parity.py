@@ -3,6 +3,8 @@ inputs.  Gate (reading R14): per (user, head) block
     max|gpu - oracle| / max|oracle| <= 2e-2 (bf16 inputs) or 1e-4 (f32 inputs)
 and |lse_gpu - lse_oracle| <= 1e-3 (bf16) / 1e-5 (f32), natural log.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -1115,3 +1117,21 @@ def test_summarize_layers(cuda_lib, lens, S, H, n_layers):
             c = slice(h * d, (h + 1) * d)
             assert block_err(g[a:b, c], ref[a:b, c]) <= 2e-2, f"user {u} head {h}"
             assert block_err(tok[u, :, h].cpu().numpy(), ref[a:a + S, c]) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_softmax_cta_pair_mode(cuda_lib):
+    """The cta_group::2 variant of the softmax kernel (VISTA_SOFTMAX_PAIR=1, off by default; the
+    switch is read once per process, so it runs in a child process): the S = 256 parity cases
+    (jagged edges, peaky / category inputs, stream-K splits, c2 at full size, large-logit shift)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, VISTA_SOFTMAX_PAIR="1")
+    sel = ("test_softmax_tcgen05_jagged_edges and 256 or test_softmax_tcgen05_peaky or "
+           "test_softmax_many_users_split or test_softmax_c2_full_size or test_softmax_key_shift or "
+           "test_softmax_duplication or test_int8_export_fused_equals_separate and 256-2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                        os.path.abspath(__file__), "-k", sel], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout

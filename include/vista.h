@@ -263,8 +263,8 @@ vista_status_t vista_summarize_bwd_qla_saved(const vista_desc_t* desc, const voi
  * segment are the seed rows), width D = H d.  Each layer, on tcgen05:
  *   [Q | K | V | G] = X [Wq | Wk | Wv | Wg]^T                       (one GEMM, four outputs)
  *   Z_uh = sum_{rows j of u} phi1(K_jh)^T V_jh;  O_rh = phi1(Q_rh) phi2(Z_uh / N_u), N_u = S + L_u
- *   X <- X + (O (.) sigmoid(G)) Wo^T                                (gate fused into the GEMM's load
- *                                                                     path, residual into its epilogue)
+ *   X <- X + (O (.) sigmoid(G)) Wo^T                                (gate fused into the QLA rows
+ *                                                                     epilogue, residual into the GEMM's)
  * The summary tokens are the first S rows of every user after the layers.
  * desc: B, S, H, d = 128, in_dtype VISTA_BF16, attn VISTA_QLA (phi1, phi2, qla_normalize), shared
  *   seeds (q_user_stride = 0); out_dtype is the dtype of tokens.

@@ -72,7 +72,10 @@ constexpr float kLn2 = 0.6931471805599453f;
 #ifndef VISTA_KSTAGES
 #define VISTA_KSTAGES 3
 #endif
-constexpr int kKStages = VISTA_KSTAGES, kVStages = 5 - VISTA_KSTAGES;
+#ifndef VISTA_VSTAGES
+#define VISTA_VSTAGES (5 - VISTA_KSTAGES)
+#endif
+constexpr int kKStages = VISTA_KSTAGES, kVStages = VISTA_VSTAGES;
 // CTA-pair mode (cta_group::2): a stage holds this CTA's half of a tile (K: 64 keys x 128
 // channels, V: 128 keys x 64 channels), so the same 160 KB of rings hold more stages
 constexpr int kPairBytes = kTileBytes / 2;
@@ -83,10 +86,15 @@ constexpr int kQOff = 0;
 constexpr int kKOff = kQOff + kTileBytes;
 constexpr int kVOff = kKOff + kKStages * kTileBytes;
 constexpr int kPairVOff = kKOff + kPairKStages * kPairBytes;
-static_assert(kPairVOff + kPairVStages * kPairBytes == kVOff + kVStages * kTileBytes, "same ring footprint");
+constexpr int kRingsEnd = kVOff + kVStages * kTileBytes > kPairVOff + kPairVStages * kPairBytes
+                              ? kVOff + kVStages * kTileBytes
+                              : kPairVOff + kPairVStages * kPairBytes;
 constexpr int kThreads = 512;
 constexpr int kTmemCols = 512;
-constexpr int kItemRing = 16;
+#ifndef VISTA_ITEM_RING
+#define VISTA_ITEM_RING 16
+#endif
+constexpr int kItemRing = VISTA_ITEM_RING;
 constexpr int kRingConsumers = 15;  // warps 1, 2, 3 and the 12 softmax / epilogue warps
 #ifndef VISTA_CTL_REGS
 #define VISTA_CTL_REGS 96
@@ -115,7 +123,7 @@ struct Bars {
     uint32_t pad;
     float ml[2][128];  // [l | m][row], the item's row statistics for the epilogue
 };
-constexpr int kBarOff = kVOff + kVStages * kTileBytes;
+constexpr int kBarOff = kRingsEnd;
 constexpr int kRingOff = kBarOff + (int)((sizeof(Bars) + 15) & ~size_t(15));
 constexpr int kSmemUsed = kRingOff + kItemRing * (int)sizeof(ItemEntry);
 constexpr int kSmem = kSmemUsed + 1024;  // + alignment slack of the dynamic smem base
@@ -291,7 +299,11 @@ __device__ __forceinline__ float exp_half(const uint32_t (&r)[2][32], float sl2,
                 ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
             float x0, x1;
             ptx::f2_unpack(x2, x0, x1);
+#ifdef VISTA_FAKE_EXP  // timing experiment only (wrong results): the exponential off the MUFU pipe
+            const uint64_t p2 = ptx::f2_fma(x2, sl2x2, sl2x2);
+#else
             const uint64_t p2 = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+#endif
             acc[j & 1] = ptx::f2_add(acc[j & 1], p2);
             float p0, p1;
             ptx::f2_unpack(p2, p0, p1);

@@ -12,9 +12,19 @@
 // sm100_target_attend_kernel (bf16, d = 128, S in {128, 256}): persistent, stream-K over the flat
 // 128-candidate tiles of the candidates' jagged layout (work.cuh).  Per item (user, head) the S x 128
 // tokens are dequantized once into shared memory (bf16, 128-B swizzle) and serve as the B operand of
-// both GEMMs: K-major for S = Q T^T, MN-major for O = P T.  Per tile: TMA of the q, k_self, v_self
-// rows; S on tcgen05 into TMEM; row softmax (one thread per candidate row, the self logit from shared
-// memory) writing P (bf16) over the S columns; O on tcgen05 (P from TMEM); epilogue adds the self term.
+// both GEMMs: K-major for S = Q T^T, MN-major for O = P T.  Warp-specialized and pipelined across
+// tiles (round 2; the first version ran every tile's load, GEMMs, softmax and stores back to back):
+//   warp 0       TMA: q and k_self tiles (2-stage ring)
+//   warp 1       MMA: S(t) = Q T^T into TMEM, then O(t) = P(t) T once the softmax wrote P(t)
+//   warps 4-11   softmax, two threads per candidate row (tokens [0, S/2) / [S/2, S), the 16x32bx2
+//                TMEM shape): the self logit q_c . k_c from the staged tiles, a two-pass softmax over
+//                [tokens; self] writing P (bf16) over each thread's own S columns
+//   warps 12-15  epilogue of tile t - 1 while the softmax works on tile t: (O + p_self v_c) / l
+//                [+ resid], bf16 / f32 rows, lse; each thread reads its own v_c row (256 contiguous
+//                bytes) from global memory ahead of the PV completion
+// The jagged tables (tile starts, candidate offsets) are staged in shared memory at the start (one
+// coalesced load instead of a chain of dependent global loads in every role's item walk).
+//   warps 4-11   also dequantize the next item's tokens once its predecessor's last PV has completed
 // simt_target_attend_kernel: CUDA cores, one warp per (candidate, head), any S >= 1, d <= 128, f32 or
 // bf16 -- the shapes the tcgen05 kernel does not take.
 #include <cuda.h>
@@ -29,17 +39,39 @@ namespace vista {
 
 bool make_kv_map(CUtensorMap* map, const void* base, int64_t total_len, int H);
 
+#ifdef VISTA_TRACE  // debug timeline of CTA 0: clock64 per (event, tile)
+__device__ unsigned long long g_ta_trace[16][64];
+#define TTRACE(ev, g) \
+    do { if (blockIdx.x == 0 && (g) < 64) g_ta_trace[ev][g] = clock64(); } while (0)
+#else
+#define TTRACE(ev, g) do { } while (0)
+#endif
+
 namespace {
 
 constexpr int kHalf = 128 * 128;  // one 64-column half of a 128-row bf16 tile
 constexpr int kTileB = 2 * kHalf;  // 32 KB
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-// smem: q, k_self, v_self tiles (96 KB), tokens T (S x 128 bf16, <= 64 KB), barriers
-constexpr int kQOff = 0, kKOff = kTileB, kVOff = 2 * kTileB, kTOff = 3 * kTileB;
-constexpr int kBarOff = kTOff + 2 * kTileB;
-constexpr int kSmem = kBarOff + 64 + 1024;
+// smem: tokens T (S x 128 bf16, two 64-column halves; 64 KB at S = 256), a 2-stage ring of (q, k_self)
+// tiles (128 KB), barriers, the per-row statistics and the jagged tables
+constexpr int kTOff = 0;
+constexpr int kQKOff = 2 * kTileB;  // stage s: q at kQKOff + 2 s kTileB, k_self at + kTileB
+constexpr int kBarOff = kQKOff + 4 * kTileB;
+constexpr int kMaxTableUsers = 1024;  // B + 1 entries of uts and row_offsets staged in smem when B < this
+
+struct TABars {
+    uint64_t qk_full[2], qk_empty[2];
+    uint64_t t_full, t_free;              // the item's tokens in smem / its last PV done (T reusable)
+    uint64_t s_full, p_full, o_full[2], o_empty[2];  // O double-buffered: the epilogue is off the chain
+    uint64_t ml_full[2], ml_empty[2];
+    uint32_t tmem_base, pad;
+    float st[2][3][128];  // per tile parity and row: 1 / l, p_self / l, lse (softmax -> epilogue)
+    int64_t uts[kMaxTableUsers], roff[kMaxTableUsers];
+};
+constexpr int kSmem = kBarOff + (int)sizeof(TABars) + 1024;
+static_assert(kSmem <= 232448, "shared memory");
 
 struct TAParams {
     const int64_t* row_offsets;
@@ -47,6 +79,7 @@ struct TAParams {
     const int8_t* codes;  // [B, S, H, 128]
     const float* tscale;  // [B, S, H]
     const float* tzp;
+    const void* v;      // v_self [R, H, 128] bf16
     const void* resid;  // [R, H, 128] (in dtype bf16) or NULL
     void* out;          // [R, H, 128]
     float* lse;         // [R, H] or NULL
@@ -79,9 +112,12 @@ template <int NS>
 __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t sT) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM) x T (MN-major)
     constexpr int halfT = NS * 128;
+    // P of tokens [0, NS/2) sits in S columns [0, NS/4), of tokens [NS/2, NS) in [NS/2, 3 NS/4): each
+    // softmax thread overwrites only S columns it has already read itself
 #pragma unroll
     for (int kk = 0; kk < NS / 16; ++kk)
-        ptx::mma_ts_w(tO, tP + kk * 8, ptx::sdesc_sw128(sT + kk * 2048, halfT, 1024), id, kk > 0);
+        ptx::mma_ts_w(tO, tP + (kk / (NS / 32)) * (NS / 2) + (kk % (NS / 32)) * 8,
+                      ptx::sdesc_sw128(sT + kk * 2048, halfT, 1024), id, kk > 0);
 }
 
 template <int NS>
@@ -91,196 +127,306 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t base = ptx::smem_u32(smem);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kBarOff);  // 0 tiles full, 1 S done, 2 P ready, 3 O done
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kBarOff + 32);
+    TABars* bars = reinterpret_cast<TABars*>(smem + kBarOff);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) TTRACE(14, 0);
     if (threadIdx.x == 0) {
-        ptx::mbar_init(&bar[0], 1);
-        ptx::mbar_init(&bar[1], 1);
-        ptx::mbar_init(&bar[2], 128);
-        ptx::mbar_init(&bar[3], 1);
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&bars->qk_full[s], 1);
+            ptx::mbar_init(&bars->qk_empty[s], 256);  // the softmax threads: self dot done, S(t) done
+        }
+        ptx::mbar_init(&bars->t_full, 256);   // warps 4-11 dequantized their share
+        ptx::mbar_init(&bars->t_free, 1);
+        ptx::mbar_init(&bars->s_full, 1);
+        ptx::mbar_init(&bars->p_full, 256);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bars->o_full[b], 1);
+            ptx::mbar_init(&bars->o_empty[b], 128);
+            ptx::mbar_init(&bars->ml_full[b], 256);
+            ptx::mbar_init(&bars->ml_empty[b], 128);
+        }
         ptx::fence_mbar_init();
     }
-    if (warp == 4) ptx::tmem_alloc(tmem_slot, 512);
+    if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
+    const bool staged = P.B < kMaxTableUsers;
+    if (staged)
+        for (int i = threadIdx.x; i <= P.B; i += kThreads) {
+            bars->uts[i] = __ldg(P.uts + i);
+            bars->roff[i] = __ldg(P.row_offsets + i);
+        }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tO = tmem + 256;  // S (and P over its first NS/2 columns) | O
+    const uint32_t tmem = bars->tmem_base;
+    const int64_t* uts = staged ? bars->uts : P.uts;
+    const int64_t* roff = staged ? bars->roff : P.row_offsets;
+    // TMEM: S (P over part of it) in [0, NS), O(t) in [NS + 128 (t % 2), NS + 128 (t % 2) + 128)
+    const uint32_t tS = tmem, tO0 = tmem + NS;
     const int H = P.H;
-    const size_t rstride = (size_t)H * 128;
-    uint32_t ph = 0;  // phase of the per-tile barriers (each completes once per tile)
     ItemIter iter;
-    iter.init(P.uts, P.B, H, blockIdx.x, gridDim.x);
+    iter.init(uts, P.B, H, blockIdx.x, gridDim.x);
     Item it;
-    while (iter.next(it, P.uts, P.B, H)) {
-        const int u = it.u, h = it.hg;
-        // ---- tokens of (u, h): int8 codes * scale + zero point -> bf16, swizzled, both halves
-        for (int x = threadIdx.x; x < NS * 8; x += kThreads) {  // x = (token i, 16-B chunk of codes)
-            const int i = x >> 3, cc = x & 7;                    // codes [16 cc, 16 cc + 16) of token i
-            const size_t tix = ((size_t)u * NS + i) * H + h;
-            const float a = __ldg(P.tscale + tix), b = __ldg(P.tzp + tix);
-            const uint4 raw = __ldg(reinterpret_cast<const uint4*>(P.codes + tix * 128) + cc);
-            const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-            uint32_t o[8];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int32_t v = (int32_t)w[e];
-                const float f0 = (float)(int8_t)(v & 0xFF), f1 = (float)(int8_t)((v >> 8) & 0xFF);
-                const float f2 = (float)(int8_t)((v >> 16) & 0xFF), f3 = (float)(v >> 24);
-                o[2 * e] = ptx::pack_bf16x2(fmaf(f0, a, b), fmaf(f1, a, b));
-                o[2 * e + 1] = ptx::pack_bf16x2(fmaf(f2, a, b), fmaf(f3, a, b));
-            }
-            // channels 16 cc .. 16 cc + 15 = 16-B bf16 chunks 2 cc, 2 cc + 1 of the row (half = cc / 4)
-            const uint32_t hb = base + kTOff + (cc >> 2) * (NS * 128);
-            const int c0 = (2 * cc) & 7;
-            sts128(hb + swz(i, c0), make_uint4(o[0], o[1], o[2], o[3]));
-            sts128(hb + swz(i, c0 + 1), make_uint4(o[4], o[5], o[6], o[7]));
-        }
-        ptx::fence_proxy_async_smem();
-        __syncthreads();
-        const int64_t R = P.row_offsets[u + 1] - P.row_offsets[u];
-        for (int t = it.t0; t < it.t1; ++t) {
-            const int64_t row0 = P.row_offsets[u] + (int64_t)t * 128;
-            const int64_t remr = R - (int64_t)t * 128;
-            const int valid = remr < 128 ? (int)remr : 128;
-            if (warp == 0) {
-                ptx::mbar_arrive_expect_tx_w(&bar[0], 3 * kTileB);
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        const uint64_t pol = ptx::policy_evict_first();
+        int g = 0;
+        while (iter.next(it, uts, P.B, H)) {
+            const int h = it.hg;
+            for (int t = it.t0; t < it.t1; ++t, ++g) {
+                const int32_t row0 = (int32_t)(roff[it.u] + (int64_t)t * 128);
+                const int st = g & 1;
+                if (g >= 2) ptx::mbar_wait(&bars->qk_empty[st], (uint32_t)((g >> 1) - 1) & 1u);
+                if (lane == 0) TTRACE(0, g);
+                ptx::mbar_arrive_expect_tx_w(&bars->qk_full[st], 2 * kTileB);
+                uint8_t* sq = smem + kQKOff + st * 2 * kTileB;
                 for (int half = 0; half < 2; ++half) {
-                    ptx::tma_load_3d_w(smem + kQOff + half * kHalf, &mapQ, &bar[0], half * 64, h, (int32_t)row0,
-                                       ptx::policy_evict_first());
-                    ptx::tma_load_3d_w(smem + kKOff + half * kHalf, &mapK, &bar[0], half * 64, h, (int32_t)row0,
-                                       ptx::policy_evict_first());
-                    ptx::tma_load_3d_w(smem + kVOff + half * kHalf, &mapV, &bar[0], half * 64, h, (int32_t)row0,
-                                       ptx::policy_evict_first());
+                    ptx::tma_load_3d_w(sq + half * kHalf, &mapQ, &bars->qk_full[st], half * 64, h, row0, pol);
+                    ptx::tma_load_3d_w(sq + kTileB + half * kHalf, &mapK, &bars->qk_full[st], half * 64, h, row0, pol);
                 }
             }
-            ptx::mbar_wait(&bar[0], ph);
-            if (warp == 4) {
+        }
+    } else if (warp == 1) {
+        // ============================ MMA issuer ============================
+        int g = 0;
+        for (int k = 0; iter.next(it, uts, P.B, H); ++k) {
+            ptx::mbar_wait(&bars->t_full, (uint32_t)k & 1u);
+            for (int t = it.t0; t < it.t1; ++t, ++g) {
+                const int st = g & 1;
+                ptx::mbar_wait(&bars->qk_full[st], (uint32_t)(g >> 1) & 1u);
+                if (lane == 0) TTRACE(1, g);
+                // S(g) overwrites the P columns PV(g - 1) read: wait for its completion
+                if (g >= 1) ptx::mbar_wait(&bars->o_full[(g - 1) & 1], (uint32_t)((g - 1) >> 1) & 1u);
                 ptx::tc_fence_after();
-                issue_scores<NS>(tS, base + kQOff, base + kTOff);
-                ptx::mma_commit_w(&bar[1]);
+                issue_scores<NS>(tS, base + kQKOff + st * 2 * kTileB, base + kTOff);
+                ptx::mma_commit_w(&bars->s_full);
+                if (lane == 0) TTRACE(2, g);
+                ptx::mbar_wait(&bars->p_full, (uint32_t)g & 1u);
+                if (lane == 0) TTRACE(3, g);
+                // O buffer g % 2: the epilogue has read O(g - 2)
+                if (g >= 2) ptx::mbar_wait(&bars->o_empty[g & 1], (uint32_t)((g >> 1) - 1) & 1u);
+                ptx::tc_fence_after();
+                issue_pv<NS>(tO0 + (g & 1) * 128, tS, base + kTOff);
+                if (lane == 0) TTRACE(4, g);
+                ptx::mma_commit_w(&bars->o_full[g & 1]);
+                if (t == it.t1 - 1) ptx::mma_commit_w(&bars->t_free);
             }
-            if (warp < 4) {
-                // ---- softmax over [tokens; self], one thread per candidate row (= TMEM lane)
-                const int row = warp * 32 + lane;
-                const uint32_t lb = (uint32_t)(warp * 32) << 16;
-                float self = 0.f;  // q_c . k_c from the staged tiles
+        }
+    } else if (warp >= 4) {
+        const bool smx = warp < 12;
+        // softmax: lane quarter wq, row half rh, token half ch; epilogue: one thread per row
+        const int wq = warp & 3, rh = (warp - 4) >> 2, ch = lane >> 4;
+        const int row = smx ? wq * 32 + rh * 16 + (lane & 15) : wq * 32 + lane;  // candidate row = TMEM lane
+        const uint32_t lb = (uint32_t)(smx ? wq * 32 + rh * 16 : wq * 32) << 16;
+        const size_t rstride = (size_t)H * 128;
+        int g = 0;
+        for (int k = 0; iter.next(it, uts, P.B, H); ++k) {
+            const int u = it.u, h = it.hg;
+            // ---- the item's tokens: int8 codes * scale + zero point -> bf16, swizzled, both halves
+            //      (the softmax warps 4-11)
+            if (threadIdx.x == 128) TTRACE(12, k);
+            if (smx) {
+                // every thread's NS / 32 chunks: all loads first (in flight together), then convert
+                constexpr int kPer = NS * 8 / 256;
+                uint4 raw[kPer];
+                float a[kPer], b[kPer];
 #pragma unroll
-                for (int half = 0; half < 2; ++half)
+                for (int n = 0; n < kPer; ++n) {
+                    const int x = threadIdx.x - 128 + 256 * n;  // x = (token i, 16-B chunk cc of its codes)
+                    const size_t tix = ((size_t)u * NS + (x >> 3)) * H + h;
+                    raw[n] = __ldg(reinterpret_cast<const uint4*>(P.codes + tix * 128) + (x & 7));
+                    a[n] = __ldg(P.tscale + tix);
+                    b[n] = __ldg(P.tzp + tix);
+                }
+                // the loads overlap the previous item's last PV; T is rewritten only after it
+                if (k >= 1) ptx::mbar_wait(&bars->t_free, (uint32_t)(k - 1) & 1u);
+#pragma unroll
+                for (int n = 0; n < kPer; ++n) {
+                    const int x = threadIdx.x - 128 + 256 * n;
+                    const int i = x >> 3, cc = x & 7;  // codes [16 cc, 16 cc + 16) of token i
+                    const uint32_t w[4] = {raw[n].x, raw[n].y, raw[n].z, raw[n].w};
+                    uint32_t o[8];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int32_t v = (int32_t)w[e];
+                        const float f0 = (float)(int8_t)(v & 0xFF), f1 = (float)(int8_t)((v >> 8) & 0xFF);
+                        const float f2 = (float)(int8_t)((v >> 16) & 0xFF), f3 = (float)(v >> 24);
+                        o[2 * e] = ptx::pack_bf16x2(fmaf(f0, a[n], b[n]), fmaf(f1, a[n], b[n]));
+                        o[2 * e + 1] = ptx::pack_bf16x2(fmaf(f2, a[n], b[n]), fmaf(f3, a[n], b[n]));
+                    }
+                    // channels 16 cc .. 16 cc + 15 = 16-B bf16 chunks 2 cc, 2 cc + 1 of the row (half = cc / 4)
+                    const uint32_t hb = base + kTOff + (cc >> 2) * (NS * 128);
+                    const int c0 = (2 * cc) & 7;
+                    sts128(hb + swz(i, c0), make_uint4(o[0], o[1], o[2], o[3]));
+                    sts128(hb + swz(i, c0 + 1), make_uint4(o[4], o[5], o[6], o[7]));
+                }
+            }
+            if (smx) {
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(&bars->t_full);
+            }
+            if (threadIdx.x == 128) TTRACE(13, k);
+            const int64_t R = roff[u + 1] - roff[u];
+            for (int t = it.t0; t < it.t1; ++t, ++g) {
+                const int st = g & 1;
+                if (smx) {
+                    // ============ softmax over [tokens; self], two threads per candidate row ============
+                    ptx::mbar_wait(&bars->qk_full[st], (uint32_t)(g >> 1) & 1u);
+                    if (threadIdx.x == 128) TTRACE(5, g);
+                    const uint32_t sq = base + kQKOff + st * 2 * kTileB;
+                    float self = 0.f;  // q_c . k_c from the staged tiles: this thread's 64 channels
 #pragma unroll 4
                     for (int c = 0; c < 8; ++c) {
-                        const uint4 qa = lds128(base + kQOff + half * kHalf + swz(row, c));
-                        const uint4 ka = lds128(base + kKOff + half * kHalf + swz(row, c));
+                        const uint4 qa = lds128(sq + ch * kHalf + swz(row, c));
+                        const uint4 ka = lds128(sq + kTileB + ch * kHalf + swz(row, c));
                         const uint32_t qw[4] = {qa.x, qa.y, qa.z, qa.w}, kw[4] = {ka.x, ka.y, ka.z, ka.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             self = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(kw[e] << 16), self);
-                            self = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(kw[e] & 0xFFFF0000u), self);
+                            self = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(kw[e] & 0xFFFF0000u),
+                                        self);
                         }
                     }
-                self *= P.scale_log2;
-                ptx::mbar_wait(&bar[1], ph);
-                ptx::tc_fence_after();
-                float m = self;
+                    self += __shfl_xor_sync(0xffffffffu, self, 16);
+                    self *= P.scale_log2;
+                    ptx::mbar_wait(&bars->s_full, (uint32_t)g & 1u);
+                    if (threadIdx.x == 128) TTRACE(6, g);
+                    ptx::mbar_arrive(&bars->qk_empty[st]);  // q (S done) and k (dot done) of this stage read
+                    ptx::tc_fence_after();
+                    // this thread: tokens [ch NS/2, ch NS/2 + NS/2) = S columns of the same range
+                    float m = self;
 #pragma unroll 1
-                for (int c = 0; c < NS / 32; ++c) {
-                    uint32_t r[32];
-                    ptx::tmem_ld32_sync(tS + lb + c * 32, r);
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]) * P.scale_log2);
-                }
-                float l = 0.f;
-#pragma unroll 1
-                for (int c = 0; c < NS / 32; ++c) {
-                    uint32_t r[32], pk[16];
-                    ptx::tmem_ld32_sync(tS + lb + c * 32, r);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const float p0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), P.scale_log2, -m));
-                        const float p1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), P.scale_log2, -m));
-                        l += p0 + p1;
-                        pk[j] = ptx::pack_bf16x2(p0, p1);
-                    }
-                    ptx::tmem_st16(tS + lb + c * 16, pk);  // P over the first NS / 2 S columns (already read)
-                }
-                const float pself = ptx::ex2(self - m);
-                l += pself;
-                ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&bar[2]);
-                // ---- epilogue: (O + p_self v_c) / l [+ resid]
-                ptx::mbar_wait(&bar[3], ph);
-                ptx::tc_fence_after();
-                const float inv = 1.f / l;
-#pragma unroll 1
-                for (int half = 0; half < 2; ++half) {
-                    float o[64];
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
+                    for (int c = 0; c < NS / 2; c += 32) {
                         uint32_t r[32];
-                        ptx::tmem_ld32_sync(tO + lb + half * 64 + c * 32, r);
+                        ptx::tmem_ld16x32bx2_x32<NS / 2>(tS + lb + c, r);
+                        ptx::tmem_wait_ld();
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) o[32 * c + j] = __uint_as_float(r[j]);
+                        for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]) * P.scale_log2);
                     }
+                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+                    if (threadIdx.x == 128) TTRACE(7, g);
+                    float l = 0.f;
+#pragma unroll 1
+                    for (int c = 0; c < NS / 2; c += 32) {
+                        uint32_t r[32], pk[16];
+                        ptx::tmem_ld16x32bx2_x32<NS / 2>(tS + lb + c, r);
+                        ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint4 va = lds128(base + kVOff + half * kHalf + swz(row, c));
-                        const uint32_t vw[4] = {va.x, va.y, va.z, va.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            o[8 * c + 2 * e] = fmaf(pself, __uint_as_float(vw[e] << 16), o[8 * c + 2 * e]) * inv;
-                            o[8 * c + 2 * e + 1] =
-                                fmaf(pself, __uint_as_float(vw[e] & 0xFFFF0000u), o[8 * c + 2 * e + 1]) * inv;
+                        for (int j = 0; j < 16; ++j) {
+                            const float p0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), P.scale_log2, -m));
+                            const float p1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), P.scale_log2, -m));
+                            l += p0 + p1;
+                            pk[j] = ptx::pack_bf16x2(p0, p1);
                         }
+                        // P of these 32 tokens: 16 columns at the start of this thread's own S range
+                        ptx::tmem_st16x32bx2_x16<NS / 2>(tS + lb + c / 2, pk);
                     }
-                    if (row < valid) {
-                        const size_t e0 = (size_t)(row0 + row) * rstride + (size_t)h * 128 + half * 64;
-                        if (P.resid) {
-                            const uint4* rs = reinterpret_cast<const uint4*>(
-                                reinterpret_cast<const __nv_bfloat16*>(P.resid) + e0);
+                    l += __shfl_xor_sync(0xffffffffu, l, 16);
+                    const float pself = ptx::ex2(self - m);
+                    l += pself;
+                    const float inv = 1.f / l;
+                    if (g >= 2) ptx::mbar_wait(&bars->ml_empty[g & 1], (uint32_t)((g >> 1) - 1) & 1u);
+                    if (ch == 0) {
+                        bars->st[g & 1][0][row] = inv;
+                        bars->st[g & 1][1][row] = pself * inv;
+                        bars->st[g & 1][2][row] = (m + __log2f(l)) * kLn2;
+                    }
+                    ptx::mbar_arrive(&bars->ml_full[g & 1]);
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars->p_full);
+                    if (threadIdx.x == 128) TTRACE(8, g);
+                } else {
+                    // ============ epilogue: (O + p_self v_c) / l [+ resid] ============
+                    const int64_t row0 = roff[u] + (int64_t)t * 128;
+                    const int64_t remr = R - (int64_t)t * 128;
+                    const int valid = remr < 128 ? (int)remr : 128;
+                    // v_c of this thread's row (clamped to the tile's last valid row), in flight
+                    // while the softmax and the PV GEMM run
+                    // (the first 64 channels now, the second 64 once the first are combined)
+                    const int vr = row < valid ? row : valid - 1;
+                    const uint4* vs = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(P.v) +
+                                                                     (size_t)(row0 + vr) * rstride + (size_t)h * 128);
+                    uint4 vh[8];
 #pragma unroll
-                            for (int c = 0; c < 8; ++c) {
-                                const uint4 ra = __ldg(rs + c);
-                                const uint32_t rw[4] = {ra.x, ra.y, ra.z, ra.w};
+                    for (int c = 0; c < 8; ++c) vh[c] = __ldg(vs + c);
+                    const int ob = g & 1;
+                    const uint32_t tO = tO0 + ob * 128;
+                    ptx::mbar_wait(&bars->ml_full[ob], (uint32_t)(g >> 1) & 1u);
+                    if (threadIdx.x == 384) TTRACE(9, g);
+                    const float inv = bars->st[ob][0][row], wself = bars->st[ob][1][row], lse = bars->st[ob][2][row];
+                    ptx::mbar_arrive(&bars->ml_empty[ob]);
+                    ptx::mbar_wait(&bars->o_full[ob], (uint32_t)(g >> 1) & 1u);
+                    if (threadIdx.x == 384) TTRACE(10, g);
+                    ptx::tc_fence_after();
+#pragma unroll 1
+                    for (int half = 0; half < 2; ++half) {
+                        float o[64];
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    o[8 * c + 2 * e] += __uint_as_float(rw[e] << 16);
-                                    o[8 * c + 2 * e + 1] += __uint_as_float(rw[e] & 0xFFFF0000u);
-                                }
+                        for (int c = 0; c < 2; ++c) {
+                            uint32_t r[32];
+                            ptx::tmem_ld32_sync(tO + lb + half * 64 + c * 32, r);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) o[32 * c + j] = __uint_as_float(r[j]);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const uint4 va = vh[c];
+                            const uint32_t vw[4] = {va.x, va.y, va.z, va.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                o[8 * c + 2 * e] = fmaf(wself, __uint_as_float(vw[e] << 16), o[8 * c + 2 * e] * inv);
+                                o[8 * c + 2 * e + 1] =
+                                    fmaf(wself, __uint_as_float(vw[e] & 0xFFFF0000u), o[8 * c + 2 * e + 1] * inv);
                             }
                         }
-                        if (P.out_bf16) {
-                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + e0);
+                        if (half == 0) {
 #pragma unroll
-                            for (int c = 0; c < 8; ++c)
-                                dst[c] = make_uint4(ptx::pack_bf16x2(o[8 * c], o[8 * c + 1]),
-                                                    ptx::pack_bf16x2(o[8 * c + 2], o[8 * c + 3]),
-                                                    ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]),
-                                                    ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7]));
-                        } else {
-                            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + e0);
+                            for (int c = 0; c < 8; ++c) vh[c] = __ldg(vs + 8 + c);
+                        }
+                        if (row < valid) {
+                            const size_t e0 = (size_t)(row0 + row) * rstride + (size_t)h * 128 + half * 64;
+                            if (P.resid) {
+                                const uint4* rs = reinterpret_cast<const uint4*>(
+                                    reinterpret_cast<const __nv_bfloat16*>(P.resid) + e0);
 #pragma unroll
-                            for (int c = 0; c < 16; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                                for (int c = 0; c < 8; ++c) {
+                                    const uint4 ra = __ldg(rs + c);
+                                    const uint32_t rw[4] = {ra.x, ra.y, ra.z, ra.w};
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        o[8 * c + 2 * e] += __uint_as_float(rw[e] << 16);
+                                        o[8 * c + 2 * e + 1] += __uint_as_float(rw[e] & 0xFFFF0000u);
+                                    }
+                                }
+                            }
+                            if (P.out_bf16) {
+                                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + e0);
+#pragma unroll
+                                for (int c = 0; c < 8; ++c)
+                                    dst[c] = make_uint4(ptx::pack_bf16x2(o[8 * c], o[8 * c + 1]),
+                                                        ptx::pack_bf16x2(o[8 * c + 2], o[8 * c + 3]),
+                                                        ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]),
+                                                        ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7]));
+                            } else {
+                                float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + e0);
+#pragma unroll
+                                for (int c = 0; c < 16; ++c)
+                                    dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                            }
                         }
                     }
+                    if (P.lse && row < valid) P.lse[(size_t)(row0 + row) * H + h] = lse;
+                    if (threadIdx.x == 384) TTRACE(11, g);
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars->o_empty[ob]);
                 }
-                if (P.lse && row < valid) P.lse[(size_t)(row0 + row) * H + h] = (m + __log2f(l)) * kLn2;
-            } else if (warp == 4) {
-                ptx::mbar_wait(&bar[2], ph);
-                ptx::tc_fence_after();
-                issue_pv<NS>(tO, tS, base + kTOff);
-                ptx::mma_commit_w(&bar[3]);
             }
-            ph ^= 1;
-            ptx::tc_fence_before();
-            __syncthreads();  // tiles, TMEM and the barriers are reused by the next tile
-            ptx::tc_fence_after();
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 4) ptx::tmem_dealloc(tmem, 512);
+    if (threadIdx.x == 0) TTRACE(15, 0);
+    if (warp == 1) ptx::tmem_dealloc(tmem, 512);
 }
 
 // ---------------------------------------------------------------- SIMT: one warp per (candidate, head)
@@ -383,6 +529,7 @@ cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offs
     P.codes = codes;
     P.tscale = tscale;
     P.tzp = tzp;
+    P.v = v_self;
     P.resid = resid;
     P.out = out;
     P.lse = lse;
@@ -399,6 +546,12 @@ cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offs
     else sm100_target_attend_kernel<128><<<p.num_sms, kThreads, kSmem, p.stream>>>(mq, mk, mv, P);
     return cudaGetLastError();
 }
+
+#ifdef VISTA_TRACE
+extern "C" int vista_debug_ta_trace(void* host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, g_ta_trace, bytes < sizeof(g_ta_trace) ? bytes : sizeof(g_ta_trace));
+}
+#endif
 
 cudaError_t launch_simt_target_attend(const Problem& p, const int64_t* row_offsets, int64_t total_rows,
                                       const int8_t* codes, const float* tscale, const float* tzp, const void* q,

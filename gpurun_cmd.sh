@@ -1,5 +1,5 @@
-mkdir -p gpurun_out/p9
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/p9/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/p9/pytest_gpu.log
-timeout 300 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-sustained --no-graph > gpurun_out/p9/c5_plain.json 2> gpurun_out/p9/c5_plain.err; echo "c5 plain exit $?"
-timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second --clock-control none -k regex:sm100_softmax_kernel -c 2 --csv --log-file gpurun_out/p9/ncu_c5_dram.csv python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-sustained --no-graph > gpurun_out/p9/ncu_c5.log 2>&1; echo "ncu exit $?"
-grep -i "dram__bytes\|duration" gpurun_out/p9/ncu_c5_dram.csv | head
+mkdir -p gpurun_out/p10
+VISTA_SOFTMAX_CMAX=2 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "softmax or c5 or int8 or partial or invariant or independence" > gpurun_out/p10/pytest_cmax2.log 2>&1; echo "pytest cmax2 exit $?"; tail -2 gpurun_out/p10/pytest_cmax2.log
+TAG=p10 VARIANTS="default prev" CFGS="c2 c5" STEPS=100 bash scripts/ab_softmax.sh
+TAG=p10 ENVS="VISTA_SOFTMAX_CMAX=2;VISTA_SOFTMAX_CMAX=8" CFGS="c5" REPS=2 bash scripts/ab_env.sh
+TAG=p10b VARIANTS="prev default" CFGS="c2" STEPS=100 bash scripts/ab_softmax.sh

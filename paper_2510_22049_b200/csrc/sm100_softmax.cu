@@ -139,6 +139,7 @@ struct Params {
     int B, S, H, G;  // G: units (groups of C*128 rows) per head
     float scale_log2;
     int q_per_user;
+    int groups;  // > 1: query-group-major work order (ItemIterG; the G groups of a unit run side by side)
     int out_v8, slot_v8;  // outputs / slots 32-B aligned: 256-bit stores
 };
 
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0 && rank == 0) {
         // record which units this cluster's partial slots will hold (read by the merge kernel)
         int s0, s1;
-        partial_slots(P.uts, P.B, HG, cid, nclusters, s0, s1);
+        partial_slots_g(P.uts, P.B, HG, cid, nclusters, s0, s1, P.groups);
         P.slot_unit[2 * cid] = s0;
         P.slot_unit[2 * cid + 1] = s1;
     }
@@ -542,8 +543,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tma_prefetch(&mapK);
             const uint64_t pol_kv = ptx::policy_evict_first();
             const uint64_t pol_q = ptx::policy_evict_last();
-            ItemIter iter;
-            iter.init(P.uts, P.B, HG, cid, nclusters);
+            // group-major order when a unit is several query groups (the groups of a (user, head)
+            // stream the same K/V tiles at the same time: the second read hits L2)
+            ItemIterG iter;
+            iter.init(P.uts, P.B, HG, cid, nclusters, P.groups);
             int stage = 0, gk = 0;
             uint32_t phase = 0;
             for (int k = 0;; ++k) {
@@ -948,10 +951,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Cluster size for S query rows: the largest power of two <= 8 dividing S / 128 (K/V slices of
 // 128 / C rows stay whole 8-row swizzle atoms).
+// VISTA_SOFTMAX_CMAX caps the cluster size (A/B: a cluster of 4 fits 132 of the 148 SMs).
+static int cluster_cap() {
+    static const int v = [] {
+        const char* e = getenv("VISTA_SOFTMAX_CMAX");
+        const int c = e ? atoi(e) : 8;
+        return (c == 1 || c == 2 || c == 4) ? c : 8;
+    }();
+    return v;
+}
 int sm100_softmax_cluster(int S) {
     const int tiles = S / 128;
+    const int cap = cluster_cap();
     int c = 1;
-    while (c < 8 && tiles % (2 * c) == 0) c *= 2;
+    while (c < cap && tiles % (2 * c) == 0) c *= 2;
     return c;
 }
 
@@ -1036,6 +1049,7 @@ static cudaError_t launch_c(const Problem& p, const Workspace& w, char* ws) {
     P.G = p.S / (C * 128);
     P.scale_log2 = p.scale * kLog2e;
     P.q_per_user = p.q_user_stride != 0;
+    P.groups = (P.G > 1 && w.num_ctas % P.G == 0) ? P.G : 1;
     P.out_v8 = (reinterpret_cast<uintptr_t>(p.outs.out) & 31) == 0;
     P.slot_v8 = (reinterpret_cast<uintptr_t>(P.slot_o) & 31) == 0;
     const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_softmax_kernel<C, PAIR>), kSmem);

@@ -12,19 +12,19 @@
 // sm100_target_attend_kernel (bf16, d = 128, S in {128, 256}): persistent, stream-K over the flat
 // 128-candidate tiles of the candidates' jagged layout (work.cuh).  Per item (user, head) the S x 128
 // tokens are dequantized once into shared memory (bf16, 128-B swizzle) and serve as the B operand of
-// both GEMMs: K-major for S = Q T^T, MN-major for O = P T.  Warp-specialized and pipelined across
-// tiles (round 2; the first version ran every tile's load, GEMMs, softmax and stores back to back):
+// both GEMMs: K-major for S = Q T^T, MN-major for O = P T.  TMEM: S [0, S), P (bf16) [256, 256 + S/2),
+// O [384, 512) -- P has its own columns, so the score GEMM of tile t + 1 runs while the softmax of
+// tile t is still exponentiating.  Warp roles:
 //   warp 0       TMA: q and k_self tiles (2-stage ring)
-//   warp 1       MMA: S(t) = Q T^T into TMEM, then O(t) = P(t) T once the softmax wrote P(t)
+//   warp 1       score GEMMs S(t) = Q_t T^T (as N = 128 halves), as soon as the softmax has read S(t-1)
+//   warp 3       PV GEMM O(t) = P(t) T once P(t) is written and the epilogue has read O(t - 1)
 //   warps 4-11   softmax, two threads per candidate row (tokens [0, S/2) / [S/2, S), the 16x32bx2
 //                TMEM shape): the self logit q_c . k_c from the staged tiles, a two-pass softmax over
-//                [tokens; self] writing P (bf16) over each thread's own S columns
-//   warps 12-15  epilogue of tile t - 1 while the softmax works on tile t: (O + p_self v_c) / l
-//                [+ resid], bf16 / f32 rows, lse; each thread reads its own v_c row (256 contiguous
-//                bytes) from global memory ahead of the PV completion
+//                [tokens; self]; also dequantize each item's tokens once its predecessor's last PV is done
+//   warps 12-15  epilogue, one thread per row: (O + p_self v_c) / l [+ resid] -> bf16 / f32 rows, lse;
+//                v_c rows prefetched from global memory; O released after its last TMEM load
 // The jagged tables (tile starts, candidate offsets) are staged in shared memory at the start (one
 // coalesced load instead of a chain of dependent global loads in every role's item walk).
-//   warps 4-11   also dequantize the next item's tokens once its predecessor's last PV has completed
 // simt_target_attend_kernel: CUDA cores, one warp per (candidate, head), any S >= 1, d <= 128, f32 or
 // bf16 -- the shapes the tcgen05 kernel does not take.
 #include <cuda.h>
@@ -63,11 +63,13 @@ constexpr int kMaxTableUsers = 1024;  // B + 1 entries of uts and row_offsets st
 
 struct TABars {
     uint64_t qk_full[2], qk_empty[2];
-    uint64_t t_full, t_free;              // the item's tokens in smem / its last PV done (T reusable)
-    uint64_t s_full, p_full, o_full[2], o_empty[2];  // O double-buffered: the epilogue is off the chain
-    uint64_t ml_full[2], ml_empty[2];
+    uint64_t t_full, t_free;    // the item's tokens in smem / its last PV done (T reusable)
+    uint64_t s_full, s_free;    // S(t) computed / read by the softmax
+    uint64_t p_full, p_free;    // P(t) written / read by PV(t)
+    uint64_t o_full, o_empty;   // O(t) computed / read by the epilogue
+    uint64_t ml_full, ml_empty;  // the row statistics of tile t, softmax -> epilogue
     uint32_t tmem_base, pad;
-    float st[2][3][128];  // per tile parity and row: 1 / l, p_self / l, lse (softmax -> epilogue)
+    float st[3][128];  // per row: 1 / l, p_self / l, lse
     int64_t uts[kMaxTableUsers], roff[kMaxTableUsers];
 };
 constexpr int kSmem = kBarOff + (int)sizeof(TABars) + 1024;
@@ -99,25 +101,25 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
 // 16-B chunk c (of 8) of row r in a SWIZZLE_128B half tile of 128-B rows
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
-template <int NS>  // N = S tokens
+template <int NS>  // N = S tokens, issued as N = 128 halves (the B operand T is one 128-B swizzle column wide)
 __device__ __forceinline__ void issue_scores(uint32_t tS, uint32_t sQ, uint32_t sT) {
-    constexpr uint32_t id = ptx::idesc_bf16_f32(128, NS, 0, 0);  // Q, T both K-major
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 0);  // Q, T both K-major
     constexpr int halfT = NS * 128;
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
-        ptx::mma_ss_w(tS, ptx::sdesc_sw128(sQ + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024),
-                      ptx::sdesc_sw128(sT + (kk >> 2) * halfT + (kk & 3) * 32, 16, 1024), id, kk > 0);
+    for (int n = 0; n < NS / 128; ++n)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+            ptx::mma_ss_w(tS + n * 128, ptx::sdesc_sw128(sQ + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024),
+                          ptx::sdesc_sw128(sT + (kk >> 2) * halfT + n * 128 * 128 + (kk & 3) * 32, 16, 1024), id,
+                          kk > 0);
 }
 template <int NS>
 __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t sT) {
-    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM) x T (MN-major)
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM, 8 columns per 16 tokens) x T (MN-major)
     constexpr int halfT = NS * 128;
-    // P of tokens [0, NS/2) sits in S columns [0, NS/4), of tokens [NS/2, NS) in [NS/2, 3 NS/4): each
-    // softmax thread overwrites only S columns it has already read itself
 #pragma unroll
     for (int kk = 0; kk < NS / 16; ++kk)
-        ptx::mma_ts_w(tO, tP + (kk / (NS / 32)) * (NS / 2) + (kk % (NS / 32)) * 8,
-                      ptx::sdesc_sw128(sT + kk * 2048, halfT, 1024), id, kk > 0);
+        ptx::mma_ts_w(tO, tP + kk * 8, ptx::sdesc_sw128(sT + kk * 2048, halfT, 1024), id, kk > 0);
 }
 
 template <int NS>
@@ -135,16 +137,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bars->qk_full[s], 1);
             ptx::mbar_init(&bars->qk_empty[s], 256);  // the softmax threads: self dot done, S(t) done
         }
-        ptx::mbar_init(&bars->t_full, 256);   // warps 4-11 dequantized their share
+        ptx::mbar_init(&bars->t_full, 256);  // warps 4-11 dequantized their share
         ptx::mbar_init(&bars->t_free, 1);
         ptx::mbar_init(&bars->s_full, 1);
+        ptx::mbar_init(&bars->s_free, 256);
         ptx::mbar_init(&bars->p_full, 256);
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&bars->o_full[b], 1);
-            ptx::mbar_init(&bars->o_empty[b], 128);
-            ptx::mbar_init(&bars->ml_full[b], 256);
-            ptx::mbar_init(&bars->ml_empty[b], 128);
-        }
+        ptx::mbar_init(&bars->p_free, 1);
+        ptx::mbar_init(&bars->o_full, 1);
+        ptx::mbar_init(&bars->o_empty, 128);
+        ptx::mbar_init(&bars->ml_full, 256);
+        ptx::mbar_init(&bars->ml_empty, 128);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
@@ -160,8 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = bars->tmem_base;
     const int64_t* uts = staged ? bars->uts : P.uts;
     const int64_t* roff = staged ? bars->roff : P.row_offsets;
-    // TMEM: S (P over part of it) in [0, NS), O(t) in [NS + 128 (t % 2), NS + 128 (t % 2) + 128)
-    const uint32_t tS = tmem, tO0 = tmem + NS;
+    const uint32_t tS = tmem, tP = tmem + 256, tO = tmem + 384;
     const int H = P.H;
     ItemIter iter;
     iter.init(uts, P.B, H, blockIdx.x, gridDim.x);
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ============================ MMA issuer ============================
+        // ============================ score GEMMs ============================
         int g = 0;
         for (int k = 0; iter.next(it, uts, P.B, H); ++k) {
             ptx::mbar_wait(&bars->t_full, (uint32_t)k & 1u);
@@ -194,21 +195,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int st = g & 1;
                 ptx::mbar_wait(&bars->qk_full[st], (uint32_t)(g >> 1) & 1u);
                 if (lane == 0) TTRACE(1, g);
-                // S(g) overwrites the P columns PV(g - 1) read: wait for its completion
-                if (g >= 1) ptx::mbar_wait(&bars->o_full[(g - 1) & 1], (uint32_t)((g - 1) >> 1) & 1u);
+                if (g >= 1) ptx::mbar_wait(&bars->s_free, (uint32_t)(g - 1) & 1u);  // the softmax read S(g - 1)
                 ptx::tc_fence_after();
                 issue_scores<NS>(tS, base + kQKOff + st * 2 * kTileB, base + kTOff);
                 ptx::mma_commit_w(&bars->s_full);
                 if (lane == 0) TTRACE(2, g);
+            }
+        }
+    } else if (warp == 3) {
+        // ============================ PV GEMMs ============================
+        int g = 0;
+        for (int k = 0; iter.next(it, uts, P.B, H); ++k) {
+            for (int t = it.t0; t < it.t1; ++t, ++g) {
                 ptx::mbar_wait(&bars->p_full, (uint32_t)g & 1u);
                 if (lane == 0) TTRACE(3, g);
-                // O buffer g % 2: the epilogue has read O(g - 2)
-                if (g >= 2) ptx::mbar_wait(&bars->o_empty[g & 1], (uint32_t)((g >> 1) - 1) & 1u);
+                if (g >= 1) ptx::mbar_wait(&bars->o_empty, (uint32_t)(g - 1) & 1u);  // epilogue read O(g - 1)
                 ptx::tc_fence_after();
-                issue_pv<NS>(tO0 + (g & 1) * 128, tS, base + kTOff);
-                if (lane == 0) TTRACE(4, g);
-                ptx::mma_commit_w(&bars->o_full[g & 1]);
+                issue_pv<NS>(tO, tP, base + kTOff);
+                ptx::mma_commit_w(&bars->o_full);
+                ptx::mma_commit_w(&bars->p_free);
                 if (t == it.t1 - 1) ptx::mma_commit_w(&bars->t_free);
+                if (lane == 0) TTRACE(4, g);
             }
         }
     } else if (warp >= 4) {
@@ -259,8 +266,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sts128(hb + swz(i, c0), make_uint4(o[0], o[1], o[2], o[3]));
                     sts128(hb + swz(i, c0 + 1), make_uint4(o[4], o[5], o[6], o[7]));
                 }
-            }
-            if (smx) {
                 ptx::fence_proxy_async_smem();
                 ptx::mbar_arrive(&bars->t_full);
             }
@@ -304,12 +309,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
                     if (threadIdx.x == 128) TTRACE(7, g);
+                    // P(g) has its own columns: free once PV(g - 1) has read them
+                    if (g >= 1) ptx::mbar_wait(&bars->p_free, (uint32_t)(g - 1) & 1u);
+                    ptx::tc_fence_after();
                     float l = 0.f;
 #pragma unroll 1
                     for (int c = 0; c < NS / 2; c += 32) {
                         uint32_t r[32], pk[16];
                         ptx::tmem_ld16x32bx2_x32<NS / 2>(tS + lb + c, r);
                         ptx::tmem_wait_ld();
+                        if (c == NS / 2 - 32) {  // last S chunk of this thread loaded: S(g + 1) may overwrite S
+                            ptx::tc_fence_before();
+                            ptx::mbar_arrive(&bars->s_free);
+                        }
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const float p0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), P.scale_log2, -m));
@@ -317,20 +329,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                             l += p0 + p1;
                             pk[j] = ptx::pack_bf16x2(p0, p1);
                         }
-                        // P of these 32 tokens: 16 columns at the start of this thread's own S range
-                        ptx::tmem_st16x32bx2_x16<NS / 2>(tS + lb + c / 2, pk);
+                        // P of these 32 tokens: 16 columns (2 tokens per column), token order
+                        ptx::tmem_st16x32bx2_x16<NS / 4>(tP + lb + c / 2, pk);
                     }
                     l += __shfl_xor_sync(0xffffffffu, l, 16);
                     const float pself = ptx::ex2(self - m);
                     l += pself;
                     const float inv = 1.f / l;
-                    if (g >= 2) ptx::mbar_wait(&bars->ml_empty[g & 1], (uint32_t)((g >> 1) - 1) & 1u);
+                    if (g >= 1) ptx::mbar_wait(&bars->ml_empty, (uint32_t)(g - 1) & 1u);
                     if (ch == 0) {
-                        bars->st[g & 1][0][row] = inv;
-                        bars->st[g & 1][1][row] = pself * inv;
-                        bars->st[g & 1][2][row] = (m + __log2f(l)) * kLn2;
+                        bars->st[0][row] = inv;
+                        bars->st[1][row] = pself * inv;
+                        bars->st[2][row] = (m + __log2f(l)) * kLn2;
                     }
-                    ptx::mbar_arrive(&bars->ml_full[g & 1]);
+                    ptx::mbar_arrive(&bars->ml_full);
                     ptx::tmem_wait_st();
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(&bars->p_full);
@@ -340,56 +352,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int64_t row0 = roff[u] + (int64_t)t * 128;
                     const int64_t remr = R - (int64_t)t * 128;
                     const int valid = remr < 128 ? (int)remr : 128;
-                    // v_c of this thread's row (clamped to the tile's last valid row), in flight
-                    // while the softmax and the PV GEMM run
-                    // (the first 64 channels now, the second 64 once the first are combined)
+                    // v_c of this thread's row (clamped to the tile's last valid row), in flight while
+                    // the softmax and the PV GEMM run
                     const int vr = row < valid ? row : valid - 1;
                     const uint4* vs = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(P.v) +
                                                                      (size_t)(row0 + vr) * rstride + (size_t)h * 128);
-                    uint4 vh[8];
+                    uint4 vrow[16];
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) vh[c] = __ldg(vs + c);
-                    const int ob = g & 1;
-                    const uint32_t tO = tO0 + ob * 128;
-                    ptx::mbar_wait(&bars->ml_full[ob], (uint32_t)(g >> 1) & 1u);
+                    for (int c = 0; c < 16; ++c) vrow[c] = __ldg(vs + c);
+                    ptx::mbar_wait(&bars->ml_full, (uint32_t)g & 1u);
                     if (threadIdx.x == 384) TTRACE(9, g);
-                    const float inv = bars->st[ob][0][row], wself = bars->st[ob][1][row], lse = bars->st[ob][2][row];
-                    ptx::mbar_arrive(&bars->ml_empty[ob]);
-                    ptx::mbar_wait(&bars->o_full[ob], (uint32_t)(g >> 1) & 1u);
+                    const float inv = bars->st[0][row], wself = bars->st[1][row], lse = bars->st[2][row];
+                    ptx::mbar_arrive(&bars->ml_empty);
+                    ptx::mbar_wait(&bars->o_full, (uint32_t)g & 1u);
                     if (threadIdx.x == 384) TTRACE(10, g);
                     ptx::tc_fence_after();
-#pragma unroll 1
-                    for (int half = 0; half < 2; ++half) {
-                        float o[64];
 #pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            uint32_t r[32];
-                            ptx::tmem_ld32_sync(tO + lb + half * 64 + c * 32, r);
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) o[32 * c + j] = __uint_as_float(r[j]);
+                    for (int q4 = 0; q4 < 4; ++q4) {  // 32 channels at a time
+                        uint32_t r[32];
+                        ptx::tmem_ld32_sync(tO + lb + q4 * 32, r);
+                        if (q4 == 3) {  // O fully read: PV(g + 1) may overwrite it
+                            ptx::tc_fence_before();
+                            ptx::mbar_arrive(&bars->o_empty);
                         }
+                        float o[32];
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            const uint4 va = vh[c];
+                        for (int c = 0; c < 4; ++c) {
+                            const uint4 va = vrow[q4 * 4 + c];
                             const uint32_t vw[4] = {va.x, va.y, va.z, va.w};
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
-                                o[8 * c + 2 * e] = fmaf(wself, __uint_as_float(vw[e] << 16), o[8 * c + 2 * e] * inv);
-                                o[8 * c + 2 * e + 1] =
-                                    fmaf(wself, __uint_as_float(vw[e] & 0xFFFF0000u), o[8 * c + 2 * e + 1] * inv);
+                                o[8 * c + 2 * e] = fmaf(wself, __uint_as_float(vw[e] << 16),
+                                                        __uint_as_float(r[8 * c + 2 * e]) * inv);
+                                o[8 * c + 2 * e + 1] = fmaf(wself, __uint_as_float(vw[e] & 0xFFFF0000u),
+                                                            __uint_as_float(r[8 * c + 2 * e + 1]) * inv);
                             }
                         }
-                        if (half == 0) {
-#pragma unroll
-                            for (int c = 0; c < 8; ++c) vh[c] = __ldg(vs + 8 + c);
-                        }
                         if (row < valid) {
-                            const size_t e0 = (size_t)(row0 + row) * rstride + (size_t)h * 128 + half * 64;
+                            const size_t eo = (size_t)(row0 + row) * rstride + (size_t)h * 128 + q4 * 32;
                             if (P.resid) {
                                 const uint4* rs = reinterpret_cast<const uint4*>(
-                                    reinterpret_cast<const __nv_bfloat16*>(P.resid) + e0);
+                                    reinterpret_cast<const __nv_bfloat16*>(P.resid) + eo);
 #pragma unroll
-                                for (int c = 0; c < 8; ++c) {
+                                for (int c = 0; c < 4; ++c) {
                                     const uint4 ra = __ldg(rs + c);
                                     const uint32_t rw[4] = {ra.x, ra.y, ra.z, ra.w};
 #pragma unroll
@@ -400,25 +405,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                             if (P.out_bf16) {
-                                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + e0);
+                                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + eo);
 #pragma unroll
-                                for (int c = 0; c < 8; ++c)
+                                for (int c = 0; c < 4; ++c)
                                     dst[c] = make_uint4(ptx::pack_bf16x2(o[8 * c], o[8 * c + 1]),
                                                         ptx::pack_bf16x2(o[8 * c + 2], o[8 * c + 3]),
                                                         ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]),
                                                         ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7]));
                             } else {
-                                float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + e0);
+                                float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + eo);
 #pragma unroll
-                                for (int c = 0; c < 16; ++c)
+                                for (int c = 0; c < 8; ++c)
                                     dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
                             }
                         }
                     }
                     if (P.lse && row < valid) P.lse[(size_t)(row0 + row) * H + h] = lse;
                     if (threadIdx.x == 384) TTRACE(11, g);
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive(&bars->o_empty[ob]);
                 }
             }
         }

@@ -13,6 +13,9 @@
 //   warps 8-15   epilogue: TMEM -> (+ residual) -> bf16, coalesced through a TMEM round trip
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "internal.h"
 #include "sm100_ptx.cuh"
@@ -59,6 +62,55 @@ __device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
     asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
                  "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                  : "memory");
+}
+
+// Epilogue of one 64-column block of a 128-row accumulator (this warp: 32 rows, TMEM address tc):
+// fp32 -> bf16 (+ residual) -> global, coalesced through a permuted TMEM round trip (after a
+// 16x256b load a quad of threads holds 128 contiguous bytes of one row).  row0 = the warp's first
+// global row; col0 = the block's first global column (residual), c_out its column in `outp`.
+__device__ __forceinline__ void store_block64(const GemmParams& P, uint32_t tc, int row0, int lane,
+                                              __nv_bfloat16* outp, int nw, int col0, int c_out) {
+    uint32_t a[32];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32_sync(tc + c * 32, r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int w = 16 * c + j;  // packed word w = columns 2w, 2w + 1
+            const int g = (w >> 1) & 3, p = w >> 3, e = w & 1;
+            a[8 * g + 2 * p + e] = ptx::pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        }
+    }
+    ptx::tmem_st32(tc, a);
+    ptx::tmem_wait_st();
+    const int p = lane & 3;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        uint32_t r[16];
+        ptx::tmem_ld16x256b_x4(tc + ((uint32_t)(16 * half) << 16), r);
+        ptx::tmem_wait_ld();
+        ptx::reg_fence(r);
+        const int ra = row0 + 16 * half + (lane >> 2);
+        uint32_t v0[8] = {r[0], r[1], r[4], r[5], r[8], r[9], r[12], r[13]};
+        uint32_t v1[8] = {r[2], r[3], r[6], r[7], r[10], r[11], r[14], r[15]};
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int row = ra + 8 * rr;
+            uint32_t* v = rr ? v1 : v0;
+            if (row >= P.M) continue;
+            if (P.resid) {  // + residual (16 contiguous bf16 of the row), added in f32
+                const uint4* rs = reinterpret_cast<const uint4*>(P.resid + (size_t)row * P.N + col0 + 16 * p);
+                const uint4 x0 = rs[0], x1 = rs[1];
+                const uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    v[e] = ptx::pack_bf16x2(__uint_as_float(v[e] << 16) + __uint_as_float(xw[e] << 16),
+                                            __uint_as_float(v[e] & 0xFFFF0000u) + __uint_as_float(xw[e] & 0xFFFF0000u));
+            }
+            st_v8(outp + (size_t)row * nw + c_out + 16 * p, *reinterpret_cast<const uint32_t(*)[8]>(v));
+        }
+    }
 }
 
 template <int SB, int ST>
@@ -161,51 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
             aph[ab] ^= 1;
             ptx::tc_fence_after();
-            const uint32_t tc = tmem + lane_bits + ab * 128 + chalf * 64;
-            uint32_t a[32];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t r[32];
-                ptx::tmem_ld32_sync(tc + c * 32, r);
-                // permuted 32x32b store back into the (read) accumulator columns: after a 16x256b load
-                // a quad of threads holds 128 contiguous bytes (64 columns) of one row
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int w = 16 * c + j;  // packed word w = columns 2w, 2w + 1
-                    const int g = (w >> 1) & 3, p = w >> 3, e = w & 1;
-                    a[8 * g + 2 * p + e] = ptx::pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-                }
-            }
-            ptx::tmem_st32(tc, a);
-            ptx::tmem_wait_st();
-            const int p = lane & 3;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint32_t r[16];
-                ptx::tmem_ld16x256b_x4(tc + ((uint32_t)(16 * half) << 16), r);
-                ptx::tmem_wait_ld();
-                ptx::reg_fence(r);
-                const int ra = m * 128 + wq * 32 + 16 * half + (lane >> 2);
-                uint32_t v0[8] = {r[0], r[1], r[4], r[5], r[8], r[9], r[12], r[13]};
-                uint32_t v1[8] = {r[2], r[3], r[6], r[7], r[10], r[11], r[14], r[15]};
-#pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                    const int row = ra + 8 * rr;
-                    uint32_t* v = rr ? v1 : v0;
-                    if (row >= P.M) continue;
-                    if (P.resid) {  // + residual (16 contiguous bf16 of the row), added in f32
-                        const uint4* rs = reinterpret_cast<const uint4*>(P.resid + (size_t)row * P.N + col0 + 16 * p);
-                        const uint4 x0 = rs[0], x1 = rs[1];
-                        const uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            v[e] = ptx::pack_bf16x2(__uint_as_float(v[e] << 16) + __uint_as_float(xw[e] << 16),
-                                                    __uint_as_float(v[e] & 0xFFFF0000u) +
-                                                        __uint_as_float(xw[e] & 0xFFFF0000u));
-                    }
-                    st_v8(outp + (size_t)row * nw + c_out + 16 * p, *reinterpret_cast<const uint32_t(*)[8]>(v));
-                }
-            }
+            store_block64(P, tmem + lane_bits + ab * 128 + chalf * 64, m * 128 + wq * 32, lane, outp, nw, col0, c_out);
             ptx::tc_fence_before();
             ptx::mbar_arrive(&bars->acc_empty[ab]);
             ab ^= 1;
@@ -214,6 +222,137 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) ptx::tmem_dealloc(tmem, 256);
+}
+
+
+// ---- CTA pair (cta_group::2): 256 x 256 output tiles.  CTA r of the pair loads the A rows
+// [256 m + 128 r, + 128) and the B rows [256 n + 128 r, + 128) of every 64-wide K block; the leader
+// issues M = 256, N = 256 MMAs over both CTAs' shared memory, each CTA accumulating its 128 rows x 256
+// columns in TMEM (double-buffered: 2 x 256 columns).  Per K block each SM reads 16 KB of A and 16 KB
+// of B from shared memory per 512 MMA clocks (64 B/clk) instead of 32 KB per 256 clocks in the
+// 128 x 128 kernel, which is shared-memory bound at half the tensor rate.
+template <int ST>
+__device__ __forceinline__ void issue_kblock2(uint32_t tacc, uint32_t base, bool acc) {
+    const uint32_t a = base + ST * kStageBytes, b = a + kBlk;
+    constexpr uint32_t id = ptx::idesc_bf16_f32(256, 256, 0, 0);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+        ptx::mma2_ss_w(tacc, ptx::sdesc_sw128(a + kk * 32, 16, 1024), ptx::sdesc_sw128(b + kk * 32, 16, 1024), id,
+                       (acc || kk > 0) ? 1u : 0u);
+}
+__device__ __forceinline__ void issue_kblock2_d(int st, uint32_t tacc, uint32_t base, bool acc) {
+    switch (st) {
+        case 0: issue_kblock2<0>(tacc, base, acc); break;
+        case 1: issue_kblock2<1>(tacc, base, acc); break;
+        case 2: issue_kblock2<2>(tacc, base, acc); break;
+        case 3: issue_kblock2<3>(tacc, base, acc); break;
+        case 4: issue_kblock2<4>(tacc, base, acc); break;
+        default: issue_kblock2<5>(tacc, base, acc); break;
+    }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    sm100_gemm2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                       const GemmParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t base = ptx::smem_u32(smem);
+    GemmBars* bars = reinterpret_cast<GemmBars*>(smem + kBarOff);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int rank = (int)ptx::cluster_ctarank();
+    const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&bars->full[s], 1);   // the leader's expect_tx + both CTAs' TMA bytes
+            ptx::mbar_init(&bars->empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bars->acc_full[b], 1);
+            ptx::mbar_init(&bars->acc_empty[b], 16);  // 8 epilogue warps of each CTA, one arrive per warp
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc2(&bars->tmem_base, 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();  // both CTAs' barriers exist before any remote signal
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
+    const int num_m = (P.M + 255) / 256, num_n = P.N / 256, nk = P.K / 64;
+    const int num_tiles = num_m * num_n;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (both CTAs): this CTA's A rows and B rows of each K block
+        ptx::tma_prefetch(&mapA);
+        ptx::tma_prefetch(&mapB);
+        const uint64_t pol_a = ptx::policy_evict_first(), pol_b = ptx::policy_evict_last();
+        int st = 0;
+        uint32_t ph = 0;
+        for (int t = pair; t < num_tiles; t += npairs) {
+            const int m = t / num_n, n = t % num_n;
+            for (int kb = 0; kb < nk; ++kb) {
+                ptx::mbar_wait(&bars->empty[st], ph ^ 1);
+                const uint32_t fl = ptx::mapa(ptx::smem_u32(&bars->full[st]), 0);
+                if (rank == 0) ptx::mbar_arrive_expect_tx_w(&bars->full[st], 2 * kStageBytes);
+                const uint32_t s = base + st * kStageBytes;
+                ptx::tma_load_3d_2sm_w(s, &mapA, fl, kb * 64, m * 256 + rank * 128, 0, pol_a);
+                ptx::tma_load_3d_2sm_w(s + kBlk, &mapB, fl, kb * 64, n * 256 + rank * 128, 0, pol_b);
+                if (++st == kStages) { st = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1 && rank == 0) {
+        // ---------------- MMA issuer (leader CTA)
+        int st = 0, ab = 0;
+        uint32_t ph = 0;
+        uint32_t aph[2] = {0, 0};
+        for (int t = pair; t < num_tiles; t += npairs) {
+            ptx::mbar_wait(&bars->acc_empty[ab], aph[ab] ^ 1);
+            aph[ab] ^= 1;
+            const uint32_t tacc = tmem + ab * 256;
+            for (int kb = 0; kb < nk; ++kb) {
+                ptx::mbar_wait(&bars->full[st], ph);
+                ptx::tc_fence_after();
+                issue_kblock2_d(st, tacc, base, kb > 0);
+                ptx::mma2_commit_mc_w(&bars->empty[st]);
+                if (++st == kStages) { st = 0; ph ^= 1; }
+            }
+            ptx::mma2_commit_mc_w(&bars->acc_full[ab]);
+            ab ^= 1;
+        }
+    } else if (warp >= 8) {
+        // ---------------- epilogue (both CTAs): this CTA's 128 rows x 256 columns of the tile
+        const int wq = warp % 4;
+        const int cq = (warp - 8) / 4;  // columns [128 cq, 128 cq + 128) of the tile
+        const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
+        const int nw = P.N / P.nsplit;
+        const uint32_t acc_empty_l = ptx::mapa(ptx::smem_u32(&bars->acc_empty[0]), 0);
+        int ab = 0;
+        uint32_t aph[2] = {0, 0};
+        for (int t = pair; t < num_tiles; t += npairs) {
+            const int m = t / num_n, n = t % num_n;
+            ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
+            aph[ab] ^= 1;
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int sb = 0; sb < 2; ++sb) {
+                const int col0 = n * 256 + cq * 128 + sb * 64;
+                const int which = col0 / nw, c_out = col0 % nw;
+                store_block64(P, tmem + lane_bits + ab * 256 + cq * 128 + sb * 64, m * 256 + rank * 128 + wq * 32,
+                              lane, P.out[which], nw, col0, c_out);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0) ptx::mbar_arrive(&bars->acc_empty[ab]);
+                else ptx::mbar_arrive_cluster(acc_empty_l + ab * 8, 1);
+            }
+            ab ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();  // no CTA leaves (deallocates) while the pair's MMAs may still target it
+    if (warp == 1) ptx::tmem_dealloc2(tmem, 512);
 }
 
 // bf16 row-major [rows, cols] as a TMA map with 64 x 128 boxes and the 128-B swizzle
@@ -241,6 +380,18 @@ cudaError_t launch_sm100_gemm(int M, int N, int K, const void* A, int64_t lda, c
     P.nsplit = nsplit;
     for (int i = 0; i < 4; ++i) P.out[i] = reinterpret_cast<__nv_bfloat16*>(outs[i < nsplit ? i : 0]);
     P.resid = reinterpret_cast<const __nv_bfloat16*>(resid);
+    static const bool pair_off = [] {
+        const char* e = getenv("VISTA_GEMM_PAIR");
+        return e && e[0] == '0';
+    }();
+    if (N % 256 == 0 && !pair_off) {  // CTA-pair 256 x 256 tiles
+        const int tiles = ((M + 255) / 256) * (N / 256);
+        const int pairs = std::min(tiles, num_sms / 2);
+        const cudaError_t a = set_smem_attr(reinterpret_cast<const void*>(sm100_gemm2_kernel), kSmem);
+        if (a != cudaSuccess) return a;
+        sm100_gemm2_kernel<<<2 * pairs, kThreads, kSmem, stream>>>(ma, mb, P);
+        return cudaGetLastError();
+    }
     const int tiles = ((M + 127) / 128) * (N / 128);
     const int grid = tiles < num_sms ? tiles : num_sms;
     const cudaError_t a = set_smem_attr(reinterpret_cast<const void*>(sm100_gemm_kernel), kSmem);

@@ -149,6 +149,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- own arm
 def run_own(args, rank, world, local_rank):
+    phase_fns = None  # by_length: (partial, all_gather, merge) callables for the per-phase breakdown
     import numpy as np
     import torch
 
@@ -347,6 +348,14 @@ def run_own(args, rank, world, local_rank):
                 out, lse = vdist.summarize_by_length(ins[0], ins[1], ins[2], ins[3], ulen, attn=args.attn,
                                                      total_len=total)
                 return [out] + ([lse] if lse is not None else [])
+
+            # the same three phases, separately callable for the breakdown (summarize_by_length's body)
+            be = vdist.CudaBackend()
+            acode = 0 if args.attn == "softmax" else 1
+            phase_fns = (lambda: be.partial(q, K, V, soff_t, total, acode),
+                         lambda pp: (vdist._all_gather(pp[0], None),
+                                     vdist._all_gather(pp[1], None) if acode == 0 else None),
+                         lambda gg: be.merge(gg[0], gg[1], q, acode, ulen))
         else:
             segs_obj = [vdist.Segment(u, a0, e0) for u, a0, e0 in seg]
             fplan = vdist.FlatPlan(all_segs, lens, rank, dev)
@@ -440,6 +449,30 @@ def run_own(args, rank, world, local_rank):
         kern_ms = sum(a.elapsed_time(b) for a, b in ev_k) / K_steps
         graph_note = (graph_note or "graph") + f"; kernel events re-timed over K eager steps ({type(exc).__name__})"
 
+    phases = None
+    if world > 1 and mode == "by_length" and phase_fns is not None:
+        # per-phase breakdown of the split-L step (eager, after the timed region):
+        # partial kernel(s), the all_gather of the partials, the merge; CUDA events, max over ranks
+        pf, xf, mf = phase_fns
+        acc = [0.0, 0.0, 0.0]
+        nrep = 5
+        for _ in range(nrep):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(stream)
+            parts = pf()
+            e[1].record(stream)
+            gathered = xf(parts)
+            e[2].record(stream)
+            mf(gathered)
+            e[3].record(stream)
+            torch.cuda.synchronize()
+            for i in range(3):
+                acc[i] += e[i].elapsed_time(e[i + 1]) / nrep
+        t = torch.tensor(acc, device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        phases = {"partial_ms": round(float(t[0]), 5), "all_gather_ms": round(float(t[1]), 5),
+                  "merge_ms": round(float(t[2]), 5),
+                  "note": "eager, 5 repetitions after the timed region, each phase max over ranks"}
     if world > 1:
         t = torch.tensor([elapsed_ms, kern_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -628,6 +661,8 @@ def run_own(args, rank, world, local_rank):
         sustained["note"] = ("SURVEY 8(d) protocol: R graph-replayed steps per run (>= 200 ms), median of 5 runs; "
                              "the sustained regime the K-step burst number sits above")
         res["sustained"] = sustained
+    if phases is not None:
+        res["phases"] = phases
     if world > 1 and args.dist_backend == "gloo":
         res["dry_run"] = ("gloo process group: the exchange is staged through host memory and the ranks may share "
                           "one GPU -- a functional run of the multi-rank path, not a scaling measurement")

@@ -12,12 +12,12 @@
 // rows' jagged layout (work.cuh), one 128x128x128 tcgen05 GEMM per tile with W_u as the B operand.
 // HBM-bound: per row-head 256 B of q read and 256 B (bf16) of o written (+ 512 B of k_self, v_self
 // with the Delta term), 2 d^2 = 32,768 flop.
-//   warp 0        TMA producer: q tiles (history rows: 3 stages of 32 KB) or q, k_self, v_self tiles
-//                 (target rows: 2 stages of 96 KB); W_u (bulk copy) per unit
+//   warp 0        TMA producer: q tiles (history rows: 3 stages of 32 KB) or q, k_self tiles
+//                 (target rows: 2 stages of 64 KB); W_u (bulk copy) per unit into one of two buffers
 //   warp 1        MMA issuer; O double-buffered in TMEM
 //   warps 4..7    transform: phi1(Q) in place (bf16), one row per thread; with Delta also the row dot
 //                 phi1(q) . phi1(k_self) (/ N_u) from the staged k tile, into shared memory
-//   warps 8..15   epilogue: TMEM (+ d_r v_self_r from the staged v tile) -> rows (bf16 coalesced
+//   warps 8..15   epilogue: TMEM (+ d_r v_self_r, the v_self row prefetched) -> rows (bf16 coalesced
 //                 through a TMEM round trip, or f32); two warps per TMEM lane quarter, 64 columns each
 // qla_rows_simt_kernel: CUDA-core path for f32 inputs or d in {32, 64} (one block per (row, head)).
 #include <cuda.h>
@@ -40,15 +40,16 @@ constexpr int kThreads = 512;
 constexpr int kXform = 128;
 constexpr int kEpi = 256;
 
-// Shared-memory geometry: history rows stage q only (3 x 32 KB); target rows stage q, k_self and
-// v_self of a tile together (2 x 96 KB), so the Delta dot and the + d v_self of the epilogue read
-// shared memory instead of re-reading rows from global memory on the tile's critical path.
+// Shared-memory geometry: history rows stage q only (3 x 32 KB); target rows stage q and k_self of
+// a tile together (2 x 64 KB) for the Delta dot, and the epilogue reads its v_self row from global
+// memory (prefetched ahead of the accumulator).  W_u is double-buffered (2 x 32 KB), so the next
+// unit's operand loads while the current unit's tiles run.
 template <bool DELTA>
 struct Geo {
     static constexpr int kStages = DELTA ? 2 : 3;
-    static constexpr int kStageBytes = DELTA ? 3 * kTile : kTile;
+    static constexpr int kStageBytes = DELTA ? 2 * kTile : kTile;
     static constexpr int kWOff = kStages * kStageBytes;
-    static constexpr int kBarOff = kWOff + kTile;
+    static constexpr int kBarOff = kWOff + 2 * kTile;
     static constexpr int kDrOff = kBarOff + 256;  // float [stage][128 rows]: the Delta dot of each row
     static constexpr int kSmem = kDrOff + kStages * 128 * 4 + 1024;
     static_assert(kSmem <= 232448, "shared memory");
@@ -57,7 +58,7 @@ struct Geo {
 struct Bars {
     uint64_t q_full[3], q_ready[3], q_empty[3];
     uint64_t acc_full[2], acc_empty[2];
-    uint64_t w_full, w_empty;
+    uint64_t w_full[2], w_empty[2];
     uint32_t tmem_base;
 };
 
@@ -69,6 +70,7 @@ struct Params {
     const int64_t* offsets;       // history offsets [B+1]: N_u for the Delta term's 1/N ...
     const int64_t* user_len;      // ... or N_u given directly ([B], may be NULL)
     const __nv_bfloat16* gate;    // [R, H, 128] or NULL: out = o (.) sigmoid(gate) (the summarizer's SGLU gate)
+    const __nv_bfloat16* v_self;  // Delta: [R, H, 128], read by the epilogue
     int out_bf16;
     int normalize;
     int B, H;
@@ -164,8 +166,8 @@ __device__ __forceinline__ void xform_tile(uint32_t qbuf, int xt) {
 
 // O = phi1(Q) W: A = phi1(Q) [row][c1] K-major, B = W [K = c1][N = c2] MN-major
 template <int SB, int ST, int WOFF>
-__device__ __forceinline__ void issue_tile(uint32_t tacc, uint32_t base) {
-    const uint32_t qb = base + ST * SB, wb = base + WOFF;
+__device__ __forceinline__ void issue_tile(uint32_t tacc, uint32_t base, uint32_t wsel) {
+    const uint32_t qb = base + ST * SB, wb = base + WOFF + wsel;
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, 128, 0, 1);
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk)
@@ -174,12 +176,12 @@ __device__ __forceinline__ void issue_tile(uint32_t tacc, uint32_t base) {
 }
 
 template <bool DELTA>
-__device__ __forceinline__ void issue_tile_d(int stage, uint32_t tacc, uint32_t base) {
+__device__ __forceinline__ void issue_tile_d(int stage, uint32_t tacc, uint32_t base, uint32_t wsel) {
     using G = Geo<DELTA>;
     switch (stage) {
-        case 0: issue_tile<G::kStageBytes, 0, G::kWOff>(tacc, base); break;
-        case 1: issue_tile<G::kStageBytes, 1 % G::kStages, G::kWOff>(tacc, base); break;
-        default: issue_tile<G::kStageBytes, 2 % G::kStages, G::kWOff>(tacc, base); break;
+        case 0: issue_tile<G::kStageBytes, 0, G::kWOff>(tacc, base, wsel); break;
+        case 1: issue_tile<G::kStageBytes, 1 % G::kStages, G::kWOff>(tacc, base, wsel); break;
+        default: issue_tile<G::kStageBytes, 2 % G::kStages, G::kWOff>(tacc, base, wsel); break;
     }
 }
 
@@ -208,8 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bars->acc_full[b], 1);
             ptx::mbar_init(&bars->acc_empty[b], kEpi);
         }
-        ptx::mbar_init(&bars->w_full, 1);
-        ptx::mbar_init(&bars->w_empty, 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bars->w_full[b], 1);
+            ptx::mbar_init(&bars->w_empty[b], 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 256);
@@ -233,9 +237,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         int k = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
-            if (k > 0) ptx::mbar_wait(&bars->w_empty, (k - 1) & 1);  // the previous unit's GEMMs are done with W
-            ptx::mbar_arrive_expect_tx_w(&bars->w_full, kTile);
-            ptx::bulk_g2s_w(base + G::kWOff, P.w_op + (size_t)(it.u * HG + it.hg) * kTile, kTile, &bars->w_full);
+            // W buffer k % 2: free once unit k - 2's GEMMs are done with it
+            if (k >= 2) ptx::mbar_wait(&bars->w_empty[k & 1], (uint32_t)((k >> 1) - 1) & 1u);
+            ptx::mbar_arrive_expect_tx_w(&bars->w_full[k & 1], kTile);
+            ptx::bulk_g2s_w(base + G::kWOff + (k & 1) * kTile, P.w_op + (size_t)(it.u * HG + it.hg) * kTile, kTile,
+                            &bars->w_full[k & 1]);
             const int64_t row0 = P.row_offsets[it.u];
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->q_empty[stage], phase ^ 1);
@@ -244,12 +250,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* st = smem + stage * G::kStageBytes;
                 for (int half = 0; half < 2; ++half) {
                     ptx::tma_load_3d_w(st + half * kHalf, &mapQ, &bars->q_full[stage], half * 64, it.hg, row, pol);
-                    if constexpr (DELTA) {
+                    if constexpr (DELTA)
                         ptx::tma_load_3d_w(st + kTile + half * kHalf, &mapK, &bars->q_full[stage], half * 64, it.hg,
                                            row, pol);
-                        ptx::tma_load_3d_w(st + 2 * kTile + half * kHalf, &mapV, &bars->q_full[stage], half * 64,
-                                           it.hg, row, pol);
-                    }
                 }
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
@@ -262,20 +265,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t aph[2] = {0, 0};
         int k = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
-            ptx::mbar_wait(&bars->w_full, k & 1);
+            ptx::mbar_wait(&bars->w_full[k & 1], (uint32_t)(k >> 1) & 1u);
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->q_ready[stage], phase);
                 ptx::mbar_wait(&bars->acc_empty[ab], aph[ab] ^ 1);
                 aph[ab] ^= 1;
                 ptx::tc_fence_after();
                 const uint32_t tacc = tmem + ab * 128;
-                issue_tile_d<DELTA>(stage, tacc, base);
+                issue_tile_d<DELTA>(stage, tacc, base, (k & 1) * kTile);
                 ptx::mma_commit_w(&bars->acc_full[ab]);
                 ptx::mma_commit_w(&bars->q_empty[stage]);
                 ab ^= 1;
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
-            ptx::mma_commit_w(&bars->w_empty);
+            ptx::mma_commit_w(&bars->w_empty[k & 1]);
             ++k;
         }
     } else if (warp >= 4 && warp < 8) {
@@ -317,6 +320,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int valid = rem < 128 ? (int)rem : 128;
                 const int64_t grow0 = row0 + (int64_t)t * 128;
                 const size_t e0 = ((size_t)grow0 * P.H + it.hg) * 128;  // element (row 0, col 0) of the tile
+                uint4 vrow[8];  // Delta: this thread's 64 v_self values, in flight while the GEMM runs
+                if constexpr (DELTA) {
+                    const int vr = row < valid ? row : valid - 1;
+                    const uint4* vs = reinterpret_cast<const uint4*>(P.v_self + e0 + (size_t)vr * rstride + chalf * 64);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) vrow[c] = __ldg(vs + c);
+                }
                 ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
                 aph[ab] ^= 1;
                 ptx::tc_fence_after();
@@ -329,13 +339,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[32 * c + j] = __uint_as_float(r[j]);
                 }
-                if constexpr (DELTA) {  // + d_r v_self_r, both from shared memory
+                if constexpr (DELTA) {  // + d_r v_self_r (d_r from shared memory, v_self prefetched)
                     ptx::mbar_wait(&bars->q_ready[stage], phase);  // orders the transform's d_r writes
                     const float dr = dr_smem[stage * 128 + row];
-                    const uint32_t vb = base + stage * G::kStageBytes + 2 * kTile + chalf * kHalf;
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
-                        const uint4 b = lds128(vb + swz_chunk(row, c));
+                        const uint4 b = vrow[c];
                         const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
@@ -343,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             o[8 * c + 2 * e + 1] = fmaf(dr, __uint_as_float(bw[e] & 0xFFFF0000u), o[8 * c + 2 * e + 1]);
                         }
                     }
-                    ptx::mbar_arrive(&bars->q_empty[stage]);  // v_self read: the stage may be refilled
+                    ptx::mbar_arrive(&bars->q_empty[stage]);  // d_r read: the stage's transform may run again
                 }
                 if (P.gate && row < valid) {  // SGLU gate (reading R23): o (.) sigmoid(g), sigmoid via one tanh
                     const uint4* gs = reinterpret_cast<const uint4*>(P.gate + e0 + (size_t)row * rstride + chalf * 64);
@@ -488,6 +497,7 @@ cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, 
     P.offsets = p.offsets;
     P.user_len = user_len;
     P.gate = reinterpret_cast<const __nv_bfloat16*>(gate);
+    P.v_self = reinterpret_cast<const __nv_bfloat16*>(v_self);
     P.normalize = p.normalize;
     P.out_bf16 = out_bf16;
     P.B = p.B;

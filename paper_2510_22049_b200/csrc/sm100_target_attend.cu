@@ -23,8 +23,8 @@
 //                [tokens; self]; also dequantize each item's tokens once its predecessor's last PV is done
 //   warps 12-15  epilogue, one thread per row: (O + p_self v_c) / l [+ resid] -> bf16 / f32 rows, lse;
 //                v_c rows prefetched from global memory; O released after its last TMEM load
-// The jagged tables (tile starts, candidate offsets) are staged in shared memory at the start (one
-// coalesced load instead of a chain of dependent global loads in every role's item walk).
+// (Staging the jagged tables in shared memory first was measured slower: 0.0370 vs 0.0354 ms at c2 --
+// the block-wide barrier after the table load delays every role, and the larger carve-out shrinks L1.)
 // simt_target_attend_kernel: CUDA cores, one warp per (candidate, head), any S >= 1, d <= 128, f32 or
 // bf16 -- the shapes the tcgen05 kernel does not take.
 #include <cuda.h>
@@ -55,11 +55,10 @@ constexpr int kThreads = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 // smem: tokens T (S x 128 bf16, two 64-column halves; 64 KB at S = 256), a 2-stage ring of (q, k_self)
-// tiles (128 KB), barriers, the per-row statistics and the jagged tables
+// tiles (128 KB), barriers and the per-row statistics
 constexpr int kTOff = 0;
 constexpr int kQKOff = 2 * kTileB;  // stage s: q at kQKOff + 2 s kTileB, k_self at + kTileB
 constexpr int kBarOff = kQKOff + 4 * kTileB;
-constexpr int kMaxTableUsers = 1024;  // B + 1 entries of uts and row_offsets staged in smem when B < this
 
 struct TABars {
     uint64_t qk_full[2], qk_empty[2];
@@ -70,7 +69,6 @@ struct TABars {
     uint64_t ml_full, ml_empty;  // the row statistics of tile t, softmax -> epilogue
     uint32_t tmem_base, pad;
     float st[3][128];  // per row: 1 / l, p_self / l, lse
-    int64_t uts[kMaxTableUsers], roff[kMaxTableUsers];
 };
 constexpr int kSmem = kBarOff + (int)sizeof(TABars) + 1024;
 static_assert(kSmem <= 232448, "shared memory");
@@ -150,18 +148,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
-    const bool staged = P.B < kMaxTableUsers;
-    if (staged)
-        for (int i = threadIdx.x; i <= P.B; i += kThreads) {
-            bars->uts[i] = __ldg(P.uts + i);
-            bars->roff[i] = __ldg(P.row_offsets + i);
-        }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = bars->tmem_base;
-    const int64_t* uts = staged ? bars->uts : P.uts;
-    const int64_t* roff = staged ? bars->roff : P.row_offsets;
+    const int64_t* uts = P.uts;
+    const int64_t* roff = P.row_offsets;
     const uint32_t tS = tmem, tP = tmem + 256, tO = tmem + 384;
     const int H = P.H;
     ItemIter iter;

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
 
     ItemIter iter;
-    iter.init(P.uts, P.B, HG, cta, num_ctas);
+    iter.init(P.uts, P.B, HG, cta, num_ctas, true);  // every role walks with full warps
     Item it;
     if (warp == 0) {
         // ---------------- TMA producer: q tiles (+ k_self, v_self tiles); W_u per unit

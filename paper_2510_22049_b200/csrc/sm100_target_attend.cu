@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tS = tmem, tP = tmem + 256, tO = tmem + 384;
     const int H = P.H;
     ItemIter iter;
-    iter.init(uts, P.B, H, blockIdx.x, gridDim.x);
+    iter.init(uts, P.B, H, blockIdx.x, gridDim.x, true);  // every role walks with full warps
     Item it;
     if (warp == 0) {
         // ============================ TMA producer ============================

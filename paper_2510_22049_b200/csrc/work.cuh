@@ -36,6 +36,26 @@ __device__ __forceinline__ int user_of_tile(const int64_t* uts, int B, int HG, i
     return lo;
 }
 
+// The same search by a whole warp (all 32 lanes, converged): 32 probes per round, so B <= 1024
+// users take two dependent loads instead of log2(B) -- the first item of a persistent CTA is on its
+// start-up path.  Requires uts non-decreasing and uts[0] = 0.
+__device__ __forceinline__ int user_of_tile_w(const int64_t* uts, int B, int HG, int t) {
+    const int lane = threadIdx.x & 31;
+    int lo = 0, hi = B - 1;  // invariant: HG * uts[lo] <= t; the answer is in [lo, hi]
+    while (hi - lo >= 32) {
+        const int step = (hi - lo + 32) / 32;
+        const int pos = min(lo + lane * step, hi);
+        const unsigned m = __ballot_sync(0xffffffffu, HG * (int)uts[pos] <= t);
+        const int k = 31 - __clz(m);  // last probe that holds (lane 0 always does)
+        const int nlo = min(lo + k * step, hi);
+        hi = k < 31 ? min(lo + (k + 1) * step - 1, hi) : hi;
+        lo = nlo;
+    }
+    const int pos = lo + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, pos <= hi && HG * (int)uts[min(pos, hi)] <= t);
+    return lo + 31 - __clz(m);
+}
+
 struct ItemIter {
     // Tile counts fit in 32 bits: sum L < 2^31 (TMA coordinates), so HG * sum T < 2^30.
     // One binary search at the first item; afterwards the walk advances user by user (a CTA's
@@ -43,18 +63,20 @@ struct ItemIter {
     // uts / B / HG come from the kernel parameters at every call (no registers held for them).
     int t, end;
     int u, base, Tu;  // current user (-1 before the first item), its first flat tile, tiles per unit
+    bool wsearch;     // every call is made by a full, converged warp: warp-wide first search
 
-    __device__ void init(const int64_t* uts, int B, int HG, int cta, int num_ctas) {
+    __device__ void init(const int64_t* uts, int B, int HG, int cta, int num_ctas, bool warp_wide = false) {
         const int T = HG * (int)uts[B];
         t = (int)(((unsigned long long)cta * (unsigned)T) / (unsigned)num_ctas);
         end = (int)(((unsigned long long)(cta + 1) * (unsigned)T) / (unsigned)num_ctas);
         u = -1;
+        wsearch = warp_wide;
     }
     __device__ bool next(Item& it, const int64_t* uts, int B, int HG) {
         if (t >= end) return false;
         it.first = u < 0;
         if (u < 0) {
-            u = user_of_tile(uts, B, HG, t);
+            u = wsearch ? user_of_tile_w(uts, B, HG, t) : user_of_tile(uts, B, HG, t);
             const int a = (int)uts[u];
             base = HG * a;
             Tu = (int)uts[u + 1] - a;

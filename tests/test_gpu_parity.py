@@ -1135,3 +1135,64 @@ def test_softmax_cta_pair_mode(cuda_lib):
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_target_attend_c2_full_size_sampled_users(cuda_lib):
+    """Stage 2 in the launch configuration bench.py --stage2 times (c2: 64 users x 256 int8 summary
+    tokens, H = 4, 256 candidates per user, bf16): the whole batch on the GPU, the oracle on sampled
+    users (candidates never see another user's tokens, so a user's block is checked alone)."""
+    vista = cuda_lib
+    B, S, H, d, cpu = 64, 256, 4, 128, 256
+    g = torch.Generator(device="cuda")
+    g.manual_seed(2024)
+    codes = torch.randint(-127, 128, (B, S, H, d), device="cuda", generator=g, dtype=torch.int8)
+    sc = (torch.randint(1, 64, (B, S, H), device="cuda", generator=g).float() / 1024.0)
+    zp = (torch.randint(-64, 64, (B, S, H), device="cuda", generator=g).float() / 128.0)
+    R = B * cpu
+    grid = lambda: (torch.randint(-128, 128, (R, H, d), device="cuda", generator=g).float() / 64).to(torch.bfloat16)  # noqa
+    cq, ck, cv = grid(), grid(), grid()
+    roff = torch.arange(B + 1, dtype=torch.int64, device="cuda") * cpu
+    o, l = vista.target_attend(codes, sc, zp, cq, ck, cv, roff, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    for u in (0, 17, 63):
+        a, b = u * cpu, (u + 1) * cpu
+        ref, rl = oracle.target_attend(codes[u:u + 1].cpu().numpy(), sc[u:u + 1].cpu().numpy(),
+                                       zp[u:u + 1].cpu().numpy(), cq[a:b].float().cpu().numpy(),
+                                       ck[a:b].float().cpu().numpy(), cv[a:b].float().cpu().numpy(), [0, cpu])
+        go, gl = o[a:b].cpu().numpy(), l[a:b].cpu().numpy()
+        for h in range(H):
+            assert block_err(go[:, h], ref[:, h]) <= 2e-2, f"user {u} head {h}"
+        # lse: the bf16 rounding of the dequantized tokens bounds the logit error (|q|_1 max|t| 2^-8 / sqrt(d))
+        tmax = (np.abs(codes[u].float().cpu().numpy()) * sc[u].cpu().numpy()[..., None]
+                + np.abs(zp[u].cpu().numpy())[..., None]).max()
+        bound = np.abs(cq[a:b].float().cpu().numpy()).sum(-1) * tmax * 2.0 ** -8 / np.sqrt(d) + 1e-3
+        assert np.all(np.abs(gl - rl) <= bound)
+
+
+@pytest.mark.gpu
+def test_summarize_layers_c2_full_size_sampled_users(cuda_lib):
+    """Two summarizer layers in the launch configuration bench.py --layers times (c2: 64 users x
+    [256 seeds; 10,000 items], D = 512, CTA-pair projection GEMMs): the whole batch on the GPU, the
+    oracle on sampled users (layers never mix users: a user's segment is checked alone)."""
+    vista = cuda_lib
+    B, S, H, d, L, n_layers = 64, 256, 4, 128, 10000, 2
+    D = H * d
+    off = np.arange(B + 1, dtype=np.int64) * (S + L)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    x = (torch.randint(-128, 128, (int(off[-1]), D), device="cuda", generator=g).float() / 64).to(torch.bfloat16)
+    W = (torch.randint(-128, 128, (n_layers, 5, D, D), device="cuda", generator=g).float()
+         / (128.0 * np.sqrt(D))).to(torch.bfloat16)
+    samples = (0, 41)
+    x_in = {u: x[off[u]:off[u + 1]].float().cpu().numpy() for u in samples}
+    tok = vista.summarize_layers(x, torch.from_numpy(off).cuda(), W, S, H, out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    W_bf = W.float().cpu().numpy()
+    for u in samples:
+        ref = oracle.summarize_layers(x_in[u], [0, S + L], W_bf, S, H)
+        gx = x[off[u]:off[u + 1]].float().cpu().numpy()
+        for h in range(H):
+            c = slice(h * d, (h + 1) * d)
+            assert block_err(gx[:, c], ref[:, c]) <= 2e-2, f"user {u} head {h}"
+            assert block_err(tok[u, :, h].cpu().numpy(), ref[:S, c]) <= 2e-2

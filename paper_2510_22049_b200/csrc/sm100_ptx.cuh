@@ -86,19 +86,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     for (int i = 0; i < VISTA_WAIT_SPIN; ++i)
         if (mbar_test_wait(bar, parity)) return;
 #endif
-#if defined(VISTA_WAIT_ASM)  // spin inside one asm block (no watchdog)
-    asm volatile(
-        "{\n\t.reg .pred P;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-        "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-#else
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
     while (!mbar_try_wait(bar, parity)) {
         if (globaltimer_ns() - t0 > 4000000000ull) __trap();
     }
-#endif
 }
 
 // ------------------------------------------------------------------ TMA

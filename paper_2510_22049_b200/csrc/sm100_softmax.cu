@@ -78,11 +78,6 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kKStages = VISTA_KSTAGES, kVStages = VISTA_VSTAGES;
 // CTA-pair mode (cta_group::2): a stage holds this CTA's half of a tile (K: 64 keys x 128
 // channels, V: 128 keys x 64 channels), so the same 160 KB of rings hold more stages
-#ifdef VISTA_Q_TMEM
-constexpr bool kQTmem = true;  // Q in TMEM (A operand of the score GEMM), P over the S columns
-#else
-constexpr bool kQTmem = false;
-#endif
 constexpr int kPairBytes = kTileBytes / 2;
 constexpr int kPairKStages = 6, kPairVStages = 4;
 constexpr int kMaxStages = 6;
@@ -118,7 +113,6 @@ struct ItemEntry {
 struct Bars {
     uint64_t it_full[kItemRing], it_empty[kItemRing];
     uint64_t q_full, q_empty;  // the item's Q tile in smem / its last S done
-    uint64_t qt_full[2], qt_empty[2];  // Q-in-TMEM variant: Q of item k in TMEM buffer k % 2
     uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages];
     uint64_t s_full[2], s_free[2];  // S(g) in buffer g % 2 complete / loaded by both softmax halves
     uint64_t p_full[2], p_free[2];  // P(g) in buffer g % 2 written (256 arrivals) / read by PV(g)
@@ -145,8 +139,6 @@ struct Params {
     int B, S, H, G;  // G: units (groups of C*128 rows) per head
     float scale_log2;
     int q_per_user;
-    const __nv_bfloat16* q;  // Q-in-TMEM variant: the seed rows, loaded by the epilogue warps
-    int64_t q_user_stride;
     int groups;  // > 1: query-group-major work order (ItemIterG; the G groups of a unit run side by side)
     int out_v8, slot_v8;  // outputs / slots 32-B aligned: 256-bit stores
 };
@@ -326,47 +318,6 @@ __device__ __forceinline__ float exp_half(const uint32_t (&r)[2][32], float sl2,
     return (la + lb) + (lc + ld);
 }
 
-// The same exponentials into registers (pk: the bf16x2 P words of this thread's 64 keys); the
-// caller stores them once the exponent offset is known to stand.
-__device__ __forceinline__ float exp_regs(const uint32_t (&r)[2][32], float sl2, float neg, uint32_t (&pk)[2][16]) {
-    const uint64_t sl2x2 = ptx::f2_pack(sl2, sl2);
-    const uint64_t negx2 = ptx::f2_pack(neg, neg);
-    uint64_t acc[2] = {ptx::f2_pack(0.f, 0.f), ptx::f2_pack(0.f, 0.f)};
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint64_t x2 = ptx::f2_fma(
-                ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
-            float x0, x1;
-            ptx::f2_unpack(x2, x0, x1);
-            const uint64_t p2 = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
-            acc[j & 1] = ptx::f2_add(acc[j & 1], p2);
-            float p0, p1;
-            ptx::f2_unpack(p2, p0, p1);
-            pk[c][j] = ptx::pack_bf16x2(p0, p1);
-        }
-    float la, lb, lc, ld;
-    ptx::f2_unpack(acc[0], la, lb);
-    ptx::f2_unpack(acc[1], lc, ld);
-    return (la + lb) + (lc + ld);
-}
-
-// max of this thread's 64 raw scores (4 independent FMNMX3 chains), then with the row's other thread
-__device__ __forceinline__ float row_max(const uint32_t (&r)[2][32]) {
-    float m4[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int c = a >> 1, o = (a & 1) * 16;
-        float m = ptx::max3(__uint_as_float(r[c][o]), __uint_as_float(r[c][o + 1]), __uint_as_float(r[c][o + 2]));
-#pragma unroll
-        for (int j = 3; j < 15; j += 2) m = ptx::max3(m, __uint_as_float(r[c][o + j]), __uint_as_float(r[c][o + j + 1]));
-        m4[a] = fmaxf(m, __uint_as_float(r[c][o + 15]));
-    }
-    const float mh = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-    return fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, 16));
-}
-
 // ---- MMA issue with compile-time geometry (descriptors stay in uniform registers) ----
 template <int KS>
 __device__ __forceinline__ void issue_S_t(uint32_t tS, uint32_t sQa, uint32_t sKa) {
@@ -387,24 +338,6 @@ __device__ __forceinline__ void issue_PV_t(uint32_t tO, uint32_t tP, uint32_t sV
     for (int kk = 0; kk < 8; ++kk)
         ptx::mma_ts_w(tO, tP + kk * 8, ptx::sdesc_sw128(sVa + VS * kTileBytes + kk * 2048, kHalfBytes, 1024), idP,
                       (acc || kk > 0) ? 1u : 0u);
-}
-template <int KS>
-__device__ __forceinline__ void issue_S_tq_t(uint32_t tS, uint32_t tQ, uint32_t sKa) {
-    // S = Q K^T with Q from TMEM (A operand, 8 columns per 16 channels) and K from stage KS
-    constexpr uint32_t idS = ptx::idesc_bf16_f32(128, 128, 0, 0);
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
-        ptx::mma_ts_w(tS, tQ + kk * 8,
-                      ptx::sdesc_sw128(sKa + KS * kTileBytes + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024), idS,
-                      kk > 0 ? 1u : 0u);
-}
-__device__ __forceinline__ void issue_S_tq(int ks, uint32_t tS, uint32_t tQ, uint32_t sKa) {
-    switch (ks) {
-        case 0: issue_S_tq_t<0>(tS, tQ, sKa); break;
-        case 1: issue_S_tq_t<1 % kKStages>(tS, tQ, sKa); break;
-        case 2: issue_S_tq_t<2 % kKStages>(tS, tQ, sKa); break;
-        default: issue_S_tq_t<3 % kKStages>(tS, tQ, sKa); break;
-    }
 }
 __device__ __forceinline__ void issue_S(int ks, uint32_t tS, uint32_t sQa, uint32_t sKa) {
     switch (ks) {
@@ -491,9 +424,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(!PAIR || C == 2, "a CTA pair is a cluster of two");
     constexpr uint16_t kMask = (uint16_t)((1u << C) - 1u);
     constexpr int KST = PAIR ? kPairKStages : kKStages, VST = PAIR ? kPairVStages : kVStages;
-    // Q-in-TMEM variant: TMEM S_0 [0,128) S_1 [128,256) O [256,384) Q_0 [384,448) Q_1 [448,512); P(g)
-    // over the first 64 columns of S buffer g % 2; the epilogue warps load each item's Q rows
-    constexpr bool QT = kQTmem && !PAIR;
     constexpr int kSlice = 128 / C;  // K/V rows this CTA loads (and multicasts) per tile
     constexpr int kRows = C * 128;   // query rows per unit
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -532,10 +462,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bars->s_free[b], PAIR ? 16 : 256);
             ptx::mbar_init(&bars->p_full[b], PAIR ? 16 : 256);
             ptx::mbar_init(&bars->p_free[b], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&bars->qt_full[b], 128);
-            ptx::mbar_init(&bars->qt_empty[b], 1);
         }
         ptx::mbar_init(&bars->pv_done, 1);
         ptx::mbar_init(&bars->o_full, 1);
@@ -607,10 +533,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!ok) break;
                 row0 = __shfl_sync(0xffffffffu, row0, 0);
                 const int h = it.hg / P.G, g = it.hg % P.G;
-                if (!QT && k >= 1) ptx::mbar_wait(&bars->q_empty, (uint32_t)(k - 1) & 1u);  // previous item's S done
+                if (k >= 1) ptx::mbar_wait(&bars->q_empty, (uint32_t)(k - 1) & 1u);  // previous item's S done
                 if (lane == 0) VTRACE(17, k);
-                if constexpr (QT) {
-                } else if constexpr (PAIR) {
+                if constexpr (PAIR) {
                     // this CTA's Q rows; completion on the leader's q_full (armed for both CTAs)
                     const uint32_t qf = ptx::mapa(ptx::smem_u32(&bars->q_full), 0);
                     if (rank == 0) ptx::mbar_arrive_expect_tx_w(&bars->q_full, 2 * kTileBytes);
@@ -692,14 +617,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             int kst = 0, g = 0;
             uint32_t kph = 0;
             for (int k = 0; fetch_item(bars, ring, k, it); ++k) {
-                if constexpr (QT) ptx::mbar_wait(&bars->qt_full[k & 1], (uint32_t)(k >> 1) & 1u);
-                else ptx::mbar_wait(&bars->q_full, (uint32_t)k & 1u);
+                ptx::mbar_wait(&bars->q_full, (uint32_t)k & 1u);
                 VTRACE(16, k);
                 for (int t = it.t0; t < it.t1; ++t, ++g) {
                     const int b = g & 1;
                     if (g >= 2) ptx::mbar_wait(&bars->s_free[b], (uint32_t)((g >> 1) - 1) & 1u);
-                    // Q-in-TMEM: P(g - 2) lives in S buffer b until PV(g - 2) has read it
-                    if (QT && g >= 2) ptx::mbar_wait(&bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
                     VTRACE(7, g);
                     ptx::mbar_wait(&bars->k_full[kst], kph);
                     VTRACE(8, g);
@@ -710,15 +632,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mma2_commit_mc_w(&bars->k_empty[kst]);
                         if (t == it.t1 - 1) ptx::mma2_commit_mc_w(&bars->q_empty);
                     } else {
-                        if constexpr (QT) issue_S_tq(kst, tmem + b * 128, tmem + 384 + (k & 1) * 64, sKa);
-                        else issue_S(kst, tmem + b * 128, sQa, sKa);
+                        issue_S(kst, tmem + b * 128, sQa, sKa);
                         ptx::mma_commit_w(&bars->s_full[b]);
                         if constexpr (C > 1) ptx::mma_commit_mc_w(&bars->k_empty[kst], kMask);
                         else ptx::mma_commit_w(&bars->k_empty[kst]);
-                        if (t == it.t1 - 1) {  // Q free once its last S completes
-                            if constexpr (QT) ptx::mma_commit_w(&bars->qt_empty[k & 1]);
-                            else ptx::mma_commit_w(&bars->q_empty);
-                        }
+                        if (t == it.t1 - 1) ptx::mma_commit_w(&bars->q_empty);  // Q free once its last S completes
                     }
                     VTRACE(0, g);
                     if (++kst == KST) { kst = 0; kph ^= 1; }
@@ -748,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mma2_commit_mc_w(&bars->v_empty[vst]);
                         if (t == it.t1 - 1) ptx::mma2_commit_mc_w(&bars->o_full);
                     } else {
-                        issue_PV(vst, tmem + 256, QT ? tmem + b * 128 : tmem + 384 + b * 64, sVa, t > it.t0);
+                        issue_PV(vst, tmem + 256, tmem + 384 + b * 64, sVa, t > it.t0);
                         ptx::mma_commit_w(&bars->p_free[b]);
                         ptx::mma_commit_w(&bars->pv_done);
                         if constexpr (C > 1) ptx::mma_commit_mc_w(&bars->v_empty[vst], kMask);
@@ -777,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = it.t0; t < it.t1; ++t, ++g) {
                 const int b = g & 1;
                 const uint32_t tS = tmem + lane_bits + b * 128;
-                const uint32_t tP = QT ? tmem + lane_bits + b * 128 : tmem + lane_bits + 384 + b * 64;
+                const uint32_t tP = tmem + lane_bits + 384 + b * 64;
                 if (row == 0 && ch == 0) {
                     VTRACE(26, g);
                     VPROBE(0, g, &bars->s_full[b], (uint32_t)(g >> 1) & 1u);
@@ -803,39 +721,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 32; ++j)
                             if (c * 32 + j >= valid) r[c][j] = __float_as_uint(-INFINITY);
                 }
-#ifdef VISTA_SPEC_MAX
-                // Speculative offset: past an item's first tile the exponentials run with the running
-                // offset m_used while the row max is computed alongside (independent instructions the
-                // scheduler interleaves with the MUFU ops, so the max leaves the critical path).  Only
-                // when a row max exceeds m_used + 8 (p > 2^8, rare once the first tiles have set the
-                // offset) are they redone with the new offset, before any P is stored.
-                if (g >= 2) {
-                    if (row == 0 && ch == 0) {
-                        VTRACE(27, g);
-                        VPROBE(1, g, &bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
-                    }
-                    ptx::mbar_wait(&bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
-                }
-                if (row == 0 && ch == 0) VTRACE(14, g);
-                uint32_t pk[2][16];
-                float lt = 0.f;
-                const bool spec = t > it.t0;
-                if (spec) lt = exp_regs(r, sl2, -m_used, pk);
-                const float mxs = row_max(r) * sl2;
-                if (row == 0 && ch == 0) VTRACE(13, g);
-                const bool need = mxs > m_used + kRescaleThreshold;
-                const bool any = __any_sync(0xffffffffu, need);
-                const float m_old = m_used;
-                if (any) {
-                    m_used = fmaxf(m_used, mxs);
-                    lt = exp_regs(r, sl2, -m_used, pk);
-                }
-                ptx::tc_fence_after();
-                if (lane == 0 && wq == 0) VTRACE(22 + 2 * rh, g);
-                ptx::tmem_st16x32bx2_x16<32>(tP, pk[0]);
-                ptx::tmem_st16x32bx2_x16<32>(tP + 16, pk[1]);
-                if (lane == 0 && wq == 0) VTRACE(23 + 2 * rh, g);
-#else
                 // row max: 4 independent FMNMX3 chains over this thread's keys, then the row's other thread
                 float m4[4];
 #pragma unroll
@@ -861,14 +746,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     VTRACE(27, g);
                     VPROBE(1, g, &bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
                 }
-                // (Q-in-TMEM: S(g) in buffer b was issued after PV(g - 2) completed)
-                if (!QT && g >= 2) ptx::mbar_wait(&bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
+                if (g >= 2) ptx::mbar_wait(&bars->p_free[b], (uint32_t)((g >> 1) - 1) & 1u);
                 if (row == 0 && ch == 0) VTRACE(14, g);
                 ptx::tc_fence_after();
                 if (lane == 0 && wq == 0) VTRACE(22 + 2 * rh, g);
                 const float lt = exp_half(r, sl2, -m_used, tP);
                 if (lane == 0 && wq == 0) VTRACE(23 + 2 * rh, g);
-#endif
                 if (any && t > it.t0) {
                     // O holds this item's sum up to PV(g - 1): wait for it, then rescale this row's
                     // 128 columns in place, 64 per thread (PV(g) cannot start before the p_full arrive)
@@ -912,38 +795,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = wq * 32 + lane;
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
         const uint32_t tO = tmem + lane_bits + 256;
-        // Q-in-TMEM: this thread's seed row of item kk into TMEM buffer kk % 2 (64 columns)
-        auto load_q = [&](const Item& qi, int kk) {
-            const int h = qi.hg / P.G, gq = qi.hg % P.G;
-            const uint4* src = reinterpret_cast<const uint4*>(
-                P.q + (P.q_per_user ? (size_t)qi.u * (size_t)P.q_user_stride : 0) +
-                ((size_t)(gq * kRows + rank * 128 + row) * P.H + h) * 128);
-            uint32_t w[2][32];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const uint4 x = __ldg(src + c);
-                w[c >> 3][(c & 7) * 4 + 0] = x.x;
-                w[c >> 3][(c & 7) * 4 + 1] = x.y;
-                w[c >> 3][(c & 7) * 4 + 2] = x.z;
-                w[c >> 3][(c & 7) * 4 + 3] = x.w;
-            }
-            const uint32_t tQ = tmem + lane_bits + 384 + (kk & 1) * 64;
-            ptx::tmem_st32(tQ, w[0]);
-            ptx::tmem_st32(tQ + 32, w[1]);
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&bars->qt_full[kk & 1]);
-        };
         bool have = fetch_item(bars, ring, 0, it);
-        if (QT && have) load_q(it, 0);
         for (int k = 0; have; ++k) {
-            Item nxt;
+            Item nxt;  // the next item is fetched ahead (its ring entry is released early)
             const bool have_n = fetch_item(bars, ring, k + 1, nxt);
-            if (QT && have_n) {
-                // buffer (k + 1) % 2 is free once item k - 1's last score GEMM has completed
-                if (k >= 1) ptx::mbar_wait(&bars->qt_empty[(k + 1) & 1], (uint32_t)(((k + 1) >> 1) - 1) & 1u);
-                load_q(nxt, k + 1);
-            }
             ptx::mbar_wait(&bars->ml_full, (uint32_t)k & 1u);
             if (row == 0) VTRACE(20, k);
             const float lsum = bars->ml[0][row];
@@ -1125,8 +980,6 @@ static cudaError_t launch_c(const Problem& p, const Workspace& w, char* ws) {
     P.scale_log2 = p.scale * kLog2e;
     P.q_per_user = p.q_user_stride != 0;
     P.groups = (P.G > 1 && w.num_ctas % P.G == 0) ? P.G : 1;
-    P.q = reinterpret_cast<const __nv_bfloat16*>(p.q);
-    P.q_user_stride = p.q_user_stride;
     P.out_v8 = (reinterpret_cast<uintptr_t>(p.outs.out) & 31) == 0;
     P.slot_v8 = (reinterpret_cast<uintptr_t>(P.slot_o) & 31) == 0;
     const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_softmax_kernel<C, PAIR>), kSmem);

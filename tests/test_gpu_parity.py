@@ -1196,3 +1196,33 @@ def test_summarize_layers_c2_full_size_sampled_users(cuda_lib):
             c = slice(h * d, (h + 1) * d)
             assert block_err(gx[:, c], ref[:, c]) <= 2e-2, f"user {u} head {h}"
             assert block_err(tok[u, :, h].cpu().numpy(), ref[:S, c]) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_qla_target_rows_from_state_c2_full_size_sampled_users(cuda_lib):
+    """QLA target rows with the Delta term (NEXT-4) in the launch configuration bench.py --qla-rows
+    target times: the c2 states from vista_summarize_partial (QLA), then 256 target rows per user
+    through vista_qla_rows_from_state (double-buffered W_u, v_self from global); sampled users vs the
+    oracle computed from the users' full histories."""
+    vista = cuda_lib
+    lens, S, H, d, q, K, V, off = _c2_full()
+    B = len(lens)
+    ot = torch.from_numpy(off).cuda()
+    z, _ = vista.summarize_partial(q, K, V, ot, int(off[-1]), attn=vista.QLA)
+    rpu = 256
+    roff = np.arange(B + 1, dtype=np.int64) * rpu
+    rng = np.random.default_rng(13)
+    qr, kr, vr = [((rng.integers(-128, 128, size=(B * rpu, H, d)) / 64.0)).astype(np.float32) for _ in range(3)]
+    ulen = torch.from_numpy(np.asarray(lens, dtype=np.int64)).cuda()
+    dev = lambda a: torch.from_numpy(a).cuda().to(torch.bfloat16)  # noqa: E731
+    out = vista.qla_rows_from_state(z, ulen, dev(qr), torch.from_numpy(roff).cuda(), B * rpu, k_self=dev(kr),
+                                    v_self=dev(vr), out_dtype=vista.F32)
+    torch.cuda.synchronize()
+    for u in (0, 33, 63):
+        a, b = int(off[u]), int(off[u + 1])
+        ra, rb = int(roff[u]), int(roff[u + 1])
+        ref = oracle.qla_rows(qr[ra:rb], [0, rpu], K[a:b].float().cpu().numpy(), V[a:b].float().cpu().numpy(),
+                              [0, b - a], k_self=kr[ra:rb], v_self=vr[ra:rb])
+        go = out[ra:rb].cpu().numpy()
+        for h in range(H):
+            assert block_err(go[:, h], ref[:, h]) <= 2e-2, f"user {u} head {h}"

@@ -329,11 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const int j = 4 * q + e;
-                            float f, d0, d1;
+                            float d0, d1;
                             if constexpr (kKp) {  // phi1'(k) (bf16) from the transform
                                 d0 = __uint_as_float(kw[e] << 16);
                                 d1 = __uint_as_float(kw[e] & 0xFFFF0000u);
                             } else {
+                                float f;  // phi1(k): not needed here
                                 phi_and_prime<PHI1>(__uint_as_float(kw[e] << 16), f, d0);
                                 phi_and_prime<PHI1>(__uint_as_float(kw[e] & 0xFFFF0000u), f, d1);
                             }

@@ -221,6 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
+    // PDL: the prologue above overlapped the tile scan; its results (uts) and everything before it
+    // on the stream are visible after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     ItemIter iter;
     iter.init(P.uts, P.B, HG, cta, num_ctas, true);  // every role walks with full warps
@@ -420,8 +423,9 @@ cudaError_t launch_phi(const Problem& p, const CUtensorMap& mq, const CUtensorMa
     using G = Geo<DELTA>;
     const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_rows_kernel<PHI1, DELTA>), G::kSmem);
     if (attr != cudaSuccess) return attr;
-    sm100_qla_rows_kernel<PHI1, DELTA><<<p.num_sms, kThreads, G::kSmem, p.stream>>>(mq, mk, mv, P);
-    return cudaGetLastError();
+    // PDL: the prologue overlaps the tile scan launched just before (griddepcontrol.wait in the kernel)
+    return launch_pdl(sm100_qla_rows_kernel<PHI1, DELTA>, dim3(p.num_sms), dim3(kThreads), G::kSmem, p.stream, mq, mk,
+                      mv, P);
 }
 
 // ---------------------------------------------------------------- SIMT: one block per (row, head)

@@ -151,6 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    // PDL: the prologue above overlapped the tile scan; its results (uts) and everything before it
+    // on the stream are visible after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t tmem = bars->tmem_base;
     const int64_t* uts = P.uts;
     const int64_t* roff = P.row_offsets;
@@ -537,9 +540,10 @@ cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offs
                                 : reinterpret_cast<const void*>(sm100_target_attend_kernel<128>);
     const cudaError_t attr = set_smem_attr(fn, kSmem);
     if (attr != cudaSuccess) return attr;
-    if (p.S == 256) sm100_target_attend_kernel<256><<<p.num_sms, kThreads, kSmem, p.stream>>>(mq, mk, mv, P);
-    else sm100_target_attend_kernel<128><<<p.num_sms, kThreads, kSmem, p.stream>>>(mq, mk, mv, P);
-    return cudaGetLastError();
+    // PDL: the prologue overlaps the tile scan launched just before (griddepcontrol.wait in the kernel)
+    if (p.S == 256)
+        return launch_pdl(sm100_target_attend_kernel<256>, dim3(p.num_sms), dim3(kThreads), kSmem, p.stream, mq, mk, mv, P);
+    return launch_pdl(sm100_target_attend_kernel<128>, dim3(p.num_sms), dim3(kThreads), kSmem, p.stream, mq, mk, mv, P);
 }
 
 #ifdef VISTA_TRACE

@@ -349,6 +349,8 @@ __global__ void merge_qla_slots_kernel(const int* __restrict__ slot_unit, int nu
 __global__ void merge_qla_slots_w_kernel(const int* __restrict__ slot_unit, int num_slots, const float* __restrict__ slot_o,
                                          const int64_t* __restrict__ offsets, int H, int phi2, int normalize,
                                          uint8_t* __restrict__ wbuf) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the state kernel's slots are complete
+    asm volatile("griddepcontrol.launch_dependents;");
     const int s = blockIdx.x;
     const int n = slot_unit[s];
     if (n < 0 || !slot_is_head(slot_unit, s, n)) return;
@@ -771,10 +773,9 @@ cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, cha
 cudaError_t launch_merge_qla_slots_w(const Problem& p, const Workspace& w, char* ws, uint8_t* wbuf) {
     const int num_slots = 2 * w.num_ctas;
     dim3 grid(num_slots, 128 / 8);
-    merge_qla_slots_w_kernel<<<grid, 256, 0, p.stream>>>(reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots,
-                                                         reinterpret_cast<const float*>(ws + w.slot_o_off), p.offsets,
-                                                         p.H, p.phi2, p.normalize, wbuf);
-    return cudaGetLastError();
+    return launch_pdl(merge_qla_slots_w_kernel, grid, dim3(256), 0, p.stream,
+                      reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots,
+                      reinterpret_cast<const float*>(ws + w.slot_o_off), p.offsets, p.H, p.phi2, p.normalize, wbuf);
 }
 
 cudaError_t launch_merge_qla_slots(const Problem& p, const Workspace& w, char* ws, float* zbuf) {

@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, kTmemCols);
     ptx::tc_fence_before();
     __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;");  // PDL: the slot merge may start its prologue
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, bars->tmem_base, 0);
 

@@ -77,6 +77,11 @@ __global__ void __launch_bounds__(256) qla_prep_q_kernel(const __nv_bfloat16* __
         }
         *reinterpret_cast<uint4*>(dst + swz(r, cc)) = pk;
     }
+    // PDL (fused path): this kernel needs nothing from its predecessor (the slot merge) and may run
+    // beside it, but the finalize after it relies on this grid's completion implying the merge's:
+    // let the finalize start its prologue, then wait for the merge before completing
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // One CTA per (128 query rows, user, head): bulk-copy the two prepared operands, one 128x128x128
@@ -107,6 +112,7 @@ __global__ void __launch_bounds__(128) sm100_qla_finalize_kernel(const uint8_t* 
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_slot, 0);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: W and phi1(Q) are complete after this
     if (empty) {  // W = phi2(0) everywhere (a constant: layout-free)
         uint8_t* sm = smem_raw + (base - ptx::smem_u32(smem_raw));
         const uint32_t c2 = ptx::pack_bf16x2(act(phi2, 0.f), act(phi2, 0.f));
@@ -203,15 +209,16 @@ cudaError_t launch_sm100_qla_finalize_fused(const Problem& p, uint8_t* ws) {
     const int bq = p.q_user_stride ? p.B : 1;
     uint8_t* wbuf = ws;
     uint8_t* abuf = wbuf + (size_t)p.B * p.H * kOp;
-    qla_prep_q_kernel<<<bq * p.H * nblk * 4, 256, 0, p.stream>>>(reinterpret_cast<const __nv_bfloat16*>(p.q),
-                                                                 p.q_user_stride, p.S, p.H, p.phi1, abuf);
+    // both with PDL: phi1(Q) runs beside the slot merge, the finalize's prologue beside phi1(Q)
+    cudaError_t e = launch_pdl(qla_prep_q_kernel, dim3(bq * p.H * nblk * 4), dim3(256), 0, p.stream,
+                               reinterpret_cast<const __nv_bfloat16*>(p.q), p.q_user_stride, p.S, p.H, p.phi1, abuf);
+    if (e != cudaSuccess) return e;
     const int smem = 2 * kOp + 1024;
     const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_finalize_kernel), smem);
     if (attr != cudaSuccess) return attr;
     dim3 grid(nblk, p.B * p.H);
-    sm100_qla_finalize_kernel<<<grid, 128, smem, p.stream>>>(abuf, wbuf, p.q_user_stride != 0, p.S, p.H, p.outs,
-                                                             p.offsets, p.phi2);
-    return cudaGetLastError();
+    return launch_pdl(sm100_qla_finalize_kernel, grid, dim3(128), smem, p.stream, (const uint8_t*)abuf,
+                      (const uint8_t*)wbuf, (int)(p.q_user_stride != 0), p.S, p.H, p.outs, p.offsets, p.phi2);
 }
 
 size_t qla_prep_q_bytes(const Problem& p) {

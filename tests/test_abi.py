@@ -111,6 +111,44 @@ def test_qla_rows_and_bwd_validation_before_launch(lib):
         assert vista.vista_summarize_bwd_workspace_size(desc, 100) > 0
 
 
+def test_layers_stage2_rows_from_state_validation_before_launch(lib):
+    """NEXT-3 layers, NEXT-4 stage 2 and rows from a saved state: argument errors are returned before
+    any launch (no GPU here)."""
+    import paper_2510_22049_b200 as vista
+    E = vista.VistaError
+    dl = vista.make_desc(2, 128, 1, 128, attn=vista.QLA)
+    need = vista.vista_summarize_layers_workspace_size(dl, 3, 1000)
+    assert need > 0
+    cases = [
+        (lambda: vista.vista_summarize_layers(dl, -1, 4096, 4096, 4096, 1000, 4096, 4096, need, stream=0), 2),  # layers < 0
+        (lambda: vista.vista_summarize_layers(vista.make_desc(2, 128, 1, 128), 3, 4096, 4096, 4096, 1000, 4096, 4096,
+                                              need, stream=0), 3),  # softmax form: the layers are QLA layers
+        (lambda: vista.vista_summarize_layers(dl, 3, 4096, 4096, 0, 1000, 4096, 4096, need, stream=0), 1),  # no offsets
+        (lambda: vista.vista_summarize_layers(dl, 3, 4096, 4104, 4096, 1000, 4096, 4096, need, stream=0), 4),  # misaligned x
+        (lambda: vista.vista_summarize_layers(dl, 3, 4096, 4096, 4096, 1000, 4096, 4096, 64, stream=0), 5),  # short workspace
+    ]
+    ds = vista.make_desc(2, 256, 1, 128)
+    ns = vista.vista_target_attend_workspace_size(ds, 512)
+    cases += [
+        (lambda: vista.vista_target_attend(ds, 4096, 4096, 4096, 4096, 4096, 4096, 0, 4096, -1, 4096, 0, 4096, ns, stream=0), 2),
+        (lambda: vista.vista_target_attend(ds, 4096, 4096, 4096, 4096, 4096, 4096, 0, 0, 512, 4096, 0, 4096, ns, stream=0), 1),
+        (lambda: vista.vista_target_attend(ds, 0, 4096, 4096, 4096, 4096, 4096, 0, 4096, 512, 4096, 0, 4096, ns, stream=0), 1),
+        (lambda: vista.vista_target_attend(ds, 4096, 4098, 4096, 4096, 4096, 4096, 0, 4096, 512, 4096, 0, 4096, ns, stream=0), 4),
+        (lambda: vista.vista_target_attend(ds, 4096, 4096, 4096, 4096, 4096, 4096, 0, 4096, 512, 4096, 0, 4096, 0, stream=0), 5),
+    ]
+    dq = vista.make_desc(2, 1, 1, 128, attn=vista.QLA)
+    nr = vista.vista_qla_rows_from_state_workspace_size(dq, 500)
+    cases += [
+        (lambda: vista.vista_qla_rows_from_state(dq, 0, 4096, 4096, 4096, 500, 0, 0, 4096, 4096, nr, stream=0), 1),  # no z
+        (lambda: vista.vista_qla_rows_from_state(dq, 4100, 4096, 4096, 4096, 500, 0, 0, 4096, 4096, nr, stream=0), 4),
+        (lambda: vista.vista_qla_rows_from_state(dq, 4096, 4096, 4096, 4096, 500, 0, 0, 4096, 4096, 1, stream=0), 5),
+    ]
+    for fn, status in cases:
+        with pytest.raises(E) as e:
+            fn()
+        assert e.value.status == status
+
+
 def test_dispatch_by_shape(lib):
     import paper_2510_22049_b200 as vista
     assert vista.vista_dispatch_name(vista.make_desc(8, 256, 4, 128)) == "sm100_softmax"

@@ -188,7 +188,7 @@ __device__ __forceinline__ void issue_tile_d(int stage, uint32_t tacc, uint32_t 
 template <int PHI1, bool DELTA>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_qla_rows_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
-                          const __grid_constant__ CUtensorMap mapV, const Params P) {
+                          const Params P) {
     using G = Geo<DELTA>;
     constexpr int kStages = G::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch(&mapQ);
         if constexpr (DELTA) {
             ptx::tma_prefetch(&mapK);
-            ptx::tma_prefetch(&mapV);
         }
         const uint64_t pol = ptx::policy_evict_first();
         int stage = 0;
@@ -418,14 +417,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int PHI1, bool DELTA>
-cudaError_t launch_phi(const Problem& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+cudaError_t launch_phi(const Problem& p, const CUtensorMap& mq, const CUtensorMap& mk,
                        const Params& P) {
     using G = Geo<DELTA>;
     const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_rows_kernel<PHI1, DELTA>), G::kSmem);
     if (attr != cudaSuccess) return attr;
     // PDL: the prologue overlaps the tile scan launched just before (griddepcontrol.wait in the kernel)
-    return launch_pdl(sm100_qla_rows_kernel<PHI1, DELTA>, dim3(p.num_sms), dim3(kThreads), G::kSmem, p.stream, mq, mk,
-                      mv, P);
+    return launch_pdl(sm100_qla_rows_kernel<PHI1, DELTA>, dim3(p.num_sms), dim3(kThreads), G::kSmem, p.stream, mq, mk, P);
 }
 
 // ---------------------------------------------------------------- SIMT: one block per (row, head)
@@ -487,12 +485,11 @@ bool qla_rows_uses_tc(const Problem& p, int64_t total_rows) {
 cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, int64_t total_rows, const int64_t* uts,
                                   const uint8_t* w_op, const void* q, const void* k_self, const void* v_self,
                                   int out_bf16, void* out, const int64_t* user_len, const void* gate) {
-    CUtensorMap mq, mk, mv;
+    CUtensorMap mq, mk;  // (v_self rows are read by the epilogue threads directly)
     if (!make_kv_map(&mq, q, total_rows, p.H)) return cudaErrorInvalidValue;
     const bool delta = k_self != nullptr;
-    if (delta && (!make_kv_map(&mk, k_self, total_rows, p.H) || !make_kv_map(&mv, v_self, total_rows, p.H)))
-        return cudaErrorInvalidValue;
-    if (!delta) mk = mv = mq;
+    if (delta && !make_kv_map(&mk, k_self, total_rows, p.H)) return cudaErrorInvalidValue;
+    if (!delta) mk = mq;
     Params P;
     P.row_offsets = row_offsets;
     P.uts = uts;
@@ -507,12 +504,12 @@ cudaError_t launch_sm100_qla_rows(const Problem& p, const int64_t* row_offsets, 
     P.B = p.B;
     P.H = p.H;
     if (delta)
-        return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU, true>(p, mq, mk, mv, P)
-             : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU, true>(p, mq, mk, mv, P)
-                                               : launch_phi<VISTA_ACT_IDENTITY, true>(p, mq, mk, mv, P);
-    return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU, false>(p, mq, mk, mv, P)
-         : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU, false>(p, mq, mk, mv, P)
-                                           : launch_phi<VISTA_ACT_IDENTITY, false>(p, mq, mk, mv, P);
+        return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU, true>(p, mq, mk, P)
+             : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU, true>(p, mq, mk, P)
+                                               : launch_phi<VISTA_ACT_IDENTITY, true>(p, mq, mk, P);
+    return p.phi1 == VISTA_ACT_SILU ? launch_phi<VISTA_ACT_SILU, false>(p, mq, mk, P)
+         : p.phi1 == VISTA_ACT_SHIFTED_ELU ? launch_phi<VISTA_ACT_SHIFTED_ELU, false>(p, mq, mk, P)
+                                           : launch_phi<VISTA_ACT_IDENTITY, false>(p, mq, mk, P);
 }
 
 cudaError_t launch_qla_rows_simt(const Problem& p, const float* z, const int64_t* row_offsets, int64_t total_rows,

@@ -123,7 +123,7 @@ __device__ __forceinline__ void issue_pv(uint32_t tO, uint32_t tP, uint32_t sT) 
 template <int NS>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_target_attend_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
-                               const __grid_constant__ CUtensorMap mapV, const TAParams P) {
+                               const TAParams P) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t base = ptx::smem_u32(smem);
@@ -517,9 +517,8 @@ cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offs
                                        const int64_t* uts, const int8_t* codes, const float* tscale, const float* tzp,
                                        const void* q, const void* k_self, const void* v_self, const void* resid,
                                        int out_bf16, void* out, float* lse) {
-    CUtensorMap mq, mk, mv;
-    if (!make_kv_map(&mq, q, total_rows, p.H) || !make_kv_map(&mk, k_self, total_rows, p.H) ||
-        !make_kv_map(&mv, v_self, total_rows, p.H))
+    CUtensorMap mq, mk;  // v_self rows are read by the epilogue threads directly
+    if (!make_kv_map(&mq, q, total_rows, p.H) || !make_kv_map(&mk, k_self, total_rows, p.H))
         return cudaErrorInvalidValue;
     TAParams P;
     P.row_offsets = row_offsets;
@@ -542,8 +541,8 @@ cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offs
     if (attr != cudaSuccess) return attr;
     // PDL: the prologue overlaps the tile scan launched just before (griddepcontrol.wait in the kernel)
     if (p.S == 256)
-        return launch_pdl(sm100_target_attend_kernel<256>, dim3(p.num_sms), dim3(kThreads), kSmem, p.stream, mq, mk, mv, P);
-    return launch_pdl(sm100_target_attend_kernel<128>, dim3(p.num_sms), dim3(kThreads), kSmem, p.stream, mq, mk, mv, P);
+        return launch_pdl(sm100_target_attend_kernel<256>, dim3(p.num_sms), dim3(kThreads), kSmem, p.stream, mq, mk, P);
+    return launch_pdl(sm100_target_attend_kernel<128>, dim3(p.num_sms), dim3(kThreads), kSmem, p.stream, mq, mk, P);
 }
 
 #ifdef VISTA_TRACE

@@ -171,15 +171,21 @@ __device__ __forceinline__ void out_store4(const OutSpec& o, int S, int H, int u
 // 4 rows, lanes over 128 channels (float4); blocks whose slot does not start a run exit at once.
 // Warp 0 lists the run's slots (lane-parallel over 32 positions at a time: a run ends at the first
 // slot holding another unit, -1 slots are unused); then the members' 32-row slabs of o (16 KB
-// each, contiguous) and lse stream into shared memory by bulk copy, two members per stage,
-// double-buffered, and the rows are combined with an online max (any run length).
+// each, contiguous) and lse stream into shared memory by bulk copy, two members per group, and
+// the rows are combined with an online max (any run length).  One stage (33 KB of smem) keeps six
+// blocks per SM resident, so the split units of a step merge in one wave; runs longer than two
+// members (very long users) load their groups one after the other.
 constexpr int kMergeRows = 32;
 constexpr int kMergeMaxRun = 320;  // >= 2 * max CTAs a unit can span + 2
 static_assert(kMergeMaxRun >= 2 * kMaxPersistentCtas + 2, "merge run list");
+#ifndef VISTA_MERGE_STAGES
+#define VISTA_MERGE_STAGES 1
+#endif
+constexpr int kMergeStages = VISTA_MERGE_STAGES;
 struct MergeSmem {
-    float o[2][2][kMergeRows * 128];  // [stage][member][row * 128 + channel]
-    float lse[2][2][kMergeRows];
-    uint64_t full[2];
+    float o[kMergeStages][2][kMergeRows * 128];  // [stage][member][row * 128 + channel]
+    float lse[kMergeStages][2][kMergeRows];
+    uint64_t full[kMergeStages];
     int list[kMergeMaxRun];
     int count, n, head;
 };
@@ -231,8 +237,7 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
             sm.n = n;
             sm.head = head && row0 < rows;
             sm.count = count;
-            ptx::mbar_init(&sm.full[0], 1);
-            ptx::mbar_init(&sm.full[1], 1);
+            for (int st = 0; st < kMergeStages; ++st) ptx::mbar_init(&sm.full[st], 1);
             ptx::fence_mbar_init();
         }
     }
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
     const int n = sm.n, R = sm.count;
     const int ngroups = (R + 1) / 2;
     auto issue = [&](int gi) {  // thread 0: bulk copies of group gi (members 2 gi, 2 gi + 1)
-        const int st = gi & 1;
+        const int st = gi % kMergeStages;
         const int k = min(2, R - 2 * gi);
         ptx::mbar_arrive_expect_tx(&sm.full[st], (uint32_t)k * (kMergeRows * 128 * 4 + kMergeRows * 4));
         for (int j = 0; j < k; ++j) {
@@ -252,10 +257,8 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
                           &sm.full[st]);
         }
     };
-    if (threadIdx.x == 0) {
-        issue(0);
-        if (ngroups > 1) issue(1);
-    }
+    if (threadIdx.x == 0)
+        for (int gi = 0; gi < kMergeStages && gi < ngroups; ++gi) issue(gi);
     float M[4], l[4];
     float4 acc[4];
 #pragma unroll
@@ -265,9 +268,9 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
         acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     for (int gi = 0; gi < ngroups; ++gi) {
-        const int st = gi & 1;
+        const int st = gi % kMergeStages;
         const int k = min(2, R - 2 * gi);
-        ptx::mbar_wait(&sm.full[st], (uint32_t)(gi >> 1) & 1u);
+        ptx::mbar_wait(&sm.full[st], (uint32_t)(gi / kMergeStages) & 1u);
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int rl = warp * 4 + r;  // row within the block's 32
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
             M[r] = Mn;
         }
         __syncthreads();  // stage st free again
-        if (threadIdx.x == 0 && gi + 2 < ngroups) issue(gi + 2);
+        if (threadIdx.x == 0 && gi + kMergeStages < ngroups) issue(gi + kMergeStages);
     }
     const int HG = H * G;
     const int u = n / HG, hg = n % HG, h = hg / G, g = hg % G;

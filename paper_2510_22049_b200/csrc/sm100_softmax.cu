@@ -34,6 +34,8 @@
 //   warps 12-15 epilogue: O / l, lse, coalesced stores (+ fused int8 export)
 // Conditional rescale (threshold 2^8): the running max used for the exponent only moves when a
 // row max exceeds it by more than 8 (log2 units); otherwise p <= 256 and O is left alone.
+// Variant (VISTA_SOFTMAX_PAIR=1, clusters of two): a CTA pair issuing cta_group::2 MMAs (M = 256),
+// each SM holding half of every K and V tile; parity-green but slower at c2.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <math.h>

@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group for N > 1 (gloo: host-staged exchange; a dry run of the multi-rank "
                          "path when fewer GPUs than ranks are visible)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="by_length split-L exchange: NCCL all_gather (default) or peer-memory stores over NVLink "
+                         "(dist.PeerExchange, CUDA IPC; one node)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -344,18 +347,32 @@ def run_own(args, rank, world, local_rank):
         ulen = torch.from_numpy(np.asarray(lens, dtype=np.int64)).to(dev)
         inputs = [q, K, V, soff_t]
         if mode == "by_length":
+            acode = 0 if args.attn == "softmax" else 1
+            xchg = None
+            if args.exchange == "p2p":  # peer-memory exchange (CUDA IPC buffers, NVLink stores)
+                part_shape = (B_all, H, S, d) if acode == 0 else (B_all, H, d, d)
+                xchg = vdist.PeerExchange(part_shape, (B_all, H, S) if acode == 0 else None)
+
             def step(ins=inputs):
                 out, lse = vdist.summarize_by_length(ins[0], ins[1], ins[2], ins[3], ulen, attn=args.attn,
-                                                     total_len=total)
+                                                     total_len=total, exchange=xchg)
                 return [out] + ([lse] if lse is not None else [])
 
             # the same three phases, separately callable for the breakdown (summarize_by_length's body)
             be = vdist.CudaBackend()
-            acode = 0 if args.attn == "softmax" else 1
-            phase_fns = (lambda: be.partial(q, K, V, soff_t, total, acode),
-                         lambda pp: (vdist._all_gather(pp[0], None),
-                                     vdist._all_gather(pp[1], None) if acode == 0 else None),
-                         lambda gg: be.merge(gg[0], gg[1], q, acode, ulen))
+            if xchg is None:
+                phase_fns = (lambda: be.partial(q, K, V, soff_t, total, acode),
+                             lambda pp: (vdist._all_gather(pp[0], None),
+                                         vdist._all_gather(pp[1], None) if acode == 0 else None),
+                             lambda gg: be.merge(gg[0], gg[1], q, acode, ulen))
+            else:
+                def _merge_release(gg):
+                    res = be.merge(gg[0], gg[1] if acode == 0 else None, q, acode, ulen)
+                    xchg.release()
+                    return res
+                phase_fns = (lambda: be.partial(q, K, V, soff_t, total, acode),
+                             lambda pp: xchg.gather(pp[0], pp[1] if acode == 0 else None),
+                             _merge_release)
         else:
             segs_obj = [vdist.Segment(u, a0, e0) for u, a0, e0 in seg]
             fplan = vdist.FlatPlan(all_segs, lens, rank, dev)
@@ -366,7 +383,9 @@ def run_own(args, rank, world, local_rank):
                 return [o for o, _ in res.values()][:1] or [ins[0]]
         items_per_step = int(off_all[-1])
         scaling = "strong"
-        parallel = f"{mode} x{world} (strong: one {args.config} batch split; all_gather of partials over NCCL)"
+        parallel = (f"{mode} x{world} (strong: one {args.config} batch split; all_gather of partials over "
+                    + ("peer memory (CUDA IPC, NVLink stores)" if (mode == "by_length" and args.exchange == "p2p")
+                       else "NCCL") + ")")
         B = B_all
     path = vista.vista_dispatch_name(vista.make_desc(B, S, H, d, in_dtype=vista.BF16, attn=attn))
 

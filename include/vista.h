@@ -310,6 +310,41 @@ vista_status_t vista_target_attend(const vista_desc_t* desc, const int8_t* codes
                                    int64_t total_rows, void* out, float* lse, void* workspace,
                                    size_t workspace_bytes, void* stream);
 
+/*
+ * Split-L exchange over peer memory (SURVEY.md 8(e) phase 2; an alternative to an NCCL all_gather of
+ * the vista_summarize_partial outputs before vista_summarize_merge).  The ranks of one node each own
+ * a receive buffer recv_o float [world][n_o] and recv_lse float [world][n_lse] (n_o = B H S d and
+ * n_lse = B H S for softmax partials), a flags and an acks array (uint32 [world]) and a uint32
+ * epoch counter, all in device memory and zero-initialized; the buffers are shared through CUDA IPC
+ * (vista_ipc_get_handle / vista_ipc_open_handle), so every rank holds device pointers to every
+ * rank's arrays (its own included).  Per step, on one stream, in this order:
+ *   vista_exchange_push(world, rank, part_o, n_o, part_lse, n_lse, recv_o[], recv_lse[], acks, epoch)
+ *       waits until acks[r] >= *epoch for all r (every rank consumed the previous step), then stores
+ *       this rank's partial into slot `rank` of every rank's receive buffer (NVLink for peers);
+ *   vista_exchange_signal(world, rank, flags[], epoch): *epoch += 1, then flags_r[rank] = *epoch on
+ *       every rank r (system-scope release);
+ *   vista_exchange_wait(world, flags, epoch): until flags[r] == *epoch for every r (acquire): the
+ *       local receive buffer holds every rank's partial (merge it with vista_summarize_merge);
+ *   vista_exchange_ack(world, rank, acks[], epoch): acks_r[rank] = *epoch on every rank r.
+ * recv_o[r], recv_lse[r], flags[r], acks[r]: HOST arrays of world device pointers (rank r's arrays);
+ * acks / flags (push / wait): this rank's own arrays.  world <= 8.  No host synchronization; the
+ * epoch lives in device memory, so the sequence can be captured in a CUDA graph.  A wait that does
+ * not complete within 4 s traps (launch error) instead of hanging.
+ */
+#define VISTA_IPC_HANDLE_BYTES 64
+vista_status_t vista_ipc_get_handle(const void* dptr, void* handle /* VISTA_IPC_HANDLE_BYTES */);
+vista_status_t vista_ipc_open_handle(const void* handle, void** dptr);
+vista_status_t vista_ipc_close(void* dptr);
+vista_status_t vista_exchange_push(int32_t world, int32_t rank, const float* part_o, int64_t n_o,
+                                   const float* part_lse, int64_t n_lse, float* const* recv_o,
+                                   float* const* recv_lse, const uint32_t* acks, const uint32_t* epoch,
+                                   void* stream);
+vista_status_t vista_exchange_signal(int32_t world, int32_t rank, uint32_t* const* flags, uint32_t* epoch,
+                                     void* stream);
+vista_status_t vista_exchange_wait(int32_t world, const uint32_t* flags, const uint32_t* epoch, void* stream);
+vista_status_t vista_exchange_ack(int32_t world, int32_t rank, uint32_t* const* acks, const uint32_t* epoch,
+                                  void* stream);
+
 /* Bytes of device workspace vista_summarize_merge needs for this descriptor (0 for softmax). */
 vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes);
 

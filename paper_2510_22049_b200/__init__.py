@@ -32,6 +32,8 @@ __all__ = [
     "vista_target_attend_workspace_size", "vista_target_attend", "target_attend",
     "vista_summarize_layers_workspace_size", "vista_summarize_layers", "summarize_layers",
     "summarize", "summarize_partial", "summarize_merge", "summarize_bwd", "qla_rows",
+    "vista_ipc_get_handle", "vista_ipc_open_handle", "vista_ipc_close", "vista_exchange_push",
+    "vista_exchange_signal", "vista_exchange_wait", "vista_exchange_ack",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
 
@@ -120,6 +122,17 @@ def load():
     lib.vista_time_next_main_kernel.argtypes = [P, P]
     lib.vista_time_next_main_kernel.restype = ctypes.c_int
     lib.vista_launch_counter.restype = ctypes.c_uint64
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    lib.vista_ipc_get_handle.argtypes = [P, P]
+    lib.vista_ipc_open_handle.argtypes = [P, PP]
+    lib.vista_ipc_close.argtypes = [P]
+    lib.vista_exchange_push.argtypes = [i32, i32, P, i64, P, i64, PP, PP, P, P, P]
+    lib.vista_exchange_signal.argtypes = [i32, i32, PP, P, P]
+    lib.vista_exchange_wait.argtypes = [i32, P, P, P]
+    lib.vista_exchange_ack.argtypes = [i32, i32, PP, P, P]
+    for f in ("vista_ipc_get_handle", "vista_ipc_open_handle", "vista_ipc_close", "vista_exchange_push",
+              "vista_exchange_signal", "vista_exchange_wait", "vista_exchange_ack"):
+        getattr(lib, f).restype = ctypes.c_int
     for f in ("vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state",
               "vista_target_attend_workspace_size", "vista_target_attend",
               "vista_summarize_layers_workspace_size", "vista_summarize_layers",
@@ -526,6 +539,54 @@ def target_attend(codes, token_scale, token_zero_point, q, k_self, v_self, row_o
     vista_target_attend(desc, codes, token_scale, token_zero_point, q, k_self, v_self, resid, row_offsets, total_rows,
                         out, lse, ws, ws.numel(), stream)
     return out, lse
+
+
+# ----------------------------------------------------------------------------- peer-memory exchange
+IPC_HANDLE_BYTES = 64
+
+
+def vista_ipc_get_handle(tensor_or_ptr) -> bytes:
+    """CUDA IPC handle (64 bytes) of a device allocation, to be opened by another process."""
+    buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(load().vista_ipc_get_handle(_ptr(tensor_or_ptr), buf), "vista_ipc_get_handle")
+    return buf.raw
+
+
+def vista_ipc_open_handle(handle: bytes) -> int:
+    """Device pointer (in this process) of another process's allocation."""
+    out = ctypes.c_void_p(0)
+    buf = ctypes.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+    _check(load().vista_ipc_open_handle(buf, ctypes.byref(out)), "vista_ipc_open_handle")
+    return int(out.value)
+
+
+def vista_ipc_close(ptr: int):
+    _check(load().vista_ipc_close(ptr), "vista_ipc_close")
+
+
+def _ptr_array(ptrs):
+    return (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+
+
+def vista_exchange_push(world, rank, part_o, n_o, part_lse, n_lse, recv_o_ptrs, recv_lse_ptrs, acks, epoch,
+                        stream=None):
+    _check(load().vista_exchange_push(int(world), int(rank), _ptr(part_o), int(n_o), _ptr(part_lse), int(n_lse),
+                                      _ptr_array(recv_o_ptrs), _ptr_array(recv_lse_ptrs) if recv_lse_ptrs else None,
+                                      _ptr(acks), _ptr(epoch), _stream(stream)), "vista_exchange_push")
+
+
+def vista_exchange_signal(world, rank, flag_ptrs, epoch, stream=None):
+    _check(load().vista_exchange_signal(int(world), int(rank), _ptr_array(flag_ptrs), _ptr(epoch), _stream(stream)),
+           "vista_exchange_signal")
+
+
+def vista_exchange_wait(world, flags, epoch, stream=None):
+    _check(load().vista_exchange_wait(int(world), _ptr(flags), _ptr(epoch), _stream(stream)), "vista_exchange_wait")
+
+
+def vista_exchange_ack(world, rank, ack_ptrs, epoch, stream=None):
+    _check(load().vista_exchange_ack(int(world), int(rank), _ptr_array(ack_ptrs), _ptr(epoch), _stream(stream)),
+           "vista_exchange_ack")
 
 
 def summarize_layers(x, x_offsets, weights, S, H, total_rows=None, *, phi1="silu", phi2="silu", normalize=True,

@@ -13,6 +13,8 @@ constexpr int kTile = 128;  // history items per tile (= TMA box rows = MMA N of
 // Upper bound on every persistent grid (one CTA per SM): the split-L merge lists a unit's run of
 // partial slots in a fixed array of 2 * kMaxPersistentCtas + 2 entries (kernels_misc.cu).
 constexpr int kMaxPersistentCtas = 159;
+constexpr int kMaxExchangeRanks = 8;  // p2p_exchange.cu: ranks of one node
+void count_launches(unsigned n);     // the library's launch counter (vista_launch_counter)
 
 enum OutMode : int { OUT_FINAL = 0, OUT_PARTIAL = 1 };
 

@@ -24,7 +24,8 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = ["partition_by_user", "partition_by_length", "partition_flat", "CudaBackend",
-           "summarize_by_length", "summarize_flat", "summarize_bwd_by_user", "FlatPlan", "Segment"]
+           "summarize_by_length", "summarize_flat", "summarize_bwd_by_user", "FlatPlan", "Segment",
+           "PeerExchange"]
 
 
 # ----------------------------------------------------------------------------- partitioners (host)
@@ -132,17 +133,99 @@ def _all_gather(t, group):
     return out.to(t.device, non_blocking=True) if staged else out
 
 
+class PeerExchange:
+    """The split-L exchange over peer memory (SURVEY.md 8(e) phase 2; vista_exchange_* in
+    include/vista.h): every rank of the node owns a receive buffer for all ranks' partials, shared
+    through CUDA IPC, and the partial of a rank is stored straight into every rank's buffer (NVLink /
+    NVSwitch peer stores), then published with a system-scope flag; the merge reads the local buffer.
+    No NCCL call and no host synchronization on the step (the epoch is a device counter, so the step
+    can be captured in a CUDA graph).  Built once per (shape, group); world <= 8.
+
+    part_shape: the partial's shape (softmax O_p [B,H,S,d]; QLA Z_p [B,H,d,d]); lse_shape: the
+    softmax lse_p shape [B,H,S] or None (QLA)."""
+
+    def __init__(self, part_shape, lse_shape=None, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        from . import (vista_ipc_get_handle, vista_ipc_open_handle)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world > 8:
+            raise ValueError("PeerExchange: at most 8 ranks (one node)")
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.part_shape, self.lse_shape = tuple(part_shape), (tuple(lse_shape) if lse_shape else None)
+        self.recv_o = torch.zeros((self.world,) + self.part_shape, dtype=torch.float32, device=dev)
+        self.recv_lse = (torch.zeros((self.world,) + self.lse_shape, dtype=torch.float32, device=dev)
+                         if self.lse_shape else None)
+        self.flags = torch.zeros(self.world, dtype=torch.int32, device=dev)
+        self.acks = torch.zeros(self.world, dtype=torch.int32, device=dev)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)  # the zeroed arrays exist before any peer writes into them
+        mine = [self.recv_o] + ([self.recv_lse] if self.recv_lse is not None else []) + [self.flags, self.acks]
+        handles = [vista_ipc_get_handle(t) for t in mine] if self.world > 1 else None
+        if self.world > 1:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, handles, group=group)
+        self._opened = []
+        cols = []
+        for r in range(self.world):
+            if r == self.rank:
+                cols.append([t.data_ptr() for t in mine])
+            else:
+                ptrs = [vista_ipc_open_handle(h) for h in allh[r]]
+                self._opened += ptrs
+                cols.append(ptrs)
+        k = 0
+        self.o_ptrs = [c[k] for c in cols]
+        k += 1
+        self.lse_ptrs = [c[k] for c in cols] if self.recv_lse is not None else None
+        k += 1 if self.recv_lse is not None else 0
+        self.flag_ptrs = [c[k] for c in cols]
+        self.ack_ptrs = [c[k + 1] for c in cols]
+        if self.world > 1:
+            dist.barrier(group=group)  # every rank mapped every buffer before the first push
+
+    def gather(self, part_o, part_lse=None, stream=None):
+        """push + signal + wait: returns the local receive buffers [world, ...] holding every rank's
+        partial (stream-ordered after this call)."""
+        from . import vista_exchange_push, vista_exchange_signal, vista_exchange_wait
+        n_o = part_o.numel()
+        n_l = part_lse.numel() if (part_lse is not None and self.recv_lse is not None) else 0
+        vista_exchange_push(self.world, self.rank, part_o, n_o, part_lse if n_l else None, n_l, self.o_ptrs,
+                            self.lse_ptrs if n_l else None, self.acks, self.epoch, stream)
+        vista_exchange_signal(self.world, self.rank, self.flag_ptrs, self.epoch, stream)
+        vista_exchange_wait(self.world, self.flags, self.epoch, stream)
+        return self.recv_o, self.recv_lse
+
+    def release(self, stream=None):
+        """ack: this rank has consumed the current epoch (after the merge read the receive buffer)."""
+        from . import vista_exchange_ack
+        vista_exchange_ack(self.world, self.rank, self.ack_ptrs, self.epoch, stream)
+
+    def close(self):
+        from . import vista_ipc_close
+        for p in self._opened:
+            vista_ipc_close(p)
+        self._opened = []
+
+
 def summarize_by_length(q, k_shard, v_shard, shard_offsets, user_len, *, attn="softmax", group=None,
-                        backend=None, total_len=None):
+                        backend=None, total_len=None, exchange=None):
     """Rank-local shard (this rank's range of every user) -> merged summary of every user on every
     rank.  shard_offsets: int64 [B+1] (device), user_len: int64 [B] total L_u (device, QLA 1/N).
-    One all_gather of the partials (softmax: O_p [B,H,S,d] + lse_p [B,H,S]; QLA: Z_p [B,H,d,d]).
-    No host synchronization: the step is capturable in a CUDA graph (NCCL)."""
+    One all_gather of the partials (softmax: O_p [B,H,S,d] + lse_p [B,H,S]; QLA: Z_p [B,H,d,d]):
+    NCCL (or gloo), or, with exchange = a PeerExchange, peer-memory stores over NVLink.
+    No host synchronization: the step is capturable in a CUDA graph."""
     backend = backend or CudaBackend()
     a = _attn_code(attn)
     if total_len is None:
         total_len = k_shard.shape[0]
     po, pl = backend.partial(q, k_shard, v_shard, shard_offsets, total_len, a)
+    if exchange is not None:
+        go, gl = exchange.gather(po, pl if a == 0 else None)
+        res = backend.merge(go, gl if a == 0 else None, q, a, user_len)
+        exchange.release()
+        return res
     go = _all_gather(po, group)
     gl = _all_gather(pl, group) if a == 0 else None
     return backend.merge(go, gl, q, a, user_len)

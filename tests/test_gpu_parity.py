@@ -1226,3 +1226,44 @@ def test_qla_target_rows_from_state_c2_full_size_sampled_users(cuda_lib):
         go = out[ra:rb].cpu().numpy()
         for h in range(H):
             assert block_err(go[:, h], ref[:, h]) <= 2e-2, f"user {u} head {h}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("attn", ["softmax", "qla"])
+def test_peer_exchange_single_rank(cuda_lib, attn):
+    """The peer-memory split-L exchange (vista_exchange_*, dist.PeerExchange) at world size 1 (one
+    GPU: the rank pushes into its own receive buffer): bitwise equal to merging the partial directly,
+    over several steps (device epochs and acks), eagerly and replayed from a CUDA graph."""
+    from paper_2510_22049_b200 import dist as vdist
+    vista = cuda_lib
+    lens = [700, 0, 129, 2050]
+    S, H, d = 256, 2, 128
+    q, k, v, off = synth.make_batch(lens, S, H, d, seed=31, backend="torch", device="cuda")
+    ot = torch.from_numpy(off).cuda()
+    ulen = torch.tensor(lens, dtype=torch.int64, device="cuda")
+    a = vista.SOFTMAX if attn == "softmax" else vista.QLA
+    be = vdist.CudaBackend()
+    po, pl = be.partial(q, k, v, ot, int(off[-1]), a)
+    ref_o, ref_l = be.merge(po[None], pl[None] if a == vista.SOFTMAX else None, q, a, ulen)
+    ex = vdist.PeerExchange(po.shape, pl.shape if a == vista.SOFTMAX else None)
+    for _ in range(3):
+        o, l = vdist.summarize_by_length(q, k, v, ot, ulen, attn=attn, total_len=int(off[-1]), exchange=ex)
+        torch.cuda.synchronize()
+        assert torch.equal(o, ref_o)
+        if a == vista.SOFTMAX:
+            assert torch.equal(l, ref_l)
+    assert int(ex.epoch.item()) == 3 and int(ex.acks[0].item()) == 3 and int(ex.flags[0].item()) == 3
+    # captured: the epoch is a device counter, so replays advance it
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        g.capture_begin()
+        o2, l2 = vdist.summarize_by_length(q, k, v, ot, ulen, attn=attn, total_len=int(off[-1]), exchange=ex)
+        g.capture_end()
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o2, ref_o)
+    assert int(ex.epoch.item()) == 5

@@ -149,6 +149,33 @@ def test_layers_stage2_rows_from_state_validation_before_launch(lib):
         assert e.value.status == status
 
 
+def test_exchange_validation_before_launch(lib):
+    """Peer-memory exchange entry points: argument errors are returned before any launch."""
+    import paper_2510_22049_b200 as vista
+    E = vista.VistaError
+    cases = [
+        (lambda: vista.vista_exchange_push(0, 0, 4096, 64, 4096, 16, [4096], [4096], 4096, 4096, stream=0), 2),
+        (lambda: vista.vista_exchange_push(2, 2, 4096, 64, 4096, 16, [4096, 8192], [4096, 8192], 4096, 4096,
+                                           stream=0), 2),  # rank >= world
+        (lambda: vista.vista_exchange_push(9, 0, 4096, 64, 4096, 16, [4096] * 9, [4096] * 9, 4096, 4096,
+                                           stream=0), 2),  # more than one node's ranks
+        (lambda: vista.vista_exchange_push(1, 0, 4096, 63, 4096, 16, [4096], [4096], 4096, 4096, stream=0), 2),
+        (lambda: vista.vista_exchange_push(1, 0, 0, 64, 4096, 16, [4096], [4096], 4096, 4096, stream=0), 1),
+        (lambda: vista.vista_exchange_push(2, 0, 4096, 64, 4096, 16, [4096, 0], [4096, 8192], 4096, 4096,
+                                           stream=0), 1),  # a NULL peer buffer
+        (lambda: vista.vista_exchange_push(1, 0, 4100, 64, 4096, 16, [4096], [4096], 4096, 4096, stream=0), 4),
+        (lambda: vista.vista_exchange_signal(1, 1, [4096], 4096, stream=0), 2),
+        (lambda: vista.vista_exchange_signal(1, 0, [4096], 0, stream=0), 1),
+        (lambda: vista.vista_exchange_wait(0, 4096, 4096, stream=0), 2),
+        (lambda: vista.vista_exchange_wait(1, 0, 4096, stream=0), 1),
+        (lambda: vista.vista_exchange_ack(1, 0, [0], 4096, stream=0), 1),
+    ]
+    for fn, status in cases:
+        with pytest.raises(E) as e:
+            fn()
+        assert e.value.status == status
+
+
 def test_dispatch_by_shape(lib):
     import paper_2510_22049_b200 as vista
     assert vista.vista_dispatch_name(vista.make_desc(8, 256, 4, 128)) == "sm100_softmax"

@@ -147,12 +147,12 @@ class PeerExchange:
     def __init__(self, part_shape, lse_shape=None, group=None, device=None):
         import torch
         import torch.distributed as dist
-        from . import (vista_ipc_get_handle, vista_ipc_open_handle)
+        from . import vista_ipc_get_handle, vista_ipc_open_handle
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         if self.world > 8:
             raise ValueError("PeerExchange: at most 8 ranks (one node)")
-        dev = device or torch.device("cuda", torch.cuda.current_device())
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.part_shape, self.lse_shape = tuple(part_shape), (tuple(lse_shape) if lse_shape else None)
         self.recv_o = torch.zeros((self.world,) + self.part_shape, dtype=torch.float32, device=dev)
         self.recv_lse = (torch.zeros((self.world,) + self.lse_shape, dtype=torch.float32, device=dev)
@@ -160,7 +160,8 @@ class PeerExchange:
         self.flags = torch.zeros(self.world, dtype=torch.int32, device=dev)
         self.acks = torch.zeros(self.world, dtype=torch.int32, device=dev)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
-        torch.cuda.synchronize(dev)  # the zeroed arrays exist before any peer writes into them
+        if dev.type == "cuda":
+            torch.cuda.synchronize(dev)  # the zeroed arrays exist before any peer writes into them
         mine = [self.recv_o] + ([self.recv_lse] if self.recv_lse is not None else []) + [self.flags, self.acks]
         handles = [vista_ipc_get_handle(t) for t in mine] if self.world > 1 else None
         if self.world > 1:

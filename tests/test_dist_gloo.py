@@ -238,3 +238,47 @@ def test_backward_by_user_all_reduces_seed_gradient(attn):
         np.testing.assert_allclose(dq, ref[0], rtol=0, atol=1e-12 * max(1.0, np.abs(ref[0]).max()))
         for n, u in enumerate(mine):
             np.testing.assert_allclose(dk[soff[n]:soff[n + 1]], ref[1][off[u]:off[u + 1]], rtol=0, atol=1e-12)
+
+
+def _peer_worker(rank, world, port, result_q):
+    """Host logic of dist.PeerExchange at world size 2: the CUDA IPC calls are replaced by a fake
+    handle / pointer scheme (CPU tensors), so the handle all_gather, the per-rank pointer tables and
+    the rank ordering are checked without GPUs."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2510_22049_b200 as vista
+        vista.vista_ipc_get_handle = lambda t: (b"R%d:%d" % (rank, t.data_ptr() % 1000003)).ljust(64, b"\0")
+        opened = []
+
+        def fake_open(h):
+            opened.append(bytes(h).rstrip(b"\0"))
+            return 10**12 + len(opened)
+        vista.vista_ipc_open_handle = fake_open
+        ex = vdist.PeerExchange((3, 2, 4, 8), (3, 2, 4), device="cpu")
+        own = [ex.recv_o.data_ptr(), ex.recv_lse.data_ptr(), ex.flags.data_ptr(), ex.acks.data_ptr()]
+        result_q.put((rank, (ex.world, ex.rank, ex.o_ptrs, ex.lse_ptrs, ex.flag_ptrs, ex.ack_ptrs, own, opened)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_host_logic_world2():
+    ctx = mp.get_context("spawn")
+    rq = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, rq)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(rq.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        world, rank, o, l, f, a, own, opened = res[r]
+        assert (world, rank) == (2, r)
+        # own arrays at index rank, the peer's (opened from its 4 handles, in order) at the other index
+        assert [o[r], l[r], f[r], a[r]] == own
+        peer = 1 - r
+        assert [o[peer], l[peer], f[peer], a[peer]] == [10**12 + i for i in range(1, 5)]
+        assert all(h.startswith(b"R%d:" % peer) for h in opened) and len(opened) == 4

@@ -102,11 +102,16 @@ constexpr int kRingConsumers = 15;  // warps 1, 2, 3 and the 12 softmax / epilog
 #define VISTA_CTL_REGS 96
 #endif
 // the launch grants 128 x 512 registers; the control warpgroup gives 32 per thread back
-// (setmaxnreg.dec) and the epilogue warpgroup takes them (setmaxnreg.inc blocks until the pool can
-// cover it); the two softmax warpgroups keep the launch's 128
+// (setmaxnreg.dec) and the softmax warpgroups take 16 each (setmaxnreg.inc blocks until the pool can
+// cover it); the epilogue warpgroup keeps whatever is left (128 by default)
 constexpr int kCtlRegs = VISTA_CTL_REGS;
-constexpr int kEpiRegs = 128 + (128 - kCtlRegs);
-static_assert(kCtlRegs % 8 == 0 && kCtlRegs <= 128 && kEpiRegs <= 256, "register split");
+#ifndef VISTA_SMX_REGS  // registers of the two softmax warpgroups (A/B p17: 144 beats 128, 152, 160)
+#define VISTA_SMX_REGS 144
+#endif
+constexpr int kSmxRegs = VISTA_SMX_REGS;
+constexpr int kEpiRegs = 128 + (128 - kCtlRegs) - 2 * (kSmxRegs - 128);
+static_assert(kCtlRegs % 8 == 0 && kSmxRegs % 8 == 0 && kEpiRegs % 8 == 0 && kCtlRegs <= 128 && kEpiRegs >= 24 &&
+                  kEpiRegs <= 256, "register split");
 
 struct ItemEntry {
     int u, hg, t0, t1, Tu, row0, len, flags;  // flags: 1 valid, 2 first, 4 last
@@ -682,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
     } else if (warp < 12) {
+        if constexpr (kSmxRegs > 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSmxRegs));
         // ============================ softmax (two threads per row) ============================
         const int wq = warp % 4;
         const int rh = (warp - 4) / 4;             // row half of the lane quarter
@@ -791,7 +797,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_arrive(&bars->ml_full);
         }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
+        if constexpr (kEpiRegs > 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
+        else if constexpr (kEpiRegs < 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
         // ============================ epilogue ============================
         const int wq = warp % 4;
         const int row = wq * 32 + lane;

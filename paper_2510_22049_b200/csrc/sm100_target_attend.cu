@@ -41,10 +41,19 @@ bool make_kv_map(CUtensorMap* map, const void* base, int64_t total_len, int H);
 
 #ifdef VISTA_TRACE  // debug timeline of CTA 0: clock64 per (event, tile)
 __device__ unsigned long long g_ta_trace[16][64];
+__device__ unsigned long long g_ta_cta[160][3];  // per CTA: globaltimer at start, after the PDL wait, at the end
 #define TTRACE(ev, g) \
     do { if (blockIdx.x == 0 && (g) < 64) g_ta_trace[ev][g] = clock64(); } while (0)
+__device__ __forceinline__ unsigned long long ta_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define CTRACE(slot) \
+    do { if (threadIdx.x == 0 && blockIdx.x < 160) g_ta_cta[blockIdx.x][slot] = ta_gtime(); } while (0)
 #else
 #define TTRACE(ev, g) do { } while (0)
+#define CTRACE(slot) do { } while (0)
 #endif
 
 namespace {
@@ -130,6 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     TABars* bars = reinterpret_cast<TABars*>(smem + kBarOff);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) TTRACE(14, 0);
+    CTRACE(0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&bars->qk_full[s], 1);
@@ -154,11 +164,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // PDL: the prologue above overlapped the tile scan; its results (uts) and everything before it
     // on the stream are visible after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    CTRACE(1);
     const uint32_t tmem = bars->tmem_base;
     const int64_t* uts = P.uts;
     const int64_t* roff = P.row_offsets;
     const uint32_t tS = tmem, tP = tmem + 256, tO = tmem + 384;
     const int H = P.H;
+    // registers: the control warpgroup (warps 0-3) gives 64 per thread back; the epilogue warpgroup
+    // (v_c rows prefetched: 64 registers live across its waits) takes 32 and the two softmax
+    // warpgroups (the dequantization's loads in flight) 16 each
+    if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
     ItemIter iter;
     iter.init(uts, P.B, H, blockIdx.x, gridDim.x, true);  // every role walks with full warps
     Item it;
@@ -213,136 +228,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) TTRACE(4, g);
             }
         }
-    } else if (warp >= 4) {
-        const bool smx = warp < 12;
-        // softmax: lane quarter wq, row half rh, token half ch; epilogue: one thread per row
-        const int wq = warp & 3, rh = (warp - 4) >> 2, ch = lane >> 4;
-        const int row = smx ? wq * 32 + rh * 16 + (lane & 15) : wq * 32 + lane;  // candidate row = TMEM lane
-        const uint32_t lb = (uint32_t)(smx ? wq * 32 + rh * 16 : wq * 32) << 16;
+    } else if (warp >= 12) {
+        // ============ epilogue: (O + p_self v_c) / l [+ resid], one thread per row ============
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 160;");
+        const int wq = warp & 3;
+        const int row = wq * 32 + lane;  // candidate row = TMEM lane
+        const uint32_t lb = (uint32_t)(wq * 32) << 16;
         const size_t rstride = (size_t)H * 128;
         int g = 0;
         for (int k = 0; iter.next(it, uts, P.B, H); ++k) {
             const int u = it.u, h = it.hg;
-            // ---- the item's tokens: int8 codes * scale + zero point -> bf16, swizzled, both halves
-            //      (the softmax warps 4-11)
-            if (threadIdx.x == 128) TTRACE(12, k);
-            if (smx) {
-                // every thread's NS / 32 chunks: all loads first (in flight together), then convert
-                constexpr int kPer = NS * 8 / 256;
-                uint4 raw[kPer];
-                float a[kPer], b[kPer];
-#pragma unroll
-                for (int n = 0; n < kPer; ++n) {
-                    const int x = threadIdx.x - 128 + 256 * n;  // x = (token i, 16-B chunk cc of its codes)
-                    const size_t tix = ((size_t)u * NS + (x >> 3)) * H + h;
-                    raw[n] = __ldg(reinterpret_cast<const uint4*>(P.codes + tix * 128) + (x & 7));
-                    a[n] = __ldg(P.tscale + tix);
-                    b[n] = __ldg(P.tzp + tix);
-                }
-                // the loads overlap the previous item's last PV; T is rewritten only after it
-                if (k >= 1) ptx::mbar_wait(&bars->t_free, (uint32_t)(k - 1) & 1u);
-#pragma unroll
-                for (int n = 0; n < kPer; ++n) {
-                    const int x = threadIdx.x - 128 + 256 * n;
-                    const int i = x >> 3, cc = x & 7;  // codes [16 cc, 16 cc + 16) of token i
-                    const uint32_t w[4] = {raw[n].x, raw[n].y, raw[n].z, raw[n].w};
-                    uint32_t o[8];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int32_t v = (int32_t)w[e];
-                        const float f0 = (float)(int8_t)(v & 0xFF), f1 = (float)(int8_t)((v >> 8) & 0xFF);
-                        const float f2 = (float)(int8_t)((v >> 16) & 0xFF), f3 = (float)(v >> 24);
-                        o[2 * e] = ptx::pack_bf16x2(fmaf(f0, a[n], b[n]), fmaf(f1, a[n], b[n]));
-                        o[2 * e + 1] = ptx::pack_bf16x2(fmaf(f2, a[n], b[n]), fmaf(f3, a[n], b[n]));
-                    }
-                    // channels 16 cc .. 16 cc + 15 = 16-B bf16 chunks 2 cc, 2 cc + 1 of the row (half = cc / 4)
-                    const uint32_t hb = base + kTOff + (cc >> 2) * (NS * 128);
-                    const int c0 = (2 * cc) & 7;
-                    sts128(hb + swz(i, c0), make_uint4(o[0], o[1], o[2], o[3]));
-                    sts128(hb + swz(i, c0 + 1), make_uint4(o[4], o[5], o[6], o[7]));
-                }
-                ptx::fence_proxy_async_smem();
-                ptx::mbar_arrive(&bars->t_full);
-            }
-            if (threadIdx.x == 128) TTRACE(13, k);
             const int64_t R = roff[u + 1] - roff[u];
             for (int t = it.t0; t < it.t1; ++t, ++g) {
-                const int st = g & 1;
-                if (smx) {
-                    // ============ softmax over [tokens; self], two threads per candidate row ============
-                    ptx::mbar_wait(&bars->qk_full[st], (uint32_t)(g >> 1) & 1u);
-                    if (threadIdx.x == 128) TTRACE(5, g);
-                    const uint32_t sq = base + kQKOff + st * 2 * kTileB;
-                    float self = 0.f;  // q_c . k_c from the staged tiles: this thread's 64 channels
-#pragma unroll 4
-                    for (int c = 0; c < 8; ++c) {
-                        const uint4 qa = lds128(sq + ch * kHalf + swz(row, c));
-                        const uint4 ka = lds128(sq + kTileB + ch * kHalf + swz(row, c));
-                        const uint32_t qw[4] = {qa.x, qa.y, qa.z, qa.w}, kw[4] = {ka.x, ka.y, ka.z, ka.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            self = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(kw[e] << 16), self);
-                            self = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(kw[e] & 0xFFFF0000u),
-                                        self);
-                        }
-                    }
-                    self += __shfl_xor_sync(0xffffffffu, self, 16);
-                    self *= P.scale_log2;
-                    ptx::mbar_wait(&bars->s_full, (uint32_t)g & 1u);
-                    if (threadIdx.x == 128) TTRACE(6, g);
-                    ptx::mbar_arrive(&bars->qk_empty[st]);  // q (S done) and k (dot done) of this stage read
-                    ptx::tc_fence_after();
-                    // this thread: tokens [ch NS/2, ch NS/2 + NS/2) = S columns of the same range
-                    float m = self;
-#pragma unroll 1
-                    for (int c = 0; c < NS / 2; c += 32) {
-                        uint32_t r[32];
-                        ptx::tmem_ld16x32bx2_x32<NS / 2>(tS + lb + c, r);
-                        ptx::tmem_wait_ld();
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]) * P.scale_log2);
-                    }
-                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
-                    if (threadIdx.x == 128) TTRACE(7, g);
-                    // P(g) has its own columns: free once PV(g - 1) has read them
-                    if (g >= 1) ptx::mbar_wait(&bars->p_free, (uint32_t)(g - 1) & 1u);
-                    ptx::tc_fence_after();
-                    float l = 0.f;
-#pragma unroll 1
-                    for (int c = 0; c < NS / 2; c += 32) {
-                        uint32_t r[32], pk[16];
-                        ptx::tmem_ld16x32bx2_x32<NS / 2>(tS + lb + c, r);
-                        ptx::tmem_wait_ld();
-                        if (c == NS / 2 - 32) {  // last S chunk of this thread loaded: S(g + 1) may overwrite S
-                            ptx::tc_fence_before();
-                            ptx::mbar_arrive(&bars->s_free);
-                        }
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const float p0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), P.scale_log2, -m));
-                            const float p1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), P.scale_log2, -m));
-                            l += p0 + p1;
-                            pk[j] = ptx::pack_bf16x2(p0, p1);
-                        }
-                        // P of these 32 tokens: 16 columns (2 tokens per column), token order
-                        ptx::tmem_st16x32bx2_x16<NS / 4>(tP + lb + c / 2, pk);
-                    }
-                    l += __shfl_xor_sync(0xffffffffu, l, 16);
-                    const float pself = ptx::ex2(self - m);
-                    l += pself;
-                    const float inv = 1.f / l;
-                    if (g >= 1) ptx::mbar_wait(&bars->ml_empty, (uint32_t)(g - 1) & 1u);
-                    if (ch == 0) {
-                        bars->st[0][row] = inv;
-                        bars->st[1][row] = pself * inv;
-                        bars->st[2][row] = (m + __log2f(l)) * kLn2;
-                    }
-                    ptx::mbar_arrive(&bars->ml_full);
-                    ptx::tmem_wait_st();
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive(&bars->p_full);
-                    if (threadIdx.x == 128) TTRACE(8, g);
-                } else {
                     // ============ epilogue: (O + p_self v_c) / l [+ resid] ============
                     const int64_t row0 = roff[u] + (int64_t)t * 128;
                     const int64_t remr = R - (int64_t)t * 128;
@@ -417,13 +314,175 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (P.lse && row < valid) P.lse[(size_t)(row0 + row) * H + h] = lse;
                     if (threadIdx.x == 384) TTRACE(11, g);
+            }
+        }
+    } else if (warp >= 4) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 144;");
+        // softmax: lane quarter wq, row half rh, token half ch
+        const int wq = warp & 3, rh = (warp - 4) >> 2, ch = lane >> 4;
+        const int row = wq * 32 + rh * 16 + (lane & 15);  // candidate row = TMEM lane
+        const uint32_t lb = (uint32_t)(wq * 32 + rh * 16) << 16;
+        int g = 0;
+        for (int k = 0; iter.next(it, uts, P.B, H); ++k) {
+            const int u = it.u, h = it.hg;
+            // ---- the item's tokens: int8 codes * scale + zero point -> bf16, swizzled, both halves
+            //      (the softmax warps 4-11)
+            if (threadIdx.x == 128) TTRACE(12, k);
+            {
+                // every thread's NS / 32 chunks: all loads first (in flight together), then convert
+                constexpr int kPer = NS * 8 / 256;
+                uint4 raw[kPer];
+                float a[kPer], b[kPer];
+#pragma unroll
+                for (int n = 0; n < kPer; ++n) {
+                    const int x = threadIdx.x - 128 + 256 * n;  // x = (token i, 16-B chunk cc of its codes)
+                    const size_t tix = ((size_t)u * NS + (x >> 3)) * H + h;
+                    raw[n] = __ldg(reinterpret_cast<const uint4*>(P.codes + tix * 128) + (x & 7));
+                    a[n] = __ldg(P.tscale + tix);
+                    b[n] = __ldg(P.tzp + tix);
                 }
+#ifdef VISTA_TRACE
+                if (threadIdx.x == 128 && blockIdx.x == 0 && k < 32) {  // when this thread's loads landed
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int n = 0; n < kPer; ++n) acc ^= raw[n].x ^ raw[n].w ^ __float_as_uint(a[n] + b[n]);
+                    unsigned long long tt;
+                    asm volatile("mov.u64 %0, %%clock64; // %1" : "=l"(tt) : "r"(acc));
+                    g_ta_trace[13][32 + k] = tt;
+                }
+#endif
+                // the loads overlap the previous item's last PV; T is rewritten only after it
+                if (k >= 1) ptx::mbar_wait(&bars->t_free, (uint32_t)(k - 1) & 1u);
+#pragma unroll
+                for (int n = 0; n < kPer; ++n) {
+                    const int x = threadIdx.x - 128 + 256 * n;
+                    const int i = x >> 3, cc = x & 7;  // codes [16 cc, 16 cc + 16) of token i
+                    const uint32_t w[4] = {raw[n].x, raw[n].y, raw[n].z, raw[n].w};
+                    uint32_t o[8];
+                    // int8 -> f32 without I2F: byte c ^ 0x80 = c + 128 placed in the mantissa of 2^23
+                    // (PRMT), then (2^23 + c + 128) - (2^23 + 128) = c exactly (FADD2); t = c scale + zp (FFMA2)
+                    const uint64_t a2 = ptx::f2_pack(a[n], a[n]), b2 = ptx::f2_pack(b[n], b[n]);
+                    const uint64_t off2 = ptx::f2_pack(-8388736.f, -8388736.f);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t x = w[e] ^ 0x80808080u;
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const float f0 = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7440u + 2 * hh));
+                            const float f1 = __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7441u + 2 * hh));
+                            float t0, t1;
+                            ptx::f2_unpack(ptx::f2_fma(ptx::f2_add(ptx::f2_pack(f0, f1), off2), a2, b2), t0, t1);
+                            o[2 * e + hh] = ptx::pack_bf16x2(t0, t1);
+                        }
+                    }
+                    // channels 16 cc .. 16 cc + 15 = 16-B bf16 chunks 2 cc, 2 cc + 1 of the row (half = cc / 4)
+                    const uint32_t hb = base + kTOff + (cc >> 2) * (NS * 128);
+                    const int c0 = (2 * cc) & 7;
+                    sts128(hb + swz(i, c0), make_uint4(o[0], o[1], o[2], o[3]));
+                    sts128(hb + swz(i, c0 + 1), make_uint4(o[4], o[5], o[6], o[7]));
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(&bars->t_full);
+                // the next item of this CTA (if any): walk a copy of the iterator now, while the tiles
+                // run, and pull that item's codes and scale / zero-point lines into L2 (its dequant
+                // then waits on L2, not HBM; the walk's uts loads are cached for the real next())
+                ItemIter la = iter;
+                Item nx;
+                if (la.next(nx, uts, P.B, H)) {
+                    const int tl = threadIdx.x - 128;  // 0..255: token tl's 128-B code line
+                    if (tl < NS) {
+                        const size_t tix = ((size_t)nx.u * NS + tl) * H + nx.hg;
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.codes + tix * 128));
+                        if ((tl & 7) == 0) {  // scale / zp: 8 tokens per 128-B line at H = 4
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.tscale + tix));
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.tzp + tix));
+                        }
+                    }
+                }
+            }
+            if (threadIdx.x == 128) TTRACE(13, k);
+            for (int t = it.t0; t < it.t1; ++t, ++g) {
+                const int st = g & 1;
+                    // ============ softmax over [tokens; self], two threads per candidate row ============
+                    ptx::mbar_wait(&bars->qk_full[st], (uint32_t)(g >> 1) & 1u);
+                    if (threadIdx.x == 128) TTRACE(5, g);
+                    const uint32_t sq = base + kQKOff + st * 2 * kTileB;
+                    float self = 0.f;  // q_c . k_c from the staged tiles: this thread's 64 channels
+#pragma unroll 4
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 qa = lds128(sq + ch * kHalf + swz(row, c));
+                        const uint4 ka = lds128(sq + kTileB + ch * kHalf + swz(row, c));
+                        const uint32_t qw[4] = {qa.x, qa.y, qa.z, qa.w}, kw[4] = {ka.x, ka.y, ka.z, ka.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            self = fmaf(__uint_as_float(qw[e] << 16), __uint_as_float(kw[e] << 16), self);
+                            self = fmaf(__uint_as_float(qw[e] & 0xFFFF0000u), __uint_as_float(kw[e] & 0xFFFF0000u),
+                                        self);
+                        }
+                    }
+                    self += __shfl_xor_sync(0xffffffffu, self, 16);
+                    self *= P.scale_log2;
+                    ptx::mbar_wait(&bars->s_full, (uint32_t)g & 1u);
+                    if (threadIdx.x == 128) TTRACE(6, g);
+                    ptx::mbar_arrive(&bars->qk_empty[st]);  // q (S done) and k (dot done) of this stage read
+                    ptx::tc_fence_after();
+                    // this thread: tokens [ch NS/2, ch NS/2 + NS/2) = S columns of the same range
+                    float m = self;
+#pragma unroll 1
+                    for (int c = 0; c < NS / 2; c += 32) {
+                        uint32_t r[32];
+                        ptx::tmem_ld16x32bx2_x32<NS / 2>(tS + lb + c, r);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]) * P.scale_log2);
+                    }
+                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+                    if (threadIdx.x == 128) TTRACE(7, g);
+                    // P(g) has its own columns: free once PV(g - 1) has read them
+                    if (g >= 1) ptx::mbar_wait(&bars->p_free, (uint32_t)(g - 1) & 1u);
+                    ptx::tc_fence_after();
+                    float l = 0.f;
+#pragma unroll 1
+                    for (int c = 0; c < NS / 2; c += 32) {
+                        uint32_t r[32], pk[16];
+                        ptx::tmem_ld16x32bx2_x32<NS / 2>(tS + lb + c, r);
+                        ptx::tmem_wait_ld();
+                        if (c == NS / 2 - 32) {  // last S chunk of this thread loaded: S(g + 1) may overwrite S
+                            ptx::tc_fence_before();
+                            ptx::mbar_arrive(&bars->s_free);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float p0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), P.scale_log2, -m));
+                            const float p1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), P.scale_log2, -m));
+                            l += p0 + p1;
+                            pk[j] = ptx::pack_bf16x2(p0, p1);
+                        }
+                        // P of these 32 tokens: 16 columns (2 tokens per column), token order
+                        ptx::tmem_st16x32bx2_x16<NS / 4>(tP + lb + c / 2, pk);
+                    }
+                    l += __shfl_xor_sync(0xffffffffu, l, 16);
+                    const float pself = ptx::ex2(self - m);
+                    l += pself;
+                    const float inv = 1.f / l;
+                    if (g >= 1) ptx::mbar_wait(&bars->ml_empty, (uint32_t)(g - 1) & 1u);
+                    if (ch == 0) {
+                        bars->st[0][row] = inv;
+                        bars->st[1][row] = pself * inv;
+                        bars->st[2][row] = (m + __log2f(l)) * kLn2;
+                    }
+                    ptx::mbar_arrive(&bars->ml_full);
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bars->p_full);
+                    if (threadIdx.x == 128) TTRACE(8, g);
             }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) TTRACE(15, 0);
+    CTRACE(2);
     if (warp == 1) ptx::tmem_dealloc(tmem, 512);
 }
 
@@ -548,6 +607,9 @@ cudaError_t launch_sm100_target_attend(const Problem& p, const int64_t* row_offs
 #ifdef VISTA_TRACE
 extern "C" int vista_debug_ta_trace(void* host, size_t bytes) {
     return (int)cudaMemcpyFromSymbol(host, g_ta_trace, bytes < sizeof(g_ta_trace) ? bytes : sizeof(g_ta_trace));
+}
+extern "C" int vista_debug_ta_cta(void* host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, g_ta_cta, bytes < sizeof(g_ta_cta) ? bytes : sizeof(g_ta_cta));
 }
 #endif
 

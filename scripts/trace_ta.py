@@ -42,3 +42,15 @@ print("g  " + " ".join(f"{n:>9s}" for n in names))
 for t in range(min(ntiles, 12)):
     print(f"{t:2d} " + " ".join(f"{rel[e, t]:9d}" for e in range(12)))
 print("items (dequant start, end):", [(int(rel[12, kk]), int(rel[13, kk])) for kk in range(4)])
+print("items (loads landed, VISTA_TRACE):", [int(rel[13, 32 + kk]) for kk in range(4)])
+
+cb = np.zeros((160, 3), dtype=np.uint64)
+lib.vista_debug_ta_cta.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+assert lib.vista_debug_ta_cta(cb.ctypes.data, cb.nbytes) == 0
+n = 148
+c = cb[:n].astype(np.int64)
+g0 = c[:, 0].min()
+st, wt, en = (c[:, 0] - g0) / 1e3, (c[:, 1] - g0) / 1e3, (c[:, 2] - g0) / 1e3
+print("per-CTA (us from the first CTA start): start max %.2f, PDL wait done min/med/max %.2f/%.2f/%.2f, "
+      "end min/med/max %.2f/%.2f/%.2f" % (st.max(), wt.min(), np.median(wt), wt.max(), en.min(), np.median(en), en.max()))
+print("end percentiles 10/50/90/100:", [round(float(np.percentile(en, p)), 2) for p in (10, 50, 90, 100)])

@@ -61,13 +61,23 @@ namespace {
 constexpr int kHalf = 128 * 128;  // one 64-column half of a 128-row bf16 tile
 constexpr int kTileB = 2 * kHalf;  // 32 KB
 constexpr int kThreads = 512;
+#ifndef VISTA_TA_EMU  // pairs out of every 4 whose exponentials run on the FMA pipe (A/B: 1 beats 0 and 2)
+#define VISTA_TA_EMU 1
+#endif
+constexpr int kTaEmu = VISTA_TA_EMU;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 // smem: tokens T (S x 128 bf16, two 64-column halves; 64 KB at S = 256), a 2-stage ring of (q, k_self)
 // tiles (128 KB), barriers and the per-row statistics
 constexpr int kTOff = 0;
 constexpr int kQKOff = 2 * kTileB;  // stage s: q at kQKOff + 2 s kTileB, k_self at + kTileB
-constexpr int kBarOff = kQKOff + 4 * kTileB;
+// output staging (epilogue): 128 rows of 256 B (v_c in by bulk copy, the bf16 result out by bulk
+// copy, one row per epilogue thread), row stride 272 B so that 8 lanes reading / writing the same
+// 16-B chunk of their rows hit distinct banks; the 16-B pad of row r holds the softmax's
+// (1 / l, p_self / l, lse) of row r
+constexpr int kStgStride = 272;
+constexpr int kStgOff = kQKOff + 4 * kTileB;
+constexpr int kBarOff = kStgOff + 128 * kStgStride;
 
 struct TABars {
     uint64_t qk_full[2], qk_empty[2];
@@ -76,10 +86,11 @@ struct TABars {
     uint64_t p_full, p_free;    // P(t) written / read by PV(t)
     uint64_t o_full, o_empty;   // O(t) computed / read by the epilogue
     uint64_t ml_full, ml_empty;  // the row statistics of tile t, softmax -> epilogue
+    uint64_t v_full;             // the tile's v_c rows in the staging rows (bulk copies)
     uint32_t tmem_base, pad;
-    float st[3][128];  // per row: 1 / l, p_self / l, lse
 };
-constexpr int kSmem = kBarOff + (int)sizeof(TABars) + 1024;
+// no alignment slack: the dynamic shared memory is declared 1024-B aligned (checked at run time)
+constexpr int kSmem = kBarOff + (int)sizeof(TABars);
 static_assert(kSmem <= 232448, "shared memory");
 
 struct TAParams {
@@ -133,8 +144,9 @@ template <int NS>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_target_attend_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
                                const TAParams P) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
+    if (ptx::smem_u32(smem) & 1023u) __trap();  // the SWIZZLE_128B operand tiles need 1024-B alignment
     const uint32_t base = ptx::smem_u32(smem);
     TABars* bars = reinterpret_cast<TABars*>(smem + kBarOff);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -155,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_init(&bars->o_empty, 128);
         ptx::mbar_init(&bars->ml_full, 256);
         ptx::mbar_init(&bars->ml_empty, 128);
+        ptx::mbar_init(&bars->v_full, 128);
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc(&bars->tmem_base, 512);
@@ -244,21 +257,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int64_t row0 = roff[u] + (int64_t)t * 128;
                     const int64_t remr = R - (int64_t)t * 128;
                     const int valid = remr < 128 ? (int)remr : 128;
-                    // v_c of this thread's row (clamped to the tile's last valid row), in flight while
-                    // the softmax and the PV GEMM run
-                    const int vr = row < valid ? row : valid - 1;
-                    const uint4* vs = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(P.v) +
-                                                                     (size_t)(row0 + vr) * rstride + (size_t)h * 128);
-                    uint4 vrow[16];
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) vrow[c] = __ldg(vs + c);
+                    // v_c of this thread's row -> its staging row (bulk copy, in flight while the softmax
+                    // and the PV GEMM run), once this thread's previous bulk store has read the row.
+                    // (One 2-D TMA load / store per tile instead was measured slower: 0.0328 vs 0.0316 ms
+                    // at c2 -- the whole tile waits for its slowest row.)
+                    const uint32_t srow = base + kStgOff + row * kStgStride;
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    if (row < valid) {
+                        ptx::mbar_arrive_expect_tx(&bars->v_full, 256);
+                        ptx::bulk_g2s(srow, reinterpret_cast<const __nv_bfloat16*>(P.v) + (size_t)(row0 + row) * rstride +
+                                                (size_t)h * 128,
+                                      256, &bars->v_full);
+                    } else {
+                        ptx::mbar_arrive(&bars->v_full);
+                    }
                     ptx::mbar_wait(&bars->ml_full, (uint32_t)g & 1u);
                     if (threadIdx.x == 384) TTRACE(9, g);
-                    const float inv = bars->st[0][row], wself = bars->st[1][row], lse = bars->st[2][row];
+                    const float* pad = reinterpret_cast<const float*>(smem + kStgOff + row * kStgStride + 256);
+                    const float inv = pad[0], wself = pad[1], lse = pad[2];
                     ptx::mbar_arrive(&bars->ml_empty);
                     ptx::mbar_wait(&bars->o_full, (uint32_t)g & 1u);
                     if (threadIdx.x == 384) TTRACE(10, g);
                     ptx::tc_fence_after();
+                    ptx::mbar_wait(&bars->v_full, (uint32_t)g & 1u);
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {  // 32 channels at a time
                         uint32_t r[32];
@@ -270,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         float o[32];
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
-                            const uint4 va = vrow[q4 * 4 + c];
+                            const uint4 va = lds128(srow + q4 * 64 + c * 16);
                             const uint32_t vw[4] = {va.x, va.y, va.z, va.w};
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
@@ -280,42 +301,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                             __uint_as_float(r[8 * c + 2 * e + 1]) * inv);
                             }
                         }
-                        if (row < valid) {
-                            const size_t eo = (size_t)(row0 + row) * rstride + (size_t)h * 128 + q4 * 32;
-                            if (P.resid) {
-                                const uint4* rs = reinterpret_cast<const uint4*>(
-                                    reinterpret_cast<const __nv_bfloat16*>(P.resid) + eo);
+                        const size_t eo = (size_t)(row0 + row) * rstride + (size_t)h * 128 + q4 * 32;
+                        if (P.resid && row < valid) {
+                            const uint4* rs = reinterpret_cast<const uint4*>(
+                                reinterpret_cast<const __nv_bfloat16*>(P.resid) + eo);
 #pragma unroll
-                                for (int c = 0; c < 4; ++c) {
-                                    const uint4 ra = __ldg(rs + c);
-                                    const uint32_t rw[4] = {ra.x, ra.y, ra.z, ra.w};
+                            for (int c = 0; c < 4; ++c) {
+                                const uint4 ra = __ldg(rs + c);
+                                const uint32_t rw[4] = {ra.x, ra.y, ra.z, ra.w};
 #pragma unroll
-                                    for (int e = 0; e < 4; ++e) {
-                                        o[8 * c + 2 * e] += __uint_as_float(rw[e] << 16);
-                                        o[8 * c + 2 * e + 1] += __uint_as_float(rw[e] & 0xFFFF0000u);
-                                    }
+                                for (int e = 0; e < 4; ++e) {
+                                    o[8 * c + 2 * e] += __uint_as_float(rw[e] << 16);
+                                    o[8 * c + 2 * e + 1] += __uint_as_float(rw[e] & 0xFFFF0000u);
                                 }
                             }
-                            if (P.out_bf16) {
-                                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + eo);
-#pragma unroll
-                                for (int c = 0; c < 4; ++c)
-                                    dst[c] = make_uint4(ptx::pack_bf16x2(o[8 * c], o[8 * c + 1]),
-                                                        ptx::pack_bf16x2(o[8 * c + 2], o[8 * c + 3]),
-                                                        ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]),
-                                                        ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7]));
-                            } else {
-                                float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + eo);
-#pragma unroll
-                                for (int c = 0; c < 8; ++c)
-                                    dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-                            }
                         }
+                        if (P.out_bf16) {  // back into the staging row (v_c of these channels is read)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                sts128(srow + q4 * 64 + c * 16,
+                                       make_uint4(ptx::pack_bf16x2(o[8 * c], o[8 * c + 1]),
+                                                  ptx::pack_bf16x2(o[8 * c + 2], o[8 * c + 3]),
+                                                  ptx::pack_bf16x2(o[8 * c + 4], o[8 * c + 5]),
+                                                  ptx::pack_bf16x2(o[8 * c + 6], o[8 * c + 7])));
+                        } else if (row < valid) {
+                            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + eo);
+#pragma unroll
+                            for (int c = 0; c < 8; ++c)
+                                dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                        }
+                    }
+                    if (P.out_bf16 && row < valid) {  // the row's 256 B to global in one bulk copy
+                        ptx::fence_proxy_async_smem();
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 256;\n\t"
+                                     "cp.async.bulk.commit_group;" ::"l"(reinterpret_cast<__nv_bfloat16*>(P.out) +
+                                                                          (size_t)(row0 + row) * rstride + (size_t)h * 128),
+                                     "r"(srow)
+                                     : "memory");
                     }
                     if (P.lse && row < valid) P.lse[(size_t)(row0 + row) * H + h] = lse;
                     if (threadIdx.x == 384) TTRACE(11, g);
             }
         }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this thread's bulk stores are complete
     } else if (warp >= 4) {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 144;");
         // softmax: lane quarter wq, row half rh, token half ch
@@ -453,8 +481,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            const float p0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), P.scale_log2, -m));
-                            const float p1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), P.scale_log2, -m));
+                            float p0, p1;
+                            if ((j & 3) < kTaEmu) {  // this pair on the FMA pipe (no masked tokens here)
+                                const uint64_t x2 = ptx::f2_fma(ptx::f2_pack(__uint_as_float(r[2 * j]),
+                                                                             __uint_as_float(r[2 * j + 1])),
+                                                                ptx::f2_pack(P.scale_log2, P.scale_log2),
+                                                                ptx::f2_pack(-m, -m));
+                                ptx::f2_unpack(ptx::exp2_emu2(x2), p0, p1);
+                            } else {
+                                p0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), P.scale_log2, -m));
+                                p1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), P.scale_log2, -m));
+                            }
                             l += p0 + p1;
                             pk[j] = ptx::pack_bf16x2(p0, p1);
                         }
@@ -467,9 +504,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float inv = 1.f / l;
                     if (g >= 1) ptx::mbar_wait(&bars->ml_empty, (uint32_t)(g - 1) & 1u);
                     if (ch == 0) {
-                        bars->st[0][row] = inv;
-                        bars->st[1][row] = pself * inv;
-                        bars->st[2][row] = (m + __log2f(l)) * kLn2;
+                        float* pad = reinterpret_cast<float*>(smem + kStgOff + row * kStgStride + 256);
+                        pad[0] = inv;
+                        pad[1] = pself * inv;
+                        pad[2] = (m + __log2f(l)) * kLn2;
                     }
                     ptx::mbar_arrive(&bars->ml_full);
                     ptx::tmem_wait_st();

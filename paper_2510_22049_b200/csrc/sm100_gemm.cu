@@ -49,6 +49,11 @@ struct GemmParams {
     const __nv_bfloat16* resid;      // [M, N] or NULL (may alias out[0])
 };
 
+// P.out[which] without a dynamically indexed copy of the parameter array in local memory
+__device__ __forceinline__ __nv_bfloat16* out_sel(const GemmParams& P, int which) {
+    return which == 0 ? P.out[0] : which == 1 ? P.out[1] : which == 2 ? P.out[2] : P.out[3];
+}
+
 __device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
     asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
                  "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
@@ -173,10 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- MMA issuer
         int st = 0, ab = 0;
         uint32_t ph = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-            ptx::mbar_wait(&bars->acc_empty[ab], aph[ab] ^ 1);
-            aph[ab] ^= 1;
+            ptx::mbar_wait(&bars->acc_empty[ab], ((aphm >> ab) & 1u) ^ 1);
+            aphm ^= 1u << ab;
             const uint32_t tacc = tmem + ab * 128;
             for (int kb = 0; kb < nk; ++kb) {
                 ptx::mbar_wait(&bars->full[st], ph);
@@ -195,14 +200,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
         const int nw = P.N / P.nsplit;  // columns of one output tensor
         int ab = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
             const int m = t / num_n, n = t % num_n;
             const int col0 = n * 128 + chalf * 64;       // global column of this warp's first column
             const int which = col0 / nw, c_out = col0 % nw;
-            __nv_bfloat16* outp = P.out[which];
-            ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
-            aph[ab] ^= 1;
+            __nv_bfloat16* outp = out_sel(P, which);
+            ptx::mbar_wait(&bars->acc_full[ab], ((aphm >> ab) & 1u));
+            aphm ^= 1u << ab;
             ptx::tc_fence_after();
             store_block64(P, tmem + lane_bits + ab * 128 + chalf * 64, m * 128 + wq * 32, lane, outp, nw, col0, c_out);
             ptx::tc_fence_before();
@@ -295,10 +300,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // ---------------- MMA issuer (leader CTA)
         int st = 0, ab = 0;
         uint32_t ph = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         for (int t = pair; t < num_tiles; t += npairs) {
-            ptx::mbar_wait(&bars->acc_empty[ab], aph[ab] ^ 1);
-            aph[ab] ^= 1;
+            ptx::mbar_wait(&bars->acc_empty[ab], ((aphm >> ab) & 1u) ^ 1);
+            aphm ^= 1u << ab;
             const uint32_t tacc = tmem + ab * 256;
             for (int kb = 0; kb < nk; ++kb) {
                 ptx::mbar_wait(&bars->full[st], ph);
@@ -318,18 +323,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int nw = P.N / P.nsplit;
         const uint32_t acc_empty_l = ptx::mapa(ptx::smem_u32(&bars->acc_empty[0]), 0);
         int ab = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         for (int t = pair; t < num_tiles; t += npairs) {
             const int m = t / num_n, n = t % num_n;
-            ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
-            aph[ab] ^= 1;
+            ptx::mbar_wait(&bars->acc_full[ab], ((aphm >> ab) & 1u));
+            aphm ^= 1u << ab;
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int sb = 0; sb < 2; ++sb) {
                 const int col0 = n * 256 + cq * 128 + sb * 64;
                 const int which = col0 / nw, c_out = col0 % nw;
                 store_block64(P, tmem + lane_bits + ab * 256 + cq * 128 + sb * 64, m * 256 + rank * 128 + wq * 32,
-                              lane, P.out[which], nw, col0, c_out);
+                              lane, out_sel(P, which), nw, col0, c_out);
             }
             ptx::tc_fence_before();
             __syncwarp();

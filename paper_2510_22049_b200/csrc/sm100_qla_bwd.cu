@@ -215,14 +215,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         int ab = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         int k = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             ptx::mbar_wait(&bars->dz_full, k & 1);
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->k_ready[stage], phase);
-                ptx::mbar_wait(&bars->acc_empty[ab], aph[ab] ^ 1);
-                aph[ab] ^= 1;
+                ptx::mbar_wait(&bars->acc_empty[ab], ((aphm >> ab) & 1u) ^ 1);
+                aphm ^= 1u << ab;
                 ptx::tc_fence_after();
                 issue_tile_d(stage, ab, tmem, base);
                 ptx::mma_commit_w(&bars->acc_full[ab]);
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = wq * 32 + lane;    // item row within the tile = TMEM lane
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
         int ab = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         // Coalesced row stores (see sm100_softmax.cu store_rows_coalesced): the 32 packed words of a
         // thread's 64-column row segment go back into the (already read) accumulator columns at
         // tcol in a permuted order and come out with the 16x256b shape, a quad of threads then
@@ -292,8 +292,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 8; ++q) kraw[q] = __ldg(src + q);
             }
-            ptx::mbar_wait(&bars->acc_full[eab], aph[eab]);
-            aph[eab] ^= 1;
+            ptx::mbar_wait(&bars->acc_full[eab], ((aphm >> eab) & 1u));
+            aphm ^= 1u << eab;
             ptx::tc_fence_after();
             if constexpr (kKp) {  // phi1'(K) of this row's 64 columns from the stage (swizzled 16-B chunks)
                 const uint32_t kp = base + est * kStageBytes + 2 * kTile + chalf * kHalf + row * 128;

@@ -264,14 +264,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- MMA issuer
         int stage = 0, ab = 0;
         uint32_t phase = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         int k = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             ptx::mbar_wait(&bars->w_full[k & 1], (uint32_t)(k >> 1) & 1u);
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->q_ready[stage], phase);
-                ptx::mbar_wait(&bars->acc_empty[ab], aph[ab] ^ 1);
-                aph[ab] ^= 1;
+                ptx::mbar_wait(&bars->acc_empty[ab], ((aphm >> ab) & 1u) ^ 1);
+                aphm ^= 1u << ab;
                 ptx::tc_fence_after();
                 const uint32_t tacc = tmem + ab * 128;
                 issue_tile_d<DELTA>(stage, tacc, base, (k & 1) * kTile);
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
         const size_t rstride = (size_t)P.H * 128;  // elements between rows
         int ab = 0, stage = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         uint32_t phase = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             const int64_t R = P.row_offsets[it.u + 1] - P.row_offsets[it.u];
@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < 8; ++c) vrow[c] = __ldg(vs + c);
                 }
-                ptx::mbar_wait(&bars->acc_full[ab], aph[ab]);
-                aph[ab] ^= 1;
+                ptx::mbar_wait(&bars->acc_full[ab], ((aphm >> ab) & 1u));
+                aphm ^= 1u << ab;
                 ptx::tc_fence_after();
                 const uint32_t tc = tmem + lane_bits + ab * 128 + chalf * 64;
                 float o[64];

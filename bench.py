@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "history items summarized/sec (S=256,d=128) + % bf16 tensor peak, 1/2/4/8 GPU"
 METRIC_STAGE2 = "stage-2 candidates scored/sec over the cached int8 summary tokens (NEXT-4; not the headline metric)"
+L2_BYTES = 126 * 1024 * 1024  # B200 L2 (the timing rule: inputs larger than L2, or rotated copies)
 TARGETS_PER_USER = 256  # --qla-rows target: candidate rows per user (NEXT-4)
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 
@@ -389,6 +390,24 @@ def run_own(args, rank, world, local_rank):
         B = B_all
     path = vista.vista_dispatch_name(vista.make_desc(B, S, H, d, in_dtype=vista.BF16, attn=attn))
 
+    # Timing rule: no step may find its inputs in L2 from the previous step.  Workloads whose inputs
+    # fit in L2 (stage 2, target rows: ~70 MB) rotate over R device copies, R x inputs > 3 x L2.
+    in_bytes = sum(x.numel() * x.element_size() for x in inputs if isinstance(x, torch.Tensor))
+    l2_note = f"inputs {in_bytes / 1e9:.2f} GB/GPU > 126 MB L2, no flush"
+    if mode == "by_user" and 0 < in_bytes < 2 * L2_BYTES:
+        n_rot = min(16, -(-3 * L2_BYTES // in_bytes))
+        rot = [inputs] + [[x.clone() if isinstance(x, torch.Tensor) else x for x in inputs] for _ in range(n_rot - 1)]
+        rot_ctr = [0]
+        base_step = step
+
+        def step(ins=None):
+            if ins is None:
+                ins = rot[rot_ctr[0] % n_rot]
+                rot_ctr[0] += 1
+            return base_step(ins)
+        l2_note = (f"inputs {in_bytes / 1e6:.1f} MB/GPU < L2: the steps rotate over {n_rot} device copies "
+                   f"({n_rot * in_bytes / 1e6:.0f} MB > 126 MB L2), no flush")
+
     # warm-up (eager: also initializes NCCL communicators and the library's per-device state)
     for _ in range(max(args.warmup, 3)):
         step()
@@ -655,7 +674,7 @@ def run_own(args, rank, world, local_rank):
         "data": "synthetic (seeded counter-based generator, bf16-exact grid values; synth/)",
         "config": {"workload": wdesc, "users_per_gpu": B, "items_per_gpu": total, "S": S, "d": d, "H": H,
                    "attn": args.attn, "parallelism": parallel, "mode": mode,
-                   "path": path, "l2": f"inputs {kv_bytes / 1e9:.2f} GB/GPU > 126 MB L2, no flush",
+                   "path": path, "l2": l2_note,
                    "pct_bf16_tensor_peak": round(100 * tflops / pk["bf16_tflops"], 2)},
         "roofline": roof,
         "clocks": clocks,

@@ -185,6 +185,20 @@ __device__ __forceinline__ void issue_tile_d(int stage, uint32_t tacc, uint32_t 
     }
 }
 
+#ifdef VISTA_TRACE  // per CTA (globaltimer): start, after the PDL wait, first W ready, first tile's MMA
+                    // issued, first tile stored, end
+__device__ unsigned long long g_rows_cta[160][6];
+__device__ __forceinline__ unsigned long long rows_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define RTRACE(slot, cond) \
+    do { if ((cond) && blockIdx.x < 160) g_rows_cta[blockIdx.x][slot] = rows_gtime(); } while (0)
+#else
+#define RTRACE(slot, cond) do { } while (0)
+#endif
+
 template <int PHI1, bool DELTA>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_qla_rows_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
@@ -199,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cta = blockIdx.x, num_ctas = gridDim.x;
     const int HG = P.H;
+    RTRACE(0, threadIdx.x == 0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&bars->q_full[s], 1);
@@ -224,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // PDL: the prologue above overlapped the tile scan; its results (uts) and everything before it
     // on the stream are visible after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    RTRACE(1, threadIdx.x == 0);
 
     ItemIter iter;
     iter.init(P.uts, P.B, HG, cta, num_ctas, true);  // every role walks with full warps
@@ -268,8 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int k = 0;
         while (iter.next(it, P.uts, P.B, HG)) {
             ptx::mbar_wait(&bars->w_full[k & 1], (uint32_t)(k >> 1) & 1u);
+            RTRACE(2, k == 0 && lane == 0);
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->q_ready[stage], phase);
+                RTRACE(3, k == 0 && t == it.t0 && lane == 0);
                 ptx::mbar_wait(&bars->acc_empty[ab], ((aphm >> ab) & 1u) ^ 1);
                 aphm ^= 1u << ab;
                 ptx::tc_fence_after();
@@ -311,6 +329,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = wq * 32 + lane;    // row within the tile = TMEM lane
         const uint32_t lane_bits = (uint32_t)(wq * 32) << 16;
         const size_t rstride = (size_t)P.H * 128;  // elements between rows
+#ifdef VISTA_TRACE
+        bool g_first = true;
+#endif
         int ab = 0, stage = 0;
         uint32_t aphm = 0;  // accumulator phases, bit b for buffer b (no local-memory array)
         uint32_t phase = 0;
@@ -406,6 +427,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&bars->acc_empty[ab]);
+                RTRACE(4, threadIdx.x == 256 && g_first);
+#ifdef VISTA_TRACE
+                g_first = false;
+#endif
                 ab ^= 1;
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
@@ -413,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    RTRACE(5, threadIdx.x == 0);
     if (warp == 1) ptx::tmem_dealloc(tmem, 256);
 }
 
@@ -531,3 +557,10 @@ cudaError_t launch_qla_rows_simt(const Problem& p, const float* z, const int64_t
 }
 
 }  // namespace vista
+
+#ifdef VISTA_TRACE
+extern "C" int vista_debug_rows_cta(void* host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, vista::g_rows_cta, bytes < sizeof(vista::g_rows_cta) ? bytes : sizeof(vista::g_rows_cta));
+}
+#endif
+

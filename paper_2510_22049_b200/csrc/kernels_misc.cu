@@ -63,6 +63,18 @@ __device__ __forceinline__ void lse_store(const OutSpec& o, int S, int H, int u,
 }
 
 // ---------------------------------------------------------------------------------------------
+#ifdef VISTA_TRACE
+__device__ unsigned long long g_scan_end;  // globaltimer when the last tile scan finished
+}  // namespace
+}  // namespace vista
+extern "C" unsigned long long vista_debug_scan_end() {
+    unsigned long long t = 0;
+    cudaMemcpyFromSymbol(&t, vista::g_scan_end, sizeof(t));
+    return t;
+}
+namespace vista {
+namespace {
+#endif
 __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, int64_t* __restrict__ uts, OutSpec outs,
                                   int S, int H, int d, int softmax, float* __restrict__ zbuf) {
     __shared__ int64_t wsum[32];
@@ -138,6 +150,14 @@ __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, in
             }
         }
     }
+#ifdef VISTA_TRACE
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_scan_end = t;
+    }
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------

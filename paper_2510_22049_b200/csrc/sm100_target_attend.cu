@@ -20,11 +20,18 @@
 //   warp 3       PV GEMM O(t) = P(t) T once P(t) is written and the epilogue has read O(t - 1)
 //   warps 4-11   softmax, two threads per candidate row (tokens [0, S/2) / [S/2, S), the 16x32bx2
 //                TMEM shape): the self logit q_c . k_c from the staged tiles, a two-pass softmax over
-//                [tokens; self]; also dequantize each item's tokens once its predecessor's last PV is done
+//                [tokens; self] (1 of every 4 exponential pairs on the FMA pipe); also dequantize each
+//                item's tokens once its predecessor's last PV is done (int8 -> f32 by PRMT + FADD2, no
+//                I2F) and pull the next item's codes into L2
 //   warps 12-15  epilogue, one thread per row: (O + p_self v_c) / l [+ resid] -> bf16 / f32 rows, lse;
-//                v_c rows prefetched from global memory; O released after its last TMEM load
-// (Staging the jagged tables in shared memory first was measured slower: 0.0370 vs 0.0354 ms at c2 --
-// the block-wide barrier after the table load delays every role, and the larger carve-out shrinks L1.)
+//                v_c in and the bf16 row out by per-row 256-B bulk copies through a staging tile
+//                (272-B row stride: bank-conflict free; the row pad carries 1/l, p_self/l, lse);
+//                O released after its last TMEM load
+// Registers (setmaxnreg): control warps 64, softmax 144, epilogue 160 -- the epilogue has its own role
+// branch so the iterator state stays in registers.
+// (Measured slower and not kept: staging the jagged tables in shared memory, 0.0370 vs 0.0354 ms at
+// c2; one 2-D TMA load / store of the whole staging tile instead of per-row bulk copies, 0.0328 vs
+// 0.0316 ms.)
 // simt_target_attend_kernel: CUDA cores, one warp per (candidate, head), any S >= 1, d <= 128, f32 or
 // bf16 -- the shapes the tcgen05 kernel does not take.
 #include <cuda.h>

@@ -81,6 +81,9 @@ __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, in
     __shared__ int64_t carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     asm volatile("griddepcontrol.launch_dependents;");  // PDL: the main kernel may start its prologue
+    // launched with PDL itself (its launch overlaps the previous kernel's tail): uts and the outputs
+    // may still be read by that kernel, so wait for it before writing anything
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid == 0) {
         carry = 0;
         uts[0] = 0;
@@ -776,9 +779,8 @@ __global__ void gather_seed_rows_kernel(const __nv_bfloat16* __restrict__ x, con
 
 // ============================================================================== launchers
 cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf) {
-    user_tiles_kernel<<<1, 1024, 0, p.stream>>>(p.offsets, p.B, uts, p.outs, p.S, p.H, p.d,
-                                                 p.attn == VISTA_SOFTMAX, zbuf);
-    return cudaGetLastError();
+    return launch_pdl(user_tiles_kernel, dim3(1), dim3(1024), 0, p.stream, p.offsets, p.B, uts, p.outs, p.S, p.H,
+                      p.d, (int)(p.attn == VISTA_SOFTMAX), zbuf);
 }
 
 cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, char* ws) {

@@ -28,6 +28,10 @@ __global__ void __launch_bounds__(256) qla_prep_w_kernel(const float* __restrict
                                                          const int64_t* __restrict__ offsets,
                                                          const int64_t* __restrict__ user_len, int H, int phi2,
                                                          int normalize, uint8_t* __restrict__ wbuf) {
+    // PDL (rows path): the launch overlaps the previous kernel's tail; Z may come from it and W may
+    // still be read by it
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int unit = blockIdx.x >> 2, u = unit / H;
     const int r = (blockIdx.x & 3) * 32 + threadIdx.x / 8, c = (threadIdx.x % 8) * 16;
     const int64_t N = user_len ? user_len[u] : (offsets[u + 1] - offsets[u]);
@@ -173,8 +177,8 @@ __global__ void __launch_bounds__(128) sm100_qla_finalize_kernel(const uint8_t* 
 
 // W_u operands for the rows path (sm100_qla_rows.cu): W = phi2(Z / N_u) from one state [B,H,d,d]
 cudaError_t launch_qla_prep_w(const Problem& p, const float* z, uint8_t* wbuf, const int64_t* user_len) {
-    qla_prep_w_kernel<<<p.B * p.H * 4, 256, 0, p.stream>>>(z, 1, 0, p.offsets, user_len, p.H, p.phi2, p.normalize, wbuf);
-    return cudaGetLastError();
+    return launch_pdl(qla_prep_w_kernel, dim3(p.B * p.H * 4), dim3(256), 0, p.stream, z, 1, (int64_t)0, p.offsets,
+                      user_len, p.H, p.phi2, p.normalize, wbuf);
 }
 
 size_t sm100_qla_finalize_workspace(const Problem& p) {

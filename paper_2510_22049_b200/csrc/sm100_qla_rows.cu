@@ -187,7 +187,7 @@ __device__ __forceinline__ void issue_tile_d(int stage, uint32_t tacc, uint32_t 
 
 #ifdef VISTA_TRACE  // per CTA (globaltimer): start, after the PDL wait, first W ready, first tile's MMA
                     // issued, first tile stored, end
-__device__ unsigned long long g_rows_cta[160][6];
+__device__ unsigned long long g_rows_cta[160][8];
 __device__ __forceinline__ unsigned long long rows_gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -314,11 +314,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             for (int t = it.t0; t < it.t1; ++t) {
                 ptx::mbar_wait(&bars->q_full[stage], phase);
+                RTRACE(6, threadIdx.x == 128 && t == it.t0 && stage == 0 && phase == 0);
                 const uint32_t sb = base + stage * G::kStageBytes;
                 if constexpr (DELTA) dr_smem[stage * 128 + r] = xform_row<PHI1, true>(sb, sb + kTile, r) * inv_n;
                 else xform_tile<PHI1>(sb, r);
                 ptx::fence_proxy_async_smem();
                 ptx::mbar_arrive(&bars->q_ready[stage]);
+                RTRACE(7, threadIdx.x == 128 && t == it.t0 && stage == 0 && phase == 0);
                 if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
         }

@@ -307,11 +307,7 @@ __device__ __forceinline__ float exp_half(const uint32_t (&r)[2][32], float sl2,
                 ptx::f2_pack(__uint_as_float(r[c][2 * j]), __uint_as_float(r[c][2 * j + 1])), sl2x2, negx2);
             float x0, x1;
             ptx::f2_unpack(x2, x0, x1);
-#ifdef VISTA_FAKE_EXP  // timing experiment only (wrong results): the exponential off the MUFU pipe
-            const uint64_t p2 = ptx::f2_fma(x2, sl2x2, sl2x2);
-#else
             const uint64_t p2 = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
-#endif
             acc[j & 1] = ptx::f2_add(acc[j & 1], p2);
             float p0, p1;
             ptx::f2_unpack(p2, p0, p1);

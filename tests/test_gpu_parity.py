@@ -1029,6 +1029,34 @@ def test_target_attend_simt(cuda_lib, S, d, dtype):
     _ta_check(vista, 3, S, 2, d, [5, 0, 9], dtype, 82, True, vista.F32, tol, ltol)
 
 
+@pytest.mark.gpu
+def test_target_attend_wide_logit_range(cuda_lib):
+    """A token far above the row's first scores (here ~775 log2 units): the one-pass softmax's
+    provisional offset would overflow, so the kernel must take its fallback (the row max, the pass
+    again) and still match the oracle."""
+    vista = cuda_lib
+    rng = np.random.default_rng(85)
+    B, S, H, d = 3, 256, 2, 128
+    codes, ts, tz, q, k, v, rs, roff = _ta_case(rng, B, S, H, d, [130, 1, 256], "bf16")
+    q = np.abs(q) * 0.5 + 0.5  # positive queries: the special tokens score high for every candidate
+    codes[:, 100] = 127
+    ts[:, 100] = 0.5
+    tz[:, 100] = 0.0
+    dev = lambda x: to_dev(x, "bf16")  # noqa: E731
+    out, lse = vista.target_attend(torch.from_numpy(codes).cuda(), torch.from_numpy(ts).cuda(),
+                                   torch.from_numpy(tz).cuda(), dev(q), dev(k), dev(v), torch.from_numpy(roff).cuda())
+    torch.cuda.synchronize()
+    ref, ref_lse = oracle.target_attend(codes, ts, tz, q, k, v, roff)
+    g = out.float().cpu().numpy()
+    assert np.all(np.isfinite(g)) and np.all(np.isfinite(lse.cpu().numpy()))
+    for u in range(B):
+        a, b = roff[u], roff[u + 1]
+        for h in range(H):
+            assert block_err(g[a:b, h], ref[a:b, h]) <= 2e-2
+            # the logits are ~1e3 (natural units): the bf16 token rounding moves them by <= 2^-8 relative
+            assert np.all(np.abs(lse[a:b, h].cpu().numpy() - ref_lse[a:b, h]) <= 2.0 ** -8 * np.abs(ref_lse[a:b, h]) + 1e-3)
+
+
 def test_target_attend_candidate_independence_bitwise(cuda_lib):
     """PAPER.md:156 "the candidates cannot attend each other": a candidate's output is bitwise the same
     whatever the other candidates of the batch (here: their values replaced), on the tcgen05 path."""

@@ -345,6 +345,25 @@ vista_status_t vista_exchange_wait(int32_t world, const uint32_t* flags, const u
 vista_status_t vista_exchange_ack(int32_t world, int32_t rank, uint32_t* const* acks, const uint32_t* epoch,
                                   void* stream);
 
+/*
+ * The same exchange fused into the softmax partial (SURVEY.md 8(e) phase 2: "the partial kernel's
+ * epilogue writes directly into peer receive buffers ... removing the collective launch").  Replaces
+ * vista_summarize_partial + vista_exchange_push: waits until acks[r] >= *epoch for every r, then
+ * computes this rank's partial exactly as vista_summarize_partial would, but its kernels (the
+ * attention epilogue, the split-unit slot merge, the empty-user fill) store every row of O_p and
+ * lse_p straight into slot `rank` of every rank's receive buffer (recv_o[r] + rank*n_o,
+ * recv_lse[r] + rank*n_lse; NVLink stores for peers).  Continue with vista_exchange_signal, _wait,
+ * vista_summarize_merge over the local receive buffer, and vista_exchange_ack.  desc->attn must be
+ * VISTA_SOFTMAX (VISTA_ERR_UNSUPPORTED otherwise); recv_o[r] 16-B aligned (32-B for 256-bit stores),
+ * recv_lse[r] 4-B aligned; other arguments as in vista_summarize_partial and vista_exchange_push.
+ */
+vista_status_t vista_summarize_partial_peers(const vista_desc_t* desc, const void* q, const void* k,
+                                             const void* v, const int64_t* offsets, int64_t total_len,
+                                             int32_t world, int32_t rank, float* const* recv_o,
+                                             float* const* recv_lse, const uint32_t* acks,
+                                             const uint32_t* epoch, void* workspace, size_t workspace_bytes,
+                                             void* stream);
+
 /* Bytes of device workspace vista_summarize_merge needs for this descriptor (0 for softmax). */
 vista_status_t vista_summarize_merge_workspace_size(const vista_desc_t* desc, size_t* bytes);
 

@@ -31,8 +31,9 @@ __all__ = [
     "vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state", "qla_rows_from_state",
     "vista_target_attend_workspace_size", "vista_target_attend", "target_attend",
     "vista_summarize_layers_workspace_size", "vista_summarize_layers", "summarize_layers",
-    "summarize", "summarize_partial", "summarize_merge", "summarize_bwd", "qla_rows",
+    "summarize", "summarize_partial", "summarize_partial_peers", "summarize_merge", "summarize_bwd", "qla_rows",
     "vista_ipc_get_handle", "vista_ipc_open_handle", "vista_ipc_close", "vista_exchange_push",
+    "vista_summarize_partial_peers",
     "vista_exchange_signal", "vista_exchange_wait", "vista_exchange_ack",
     "SOFTMAX", "QLA", "F32", "BF16", "ACT",
 ]
@@ -130,8 +131,9 @@ def load():
     lib.vista_exchange_signal.argtypes = [i32, i32, PP, P, P]
     lib.vista_exchange_wait.argtypes = [i32, P, P, P]
     lib.vista_exchange_ack.argtypes = [i32, i32, PP, P, P]
+    lib.vista_summarize_partial_peers.argtypes = [DP, P, P, P, P, i64, i32, i32, PP, PP, P, P, P, sz, P]
     for f in ("vista_ipc_get_handle", "vista_ipc_open_handle", "vista_ipc_close", "vista_exchange_push",
-              "vista_exchange_signal", "vista_exchange_wait", "vista_exchange_ack"):
+              "vista_exchange_signal", "vista_exchange_wait", "vista_exchange_ack", "vista_summarize_partial_peers"):
         getattr(lib, f).restype = ctypes.c_int
     for f in ("vista_qla_rows_from_state_workspace_size", "vista_qla_rows_from_state",
               "vista_target_attend_workspace_size", "vista_target_attend",
@@ -452,6 +454,18 @@ def summarize_partial(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=N
     return po, pl
 
 
+def summarize_partial_peers(q, k, v, offsets, total_len, exchange, *, scale=None, workspace=None, stream=None):
+    """Softmax partial over one history shard with the split-L exchange fused into its stores: the rows
+    land in slot `exchange.rank` of every rank's receive buffer (exchange: a dist.PeerExchange).
+    Returns nothing; follow with exchange.signal_wait() and the merge."""
+    if total_len is None:
+        total_len = k.shape[0]
+    desc = _desc_for(q, k, offsets, SOFTMAX, scale, "silu", "silu", True, None)
+    ws, need = _workspace(desc, total_len, q.device, workspace, 0)
+    vista_summarize_partial_peers(desc, q, k, v, offsets, total_len, exchange.world, exchange.rank, exchange.o_ptrs,
+                                  exchange.lse_ptrs, exchange.acks, exchange.epoch, ws, ws.numel(), stream)
+
+
 def summarize_bwd(q, k, v, offsets, total_len, dout, *, attn=QLA, phi1="silu", phi2="silu", normalize=True,
                   out=None, lse=None, z=None, workspace=None, stream=None):
     """Backward of summarize (NEXT-2): returns (dq, dk, dv).  dq float32 [S,H,d] (shared seeds,
@@ -573,6 +587,17 @@ def vista_exchange_push(world, rank, part_o, n_o, part_lse, n_lse, recv_o_ptrs, 
     _check(load().vista_exchange_push(int(world), int(rank), _ptr(part_o), int(n_o), _ptr(part_lse), int(n_lse),
                                       _ptr_array(recv_o_ptrs), _ptr_array(recv_lse_ptrs) if recv_lse_ptrs else None,
                                       _ptr(acks), _ptr(epoch), _stream(stream)), "vista_exchange_push")
+
+
+def vista_summarize_partial_peers(desc, q, k, v, offsets, total_len, world, rank, recv_o_ptrs, recv_lse_ptrs, acks,
+                                  epoch, workspace, workspace_bytes, stream=None):
+    """The softmax partial with the exchange fused into its stores (include/vista.h): every row goes
+    straight into slot `rank` of every rank's receive buffer."""
+    _check(load().vista_summarize_partial_peers(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                                                int(total_len), int(world), int(rank), _ptr_array(recv_o_ptrs),
+                                                _ptr_array(recv_lse_ptrs), _ptr(acks), _ptr(epoch), _ptr(workspace),
+                                                int(workspace_bytes), _stream(stream)),
+           "vista_summarize_partial_peers")
 
 
 def vista_exchange_signal(world, rank, flag_ptrs, epoch, stream=None):

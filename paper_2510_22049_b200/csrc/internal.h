@@ -15,6 +15,8 @@ constexpr int kTile = 128;  // history items per tile (= TMA box rows = MMA N of
 constexpr int kMaxPersistentCtas = 159;
 constexpr int kMaxExchangeRanks = 8;  // p2p_exchange.cu: ranks of one node
 void count_launches(unsigned n);     // the library's launch counter (vista_launch_counter)
+// p2p_exchange.cu: spin until every rank acknowledged the current epoch (the fused exchange's first step)
+cudaError_t launch_exchange_wait_acks(int world, const uint32_t* acks, const uint32_t* epoch, cudaStream_t stream);
 
 enum OutMode : int { OUT_FINAL = 0, OUT_PARTIAL = 1 };
 
@@ -59,6 +61,16 @@ struct OutSpec {
     float* qzp;
 };
 
+// The fused split-L exchange (vista_summarize_partial_peers): n > 0 -> every partial-mode row and lse
+// (softmax) is stored to these n destinations instead of OutSpec out / lse -- the node's receive
+// buffers, already offset to this rank's slot.  A separate kernel argument (not in OutSpec), so the
+// kernels that never see it compile exactly as before.
+struct PeerSpec {
+    int n;
+    float* o[kMaxExchangeRanks];
+    float* lse[kMaxExchangeRanks];
+};
+
 // Everything a launch needs (filled by the ABI layer after validation).
 struct Problem {
     int B, S, H, d;
@@ -73,9 +85,12 @@ struct Problem {
     const void* v;
     const int64_t* offsets;
     OutSpec outs;
+    PeerSpec peers;            // fused exchange destinations (softmax partial); n = 0: none
     cudaStream_t stream;
     int num_sms;
 };
+
+
 
 // Workspace carve-up (all offsets 256-B aligned).
 struct Workspace {

@@ -76,7 +76,8 @@ namespace vista {
 namespace {
 #endif
 __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, int64_t* __restrict__ uts, OutSpec outs,
-                                  int S, int H, int d, int softmax, float* __restrict__ zbuf) {
+                                  int S, int H, int d, int softmax, float* __restrict__ zbuf,
+                                  const __grid_constant__ PeerSpec pe) {
     __shared__ int64_t wsum[32];
     __shared__ int64_t carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -129,6 +130,15 @@ __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, in
             const int uu = base + warp * 32 + __ffs(m) - 1;
             m &= m - 1;
             if (softmax) {
+                if (outs.mode == OUT_PARTIAL && pe.n > 0) {  // fused exchange: every receive buffer
+#pragma unroll
+                    for (int r = 0; r < kMaxExchangeRanks; ++r) {
+                        if (r >= pe.n) break;
+                        for (size_t e = lane; e < n_sm; e += 32) pe.o[r][(size_t)uu * n_sm + e] = 0.f;
+                        for (int e = lane; e < H * S; e += 32) pe.lse[r][(size_t)uu * H * S + e] = -INFINITY;
+                    }
+                    continue;
+                }
                 if (outs.mode == OUT_PARTIAL) {
                     float* o = reinterpret_cast<float*>(outs.out) + (size_t)uu * n_sm;
                     for (size_t e = lane; e < n_sm; e += 32) o[e] = 0.f;
@@ -190,6 +200,34 @@ __device__ __forceinline__ void out_store4(const OutSpec& o, int S, int H, int u
     }
 }
 
+// The fused split-L exchange (PeerSpec, vista_summarize_partial_peers): a partial-mode row / lse to
+// every rank's receive buffer instead of outs.
+__device__ __forceinline__ void out_store4_p(const OutSpec& o, const PeerSpec& pe, int S, int H, int u, int h, int i,
+                                             int c, float4 v) {
+    if (o.mode == OUT_PARTIAL && pe.n > 0) {
+        const size_t idx = (((size_t)u * H + h) * S + i) * 128 + c;
+#pragma unroll
+        for (int r = 0; r < kMaxExchangeRanks; ++r) {
+            if (r >= pe.n) break;
+            *reinterpret_cast<float4*>(pe.o[r] + idx) = v;
+        }
+        return;
+    }
+    out_store4(o, S, H, u, h, i, c, v);
+}
+__device__ __forceinline__ void lse_store_p(const OutSpec& o, const PeerSpec& pe, int S, int H, int u, int h, int i,
+                                            float val) {
+    if (o.mode == OUT_PARTIAL && pe.n > 0) {
+#pragma unroll
+        for (int r = 0; r < kMaxExchangeRanks; ++r) {
+            if (r >= pe.n) break;
+            pe.lse[r][((size_t)u * H + h) * S + i] = val;
+        }
+        return;
+    }
+    lse_store(o, S, H, u, h, i, val);
+}
+
 // LSE merge of the run of partial slots of each split unit.  Block = (slot s, 32 rows), 8 warps x
 // 4 rows, lanes over 128 channels (float4); blocks whose slot does not start a run exit at once.
 // Warp 0 lists the run's slots (lane-parallel over 32 positions at a time: a run ends at the first
@@ -216,7 +254,8 @@ struct MergeSmem {
 __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __restrict__ slot_unit, int num_slots,
                                                                   const float* __restrict__ slot_o,
                                                                   const float* __restrict__ slot_lse, int rows,
-                                                                  OutSpec outs, int S, int H, int G) {
+                                                                  OutSpec outs, int S, int H, int G,
+                                                                  const __grid_constant__ PeerSpec pe) {
     extern __shared__ __align__(128) uint8_t merge_smem_raw[];
     MergeSmem& sm = *reinterpret_cast<MergeSmem*>(merge_smem_raw);
     // PDL: launched while the summarization kernel runs; its slots are complete after this
@@ -324,7 +363,7 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
         const float inv = 1.f / l[r];
         const float4 v = make_float4(acc[r].x * inv, acc[r].y * inv, acc[r].z * inv, acc[r].w * inv);
         const int i = g * rows + row;
-        out_store4(outs, S, H, u, h, i, lane * 4, v);
+        out_store4_p(outs, pe, S, H, u, h, i, lane * 4, v);
         if (outs.codes) {  // NEXT-1 fused int8 export of the merged row, as stored
             float x[4] = {v.x, v.y, v.z, v.w};
             if (outs.out_bf16)
@@ -346,7 +385,7 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
                 outs.qzp[orow] = z;
             }
         }
-        if (lane == 0) lse_store(outs, S, H, u, h, i, M[r] + logf(l[r]));
+        if (lane == 0) lse_store_p(outs, pe, S, H, u, h, i, M[r] + logf(l[r]));
     }
 }
 
@@ -780,7 +819,7 @@ __global__ void gather_seed_rows_kernel(const __nv_bfloat16* __restrict__ x, con
 // ============================================================================== launchers
 cudaError_t launch_user_tiles(const Problem& p, int64_t* uts, float* zbuf) {
     return launch_pdl(user_tiles_kernel, dim3(1), dim3(1024), 0, p.stream, p.offsets, p.B, uts, p.outs, p.S, p.H,
-                      p.d, (int)(p.attn == VISTA_SOFTMAX), zbuf);
+                      p.d, (int)(p.attn == VISTA_SOFTMAX), zbuf, p.peers);
 }
 
 cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, char* ws) {
@@ -792,7 +831,7 @@ cudaError_t launch_merge_softmax_slots(const Problem& p, const Workspace& w, cha
                       reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots,
                       reinterpret_cast<const float*>(ws + w.slot_o_off),
                       reinterpret_cast<const float*>(ws + w.slot_lse_off), w.rows_per_unit, p.outs, p.S, p.H,
-                      p.S / w.rows_per_unit);
+                      p.S / w.rows_per_unit, p.peers);
 }
 
 cudaError_t launch_merge_qla_slots_w(const Problem& p, const Workspace& w, char* ws, uint8_t* wbuf) {

@@ -16,6 +16,9 @@
 //           overwrite its receive buffer in the next push
 // Deadlock-free by construction: every rank runs push, signal, wait, merge, ack in stream order, and
 // a push of epoch e+1 only waits for acks of e, which every rank publishes after its own wait for e.
+// Fused form (softmax): vista_summarize_partial_peers replaces the push -- the ack wait runs first,
+// then the partial's own epilogue / slot-merge / empty-user stores go straight into every rank's
+// receive buffer (slot `rank`) over NVLink; signal, wait, merge and ack as above.
 // Waits spin with a 4-second watchdog trap (a protocol bug becomes a launch error, not a hang).
 #include <cuda_runtime.h>
 
@@ -97,6 +100,13 @@ __global__ void xack_kernel(XPtrs dst, int world, int rank, const uint32_t* epoc
     for (int r = 0; r < world; ++r) st_release_sys(dst.f[r] + rank, e);
 }
 
+// the fused exchange (vista_summarize_partial_peers): before the partial's kernels store into the
+// peers' receive buffers, every peer must have consumed the previous epoch
+__global__ void xwait_acks_kernel(const uint32_t* acks, int world, const uint32_t* epoch) {
+    const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(epoch);
+    if ((int)threadIdx.x < world) spin_until_ge(acks + threadIdx.x, e);
+}
+
 bool fill(XPtrs& x, int world, float* const* o, float* const* l, uint32_t* const* f) {
     std::memset(&x, 0, sizeof(x));
     for (int r = 0; r < world; ++r) {
@@ -109,6 +119,12 @@ bool fill(XPtrs& x, int world, float* const* o, float* const* l, uint32_t* const
 }
 
 }  // namespace
+
+cudaError_t launch_exchange_wait_acks(int world, const uint32_t* acks, const uint32_t* epoch, cudaStream_t stream) {
+    xwait_acks_kernel<<<1, 32, 0, stream>>>(acks, world, epoch);
+    return cudaGetLastError();
+}
+
 }  // namespace vista
 
 using namespace vista;

@@ -193,7 +193,8 @@ __device__ __forceinline__ void st_f32x32(float* dst, const float (&o)[32], bool
 }
 
 // writes 32 consecutive channels [c0, c0+32) of one normalized output row (row within the unit)
-__device__ __forceinline__ void store_row(const Params& P, const Item& it, int slot_base, int row_in_unit,
+template <bool PEERS>
+__device__ __forceinline__ void store_row(const Params& P, const PeerSpec& pe, const Item& it, int slot_base, int row_in_unit,
                                           const float (&o)[32], int c0, int NQrows) {
     const int h = it.hg / P.G, g = it.hg % P.G;
     if (!item_complete(it)) {
@@ -203,8 +204,16 @@ __device__ __forceinline__ void store_row(const Params& P, const Item& it, int s
     }
     const int i = g * NQrows + row_in_unit;
     if (P.outs.mode == OUT_PARTIAL) {
-        st_f32x32(reinterpret_cast<float*>(P.outs.out) + (((size_t)it.u * P.H + h) * P.S + i) * 128 + c0, o,
-                  P.out_v8);
+        const size_t idx = (((size_t)it.u * P.H + h) * P.S + i) * 128 + c0;
+        if constexpr (PEERS) {  // fused exchange: every rank's receive buffer
+#pragma unroll
+            for (int r = 0; r < kMaxExchangeRanks; ++r) {
+                if (r >= pe.n) break;
+                st_f32x32(pe.o[r] + idx, o, P.out_v8);
+            }
+        } else {
+            st_f32x32(reinterpret_cast<float*>(P.outs.out) + idx, o, P.out_v8);
+        }
         return;
     }
     const size_t base = (((size_t)it.u * P.S + i) * P.H + h) * 128 + c0;
@@ -225,15 +234,27 @@ __device__ __forceinline__ void store_row(const Params& P, const Item& it, int s
 }
 
 // lse of one row (natural log): partial slot, partial output or the caller's lse (if any)
-__device__ __forceinline__ void store_lse(const Params& P, const Item& it, int slot_base, int row, float lse,
+template <bool PEERS>
+__device__ __forceinline__ void store_lse(const Params& P, const PeerSpec& pe, const Item& it, int slot_base, int row, float lse,
                                           int NQrows) {
     if (!item_complete(it)) {
         P.slot_lse[(size_t)item_slot(it, slot_base) * NQrows + row] = lse;
         return;
     }
-    if (!P.outs.lse) return;
     const int h = it.hg / P.G, g = it.hg % P.G;
-    P.outs.lse[((size_t)it.u * P.H + h) * P.S + g * NQrows + row] = lse;
+    const size_t idx = ((size_t)it.u * P.H + h) * P.S + g * NQrows + row;
+    if constexpr (PEERS) {
+        if (P.outs.mode == OUT_PARTIAL) {  // fused exchange: every rank's receive buffer
+#pragma unroll
+            for (int r = 0; r < kMaxExchangeRanks; ++r) {
+                if (r >= pe.n) break;
+                pe.lse[r][idx] = lse;
+            }
+            return;
+        }
+    }
+    if (!P.outs.lse) return;
+    P.outs.lse[idx] = lse;
 }
 
 // Start of output row `row` (row within the unit) of item `it`: a partial slot row (f32) for a
@@ -255,7 +276,8 @@ __device__ __forceinline__ char* out_row_ptr(const Params& P, const Item& it, in
 // already read) in a permuted column order and come out again with the 16x256b shape, where the 4
 // threads of a quad hold 128 contiguous bytes of one row: each warp store then writes 8 full
 // 128-B lines.  Column 8g + 2p + e holds word 8p + 2g + e (g < 4) or 32 + 8p + 2(g-4) + e (g >= 4).
-__device__ __forceinline__ void store_rows_coalesced(const Params& P, const Item& it, int slot_base, int row0,
+template <bool PEERS>
+__device__ __forceinline__ void store_rows_coalesced(const Params& P, const PeerSpec& pe, const Item& it, int slot_base, int row0,
                                                      int NQrows, uint32_t tcol_warp, const uint32_t (&v)[64],
                                                      int boff) {
     const int lane = threadIdx.x & 31;
@@ -283,6 +305,21 @@ __device__ __forceinline__ void store_rows_coalesced(const Params& P, const Item
         const uint32_t a1[8] = {r[16], r[17], r[20], r[21], r[24], r[25], r[28], r[29]};
         const uint32_t b0[8] = {r[2], r[3], r[6], r[7], r[10], r[11], r[14], r[15]};
         const uint32_t b1[8] = {r[18], r[19], r[22], r[23], r[26], r[27], r[30], r[31]};
+        if constexpr (PEERS) if (P.outs.mode == OUT_PARTIAL && item_complete(it)) {
+            // fused split-L exchange: the same bytes into every rank's receive buffer (NVLink stores)
+            const size_t da = (size_t)(reinterpret_cast<uintptr_t>(pa) - reinterpret_cast<uintptr_t>(P.outs.out));
+            const size_t db = (size_t)(reinterpret_cast<uintptr_t>(pb) - reinterpret_cast<uintptr_t>(P.outs.out));
+#pragma unroll
+            for (int q = 0; q < kMaxExchangeRanks; ++q) {
+                if (q >= pe.n) break;
+                char* base = reinterpret_cast<char*>(pe.o[q]);
+                st_v8(base + da, a0);
+                st_v8(base + da + 128, a1);
+                st_v8(base + db, b0);
+                st_v8(base + db + 128, b1);
+            }
+            continue;
+        }
         st_v8(pa, a0);
         st_v8(pa + 128, a1);
         st_v8(pb, b0);
@@ -412,10 +449,13 @@ __device__ __forceinline__ void warp_arrive_leader(uint64_t* bar, int rank) {
     }
 }
 
-template <int C, bool PAIR>
+// PEERS: the fused split-L exchange (vista_summarize_partial_peers) -- partial rows to every rank's
+// receive buffer; a separate instantiation so the default kernel carries none of it
+template <int C, bool PAIR, bool PEERS = false>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_softmax_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
-                         const __grid_constant__ CUtensorMap mapV, const Params P) {
+                         const __grid_constant__ CUtensorMap mapV, const Params P,
+                         const __grid_constant__ PeerSpec peers) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem + kQOff;
@@ -833,7 +873,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const size_t orow = ((size_t)it.u * P.S + g * kRows + urow) * P.H + h;
                     i8_export_row_bf16(v, P.outs.codes + orow * 128, P.outs.qscale + orow, P.outs.qzp + orow);
                 }
-                store_rows_coalesced(P, it, cid, rank * 128 + wq * 32, kRows, tO, v, 0);
+                store_rows_coalesced<PEERS>(P, peers, it, cid, rank * 128 + wq * 32, kRows, tO, v, 0);
             } else if (coalesced) {
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
@@ -845,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j) v[c * 32 + j] = __float_as_uint(__uint_as_float(o[j]) * inv_l);
                     }
-                    store_rows_coalesced(P, it, cid, rank * 128 + wq * 32, kRows, tO + hh * 64, v, hh * 256);
+                    store_rows_coalesced<PEERS>(P, peers, it, cid, rank * 128 + wq * 32, kRows, tO + hh * 64, v, hh * 256);
                 }
             } else {
 #pragma unroll
@@ -855,10 +895,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float of[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) of[j] = __uint_as_float(o[j]) * inv_l;
-                    store_row(P, it, cid, urow, of, c * 32, kRows);
+                    store_row<PEERS>(P, peers, it, cid, urow, of, c * 32, kRows);
                 }
             }
-            store_lse(P, it, cid, urow, lse, kRows);
+            store_lse<PEERS>(P, peers, it, cid, urow, lse, kRows);
             ptx::tc_fence_before();
             if constexpr (PAIR) warp_arrive_leader(&bars->o_empty, rank);
             else ptx::mbar_arrive(&bars->o_empty);
@@ -986,8 +1026,15 @@ static cudaError_t launch_c(const Problem& p, const Workspace& w, char* ws) {
     P.q_per_user = p.q_user_stride != 0;
     P.groups = (P.G > 1 && w.num_ctas % P.G == 0) ? P.G : 1;
     P.out_v8 = (reinterpret_cast<uintptr_t>(p.outs.out) & 31) == 0;
+    for (int r = 0; r < p.peers.n; ++r)  // fused exchange: the rows also go to every receive buffer
+        P.out_v8 = P.out_v8 && (reinterpret_cast<uintptr_t>(p.peers.o[r]) & 31) == 0;
     P.slot_v8 = (reinterpret_cast<uintptr_t>(P.slot_o) & 31) == 0;
-    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_softmax_kernel<C, PAIR>), kSmem);
+    // the fused-exchange instantiation only for the softmax partial with peers (not the CTA-pair mode)
+    const bool peers = p.outs.mode == OUT_PARTIAL && p.peers.n > 0;
+    if (PAIR && peers) return cudaErrorNotSupported;  // the CTA-pair mode (off by default) has no fused exchange
+    const void* fn = peers ? reinterpret_cast<const void*>(sm100_softmax_kernel<C, PAIR, !PAIR>)
+                           : reinterpret_cast<const void*>(sm100_softmax_kernel<C, PAIR>);
+    const cudaError_t attr = set_smem_attr(fn, kSmem);
     if (attr != cudaSuccess) return attr;
     cudaLaunchAttribute attrs[2];
     cudaLaunchConfig_t cfg = cluster_config<C>(dim3(C * w.num_ctas), p.stream, attrs);
@@ -995,7 +1042,8 @@ static cudaError_t launch_c(const Problem& p, const Workspace& w, char* ws) {
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
 #endif
-    return cudaLaunchKernelEx(&cfg, sm100_softmax_kernel<C, PAIR>, mq, mk, mv, P);
+    if (peers) return cudaLaunchKernelEx(&cfg, sm100_softmax_kernel<C, PAIR, !PAIR>, mq, mk, mv, P, p.peers);
+    return cudaLaunchKernelEx(&cfg, sm100_softmax_kernel<C, PAIR>, mq, mk, mv, P, p.peers);
 }
 
 #ifdef VISTA_TRACE

@@ -212,7 +212,7 @@ vista_status_t vista_summarize_workspace_size(const vista_desc_t* desc, int64_t 
 
 static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k, const void* v,
                           const int64_t* offsets, int64_t total_len, OutSpec outs, void* workspace,
-                          size_t workspace_bytes, void* stream) {
+                          size_t workspace_bytes, void* stream, const PeerSpec* peers = nullptr) {
     vista_status_t st = validate_desc(desc);
     if (st != VISTA_OK) return st;
     if (total_len < 0) return VISTA_ERR_INVALID;
@@ -228,6 +228,10 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
     p.v = v;
     p.offsets = offsets;
     p.outs = outs;
+    if (peers) {
+        p.peers = *peers;  // the fused exchange: tcgen05 softmax path only
+        if (choose_path(p) != PATH_SM100_SOFTMAX) return VISTA_ERR_UNSUPPORTED;
+    }
     p.stream = reinterpret_cast<cudaStream_t>(stream);
     if (p.B == 0) return VISTA_OK;
     const bool partial = outs.mode == OUT_PARTIAL;
@@ -328,6 +332,38 @@ vista_status_t vista_summarize_partial(const vista_desc_t* desc, const void* q, 
     if (!desc) return VISTA_ERR_NULL;
     OutSpec o{OUT_PARTIAL, 0, part_o, desc->attn == VISTA_SOFTMAX ? part_lse : nullptr};
     return run(desc, q, k, v, offsets, total_len, o, workspace, workspace_bytes, stream);
+}
+
+vista_status_t vista_summarize_partial_peers(const vista_desc_t* desc, const void* q, const void* k, const void* v,
+                                             const int64_t* offsets, int64_t total_len, int32_t world, int32_t rank,
+                                             float* const* recv_o, float* const* recv_lse, const uint32_t* acks,
+                                             const uint32_t* epoch, void* workspace, size_t workspace_bytes,
+                                             void* stream) {
+    if (!desc) return VISTA_ERR_NULL;
+    if (desc->attn != VISTA_SOFTMAX) return VISTA_ERR_UNSUPPORTED;
+    if (world < 1 || world > kMaxExchangeRanks || rank < 0 || rank >= world) return VISTA_ERR_INVALID;
+    if (!recv_o || !recv_lse || !acks || !epoch) return VISTA_ERR_NULL;
+    vista_status_t st = validate_desc(desc);
+    if (st != VISTA_OK) return st;
+    const size_t n_l = (size_t)desc->num_users * desc->num_heads * desc->num_summary;
+    const size_t n_o = n_l * desc->head_dim;
+    PeerSpec pe{};
+    pe.n = world;
+    for (int r = 0; r < world; ++r) {
+        if (!recv_o[r] || !recv_lse[r]) return VISTA_ERR_NULL;
+        if (!aligned16(recv_o[r]) || (reinterpret_cast<uintptr_t>(recv_lse[r]) & 3)) return VISTA_ERR_MISALIGNED;
+        pe.o[r] = recv_o[r] + (size_t)rank * n_o;
+        pe.lse[r] = recv_lse[r] + (size_t)rank * n_l;
+    }
+    // this rank's own slot: the base the kernels' row offsets are taken from (and what the checks see)
+    OutSpec o{OUT_PARTIAL, 0, pe.o[rank], pe.lse[rank]};
+    if (total_len < 0) return VISTA_ERR_INVALID;
+    if (desc->num_users > 0 && choose_path(make_problem(desc, total_len)) != PATH_SM100_SOFTMAX)
+        return VISTA_ERR_UNSUPPORTED;  // the fused stores exist on the tcgen05 softmax path
+    cudaError_t e = launch_exchange_wait_acks(world, acks, epoch, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    count_launches(1);
+    return run(desc, q, k, v, offsets, total_len, o, workspace, workspace_bytes, stream, &pe);
 }
 
 // ---- shared key prefix: attention / state over [prefix keys; history] (reading R18).

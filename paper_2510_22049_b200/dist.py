@@ -91,6 +91,11 @@ class CudaBackend:
     def partial(self, q, k, v, offsets, total_len, attn):
         return self.v.summarize_partial(q, k, v, offsets, total_len, attn=attn, **self.kw)
 
+    def partial_peers(self, q, k, v, offsets, total_len, exchange):
+        """Softmax partial whose kernels store straight into every rank's receive buffer."""
+        kw = {k2: v2 for k2, v2 in self.kw.items() if k2 in ("scale", "workspace", "stream")}
+        self.v.summarize_partial_peers(q, k, v, offsets, total_len, exchange, **kw)
+
     def merge(self, part_o, part_lse, q, attn, user_len):
         return self.v.summarize_merge(part_o, part_lse, q=q, attn=attn, user_len=user_len, **self.kw)
 
@@ -198,6 +203,14 @@ class PeerExchange:
         vista_exchange_wait(self.world, self.flags, self.epoch, stream)
         return self.recv_o, self.recv_lse
 
+    def signal_wait(self, stream=None):
+        """signal + wait after a fused partial (vista_summarize_partial_peers already stored this rank's
+        rows into every receive buffer): returns the local receive buffers [world, ...]."""
+        from . import vista_exchange_signal, vista_exchange_wait
+        vista_exchange_signal(self.world, self.rank, self.flag_ptrs, self.epoch, stream)
+        vista_exchange_wait(self.world, self.flags, self.epoch, stream)
+        return self.recv_o, self.recv_lse
+
     def release(self, stream=None):
         """ack: this rank has consumed the current epoch (after the merge read the receive buffer)."""
         from . import vista_exchange_ack
@@ -211,16 +224,24 @@ class PeerExchange:
 
 
 def summarize_by_length(q, k_shard, v_shard, shard_offsets, user_len, *, attn="softmax", group=None,
-                        backend=None, total_len=None, exchange=None):
+                        backend=None, total_len=None, exchange=None, fused=True):
     """Rank-local shard (this rank's range of every user) -> merged summary of every user on every
     rank.  shard_offsets: int64 [B+1] (device), user_len: int64 [B] total L_u (device, QLA 1/N).
     One all_gather of the partials (softmax: O_p [B,H,S,d] + lse_p [B,H,S]; QLA: Z_p [B,H,d,d]):
-    NCCL (or gloo), or, with exchange = a PeerExchange, peer-memory stores over NVLink.
+    NCCL (or gloo), or, with exchange = a PeerExchange, peer-memory stores over NVLink -- for softmax
+    (fused=True) made by the partial's own kernels, else by a push kernel after it.
     No host synchronization: the step is capturable in a CUDA graph."""
     backend = backend or CudaBackend()
     a = _attn_code(attn)
     if total_len is None:
         total_len = k_shard.shape[0]
+    if exchange is not None and fused and a == 0 and hasattr(backend, "partial_peers"):
+        # the exchange fused into the partial's stores (SURVEY 8(e) phase 2): no push, no collective
+        backend.partial_peers(q, k_shard, v_shard, shard_offsets, total_len, exchange)
+        go, gl = exchange.signal_wait()
+        res = backend.merge(go, gl, q, a, user_len)
+        exchange.release()
+        return res
     po, pl = backend.partial(q, k_shard, v_shard, shard_offsets, total_len, a)
     if exchange is not None:
         go, gl = exchange.gather(po, pl if a == 0 else None)

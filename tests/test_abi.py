@@ -170,6 +170,19 @@ def test_exchange_validation_before_launch(lib):
         (lambda: vista.vista_exchange_wait(1, 0, 4096, stream=0), 1),
         (lambda: vista.vista_exchange_ack(1, 0, [0], 4096, stream=0), 1),
     ]
+    d = vista.make_desc(2, 256, 2, 128)
+    dq = vista.make_desc(2, 256, 2, 128, attn=vista.QLA)
+    pp = lambda desc, world, rank, o, l, acks=4096, ep=4096: (  # noqa: E731
+        lambda: vista.vista_summarize_partial_peers(desc, 4096, 4096, 4096, 4096, 64, world, rank, o, l, acks, ep,
+                                                    4096, 1 << 20, stream=0))
+    cases += [
+        (pp(dq, 1, 0, [4096], [4096]), 3),  # the fused exchange is softmax only
+        (pp(d, 0, 0, [4096], [4096]), 2),
+        (pp(d, 2, 2, [4096, 8192], [4096, 8192]), 2),  # rank >= world
+        (pp(d, 1, 0, [4096], [4096], acks=0), 1),
+        (pp(d, 2, 0, [4096, 0], [4096, 8192]), 1),  # a NULL peer buffer
+        (pp(d, 1, 0, [4100], [4096]), 4),  # receive buffer not 16-B aligned
+    ]
     for fn, status in cases:
         with pytest.raises(E) as e:
             fn()

@@ -1257,11 +1257,14 @@ def test_qla_target_rows_from_state_c2_full_size_sampled_users(cuda_lib):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("attn", ["softmax", "qla"])
-def test_peer_exchange_single_rank(cuda_lib, attn):
+@pytest.mark.parametrize("attn,fused", [("softmax", True), ("softmax", False), ("qla", False)])
+def test_peer_exchange_single_rank(cuda_lib, attn, fused):
     """The peer-memory split-L exchange (vista_exchange_*, dist.PeerExchange) at world size 1 (one
     GPU: the rank pushes into its own receive buffer): bitwise equal to merging the partial directly,
-    over several steps (device epochs and acks), eagerly and replayed from a CUDA graph."""
+    over several steps (device epochs and acks), eagerly and replayed from a CUDA graph.  fused: the
+    softmax partial's own kernels store into the receive buffers (vista_summarize_partial_peers; the
+    batch has an empty user and split units, so the empty-user fill and the slot merge store there
+    too) -- the buffer must hold exactly the bytes of the plain partial."""
     from paper_2510_22049_b200 import dist as vdist
     vista = cuda_lib
     lens = [700, 0, 129, 2050]
@@ -1275,11 +1278,15 @@ def test_peer_exchange_single_rank(cuda_lib, attn):
     ref_o, ref_l = be.merge(po[None], pl[None] if a == vista.SOFTMAX else None, q, a, ulen)
     ex = vdist.PeerExchange(po.shape, pl.shape if a == vista.SOFTMAX else None)
     for _ in range(3):
-        o, l = vdist.summarize_by_length(q, k, v, ot, ulen, attn=attn, total_len=int(off[-1]), exchange=ex)
+        o, l = vdist.summarize_by_length(q, k, v, ot, ulen, attn=attn, total_len=int(off[-1]), exchange=ex,
+                                         fused=fused)
         torch.cuda.synchronize()
         assert torch.equal(o, ref_o)
         if a == vista.SOFTMAX:
             assert torch.equal(l, ref_l)
+        assert torch.equal(ex.recv_o[0], po)
+        if a == vista.SOFTMAX:
+            assert torch.equal(ex.recv_lse[0], pl)
     assert int(ex.epoch.item()) == 3 and int(ex.acks[0].item()) == 3 and int(ex.flags[0].item()) == 3
     # captured: the epoch is a device counter, so replays advance it
     s = torch.cuda.Stream()
@@ -1287,7 +1294,8 @@ def test_peer_exchange_single_rank(cuda_lib, attn):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
         g.capture_begin()
-        o2, l2 = vdist.summarize_by_length(q, k, v, ot, ulen, attn=attn, total_len=int(off[-1]), exchange=ex)
+        o2, l2 = vdist.summarize_by_length(q, k, v, ot, ulen, attn=attn, total_len=int(off[-1]), exchange=ex,
+                                           fused=fused)
         g.capture_end()
     torch.cuda.current_stream().wait_stream(s)
     for _ in range(2):

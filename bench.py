@@ -66,9 +66,10 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group for N > 1 (gloo: host-staged exchange; a dry run of the multi-rank "
                          "path when fewer GPUs than ranks are visible)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p", "p2p-push"],
                     help="by_length split-L exchange: NCCL all_gather (default) or peer-memory stores over NVLink "
-                         "(dist.PeerExchange, CUDA IPC; one node)")
+                         "(dist.PeerExchange, CUDA IPC; one node) -- p2p: made by the softmax partial's own "
+                         "kernels (vista_summarize_partial_peers), p2p-push: by a push kernel after the partial")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -350,13 +351,14 @@ def run_own(args, rank, world, local_rank):
         if mode == "by_length":
             acode = 0 if args.attn == "softmax" else 1
             xchg = None
-            if args.exchange == "p2p":  # peer-memory exchange (CUDA IPC buffers, NVLink stores)
+            fused = args.exchange == "p2p" and acode == 0
+            if args.exchange in ("p2p", "p2p-push"):  # peer-memory exchange (CUDA IPC buffers, NVLink stores)
                 part_shape = (B_all, H, S, d) if acode == 0 else (B_all, H, d, d)
                 xchg = vdist.PeerExchange(part_shape, (B_all, H, S) if acode == 0 else None)
 
             def step(ins=inputs):
                 out, lse = vdist.summarize_by_length(ins[0], ins[1], ins[2], ins[3], ulen, attn=args.attn,
-                                                     total_len=total, exchange=xchg)
+                                                     total_len=total, exchange=xchg, fused=fused)
                 return [out] + ([lse] if lse is not None else [])
 
             # the same three phases, separately callable for the breakdown (summarize_by_length's body)
@@ -371,9 +373,14 @@ def run_own(args, rank, world, local_rank):
                     res = be.merge(gg[0], gg[1] if acode == 0 else None, q, acode, ulen)
                     xchg.release()
                     return res
-                phase_fns = (lambda: be.partial(q, K, V, soff_t, total, acode),
-                             lambda pp: xchg.gather(pp[0], pp[1] if acode == 0 else None),
-                             _merge_release)
+                if fused:  # partial + stores into every receive buffer | signal + wait | merge
+                    phase_fns = (lambda: be.partial_peers(q, K, V, soff_t, total, xchg),
+                                 lambda pp: xchg.signal_wait(),
+                                 _merge_release)
+                else:
+                    phase_fns = (lambda: be.partial(q, K, V, soff_t, total, acode),
+                                 lambda pp: xchg.gather(pp[0], pp[1] if acode == 0 else None),
+                                 _merge_release)
         else:
             segs_obj = [vdist.Segment(u, a0, e0) for u, a0, e0 in seg]
             fplan = vdist.FlatPlan(all_segs, lens, rank, dev)
@@ -385,8 +392,10 @@ def run_own(args, rank, world, local_rank):
         items_per_step = int(off_all[-1])
         scaling = "strong"
         parallel = (f"{mode} x{world} (strong: one {args.config} batch split; all_gather of partials over "
-                    + ("peer memory (CUDA IPC, NVLink stores)" if (mode == "by_length" and args.exchange == "p2p")
-                       else "NCCL") + ")")
+                    + (("peer memory (CUDA IPC, NVLink stores"
+                        + (", fused into the partial's kernels)" if args.exchange == "p2p" and args.attn == "softmax"
+                           else ", push kernel)"))
+                       if (mode == "by_length" and args.exchange != "nccl") else "NCCL") + ")")
         B = B_all
     path = vista.vista_dispatch_name(vista.make_desc(B, S, H, d, in_dtype=vista.BF16, attn=attn))
 

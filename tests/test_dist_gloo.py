@@ -282,3 +282,48 @@ def test_peer_exchange_host_logic_world2():
         peer = 1 - r
         assert [o[peer], l[peer], f[peer], a[peer]] == [10**12 + i for i in range(1, 5)]
         assert all(h.startswith(b"R%d:" % peer) for h in opened) and len(opened) == 4
+
+
+def test_by_length_fused_exchange_call_order():
+    """summarize_by_length with a peer exchange and fused=True (softmax): the backend's partial_peers
+    stores the partial (no separate partial / push), then signal_wait hands the receive buffers to the
+    merge, then release -- in that order; QLA and fused=False take the push path."""
+    calls = []
+
+    class Ex:
+        recv = (torch.ones(1, 2), torch.zeros(1, 2))
+
+        def signal_wait(self, stream=None):
+            calls.append("signal_wait")
+            return self.recv
+
+        def gather(self, po, pl=None, stream=None):
+            calls.append("gather")
+            return self.recv
+
+        def release(self, stream=None):
+            calls.append("release")
+
+    class Be:
+        def partial_peers(self, q, k, v, off, total, ex):
+            calls.append("partial_peers")
+
+        def partial(self, q, k, v, off, total, attn):
+            calls.append("partial")
+            return torch.ones(2), (torch.zeros(2) if attn == 0 else None)
+
+        def merge(self, go, gl, q, attn, ulen):
+            calls.append("merge")
+            return go, gl
+
+    ex, be = Ex(), Be()
+    out = vdist.summarize_by_length(None, None, None, None, None, attn="softmax", backend=be, total_len=0,
+                                    exchange=ex)
+    assert calls == ["partial_peers", "signal_wait", "merge", "release"] and out[0] is Ex.recv[0]
+    calls.clear()
+    vdist.summarize_by_length(None, None, None, None, None, attn="softmax", backend=be, total_len=0, exchange=ex,
+                              fused=False)
+    assert calls == ["partial", "gather", "merge", "release"]
+    calls.clear()
+    vdist.summarize_by_length(None, None, None, None, None, attn="qla", backend=be, total_len=0, exchange=ex)
+    assert calls == ["partial", "gather", "merge", "release"]

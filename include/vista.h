@@ -346,16 +346,18 @@ vista_status_t vista_exchange_ack(int32_t world, int32_t rank, uint32_t* const* 
                                   void* stream);
 
 /*
- * The same exchange fused into the softmax partial (SURVEY.md 8(e) phase 2: "the partial kernel's
- * epilogue writes directly into peer receive buffers ... removing the collective launch").  Replaces
+ * The same exchange fused into the partial (SURVEY.md 8(e) phase 2: "the partial kernel's epilogue
+ * writes directly into peer receive buffers ... removing the collective launch").  Replaces
  * vista_summarize_partial + vista_exchange_push: waits until acks[r] >= *epoch for every r, then
  * computes this rank's partial exactly as vista_summarize_partial would, but its kernels (the
- * attention epilogue, the split-unit slot merge, the empty-user fill) store every row of O_p and
- * lse_p straight into slot `rank` of every rank's receive buffer (recv_o[r] + rank*n_o,
- * recv_lse[r] + rank*n_lse; NVLink stores for peers).  Continue with vista_exchange_signal, _wait,
- * vista_summarize_merge over the local receive buffer, and vista_exchange_ack.  desc->attn must be
- * VISTA_SOFTMAX (VISTA_ERR_UNSUPPORTED otherwise); recv_o[r] 16-B aligned (32-B for 256-bit stores),
- * recv_lse[r] 4-B aligned; other arguments as in vista_summarize_partial and vista_exchange_push.
+ * attention / state epilogue, the split-unit slot merge, the empty-user fill) store every row of
+ * the partial straight into slot `rank` of every rank's receive buffer (NVLink stores for peers):
+ * softmax O_p at recv_o[r] + rank*B*H*S*d and lse_p at recv_lse[r] + rank*B*H*S; QLA Z_p at
+ * recv_o[r] + rank*B*H*d*d (recv_lse unused, may be NULL).  Continue with vista_exchange_signal,
+ * _wait, vista_summarize_merge over the local receive buffer, and vista_exchange_ack.  The tcgen05
+ * paths only (bf16, d = 128; VISTA_ERR_UNSUPPORTED otherwise); recv_o[r] 16-B aligned (32-B for
+ * 256-bit stores), recv_lse[r] 4-B aligned; other arguments as in vista_summarize_partial and
+ * vista_exchange_push.
  */
 vista_status_t vista_summarize_partial_peers(const vista_desc_t* desc, const void* q, const void* k,
                                              const void* v, const int64_t* offsets, int64_t total_len,

@@ -454,16 +454,18 @@ def summarize_partial(q, k, v, offsets, total_len=None, *, attn=SOFTMAX, scale=N
     return po, pl
 
 
-def summarize_partial_peers(q, k, v, offsets, total_len, exchange, *, scale=None, workspace=None, stream=None):
-    """Softmax partial over one history shard with the split-L exchange fused into its stores: the rows
-    land in slot `exchange.rank` of every rank's receive buffer (exchange: a dist.PeerExchange).
-    Returns nothing; follow with exchange.signal_wait() and the merge."""
+def summarize_partial_peers(q, k, v, offsets, total_len, exchange, *, attn=SOFTMAX, scale=None, phi1="silu",
+                            phi2="silu", normalize=True, workspace=None, stream=None):
+    """Partial over one history shard with the split-L exchange fused into its stores: softmax O_p / lse_p
+    rows or QLA Z_p rows land in slot `exchange.rank` of every rank's receive buffer (exchange: a
+    dist.PeerExchange).  Returns nothing; follow with exchange.signal_wait() and the merge."""
     if total_len is None:
         total_len = k.shape[0]
-    desc = _desc_for(q, k, offsets, SOFTMAX, scale, "silu", "silu", True, None)
+    desc = _desc_for(q, k, offsets, attn, scale, phi1, phi2, normalize, None)
     ws, need = _workspace(desc, total_len, q.device, workspace, 0)
     vista_summarize_partial_peers(desc, q, k, v, offsets, total_len, exchange.world, exchange.rank, exchange.o_ptrs,
-                                  exchange.lse_ptrs, exchange.acks, exchange.epoch, ws, ws.numel(), stream)
+                                  exchange.lse_ptrs if attn == SOFTMAX else None, exchange.acks, exchange.epoch, ws,
+                                  ws.numel(), stream)
 
 
 def summarize_bwd(q, k, v, offsets, total_len, dout, *, attn=QLA, phi1="silu", phi2="silu", normalize=True,
@@ -595,7 +597,8 @@ def vista_summarize_partial_peers(desc, q, k, v, offsets, total_len, world, rank
     straight into slot `rank` of every rank's receive buffer."""
     _check(load().vista_summarize_partial_peers(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
                                                 int(total_len), int(world), int(rank), _ptr_array(recv_o_ptrs),
-                                                _ptr_array(recv_lse_ptrs), _ptr(acks), _ptr(epoch), _ptr(workspace),
+                                                _ptr_array(recv_lse_ptrs) if recv_lse_ptrs else None, _ptr(acks),
+                                                _ptr(epoch), _ptr(workspace),
                                                 int(workspace_bytes), _stream(stream)),
            "vista_summarize_partial_peers")
 

@@ -158,6 +158,12 @@ __global__ void user_tiles_kernel(const int64_t* __restrict__ offsets, int B, in
                         outs.qzp[(size_t)uu * S * H + e] = 0.f;
                     }
                 }
+            } else if (pe.n > 0 && outs.mode == OUT_PARTIAL) {  // fused exchange: every receive buffer
+#pragma unroll
+                for (int r = 0; r < kMaxExchangeRanks; ++r) {
+                    if (r >= pe.n) break;
+                    for (size_t e = lane; e < n_z; e += 32) pe.o[r][(size_t)uu * n_z + e] = 0.f;
+                }
             } else if (zbuf) {
                 for (size_t e = lane; e < n_z; e += 32) zbuf[(size_t)uu * n_z + e] = 0.f;
             }
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(256) merge_softmax_slots_kernel(const int* __r
 
 // Sum the run of QLA state slots of each split unit into zbuf[unit] (d = 128 rows of 128).
 __global__ void merge_qla_slots_kernel(const int* __restrict__ slot_unit, int num_slots, const float* __restrict__ slot_o,
-                                       float* __restrict__ zbuf) {
+                                       float* __restrict__ zbuf, const __grid_constant__ PeerSpec pe) {
     const int s = blockIdx.x;
     const int n = slot_unit[s];
     if (n < 0 || !slot_is_head(slot_unit, s, n)) return;
@@ -406,6 +412,14 @@ __global__ void merge_qla_slots_kernel(const int* __restrict__ slot_unit, int nu
         acc.y += o.y;
         acc.z += o.z;
         acc.w += o.w;
+    }
+    if (pe.n > 0) {  // fused exchange: every rank's receive buffer
+#pragma unroll
+        for (int r = 0; r < kMaxExchangeRanks; ++r) {
+            if (r >= pe.n) break;
+            reinterpret_cast<float4*>(pe.o[r] + ((size_t)n * 128 + row) * 128)[lane] = acc;
+        }
+        return;
     }
     reinterpret_cast<float4*>(zbuf + ((size_t)n * 128 + row) * 128)[lane] = acc;
 }
@@ -846,7 +860,8 @@ cudaError_t launch_merge_qla_slots(const Problem& p, const Workspace& w, char* w
     const int num_slots = 2 * w.num_ctas;
     dim3 grid(num_slots, 128 / 8);
     merge_qla_slots_kernel<<<grid, 256, 0, p.stream>>>(reinterpret_cast<const int*>(ws + w.slot_unit_off), num_slots,
-                                                       reinterpret_cast<const float*>(ws + w.slot_o_off), zbuf);
+                                                       reinterpret_cast<const float*>(ws + w.slot_o_off), zbuf,
+                                                       p.outs.mode == OUT_PARTIAL ? p.peers : PeerSpec{});
     return cudaGetLastError();
 }
 

@@ -130,10 +130,12 @@ __device__ __forceinline__ void issue_Z_s(int st, uint32_t tmem, uint32_t base, 
     }
 }
 
-template <int PHI1>
+// PEERS: the fused split-L exchange (vista_summarize_partial_peers, QLA) -- complete units' Z to every
+// rank's receive buffer; a separate instantiation so the default kernel carries none of it
+template <int PHI1, bool PEERS = false>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_qla_state_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
-                           const Params P) {
+                           const Params P, const __grid_constant__ PeerSpec peers) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + kBarOff);
@@ -278,12 +280,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 continue;
             }
             float* dst;
-            if (item_complete(it)) dst = P.zbuf + ((size_t)(it.u * HG + it.hg) * 128 + c1) * 128;
+            const bool comp = item_complete(it);
+            const size_t zoff = ((size_t)(it.u * HG + it.hg) * 128 + c1) * 128;
+            if (comp) dst = P.zbuf + zoff;
             else dst = P.slot_o + ((size_t)item_slot(it, cta) * 128 + c1) * 128;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 uint32_t r[32];
                 ptx::tmem_ld32_sync(tmem + lane_bits + zb * 128 + chalf * 64 + c * 32, r);
+                if (PEERS && comp) {  // fused exchange: the row of Z into every rank's receive buffer
+#pragma unroll
+                    for (int q = 0; q < kMaxExchangeRanks; ++q) {
+                        if (q >= peers.n) break;
+                        float4* d4 = reinterpret_cast<float4*>(peers.o[q] + zoff + chalf * 64 + c * 32);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                    }
+                    continue;
+                }
                 float4* d4 = reinterpret_cast<float4*>(dst + chalf * 64 + c * 32);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -305,9 +321,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int PHI1>
 static cudaError_t launch_phi(const Problem& p, const Workspace& w, const CUtensorMap& mk, const CUtensorMap& mv,
                               const Params& P) {
-    const cudaError_t attr = set_smem_attr(reinterpret_cast<const void*>(sm100_qla_state_kernel<PHI1>), kSmem);
+    const bool peers = p.outs.mode == OUT_PARTIAL && p.peers.n > 0 && P.wbuf == nullptr;
+    const void* fn = peers ? reinterpret_cast<const void*>(sm100_qla_state_kernel<PHI1, true>)
+                           : reinterpret_cast<const void*>(sm100_qla_state_kernel<PHI1>);
+    const cudaError_t attr = set_smem_attr(fn, kSmem);
     if (attr != cudaSuccess) return attr;
-    sm100_qla_state_kernel<PHI1><<<w.num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P);
+    if (peers) sm100_qla_state_kernel<PHI1, true><<<w.num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P, p.peers);
+    else sm100_qla_state_kernel<PHI1><<<w.num_ctas, kThreads, kSmem, p.stream>>>(mk, mv, P, p.peers);
     return cudaGetLastError();
 }
 

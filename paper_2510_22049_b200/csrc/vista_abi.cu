@@ -229,8 +229,9 @@ static vista_status_t run(const vista_desc_t* desc, const void* q, const void* k
     p.offsets = offsets;
     p.outs = outs;
     if (peers) {
-        p.peers = *peers;  // the fused exchange: tcgen05 softmax path only
-        if (choose_path(p) != PATH_SM100_SOFTMAX) return VISTA_ERR_UNSUPPORTED;
+        p.peers = *peers;  // the fused exchange: tcgen05 paths only
+        const Path pp = choose_path(p);
+        if (pp != PATH_SM100_SOFTMAX && pp != PATH_SM100_QLA) return VISTA_ERR_UNSUPPORTED;
     }
     p.stream = reinterpret_cast<cudaStream_t>(stream);
     if (p.B == 0) return VISTA_OK;
@@ -340,26 +341,30 @@ vista_status_t vista_summarize_partial_peers(const vista_desc_t* desc, const voi
                                              const uint32_t* epoch, void* workspace, size_t workspace_bytes,
                                              void* stream) {
     if (!desc) return VISTA_ERR_NULL;
-    if (desc->attn != VISTA_SOFTMAX) return VISTA_ERR_UNSUPPORTED;
     if (world < 1 || world > kMaxExchangeRanks || rank < 0 || rank >= world) return VISTA_ERR_INVALID;
-    if (!recv_o || !recv_lse || !acks || !epoch) return VISTA_ERR_NULL;
+    const bool softmax = desc->attn == VISTA_SOFTMAX;
+    if (!recv_o || (softmax && !recv_lse) || !acks || !epoch) return VISTA_ERR_NULL;
     vista_status_t st = validate_desc(desc);
     if (st != VISTA_OK) return st;
-    const size_t n_l = (size_t)desc->num_users * desc->num_heads * desc->num_summary;
-    const size_t n_o = n_l * desc->head_dim;
+    // per rank slot: softmax O_p [B,H,S,d] + lse_p [B,H,S]; QLA Z_p [B,H,d,d]
+    const size_t n_l = softmax ? (size_t)desc->num_users * desc->num_heads * desc->num_summary : 0;
+    const size_t n_o = softmax ? n_l * desc->head_dim
+                               : (size_t)desc->num_users * desc->num_heads * desc->head_dim * desc->head_dim;
     PeerSpec pe{};
     pe.n = world;
     for (int r = 0; r < world; ++r) {
-        if (!recv_o[r] || !recv_lse[r]) return VISTA_ERR_NULL;
-        if (!aligned16(recv_o[r]) || (reinterpret_cast<uintptr_t>(recv_lse[r]) & 3)) return VISTA_ERR_MISALIGNED;
+        if (!recv_o[r] || (softmax && !recv_lse[r])) return VISTA_ERR_NULL;
+        if (!aligned16(recv_o[r]) || (softmax && (reinterpret_cast<uintptr_t>(recv_lse[r]) & 3)))
+            return VISTA_ERR_MISALIGNED;
         pe.o[r] = recv_o[r] + (size_t)rank * n_o;
-        pe.lse[r] = recv_lse[r] + (size_t)rank * n_l;
+        pe.lse[r] = softmax ? recv_lse[r] + (size_t)rank * n_l : nullptr;
     }
     // this rank's own slot: the base the kernels' row offsets are taken from (and what the checks see)
     OutSpec o{OUT_PARTIAL, 0, pe.o[rank], pe.lse[rank]};
     if (total_len < 0) return VISTA_ERR_INVALID;
-    if (desc->num_users > 0 && choose_path(make_problem(desc, total_len)) != PATH_SM100_SOFTMAX)
-        return VISTA_ERR_UNSUPPORTED;  // the fused stores exist on the tcgen05 softmax path
+    const Path path = desc->num_users > 0 ? choose_path(make_problem(desc, total_len)) : PATH_NONE;
+    if (desc->num_users > 0 && path != PATH_SM100_SOFTMAX && path != PATH_SM100_QLA)
+        return VISTA_ERR_UNSUPPORTED;  // the fused stores exist on the tcgen05 paths
     cudaError_t e = launch_exchange_wait_acks(world, acks, epoch, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e);
     count_launches(1);

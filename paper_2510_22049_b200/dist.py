@@ -91,10 +91,9 @@ class CudaBackend:
     def partial(self, q, k, v, offsets, total_len, attn):
         return self.v.summarize_partial(q, k, v, offsets, total_len, attn=attn, **self.kw)
 
-    def partial_peers(self, q, k, v, offsets, total_len, exchange):
-        """Softmax partial whose kernels store straight into every rank's receive buffer."""
-        kw = {k2: v2 for k2, v2 in self.kw.items() if k2 in ("scale", "workspace", "stream")}
-        self.v.summarize_partial_peers(q, k, v, offsets, total_len, exchange, **kw)
+    def partial_peers(self, q, k, v, offsets, total_len, exchange, attn=0):
+        """Partial whose kernels store straight into every rank's receive buffer (softmax or QLA)."""
+        self.v.summarize_partial_peers(q, k, v, offsets, total_len, exchange, attn=attn, **self.kw)
 
     def merge(self, part_o, part_lse, q, attn, user_len):
         return self.v.summarize_merge(part_o, part_lse, q=q, attn=attn, user_len=user_len, **self.kw)
@@ -228,18 +227,18 @@ def summarize_by_length(q, k_shard, v_shard, shard_offsets, user_len, *, attn="s
     """Rank-local shard (this rank's range of every user) -> merged summary of every user on every
     rank.  shard_offsets: int64 [B+1] (device), user_len: int64 [B] total L_u (device, QLA 1/N).
     One all_gather of the partials (softmax: O_p [B,H,S,d] + lse_p [B,H,S]; QLA: Z_p [B,H,d,d]):
-    NCCL (or gloo), or, with exchange = a PeerExchange, peer-memory stores over NVLink -- for softmax
-    (fused=True) made by the partial's own kernels, else by a push kernel after it.
+    NCCL (or gloo), or, with exchange = a PeerExchange, peer-memory stores over NVLink -- made by the
+    partial's own kernels (fused=True), else by a push kernel after it.
     No host synchronization: the step is capturable in a CUDA graph."""
     backend = backend or CudaBackend()
     a = _attn_code(attn)
     if total_len is None:
         total_len = k_shard.shape[0]
-    if exchange is not None and fused and a == 0 and hasattr(backend, "partial_peers"):
+    if exchange is not None and fused and hasattr(backend, "partial_peers"):
         # the exchange fused into the partial's stores (SURVEY 8(e) phase 2): no push, no collective
-        backend.partial_peers(q, k_shard, v_shard, shard_offsets, total_len, exchange)
+        backend.partial_peers(q, k_shard, v_shard, shard_offsets, total_len, exchange, a)
         go, gl = exchange.signal_wait()
-        res = backend.merge(go, gl, q, a, user_len)
+        res = backend.merge(go, gl if a == 0 else None, q, a, user_len)
         exchange.release()
         return res
     po, pl = backend.partial(q, k_shard, v_shard, shard_offsets, total_len, a)

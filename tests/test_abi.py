@@ -176,7 +176,7 @@ def test_exchange_validation_before_launch(lib):
         lambda: vista.vista_summarize_partial_peers(desc, 4096, 4096, 4096, 4096, 64, world, rank, o, l, acks, ep,
                                                     4096, 1 << 20, stream=0))
     cases += [
-        (pp(dq, 1, 0, [4096], [4096]), 3),  # the fused exchange is softmax only
+        (pp(dq, 1, 0, [4100], None), 4),  # QLA: no lse buffers; Z buffer not 16-B aligned
         (pp(d, 0, 0, [4096], [4096]), 2),
         (pp(d, 2, 2, [4096, 8192], [4096, 8192]), 2),  # rank >= world
         (pp(d, 1, 0, [4096], [4096], acks=0), 1),

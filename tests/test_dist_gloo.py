@@ -287,7 +287,7 @@ def test_peer_exchange_host_logic_world2():
 def test_by_length_fused_exchange_call_order():
     """summarize_by_length with a peer exchange and fused=True (softmax): the backend's partial_peers
     stores the partial (no separate partial / push), then signal_wait hands the receive buffers to the
-    merge, then release -- in that order; QLA and fused=False take the push path."""
+    merge, then release -- in that order (softmax and QLA); fused=False takes the push path."""
     calls = []
 
     class Ex:
@@ -305,7 +305,7 @@ def test_by_length_fused_exchange_call_order():
             calls.append("release")
 
     class Be:
-        def partial_peers(self, q, k, v, off, total, ex):
+        def partial_peers(self, q, k, v, off, total, ex, attn=0):
             calls.append("partial_peers")
 
         def partial(self, q, k, v, off, total, attn):
@@ -326,4 +326,4 @@ def test_by_length_fused_exchange_call_order():
     assert calls == ["partial", "gather", "merge", "release"]
     calls.clear()
     vdist.summarize_by_length(None, None, None, None, None, attn="qla", backend=be, total_len=0, exchange=ex)
-    assert calls == ["partial", "gather", "merge", "release"]
+    assert calls == ["partial_peers", "signal_wait", "merge", "release"]

@@ -1257,14 +1257,14 @@ def test_qla_target_rows_from_state_c2_full_size_sampled_users(cuda_lib):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("attn,fused", [("softmax", True), ("softmax", False), ("qla", False)])
+@pytest.mark.parametrize("attn,fused", [("softmax", True), ("softmax", False), ("qla", True), ("qla", False)])
 def test_peer_exchange_single_rank(cuda_lib, attn, fused):
     """The peer-memory split-L exchange (vista_exchange_*, dist.PeerExchange) at world size 1 (one
     GPU: the rank pushes into its own receive buffer): bitwise equal to merging the partial directly,
     over several steps (device epochs and acks), eagerly and replayed from a CUDA graph.  fused: the
-    softmax partial's own kernels store into the receive buffers (vista_summarize_partial_peers; the
-    batch has an empty user and split units, so the empty-user fill and the slot merge store there
-    too) -- the buffer must hold exactly the bytes of the plain partial."""
+    partial's own kernels store into the receive buffers (vista_summarize_partial_peers; the batch
+    has an empty user and split units, so the empty-user fill and the slot merge store there too) --
+    the buffer must hold exactly the bytes of the plain partial."""
     from paper_2510_22049_b200 import dist as vdist
     vista = cuda_lib
     lens = [700, 0, 129, 2050]

@@ -68,8 +68,8 @@ def parse():
                          "path when fewer GPUs than ranks are visible)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p", "p2p-push"],
                     help="by_length split-L exchange: NCCL all_gather (default) or peer-memory stores over NVLink "
-                         "(dist.PeerExchange, CUDA IPC; one node) -- p2p: made by the softmax partial's own "
-                         "kernels (vista_summarize_partial_peers), p2p-push: by a push kernel after the partial")
+                         "(dist.PeerExchange, CUDA IPC; one node) -- p2p: made by the partial's own kernels "
+                         "(vista_summarize_partial_peers), p2p-push: by a push kernel after the partial")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -351,7 +351,7 @@ def run_own(args, rank, world, local_rank):
         if mode == "by_length":
             acode = 0 if args.attn == "softmax" else 1
             xchg = None
-            fused = args.exchange == "p2p" and acode == 0
+            fused = args.exchange == "p2p"
             if args.exchange in ("p2p", "p2p-push"):  # peer-memory exchange (CUDA IPC buffers, NVLink stores)
                 part_shape = (B_all, H, S, d) if acode == 0 else (B_all, H, d, d)
                 xchg = vdist.PeerExchange(part_shape, (B_all, H, S) if acode == 0 else None)
@@ -374,7 +374,7 @@ def run_own(args, rank, world, local_rank):
                     xchg.release()
                     return res
                 if fused:  # partial + stores into every receive buffer | signal + wait | merge
-                    phase_fns = (lambda: be.partial_peers(q, K, V, soff_t, total, xchg),
+                    phase_fns = (lambda: be.partial_peers(q, K, V, soff_t, total, xchg, acode),
                                  lambda pp: xchg.signal_wait(),
                                  _merge_release)
                 else:
@@ -393,8 +393,7 @@ def run_own(args, rank, world, local_rank):
         scaling = "strong"
         parallel = (f"{mode} x{world} (strong: one {args.config} batch split; all_gather of partials over "
                     + (("peer memory (CUDA IPC, NVLink stores"
-                        + (", fused into the partial's kernels)" if args.exchange == "p2p" and args.attn == "softmax"
-                           else ", push kernel)"))
+                        + (", fused into the partial's kernels)" if args.exchange == "p2p" else ", push kernel)"))
                        if (mode == "by_length" and args.exchange != "nccl") else "NCCL") + ")")
         B = B_all
     path = vista.vista_dispatch_name(vista.make_desc(B, S, H, d, in_dtype=vista.BF16, attn=attn))

@@ -177,6 +177,8 @@ def test_exchange_validation_before_launch(lib):
                                                     4096, 1 << 20, stream=0))
     cases += [
         (pp(dq, 1, 0, [4100], None), 4),  # QLA: no lse buffers; Z buffer not 16-B aligned
+        (pp(vista.make_desc(2, 256, 2, 64), 1, 0, [4096], [4096]), 3),  # d = 64: CUDA-core path, no fused stores
+        (pp(vista.make_desc(2, 200, 2, 128), 1, 0, [4096], [4096]), 3),  # S % 128 != 0: likewise
         (pp(d, 0, 0, [4096], [4096]), 2),
         (pp(d, 2, 2, [4096, 8192], [4096, 8192]), 2),  # rank >= world
         (pp(d, 1, 0, [4096], [4096], acks=0), 1),

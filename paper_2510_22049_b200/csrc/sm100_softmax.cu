@@ -868,12 +868,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                         v[c * 16 + j] = ptx::pack_bf16x2(__uint_as_float(o[2 * j]) * inv_l,
                                                          __uint_as_float(o[2 * j + 1]) * inv_l);
                 }
-                if (P.outs.codes) {  // NEXT-1: int8 export of the row, as stored (bf16)
+                if (P.outs.codes) {
+                    store_rows_coalesced<PEERS>(P, peers, it, cid, rank * 128 + wq * 32, kRows, tO, v, 0);
+                    // O is read (and its round trip done): the next item's PV may start while this
+                    // thread exports the row from registers (NEXT-1 int8 export, the row as stored)
+                    ptx::tc_fence_before();
+                    if constexpr (PAIR) warp_arrive_leader(&bars->o_empty, rank);
+                    else ptx::mbar_arrive(&bars->o_empty);
                     const int h = it.hg / P.G, g = it.hg % P.G;
                     const size_t orow = ((size_t)it.u * P.S + g * kRows + urow) * P.H + h;
                     i8_export_row_bf16(v, P.outs.codes + orow * 128, P.outs.qscale + orow, P.outs.qzp + orow);
+                } else {
+                    store_rows_coalesced<PEERS>(P, peers, it, cid, rank * 128 + wq * 32, kRows, tO, v, 0);
+                    ptx::tc_fence_before();
+                    if constexpr (PAIR) warp_arrive_leader(&bars->o_empty, rank);
+                    else ptx::mbar_arrive(&bars->o_empty);
                 }
-                store_rows_coalesced<PEERS>(P, peers, it, cid, rank * 128 + wq * 32, kRows, tO, v, 0);
             } else if (coalesced) {
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
@@ -898,10 +908,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     store_row<PEERS>(P, peers, it, cid, urow, of, c * 32, kRows);
                 }
             }
+            if (!(coalesced && out16)) {  // (the bf16 coalesced path released O above)
+                ptx::tc_fence_before();
+                if constexpr (PAIR) warp_arrive_leader(&bars->o_empty, rank);
+                else ptx::mbar_arrive(&bars->o_empty);
+            }
             store_lse<PEERS>(P, peers, it, cid, urow, lse, kRows);
-            ptx::tc_fence_before();
-            if constexpr (PAIR) warp_arrive_leader(&bars->o_empty, rank);
-            else ptx::mbar_arrive(&bars->o_empty);
             if (row == 0) VTRACE(19, k);
             it = nxt;
             have = have_n;

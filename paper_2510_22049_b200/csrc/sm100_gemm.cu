@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- TMA producer
         ptx::tma_prefetch(&mapA);
         ptx::tma_prefetch(&mapB);
-        const uint64_t pol_a = ptx::policy_evict_first(), pol_b = ptx::policy_evict_last();
+        // A rows are shared by the CTAs on the N tiles of an M block: kept in L2 (as in the pair kernel)
+        const uint64_t pol_a = ptx::policy_evict_last(), pol_b = ptx::policy_evict_last();
         int st = 0;
         uint32_t ph = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -281,7 +282,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // ---------------- TMA producer (both CTAs): this CTA's A rows and B rows of each K block
         ptx::tma_prefetch(&mapA);
         ptx::tma_prefetch(&mapB);
-        const uint64_t pol_a = ptx::policy_evict_first(), pol_b = ptx::policy_evict_last();
+        // A rows are read by the pairs working on the num_n output tiles of an M block at about the
+        // same time: kept in L2 for the others (A/B: evict_first read A ~3x from DRAM, QKVG GEMM
+        // 1.18 ms; evict_normal 1.04; evict_last 1.03)
+#ifndef VISTA_GEMM_APOL
+#define VISTA_GEMM_APOL 2
+#endif
+        const uint64_t pol_a = VISTA_GEMM_APOL == 0 ? ptx::policy_evict_first()
+                             : VISTA_GEMM_APOL == 1 ? ptx::policy_evict_normal() : ptx::policy_evict_last();
+        const uint64_t pol_b = ptx::policy_evict_last();
         int st = 0;
         uint32_t ph = 0;
         for (int t = pair; t < num_tiles; t += npairs) {

@@ -64,8 +64,25 @@ __device__ __forceinline__ void st_v8(void* p, const uint32_t (&v)[8]) {
 // fp32 -> bf16 (+ residual) -> global, coalesced through a permuted TMEM round trip (after a
 // 16x256b load a quad of threads holds 128 contiguous bytes of one row).  row0 = the warp's first
 // global row; col0 = the block's first global column (residual), c_out its column in `outp`.
+template <bool RESID>  // RESID: P.resid is set (a separate instantiation: no prefetch registers otherwise)
 __device__ __forceinline__ void store_block64(const GemmParams& P, uint32_t tc, int row0, int lane,
                                               __nv_bfloat16* outp, int nw, int col0, int c_out) {
+    // the residual rows this thread adds, loaded first: their latency overlaps the TMEM round trip
+    // (loaded after it, every half waited for its own loads -- the output GEMM was latency-bound)
+    uint4 xr[2][2][2];
+    if constexpr (RESID) {
+#pragma unroll
+        for (int half = 0; half < 2; ++half)
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const int row = row0 + 16 * half + (lane >> 2) + 8 * rr;
+                if (row < P.M) {
+                    const uint4* rs = reinterpret_cast<const uint4*>(P.resid + (size_t)row * P.N + col0 + 16 * (lane & 3));
+                    xr[half][rr][0] = rs[0];
+                    xr[half][rr][1] = rs[1];
+                }
+            }
+    }
     uint32_t a[32];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
@@ -95,9 +112,8 @@ __device__ __forceinline__ void store_block64(const GemmParams& P, uint32_t tc, 
             const int row = ra + 8 * rr;
             uint32_t* v = rr ? v1 : v0;
             if (row >= P.M) continue;
-            if (P.resid) {  // + residual (16 contiguous bf16 of the row), added in f32
-                const uint4* rs = reinterpret_cast<const uint4*>(P.resid + (size_t)row * P.N + col0 + 16 * p);
-                const uint4 x0 = rs[0], x1 = rs[1];
+            if constexpr (RESID) {  // + residual (16 contiguous bf16 of the row), added in f32
+                const uint4 x0 = xr[half][rr][0], x1 = xr[half][rr][1];
                 const uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
@@ -129,6 +145,7 @@ __device__ __forceinline__ void issue_kblock_d(int st, uint32_t tacc, uint32_t b
     }
 }
 
+template <bool RESID>
 __global__ void __launch_bounds__(kThreads, 1)
     sm100_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                       const GemmParams P) {
@@ -210,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&bars->acc_full[ab], ((aphm >> ab) & 1u));
             aphm ^= 1u << ab;
             ptx::tc_fence_after();
-            store_block64(P, tmem + lane_bits + ab * 128 + chalf * 64, m * 128 + wq * 32, lane, outp, nw, col0, c_out);
+            store_block64<RESID>(P, tmem + lane_bits + ab * 128 + chalf * 64, m * 128 + wq * 32, lane, outp, nw, col0,
+                                 c_out);
             ptx::tc_fence_before();
             ptx::mbar_arrive(&bars->acc_empty[ab]);
             ab ^= 1;
@@ -248,6 +266,7 @@ __device__ __forceinline__ void issue_kblock2_d(int st, uint32_t tacc, uint32_t 
     }
 }
 
+template <bool RESID>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     sm100_gemm2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                        const GemmParams P) {
@@ -342,7 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int sb = 0; sb < 2; ++sb) {
                 const int col0 = n * 256 + cq * 128 + sb * 64;
                 const int which = col0 / nw, c_out = col0 % nw;
-                store_block64(P, tmem + lane_bits + ab * 256 + cq * 128 + sb * 64, m * 256 + rank * 128 + wq * 32,
+                store_block64<RESID>(P, tmem + lane_bits + ab * 256 + cq * 128 + sb * 64, m * 256 + rank * 128 + wq * 32,
                               lane, out_sel(P, which), nw, col0, c_out);
             }
             ptx::tc_fence_before();
@@ -392,16 +411,22 @@ cudaError_t launch_sm100_gemm(int M, int N, int K, const void* A, int64_t lda, c
     if (N % 256 == 0 && !pair_off) {  // CTA-pair 256 x 256 tiles
         const int tiles = ((M + 255) / 256) * (N / 256);
         const int pairs = std::min(tiles, num_sms / 2);
-        const cudaError_t a = set_smem_attr(reinterpret_cast<const void*>(sm100_gemm2_kernel), kSmem);
+        const void* fn2 = P.resid ? reinterpret_cast<const void*>(sm100_gemm2_kernel<true>)
+                                  : reinterpret_cast<const void*>(sm100_gemm2_kernel<false>);
+        const cudaError_t a = set_smem_attr(fn2, kSmem);
         if (a != cudaSuccess) return a;
-        sm100_gemm2_kernel<<<2 * pairs, kThreads, kSmem, stream>>>(ma, mb, P);
+        if (P.resid) sm100_gemm2_kernel<true><<<2 * pairs, kThreads, kSmem, stream>>>(ma, mb, P);
+        else sm100_gemm2_kernel<false><<<2 * pairs, kThreads, kSmem, stream>>>(ma, mb, P);
         return cudaGetLastError();
     }
     const int tiles = ((M + 127) / 128) * (N / 128);
     const int grid = tiles < num_sms ? tiles : num_sms;
-    const cudaError_t a = set_smem_attr(reinterpret_cast<const void*>(sm100_gemm_kernel), kSmem);
+    const void* fn = P.resid ? reinterpret_cast<const void*>(sm100_gemm_kernel<true>)
+                             : reinterpret_cast<const void*>(sm100_gemm_kernel<false>);
+    const cudaError_t a = set_smem_attr(fn, kSmem);
     if (a != cudaSuccess) return a;
-    sm100_gemm_kernel<<<grid, kThreads, kSmem, stream>>>(ma, mb, P);
+    if (P.resid) sm100_gemm_kernel<true><<<grid, kThreads, kSmem, stream>>>(ma, mb, P);
+    else sm100_gemm_kernel<false><<<grid, kThreads, kSmem, stream>>>(ma, mb, P);
     return cudaGetLastError();
 }
 
